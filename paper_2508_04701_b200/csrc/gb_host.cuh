@@ -1,0 +1,356 @@
+// gb_host.cuh — group-by planning (agg -> state mapping, slot layout), the host driver
+// (table sizing, strategy, retry on a full table) and result extraction/emission.
+#pragma once
+#include <cstring>
+
+#include "compact.cuh"
+#include "groupby.cuh"
+
+namespace sx {
+
+struct GbPlan {
+  Layout L;
+  sx_expr state_expr[kMaxStates];
+  int nkeys;
+  int key_types[2];
+  int key_fn[2];
+  int out_key_type[2];
+  int naggs;
+  int agg_op[SX_MAX_AGGS];
+  int agg_state[SX_MAX_AGGS];   // SUM/MIN/MAX/AVG: state holding the value
+  int agg_scale[SX_MAX_AGGS];
+  int count_state;              // -1 if none
+  int has_having;
+  sx_having hv;
+};
+
+inline bool expr_equal(const sx_expr& a, const sx_expr& b) {
+  if (a.nterms != b.nterms) return false;
+  for (int t = 0; t < a.nterms; ++t) {
+    if (a.t[t].coef != b.t[t].coef || a.t[t].nf != b.t[t].nf) return false;
+    for (int f = 0; f < a.t[t].nf; ++f)
+      if (a.t[t].f[f].col != b.t[t].f[f].col || a.t[t].f[f].mul != b.t[t].f[f].mul || a.t[t].f[f].add != b.t[t].f[f].add)
+        return false;
+  }
+  return true;
+}
+
+inline sx_status gb_plan(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* keys, int nkeys, const sx_agg* aggs,
+                         int naggs, const sx_having* having, GbPlan* P) {
+  std::memset(P, 0, sizeof(*P));
+  if (nkeys < 0 || nkeys > 2) return set_err(ctx, SX_EINVAL, "nkeys %d (0..2)", nkeys);
+  if (naggs < 0 || naggs > SX_MAX_AGGS) return set_err(ctx, SX_EINVAL, "naggs %d (0..%d)", naggs, SX_MAX_AGGS);
+  P->nkeys = nkeys;
+  int kbits_total = 0;
+  for (int k = 0; k < nkeys; ++k) {
+    int c = keys[k].col;
+    if (c < 0 || c >= ncols) return set_err(ctx, SX_EINVAL, "key column %d out of range", c);
+    int t = cols[c].type;
+    if (t != SX_U8 && t != SX_I32 && t != SX_DATE32 && t != SX_I64) return set_err(ctx, SX_ETYPE, "key type %d", t);
+    if (keys[k].fn == SX_KEY_YEAR && t != SX_DATE32) return set_err(ctx, SX_ETYPE, "SX_KEY_YEAR needs a DATE32 key");
+    if (keys[k].fn != SX_KEY_IDENTITY && keys[k].fn != SX_KEY_YEAR) return set_err(ctx, SX_EINVAL, "key fn %d", keys[k].fn);
+    P->key_types[k] = t;
+    P->key_fn[k] = keys[k].fn;
+    P->out_key_type[k] = keys[k].fn == SX_KEY_YEAR ? SX_I32 : t;
+    int b = keys[k].fn == SX_KEY_YEAR ? 32 : key_bits(t);
+    if (nkeys == 2 && b > 32) return set_err(ctx, SX_ETYPE, "two-column group keys must each be <= 32 bits");
+    kbits_total += b;
+  }
+  Layout& L = P->L;
+  L.key_bytes = nkeys == 0 ? 0 : (kbits_total <= 32 ? 4 : 8);
+  // states
+  int nst = 0;
+  P->count_state = -1;
+  auto add_state = [&](int kind, const sx_expr* e) -> int {
+    for (int s = 0; s < nst; ++s)
+      if (L.kind[s] == kind && (kind == ST_COUNT || expr_equal(P->state_expr[s], *e))) return s;
+    L.kind[nst] = kind;
+    if (e) P->state_expr[nst] = *e;
+    else std::memset(&P->state_expr[nst], 0, sizeof(sx_expr));
+    return nst++;
+  };
+  P->naggs = naggs;
+  for (int a = 0; a < naggs; ++a) {
+    int op = aggs[a].op;
+    if (op != SX_COUNT) SX_TRY(check_expr(ctx, cols, ncols, aggs[a].value));
+    if (nst >= kMaxStates - 1 && op == SX_AVG) return set_err(ctx, SX_EINVAL, "too many aggregate states");
+    P->agg_op[a] = op;
+    P->agg_scale[a] = aggs[a].scale;
+    switch (op) {
+      case SX_SUM: P->agg_state[a] = add_state(ST_SUM, &aggs[a].value); break;
+      case SX_COUNT: P->agg_state[a] = P->count_state = add_state(ST_COUNT, nullptr); break;
+      case SX_MIN: P->agg_state[a] = add_state(ST_MIN, &aggs[a].value); break;
+      case SX_MAX: P->agg_state[a] = add_state(ST_MAX, &aggs[a].value); break;
+      case SX_AVG:
+        P->agg_state[a] = add_state(ST_SUM, &aggs[a].value);
+        P->count_state = add_state(ST_COUNT, nullptr);
+        if (aggs[a].scale < 0 || aggs[a].scale > 18) return set_err(ctx, SX_EINVAL, "avg scale %d", aggs[a].scale);
+        break;
+      default: return set_err(ctx, SX_EINVAL, "aggregate op %d", op);
+    }
+    if (nst > kMaxStates) return set_err(ctx, SX_EINVAL, "too many aggregate states");
+  }
+  if (nkeys == 0 && P->count_state < 0) {
+    if (nst >= kMaxStates) return set_err(ctx, SX_EINVAL, "too many aggregate states");
+    P->count_state = add_state(ST_COUNT, nullptr);
+  }
+  L.nst = nst;
+  // byte layout: key, then 8-byte fields, then 4-byte sum-hi fields (first one packed next to a 4-byte key)
+  int off = L.key_bytes;
+  int n4 = 0;
+  for (int s = 0; s < nst; ++s) n4 += L.kind[s] == ST_SUM;
+  int first4 = -1;
+  if (L.key_bytes == 4 && n4 > 0) {
+    for (int s = 0; s < nst && first4 < 0; ++s)
+      if (L.kind[s] == ST_SUM) first4 = s;
+    L.off4[first4] = 4;
+    off = 8;
+  }
+  off = (off + 7) & ~7;
+  for (int s = 0; s < nst; ++s) { L.off8[s] = off; off += 8; }
+  for (int s = 0; s < nst; ++s)
+    if (L.kind[s] == ST_SUM && s != first4) { L.off4[s] = off; off += 4; }
+  L.slot_bytes = (off + 7) & ~7;
+  if (L.slot_bytes == 0) L.slot_bytes = 8;
+  P->has_having = having != nullptr;
+  if (having) {
+    if (having->agg < 0 || having->agg >= naggs) return set_err(ctx, SX_EINVAL, "having agg index out of range");
+    if (P->agg_op[having->agg] == SX_AVG) return set_err(ctx, SX_EUNSUPPORTED, "HAVING on AVG");
+    if (having->op < SX_LT || having->op > SX_BETWEEN) return set_err(ctx, SX_EINVAL, "having op");
+    P->hv = *having;
+  }
+  return SX_OK;
+}
+
+// ------------------------------------------------------------------------ extraction
+struct SlotFn {
+  const uint8_t* slots;
+  uint64_t cap;
+  int slot_bytes, key_bytes;
+  const int* side_used;
+  int has_having, hv_kind, hv_op, hv_off8, hv_off4;
+  int64_t hv_lo, hv_hi;
+  __device__ __forceinline__ bool hv_ok(const uint8_t* p) const {
+    if (!has_having) return true;
+    if (hv_kind == ST_SUM) {
+      __int128 v = ((__int128)(*(const int*)(p + hv_off4)) << 64) | (__int128)(*(const unsigned long long*)(p + hv_off8));
+      __int128 lo = hv_lo, hi = hv_hi;
+      switch (hv_op) {
+        case SX_LT: return v < lo;
+        case SX_LE: return v <= lo;
+        case SX_GT: return v > lo;
+        case SX_GE: return v >= lo;
+        case SX_EQ: return v == lo;
+        case SX_NE: return v != lo;
+        default: return lo <= v && v <= hi;
+      }
+    }
+    unsigned long long u = *(const unsigned long long*)(p + hv_off8);
+    int64_t v = hv_kind == ST_COUNT ? (int64_t)u
+              : hv_kind == ST_MAX ? (int64_t)(u ^ 0x8000000000000000ull)
+                                  : (int64_t)(~u ^ 0x8000000000000000ull);
+    return cmp(hv_op, v, hv_lo, hv_hi);
+  }
+  template <int ITEMS>
+  __device__ __forceinline__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+                                       int32_t (&aux)[ITEMS]) const {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      bool occ = false;
+      if (valid[i]) {
+        const uint8_t* p = slots + (uint64_t)row[i] * slot_bytes;
+        if (key_bytes == 0) occ = true;
+        else if ((uint64_t)row[i] == cap) occ = *side_used != 0;
+        else if (key_bytes == 4) occ = *(const unsigned*)p != 0u;
+        else occ = *(const unsigned long long*)p != 0ull;
+        occ = occ && hv_ok(p);
+      }
+      alive[i] = occ;
+    }
+  }
+};
+
+struct EmitArgs {
+  const uint8_t* slots;
+  const int32_t* ids;
+  int64_t n;
+  uint64_t cap;
+  Layout L;
+  int nkeys;
+  int out_key_type[2];
+  void* out_key[2];
+  int naggs;
+  int agg_op[SX_MAX_AGGS];
+  int agg_state[SX_MAX_AGGS];
+  int agg_scale[SX_MAX_AGGS];
+  int count_state;
+  void* out_agg[SX_MAX_AGGS];
+};
+
+__device__ __forceinline__ void put_key(void* dst, int type, int64_t i, int64_t v) {
+  switch (type) {
+    case SX_U8: ((uint8_t*)dst)[i] = (uint8_t)v; break;
+    case SX_I32:
+    case SX_DATE32: ((int32_t*)dst)[i] = (int32_t)v; break;
+    default: ((int64_t*)dst)[i] = v; break;
+  }
+}
+
+__device__ __forceinline__ double i128_to_double(unsigned long long lo, long long hi) {
+  if ((hi == 0 && (long long)lo >= 0) || (hi == -1 && (long long)lo < 0)) return (double)(long long)lo;
+  return (double)hi * 18446744073709551616.0 + (double)lo;
+}
+
+__global__ void k_gb_emit(const __grid_constant__ EmitArgs a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t slot = (uint64_t)a.ids[i];
+    const uint8_t* p = a.slots + slot * a.L.slot_bytes;
+    if (a.nkeys > 0) {
+      uint64_t k = 0;
+      if (slot != a.cap) k = a.L.key_bytes == 4 ? (uint64_t)*(const unsigned*)p : *(const unsigned long long*)p;
+      if (a.nkeys == 1) {
+        int64_t v = a.L.key_bytes == 4 ? (int64_t)(int32_t)(uint32_t)k : (int64_t)k;
+        if (a.out_key_type[0] == SX_U8) v = (uint8_t)k;
+        put_key(a.out_key[0], a.out_key_type[0], i, v);
+      } else {
+        int64_t k0 = (int32_t)(uint32_t)(k >> 32), k1 = (int32_t)(uint32_t)k;
+        if (a.out_key_type[0] == SX_U8) k0 = (uint8_t)(k >> 32);
+        if (a.out_key_type[1] == SX_U8) k1 = (uint8_t)k;
+        put_key(a.out_key[0], a.out_key_type[0], i, k0);
+        put_key(a.out_key[1], a.out_key_type[1], i, k1);
+      }
+    }
+    unsigned long long count = a.count_state >= 0 ? *(const unsigned long long*)(p + a.L.off8[a.count_state]) : 0;
+    for (int j = 0; j < a.naggs; ++j) {
+      int s = a.agg_state[j];
+      unsigned long long u = *(const unsigned long long*)(p + a.L.off8[s]);
+      switch (a.agg_op[j]) {
+        case SX_SUM: {
+          long long hi = *(const int*)(p + a.L.off4[s]);
+          ((longlong2*)a.out_agg[j])[i] = make_longlong2((long long)u, hi);
+          break;
+        }
+        case SX_COUNT: ((long long*)a.out_agg[j])[i] = (long long)count; break;
+        case SX_MIN: ((long long*)a.out_agg[j])[i] = (long long)(~u ^ 0x8000000000000000ull); break;
+        case SX_MAX: ((long long*)a.out_agg[j])[i] = (long long)(u ^ 0x8000000000000000ull); break;
+        default: {  // AVG = (double)sum / (double)count / 10^scale (reading R3)
+          long long hi = *(const int*)(p + a.L.off4[s]);
+          double sc = 1.0;
+          for (int q = 0; q < a.agg_scale[j]; ++q) sc *= 10.0;
+          ((double*)a.out_agg[j])[i] = i128_to_double(u, hi) / (double)count / sc;
+          break;
+        }
+      }
+    }
+  }
+}
+
+inline int agg_out_type(int op) {
+  switch (op) {
+    case SX_SUM: return SX_I128;
+    case SX_AVG: return SX_F64;
+    default: return SX_I64;
+  }
+}
+
+inline uint64_t pow2_at_least(uint64_t x) {
+  uint64_t c = 16;
+  while (c < x) c <<= 1;
+  return c;
+}
+
+// Run the aggregation with RowFn and produce the outputs.  `force_small` selects K9.
+template <class RowFn>
+sx_status gb_run(sx_ctx* ctx, const RowFn& fn, const GbPlan& P, const int32_t* sel, int64_t n, int64_t groups_hint,
+                 sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups, int force_small = -1) {
+  Scratch scr(ctx);
+  const Layout& L = P.L;
+  bool keyless = P.nkeys == 0;
+  bool small = keyless || (groups_hint >= 1 && groups_hint <= 4);
+  if (force_small >= 0) small = force_small != 0;
+  uint64_t cap = keyless ? 1 : pow2_at_least(groups_hint > 0 ? (uint64_t)(2 * groups_hint)
+                                                             : (uint64_t)(2 * (n < (1 << 20) ? n : (1 << 20))));
+  uint8_t* table = nullptr;
+  int32_t* ids = nullptr;
+  int64_t ng = 0;
+  int flags[4];
+  for (int attempt = 0;; ++attempt) {
+    uint64_t nslots = keyless ? 1 : cap + 1;
+    SX_TRY(scr.get(&table, nslots * L.slot_bytes));
+    SX_CUDA(cudaMemsetAsync(table, 0, nslots * L.slot_bytes, ctx->stream));
+    SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
+    Table t{table, keyless ? 0 : cap - 1, ctx->d_flags + 2, ctx->d_flags + 1};
+    if (n > 0) {
+      unsigned grid = persistent_grid(ctx, 4, (n + kBlock - 1) / kBlock);
+      if (small) k_gb_small<RowFn, 4, kMaxStates><<<grid, kBlock, 0, ctx->stream>>>(fn, sel, n, L, t);
+      else k_gb_global<RowFn><<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(fn, sel, n, L, t);
+      SX_CHECK_LAUNCH();
+    }
+    SlotFn sf;
+    sf.slots = table;
+    sf.cap = keyless ? 1 : cap;
+    sf.slot_bytes = L.slot_bytes;
+    sf.key_bytes = L.key_bytes;
+    sf.side_used = ctx->d_flags + 2;
+    sf.has_having = P.has_having;
+    if (P.has_having) {
+      int s = P.agg_state[P.hv.agg];
+      sf.hv_kind = L.kind[s];
+      sf.hv_off8 = L.off8[s];
+      sf.hv_off4 = L.off4[s];
+      sf.hv_op = P.hv.op;
+      sf.hv_lo = P.hv.lo;
+      sf.hv_hi = P.hv.hi;
+    }
+    SX_TRY(scr.get(&ids, nslots));
+    GatherSpec none;
+    none.n = 0;
+    SX_TRY(run_compact(ctx, sf, (int64_t)nslots, nullptr, ids, nullptr, none, &ng));
+    SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
+    if (flags[0]) return set_err(ctx, SX_EOVERFLOW, "a value expression left int64");
+    if (!flags[1]) break;
+    // table full: the hint was too small; retry at an upper bound (G <= n)
+    if (attempt >= 2) return set_err(ctx, SX_ENOMEM, "aggregation table full after resizing");
+    dfree(ctx, table); scr.release(table);
+    dfree(ctx, ids); scr.release(ids);
+    cap = pow2_at_least((uint64_t)(2 * n > 32 ? 2 * n : 32));
+    small = false;
+  }
+  // outputs
+  EmitArgs ea;
+  std::memset(&ea, 0, sizeof(ea));
+  ea.slots = table;
+  ea.ids = ids;
+  ea.n = ng;
+  ea.cap = keyless ? 1 : cap;
+  ea.L = L;
+  ea.nkeys = P.nkeys;
+  ea.naggs = P.naggs;
+  ea.count_state = P.count_state;
+  for (int k = 0; k < P.nkeys; ++k) {
+    ea.out_key_type[k] = P.out_key_type[k];
+    SX_TRY(scr.get((char**)&ea.out_key[k], (size_t)ng * type_width(P.out_key_type[k])));
+  }
+  for (int j = 0; j < P.naggs; ++j) {
+    ea.agg_op[j] = P.agg_op[j];
+    ea.agg_state[j] = P.agg_state[j];
+    ea.agg_scale[j] = P.agg_scale[j];
+    SX_TRY(scr.get((char**)&ea.out_agg[j], (size_t)ng * type_width(agg_out_type(P.agg_op[j]))));
+  }
+  if (ng > 0) {
+    k_gb_emit<<<persistent_grid(ctx, 8, (ng + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(ea);
+    SX_CHECK_LAUNCH();
+  }
+  for (int k = 0; k < P.nkeys; ++k) {
+    out_keys[k] = sx_col{P.out_key_type[k], 0, ng, ea.out_key[k], nullptr, nullptr};
+    scr.release(ea.out_key[k]);
+  }
+  for (int j = 0; j < P.naggs; ++j) {
+    out_aggs[j] = sx_col{agg_out_type(P.agg_op[j]), 0, ng, ea.out_agg[j], nullptr, nullptr};
+    scr.release(ea.out_agg[j]);
+  }
+  *out_ngroups = ng;
+  return SX_OK;
+}
+
+}  // namespace sx

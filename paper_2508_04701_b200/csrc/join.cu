@@ -1,0 +1,379 @@
+// join.cu — H4/H6: open-addressing hash join build (K5) and probe (K6).
+//
+// PAPER.md P:96 / P:254 (joins via libcudf, here our own kernels)
+// (joins dominate join-heavy queries), P:268 ("hash tables" live in the
+// processing region).  Table: power-of-two slots, load <= 0.5, linear probing,
+// hash = murmur3 fmix64 (reading R14), duplicates kept.
+//   key_bytes 4: slot u64 = (row << 32) | key32, claimed by one 64-bit CAS.
+//   key_bytes 8: slot {u64 key; u32 row; u32 pad}, claimed by a 32-bit CAS on
+//                row, key stored after (probes run in a later kernel).
+// EMPTY: row word 0xFFFFFFFF (never a valid int32 row id).
+#include "compact.cuh"
+#include "filter.cuh"
+#include "join.cuh"
+
+using namespace sx;
+
+namespace sx {
+
+__device__ __forceinline__ uint64_t key_of(const DCol* cols, int nkeys, int kc0, int kc1, int64_t r) {
+  if (nkeys == 1) return (uint64_t)ldv(cols[kc0], r);
+  return ((uint64_t)(uint32_t)ldv(cols[kc0], r) << 32) | (uint32_t)ldv(cols[kc1], r);
+}
+
+struct BuildArgs {
+  DCol cols[SX_MAX_COLS];
+  DPred preds[SX_MAX_PREDS];
+  int np, nkeys, kc0, kc1, key_bytes;
+  const int32_t* sel;
+  int64_t n;
+  void* slots;
+  uint64_t mask;
+  unsigned long long* inserted;
+};
+
+__global__ void __launch_bounds__(kBlock) k_build(const __grid_constant__ BuildArgs a) {
+  int64_t cnt = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < a.n; idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = a.sel ? (int64_t)__ldg(a.sel + idx) : idx;
+    if (!eval_conj(a.cols, a.preds, a.np, r)) continue;
+    uint64_t key = key_of(a.cols, a.nkeys, a.kc0, a.kc1, r);
+    uint64_t h = hash64(key) & a.mask;
+    if (a.key_bytes == 4) {
+      unsigned long long* s = (unsigned long long*)a.slots;
+      unsigned long long v = ((unsigned long long)(uint32_t)r << 32) | (uint32_t)key;
+      while (atomicCAS(s + h, ~0ull, v) != ~0ull) h = (h + 1) & a.mask;
+    } else {
+      HtSlot8* s = (HtSlot8*)a.slots;
+      while (atomicCAS(&s[h].row, 0xffffffffu, (unsigned)r) != 0xffffffffu) h = (h + 1) & a.mask;
+      s[h].key = key;
+    }
+    ++cnt;
+  }
+  // warp-aggregated count of inserted rows
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(a.inserted, (unsigned long long)cnt);
+}
+
+// Probe functor for the ordered compaction skeleton (semi / anti / inner on a unique build).
+struct ProbeFn {
+  DCol cols[SX_MAX_COLS];
+  DPred preds[SX_MAX_PREDS];
+  int np, nkeys, kc0, kc1, key_bytes, anti;
+  const void* slots;
+  uint64_t mask;
+  template <int ITEMS>
+  __device__ __forceinline__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+                                       int32_t (&aux)[ITEMS]) const {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i];
+    for (int p = 0; p < np; ++p) apply_pred<ITEMS>(cols[preds[p].col], preds[p], row, alive);
+    uint64_t key[ITEMS], h[ITEMS];
+    bool pend[ITEMS], found[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = alive[i] ? key_of(cols, nkeys, kc0, kc1, row[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      h[i] = hash64(key[i]) & mask;
+      pend[i] = alive[i];
+      found[i] = false;
+    }
+    bool any = true;
+    while (any) {
+      any = false;
+      if (key_bytes == 4) {
+        unsigned long long s[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) s[i] = pend[i] ? __ldg((const unsigned long long*)slots + h[i]) : ~0ull;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          if (!pend[i]) continue;
+          if ((uint32_t)(s[i] >> 32) == 0xffffffffu) pend[i] = false;
+          else if ((uint32_t)s[i] == (uint32_t)key[i]) { found[i] = true; aux[i] = (int32_t)(s[i] >> 32); pend[i] = false; }
+          else { h[i] = (h[i] + 1) & mask; any = true; }
+        }
+      } else {
+        longlong2 s[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) s[i] = pend[i] ? __ldg((const longlong2*)slots + h[i]) : make_longlong2(0, -1);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          if (!pend[i]) continue;
+          uint32_t rw = (uint32_t)(unsigned long long)s[i].y;
+          if (rw == 0xffffffffu) pend[i] = false;
+          else if ((uint64_t)s[i].x == key[i]) { found[i] = true; aux[i] = (int32_t)rw; pend[i] = false; }
+          else { h[i] = (h[i] + 1) & mask; any = true; }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) alive[i] = alive[i] && (anti ? !found[i] : found[i]);
+  }
+};
+
+// INNER join on a non-unique build: every match emitted; output slots by warp-aggregated atomics.
+struct InnerArgs {
+  DCol cols[SX_MAX_COLS];
+  DPred preds[SX_MAX_PREDS];
+  int np, nkeys, kc0, kc1, key_bytes;
+  const int32_t* sel;
+  int64_t n;
+  const void* slots;
+  uint64_t mask;
+  int32_t* out_probe;
+  int32_t* out_build;
+  int64_t cap;
+  unsigned long long* counter;
+};
+
+__global__ void __launch_bounds__(kBlock) k_probe_inner(const __grid_constant__ InnerArgs a,
+                                                        const __grid_constant__ GatherSpec gs) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // iterate so that whole warps stay converged: loop bound uniform per warp
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < a.n; base += stride) {
+    int64_t idx = base + lane;
+    bool alive = idx < a.n;
+    int64_t r = 0;
+    if (alive) {
+      r = a.sel ? (int64_t)__ldg(a.sel + idx) : idx;
+      alive = eval_conj(a.cols, a.preds, a.np, r);
+    }
+    uint64_t key = alive ? key_of(a.cols, a.nkeys, a.kc0, a.kc1, r) : 0;
+    uint64_t h = hash64(key) & a.mask;
+    bool pend = alive;
+    while (__any_sync(kFull, pend)) {
+      bool hit = false;
+      int32_t brow = -1;
+      if (pend) {
+        if (a.key_bytes == 4) {
+          unsigned long long s = __ldg((const unsigned long long*)a.slots + h);
+          if ((uint32_t)(s >> 32) == 0xffffffffu) pend = false;
+          else if ((uint32_t)s == (uint32_t)key) { hit = true; brow = (int32_t)(s >> 32); }
+        } else {
+          longlong2 s = __ldg((const longlong2*)a.slots + h);
+          uint32_t rw = (uint32_t)(unsigned long long)s.y;
+          if (rw == 0xffffffffu) pend = false;
+          else if ((uint64_t)s.x == key) { hit = true; brow = (int32_t)rw; }
+        }
+        h = (h + 1) & a.mask;
+      }
+      unsigned b = __ballot_sync(kFull, hit);
+      if (b) {
+        unsigned long long base_pos = 0;
+        if (lane == __ffs(b) - 1) base_pos = atomicAdd(a.counter, (unsigned long long)__popc(b));
+        base_pos = __shfl_sync(kFull, base_pos, __ffs(b) - 1);
+        if (hit) {
+          int64_t pos = (int64_t)base_pos + __popc(b & lt);
+          if (pos < a.cap) {
+            a.out_probe[pos] = (int32_t)r;
+            a.out_build[pos] = brow;
+            for (int g = 0; g < gs.n; ++g) gather_one(gs.g[g], pos, gs.g[g].by_aux ? (int64_t)brow : r);
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace sx
+
+namespace {
+
+sx_status resolve_keys(sx_ctx* ctx, const sx_col* cols, int ncols, const int32_t* key_cols, int nkeys, int* kb,
+                       int types[2]) {
+  if (nkeys < 1 || nkeys > 2 || !key_cols) return set_err(ctx, SX_EINVAL, "join needs 1 or 2 key columns");
+  for (int k = 0; k < nkeys; ++k) {
+    if (key_cols[k] < 0 || key_cols[k] >= ncols) return set_err(ctx, SX_EINVAL, "key column out of range");
+    int t = cols[key_cols[k]].type;
+    if (t != SX_I32 && t != SX_DATE32 && t != SX_I64 && t != SX_U8)
+      return set_err(ctx, SX_ETYPE, "join key type %d unsupported", t);
+    if (nkeys == 2 && key_bits(t) > 32) return set_err(ctx, SX_ETYPE, "two-column keys must each be <= 32 bits");
+    types[k] = t;
+  }
+  *kb = (nkeys == 1 && key_bits(types[0]) <= 32) ? 4 : 8;
+  return SX_OK;
+}
+
+}  // namespace
+
+SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, const int32_t* key_cols, int nkeys,
+                                  const sx_sel* in_sel, const sx_pred* where, int nwhere, int unique_hint,
+                                  sx_ht** out) {
+  if (!ctx || !out) return SX_EINVAL;
+  *out = nullptr;
+  ProfScope ps(ctx, "hash_build");
+  BuildArgs a{};
+  SX_TRY(to_dcols(ctx, cols, ncols, a.cols));
+  SX_TRY(check_preds(ctx, cols, ncols, where, nwhere, a.preds));
+  int types[2] = {SX_I32, SX_I32};
+  SX_TRY(resolve_keys(ctx, cols, ncols, key_cols, nkeys, &a.key_bytes, types));
+  a.np = nwhere;
+  a.nkeys = nkeys;
+  a.kc0 = key_cols[0];
+  a.kc1 = nkeys > 1 ? key_cols[1] : 0;
+  int64_t n = in_sel ? in_sel->len : cols[key_cols[0]].len;
+  if (n > INT32_MAX) return set_err(ctx, SX_EINDEX, "build side exceeds INT32_MAX rows");
+  uint64_t cap = 64;
+  while (cap < (uint64_t)(2 * n)) cap <<= 1;
+  size_t slot_bytes = a.key_bytes == 4 ? 8 : 16;
+  sx_ht* ht = new sx_ht();
+  ht->key_bytes = a.key_bytes;
+  ht->key_types[0] = types[0];
+  ht->key_types[1] = types[1];
+  ht->nkeys = nkeys;
+  ht->unique = unique_hint != 0;
+  ht->cap = cap;
+  sx_status s = alloc(ctx, (char**)&ht->slots, cap * slot_bytes);
+  if (s != SX_OK) {
+    delete ht;
+    return s;
+  }
+  cudaMemsetAsync(ht->slots, 0xff, cap * slot_bytes, ctx->stream);
+  unsigned long long* ins = (unsigned long long*)ctx->d_counters;
+  cudaMemsetAsync(ins, 0, 8, ctx->stream);
+  a.sel = in_sel ? in_sel->idx : nullptr;
+  a.n = n;
+  a.slots = ht->slots;
+  a.mask = cap - 1;
+  a.inserted = ins;
+  if (n > 0) k_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  int64_t rows = 0;
+  if (e == cudaSuccess) s = read_i64(ctx, ins, &rows);
+  if (e != cudaSuccess || s != SX_OK) {
+    dfree(ctx, ht->slots);
+    delete ht;
+    return e != cudaSuccess ? set_err(ctx, SX_ECUDA, "build: %s", cudaGetErrorString(e)) : s;
+  }
+  ht->rows = rows;
+  *out = ht;
+  return SX_OK;
+}
+
+SX_EXPORT int64_t sx_ht_rows(const sx_ht* ht) { return ht ? ht->rows : 0; }
+
+SX_EXPORT void sx_ht_destroy(sx_ctx* ctx, sx_ht* ht) {
+  if (!ht) return;
+  if (ctx) dfree(ctx, ht->slots);
+  delete ht;
+}
+
+SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* probe_cols, int nprobe_cols,
+                                  const int32_t* key_cols, int nkeys, const sx_sel* in_sel, const sx_pred* where,
+                                  int nwhere, int join_type, const sx_col* build_cols, int nbuild_cols,
+                                  const int32_t* bp, int nbp, const int32_t* pp, int npp, sx_sel* out_probe,
+                                  sx_sel* out_build, sx_col* out_payload) {
+  if (!ctx || !ht || !out_probe) return SX_EINVAL;
+  *out_probe = sx_sel{0, nullptr};
+  if (out_build) *out_build = sx_sel{0, nullptr};
+  for (int i = 0; out_payload && i < nbp + npp && i < kMaxGather; ++i) out_payload[i] = sx_col{};
+  ProfScope ps(ctx, join_type == SX_INNER ? "probe_inner" : (join_type == SX_SEMI ? "probe_semi" : "probe_anti"));
+  if (join_type < SX_INNER || join_type > SX_ANTI) return set_err(ctx, SX_EINVAL, "join type %d", join_type);
+  if (join_type == SX_INNER && !out_build) return set_err(ctx, SX_EINVAL, "INNER join needs out_build");
+  if (join_type != SX_INNER && nbp > 0) return set_err(ctx, SX_EINVAL, "build payload only for INNER joins");
+  if (nbp + npp > kMaxGather || nbp < 0 || npp < 0) return set_err(ctx, SX_EINVAL, "too many payload columns");
+  if ((nbp + npp) > 0 && !out_payload) return set_err(ctx, SX_EINVAL, "out_payload is NULL");
+  DCol pcols[SX_MAX_COLS], bcols[SX_MAX_COLS];
+  SX_TRY(to_dcols(ctx, probe_cols, nprobe_cols, pcols));
+  if (nbp > 0) SX_TRY(to_dcols(ctx, build_cols, nbuild_cols, bcols));
+  DPred preds[SX_MAX_PREDS];
+  SX_TRY(check_preds(ctx, probe_cols, nprobe_cols, where, nwhere, preds));
+  int kb = 4, types[2];
+  SX_TRY(resolve_keys(ctx, probe_cols, nprobe_cols, key_cols, nkeys, &kb, types));
+  if (nkeys != ht->nkeys || kb != ht->key_bytes)
+    return set_err(ctx, SX_ETYPE, "probe key shape (%d keys, %d bytes) differs from the build (%d, %d)", nkeys, kb,
+                   ht->nkeys, ht->key_bytes);
+  int64_t n = in_sel ? in_sel->len : probe_cols[key_cols[0]].len;
+  if (n > INT32_MAX) return set_err(ctx, SX_EINDEX, "probe side exceeds INT32_MAX rows");
+  Scratch scr(ctx);
+  GatherSpec gs;
+  gs.n = nbp + npp;
+  for (int g = 0; g < nbp; ++g) {
+    if (bp[g] < 0 || bp[g] >= nbuild_cols) return set_err(ctx, SX_EINVAL, "build payload column out of range");
+    gs.g[g].src = bcols[bp[g]];
+    gs.g[g].by_aux = 1;
+    gs.g[g].width = type_width(build_cols[bp[g]].type);
+    if (!gs.g[g].width) return set_err(ctx, SX_ETYPE, "payload must be fixed-width");
+  }
+  for (int g = 0; g < npp; ++g) {
+    if (pp[g] < 0 || pp[g] >= nprobe_cols) return set_err(ctx, SX_EINVAL, "probe payload column out of range");
+    gs.g[nbp + g].src = pcols[pp[g]];
+    gs.g[nbp + g].by_aux = 0;
+    gs.g[nbp + g].width = type_width(probe_cols[pp[g]].type);
+    if (!gs.g[nbp + g].width) return set_err(ctx, SX_ETYPE, "payload must be fixed-width");
+  }
+  const int32_t* isel = in_sel ? in_sel->idx : nullptr;
+  int64_t count = 0;
+  int32_t *op = nullptr, *ob = nullptr;
+  if (join_type != SX_INNER || ht->unique) {
+    // ordered compaction: each probe row emits at most one output
+    ProbeFn f;
+    for (int i = 0; i < nprobe_cols; ++i) f.cols[i] = pcols[i];
+    for (int i = 0; i < nwhere; ++i) f.preds[i] = preds[i];
+    f.np = nwhere;
+    f.nkeys = nkeys;
+    f.kc0 = key_cols[0];
+    f.kc1 = nkeys > 1 ? key_cols[1] : 0;
+    f.key_bytes = kb;
+    f.anti = join_type == SX_ANTI;
+    f.slots = ht->slots;
+    f.mask = ht->cap - 1;
+    SX_TRY(scr.get(&op, (size_t)n));
+    if (join_type == SX_INNER) SX_TRY(scr.get(&ob, (size_t)n));
+    for (int g = 0; g < gs.n; ++g) SX_TRY(scr.get((char**)&gs.g[g].dst, (size_t)n * gs.g[g].width));
+    SX_TRY(run_compact(ctx, f, n, isel, op, ob, gs, &count));
+  } else {
+    InnerArgs a{};
+    for (int i = 0; i < nprobe_cols; ++i) a.cols[i] = pcols[i];
+    for (int i = 0; i < nwhere; ++i) a.preds[i] = preds[i];
+    a.np = nwhere;
+    a.nkeys = nkeys;
+    a.kc0 = key_cols[0];
+    a.kc1 = nkeys > 1 ? key_cols[1] : 0;
+    a.key_bytes = kb;
+    a.sel = isel;
+    a.n = n;
+    a.slots = ht->slots;
+    a.mask = ht->cap - 1;
+    a.counter = (unsigned long long*)ctx->d_counters;
+    int64_t cap = n > 1024 ? n : 1024;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      SX_TRY(scr.get(&op, (size_t)cap));
+      SX_TRY(scr.get(&ob, (size_t)cap));
+      for (int g = 0; g < gs.n; ++g) SX_TRY(scr.get((char**)&gs.g[g].dst, (size_t)cap * gs.g[g].width));
+      a.out_probe = op;
+      a.out_build = ob;
+      a.cap = cap;
+      SX_CUDA(cudaMemsetAsync(a.counter, 0, 8, ctx->stream));
+      if (n > 0) k_probe_inner<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(a, gs);
+      SX_CHECK_LAUNCH();
+      SX_TRY(read_i64(ctx, a.counter, &count));
+      if (count <= cap) break;
+      if (count > INT32_MAX) return set_err(ctx, SX_EINDEX, "join output exceeds INT32_MAX rows");
+      // too small: release and retry at the exact size
+      dfree(ctx, op); scr.release(op);
+      dfree(ctx, ob); scr.release(ob);
+      for (int g = 0; g < gs.n; ++g) { dfree(ctx, gs.g[g].dst); scr.release(gs.g[g].dst); }
+      cap = count;
+    }
+  }
+  out_probe->len = count;
+  out_probe->idx = op;
+  scr.release(op);
+  if (join_type == SX_INNER) {
+    out_build->len = count;
+    out_build->idx = ob;
+    scr.release(ob);
+  }
+  for (int g = 0; g < gs.n; ++g) {
+    const sx_col& src = g < nbp ? build_cols[bp[g]] : probe_cols[pp[g - nbp]];
+    out_payload[g] = src;
+    out_payload[g].len = count;
+    out_payload[g].data = gs.g[g].dst;
+    out_payload[g].offsets = nullptr;
+    scr.release(gs.g[g].dst);
+  }
+  return SX_OK;
+}

@@ -1,0 +1,416 @@
+// sort.cu — H9: sx_sort_topk (K13 LSD radix sort, K14 radix-select top-k), CUB-free.
+//
+// PAPER.md P:191 (sorting via libcudf; here our kernels), P:422 (order-by inputs are small).
+// Keys are encoded into order-preserving unsigned 32-bit words, most significant first
+// (sign bit flipped; descending = bitwise NOT), followed by the input position, which makes
+// every composite key unique and the result stable.  Digits (8 bits) on which
+// all rows agree are skipped, so a sort costs passes only over bits that vary.
+//   n <= 2048          : one CTA bitonic sort in shared memory
+//   k <= 1024 (< n)    : radix select of the k-th key (one pass per varying digit, MSB first),
+//                        ordered compaction of the k winners, bitonic sort of those
+//   otherwise          : LSD radix sort (per pass: tile histograms, per-digit scan, stable scatter)
+#include "compact.cuh"
+
+using namespace sx;
+
+namespace {
+
+constexpr int kMaxWords = 9;  // <= 8 key words + position
+constexpr int kBitonicMax = 2048;
+
+struct EncArgs {
+  DCol cols[4];
+  int types[4];
+  int desc[4];
+  int nkeys;
+  int nwords;  // including the position word
+  const int32_t* sel;
+  int64_t n;
+  uint32_t* words[kMaxWords];  // SoA
+  unsigned* diff;              // [nwords]
+};
+
+__device__ __forceinline__ int encode_row(const EncArgs& a, int64_t r, int64_t pos, uint32_t* w) {
+  int k = 0;
+  for (int c = 0; c < a.nkeys; ++c) {
+    uint32_t m = a.desc[c] ? 0xffffffffu : 0u;
+    switch (a.types[c]) {
+      case SX_U8: w[k++] = ((uint32_t)((const uint8_t*)a.cols[c].p)[r]) ^ m; break;
+      case SX_I32:
+      case SX_DATE32: w[k++] = ((uint32_t)((const int32_t*)a.cols[c].p)[r] ^ 0x80000000u) ^ m; break;
+      case SX_I128: {
+        const long long* p = (const long long*)a.cols[c].p + 2 * r;
+        uint64_t lo = (uint64_t)p[0], hi = (uint64_t)p[1] ^ 0x8000000000000000ull;
+        w[k++] = (uint32_t)(hi >> 32) ^ m;
+        w[k++] = (uint32_t)hi ^ m;
+        w[k++] = (uint32_t)(lo >> 32) ^ m;
+        w[k++] = (uint32_t)lo ^ m;
+        break;
+      }
+      default: {
+        uint64_t u = (uint64_t)((const long long*)a.cols[c].p)[r] ^ 0x8000000000000000ull;
+        w[k++] = (uint32_t)(u >> 32) ^ m;
+        w[k++] = (uint32_t)u ^ m;
+        break;
+      }
+    }
+  }
+  w[k++] = (uint32_t)pos;
+  return k;
+}
+
+__global__ void k_encode(const __grid_constant__ EncArgs a) {
+  uint32_t w0[kMaxWords], w[kMaxWords];
+  int64_t r0 = a.sel ? (int64_t)a.sel[0] : 0;
+  encode_row(a, r0, 0, w0);
+  unsigned acc[kMaxWords];
+  for (int j = 0; j < kMaxWords; ++j) acc[j] = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = a.sel ? (int64_t)a.sel[i] : i;
+    encode_row(a, r, i, w);
+    for (int j = 0; j < a.nwords; ++j) {
+      a.words[j][i] = w[j];
+      acc[j] |= w[j] ^ w0[j];
+    }
+  }
+  for (int j = 0; j < a.nwords; ++j) {
+    unsigned v = acc[j];
+    for (int o = 16; o > 0; o >>= 1) v |= __shfl_xor_sync(kFull, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicOr(a.diff + j, v);
+  }
+}
+
+struct Words {
+  uint32_t* w[kMaxWords];
+  int nwords;
+};
+
+__device__ __forceinline__ bool key_less(const uint32_t* a, const uint32_t* b, int nw) {
+  for (int j = 0; j < nw; ++j)
+    if (a[j] != b[j]) return a[j] < b[j];
+  return false;
+}
+
+// Bitonic sort of m <= 2048 rows (given by positions `pos`, or 0..m-1) in one CTA; writes
+// out_perm[0..min(k,m)) = original row ids.
+__global__ void __launch_bounds__(1024) k_bitonic(const __grid_constant__ Words W, const int32_t* pos, int64_t m,
+                                                  int64_t k, const int32_t* sel, int32_t* out_perm) {
+  extern __shared__ uint32_t sm[];  // [N][nwords]
+  int nw = W.nwords;
+  int N = 1;
+  while (N < m) N <<= 1;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    for (int j = 0; j < nw; ++j) {
+      uint32_t v = 0xffffffffu;
+      if (i < m) {
+        int64_t p = pos ? pos[i] : i;
+        v = W.w[j][p];
+      }
+      sm[i * nw + j] = v;
+    }
+  }
+  __syncthreads();
+  uint32_t ta[kMaxWords], tb[kMaxWords];
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool up = ((lo & size) == 0);
+        for (int j = 0; j < nw; ++j) { ta[j] = sm[lo * nw + j]; tb[j] = sm[hi * nw + j]; }
+        bool sw = up ? key_less(tb, ta, nw) : key_less(ta, tb, nw);
+        if (sw)
+          for (int j = 0; j < nw; ++j) { sm[lo * nw + j] = tb[j]; sm[hi * nw + j] = ta[j]; }
+      }
+      __syncthreads();
+    }
+  }
+  int64_t outn = k < m ? k : m;
+  for (int i = threadIdx.x; i < outn; i += blockDim.x) {
+    int64_t p = sm[i * nw + (nw - 1)];  // position word
+    out_perm[i] = sel ? sel[p] : (int32_t)p;
+  }
+}
+
+// ---- radix select -------------------------------------------------------------------
+struct SelState {
+  unsigned long long k_rem;
+  int chosen;  // digit chosen in the previous pass (-1: none / reject all)
+  int pad;
+};
+
+__global__ void k_sel_hist(const __grid_constant__ Words W, int64_t n, uint8_t* state_flags, int pword, int pshift,
+                           int cword, int cshift, const SelState* st, unsigned* hist, int first) {
+  __shared__ unsigned h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  int chosen = st->chosen;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t f = first ? 1 : state_flags[i];  // 1 active, 2 accepted, 0 rejected
+    if (!first && f == 1) {
+      int d = (W.w[pword][i] >> pshift) & 0xff;
+      f = d < chosen ? 2 : (d == chosen ? 1 : 0);
+      state_flags[i] = f;
+    } else if (first) {
+      state_flags[i] = 1;
+    }
+    if (f == 1 && cword >= 0) atomicAdd(&h[(W.w[cword][i] >> cshift) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+__global__ void k_sel_choose(unsigned* hist, SelState* st) {
+  // one warp: find smallest digit b with cumulative count >= k_rem
+  if (threadIdx.x == 0) {
+    unsigned long long krem = st->k_rem, cum = 0;
+    int b = -1;
+    if (krem > 0) {
+      for (int d = 0; d < 256; ++d) {
+        if (cum + hist[d] >= krem) { b = d; break; }
+        cum += hist[d];
+      }
+    }
+    st->chosen = b;
+    st->k_rem = krem - cum;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+}
+
+struct AcceptedFn {
+  const uint8_t* flags;
+  template <int ITEMS>
+  __device__ __forceinline__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+                                       int32_t (&aux)[ITEMS]) const {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i] && flags[row[i]] != 0;
+  }
+};
+
+// ---- LSD radix sort -----------------------------------------------------------------
+constexpr int kLsdTile = 256;
+
+__global__ void __launch_bounds__(kLsdTile) k_lsd_hist(const uint32_t* __restrict__ dw, int shift, int64_t n,
+                                                       unsigned* counts /* [256][ntiles] */, int64_t ntiles) {
+  __shared__ unsigned h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t i = blockIdx.x * (int64_t)kLsdTile + threadIdx.x;
+  if (i < n) atomicAdd(&h[(dw[i] >> shift) & 0xff], 1u);
+  __syncthreads();
+  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of counts in digit-major order (one CTA; the array is 256 * ntiles long)
+__global__ void __launch_bounds__(1024) k_lsd_scan(unsigned* counts, int64_t len) {
+  __shared__ unsigned long long carry;
+  __shared__ unsigned long long wsum[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < len; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    unsigned long long v = i < len ? counts[i] : 0;
+    unsigned long long x = v;
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      unsigned long long t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(kFull, t, o);
+        if (lane >= o) t += y;
+      }
+      wsum[lane] = t;
+    }
+    __syncthreads();
+    unsigned long long incl = x + (w ? wsum[w - 1] : 0) + carry;
+    if (i < len) counts[i] = (unsigned)(incl - v);
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = incl;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kLsdTile) k_lsd_scatter(const __grid_constant__ Words src, const __grid_constant__ Words dst,
+                                                          int dword, int shift, int64_t n, const unsigned* offsets,
+                                                          int64_t ntiles) {
+  __shared__ unsigned wc[kLsdTile / 32][256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int d = threadIdx.x; d < 256; d += blockDim.x)
+    for (int q = 0; q < kLsdTile / 32; ++q) wc[q][d] = 0;
+  __syncthreads();
+  int64_t i = blockIdx.x * (int64_t)kLsdTile + threadIdx.x;
+  bool valid = i < n;
+  int d = valid ? (int)((src.w[dword][i] >> shift) & 0xff) : 256 + lane;  // unique dummy digits for invalid lanes
+  unsigned peers = __match_any_sync(kFull, d);
+  int rank = __popc(peers & lanemask_lt());
+  if (valid && rank == 0) wc[w][d] = __popc(peers);
+  __syncthreads();
+  // exclusive prefix over warps for each digit
+  if (threadIdx.x < 256) {
+    unsigned run = 0;
+    for (int q = 0; q < kLsdTile / 32; ++q) {
+      unsigned c = wc[q][threadIdx.x];
+      wc[q][threadIdx.x] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (valid) {
+    int64_t pos = (int64_t)offsets[(int64_t)d * ntiles + blockIdx.x] + wc[w][d] + rank;
+    for (int j = 0; j < src.nwords; ++j) dst.w[j][pos] = src.w[j][i];
+  }
+}
+
+}  // namespace
+
+SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_sortkey* keys, int nkeys,
+                                 const sx_sel* in_sel, int64_t k, sx_sel* out_perm) {
+  if (!ctx || !out_perm || (nkeys > 0 && !keys)) return SX_EINVAL;
+  *out_perm = sx_sel{0, nullptr};
+  ProfScope ps(ctx, "sort_topk");
+  if (nkeys < 1 || nkeys > 4) return set_err(ctx, SX_EINVAL, "nkeys %d (1..4)", nkeys);
+  EncArgs ea{};
+  int nwords = 1;
+  int64_t n = -1;
+  for (int c = 0; c < nkeys; ++c) {
+    int col = keys[c].col;
+    if (col < 0 || col >= ncols) return set_err(ctx, SX_EINVAL, "sort key column out of range");
+    const sx_col& sc = cols[col];
+    if (sc.validity) return set_err(ctx, SX_EUNSUPPORTED, "validity bitmaps unsupported");
+    int t = sc.type;
+    int w = (t == SX_U8 || t == SX_I32 || t == SX_DATE32) ? 1 : (t == SX_I64 || t == SX_DEC64) ? 2 : t == SX_I128 ? 4 : 0;
+    if (!w) return set_err(ctx, SX_ETYPE, "sort key type %d unsupported", t);
+    nwords += w;
+    ea.cols[c] = DCol{sc.data, t, 0};
+    ea.types[c] = t;
+    ea.desc[c] = keys[c].desc != 0;
+    if (n < 0) n = sc.len;
+  }
+  if (nwords > kMaxWords) return set_err(ctx, SX_EINVAL, "sort key too wide (%d words)", nwords);
+  if (in_sel) n = in_sel->len;
+  if (n > INT32_MAX) return set_err(ctx, SX_EINDEX, "sort input exceeds INT32_MAX rows");
+  int64_t outn = (k < 0 || k > n) ? n : k;
+  Scratch scr(ctx);
+  int32_t* perm;
+  SX_TRY(scr.get(&perm, (size_t)(outn > 0 ? outn : 1)));
+  if (outn == 0) {
+    out_perm->idx = perm;
+    scr.release(perm);
+    return SX_OK;
+  }
+  ea.nkeys = nkeys;
+  ea.nwords = nwords;
+  ea.sel = in_sel ? in_sel->idx : nullptr;
+  ea.n = n;
+  Words W{};
+  W.nwords = nwords;
+  for (int j = 0; j < nwords; ++j) {
+    SX_TRY(scr.get(&ea.words[j], (size_t)n));
+    W.w[j] = ea.words[j];
+  }
+  unsigned* diff;
+  SX_TRY(scr.get(&diff, kMaxWords));
+  SX_CUDA(cudaMemsetAsync(diff, 0, kMaxWords * sizeof(unsigned), ctx->stream));
+  k_encode<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(ea);
+  SX_CHECK_LAUNCH();
+  const int32_t* sel = in_sel ? in_sel->idx : nullptr;
+  if (n <= kBitonicMax) {
+    size_t smem = (size_t)kBitonicMax * nwords * sizeof(uint32_t);
+    SX_CUDA(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_bitonic<<<1, 1024, smem, ctx->stream>>>(W, nullptr, n, outn, sel, perm);
+    SX_CHECK_LAUNCH();
+    out_perm->len = outn;
+    out_perm->idx = perm;
+    scr.release(perm);
+    return SX_OK;
+  }
+  unsigned hdiff[kMaxWords];
+  SX_CUDA(cudaMemcpyAsync(hdiff, diff, sizeof(unsigned) * kMaxWords, cudaMemcpyDeviceToHost, ctx->stream));
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  // varying digits, most significant first: (word, shift)
+  std::vector<std::pair<int, int>> digits;
+  for (int j = 0; j < nwords; ++j)
+    for (int s = 24; s >= 0; s -= 8)
+      if ((hdiff[j] >> s) & 0xff) digits.push_back({j, s});
+  if (outn <= 1024 && outn < n) {
+    // radix select of the outn-th smallest composite key
+    uint8_t* flags;
+    unsigned* hist;
+    SelState* st;
+    SX_TRY(scr.get(&flags, (size_t)n));
+    SX_TRY(scr.get(&hist, 256));
+    SX_TRY(scr.get(&st, 1));
+    SelState h0{(unsigned long long)outn, -1, 0};
+    SX_CUDA(cudaMemcpyAsync(st, &h0, sizeof(h0), cudaMemcpyHostToDevice, ctx->stream));
+    SX_CUDA(cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned), ctx->stream));
+    unsigned grid = persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock);
+    int pw = -1, psh = 0;
+    for (size_t p = 0; p <= digits.size(); ++p) {
+      int cw = p < digits.size() ? digits[p].first : -1;
+      int csh = p < digits.size() ? digits[p].second : 0;
+      k_sel_hist<<<grid, kBlock, 0, ctx->stream>>>(W, n, flags, pw, psh, cw, csh, st, hist, p == 0);
+      SX_CHECK_LAUNCH();
+      if (cw >= 0) {
+        k_sel_choose<<<1, 256, 0, ctx->stream>>>(hist, st);
+        SX_CHECK_LAUNCH();
+      }
+      pw = cw;
+      psh = csh;
+    }
+    // all digits decided: the remaining active rows equal the k-th key exactly (unique keys) -> accepted
+    int32_t* winners;
+    SX_TRY(scr.get(&winners, (size_t)n));
+    AcceptedFn af{flags};
+    GatherSpec none;
+    none.n = 0;
+    int64_t m = 0;
+    SX_TRY(run_compact(ctx, af, n, nullptr, winners, nullptr, none, &m));
+    if (m != outn) return set_err(ctx, SX_ECUDA, "radix select produced %lld of %lld rows", (long long)m, (long long)outn);
+    size_t smem = (size_t)kBitonicMax * nwords * sizeof(uint32_t);
+    SX_CUDA(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_bitonic<<<1, 1024, smem, ctx->stream>>>(W, winners, m, outn, sel, perm);
+    SX_CHECK_LAUNCH();
+  } else {
+    // LSD radix sort over the varying digits, least significant first
+    Words W2{};
+    W2.nwords = nwords;
+    for (int j = 0; j < nwords; ++j) SX_TRY(scr.get(&W2.w[j], (size_t)n));
+    int64_t ntiles = (n + kLsdTile - 1) / kLsdTile;
+    unsigned* counts;
+    SX_TRY(scr.get(&counts, (size_t)(256 * ntiles)));
+    Words* a = &W;
+    Words* b = &W2;
+    for (int p = (int)digits.size() - 1; p >= 0; --p) {
+      k_lsd_hist<<<(unsigned)ntiles, kLsdTile, 0, ctx->stream>>>(a->w[digits[p].first], digits[p].second, n, counts, ntiles);
+      k_lsd_scan<<<1, 1024, 0, ctx->stream>>>(counts, 256 * ntiles);
+      k_lsd_scatter<<<(unsigned)ntiles, kLsdTile, 0, ctx->stream>>>(*a, *b, digits[p].first, digits[p].second, n, counts, ntiles);
+      SX_CHECK_LAUNCH();
+      std::swap(a, b);
+    }
+    // positions (last word) of the first outn sorted rows -> row ids
+    GatherSpec none;
+    none.n = 0;
+    (void)none;
+    sx_sel possel{outn, (int32_t*)a->w[nwords - 1]};
+    if (sel) {
+      sx_col selcol{SX_I32, 0, n, sel, nullptr, nullptr};
+      sx_col g;
+      SX_TRY(sx_gather(ctx, &selcol, &possel, &g));
+      SX_CUDA(cudaMemcpyAsync(perm, g.data, outn * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+      dfree(ctx, (void*)g.data);
+    } else {
+      SX_CUDA(cudaMemcpyAsync(perm, a->w[nwords - 1], outn * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  }
+  out_perm->len = outn;
+  out_perm->idx = perm;
+  scr.release(perm);
+  return SX_OK;
+}

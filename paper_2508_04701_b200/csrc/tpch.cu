@@ -1,0 +1,457 @@
+// tpch.cu — fixed-plan executor for TPC-H Q1/Q3/Q6/Q9/Q18 (stands in for the Substrait
+// consumer, BASELINE.json north_star).  Each plan is a sequence of sx_* operator calls
+// (SURVEY.md §8(a) "Per-query fixed plans"); every step runs in libsx kernels; the only
+// host work is argument marshalling and the final device->host copy of the (tiny) result.
+// Semantics: SURVEY §8(c) "Definitions"; readings R1..R21 in DESIGN.md.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace sx;
+
+namespace {
+
+// Owns intermediate device buffers and hash tables of one query.
+struct Bag {
+  sx_ctx* ctx;
+  std::vector<void*> bufs;
+  std::vector<sx_ht*> hts;
+  explicit Bag(sx_ctx* c) : ctx(c) {}
+  ~Bag() {
+    for (void* p : bufs) sx_free(ctx, p);
+    for (sx_ht* h : hts) sx_ht_destroy(ctx, h);
+  }
+  void keep(const sx_sel& s) { if (s.idx) bufs.push_back(s.idx); }
+  void keep(const sx_col& c) { if (c.data) bufs.push_back((void*)c.data); }
+  void keep(const sx_col* c, int n) { for (int i = 0; i < n; ++i) keep(c[i]); }
+  void keep(sx_ht* h) { if (h) hts.push_back(h); }
+};
+
+sx_factor F(int col, int64_t mul = 1, int64_t add = 0) { return sx_factor{col, 0, mul, add}; }
+
+sx_expr E1(int64_t coef, std::initializer_list<sx_factor> fs) {
+  sx_expr e;
+  std::memset(&e, 0, sizeof e);
+  e.nterms = 1;
+  e.t[0].coef = coef;
+  e.t[0].nf = (int32_t)fs.size();
+  int i = 0;
+  for (auto& f : fs) e.t[0].f[i++] = f;
+  return e;
+}
+
+sx_agg A(int op, sx_expr e, int scale = 0) { return sx_agg{op, scale, e}; }
+sx_agg Count() { sx_agg a; std::memset(&a, 0, sizeof a); a.op = SX_COUNT; return a; }
+
+sx_pred P(int col, int op, int64_t lo, int64_t hi = 0) { return sx_pred{col, op, lo, hi, nullptr, 0, 0}; }
+
+// Copy a device column to host (caller syncs).
+sx_status d2h(sx_ctx* ctx, const sx_col& c, std::vector<uint8_t>& out) {
+  size_t bytes = (size_t)c.len * type_width(c.type);
+  out.resize(bytes + 16);
+  if (bytes) SX_CUDA(cudaMemcpyAsync(out.data(), c.data, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return SX_OK;
+}
+
+template <class T>
+T at(const std::vector<uint8_t>& v, int64_t i) {
+  T x;
+  std::memcpy(&x, v.data() + i * sizeof(T), sizeof(T));
+  return x;
+}
+
+int64_t key_at(const std::vector<uint8_t>& v, int type, int64_t i) {
+  switch (type) {
+    case SX_U8: return v[i];
+    case SX_I32: case SX_DATE32: return at<int32_t>(v, i);
+    default: return at<int64_t>(v, i);
+  }
+}
+
+sx_i128 i128_at(const std::vector<uint8_t>& v, int64_t i) {
+  sx_i128 r;
+  std::memcpy(&r, v.data() + 16 * i, 16);
+  return r;
+}
+
+// Gather `cols` by the permutation and copy them to host (one sync at the end).
+sx_status fetch_rows(sx_ctx* ctx, Bag& bag, const sx_col* cols, int n, const sx_sel& perm,
+                     std::vector<std::vector<uint8_t>>& host) {
+  host.assign(n, {});
+  for (int i = 0; i < n; ++i) {
+    sx_col g;
+    SX_TRY(sx_gather(ctx, &cols[i], &perm, &g));
+    bag.keep(g);
+    SX_TRY(d2h(ctx, g, host[i]));
+  }
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SX_OK;
+}
+
+__global__ void k_lookup_rank(const int32_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ rank_of,
+                              int32_t nrank, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k = keys[i];
+    out[i] = (k >= 0 && k < nrank) ? rank_of[k] : nrank + k;
+  }
+}
+
+static const char* kNation[25] = {"ALGERIA", "ARGENTINA", "BRAZIL", "CANADA", "EGYPT", "ETHIOPIA", "FRANCE",
+                                  "GERMANY", "INDIA", "INDONESIA", "IRAN", "IRAQ", "JAPAN", "JORDAN", "KENYA",
+                                  "MOROCCO", "MOZAMBIQUE", "PERU", "CHINA", "ROMANIA", "SAUDI ARABIA", "VIETNAM",
+                                  "RUSSIA", "UNITED KINGDOM", "UNITED STATES"};
+
+}  // namespace
+
+SX_EXPORT void sx_tpch_default_params(sx_tpch_params* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->q1_shipdate_max = 10471;
+  p->q3_segment = 1;
+  p->q3_date = 9204;
+  p->q6_date_lo = 8766;
+  p->q6_date_hi = 9131;
+  p->q6_disc_lo = 5;
+  p->q6_disc_hi = 7;
+  p->q6_qty_lt = 2400;
+  std::strcpy(p->q9_color, "green");
+  p->q18_qty_gt = 30000;
+  p->q3_limit = 10;
+  p->q18_limit = 100;
+}
+
+// ------------------------------------------------------------------------------------- Q1
+SX_EXPORT sx_status sx_tpch_q1(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tpch_params* p, sx_q1_row* out,
+                               int64_t cap, int64_t* nrows) {
+  if (!ctx || !t || !p || !nrows) return SX_EINVAL;
+  *nrows = 0;
+  ProfScope ps(ctx, "Q1");
+  Bag bag(ctx);
+  sx_col cols[7] = {t->l_shipdate, t->l_returnflag, t->l_linestatus, t->l_quantity, t->l_extendedprice, t->l_discount,
+                    t->l_tax};
+  sx_key keys[2] = {{1, SX_KEY_IDENTITY}, {2, SX_KEY_IDENTITY}};
+  sx_pred where = P(0, SX_LE, p->q1_shipdate_max);
+  sx_agg aggs[8] = {
+      A(SX_SUM, E1(1, {F(3)})),                                  // sum_qty            scale 2
+      A(SX_SUM, E1(1, {F(4)})),                                  // sum_base_price     scale 2
+      A(SX_SUM, E1(1, {F(4), F(5, -1, 100)})),                   // sum_disc_price     scale 4
+      A(SX_SUM, E1(1, {F(4), F(5, -1, 100), F(6, 1, 100)})),     // sum_charge         scale 6
+      A(SX_AVG, E1(1, {F(3)}), 2),                               // avg_qty
+      A(SX_AVG, E1(1, {F(4)}), 2),                               // avg_price
+      A(SX_AVG, E1(1, {F(5)}), 2),                               // avg_disc
+      Count()};                                                  // count_order
+  sx_col ok[2], oa[8];
+  int64_t ng = 0;
+  SX_TRY(sx_groupby_agg(ctx, cols, 7, keys, 2, nullptr, &where, 1, aggs, 8, nullptr, 4, ok, oa, &ng));
+  bag.keep(ok, 2);
+  bag.keep(oa, 8);
+  // order by l_returnflag, l_linestatus
+  sx_col sk[2] = {ok[0], ok[1]};
+  sx_sortkey sks[2] = {{0, 0}, {1, 0}};
+  sx_sel perm;
+  SX_TRY(sx_sort_topk(ctx, sk, 2, sks, 2, nullptr, -1, &perm));
+  bag.keep(perm);
+  sx_col all[10] = {ok[0], ok[1], oa[0], oa[1], oa[2], oa[3], oa[4], oa[5], oa[6], oa[7]};
+  std::vector<std::vector<uint8_t>> h;
+  SX_TRY(fetch_rows(ctx, bag, all, 10, perm, h));
+  if (perm.len > cap) return set_err(ctx, SX_EINVAL, "Q1: %lld rows > cap", (long long)perm.len);
+  for (int64_t i = 0; i < perm.len; ++i) {
+    sx_q1_row& r = out[i];
+    std::memset(&r, 0, sizeof r);
+    r.returnflag = h[0][i];
+    r.linestatus = h[1][i];
+    r.sum_qty = i128_at(h[2], i);
+    r.sum_base_price = i128_at(h[3], i);
+    r.sum_disc_price = i128_at(h[4], i);
+    r.sum_charge = i128_at(h[5], i);
+    r.avg_qty = at<double>(h[6], i);
+    r.avg_price = at<double>(h[7], i);
+    r.avg_disc = at<double>(h[8], i);
+    r.count_order = at<int64_t>(h[9], i);
+  }
+  *nrows = perm.len;
+  return SX_OK;
+}
+
+// ------------------------------------------------------------------------------------- Q6
+SX_EXPORT sx_status sx_tpch_q6(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tpch_params* p, sx_q6_row* out,
+                               int64_t* nrows) {
+  if (!ctx || !t || !p || !nrows || !out) return SX_EINVAL;
+  *nrows = 0;
+  ProfScope ps(ctx, "Q6");
+  Bag bag(ctx);
+  sx_col cols[4] = {t->l_shipdate, t->l_discount, t->l_quantity, t->l_extendedprice};
+  sx_pred where[4] = {P(0, SX_GE, p->q6_date_lo), P(0, SX_LT, p->q6_date_hi),
+                      P(1, SX_BETWEEN, p->q6_disc_lo, p->q6_disc_hi), P(2, SX_LT, p->q6_qty_lt)};
+  sx_agg aggs[2] = {A(SX_SUM, E1(1, {F(3), F(1)})), Count()};  // sum(l_extendedprice*l_discount) scale 4
+  sx_col oa[2];
+  int64_t ng = 0;
+  SX_TRY(sx_groupby_agg(ctx, cols, 4, nullptr, 0, nullptr, where, 4, aggs, 2, nullptr, 1, nullptr, oa, &ng));
+  bag.keep(oa, 2);
+  std::vector<uint8_t> hs, hc;
+  SX_TRY(d2h(ctx, oa[0], hs));
+  SX_TRY(d2h(ctx, oa[1], hc));
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memset(out, 0, sizeof *out);
+  out->revenue = i128_at(hs, 0);
+  out->is_null = at<int64_t>(hc, 0) == 0;
+  *nrows = 1;
+  return SX_OK;
+}
+
+// ------------------------------------------------------------------------------------- Q3
+SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tpch_params* p, sx_q3_row* out,
+                               int64_t cap, int64_t* nrows) {
+  if (!ctx || !t || !p || !nrows) return SX_EINVAL;
+  *nrows = 0;
+  ProfScope ps(ctx, "Q3");
+  Bag bag(ctx);
+  // 1. C = {c_custkey | c_mktsegment = SEGMENT}
+  sx_col ccols[2] = {t->c_custkey, t->c_mktsegment};
+  sx_pred cseg = P(1, SX_EQ, p->q3_segment);
+  sx_sel sel_c;
+  SX_TRY(sx_filter(ctx, ccols, 2, &cseg, 1, nullptr, nullptr, 0, &sel_c, nullptr));
+  bag.keep(sel_c);
+  int32_t k0 = 0;
+  sx_ht* ht_c;
+  SX_TRY(sx_hash_build(ctx, ccols, 2, &k0, 1, &sel_c, nullptr, 0, 1, &ht_c));
+  bag.keep(ht_c);
+  // 2. orders with o_orderdate < DATE and o_custkey in C (semi join), then build orderkey -> row
+  sx_col ocols[2] = {t->o_custkey, t->o_orderdate};
+  sx_pred odate = P(1, SX_LT, p->q3_date);
+  sx_sel sel_o;
+  SX_TRY(sx_hash_probe(ctx, ht_c, ocols, 2, &k0, 1, nullptr, &odate, 1, SX_SEMI, nullptr, 0, nullptr, 0, nullptr, 0,
+                       &sel_o, nullptr, nullptr));
+  bag.keep(sel_o);
+  sx_col okey[1] = {t->o_orderkey};
+  sx_ht* ht_o;
+  SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, 1, &ht_o));
+  bag.keep(ht_o);
+  // 3. lineitem with l_shipdate > DATE joined to those orders (unique build: ordered output)
+  sx_col lcols[4] = {t->l_orderkey, t->l_shipdate, t->l_extendedprice, t->l_discount};
+  sx_pred lship = P(1, SX_GT, p->q3_date);
+  sx_col bcols[2] = {t->o_orderdate, t->o_shippriority};
+  int32_t bp[2] = {0, 1}, pp[3] = {0, 2, 3};
+  sx_sel jp, jb;
+  sx_col pay[5];  // o_orderdate, o_shippriority, l_orderkey, ext, disc
+  SX_TRY(sx_hash_probe(ctx, ht_o, lcols, 4, &k0, 1, nullptr, &lship, 1, SX_INNER, bcols, 2, bp, 2, pp, 3, &jp, &jb, pay));
+  bag.keep(jp);
+  bag.keep(jb);
+  bag.keep(pay, 5);
+  // 4. group by l_orderkey: revenue = sum(ext*(100-disc)) [scale 4]; o_orderdate, o_shippriority are
+  //    functionally dependent on the key and carried with min() (reading R7)
+  sx_col gcols[5] = {pay[2], pay[3], pay[4], pay[0], pay[1]};
+  sx_key gk = {0, SX_KEY_IDENTITY};
+  sx_agg gaggs[3] = {A(SX_SUM, E1(1, {F(1), F(2, -1, 100)})), A(SX_MIN, E1(1, {F(3)})), A(SX_MIN, E1(1, {F(4)}))};
+  sx_col gok[1], goa[3];
+  int64_t ng = 0;
+  SX_TRY(sx_groupby_agg(ctx, gcols, 5, &gk, 1, nullptr, nullptr, 0, gaggs, 3, nullptr, jp.len / 2 + 1, gok, goa, &ng));
+  bag.keep(gok, 1);
+  bag.keep(goa, 3);
+  // 5. order by revenue desc, o_orderdate asc, l_orderkey asc (reading R6); limit
+  sx_col scols[3] = {goa[0], goa[1], gok[0]};
+  sx_sortkey sks[3] = {{0, 1}, {1, 0}, {2, 0}};
+  sx_sel perm;
+  SX_TRY(sx_sort_topk(ctx, scols, 3, sks, 3, nullptr, p->q3_limit, &perm));
+  bag.keep(perm);
+  sx_col all[4] = {gok[0], goa[0], goa[1], goa[2]};
+  std::vector<std::vector<uint8_t>> h;
+  SX_TRY(fetch_rows(ctx, bag, all, 4, perm, h));
+  if (perm.len > cap) return set_err(ctx, SX_EINVAL, "Q3: %lld rows > cap", (long long)perm.len);
+  for (int64_t i = 0; i < perm.len; ++i) {
+    out[i].l_orderkey = key_at(h[0], gok[0].type, i);
+    out[i].revenue = i128_at(h[1], i);
+    out[i].o_orderdate = (int32_t)at<int64_t>(h[2], i);
+    out[i].o_shippriority = (int32_t)at<int64_t>(h[3], i);
+  }
+  *nrows = perm.len;
+  return SX_OK;
+}
+
+// ------------------------------------------------------------------------------------- Q9
+SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tpch_params* p, sx_q9_row* out,
+                               int64_t cap, int64_t* nrows) {
+  if (!ctx || !t || !p || !nrows) return SX_EINVAL;
+  *nrows = 0;
+  ProfScope ps(ctx, "Q9");
+  Bag bag(ctx);
+  int32_t k0 = 0;
+  // 1. P = {p_partkey | p_name like '%COLOR%'}
+  sx_col pn[1] = {t->p_name};
+  sx_pred like = sx_pred{0, SX_CONTAINS, 0, 0, p->q9_color, (int32_t)strnlen(p->q9_color, sizeof p->q9_color), 0};
+  sx_sel sel_p;
+  SX_TRY(sx_filter(ctx, pn, 1, &like, 1, nullptr, nullptr, 0, &sel_p, nullptr));
+  bag.keep(sel_p);
+  sx_col pk[1] = {t->p_partkey};
+  sx_ht* ht_p;
+  SX_TRY(sx_hash_build(ctx, pk, 1, &k0, 1, &sel_p, nullptr, 0, 1, &ht_p));
+  bag.keep(ht_p);
+  // 2. lineitem semi-join P, materialising the columns the plan needs
+  sx_col lcols[6] = {t->l_partkey, t->l_suppkey, t->l_orderkey, t->l_quantity, t->l_extendedprice, t->l_discount};
+  int32_t lpp[6] = {0, 1, 2, 3, 4, 5};
+  sx_sel sel_l;
+  sx_col L2[6];
+  SX_TRY(sx_hash_probe(ctx, ht_p, lcols, 6, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0, lpp, 6, &sel_l,
+                       nullptr, L2));
+  bag.keep(sel_l);
+  bag.keep(L2, 6);
+  // 3. partsupp semi-join P, build (ps_partkey, ps_suppkey) -> row
+  sx_col pscols[3] = {t->ps_partkey, t->ps_suppkey, t->ps_supplycost};
+  sx_sel sel_ps;
+  SX_TRY(sx_hash_probe(ctx, ht_p, pscols, 3, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0, nullptr, 0,
+                       &sel_ps, nullptr, nullptr));
+  bag.keep(sel_ps);
+  int32_t k01[2] = {0, 1};
+  sx_ht* ht_ps;
+  SX_TRY(sx_hash_build(ctx, pscols, 3, k01, 2, &sel_ps, nullptr, 0, 1, &ht_ps));
+  bag.keep(ht_ps);
+  // 4. lineitem'' join partsupp on (partkey, suppkey) -> supplycost
+  int32_t bp4[1] = {2}, pp4[5] = {1, 2, 3, 4, 5};
+  sx_sel j4p, j4b;
+  sx_col L3[6];  // supplycost, suppkey, orderkey, qty, ext, disc
+  SX_TRY(sx_hash_probe(ctx, ht_ps, L2, 6, k01, 2, nullptr, nullptr, 0, SX_INNER, pscols, 3, bp4, 1, pp4, 5, &j4p, &j4b, L3));
+  bag.keep(j4p);
+  bag.keep(j4b);
+  bag.keep(L3, 6);
+  // 5. join supplier on suppkey -> s_nationkey
+  sx_col scols[2] = {t->s_suppkey, t->s_nationkey};
+  sx_ht* ht_s;
+  SX_TRY(sx_hash_build(ctx, scols, 2, &k0, 1, nullptr, nullptr, 0, 1, &ht_s));
+  bag.keep(ht_s);
+  int32_t ks = 1, bp5[1] = {1}, pp5[5] = {0, 2, 3, 4, 5};
+  sx_sel j5p, j5b;
+  sx_col L4[6];  // nationkey, supplycost, orderkey, qty, ext, disc
+  SX_TRY(sx_hash_probe(ctx, ht_s, L3, 6, &ks, 1, nullptr, nullptr, 0, SX_INNER, scols, 2, bp5, 1, pp5, 5, &j5p, &j5b, L4));
+  bag.keep(j5p);
+  bag.keep(j5b);
+  bag.keep(L4, 6);
+  // 6. join orders on orderkey -> o_orderdate (build the smaller side: lineitem'''s orderkeys)
+  int32_t kl = 2;
+  sx_ht* ht_l;
+  SX_TRY(sx_hash_build(ctx, L4, 6, &kl, 1, nullptr, nullptr, 0, 0, &ht_l));
+  bag.keep(ht_l);
+  sx_col ocols[2] = {t->o_orderkey, t->o_orderdate};
+  int32_t bp6[5] = {0, 1, 3, 4, 5}, pp6[1] = {1};
+  sx_sel j6p, j6b;
+  sx_col L5[6];  // nationkey, supplycost, qty, ext, disc, orderdate
+  SX_TRY(sx_hash_probe(ctx, ht_l, ocols, 2, &k0, 1, nullptr, nullptr, 0, SX_INNER, L4, 6, bp6, 5, pp6, 1, &j6p, &j6b, L5));
+  bag.keep(j6p);
+  bag.keep(j6b);
+  bag.keep(L5, 6);
+  // 7. group by (nation, year(o_orderdate)): sum(ext*(100-disc) - supplycost*qty) [scale 4]
+  sx_key gk[2] = {{0, SX_KEY_IDENTITY}, {5, SX_KEY_YEAR}};
+  sx_agg ga;
+  std::memset(&ga, 0, sizeof ga);
+  ga.op = SX_SUM;
+  ga.value.nterms = 2;
+  ga.value.t[0].coef = 1;
+  ga.value.t[0].nf = 2;
+  ga.value.t[0].f[0] = F(3);
+  ga.value.t[0].f[1] = F(4, -1, 100);
+  ga.value.t[1].coef = -1;
+  ga.value.t[1].nf = 2;
+  ga.value.t[1].f[0] = F(1);
+  ga.value.t[1].f[1] = F(2);
+  sx_col gok[2], goa[1];
+  int64_t ng = 0;
+  SX_TRY(sx_groupby_agg(ctx, L5, 6, gk, 2, nullptr, nullptr, 0, &ga, 1, nullptr, 256, gok, goa, &ng));
+  bag.keep(gok, 2);
+  bag.keep(goa, 1);
+  // 8. order by n_name asc (string order of the nation dimension), o_year desc
+  std::vector<int> order(25);
+  for (int i = 0; i < 25; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [](int a, int b) { return std::strcmp(kNation[a], kNation[b]) < 0; });
+  int32_t rank_h[25];
+  for (int r = 0; r < 25; ++r) rank_h[order[r]] = r;
+  int32_t *rank_d, *rk;
+  SX_TRY(alloc(ctx, &rank_d, 25));
+  bag.bufs.push_back(rank_d);
+  SX_CUDA(cudaMemcpyAsync(rank_d, rank_h, sizeof rank_h, cudaMemcpyHostToDevice, ctx->stream));
+  SX_TRY(alloc(ctx, &rk, (size_t)(ng > 0 ? ng : 1)));
+  bag.bufs.push_back(rk);
+  if (ng > 0) k_lookup_rank<<<(unsigned)((ng + 255) / 256), 256, 0, ctx->stream>>>((const int32_t*)gok[0].data, ng, rank_d, 25, rk);
+  SX_CHECK_LAUNCH();
+  sx_col scol[2] = {sx_col{SX_I32, 0, ng, rk, nullptr, nullptr}, gok[1]};
+  sx_sortkey sks[2] = {{0, 0}, {1, 1}};
+  sx_sel perm;
+  SX_TRY(sx_sort_topk(ctx, scol, 2, sks, 2, nullptr, -1, &perm));
+  bag.keep(perm);
+  sx_col all[3] = {gok[0], gok[1], goa[0]};
+  std::vector<std::vector<uint8_t>> h;
+  SX_TRY(fetch_rows(ctx, bag, all, 3, perm, h));
+  if (perm.len > cap) return set_err(ctx, SX_EINVAL, "Q9: %lld rows > cap", (long long)perm.len);
+  for (int64_t i = 0; i < perm.len; ++i) {
+    out[i].nationkey = at<int32_t>(h[0], i);
+    out[i].o_year = at<int32_t>(h[1], i);
+    out[i].sum_profit = i128_at(h[2], i);
+  }
+  *nrows = perm.len;
+  return SX_OK;
+}
+
+// ------------------------------------------------------------------------------------- Q18
+SX_EXPORT sx_status sx_tpch_q18(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tpch_params* p, sx_q18_row* out,
+                                int64_t cap, int64_t* nrows) {
+  if (!ctx || !t || !p || !nrows) return SX_EINVAL;
+  *nrows = 0;
+  ProfScope ps(ctx, "Q18");
+  Bag bag(ctx);
+  int32_t k0 = 0;
+  // 1. subquery: l_orderkey groups with sum(l_quantity) > QUANTITY
+  sx_col lcols[2] = {t->l_orderkey, t->l_quantity};
+  sx_key gk = {0, SX_KEY_IDENTITY};
+  sx_agg ga = A(SX_SUM, E1(1, {F(1)}));
+  sx_having hv = {0, SX_GT, p->q18_qty_gt, 0};
+  sx_col gok[1], goa[1];
+  int64_t ng = 0;
+  SX_TRY(sx_groupby_agg(ctx, lcols, 2, &gk, 1, nullptr, nullptr, 0, &ga, 1, &hv, t->o_orderkey.len, gok, goa, &ng));
+  bag.keep(gok, 1);
+  bag.keep(goa, 1);
+  // 2. orders with o_orderkey in that set; carry sum(l_quantity) from the group-by (equal to the
+  //    literal re-aggregation over the joined lineitems; reading for Q18)
+  sx_col big[2] = {gok[0], goa[0]};
+  sx_ht* ht_b;
+  SX_TRY(sx_hash_build(ctx, big, 2, &k0, 1, nullptr, nullptr, 0, 1, &ht_b));
+  bag.keep(ht_b);
+  sx_col ocols[4] = {t->o_orderkey, t->o_custkey, t->o_orderdate, t->o_totalprice};
+  int32_t bp[1] = {1}, pp[4] = {0, 1, 2, 3};
+  sx_sel jp, jb;
+  sx_col C[5];  // sum_qty, orderkey, custkey, orderdate, totalprice
+  SX_TRY(sx_hash_probe(ctx, ht_b, ocols, 4, &k0, 1, nullptr, nullptr, 0, SX_INNER, big, 2, bp, 1, pp, 4, &jp, &jb, C));
+  bag.keep(jp);
+  bag.keep(jb);
+  bag.keep(C, 5);
+  // 3. join customer on custkey (build the small candidate side)
+  int32_t kc = 2;
+  sx_ht* ht_c;
+  SX_TRY(sx_hash_build(ctx, C, 5, &kc, 1, nullptr, nullptr, 0, 0, &ht_c));
+  bag.keep(ht_c);
+  sx_col cc[1] = {t->c_custkey};
+  int32_t bp3[5] = {0, 1, 2, 3, 4};
+  sx_sel j3p, j3b;
+  sx_col R[5];
+  SX_TRY(sx_hash_probe(ctx, ht_c, cc, 1, &k0, 1, nullptr, nullptr, 0, SX_INNER, C, 5, bp3, 5, nullptr, 0, &j3p, &j3b, R));
+  bag.keep(j3p);
+  bag.keep(j3b);
+  bag.keep(R, 5);
+  // 4. order by o_totalprice desc, o_orderdate asc, o_orderkey asc (reading R6); limit
+  sx_col scols[3] = {R[4], R[3], R[1]};
+  sx_sortkey sks[3] = {{0, 1}, {1, 0}, {2, 0}};
+  sx_sel perm;
+  SX_TRY(sx_sort_topk(ctx, scols, 3, sks, 3, nullptr, p->q18_limit, &perm));
+  bag.keep(perm);
+  std::vector<std::vector<uint8_t>> h;
+  SX_TRY(fetch_rows(ctx, bag, R, 5, perm, h));
+  if (perm.len > cap) return set_err(ctx, SX_EINVAL, "Q18: %lld rows > cap", (long long)perm.len);
+  for (int64_t i = 0; i < perm.len; ++i) {
+    out[i].o_orderkey = key_at(h[1], R[1].type, i);
+    out[i].c_custkey = at<int32_t>(h[2], i);
+    out[i].o_orderdate = at<int32_t>(h[3], i);
+    out[i].o_totalprice = at<int64_t>(h[4], i);
+    out[i].sum_qty = i128_at(h[0], i);
+  }
+  *nrows = perm.len;
+  return SX_OK;
+}

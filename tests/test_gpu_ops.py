@@ -1,0 +1,287 @@
+"""Operator parity: libsx CUDA kernels (through the C ABI) vs the CPU oracle, element by element.
+
+Sizes span several tiles (2048 rows per compaction tile) with ragged tails; edge cases:
+empty input, all/none selected, duplicate keys, negative and extreme keys, key 0 (the
+aggregation table's EMPTY value), one group, every row its own group.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2508_04701_b200 as sx  # noqa: E402
+from paper_2508_04701_b200 import _abi as A  # noqa: E402
+
+SIZES = [0, 1, 2047, 2048, 2049, 100_003]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return sx.Ctx(0)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def c(t, typ=None):
+    return sx.col(t, typ)
+
+
+def i128_rows(t):
+    a = t.cpu().numpy()
+    return [(int(lo) & ((1 << 64) - 1)) | (int(hi) << 64) for lo, hi in a]
+
+
+# ------------------------------------------------------------------------------------- filter
+@pytest.mark.parametrize("n", SIZES)
+def test_filter_conjunction(ctx, n):
+    rng = np.random.default_rng(n + 1)
+    a = rng.integers(-100, 100, n).astype(np.int32)
+    b = rng.integers(0, 256, n).astype(np.uint8)
+    d = rng.integers(-(2**62), 2**62, n).astype(np.int64)
+    ta, tb, td = dev(a), dev(b), dev(d)
+    cols = [c(ta), c(tb), c(td)]
+    for conj in ([(0, "ge", -10), (1, "ne", 7), (2, "gt", 0)], [(0, "between", -5, 5)], [(1, "eq", 3)],
+                 [(2, "le", -(2**61)), (0, "lt", 50)], []):
+        sel, gathered = ctx.filter(cols, conj, gather=[0, 2])
+        want = oracle.filter([a, b, d], conj) if conj else np.arange(n, dtype=np.int32)
+        assert np.array_equal(sel.cpu().numpy(), want)
+        assert np.array_equal(gathered[0].cpu().numpy(), a[want])
+        assert np.array_equal(gathered[1].cpu().numpy(), d[want])
+
+
+def test_filter_in_sel(ctx):
+    rng = np.random.default_rng(5)
+    n = 50_000
+    a = rng.integers(0, 1000, n).astype(np.int64)
+    base = np.sort(rng.choice(n, 20_000, replace=False)).astype(np.int32)
+    sel, _ = ctx.filter([c(dev(a))], [(0, "lt", 300)], in_sel=dev(base))
+    assert np.array_equal(sel.cpu().numpy(), base[a[base] < 300])
+
+
+@pytest.mark.parametrize("pattern", [b"green", b"g", b"zz", b"een ap"])
+def test_filter_contains(ctx, pattern):
+    import gen
+
+    p = gen.cpu_tables(20, seed=3, tables=("part",))["part"]
+    offs, chars = p["p_name_offsets"], p["p_name_chars"]
+    sel, _ = ctx.filter([sx.col(dev(chars), A.SX_STR, offsets=dev(offs))], [(0, "contains", pattern)])
+    assert np.array_equal(sel.cpu().numpy(), oracle.contains(offs, chars, pattern))
+
+
+# ------------------------------------------------------------------------------------- group-by
+def canon(keys, aggs, ops):
+    """GPU outputs -> rows sorted by key (canonical ORDER BY)."""
+    cols = [k.cpu().numpy().astype(np.int64).tolist() for k in keys]
+    vals = []
+    for t, op in zip(aggs, ops):
+        if op == "sum":
+            vals.append(i128_rows(t))
+        elif op == "avg":
+            vals.append(t.cpu().numpy().tolist())
+        else:
+            vals.append(t.cpu().numpy().tolist())
+    rows = list(zip(*cols, *vals)) if (cols or vals) else []
+    return sorted(rows, key=lambda r: r[: len(keys)])
+
+
+def check_gb(got, want):
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        for x, y in zip(g, w):
+            if isinstance(y, float):
+                assert abs(x - y) <= 1e-9 * max(1.0, abs(y)), (g, w)
+            else:
+                assert x == y, (g, w)
+
+
+AGGS = [("sum", [(1, [(2, 1, 0), (3, -1, 100)])]), ("count", []), ("min", [(1, [(2, 1, 0)])]),
+        ("max", [(1, [(2, 1, 0)])]), ("avg", [(1, [(3, 1, 0)])], 2), ("sum", [(1, [(2, 1, 0)]), (-3, [(3, 1, 7)])])]
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("ng,hint", [(3, 4), (4, 4), (300, 512), (5000, 0), (None, 0)])
+def test_groupby_one_key(ctx, n, ng, hint):
+    rng = np.random.default_rng(n + (ng or 0))
+    dom = ng if ng else max(n, 1)
+    k = rng.integers(-(dom // 2), dom - dom // 2, n).astype(np.int32)  # includes key 0 (EMPTY) and negatives
+    v = rng.integers(-(10**12), 10**12, n).astype(np.int64)
+    w = rng.integers(0, 100, n).astype(np.int64)
+    cols = [c(dev(k)), c(dev(k)), c(dev(v)), c(dev(w))]
+    keys, aggs, g = ctx.groupby(cols, [(0, "id")], AGGS, groups_hint=hint)
+    got = canon(keys, aggs, [a[0] for a in AGGS])
+    want = oracle.groupby([k, k, v, w], [0], AGGS)
+    check_gb(got, want)
+    assert g == len(want)
+
+
+@pytest.mark.parametrize("hint", [4, 64])
+def test_groupby_two_u8_keys_where(ctx, hint):
+    rng = np.random.default_rng(11)
+    n = 70_001
+    a = rng.choice(np.array([ord("A"), ord("N"), ord("R")], np.uint8), n)
+    b = rng.choice(np.array([ord("F"), ord("O")], np.uint8), n)
+    s = rng.integers(0, 100, n).astype(np.int32)
+    v = rng.integers(0, 10**9, n).astype(np.int64)
+    cols = [c(dev(a)), c(dev(b)), c(dev(s)), c(dev(v))]
+    aggs = [("sum", [(1, [(3, 1, 0), (2, -1, 100)])]), ("avg", [(1, [(3, 1, 0)])], 2), ("count", [])]
+    keys, outs, g = ctx.groupby(cols, [(0, "id"), (1, "id")], aggs, where=[(2, "le", 80)], groups_hint=hint)
+    got = canon(keys, outs, [x[0] for x in aggs])
+    m = s <= 80
+    want = oracle.groupby([a[m], b[m], s[m], v[m]], [0, 1], aggs)
+    check_gb(got, want)
+
+
+def test_groupby_year_key_and_i64_key(ctx):
+    rng = np.random.default_rng(12)
+    n = 40_000
+    d = rng.integers(-1000, 20000, n).astype(np.int32)
+    k64 = rng.integers(-(2**62), 2**62, n).astype(np.int64) // 1000 * 1000
+    k64[::7] = 0
+    v = rng.integers(-1000, 1000, n).astype(np.int64)
+    cols = [sx.col(dev(d), A.SX_DATE32), c(dev(v)), c(dev(k64))]
+    keys, outs, g = ctx.groupby(cols, [(0, "year")], [("sum", [(1, [(1, 1, 0)])])], groups_hint=64)
+    years = np.array([oracle.civil_year(int(x)) for x in d], np.int64)
+    want = oracle.groupby([years, v], [0], [("sum", [(1, [(1, 1, 0)])])])
+    check_gb(canon(keys, outs, ["sum"]), want)
+    keys, outs, g = ctx.groupby(cols, [(2, "id")], [("count", []), ("max", [(1, [(1, 1, 0)])])], groups_hint=n)
+    want = oracle.groupby([k64, v], [0], [("count", []), ("max", [(1, [(1, 1, 0)])])])
+    check_gb(canon(keys, outs, ["count", "max"]), want)
+
+
+@pytest.mark.parametrize("n", [0, 1, 5000, 100_003])
+def test_groupby_keyless_reduce(ctx, n):
+    rng = np.random.default_rng(n)
+    a = rng.integers(0, 100, n).astype(np.int32)
+    v = rng.integers(-(10**15), 10**15, n).astype(np.int64)
+    cols = [c(dev(a)), c(dev(v))]
+    aggs = [("sum", [(1, [(1, 1, 0)])]), ("count", []), ("min", [(1, [(1, 1, 0)])])]
+    keys, outs, g = ctx.groupby(cols, [], aggs, where=[(0, "lt", 40)])
+    assert g == 1
+    m = a < 40
+    cnt = int(outs[1].cpu().item())
+    assert cnt == int(m.sum())
+    if cnt:
+        assert i128_rows(outs[0])[0] == sum(int(x) for x in v[m])
+        assert int(outs[2].cpu().item()) == int(v[m].min())
+
+
+def test_groupby_having_and_sel(ctx):
+    rng = np.random.default_rng(21)
+    n = 200_000
+    k = np.sort(rng.integers(1, 40_000, n)).astype(np.int32)  # clustered keys (run pre-reduction)
+    q = rng.integers(1, 51, n).astype(np.int64) * 100
+    base = np.sort(rng.choice(n, n // 2, replace=False)).astype(np.int32)
+    cols = [c(dev(k)), c(dev(q))]
+    keys, outs, g = ctx.groupby(cols, [(0, "id")], [("sum", [(1, [(1, 1, 0)])])], in_sel=dev(base),
+                                having=(0, "gt", 1200), groups_hint=40_000)
+    want = [r for r in oracle.groupby([k[base], q[base]], [0], [("sum", [(1, [(1, 1, 0)])])]) if r[1] > 1200]
+    check_gb(canon(keys, outs, ["sum"]), want)
+
+
+def test_groupby_expression_overflow_is_an_error(ctx):
+    v = np.array([2**62, 3], np.int64)
+    with pytest.raises(sx.SxError) as e:
+        ctx.groupby([c(dev(v))], [], [("sum", [(4, [(0, 1, 0)])])])
+    assert e.value.status == A.SX_EOVERFLOW
+
+
+# ------------------------------------------------------------------------------------- joins
+@pytest.mark.parametrize("nb,np_,dom", [(0, 100, 10), (1, 1, 1), (3000, 5000, 1000), (20_000, 100_003, 40_000),
+                                        (5000, 70_000, 2**40)])
+def test_join_types(ctx, nb, np_, dom):
+    rng = np.random.default_rng(nb + np_)
+    dt = np.int64 if dom > 2**31 else np.int32
+    bk = rng.integers(-dom, dom, nb).astype(dt)
+    pk = rng.integers(-dom, dom, np_).astype(dt)
+    bpay = rng.integers(0, 10**9, nb).astype(np.int64)
+    ppay = rng.integers(0, 255, np_).astype(np.uint8)
+    tb, tp = dev(bk), dev(pk)
+    ht = ctx.hash_build([c(tb), c(dev(bpay))], [0])
+    assert ht.rows == nb
+    p, b, pay = ctx.hash_probe(ht, [c(tp), c(dev(ppay))], [0], "inner", build_cols=[c(tb), c(dev(bpay))], bp=[1], pp=[1])
+    wp, wb = oracle.join(bk, pk, "inner")
+    got = sorted(zip(p.cpu().numpy().tolist(), b.cpu().numpy().tolist()))
+    assert got == sorted(zip(wp.tolist(), wb.tolist()))
+    pr, br = p.cpu().numpy(), b.cpu().numpy()
+    assert np.array_equal(pay[0].cpu().numpy(), bpay[br]) and np.array_equal(pay[1].cpu().numpy(), ppay[pr])
+    s, _, _ = ctx.hash_probe(ht, [c(tp)], [0], "semi")
+    assert np.array_equal(s.cpu().numpy(), oracle.join(bk, pk, "semi"))
+    a, _, _ = ctx.hash_probe(ht, [c(tp)], [0], "anti")
+    assert np.array_equal(a.cpu().numpy(), oracle.join(bk, pk, "anti"))
+
+
+def test_join_unique_build_two_keys_where(ctx):
+    rng = np.random.default_rng(3)
+    nb = 30_000
+    k1 = rng.integers(1, 5000, nb).astype(np.int32)
+    k2 = rng.integers(1, 1000, nb).astype(np.int32)
+    packed = (k1.astype(np.int64) << 32) | k2.astype(np.int64)
+    _, first = np.unique(packed, return_index=True)
+    k1, k2 = k1[np.sort(first)], k2[np.sort(first)]
+    nb = len(k1)
+    cost = rng.integers(100, 100000, nb).astype(np.int64)
+    n = 150_000
+    idx = rng.integers(0, nb, n)
+    p1, p2 = k1[idx].copy(), k2[idx].copy()
+    p2[::5] += 1000  # misses
+    f = rng.integers(0, 10, n).astype(np.int32)
+    ht = ctx.hash_build([c(dev(k1)), c(dev(k2)), c(dev(cost))], [0, 1], unique=True)
+    p, b, pay = ctx.hash_probe(ht, [c(dev(p1)), c(dev(p2)), c(dev(f))], [0, 1], "inner", where=[(2, "lt", 7)],
+                               build_cols=[c(dev(k1)), c(dev(k2)), c(dev(cost))], bp=[2], pp=[2])
+    bpk = (k1.astype(np.int64) << 32) | k2.astype(np.int64)
+    ppk = (p1.astype(np.int64) << 32) | p2.astype(np.int64)
+    wp, wb = oracle.join(bpk, np.where(f < 7, ppk, np.int64(-1)), "inner")
+    # unique build: output is ordered by probe row
+    assert np.array_equal(p.cpu().numpy(), wp) and np.array_equal(b.cpu().numpy(), wb)
+    assert np.array_equal(pay[0].cpu().numpy(), cost[wb])
+    assert np.array_equal(pay[1].cpu().numpy(), f[wp])
+
+
+# ------------------------------------------------------------------------------------- sort / top-k
+def as_i128_tensor(vals):
+    arr = np.array([[v & ((1 << 64) - 1), v >> 64] for v in vals], dtype=object)
+    lo = np.array([int(x) if x < 2**63 else int(x) - 2**64 for x in arr[:, 0]], np.int64) if len(vals) else np.zeros(0, np.int64)
+    hi = np.array([int(x) for x in arr[:, 1]], np.int64) if len(vals) else np.zeros(0, np.int64)
+    return torch.from_numpy(np.stack([lo, hi], axis=1) if len(vals) else np.zeros((0, 2), np.int64)).cuda()
+
+
+@pytest.mark.parametrize("n", [1, 2, 1000, 2048, 2049, 50_000, 300_001])
+@pytest.mark.parametrize("k", [-1, 1, 10, 100, 1024])
+def test_sort_topk(ctx, n, k):
+    rng = np.random.default_rng(n * 7 + k)
+    a = rng.integers(0, 5, n).astype(np.int32)  # many ties -> stability matters
+    b = [int(x) for x in rng.integers(-(2**40), 2**40, n)]
+    b = [x * (2**50) + 3 for x in b]  # beyond int64: exercise I128 words
+    d = rng.integers(8000, 10500, n).astype(np.int32)
+    u = rng.integers(0, 256, n).astype(np.uint8)
+    cols = [sx.col(dev(a), A.SX_I32), sx.col(as_i128_tensor(b), A.SX_I128), sx.col(dev(d), A.SX_DATE32), c(dev(u))]
+    for keys in ([(0, 0), (1, 1)], [(1, 1), (2, 0)], [(3, 1)], [(2, 0), (0, 1), (3, 0)]):
+        perm = ctx.sort_topk(cols, keys, k)
+        src = [a.tolist(), b, d.tolist(), u.tolist()]
+        want = oracle.sort([src[i] for i, _ in keys], [1 if dd else 0 for _, dd in keys], k)
+        assert np.array_equal(perm.cpu().numpy(), want), keys
+
+
+def test_sort_with_sel(ctx):
+    rng = np.random.default_rng(8)
+    n = 20_000
+    v = rng.integers(-1000, 1000, n).astype(np.int64)
+    base = np.sort(rng.choice(n, 7000, replace=False)).astype(np.int32)
+    perm = ctx.sort_topk([c(dev(v))], [(0, 1)], 50, in_sel=dev(base))
+    want = base[oracle.sort([v[base].tolist()], [1], 50)]
+    assert np.array_equal(perm.cpu().numpy(), want)
+
+
+def test_gather(ctx):
+    rng = np.random.default_rng(1)
+    v = rng.integers(-5, 5, 10_000).astype(np.int64)
+    s = rng.integers(0, 10_000, 777).astype(np.int32)
+    assert np.array_equal(ctx.gather(c(dev(v)), dev(s)).cpu().numpy(), v[s])

@@ -1,0 +1,100 @@
+"""Query parity: the fixed-plan executor (sx_tpch_q*, through the C ABI) vs the CPU oracle on the
+same seeded TPC-H-shaped data.  Integer/decimal outputs bit-exact, avg within 1e-9 relative
+(north_star).  Small SF: oracle computed live; larger SF: oracle answers committed under
+tests/golden/ by oracle/make_answers.py.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from tests.helpers import GOLDEN, diff_rows, golden_tables, load_golden, rows_equal
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2508_04701_b200 as sx  # noqa: E402
+from paper_2508_04701_b200 import tpch  # noqa: E402
+
+QUERIES = ["q1", "q6", "q3", "q9", "q18"]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return sx.Ctx(0)
+
+
+def to_dev(t):
+    return {tn: {cn: torch.from_numpy(np.ascontiguousarray(a)).cuda() for cn, a in cols.items()}
+            for tn, cols in t.items()}
+
+
+@pytest.mark.parametrize("name", ["q1", "q6", "q6_empty", "q3", "q9", "q18"])
+def test_hand_tables(ctx, name):
+    case = load_golden("hand_queries.json")[name]
+    q = name.split("_")[0]
+    host = golden_tables(case["tables"], key_dtype=np.int32)
+    got = tpch.Tpch(ctx, to_dev(host)).run(q)
+    want = [tuple(r) for r in case["answer"]]
+    assert rows_equal(got, want), diff_rows(got, want)
+
+
+@pytest.fixture(scope="module", params=[10, 100])
+def small(request, ctx):
+    host = gen.cpu_tables(request.param, seed=42)
+    return request.param, host, tpch.Tpch(ctx, to_dev(host))
+
+
+@pytest.mark.parametrize("q", QUERIES)
+def test_query_vs_live_oracle(small, q):
+    sfm, host, T = small
+    want = oracle.run_query(q, host)
+    got = T.run(q)
+    assert rows_equal(got, want), diff_rows(got, want)
+
+
+def test_query_params_vs_oracle(small):
+    sfm, host, T = small
+    for over in (dict(q18_qty_gt=25000), dict(q18_qty_gt=20000)):
+        got = T.run("q18", tpch.default_params(**over))
+        want = oracle.run_query("q18", host, oracle.default_params(**over))
+        assert rows_equal(got, want), diff_rows(got, want)
+    got = T.run("q3", tpch.default_params(q3_limit=500, q3_date=9500, q3_segment=3))
+    want = oracle.run_query("q3", host, oracle.default_params(q3_date=9500, q3_segment=3), limit=500)
+    assert rows_equal(got, want), diff_rows(got, want)
+    got = T.run("q9", tpch.default_params(q9_color="blue"))
+    want = oracle.run_query("q9", host, oracle.default_params(q9_color="blue"))
+    assert rows_equal(got, want), diff_rows(got, want)
+
+
+def test_gpu_generator_matches_cpu_generator():
+    cpu = gen.cpu_tables(10, seed=42)
+    g = gen.gpu_tables(10, seed=42)
+    for t in cpu:
+        for cname in cpu[t]:
+            assert np.array_equal(g[t][cname].cpu().numpy(), cpu[t][cname]), (t, cname)
+
+
+@pytest.mark.parametrize("sfm", [1000, 10000])
+def test_query_vs_committed_answers(ctx, sfm):
+    path = os.path.join(GOLDEN, f"answers_sf{sfm}_seed42.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    ans = json.load(open(path))
+    T = tpch.Tpch(ctx, gen.gpu_tables(sfm, seed=42))
+    for q in QUERIES:
+        if q not in ans["answers"]:
+            continue
+        want = [tuple(r) for r in ans["answers"][q]]
+        if q == "q9":
+            want = [(oracle.NATIONS[r[0]], r[1], r[2]) for r in want]
+        if q == "q18":
+            want = [(oracle.c_name(r[0]),) + tuple(r) for r in want]
+        got = T.run(q)
+        assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
