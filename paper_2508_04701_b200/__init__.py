@@ -52,8 +52,10 @@ def col(t, type: int | None = None, scale: int = 0, offsets=None) -> A.Col:
     if type is None:
         type = _DTYPE_TYPE[str(t.dtype)]
     n = t.shape[0] if type != A.SX_STR else offsets.shape[0] - 1
-    return A.Col(type, scale, n, t.data_ptr() if t.numel() else None,
-                 offsets.data_ptr() if offsets is not None else None, None)
+    c = A.Col(type, scale, n, t.data_ptr() if t.numel() else None,
+              offsets.data_ptr() if offsets is not None else None, None)
+    c._keep = (t, offsets)  # the struct borrows the tensors' memory: keep them alive with it
+    return c
 
 
 def expr(terms) -> A.Expr:

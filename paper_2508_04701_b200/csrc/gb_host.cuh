@@ -57,7 +57,8 @@ inline sx_status gb_plan(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_ke
     kbits_total += b;
   }
   Layout& L = P->L;
-  L.key_bytes = nkeys == 0 ? 0 : (kbits_total <= 32 ? 4 : 8);
+  // two keys are packed as (k0 << 32) | k1, so they always need the 8-byte key field
+  L.key_bytes = nkeys == 0 ? 0 : (nkeys == 1 && kbits_total <= 32 ? 4 : 8);
   // states
   int nst = 0;
   P->count_state = -1;

@@ -318,6 +318,7 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
   unsigned* diff;
   SX_TRY(scr.get(&diff, kMaxWords));
   SX_CUDA(cudaMemsetAsync(diff, 0, kMaxWords * sizeof(unsigned), ctx->stream));
+  ea.diff = diff;
   k_encode<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(ea);
   SX_CHECK_LAUNCH();
   const int32_t* sel = in_sel ? in_sel->idx : nullptr;
