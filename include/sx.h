@@ -91,6 +91,8 @@ sx_status sx_free(sx_ctx* ctx, void* p);       /* stream-ordered free of any lib
 sx_status sx_sync(sx_ctx* ctx);                /* wait for the ctx stream */
 /* Stream-ordered copy between any two pointers (cudaMemcpyDefault); binding helper. */
 sx_status sx_memcpy(sx_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* Number of CUDA kernels libsx launched on this ctx since the last reset (reset != 0 zeroes it). */
+int64_t sx_launch_count(sx_ctx* ctx, int reset);
 /* Per-operator device timing (CUDA events around each sx_* call; Fig. 5 analog). */
 sx_status sx_profile_enable(sx_ctx* ctx, int on);
 /* Fills up to cap entries of (name, milliseconds) for calls since the last read; returns count in *n. */

@@ -113,7 +113,7 @@ class Q18Row(C.Structure):
 
 # every symbol include/sx.h declares (checked by tests/test_abi.py)
 EXPORTS = ["sx_ctx_create", "sx_ctx_destroy", "sx_last_error", "sx_free", "sx_sync", "sx_memcpy", "sx_profile_enable",
-           "sx_profile_read", "sx_filter", "sx_groupby_agg", "sx_hash_build", "sx_hash_probe", "sx_ht_rows",
+           "sx_profile_read", "sx_launch_count", "sx_filter", "sx_groupby_agg", "sx_hash_build", "sx_hash_probe", "sx_ht_rows",
            "sx_ht_destroy", "sx_sort_topk", "sx_gather", "sx_tpch_default_params", "sx_tpch_q1", "sx_tpch_q6",
            "sx_tpch_q3", "sx_tpch_q9", "sx_tpch_q18"]
 
@@ -134,6 +134,8 @@ def load(path: str = LIB_PATH):
     L.sx_sync.argtypes = [vp]
     L.sx_memcpy.argtypes = [vp, vp, vp, C.c_size_t]
     L.sx_profile_enable.argtypes = [vp, i32]
+    L.sx_launch_count.argtypes = [vp, i32]
+    L.sx_launch_count.restype = i64
     L.sx_profile_read.argtypes = [vp, vp, vp, i32, P(C.c_int)]
     L.sx_filter.argtypes = [vp, P(Col), i32, P(Pred), i32, P(Sel), vp, i32, P(Sel), P(Col)]
     L.sx_groupby_agg.argtypes = [vp, P(Col), i32, P(Key), i32, P(Sel), P(Pred), i32, P(Agg), i32, P(Having), i64,

@@ -34,6 +34,7 @@ struct sx_ctx {
   unsigned int* d_counters = nullptr;  // tile counters etc. (64 entries)
   int64_t* h_pinned = nullptr;     // pinned host scratch for size reads (64 entries)
   bool profile = false;
+  int64_t launches = 0;            // kernels launched by libsx on this ctx (sx_launch_count)
   struct Prof { char name[32]; cudaEvent_t a, b; };
   std::vector<Prof> prof;
 };
@@ -69,6 +70,10 @@ inline sx_status set_err(sx_ctx* c, sx_status s, const char* fmt, ...) {
   } while (0)
 
 #define SX_CHECK_LAUNCH() SX_CUDA(cudaGetLastError())
+
+// Launch-configuration stream argument that also counts the launch (evaluated only when the
+// launch statement executes).
+#define SX_STREAM(c) ((++(c)->launches), (c)->stream)
 
 #define SX_TRY(expr)                    \
   do {                                  \

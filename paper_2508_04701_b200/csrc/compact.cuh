@@ -108,9 +108,9 @@ sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel,
   SX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), ctx->stream));
   unsigned grid = persistent_grid(ctx, 8, ntiles);
   if (in_sel)
-    k_compact<F, true, ITEMS><<<grid, kBlock, 0, ctx->stream>>>(f, n, in_sel, out_sel, out_aux, gs, status, ctr, ntiles);
+    k_compact<F, true, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, out_sel, out_aux, gs, status, ctr, ntiles);
   else
-    k_compact<F, false, ITEMS><<<grid, kBlock, 0, ctx->stream>>>(f, n, in_sel, out_sel, out_aux, gs, status, ctr, ntiles);
+    k_compact<F, false, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, out_sel, out_aux, gs, status, ctr, ntiles);
   SX_CHECK_LAUNCH();
   int64_t last;
   SX_TRY(read_i64(ctx, status + (ntiles - 1), &last));

@@ -109,10 +109,10 @@ SX_EXPORT sx_status sx_gather(sx_ctx* ctx, const sx_col* col, const sx_sel* sel,
   unsigned grid = persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock);
   if (n > 0) {
     switch (w) {
-      case 1: k_gather<uint8_t><<<grid, kBlock, 0, ctx->stream>>>((const uint8_t*)col->data, sel->idx, n, (uint8_t*)dst); break;
-      case 4: k_gather<int32_t><<<grid, kBlock, 0, ctx->stream>>>((const int32_t*)col->data, sel->idx, n, (int32_t*)dst); break;
-      case 8: k_gather<long long><<<grid, kBlock, 0, ctx->stream>>>((const long long*)col->data, sel->idx, n, (long long*)dst); break;
-      default: k_gather<longlong2><<<grid, kBlock, 0, ctx->stream>>>((const longlong2*)col->data, sel->idx, n, (longlong2*)dst); break;
+      case 1: k_gather<uint8_t><<<grid, kBlock, 0, SX_STREAM(ctx)>>>((const uint8_t*)col->data, sel->idx, n, (uint8_t*)dst); break;
+      case 4: k_gather<int32_t><<<grid, kBlock, 0, SX_STREAM(ctx)>>>((const int32_t*)col->data, sel->idx, n, (int32_t*)dst); break;
+      case 8: k_gather<long long><<<grid, kBlock, 0, SX_STREAM(ctx)>>>((const long long*)col->data, sel->idx, n, (long long*)dst); break;
+      default: k_gather<longlong2><<<grid, kBlock, 0, SX_STREAM(ctx)>>>((const longlong2*)col->data, sel->idx, n, (longlong2*)dst); break;
     }
   }
   cudaError_t e = cudaGetLastError();
@@ -132,4 +132,11 @@ SX_EXPORT sx_status sx_memcpy(sx_ctx* ctx, void* dst, const void* src, size_t by
   if (!ctx) return SX_EINVAL;
   if (bytes) SX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
   return SX_OK;
+}
+
+SX_EXPORT int64_t sx_launch_count(sx_ctx* ctx, int reset) {
+  if (!ctx) return -1;
+  int64_t n = ctx->launches;
+  if (reset) ctx->launches = 0;
+  return n;
 }

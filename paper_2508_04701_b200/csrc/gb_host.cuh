@@ -283,8 +283,8 @@ sx_status gb_run(sx_ctx* ctx, const RowFn& fn, const GbPlan& P, const int32_t* s
     Table t{table, keyless ? 0 : cap - 1, ctx->d_flags + 2, ctx->d_flags + 1};
     if (n > 0) {
       unsigned grid = persistent_grid(ctx, 4, (n + kBlock - 1) / kBlock);
-      if (small) k_gb_small<RowFn, 4, kMaxStates><<<grid, kBlock, 0, ctx->stream>>>(fn, sel, n, L, t);
-      else k_gb_global<RowFn><<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(fn, sel, n, L, t);
+      if (small) k_gb_small<RowFn, 4, kMaxStates><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(fn, sel, n, L, t);
+      else k_gb_global<RowFn><<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(fn, sel, n, L, t);
       SX_CHECK_LAUNCH();
     }
     SlotFn sf;
@@ -339,7 +339,7 @@ sx_status gb_run(sx_ctx* ctx, const RowFn& fn, const GbPlan& P, const int32_t* s
     SX_TRY(scr.get((char**)&ea.out_agg[j], (size_t)ng * type_width(agg_out_type(P.agg_op[j]))));
   }
   if (ng > 0) {
-    k_gb_emit<<<persistent_grid(ctx, 8, (ng + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(ea);
+    k_gb_emit<<<persistent_grid(ctx, 8, (ng + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(ea);
     SX_CHECK_LAUNCH();
   }
   for (int k = 0; k < P.nkeys; ++k) {

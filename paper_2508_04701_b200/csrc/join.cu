@@ -238,7 +238,7 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
   a.slots = ht->slots;
   a.mask = cap - 1;
   a.inserted = ins;
-  if (n > 0) k_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(a);
+  if (n > 0) k_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
   cudaError_t e = cudaGetLastError();
   int64_t rows = 0;
   if (e == cudaSuccess) s = read_i64(ctx, ins, &rows);
@@ -347,7 +347,7 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
       a.out_build = ob;
       a.cap = cap;
       SX_CUDA(cudaMemsetAsync(a.counter, 0, 8, ctx->stream));
-      if (n > 0) k_probe_inner<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(a, gs);
+      if (n > 0) k_probe_inner<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a, gs);
       SX_CHECK_LAUNCH();
       SX_TRY(read_i64(ctx, a.counter, &count));
       if (count <= cap) break;

@@ -319,13 +319,13 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
   SX_TRY(scr.get(&diff, kMaxWords));
   SX_CUDA(cudaMemsetAsync(diff, 0, kMaxWords * sizeof(unsigned), ctx->stream));
   ea.diff = diff;
-  k_encode<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(ea);
+  k_encode<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(ea);
   SX_CHECK_LAUNCH();
   const int32_t* sel = in_sel ? in_sel->idx : nullptr;
   if (n <= kBitonicMax) {
     size_t smem = (size_t)kBitonicMax * nwords * sizeof(uint32_t);
     SX_CUDA(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_bitonic<<<1, 1024, smem, ctx->stream>>>(W, nullptr, n, outn, sel, perm);
+    k_bitonic<<<1, 1024, smem, SX_STREAM(ctx)>>>(W, nullptr, n, outn, sel, perm);
     SX_CHECK_LAUNCH();
     out_perm->len = outn;
     out_perm->idx = perm;
@@ -356,10 +356,10 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
     for (size_t p = 0; p <= digits.size(); ++p) {
       int cw = p < digits.size() ? digits[p].first : -1;
       int csh = p < digits.size() ? digits[p].second : 0;
-      k_sel_hist<<<grid, kBlock, 0, ctx->stream>>>(W, n, flags, pw, psh, cw, csh, st, hist, p == 0);
+      k_sel_hist<<<grid, kBlock, 0, SX_STREAM(ctx)>>>(W, n, flags, pw, psh, cw, csh, st, hist, p == 0);
       SX_CHECK_LAUNCH();
       if (cw >= 0) {
-        k_sel_choose<<<1, 256, 0, ctx->stream>>>(hist, st);
+        k_sel_choose<<<1, 256, 0, SX_STREAM(ctx)>>>(hist, st);
         SX_CHECK_LAUNCH();
       }
       pw = cw;
@@ -376,7 +376,7 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
     if (m != outn) return set_err(ctx, SX_ECUDA, "radix select produced %lld of %lld rows", (long long)m, (long long)outn);
     size_t smem = (size_t)kBitonicMax * nwords * sizeof(uint32_t);
     SX_CUDA(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_bitonic<<<1, 1024, smem, ctx->stream>>>(W, winners, m, outn, sel, perm);
+    k_bitonic<<<1, 1024, smem, SX_STREAM(ctx)>>>(W, winners, m, outn, sel, perm);
     SX_CHECK_LAUNCH();
   } else {
     // LSD radix sort over the varying digits, least significant first
@@ -389,9 +389,9 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
     Words* a = &W;
     Words* b = &W2;
     for (int p = (int)digits.size() - 1; p >= 0; --p) {
-      k_lsd_hist<<<(unsigned)ntiles, kLsdTile, 0, ctx->stream>>>(a->w[digits[p].first], digits[p].second, n, counts, ntiles);
-      k_lsd_scan<<<1, 1024, 0, ctx->stream>>>(counts, 256 * ntiles);
-      k_lsd_scatter<<<(unsigned)ntiles, kLsdTile, 0, ctx->stream>>>(*a, *b, digits[p].first, digits[p].second, n, counts, ntiles);
+      k_lsd_hist<<<(unsigned)ntiles, kLsdTile, 0, SX_STREAM(ctx)>>>(a->w[digits[p].first], digits[p].second, n, counts, ntiles);
+      k_lsd_scan<<<1, 1024, 0, SX_STREAM(ctx)>>>(counts, 256 * ntiles);
+      k_lsd_scatter<<<(unsigned)ntiles, kLsdTile, 0, SX_STREAM(ctx)>>>(*a, *b, digits[p].first, digits[p].second, n, counts, ntiles);
       SX_CHECK_LAUNCH();
       std::swap(a, b);
     }

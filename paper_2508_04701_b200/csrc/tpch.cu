@@ -371,7 +371,7 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   SX_CUDA(cudaMemcpyAsync(rank_d, rank_h, sizeof rank_h, cudaMemcpyHostToDevice, ctx->stream));
   SX_TRY(alloc(ctx, &rk, (size_t)(ng > 0 ? ng : 1)));
   bag.bufs.push_back(rk);
-  if (ng > 0) k_lookup_rank<<<(unsigned)((ng + 255) / 256), 256, 0, ctx->stream>>>((const int32_t*)gok[0].data, ng, rank_d, 25, rk);
+  if (ng > 0) k_lookup_rank<<<(unsigned)((ng + 255) / 256), 256, 0, SX_STREAM(ctx)>>>((const int32_t*)gok[0].data, ng, rank_d, 25, rk);
   SX_CHECK_LAUNCH();
   sx_col scol[2] = {sx_col{SX_I32, 0, ng, rk, nullptr, nullptr}, gok[1]};
   sx_sortkey sks[2] = {{0, 0}, {1, 1}};
