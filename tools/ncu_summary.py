@@ -13,7 +13,7 @@ def main(path):
     hdr, data = rows[hi], rows[hi + 1:]
     ki, mi, vi, ui, idi = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit", "ID"))
     per, names = collections.defaultdict(dict), {}
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3,
              "second": 1}
     for r in data:
         per[r[idi]][r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
