@@ -197,7 +197,11 @@ __device__ __forceinline__ bool eval_conj(const DCol* cols, const DPred* preds, 
 }
 
 // ---------------------------------------------------------------------------- exact int64 arithmetic
+__device__ __forceinline__ bool fits_i32(int64_t a) { return (uint64_t)(a + 0x80000000ll) < 0x100000000ull; }
+
 __device__ __forceinline__ int64_t mul_ck(int64_t a, int64_t b, bool& ovf) {
+  // fast path: both operands in int32 range -> one IMAD.WIDE, cannot overflow int64
+  if (fits_i32(a) && fits_i32(b)) return (int64_t)(int32_t)a * (int64_t)(int32_t)b;
   int64_t lo = (int64_t)((uint64_t)a * (uint64_t)b);
   int64_t hi = __mul64hi(a, b);
   ovf |= (hi != (lo >> 63));

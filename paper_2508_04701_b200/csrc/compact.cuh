@@ -9,7 +9,7 @@
 // outputs are written once.
 //
 // Functor interface:
-//   template <int ITEMS> __device__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS],
+//   template <int ITEMS> __device__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS],
 //                                            bool (&alive)[ITEMS], int32_t (&aux)[ITEMS]) const;
 // The functor sees all of a thread's rows at once so it can issue their loads
 // back to back (memory-level parallelism), then evaluate.
@@ -36,19 +36,19 @@ __global__ void __launch_bounds__(kBlock) k_compact(const __grid_constant__ F f,
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
     const int64_t base = tile * (int64_t)(kBlock * ITEMS);
-    int64_t row[ITEMS];
+    int32_t row[ITEMS];
     bool valid[ITEMS], alive[ITEMS];
     int32_t aux[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
       valid[i] = idx < n;
-      row[i] = idx;
+      row[i] = (int32_t)idx;
       aux[i] = -1;
     }
     if (HAS_SEL) {
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) row[i] = valid[i] ? (int64_t)__ldg(in_sel + row[i]) : 0;
+      for (int i = 0; i < ITEMS; ++i) row[i] = valid[i] ? __ldg(in_sel + row[i]) : 0;
     }
     f.template eval<ITEMS>(row, valid, alive, aux);
     unsigned ball[ITEMS];

@@ -9,7 +9,7 @@ namespace sx {
 // being alive (short-circuit at row granularity: sectors of dead rows are never fetched)
 // and issued back to back for memory-level parallelism; type and op switches are uniform.
 template <int ITEMS>
-__device__ __forceinline__ void apply_pred(const DCol& c, const DPred& q, const int64_t (&row)[ITEMS],
+__device__ __forceinline__ void apply_pred(const DCol& c, const DPred& q, const int32_t (&row)[ITEMS],
                                            bool (&alive)[ITEMS]) {
   int64_t x[ITEMS];
   switch (c.type) {
@@ -57,7 +57,7 @@ struct ConjFn {
   DPred preds[SX_MAX_PREDS];
   int np;
   template <int ITEMS>
-  __device__ __forceinline__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+  __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
                                        int32_t (&aux)[ITEMS]) const {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i];
@@ -86,7 +86,7 @@ struct ContainsFn {
     return false;
   }
   template <int ITEMS>
-  __device__ __forceinline__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+  __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
                                        int32_t (&aux)[ITEMS]) const {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i] && contains(row[i]);

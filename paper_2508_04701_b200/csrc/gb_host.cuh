@@ -1,6 +1,7 @@
 // gb_host.cuh — group-by planning (agg -> state mapping, slot layout), the host driver
 // (table sizing, strategy, retry on a full table) and result extraction/emission.
 #pragma once
+#include <algorithm>
 #include <cstring>
 
 #include "compact.cuh"
@@ -153,7 +154,7 @@ struct SlotFn {
     return cmp(hv_op, v, hv_lo, hv_hi);
   }
   template <int ITEMS>
-  __device__ __forceinline__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+  __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
                                        int32_t (&aux)[ITEMS]) const {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -202,7 +203,7 @@ __device__ __forceinline__ double i128_to_double(unsigned long long lo, long lon
   return (double)hi * 18446744073709551616.0 + (double)lo;
 }
 
-__global__ void k_gb_emit(const __grid_constant__ EmitArgs a) {
+static __global__ void k_gb_emit(const __grid_constant__ EmitArgs a) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t slot = (uint64_t)a.ids[i];
     const uint8_t* p = a.slots + slot * a.L.slot_bytes;
@@ -261,16 +262,18 @@ inline uint64_t pow2_at_least(uint64_t x) {
 }
 
 // Run the aggregation with RowFn and produce the outputs.  `force_small` selects K9.
-template <class RowFn>
-sx_status gb_run(sx_ctx* ctx, const RowFn& fn, const GbPlan& P, const int32_t* sel, int64_t n, int64_t groups_hint,
-                 sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups, int force_small = -1) {
+template <class Prog>
+sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* sel, int64_t n,
+                        int64_t groups_hint, sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups,
+                        int force_small = -1) {
   Scratch scr(ctx);
   const Layout& L = P.L;
   bool keyless = P.nkeys == 0;
-  bool small = keyless || (groups_hint >= 1 && groups_hint <= 4);
+  bool small = keyless || (groups_hint >= 1 && groups_hint <= kSmallSlots);
   if (force_small >= 0) small = force_small != 0;
-  uint64_t cap = keyless ? 1 : pow2_at_least(groups_hint > 0 ? (uint64_t)(2 * groups_hint)
-                                                             : (uint64_t)(2 * (n < (1 << 20) ? n : (1 << 20))));
+  // load factor <= 0.75 (linear probing); unknown hint: size for min(n, 2^20) groups, retry if full
+  uint64_t want = groups_hint > 0 ? (uint64_t)groups_hint : (uint64_t)(n < (1 << 20) ? n : (1 << 20));
+  uint64_t cap = keyless ? 1 : pow2_at_least(want + want / 3 + 1);
   uint8_t* table = nullptr;
   int32_t* ids = nullptr;
   int64_t ng = 0;
@@ -282,9 +285,19 @@ sx_status gb_run(sx_ctx* ctx, const RowFn& fn, const GbPlan& P, const int32_t* s
     SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
     Table t{table, keyless ? 0 : cap - 1, ctx->d_flags + 2, ctx->d_flags + 1};
     if (n > 0) {
-      unsigned grid = persistent_grid(ctx, 4, (n + kBlock - 1) / kBlock);
-      if (small) k_gb_small<RowFn, 4, kMaxStates><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(fn, sel, n, L, t);
-      else k_gb_global<RowFn><<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(fn, sel, n, L, t);
+      if (small) {
+        size_t smem = (size_t)kSmallSlots * L.nst * kSmallThreads * sizeof(unsigned long long);
+        SX_CUDA(cudaFuncSetAttribute(k_gb_small<Prog, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_small<Prog, 4>, kSmallThreads, smem));
+        if (per_sm < 1) per_sm = 1;
+        int64_t tiles = (n + (int64_t)kSmallThreads * 4 - 1) / ((int64_t)kSmallThreads * 4);
+        unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, tiles);
+        k_gb_small<Prog, 4><<<grid, kSmallThreads, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, t);
+      } else {
+        int64_t tiles = (n + 32 * 4 - 1) / (32 * 4) / (kBlock / 32) + 1;
+        k_gb_global<Prog, 4><<<persistent_grid(ctx, 8, tiles), kBlock, 0, SX_STREAM(ctx)>>>(prog, sel, n, L, t);
+      }
       SX_CHECK_LAUNCH();
     }
     SlotFn sf;

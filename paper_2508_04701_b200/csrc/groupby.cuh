@@ -1,18 +1,22 @@
-// groupby.cuh — hash group-by skeletons (K9 register-privatised small-G, K11
-// global open addressing) shared by the generic sx_groupby_agg and the
-// fixed-plan executor's compile-time-specialised row functors.
+// groupby.cuh — hash group-by kernels (K9 privatised small-G, K11 global open addressing).
 //
-// Aggregation table: AoS slots of `slot_bytes`; key field first (4 or 8 bytes,
-// 0 = EMPTY; a real key 0 goes to the side slot at index cap, flagged in
-// d_flags[2]).  States:
-//   SUM/AVG: {u64 lo at off8; i32 hi at off4}  (96-bit two's complement; cannot
-//            overflow: <= 2^31 rows x |v| < 2^63 < 2^94)
+// Row evaluation is "vectorised across rows, interpreted across columns": every thread holds
+// ITEMS rows; each predicate / key / expression factor is applied to all ITEMS rows at once, so
+// the column loads of ITEMS rows are issued back to back (memory-level parallelism) while the
+// operator description stays a runtime program (no dynamic register indexing: the item index is
+// compile-time, the column index is warp-uniform).
+//
+// Aggregation table: AoS slots of `slot_bytes`; key field first (4 or 8 bytes, 0 = EMPTY; a real
+// key 0 goes to the side slot at index cap, flagged in d_flags[2]).  States:
+//   SUM/AVG: {u64 lo at off8; i32 hi at off4}  (96-bit two's complement; cannot overflow:
+//            <= 2^31 rows x |v| < 2^63 < 2^94)
 //   COUNT:   u64 at off8
-//   MIN/MAX: u64 at off8, order-preserving u = v ^ 2^63; MAX stores u, MIN stores ~u,
-//            both updated with atomicMax so an all-zero slot is the identity.
+//   MIN/MAX: u64 at off8, order-preserving u = v ^ 2^63; MAX stores u, MIN stores ~u, both
+//            updated with atomicMax so an all-zero slot is the identity.
 // The whole table is zero-initialised with one memset.
 #pragma once
 #include "common.cuh"
+#include "filter.cuh"
 
 namespace sx {
 
@@ -35,6 +39,153 @@ struct Table {
   int* full;         // d_flags + 1
 };
 
+// The runtime "program" of one group-by: predicates, keys and one expression per state.
+struct GbArgs {
+  DCol cols[SX_MAX_COLS];
+  DPred preds[SX_MAX_PREDS];
+  int np;
+  int nkeys;
+  int kc[2];
+  int kfn[2];
+  sx_expr expr[kMaxStates];
+  int* ovf_flag;
+};
+
+// ------------------------------------------------------------------------------ batched evaluation
+template <int ITEMS>
+__device__ __forceinline__ void load_col(const DCol& c, const int32_t (&row)[ITEMS], const bool (&alive)[ITEMS],
+                                         int64_t (&x)[ITEMS]) {
+  switch (c.type) {
+    case SX_U8: {
+      const uint8_t* p = (const uint8_t*)c.p;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) x[i] = alive[i] ? (int64_t)__ldg(p + row[i]) : 0;
+      break;
+    }
+    case SX_I32:
+    case SX_DATE32: {
+      const int32_t* p = (const int32_t*)c.p;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) x[i] = alive[i] ? (int64_t)__ldg(p + row[i]) : 0;
+      break;
+    }
+    default: {
+      const long long* p = (const long long*)c.p;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) x[i] = alive[i] ? (int64_t)__ldg(p + row[i]) : 0;
+      break;
+    }
+  }
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void eval_expr_batch(const sx_expr& e, const DCol* cols, const int32_t (&row)[ITEMS],
+                                                const bool (&alive)[ITEMS], int64_t (&v)[ITEMS], bool& ovf) {
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) v[i] = 0;
+  for (int t = 0; t < e.nterms; ++t) {
+    const int64_t coef = e.t[t].coef;
+    int64_t p[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) p[i] = coef;
+    for (int f = 0; f < e.t[t].nf; ++f) {
+      const sx_factor& fc = e.t[t].f[f];
+      int64_t x[ITEMS];
+      load_col<ITEMS>(cols[fc.col], row, alive, x);
+      const int64_t mul = fc.mul, add = fc.add;
+      if (mul == -1) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          ovf |= x[i] == INT64_MIN;
+          x[i] = -x[i];
+        }
+      } else if (mul != 1) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) x[i] = mul_ck(mul, x[i], ovf);
+      }
+      if (add != 0) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) x[i] = add_ck(x[i], add, ovf);
+      }
+      if (f == 0 && coef == 1) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) p[i] = x[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) p[i] = mul_ck(p[i], x[i], ovf);
+      }
+    }
+    if (t == 0) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) v[i] = p[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) v[i] = add_ck(v[i], p[i], ovf);
+    }
+  }
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void eval_where_keys(const GbArgs& A, const int32_t (&row)[ITEMS], bool (&alive)[ITEMS],
+                                                uint64_t (&key)[ITEMS]) {
+  for (int p = 0; p < A.np; ++p) apply_pred<ITEMS>(A.cols[A.preds[p].col], A.preds[p], row, alive);
+  if (A.nkeys == 0) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = 0;
+    return;
+  }
+  int64_t k0[ITEMS];
+  load_col<ITEMS>(A.cols[A.kc[0]], row, alive, k0);
+  if (A.kfn[0] == SX_KEY_YEAR) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) k0[i] = civil_year((int32_t)k0[i]);
+  }
+  if (A.nkeys == 1) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = (uint64_t)k0[i];
+    return;
+  }
+  int64_t k1[ITEMS];
+  load_col<ITEMS>(A.cols[A.kc[1]], row, alive, k1);
+  if (A.kfn[1] == SX_KEY_YEAR) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) k1[i] = civil_year((int32_t)k1[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) key[i] = ((uint64_t)(uint32_t)k0[i] << 32) | (uint32_t)k1[i];
+}
+
+// ------------------------------------------------------------------------------ row programs
+// The kernels below are templated on a row program P providing
+//   static constexpr int kMaxNst;                                    (states, upper bound)
+//   int kind(int a, const Layout& L) const;                          (state kind)
+//   template <int I> struct Cache;                                   (per-thread row cache)
+//   template <int I> void where_keys(row, alive, key, cache) const;  (filter + group key + loads)
+//   template <int I> void state(int a, row, alive, cache, v, bool& ovf) const;  (state a's values)
+//   int* ovf_flag;
+// InterpProg runs the runtime program of sx_groupby_agg; the fixed-plan executor plugs in
+// compile-time programs (tpch.cu) whose state loop unrolls, so shared column loads and common
+// subexpressions are computed once per row.
+struct InterpProg {
+  GbArgs A;
+  int* ovf_flag;
+  static constexpr int kMaxNst = kMaxStates;
+  template <int ITEMS>
+  struct Cache {};
+  __device__ __forceinline__ int kind(int a, const Layout& L) const { return L.kind[a]; }
+  template <int ITEMS>
+  __device__ __forceinline__ void where_keys(const int32_t (&row)[ITEMS], bool (&alive)[ITEMS],
+                                             uint64_t (&key)[ITEMS], Cache<ITEMS>&) const {
+    eval_where_keys<ITEMS>(A, row, alive, key);
+  }
+  template <int ITEMS>
+  __device__ __forceinline__ void state(int a, const int32_t (&row)[ITEMS], const bool (&alive)[ITEMS],
+                                        const Cache<ITEMS>&, int64_t (&v)[ITEMS], bool& ovf) const {
+    eval_expr_batch<ITEMS>(A.expr[a], A.cols, row, alive, v, ovf);
+  }
+};
+
+// ------------------------------------------------------------------------------ table access
 __device__ __forceinline__ uint8_t* slot_ptr(const Table& t, int slot_bytes, uint64_t i) {
   return t.slots + i * (uint64_t)slot_bytes;
 }
@@ -74,187 +225,272 @@ __device__ __forceinline__ uint8_t* find_or_insert(const Table& t, const Layout&
 
 __device__ __forceinline__ unsigned long long order_u(int64_t v) { return (unsigned long long)v ^ 0x8000000000000000ull; }
 
-// Apply one row's (or a pre-reduced segment's) state values to a slot.
-// sum states carry a 96-bit value {lo, hi}; count in cnt; min/max in lo (as int64).
-__device__ __forceinline__ void apply_states(uint8_t* s, const Layout& L, const unsigned long long* lo,
-                                             const int32_t* hi, unsigned long long cnt) {
-  for (int a = 0; a < L.nst; ++a) {
-    switch (L.kind[a]) {
-      case ST_SUM:
-        atomic_add_sum96((unsigned long long*)(s + L.off8[a]), (int*)(s + L.off4[a]), (int64_t)lo[a], hi[a]);
-        break;
-      case ST_COUNT: atomicAdd((unsigned long long*)(s + L.off8[a]), cnt); break;
-      case ST_MIN: atomicMax((unsigned long long*)(s + L.off8[a]), ~order_u((int64_t)lo[a])); break;
-      default: atomicMax((unsigned long long*)(s + L.off8[a]), order_u((int64_t)lo[a])); break;
-    }
+// Apply one (possibly pre-reduced) state value to a slot.
+// SUM: {lo, hi} 96-bit; COUNT: cnt in lo; MIN/MAX: value in lo (as int64).
+__device__ __forceinline__ void apply_state(uint8_t* s, const Layout& L, int a, unsigned long long lo, int32_t hi) {
+  switch (L.kind[a]) {
+    case ST_SUM: atomic_add_sum96((unsigned long long*)(s + L.off8[a]), (int*)(s + L.off4[a]), (int64_t)lo, hi); break;
+    case ST_COUNT: atomicAdd((unsigned long long*)(s + L.off8[a]), lo); break;
+    case ST_MIN: atomicMax((unsigned long long*)(s + L.off8[a]), ~order_u((int64_t)lo)); break;
+    default: atomicMax((unsigned long long*)(s + L.off8[a]), order_u((int64_t)lo)); break;
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// K11: global open-addressing aggregation.  Rows are taken warp-contiguously; runs of equal keys
-// in consecutive lanes (clustered inputs, e.g. lineitem by orderkey) are pre-reduced with a
-// segmented warp scan so only each run's tail lane touches the table.
-// RowFn: __device__ bool row(int64_t r, uint64_t& key, int64_t (&v)[kMaxStates]) const
-//        (returns false if the row is filtered out); int nst(); kind(a).
-template <class RowFn>
-__global__ void __launch_bounds__(kBlock) k_gb_global(const __grid_constant__ RowFn fn, const int32_t* __restrict__ sel,
+// ------------------------------------------------------------------------------ K11: global
+// Each warp owns tiles of 32*ITEMS consecutive rows; item i of lane l is row base + 32*i + l, so
+// runs of equal keys in consecutive lanes (clustered inputs, e.g. lineitem by orderkey) are
+// pre-reduced with a segmented warp scan and only each run's tail lane touches the table.
+template <class P, int ITEMS>
+__global__ void __launch_bounds__(kBlock, 3) k_gb_global(const __grid_constant__ P prog, const int32_t* __restrict__ sel,
                                                       int64_t n, const __grid_constant__ Layout L, Table t) {
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
-    int64_t idx = base + lane;
-    bool alive = idx < n;
-    uint64_t key = 0;
-    int64_t v[kMaxStates];
-    if (alive) {
-      int64_t r = sel ? (int64_t)__ldg(sel + idx) : idx;
-      alive = fn.row(r, key, v);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  bool ovf = false;
+  for (int64_t base = warp * 32 * ITEMS; base < n; base += nwarps * 32 * ITEMS) {
+    int32_t row[ITEMS];
+    bool alive[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      int64_t idx = base + 32 * i + lane;
+      alive[i] = idx < n;
+      row[i] = alive[i] ? (sel ? __ldg(sel + idx) : (int32_t)idx) : 0;
     }
-    // segmented inclusive scan over lanes: a segment = maximal run of alive lanes with equal key
-    uint64_t pkey = __shfl_up_sync(kFull, key, 1);
-    bool palive = __shfl_up_sync(kFull, alive, 1);
-    bool head = !alive || lane == 0 || !palive || pkey != key;
-    unsigned heads = __ballot_sync(kFull, head);
-    uint64_t nkey = __shfl_down_sync(kFull, key, 1);
-    bool nalive = __shfl_down_sync(kFull, alive, 1);
-    bool tail = alive && (lane == 31 || !nalive || nkey != key);
-    // segment start lane for this lane
-    unsigned below = heads & (0xffffffffu >> (31 - lane));  // heads at lanes <= lane
-    int seg_start = 31 - __clz(below);
-    unsigned long long lo[kMaxStates];
-    int32_t hi[kMaxStates];
-    unsigned long long cnt = alive ? 1 : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      unsigned long long c2 = __shfl_up_sync(kFull, cnt, o);
-      if (lane - o >= seg_start) cnt += c2;
+    uint64_t key[ITEMS];
+    typename P::template Cache<ITEMS> cache;
+    prog.template where_keys<ITEMS>(row, alive, key, cache);
+    // per item: segment structure and the tail lane's slot
+    unsigned seg_start[ITEMS];
+    bool tail[ITEMS];
+    uint8_t* slot[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      uint64_t pk = __shfl_up_sync(kFull, key[i], 1);
+      bool pa = __shfl_up_sync(kFull, alive[i], 1);
+      bool head = !alive[i] || lane == 0 || !pa || pk != key[i];
+      unsigned heads = __ballot_sync(kFull, head);
+      uint64_t nk = __shfl_down_sync(kFull, key[i], 1);
+      bool na = __shfl_down_sync(kFull, alive[i], 1);
+      tail[i] = alive[i] && (lane == 31 || !na || nk != key[i]);
+      seg_start[i] = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+      slot[i] = tail[i] ? find_or_insert(t, L, key[i]) : nullptr;
     }
-    for (int a = 0; a < L.nst; ++a) {
-      int k = L.kind[a];
-      if (k == ST_COUNT) continue;
-      if (k == ST_SUM) {
-        unsigned long long l = alive ? (unsigned long long)v[a] : 0;
-        int32_t h = alive ? (v[a] < 0 ? -1 : 0) : 0;
-        for (int o = 1; o < 32; o <<= 1) {
-          unsigned long long l2 = __shfl_up_sync(kFull, l, o);
-          int32_t h2 = __shfl_up_sync(kFull, h, o);
-          if (lane - o >= seg_start) {
-            unsigned long long s = l + l2;
-            h += h2 + (s < l ? 1 : 0);
-            l = s;
-          }
-        }
-        lo[a] = l;
-        hi[a] = h;
+#pragma unroll
+    for (int a = 0; a < P::kMaxNst; ++a) {
+      if (a >= L.nst) break;
+      const int kd = prog.kind(a, L);
+      int64_t v[ITEMS];
+      if (kd == ST_COUNT) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) v[i] = alive[i] ? 1 : 0;
       } else {
-        int64_t m = alive ? v[a] : (k == ST_MIN ? INT64_MAX : INT64_MIN);
-        for (int o = 1; o < 32; o <<= 1) {
-          int64_t m2 = __shfl_up_sync(kFull, m, o);
-          if (lane - o >= seg_start) m = (k == ST_MIN) ? (m2 < m ? m2 : m) : (m2 > m ? m2 : m);
+        prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
+      }
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        if (kd == ST_SUM || kd == ST_COUNT) {
+          unsigned long long l = alive[i] ? (unsigned long long)v[i] : 0;
+          int32_t h = (alive[i] && v[i] < 0) ? -1 : 0;
+          for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long l2 = __shfl_up_sync(kFull, l, o);
+            int32_t h2 = __shfl_up_sync(kFull, h, o);
+            if (lane - o >= (int)seg_start[i]) {
+              unsigned long long s = l + l2;
+              h += h2 + (s < l ? 1 : 0);
+              l = s;
+            }
+          }
+          if (slot[i]) apply_state(slot[i], L, a, l, h);
+        } else {
+          int64_t m = alive[i] ? v[i] : (kd == ST_MIN ? INT64_MAX : INT64_MIN);
+          for (int o = 1; o < 32; o <<= 1) {
+            int64_t m2 = __shfl_up_sync(kFull, m, o);
+            if (lane - o >= (int)seg_start[i]) m = (kd == ST_MIN) ? (m2 < m ? m2 : m) : (m2 > m ? m2 : m);
+          }
+          if (slot[i]) apply_state(slot[i], L, a, (unsigned long long)m, 0);
         }
-        lo[a] = (unsigned long long)m;
-        hi[a] = 0;
       }
     }
-    if (tail) {
-      uint8_t* s = find_or_insert(t, L, key);
-      if (s) apply_states(s, L, lo, hi, cnt);
-    }
   }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
 }
 
-// ---------------------------------------------------------------------------------------------
-// K9: register-privatised aggregation for very few groups (Q1: 4; keyless reduce: 1).
-// Each thread keeps NSLOT (key -> states) slots in registers.  Sums are exact without any
-// overflow check: v = vh * 2^32 + vl is accumulated as sum(vl) in u64 and sum(vh) in i64
-// (neither can overflow for < 2^31 rows).  A row whose key finds no free slot goes straight to
-// the global table.  Slots are flushed to the global table once per thread at the end.
-template <class RowFn, int NSLOT, int NST>
-__global__ void __launch_bounds__(kBlock) k_gb_small(const __grid_constant__ RowFn fn, const int32_t* __restrict__ sel,
-                                                     int64_t n, const __grid_constant__ Layout L, Table t) {
-  uint64_t skey[NSLOT];
-  bool used[NSLOT];
-  unsigned long long cnt[NSLOT];
-  unsigned long long al[NSLOT][NST];  // SUM: sum of low 32-bit halves; MIN/MAX: ordered u (max)
-  long long ah[NSLOT][NST];           // SUM: sum of high halves
-#pragma unroll
-  for (int k = 0; k < NSLOT; ++k) {
-    used[k] = false;
-    skey[k] = 0;
-    cnt[k] = 0;
-#pragma unroll
-    for (int a = 0; a < NST; ++a) { al[k][a] = 0; ah[k][a] = 0; }
+// ------------------------------------------------------------------------------ K9: small G
+// Shared-memory privatised aggregation for very few groups (Q1: 4; keyless reduce: 1).
+// Each thread owns NSLOT (key -> state vector) slots; slot keys live in registers, the state
+// accumulators in a lane-private shared-memory column (acc[(slot*nst + state) * nthreads + tid]),
+// so a row's slot index can be dynamic without register indexing and without any atomics.
+// SUM accumulates in int64 with overflow detection: on overflow the old partial is flushed to the
+// global table (exact) and the accumulator restarts.  A row whose key finds no free slot goes to
+// the global table directly.  At the end every CTA merges its threads' slots in a small
+// shared-memory table (smem atomics), then adds each merged entry to the global table once.
+constexpr int kSmallSlots = 4;
+constexpr int kSmallThreads = 512;
+constexpr int kCtaTable = 32;
+
+template <class P, int ITEMS>
+__global__ void __launch_bounds__(kSmallThreads, 2) k_gb_small(const __grid_constant__ P prog,
+                                                            const int32_t* __restrict__ sel, int64_t n,
+                                                            const __grid_constant__ Layout L, Table t) {
+  extern __shared__ unsigned long long acc[];  // [kSmallSlots * nst][nthreads]
+  __shared__ unsigned long long ct_key[kCtaTable];
+  __shared__ int ct_used[kCtaTable];
+  __shared__ unsigned long long ct_lo[kCtaTable][kMaxStates];
+  __shared__ int ct_hi[kCtaTable][kMaxStates];
+  const int tid = threadIdx.x, nt = blockDim.x, nst = L.nst;
+  for (int j = 0; j < kSmallSlots * nst; ++j) acc[j * nt + tid] = 0;
+  for (int j = tid; j < kCtaTable; j += nt) {
+    ct_used[j] = 0;
+    ct_key[j] = 0;
+    for (int a = 0; a < kMaxStates; ++a) { ct_lo[j][a] = 0; ct_hi[j][a] = 0; }
   }
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += stride) {
-    int64_t r = sel ? (int64_t)__ldg(sel + idx) : idx;
-    uint64_t key = 0;
-    int64_t v[kMaxStates];
-    if (!fn.row(r, key, v)) continue;
-    int s = -1;
+  uint64_t skey[kSmallSlots];
+  bool used[kSmallSlots];
 #pragma unroll
-    for (int k = 0; k < NSLOT; ++k)
-      if (used[k] && skey[k] == key) s = k;
-    if (s < 0) {
+  for (int k = 0; k < kSmallSlots; ++k) { skey[k] = 0; used[k] = false; }
+  bool ovf = false;
+  const int64_t tile = (int64_t)nt * ITEMS;
+  for (int64_t base = blockIdx.x * tile; base < n; base += (int64_t)gridDim.x * tile) {
+    int32_t row[ITEMS];
+    bool alive[ITEMS];
 #pragma unroll
-      for (int k = NSLOT - 1; k >= 0; --k)
-        if (!used[k]) s = k;
-      if (s >= 0) {
+    for (int i = 0; i < ITEMS; ++i) {
+      int64_t idx = base + (int64_t)i * nt + tid;
+      alive[i] = idx < n;
+      row[i] = alive[i] ? (sel ? __ldg(sel + idx) : (int32_t)idx) : 0;
+    }
+    uint64_t key[ITEMS];
+    typename P::template Cache<ITEMS> cache;
+    prog.template where_keys<ITEMS>(row, alive, key, cache);
+    int s[ITEMS];
 #pragma unroll
-        for (int k = 0; k < NSLOT; ++k)
-          if (k == s) { used[k] = true; skey[k] = key; }
+    for (int i = 0; i < ITEMS; ++i) {
+      s[i] = -1;
+      if (!alive[i]) continue;
+#pragma unroll
+      for (int k = 0; k < kSmallSlots; ++k)
+        if (used[k] && skey[k] == key[i]) s[i] = k;
+      if (s[i] < 0) {
+#pragma unroll
+        for (int k = kSmallSlots - 1; k >= 0; --k)
+          if (!used[k]) s[i] = k;
+        if (s[i] >= 0) {
+#pragma unroll
+          for (int k = 0; k < kSmallSlots; ++k)
+            if (k == s[i]) { used[k] = true; skey[k] = key[i]; }
+        }
       }
     }
-    if (s < 0) {  // slots exhausted: this row goes to the global table directly
-      uint8_t* p = find_or_insert(t, L, key);
-      if (p) {
-        unsigned long long lo[kMaxStates];
-        int32_t hi[kMaxStates];
-        for (int a = 0; a < L.nst; ++a) { lo[a] = (unsigned long long)v[a]; hi[a] = v[a] < 0 ? -1 : 0; }
-        apply_states(p, L, lo, hi, 1);
-      }
-      continue;
+    // smem cell index of (slot, state 0) per item; -1: not aggregated here (filtered or no slot)
+    int cell0[ITEMS];
+    bool slow = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      cell0[i] = (alive[i] && s[i] >= 0) ? s[i] * nst * nt + tid : -1;
+      slow |= alive[i] && s[i] < 0;
     }
 #pragma unroll
-    for (int k = 0; k < NSLOT; ++k) {
-      if (k != s) continue;
-      cnt[k] += 1;
+    for (int a = 0; a < P::kMaxNst; ++a) {
+      if (a >= nst) break;
+      const int kd = prog.kind(a, L);
+      const int aoff = a * nt;
+      int64_t v[ITEMS];
+      if (kd == ST_COUNT) {
 #pragma unroll
-      for (int a = 0; a < NST; ++a) {
-        if (a >= L.nst) break;
-        const int kd = L.kind[a];
+        for (int i = 0; i < ITEMS; ++i)
+          if (cell0[i] >= 0) acc[cell0[i] + aoff] += 1;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) v[i] = 1;
+      } else {
+        prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
         if (kd == ST_SUM) {
-          al[k][a] += (unsigned long long)(uint32_t)v[a];
-          ah[k][a] += (long long)(v[a] >> 32);
-        } else if (kd == ST_MIN) {
-          unsigned long long u = ~order_u(v[a]);
-          al[k][a] = u > al[k][a] ? u : al[k][a];
-        } else if (kd == ST_MAX) {
-          unsigned long long u = order_u(v[a]);
-          al[k][a] = u > al[k][a] ? u : al[k][a];
+#pragma unroll
+          for (int i = 0; i < ITEMS; ++i) {
+            if (cell0[i] < 0) continue;
+            unsigned long long* cell = &acc[cell0[i] + aoff];
+            int64_t o = (int64_t)*cell, nv = (int64_t)((unsigned long long)o + (unsigned long long)v[i]);
+            if (((o ^ nv) & (v[i] ^ nv)) < 0) {  // int64 overflow: flush the partial exactly
+              uint8_t* p = find_or_insert(t, L, key[i]);
+              if (p) apply_state(p, L, a, (unsigned long long)o, o < 0 ? -1 : 0);
+              nv = v[i];
+            }
+            *cell = (unsigned long long)nv;
+          }
+        } else {
+          const bool mn = kd == ST_MIN;
+#pragma unroll
+          for (int i = 0; i < ITEMS; ++i) {
+            if (cell0[i] < 0) continue;
+            unsigned long long* cell = &acc[cell0[i] + aoff];
+            unsigned long long u = mn ? ~order_u(v[i]) : order_u(v[i]), old = *cell;
+            *cell = u > old ? u : old;
+          }
+        }
+      }
+      if (slow) {  // rows whose key found no free register slot: straight to the global table
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          if (!alive[i] || s[i] >= 0) continue;
+          uint8_t* p = find_or_insert(t, L, key[i]);
+          if (p) apply_state(p, L, a, (unsigned long long)v[i], (kd == ST_SUM && v[i] < 0) ? -1 : 0);
         }
       }
     }
   }
-  // flush
+  if (ovf) atomicExch(prog.ovf_flag, 1);
+  __syncthreads();
+  // CTA merge: each thread's used slots into the shared table (smem atomics), overflow to global
 #pragma unroll
-  for (int k = 0; k < NSLOT; ++k) {
+  for (int k = 0; k < kSmallSlots; ++k) {
     if (!used[k]) continue;
-    uint8_t* p = find_or_insert(t, L, skey[k]);
-    if (!p) continue;
-#pragma unroll
-    for (int a = 0; a < NST; ++a) {
-      if (a >= L.nst) break;
-      const int kd = L.kind[a];
-      if (kd == ST_SUM) {
-        // total = ah * 2^32 + al  (al < 2^63, |ah| < 2^62) as a 96-bit {lo, hi}
-        __int128 tot = ((__int128)ah[k][a] << 32) + (__int128)al[k][a];
-        atomic_add_sum96((unsigned long long*)(p + L.off8[a]), (int*)(p + L.off4[a]), (int64_t)(unsigned long long)tot,
-                         (int32_t)(tot >> 64));
-      } else if (kd == ST_COUNT) {
-        atomicAdd((unsigned long long*)(p + L.off8[a]), cnt[k]);
-      } else {
-        atomicMax((unsigned long long*)(p + L.off8[a]), al[k][a]);
+    uint64_t key = skey[k];
+    int e = (int)(hash64(key) & (kCtaTable - 1)), found = -1;
+    for (int probe = 0; probe < kCtaTable; ++probe) {
+      int u = atomicCAS(&ct_used[e], 0, 1);
+      if (u == 0) {  // claimed an empty entry: publish the key
+        atomicExch(&ct_key[e], (unsigned long long)key);
+        atomicExch(&ct_used[e], 2);
+        found = e;
+        break;
       }
+      while (*(volatile int*)&ct_used[e] == 1) {
+      }
+      if (*(volatile unsigned long long*)&ct_key[e] == key) { found = e; break; }
+      e = (e + 1) & (kCtaTable - 1);
+    }
+    for (int a = 0; a < nst; ++a) {
+      unsigned long long val = acc[(k * nst + a) * nt + tid];
+      const int kd = L.kind[a];
+      if (found < 0) {
+        uint8_t* p = find_or_insert(t, L, key);
+        if (!p) continue;
+        if (kd == ST_SUM) apply_state(p, L, a, val, (int64_t)val < 0 ? -1 : 0);
+        else if (kd == ST_COUNT) apply_state(p, L, a, val, 0);
+        else atomicMax((unsigned long long*)(p + L.off8[a]), val);
+        continue;
+      }
+      if (kd == ST_SUM) {
+        unsigned long long old = atomicAdd(&ct_lo[found][a], val);
+        int h = ((int64_t)val < 0 ? -1 : 0) + ((old + val) < old ? 1 : 0);
+        if (h) atomicAdd(&ct_hi[found][a], h);
+      } else if (kd == ST_COUNT) {
+        atomicAdd(&ct_lo[found][a], val);
+      } else {
+        atomicMax(&ct_lo[found][a], val);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < kCtaTable; e += nt) {
+    if (ct_used[e] != 2) continue;
+    uint8_t* p = find_or_insert(t, L, ct_key[e]);
+    if (!p) continue;
+    for (int a = 0; a < nst; ++a) {
+      const int kd = L.kind[a];
+      if (kd == ST_SUM) atomic_add_sum96((unsigned long long*)(p + L.off8[a]), (int*)(p + L.off4[a]),
+                                         (int64_t)ct_lo[e][a], ct_hi[e][a]);
+      else if (kd == ST_COUNT) atomicAdd((unsigned long long*)(p + L.off8[a]), ct_lo[e][a]);
+      else atomicMax((unsigned long long*)(p + L.off8[a]), ct_lo[e][a]);
     }
   }
 }

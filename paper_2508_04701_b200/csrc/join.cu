@@ -63,7 +63,7 @@ struct ProbeFn {
   const void* slots;
   uint64_t mask;
   template <int ITEMS>
-  __device__ __forceinline__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+  __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
                                        int32_t (&aux)[ITEMS]) const {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i];

@@ -182,7 +182,7 @@ __global__ void k_sel_choose(unsigned* hist, SelState* st) {
 struct AcceptedFn {
   const uint8_t* flags;
   template <int ITEMS>
-  __device__ __forceinline__ void eval(const int64_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+  __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
                                        int32_t (&aux)[ITEMS]) const {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i] && flags[row[i]] != 0;

@@ -9,10 +9,158 @@
 #include <vector>
 
 #include "common.cuh"
+#include "gb_host.cuh"
 
 using namespace sx;
 
 namespace {
+
+// ------------------------------------------------------------------------------------------
+// Compile-time row programs for the plans' dominant group-bys (see groupby.cuh "row programs").
+// Same kernels and table layout as sx_groupby_agg; the expressions are compiled instead of
+// interpreted, so each column is loaded once per row and shared subexpressions are reused.
+// State order = the order gb_plan() derives from the plan's aggregate list (checked on the host).
+__device__ __forceinline__ int64_t sub_ck(int64_t a, int64_t b, bool& ovf) {
+  int64_t s = (int64_t)((uint64_t)a - (uint64_t)b);
+  ovf |= ((a ^ b) & (a ^ s)) < 0;
+  return s;
+}
+
+// Q1: where l_shipdate <= X; key (l_returnflag, l_linestatus);
+// states: 0 sum(qty) 1 sum(ext) 2 sum(ext*(100-disc)) 3 sum(ext*(100-disc)*(100+tax)) 4 count 5 sum(disc)
+struct Q1Prog {
+  const int32_t* ship;
+  const uint8_t *rf, *ls;
+  const long long *qty, *ext, *disc, *tax;
+  int32_t ship_max;
+  int* ovf_flag;
+  static constexpr int kMaxNst = 6;
+  template <int I>
+  struct Cache { int64_t qty[I], ext[I], disc[I], tax[I]; };
+  __device__ __forceinline__ int kind(int a, const Layout&) const { return a == 4 ? ST_COUNT : ST_SUM; }
+  template <int I>
+  __device__ __forceinline__ void where_keys(const int32_t (&row)[I], bool (&alive)[I], uint64_t (&key)[I],
+                                             Cache<I>& c) const {
+    int32_t sd[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) sd[i] = alive[i] ? __ldg(ship + row[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) alive[i] = alive[i] && sd[i] <= ship_max;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      uint32_t r = alive[i] ? __ldg(rf + row[i]) : 0, l = alive[i] ? __ldg(ls + row[i]) : 0;
+      key[i] = ((uint64_t)r << 32) | l;
+      c.qty[i] = alive[i] ? __ldg(qty + row[i]) : 0;
+      c.ext[i] = alive[i] ? __ldg(ext + row[i]) : 0;
+      c.disc[i] = alive[i] ? __ldg(disc + row[i]) : 0;
+      c.tax[i] = alive[i] ? __ldg(tax + row[i]) : 0;
+    }
+  }
+  template <int I>
+  __device__ __forceinline__ void state(int a, const int32_t (&)[I], const bool (&)[I], const Cache<I>& c,
+                                        int64_t (&v)[I], bool& ovf) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      switch (a) {
+        case 0: v[i] = c.qty[i]; break;
+        case 1: v[i] = c.ext[i]; break;
+        case 2: v[i] = mul_ck(c.ext[i], sub_ck(100, c.disc[i], ovf), ovf); break;
+        case 3: v[i] = mul_ck(mul_ck(c.ext[i], sub_ck(100, c.disc[i], ovf), ovf), add_ck(c.tax[i], 100, ovf), ovf); break;
+        case 4: v[i] = 1; break;
+        default: v[i] = c.disc[i]; break;
+      }
+    }
+  }
+};
+
+// Q6: keyless; where date in [lo, hi), disc in [dlo, dhi], qty < qlt (each column loaded only for
+// rows still alive); states: 0 sum(ext*disc) 1 count
+struct Q6Prog {
+  const int32_t* ship;
+  const long long *disc, *qty, *ext;
+  int32_t date_lo, date_hi;
+  int64_t disc_lo, disc_hi, qty_lt;
+  int* ovf_flag;
+  static constexpr int kMaxNst = 2;
+  template <int I>
+  struct Cache { int64_t ext[I], disc[I]; };
+  __device__ __forceinline__ int kind(int a, const Layout&) const { return a == 1 ? ST_COUNT : ST_SUM; }
+  template <int I>
+  __device__ __forceinline__ void where_keys(const int32_t (&row)[I], bool (&alive)[I], uint64_t (&key)[I],
+                                             Cache<I>& c) const {
+    int32_t sd[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) sd[i] = alive[i] ? __ldg(ship + row[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) alive[i] = alive[i] && sd[i] >= date_lo && sd[i] < date_hi;
+#pragma unroll
+    for (int i = 0; i < I; ++i) c.disc[i] = alive[i] ? __ldg(disc + row[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) alive[i] = alive[i] && c.disc[i] >= disc_lo && c.disc[i] <= disc_hi;
+    int64_t q[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) q[i] = alive[i] ? __ldg(qty + row[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      alive[i] = alive[i] && q[i] < qty_lt;
+      c.ext[i] = alive[i] ? __ldg(ext + row[i]) : 0;
+      key[i] = 0;
+    }
+  }
+  template <int I>
+  __device__ __forceinline__ void state(int a, const int32_t (&)[I], const bool (&)[I], const Cache<I>& c,
+                                        int64_t (&v)[I], bool& ovf) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) v[i] = a == 0 ? mul_ck(c.ext[i], c.disc[i], ovf) : 1;
+  }
+};
+
+// Q18 subquery: group lineitem by l_orderkey; state 0 sum(l_quantity)
+template <typename KT>
+struct Q18Prog {
+  const KT* okey;
+  const long long* qty;
+  int* ovf_flag;
+  static constexpr int kMaxNst = 1;
+  template <int I>
+  struct Cache { int64_t q[I]; };
+  __device__ __forceinline__ int kind(int, const Layout&) const { return ST_SUM; }
+  template <int I>
+  __device__ __forceinline__ void where_keys(const int32_t (&row)[I], bool (&alive)[I], uint64_t (&key)[I],
+                                             Cache<I>& c) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      key[i] = alive[i] ? (uint64_t)(int64_t)__ldg(okey + row[i]) : 0;
+      c.q[i] = alive[i] ? __ldg(qty + row[i]) : 0;
+    }
+  }
+  template <int I>
+  __device__ __forceinline__ void state(int, const int32_t (&)[I], const bool (&)[I], const Cache<I>& c,
+                                        int64_t (&v)[I], bool&) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) v[i] = c.q[i];
+  }
+};
+
+// Column width checks for the compiled plans (other layouts take the interpreted operator path).
+bool w1(const sx_col& c) { return c.type == SX_U8 && !c.validity; }
+bool w4(const sx_col& c) { return (c.type == SX_I32 || c.type == SX_DATE32) && !c.validity; }
+bool w8(const sx_col& c) { return (c.type == SX_I64 || c.type == SX_DEC64) && !c.validity; }
+sx_status to_dcols_check(sx_ctx* ctx, const sx_col* cols, int n) {
+  DCol d[SX_MAX_COLS];
+  return to_dcols(ctx, cols, n, d);
+}
+
+// The compiled program must see exactly the states gb_plan() derived from the aggregate list.
+sx_status check_states(sx_ctx* ctx, const GbPlan& P, std::initializer_list<int> kinds) {
+  int a = 0;
+  for (int k : kinds) {
+    if (a >= P.L.nst || P.L.kind[a] != k) return set_err(ctx, SX_EINVAL, "compiled plan/state layout mismatch");
+    ++a;
+  }
+  if (a != P.L.nst) return set_err(ctx, SX_EINVAL, "compiled plan/state count mismatch");
+  return SX_OK;
+}
 
 // Owns intermediate device buffers and hash tables of one query.
 struct Bag {
@@ -144,7 +292,21 @@ SX_EXPORT sx_status sx_tpch_q1(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       Count()};                                                  // count_order
   sx_col ok[2], oa[8];
   int64_t ng = 0;
-  SX_TRY(sx_groupby_agg(ctx, cols, 7, keys, 2, nullptr, &where, 1, aggs, 8, nullptr, 4, ok, oa, &ng));
+  if (w4(t->l_shipdate) && w1(t->l_returnflag) && w1(t->l_linestatus) && w8(t->l_quantity) &&
+      w8(t->l_extendedprice) && w8(t->l_discount) && w8(t->l_tax)) {
+    ProfScope pg(ctx, "groupby");
+    GbPlan plan;
+    SX_TRY(to_dcols_check(ctx, cols, 7));
+    SX_TRY(gb_plan(ctx, cols, 7, keys, 2, aggs, 8, nullptr, &plan));
+    SX_TRY(check_states(ctx, plan, {ST_SUM, ST_SUM, ST_SUM, ST_SUM, ST_COUNT, ST_SUM}));
+    Q1Prog prog{(const int32_t*)t->l_shipdate.data, (const uint8_t*)t->l_returnflag.data,
+                (const uint8_t*)t->l_linestatus.data, (const long long*)t->l_quantity.data,
+                (const long long*)t->l_extendedprice.data, (const long long*)t->l_discount.data,
+                (const long long*)t->l_tax.data, p->q1_shipdate_max, ctx->d_flags};
+    SX_TRY(gb_run(ctx, prog, plan, nullptr, t->l_shipdate.len, 4, ok, oa, &ng));
+  } else {
+    SX_TRY(sx_groupby_agg(ctx, cols, 7, keys, 2, nullptr, &where, 1, aggs, 8, nullptr, 4, ok, oa, &ng));
+  }
   bag.keep(ok, 2);
   bag.keep(oa, 8);
   // order by l_returnflag, l_linestatus
@@ -188,7 +350,19 @@ SX_EXPORT sx_status sx_tpch_q6(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   sx_agg aggs[2] = {A(SX_SUM, E1(1, {F(3), F(1)})), Count()};  // sum(l_extendedprice*l_discount) scale 4
   sx_col oa[2];
   int64_t ng = 0;
-  SX_TRY(sx_groupby_agg(ctx, cols, 4, nullptr, 0, nullptr, where, 4, aggs, 2, nullptr, 1, nullptr, oa, &ng));
+  if (w4(t->l_shipdate) && w8(t->l_discount) && w8(t->l_quantity) && w8(t->l_extendedprice)) {
+    ProfScope pg(ctx, "groupby");
+    GbPlan plan;
+    SX_TRY(to_dcols_check(ctx, cols, 4));
+    SX_TRY(gb_plan(ctx, cols, 4, nullptr, 0, aggs, 2, nullptr, &plan));
+    SX_TRY(check_states(ctx, plan, {ST_SUM, ST_COUNT}));
+    Q6Prog prog{(const int32_t*)t->l_shipdate.data, (const long long*)t->l_discount.data,
+                (const long long*)t->l_quantity.data, (const long long*)t->l_extendedprice.data, p->q6_date_lo,
+                p->q6_date_hi, p->q6_disc_lo, p->q6_disc_hi, p->q6_qty_lt, ctx->d_flags};
+    SX_TRY(gb_run(ctx, prog, plan, nullptr, t->l_shipdate.len, 1, nullptr, oa, &ng));
+  } else {
+    SX_TRY(sx_groupby_agg(ctx, cols, 4, nullptr, 0, nullptr, where, 4, aggs, 2, nullptr, 1, nullptr, oa, &ng));
+  }
   bag.keep(oa, 2);
   std::vector<uint8_t> hs, hc;
   SX_TRY(d2h(ctx, oa[0], hs));
@@ -406,7 +580,22 @@ SX_EXPORT sx_status sx_tpch_q18(sx_ctx* ctx, const sx_tpch_tables* t, const sx_t
   sx_having hv = {0, SX_GT, p->q18_qty_gt, 0};
   sx_col gok[1], goa[1];
   int64_t ng = 0;
-  SX_TRY(sx_groupby_agg(ctx, lcols, 2, &gk, 1, nullptr, nullptr, 0, &ga, 1, &hv, t->o_orderkey.len, gok, goa, &ng));
+  if (w8(t->l_quantity) && (w4(t->l_orderkey) || w8(t->l_orderkey))) {
+    ProfScope pg(ctx, "groupby");
+    GbPlan plan;
+    SX_TRY(to_dcols_check(ctx, lcols, 2));
+    SX_TRY(gb_plan(ctx, lcols, 2, &gk, 1, &ga, 1, &hv, &plan));
+    SX_TRY(check_states(ctx, plan, {ST_SUM}));
+    if (w4(t->l_orderkey)) {
+      Q18Prog<int32_t> prog{(const int32_t*)t->l_orderkey.data, (const long long*)t->l_quantity.data, ctx->d_flags};
+      SX_TRY(gb_run(ctx, prog, plan, nullptr, t->l_orderkey.len, t->o_orderkey.len, gok, goa, &ng));
+    } else {
+      Q18Prog<long long> prog{(const long long*)t->l_orderkey.data, (const long long*)t->l_quantity.data, ctx->d_flags};
+      SX_TRY(gb_run(ctx, prog, plan, nullptr, t->l_orderkey.len, t->o_orderkey.len, gok, goa, &ng));
+    }
+  } else {
+    SX_TRY(sx_groupby_agg(ctx, lcols, 2, &gk, 1, nullptr, nullptr, 0, &ga, 1, &hv, t->o_orderkey.len, gok, goa, &ng));
+  }
   bag.keep(gok, 1);
   bag.keep(goa, 1);
   // 2. orders with o_orderkey in that set; carry sum(l_quantity) from the group-by (equal to the
