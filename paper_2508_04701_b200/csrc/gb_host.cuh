@@ -286,7 +286,7 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
     Table t{table, keyless ? 0 : cap - 1, ctx->d_flags + 2, ctx->d_flags + 1};
     if (n > 0) {
       if (small) {
-        size_t smem = (size_t)kSmallSlots * L.nst * kSmallThreads * sizeof(unsigned long long);
+        size_t smem = small_smem_bytes(L.nst);
         SX_CUDA(cudaFuncSetAttribute(k_gb_small<Prog, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
         SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_small<Prog, 4>, kSmallThreads, smem));

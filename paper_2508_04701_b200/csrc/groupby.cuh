@@ -318,37 +318,53 @@ __global__ void __launch_bounds__(kBlock, 3) k_gb_global(const __grid_constant__
 // ------------------------------------------------------------------------------ K9: small G
 // Shared-memory privatised aggregation for very few groups (Q1: 4; keyless reduce: 1).
 // Each thread owns NSLOT (key -> state vector) slots; slot keys live in registers, the state
-// accumulators in a lane-private shared-memory column (acc[(slot*nst + state) * nthreads + tid]),
+// accumulators in a lane-private shared-memory column (cell = (slot*nst + state)*nthreads + tid),
 // so a row's slot index can be dynamic without register indexing and without any atomics.
-// SUM accumulates in int64 with overflow detection: on overflow the old partial is flushed to the
-// global table (exact) and the accumulator restarts.  A row whose key finds no free slot goes to
-// the global table directly.  At the end every CTA merges its threads' slots in a small
-// shared-memory table (smem atomics), then adds each merged entry to the global table once.
-constexpr int kSmallSlots = 4;
+// SUM is exact without overflow checks: a branch-free 64-bit add into `lo` plus a 32-bit carry
+// counter `hi` (value = hi*2^64 + lo) that only changes when the add carries out of (or borrows
+// into) 64 bits — carry != sign(v) — which is rare and predicated.  A row whose key finds no
+// free slot goes to the global table directly.  At the end every CTA merges its threads' slots in
+// a small shared-memory table (smem atomics) and adds each merged entry to the global table once.
+constexpr int kSmallSlots = 4;  // + 1 per-thread trash slot that absorbs filtered rows branch-free
 constexpr int kSmallThreads = 512;
 constexpr int kCtaTable = 32;
+
+inline size_t small_smem_bytes(int nst) {
+  return (size_t)(kSmallSlots + 1) * nst * kSmallThreads * (sizeof(unsigned long long) + sizeof(int));
+}
+
+// Cold path kept out of line (keeps the hot loop small for the instruction cache).
+static __device__ __noinline__ void gb_row_to_global(const Table& t, const Layout& L, uint64_t key, int a, int64_t v) {
+  uint8_t* p = find_or_insert(t, L, key);
+  if (p) apply_state(p, L, a, (unsigned long long)v, (L.kind[a] == ST_SUM && v < 0) ? -1 : 0);
+}
 
 template <class P, int ITEMS>
 __global__ void __launch_bounds__(kSmallThreads, 2) k_gb_small(const __grid_constant__ P prog,
                                                             const int32_t* __restrict__ sel, int64_t n,
                                                             const __grid_constant__ Layout L, Table t) {
-  extern __shared__ unsigned long long acc[];  // [kSmallSlots * nst][nthreads]
+  extern __shared__ unsigned long long acc[];  // lo: [kSmallSlots * nst][nthreads], then hi (int)
   __shared__ unsigned long long ct_key[kCtaTable];
   __shared__ int ct_used[kCtaTable];
   __shared__ unsigned long long ct_lo[kCtaTable][kMaxStates];
   __shared__ int ct_hi[kCtaTable][kMaxStates];
   const int tid = threadIdx.x, nt = blockDim.x, nst = L.nst;
-  for (int j = 0; j < kSmallSlots * nst; ++j) acc[j * nt + tid] = 0;
+  int* acc_hi = (int*)(acc + (size_t)(kSmallSlots + 1) * nst * nt);
+  for (int j = 0; j < (kSmallSlots + 1) * nst; ++j) {
+    acc[j * nt + tid] = 0;
+    acc_hi[j * nt + tid] = 0;
+  }
   for (int j = tid; j < kCtaTable; j += nt) {
     ct_used[j] = 0;
     ct_key[j] = 0;
     for (int a = 0; a < kMaxStates; ++a) { ct_lo[j][a] = 0; ct_hi[j][a] = 0; }
   }
   uint64_t skey[kSmallSlots];
-  bool used[kSmallSlots];
+  unsigned used = 0;  // bit k: slot k holds skey[k]
 #pragma unroll
-  for (int k = 0; k < kSmallSlots; ++k) { skey[k] = 0; used[k] = false; }
+  for (int k = 0; k < kSmallSlots; ++k) skey[k] = 0;
   bool ovf = false;
+  const int stride_slot = nst * nt;
   const int64_t tile = (int64_t)nt * ITEMS;
   for (int64_t base = blockIdx.x * tile; base < n; base += (int64_t)gridDim.x * tile) {
     int32_t row[ITEMS];
@@ -362,32 +378,24 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_gb_small(const __grid_cons
     uint64_t key[ITEMS];
     typename P::template Cache<ITEMS> cache;
     prog.template where_keys<ITEMS>(row, alive, key, cache);
-    int s[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      s[i] = -1;
-      if (!alive[i]) continue;
-#pragma unroll
-      for (int k = 0; k < kSmallSlots; ++k)
-        if (used[k] && skey[k] == key[i]) s[i] = k;
-      if (s[i] < 0) {
-#pragma unroll
-        for (int k = kSmallSlots - 1; k >= 0; --k)
-          if (!used[k]) s[i] = k;
-        if (s[i] >= 0) {
-#pragma unroll
-          for (int k = 0; k < kSmallSlots; ++k)
-            if (k == s[i]) { used[k] = true; skey[k] = key[i]; }
-        }
-      }
-    }
-    // smem cell index of (slot, state 0) per item; -1: not aggregated here (filtered or no slot)
+    // slot per item: match, else claim the lowest free slot, else -1 (global path)
     int cell0[ITEMS];
     bool slow = false;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-      cell0[i] = (alive[i] && s[i] >= 0) ? s[i] * nst * nt + tid : -1;
-      slow |= alive[i] && s[i] < 0;
+      int s = -1;
+#pragma unroll
+      for (int k = 0; k < kSmallSlots; ++k)
+        if (((used >> k) & 1u) && skey[k] == key[i]) s = k;
+      if (alive[i] && s < 0 && used != (1u << kSmallSlots) - 1) {
+        s = __ffs(~used) - 1;
+#pragma unroll
+        for (int k = 0; k < kSmallSlots; ++k)
+          if (k == s) skey[k] = key[i];
+        used |= 1u << s;
+      }
+      cell0[i] = (alive[i] && s >= 0 ? s : kSmallSlots) * stride_slot + tid;  // kSmallSlots = trash
+      slow |= alive[i] && s < 0;
     }
 #pragma unroll
     for (int a = 0; a < P::kMaxNst; ++a) {
@@ -397,42 +405,35 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_gb_small(const __grid_cons
       int64_t v[ITEMS];
       if (kd == ST_COUNT) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i)
-          if (cell0[i] >= 0) acc[cell0[i] + aoff] += 1;
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) v[i] = 1;
+        for (int i = 0; i < ITEMS; ++i) {
+          v[i] = 1;
+          acc[cell0[i] + aoff] += 1;
+        }
       } else {
         prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
         if (kd == ST_SUM) {
 #pragma unroll
           for (int i = 0; i < ITEMS; ++i) {
-            if (cell0[i] < 0) continue;
-            unsigned long long* cell = &acc[cell0[i] + aoff];
-            int64_t o = (int64_t)*cell, nv = (int64_t)((unsigned long long)o + (unsigned long long)v[i]);
-            if (((o ^ nv) & (v[i] ^ nv)) < 0) {  // int64 overflow: flush the partial exactly
-              uint8_t* p = find_or_insert(t, L, key[i]);
-              if (p) apply_state(p, L, a, (unsigned long long)o, o < 0 ? -1 : 0);
-              nv = v[i];
-            }
-            *cell = (unsigned long long)nv;
+            const int c = cell0[i] + aoff;
+            unsigned long long lo = acc[c], nl = lo + (unsigned long long)v[i];
+            acc[c] = nl;
+            bool carry = nl < lo, neg = v[i] < 0;
+            if (carry != neg) acc_hi[c] += carry ? 1 : -1;
           }
         } else {
           const bool mn = kd == ST_MIN;
 #pragma unroll
           for (int i = 0; i < ITEMS; ++i) {
-            if (cell0[i] < 0) continue;
-            unsigned long long* cell = &acc[cell0[i] + aoff];
-            unsigned long long u = mn ? ~order_u(v[i]) : order_u(v[i]), old = *cell;
-            *cell = u > old ? u : old;
+            const int c = cell0[i] + aoff;
+            unsigned long long u = mn ? ~order_u(v[i]) : order_u(v[i]), old = acc[c];
+            acc[c] = u > old ? u : old;
           }
         }
       }
       if (slow) {  // rows whose key found no free register slot: straight to the global table
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-          if (!alive[i] || s[i] >= 0) continue;
-          uint8_t* p = find_or_insert(t, L, key[i]);
-          if (p) apply_state(p, L, a, (unsigned long long)v[i], (kd == ST_SUM && v[i] < 0) ? -1 : 0);
+          if (alive[i] && cell0[i] >= kSmallSlots * stride_slot) gb_row_to_global(t, L, key[i], a, v[i]);
         }
       }
     }
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_gb_small(const __grid_cons
   // CTA merge: each thread's used slots into the shared table (smem atomics), overflow to global
 #pragma unroll
   for (int k = 0; k < kSmallSlots; ++k) {
-    if (!used[k]) continue;
+    if (!((used >> k) & 1u)) continue;
     uint64_t key = skey[k];
     int e = (int)(hash64(key) & (kCtaTable - 1)), found = -1;
     for (int probe = 0; probe < kCtaTable; ++probe) {
@@ -459,19 +460,21 @@ __global__ void __launch_bounds__(kSmallThreads, 2) k_gb_small(const __grid_cons
       e = (e + 1) & (kCtaTable - 1);
     }
     for (int a = 0; a < nst; ++a) {
-      unsigned long long val = acc[(k * nst + a) * nt + tid];
+      const int c = (k * nst + a) * nt + tid;
+      unsigned long long val = acc[c];
+      int hv = acc_hi[c];
       const int kd = L.kind[a];
       if (found < 0) {
         uint8_t* p = find_or_insert(t, L, key);
         if (!p) continue;
-        if (kd == ST_SUM) apply_state(p, L, a, val, (int64_t)val < 0 ? -1 : 0);
+        if (kd == ST_SUM) apply_state(p, L, a, val, hv);
         else if (kd == ST_COUNT) apply_state(p, L, a, val, 0);
         else atomicMax((unsigned long long*)(p + L.off8[a]), val);
         continue;
       }
       if (kd == ST_SUM) {
         unsigned long long old = atomicAdd(&ct_lo[found][a], val);
-        int h = ((int64_t)val < 0 ? -1 : 0) + ((old + val) < old ? 1 : 0);
+        int h = hv + ((old + val) < old ? 1 : 0);
         if (h) atomicAdd(&ct_hi[found][a], h);
       } else if (kd == ST_COUNT) {
         atomicAdd(&ct_lo[found][a], val);

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kBlock) k_build(const __grid_constant__ BuildA
     int64_t r = a.sel ? (int64_t)__ldg(a.sel + idx) : idx;
     if (!eval_conj(a.cols, a.preds, a.np, r)) continue;
     uint64_t key = key_of(a.cols, a.nkeys, a.kc0, a.kc1, r);
-    uint64_t h = hash64(key) & a.mask;
+    uint64_t h = table_hash(key, a.key_bytes) & a.mask;
     if (a.key_bytes == 4) {
       unsigned long long* s = (unsigned long long*)a.slots;
       unsigned long long v = ((unsigned long long)(uint32_t)r << 32) | (uint32_t)key;
@@ -74,7 +74,7 @@ struct ProbeFn {
     for (int i = 0; i < ITEMS; ++i) key[i] = alive[i] ? key_of(cols, nkeys, kc0, kc1, row[i]) : 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-      h[i] = hash64(key[i]) & mask;
+      h[i] = table_hash(key[i], key_bytes) & mask;
       pend[i] = alive[i];
       found[i] = false;
     }
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kBlock) k_probe_inner(const __grid_constant__ 
       alive = eval_conj(a.cols, a.preds, a.np, r);
     }
     uint64_t key = alive ? key_of(a.cols, a.nkeys, a.kc0, a.kc1, r) : 0;
-    uint64_t h = hash64(key) & a.mask;
+    uint64_t h = table_hash(key, a.key_bytes) & a.mask;
     bool pend = alive;
     while (__any_sync(kFull, pend)) {
       bool hit = false;
@@ -323,7 +323,27 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     SX_TRY(scr.get(&op, (size_t)n));
     if (join_type == SX_INNER) SX_TRY(scr.get(&ob, (size_t)n));
     for (int g = 0; g < gs.n; ++g) SX_TRY(scr.get((char**)&gs.g[g].dst, (size_t)n * gs.g[g].width));
-    SX_TRY(run_compact(ctx, f, n, isel, op, ob, gs, &count));
+    auto run_t = [&](auto ft) -> sx_status {
+      for (int i = 0; i < nprobe_cols; ++i) ft.cols[i] = pcols[i];
+      for (int i = 0; i < nwhere; ++i) ft.preds[i] = preds[i];
+      ft.np = nwhere;
+      ft.k0 = (decltype(ft.k0))probe_cols[key_cols[0]].data;
+      ft.k1 = nkeys > 1 ? (const int32_t*)probe_cols[key_cols[1]].data : nullptr;
+      ft.slots = ht->slots;
+      ft.mask = (uint32_t)(ht->cap - 1);
+      ft.anti = join_type == SX_ANTI;
+      return run_compact<decltype(ft), 4>(ctx, ft, n, isel, op, ob, gs, &count);
+    };
+    auto is32 = [&](int c) { int t = probe_cols[key_cols[c]].type; return t == SX_I32 || t == SX_DATE32; };
+    if (ht->cap <= (1ull << 32) && nkeys == 1 && kb == 4 && is32(0)) {
+      SX_TRY(run_t(ProbeFnT<int32_t, 1, 4>{}));
+    } else if (ht->cap <= (1ull << 32) && nkeys == 1 && kb == 8 && probe_cols[key_cols[0]].type == SX_I64) {
+      SX_TRY(run_t(ProbeFnT<long long, 1, 8>{}));
+    } else if (ht->cap <= (1ull << 32) && nkeys == 2 && is32(0) && is32(1)) {
+      SX_TRY(run_t(ProbeFnT<int32_t, 2, 8>{}));
+    } else {
+      SX_TRY(run_compact(ctx, f, n, isel, op, ob, gs, &count));
+    }
   } else {
     InnerArgs a{};
     for (int i = 0; i < nprobe_cols; ++i) a.cols[i] = pcols[i];

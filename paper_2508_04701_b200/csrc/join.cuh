@@ -1,11 +1,107 @@
-// join.cuh — hash-table slot layout shared by join.cu and the executor.
+// join.cuh — hash-table slot layout, the table hash and the specialised probe functors.
 #pragma once
 #include <stdint.h>
 
+#include "common.cuh"
+#include "filter.cuh"
+
 namespace sx {
+
 struct __align__(16) HtSlot8 {
   unsigned long long key;
   unsigned int row;  // 0xFFFFFFFF = empty
   unsigned int pad;
 };
+
+// murmur3 fmix32 (bijective on u32): the slot hash for 32-bit keys (tables <= 2^32 slots).
+__host__ __device__ __forceinline__ uint32_t hash32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+
+// Slot hash used by build and every probe path: 32-bit keys hash in 32 bits, others in 64.
+__device__ __forceinline__ uint64_t table_hash(uint64_t key, int key_bytes) {
+  return key_bytes == 4 ? (uint64_t)hash32((uint32_t)key) : hash64(key);
+}
+
+// Probe functor specialised on the key column type KT (int32_t / long long), the number of key
+// columns NK (2: two int32 columns packed (k0 << 32) | k1, reading R11) and the table layout KB.
+// All ITEMS key loads are issued back to back, then all first-slot loads, then the (rare) longer
+// chains; semi/anti/unique-inner emit at most one output per probe row (ordered compaction).
+template <typename KT, int NK, int KB>
+struct ProbeFnT {
+  DCol cols[SX_MAX_COLS];
+  DPred preds[SX_MAX_PREDS];
+  int np;
+  const KT* k0;
+  const int32_t* k1;
+  const void* slots;
+  uint32_t mask;
+  int anti;
+  template <int ITEMS>
+  __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+                                       int32_t (&aux)[ITEMS]) const {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i];
+    for (int p = 0; p < np; ++p) apply_pred<ITEMS>(cols[preds[p].col], preds[p], row, alive);
+    uint64_t key[ITEMS];
+    uint32_t h[ITEMS];
+    bool pend[ITEMS], found[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = alive[i] ? (uint64_t)(int64_t)__ldg(k0 + row[i]) : 0;
+    if (NK == 2) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        key[i] = (key[i] << 32) | (uint32_t)(alive[i] ? __ldg(k1 + row[i]) : 0);
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      h[i] = (uint32_t)(KB == 4 ? hash32((uint32_t)key[i]) : hash64(key[i])) & mask;
+      pend[i] = alive[i];
+      found[i] = false;
+    }
+    bool any = true;
+    while (any) {
+      any = false;
+      if (KB == 4) {
+        unsigned long long s[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) s[i] = pend[i] ? __ldg((const unsigned long long*)slots + h[i]) : ~0ull;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          if (!pend[i]) continue;
+          uint32_t rw = (uint32_t)(s[i] >> 32);
+          bool empty = rw == 0xffffffffu, hit = !empty && (uint32_t)s[i] == (uint32_t)key[i];
+          found[i] |= hit;
+          if (hit) aux[i] = (int32_t)rw;
+          pend[i] = !empty && !hit;
+          h[i] = (h[i] + 1) & mask;
+          any |= pend[i];
+        }
+      } else {
+        longlong2 s[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) s[i] = pend[i] ? __ldg((const longlong2*)slots + h[i]) : make_longlong2(0, -1);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          if (!pend[i]) continue;
+          uint32_t rw = (uint32_t)(unsigned long long)s[i].y;
+          bool empty = rw == 0xffffffffu, hit = !empty && (uint64_t)s[i].x == key[i];
+          found[i] |= hit;
+          if (hit) aux[i] = (int32_t)rw;
+          pend[i] = !empty && !hit;
+          h[i] = (h[i] + 1) & mask;
+          any |= pend[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) alive[i] = alive[i] && (anti ? !found[i] : found[i]);
+  }
+};
+
 }  // namespace sx
