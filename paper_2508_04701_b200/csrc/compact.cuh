@@ -91,6 +91,16 @@ __global__ void __launch_bounds__(kBlock) k_compact(const __grid_constant__ F f,
   }
 }
 
+// Dense materialisation: out column g [i] = src[sel[i]] (or src[aux[i]] for build-side payload).
+static __global__ void __launch_bounds__(kBlock) k_gather_multi(const int32_t* __restrict__ sel,
+                                                               const int32_t* __restrict__ aux, int64_t n,
+                                                               const __grid_constant__ GatherSpec gs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = __ldg(sel + i), a = aux ? (int64_t)__ldg(aux + i) : 0;
+    for (int g = 0; g < gs.n; ++g) gather_one(gs.g[g], i, gs.g[g].by_aux ? a : r);
+  }
+}
+
 // Host driver: runs the skeleton over n positions; returns the output count (one D2H read).
 // out_sel / out_aux / gather destinations must have capacity >= n.
 template <class F, int ITEMS = 8>
@@ -107,14 +117,23 @@ sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel,
   unsigned int* ctr = ctx->d_counters;
   SX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), ctx->stream));
   unsigned grid = persistent_grid(ctx, 8, ntiles);
+  // Payload columns are gathered in a dense post-pass (one thread per output row) rather than
+  // inside the scan, where only the (few) surviving lanes of each warp would be active.
+  GatherSpec none;
+  none.n = 0;
   if (in_sel)
-    k_compact<F, true, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, out_sel, out_aux, gs, status, ctr, ntiles);
+    k_compact<F, true, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, out_sel, out_aux, none, status, ctr, ntiles);
   else
-    k_compact<F, false, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, out_sel, out_aux, gs, status, ctr, ntiles);
+    k_compact<F, false, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, out_sel, out_aux, none, status, ctr, ntiles);
   SX_CHECK_LAUNCH();
   int64_t last;
   SX_TRY(read_i64(ctx, status + (ntiles - 1), &last));
   *out_count = (int64_t)((unsigned long long)last & ((1ull << 62) - 1));
+  if (gs.n > 0 && *out_count > 0) {
+    k_gather_multi<<<persistent_grid(ctx, 8, (*out_count + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+        out_sel, out_aux, *out_count, gs);
+    SX_CHECK_LAUNCH();
+  }
   return SX_OK;
 }
 

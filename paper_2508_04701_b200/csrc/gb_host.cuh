@@ -2,6 +2,7 @@
 // (table sizing, strategy, retry on a full table) and result extraction/emission.
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "compact.cuh"
@@ -127,9 +128,9 @@ inline sx_status gb_plan(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_ke
 // ------------------------------------------------------------------------ extraction
 struct SlotFn {
   const uint8_t* slots;
-  uint64_t cap;
+  uint64_t cap;     // slots per (sub-)table; sub-table s occupies [s*(cap+1), (s+1)*(cap+1)), side slot last
   int slot_bytes, key_bytes;
-  const int* side_used;
+  const int* side_used;  // one flag per sub-table
   int has_having, hv_kind, hv_op, hv_off8, hv_off4;
   int64_t hv_lo, hv_hi;
   __device__ __forceinline__ bool hv_ok(const uint8_t* p) const {
@@ -162,7 +163,7 @@ struct SlotFn {
       if (valid[i]) {
         const uint8_t* p = slots + (uint64_t)row[i] * slot_bytes;
         if (key_bytes == 0) occ = true;
-        else if ((uint64_t)row[i] == cap) occ = *side_used != 0;
+        else if ((uint64_t)row[i] % (cap + 1) == cap) occ = side_used[(uint64_t)row[i] / (cap + 1)] != 0;
         else if (key_bytes == 4) occ = *(const unsigned*)p != 0u;
         else occ = *(const unsigned long long*)p != 0ull;
         occ = occ && hv_ok(p);
@@ -209,7 +210,7 @@ static __global__ void k_gb_emit(const __grid_constant__ EmitArgs a) {
     const uint8_t* p = a.slots + slot * a.L.slot_bytes;
     if (a.nkeys > 0) {
       uint64_t k = 0;
-      if (slot != a.cap) k = a.L.key_bytes == 4 ? (uint64_t)*(const unsigned*)p : *(const unsigned long long*)p;
+      if (slot % (a.cap + 1) != a.cap) k = a.L.key_bytes == 4 ? (uint64_t)*(const unsigned*)p : *(const unsigned long long*)p;
       if (a.nkeys == 1) {
         int64_t v = a.L.key_bytes == 4 ? (int64_t)(int32_t)(uint32_t)k : (int64_t)k;
         if (a.out_key_type[0] == SX_U8) v = (uint8_t)k;
@@ -261,11 +262,14 @@ inline uint64_t pow2_at_least(uint64_t x) {
   return c;
 }
 
-// Run the aggregation with RowFn and produce the outputs.  `force_small` selects K9.
+// Run the aggregation with program `prog` and produce the outputs.  `force_small` selects K9.
+// Strategies: K9 (keyless / <= kSmallSlots groups), K11 into one table when it fits in half the
+// L2, otherwise partitioned K11 (records into 2^pbits hash partitions, each merged into an
+// L2-resident sub-table).  A table that fills up (bad hint) is resized and the step redone.
 template <class Prog>
 sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* sel, int64_t n,
-                        int64_t groups_hint, sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups,
-                        int force_small = -1) {
+                 int64_t groups_hint, sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups,
+                 int force_small = -1) {
   Scratch scr(ctx);
   const Layout& L = P.L;
   bool keyless = P.nkeys == 0;
@@ -276,36 +280,115 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
   uint64_t cap = keyless ? 1 : pow2_at_least(want + want / 3 + 1);
   uint8_t* table = nullptr;
   int32_t* ids = nullptr;
+  int* side = nullptr;
   int64_t ng = 0;
   int flags[4];
+  uint64_t cap_p = cap;  // slots per sub-table
+  bool no_part = false;
+  int nsub = 1;
   for (int attempt = 0;; ++attempt) {
-    uint64_t nslots = keyless ? 1 : cap + 1;
+    // partition when the table would not stay L2-resident
+    int pbits = 0;
+    // (opt-in until phase A beats the single HBM table: SX_GB_PARTITION=1)
+    static const bool part_enabled = getenv("SX_GB_PARTITION") && getenv("SX_GB_PARTITION")[0] == '1';
+    if (part_enabled && !small && !keyless && !no_part && cap * (uint64_t)L.slot_bytes > ctx->l2_bytes / 2) {
+      while (pbits < 8 && (cap >> pbits) * (uint64_t)L.slot_bytes > ctx->l2_bytes / 4) ++pbits;
+    }
+    nsub = 1 << pbits;
+    cap_p = keyless ? 1 : cap >> pbits;
+    uint64_t nslots = keyless ? 1 : (uint64_t)nsub * (cap_p + 1);
     SX_TRY(scr.get(&table, nslots * L.slot_bytes));
     SX_CUDA(cudaMemsetAsync(table, 0, nslots * L.slot_bytes, ctx->stream));
     SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
-    Table t{table, keyless ? 0 : cap - 1, ctx->d_flags + 2, ctx->d_flags + 1};
-    if (n > 0) {
-      if (small) {
-        size_t smem = small_smem_bytes(L.nst);
-        SX_CUDA(cudaFuncSetAttribute(k_gb_small<Prog, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0;
-        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_small<Prog, 4>, kSmallThreads, smem));
-        if (per_sm < 1) per_sm = 1;
-        int64_t tiles = (n + (int64_t)kSmallThreads * 4 - 1) / ((int64_t)kSmallThreads * 4);
-        unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, tiles);
-        k_gb_small<Prog, 4><<<grid, kSmallThreads, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, t);
-      } else {
-        int64_t tiles = (n + 32 * 4 - 1) / (32 * 4) / (kBlock / 32) + 1;
-        k_gb_global<Prog, 4><<<persistent_grid(ctx, 8, tiles), kBlock, 0, SX_STREAM(ctx)>>>(prog, sel, n, L, t);
-      }
+    SX_TRY(scr.get(&side, (size_t)nsub));
+    SX_CUDA(cudaMemsetAsync(side, 0, nsub * sizeof(int), ctx->stream));
+    Table t{table, keyless ? 0 : cap_p - 1, side, ctx->d_flags + 1};
+    bool part_overflow = false;
+    if (n > 0 && small) {
+      size_t smem = small_smem_bytes(L.nst);
+      SX_CUDA(cudaFuncSetAttribute(k_gb_small<Prog, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_small<Prog, 4>, kSmallThreads, smem));
+      if (per_sm < 1) per_sm = 1;
+      int64_t tiles = (n + (int64_t)kSmallThreads * 4 - 1) / ((int64_t)kSmallThreads * 4);
+      unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, tiles);
+      k_gb_small<Prog, 4><<<grid, kSmallThreads, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, t);
       SX_CHECK_LAUNCH();
+    } else if (n > 0 && nsub == 1) {
+      int64_t tiles = (n + 32 * 4 - 1) / (32 * 4) / (kBlock / 32) + 1;
+      k_gb_global<Prog, 4><<<persistent_grid(ctx, 8, tiles), kBlock, 0, SX_STREAM(ctx)>>>(prog, sel, n, L, t);
+      SX_CHECK_LAUNCH();
+    } else if (n > 0) {
+      // phase A: evaluate + pre-reduce runs + scatter partial records into hash partitions
+      PartOut po;
+      std::memset(&po, 0, sizeof po);
+      po.pbits = pbits;
+      po.regcap = n / nsub + n / nsub / 4 + 4096;
+      int64_t total = po.regcap * nsub;
+      SX_TRY(scr.get(&po.key, (size_t)total));
+      for (int a = 0; a < L.nst; ++a) {
+        SX_TRY(scr.get(&po.lo[a], (size_t)total));
+        if (L.kind[a] == ST_SUM) SX_TRY(scr.get(&po.hi[a], (size_t)total));
+      }
+      SX_TRY(scr.get(&po.cursor, (size_t)nsub));
+      SX_CUDA(cudaMemsetAsync(po.cursor, 0, nsub * sizeof(unsigned), ctx->stream));
+      po.overflow = ctx->d_flags + 3;
+      // write-combining staging: ~160 KB of shared memory per CTA, one CTA per SM
+      size_t rec = 8 + 8 * (size_t)L.nst + 4 * (size_t)L.nst;
+      int wc_cap = (int)std::min<size_t>(128, (160u << 10) / ((size_t)nsub * rec));
+      if (wc_cap < 8) wc_cap = 8;
+      size_t smem = (size_t)nsub * wc_cap * rec;
+      // expected records per partition per tile ~ tile_rows / nsub; flush at ~half the region
+      int wc_tiles = std::max(1, (int)(wc_cap / 2 * nsub / 1024));
+      SX_CUDA(cudaFuncSetAttribute(k_gb_part<Prog, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int64_t tiles = (n + (int64_t)kBlock * 4 - 1) / ((int64_t)kBlock * 4);
+      unsigned grid = (unsigned)std::min<int64_t>(ctx->num_sms, tiles);
+      k_gb_part<Prog, 4><<<grid, kBlock, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, po, wc_cap, wc_tiles);
+      SX_CHECK_LAUNCH();
+      std::vector<unsigned> cnt((size_t)nsub);
+      SX_CUDA(cudaMemcpyAsync(cnt.data(), po.cursor, nsub * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+      SX_CUDA(cudaMemcpyAsync(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      SX_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (flags[3]) {
+        part_overflow = true;  // a skewed partition: redo unpartitioned
+      } else {
+        // phase B: one launch per partition, each into its own L2-resident sub-table
+        for (int q = 0; q < nsub; ++q) {
+          if (!cnt[q]) continue;
+          MergeArgs m;
+          std::memset(&m, 0, sizeof m);
+          int64_t off = (int64_t)q * po.regcap;
+          m.key = po.key + off;
+          for (int a = 0; a < L.nst; ++a) {
+            m.lo[a] = po.lo[a] + off;
+            m.hi[a] = po.hi[a] ? po.hi[a] + off : nullptr;
+          }
+          m.n = cnt[q];
+          Table tq{table + (uint64_t)q * (cap_p + 1) * L.slot_bytes, cap_p - 1, side + q, ctx->d_flags + 1};
+          k_gb_merge_records<<<persistent_grid(ctx, 8, (m.n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(m, L, tq);
+          SX_CHECK_LAUNCH();
+        }
+      }
+      for (int a = 0; a < L.nst; ++a) {
+        dfree(ctx, po.lo[a]); scr.release(po.lo[a]);
+        if (po.hi[a]) { dfree(ctx, po.hi[a]); scr.release(po.hi[a]); }
+      }
+      dfree(ctx, po.key); scr.release(po.key);
+    }
+    if (part_overflow) {
+      if (attempt >= 2) return set_err(ctx, SX_ENOMEM, "partitioned aggregation overflow");
+      dfree(ctx, table); scr.release(table);
+      // fall back to a single HBM table
+      small = false;
+      no_part = true;
+      continue;
     }
     SlotFn sf;
     sf.slots = table;
-    sf.cap = keyless ? 1 : cap;
+    sf.cap = keyless ? 1 : cap_p;
     sf.slot_bytes = L.slot_bytes;
     sf.key_bytes = L.key_bytes;
-    sf.side_used = ctx->d_flags + 2;
+    sf.side_used = side;
     sf.has_having = P.has_having;
     if (P.has_having) {
       int s = P.agg_state[P.hv.agg];
@@ -336,7 +419,7 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
   ea.slots = table;
   ea.ids = ids;
   ea.n = ng;
-  ea.cap = keyless ? 1 : cap;
+  ea.cap = keyless ? 1 : cap_p;
   ea.L = L;
   ea.nkeys = P.nkeys;
   ea.naggs = P.naggs;

@@ -315,6 +315,199 @@ __global__ void __launch_bounds__(kBlock, 3) k_gb_global(const __grid_constant__
   if (ovf) atomicExch(prog.ovf_flag, 1);
 }
 
+// ------------------------------------------------------------------------------ partitioned K11
+// Large G (table >> L2, e.g. Q18's 1.5e8 orderkeys): random updates into an HBM-resident table
+// cost ~128 B of DRAM traffic each.  Instead, phase A evaluates the rows exactly like k_gb_global
+// (filter, key, states, segmented warp pre-reduction of runs) but the run-tail lanes append a
+// partial-aggregate record (key, state partials) to one of 2^pbits hash partitions (top hash
+// bits; the table slot uses the low bits).  Phase B merges each partition's records into its own
+// L2-resident sub-table (k_gb_merge_records).  Records: SoA, region p holds <= regcap records.
+struct PartOut {
+  unsigned long long* key;      // [P * regcap]
+  unsigned long long* lo[kMaxStates];
+  int* hi[kMaxStates];          // SUM states only
+  unsigned int* cursor;         // [P]
+  int64_t regcap;
+  int pbits;
+  int* overflow;
+};
+
+// Shared-memory write combining: each CTA keeps, per partition, a region of `wc_cap` staged
+// records; run tails append with a shared atomic, and every `wc_tiles` tiles (or when a region
+// could overflow) the CTA reserves each partition's chunk with one global atomic and writes it out
+// contiguously.  A record that finds its staging region full is written directly (rare).
+template <class P, int ITEMS>
+__global__ void __launch_bounds__(kBlock, 1) k_gb_part(const __grid_constant__ P prog, const int32_t* __restrict__ sel,
+                                                       int64_t n, const __grid_constant__ Layout L,
+                                                       const __grid_constant__ PartOut o, int wc_cap, int wc_tiles) {
+  extern __shared__ unsigned long long wc[];  // [nparts * wc_cap] keys, then per state lo, then hi (int)
+  __shared__ int wcnt[1024];
+  __shared__ unsigned long long wbase[1024];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int nparts = 1 << o.pbits;
+  const int nst = L.nst;
+  const int64_t R = (int64_t)nparts * wc_cap;
+  unsigned long long* s_key = wc;
+  auto s_lo = [&](int a) { return wc + R * (1 + a); };
+  int* s_hi_base = (int*)(wc + R * (1 + nst));
+  for (int q = threadIdx.x; q < nparts; q += blockDim.x) wcnt[q] = 0;
+  __syncthreads();
+  const unsigned lt = lanemask_lt();
+  bool ovf = false;
+  const int64_t tile_rows = (int64_t)nwarp * 32 * ITEMS;
+  const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
+  int since_flush = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles + 0; tile += gridDim.x) {
+    const int64_t base = tile * tile_rows + (int64_t)wid * 32 * ITEMS;
+    int32_t row[ITEMS];
+    bool alive[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      int64_t idx = base + 32 * i + lane;
+      alive[i] = idx < n;
+      row[i] = alive[i] ? (sel ? __ldg(sel + idx) : (int32_t)idx) : 0;
+    }
+    uint64_t key[ITEMS];
+    typename P::template Cache<ITEMS> cache;
+    prog.template where_keys<ITEMS>(row, alive, key, cache);
+    unsigned seg_start[ITEMS];
+    int spos[ITEMS];      // staging index of this lane's run tail (-1: none / direct)
+    int64_t dpos[ITEMS];  // direct global index when staging is full (-1: none)
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      uint64_t pk = __shfl_up_sync(kFull, key[i], 1);
+      bool pa = __shfl_up_sync(kFull, alive[i], 1);
+      bool head = !alive[i] || lane == 0 || !pa || pk != key[i];
+      unsigned heads = __ballot_sync(kFull, head);
+      uint64_t nk = __shfl_down_sync(kFull, key[i], 1);
+      bool na = __shfl_down_sync(kFull, alive[i], 1);
+      bool tail = alive[i] && (lane == 31 || !na || nk != key[i]);
+      seg_start[i] = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+      spos[i] = -1;
+      dpos[i] = -1;
+      if (tail) {
+        unsigned part = (unsigned)(hash64(key[i]) >> (64 - o.pbits));
+        int r = atomicAdd(&wcnt[part], 1);
+        if (r < wc_cap) {
+          spos[i] = (int)part * wc_cap + r;
+          s_key[spos[i]] = key[i];
+        } else {
+          unsigned long long g = atomicAdd(o.cursor + part, 1u);
+          if ((int64_t)g < o.regcap) {
+            dpos[i] = (int64_t)part * o.regcap + (int64_t)g;
+            o.key[dpos[i]] = key[i];
+          } else {
+            atomicExch(o.overflow, 1);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < P::kMaxNst; ++a) {
+      if (a >= nst) break;
+      const int kd = prog.kind(a, L);
+      int64_t v[ITEMS];
+      if (kd == ST_COUNT) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) v[i] = alive[i] ? 1 : 0;
+      } else {
+        prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
+      }
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        unsigned long long l;
+        int32_t h = 0;
+        if (kd == ST_SUM || kd == ST_COUNT) {
+          l = alive[i] ? (unsigned long long)v[i] : 0;
+          h = (alive[i] && v[i] < 0) ? -1 : 0;
+          for (int q = 1; q < 32; q <<= 1) {
+            unsigned long long l2 = __shfl_up_sync(kFull, l, q);
+            int32_t h2 = __shfl_up_sync(kFull, h, q);
+            if (lane - q >= (int)seg_start[i]) {
+              unsigned long long s2 = l + l2;
+              h += h2 + (s2 < l ? 1 : 0);
+              l = s2;
+            }
+          }
+        } else {
+          int64_t m = alive[i] ? v[i] : (kd == ST_MIN ? INT64_MAX : INT64_MIN);
+          for (int q = 1; q < 32; q <<= 1) {
+            int64_t m2 = __shfl_up_sync(kFull, m, q);
+            if (lane - q >= (int)seg_start[i]) m = (kd == ST_MIN) ? (m2 < m ? m2 : m) : (m2 > m ? m2 : m);
+          }
+          l = (unsigned long long)m;
+        }
+        if (spos[i] >= 0) {
+          s_lo(a)[spos[i]] = l;
+          if (kd == ST_SUM) s_hi_base[R * a + spos[i]] = h;
+        } else if (dpos[i] >= 0) {
+          o.lo[a][dpos[i]] = l;
+          if (kd == ST_SUM) o.hi[a][dpos[i]] = h;
+        }
+      }
+    }
+    // flush every wc_tiles tiles and after the CTA's last tile
+    ++since_flush;
+    bool last = tile + gridDim.x >= ntiles;
+    if (since_flush >= wc_tiles || last) {
+      since_flush = 0;
+      __syncthreads();
+      for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
+        int c = wcnt[q] < wc_cap ? wcnt[q] : wc_cap;
+        wcnt[q] = c;
+        wbase[q] = c ? atomicAdd(o.cursor + q, (unsigned)c) : 0;
+      }
+      __syncthreads();
+      for (int q = wid; q < nparts; q += nwarp) {
+        int c = wcnt[q];
+        for (int j = lane; j < c; j += 32) {
+          int64_t g = (int64_t)wbase[q] + j;
+          if (g >= o.regcap) {
+            atomicExch(o.overflow, 1);
+            continue;
+          }
+          int64_t dst = (int64_t)q * o.regcap + g;
+          int src = q * wc_cap + j;
+          o.key[dst] = s_key[src];
+          for (int a = 0; a < nst; ++a) {
+            o.lo[a][dst] = s_lo(a)[src];
+            if (L.kind[a] == ST_SUM) o.hi[a][dst] = s_hi_base[R * a + src];
+          }
+        }
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < nparts; q += blockDim.x) wcnt[q] = 0;
+      __syncthreads();
+    }
+  }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
+}
+
+// Phase B: merge partition p's records (partial states) into its L2-resident sub-table.
+struct MergeArgs {
+  const unsigned long long* key;
+  const unsigned long long* lo[kMaxStates];
+  const int* hi[kMaxStates];
+  int64_t n;
+};
+
+static __global__ void __launch_bounds__(kBlock) k_gb_merge_records(const __grid_constant__ MergeArgs m,
+                                                             const __grid_constant__ Layout L, Table t) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m.n; r += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t* p = find_or_insert(t, L, __ldg(m.key + r));
+    if (!p) continue;
+    for (int a = 0; a < L.nst; ++a) {
+      unsigned long long lo = __ldg(m.lo[a] + r);
+      switch (L.kind[a]) {
+        case ST_SUM: atomic_add_sum96((unsigned long long*)(p + L.off8[a]), (int*)(p + L.off4[a]), (int64_t)lo, __ldg(m.hi[a] + r)); break;
+        case ST_COUNT: atomicAdd((unsigned long long*)(p + L.off8[a]), lo); break;
+        case ST_MIN: atomicMax((unsigned long long*)(p + L.off8[a]), ~order_u((int64_t)lo)); break;
+        default: atomicMax((unsigned long long*)(p + L.off8[a]), order_u((int64_t)lo)); break;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------ K9: small G
 // Shared-memory privatised aggregation for very few groups (Q1: 4; keyless reduce: 1).
 // Each thread owns NSLOT (key -> state vector) slots; slot keys live in registers, the state
@@ -340,7 +533,7 @@ static __device__ __noinline__ void gb_row_to_global(const Table& t, const Layou
 }
 
 template <class P, int ITEMS>
-__global__ void __launch_bounds__(kSmallThreads, 2) k_gb_small(const __grid_constant__ P prog,
+__global__ void __launch_bounds__(kSmallThreads, (P::kMaxNst <= 2 ? 2 : 1)) k_gb_small(const __grid_constant__ P prog,
                                                             const int32_t* __restrict__ sel, int64_t n,
                                                             const __grid_constant__ Layout L, Table t) {
   extern __shared__ unsigned long long acc[];  // lo: [kSmallSlots * nst][nthreads], then hi (int)

@@ -218,6 +218,7 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
   uint64_t cap = 64;
   while (cap < (uint64_t)(2 * n)) cap <<= 1;
   size_t slot_bytes = a.key_bytes == 4 ? 8 : 16;
+  if (cap * slot_bytes * 2 <= (32ull << 20)) cap <<= 1;  // small (L2-resident) tables: load <= 0.25
   sx_ht* ht = new sx_ht();
   ht->key_bytes = a.key_bytes;
   ht->key_types[0] = types[0];

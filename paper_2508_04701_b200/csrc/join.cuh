@@ -65,23 +65,42 @@ struct ProbeFnT {
       found[i] = false;
     }
     bool any = true;
-    while (any) {
-      any = false;
-      if (KB == 4) {
-        unsigned long long s[ITEMS];
+    if (KB == 4) {
+      // two 8-byte slots per 16-byte load: the aligned pair holding h, then h+2, ...  In the first
+      // pair of an odd h the even slot precedes the home slot: it can never hold this key (equal
+      // keys share the home slot and lie at or after it) and its emptiness must not stop the scan.
+      bool first[ITEMS];
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) s[i] = pend[i] ? __ldg((const unsigned long long*)slots + h[i]) : ~0ull;
+      for (int i = 0; i < ITEMS; ++i) {
+        first[i] = (h[i] & 1u) != 0;
+        h[i] &= ~1u;
+      }
+      while (any) {
+        any = false;
+        ulonglong2 s[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+          s[i] = pend[i] ? __ldg((const ulonglong2*)slots + (h[i] >> 1)) : make_ulonglong2(~0ull, ~0ull);
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           if (!pend[i]) continue;
-          uint32_t rw = (uint32_t)(s[i] >> 32);
-          bool empty = rw == 0xffffffffu, hit = !empty && (uint32_t)s[i] == (uint32_t)key[i];
-          found[i] |= hit;
-          if (hit) aux[i] = (int32_t)rw;
-          pend[i] = !empty && !hit;
-          h[i] = (h[i] + 1) & mask;
+          uint32_t r0 = (uint32_t)(s[i].x >> 32), r1 = (uint32_t)(s[i].y >> 32);
+          bool e0 = r0 == 0xffffffffu && !first[i], e1 = r1 == 0xffffffffu;
+          bool h0 = r0 != 0xffffffffu && !first[i] && (uint32_t)s[i].x == (uint32_t)key[i];
+          bool h1 = !e0 && !h0 && r1 != 0xffffffffu && (uint32_t)s[i].y == (uint32_t)key[i];
+          found[i] |= h0 || h1;
+          if (h0) aux[i] = (int32_t)r0;
+          if (h1) aux[i] = (int32_t)r1;
+          pend[i] = !(e0 || h0 || e1 || h1);
+          first[i] = false;
+          h[i] = (h[i] + 2) & mask;
           any |= pend[i];
         }
+      }
+    }
+    while (any) {
+      any = false;
+      if (KB == 4) {
       } else {
         longlong2 s[ITEMS];
 #pragma unroll
