@@ -131,6 +131,7 @@ struct SlotFn {
   uint64_t cap;     // slots per (sub-)table; sub-table s occupies [s*(cap+1), (s+1)*(cap+1)), side slot last
   int slot_bytes, key_bytes;
   const int* side_used;  // one flag per sub-table
+  int nsub;
   int has_having, hv_kind, hv_op, hv_off8, hv_off4;
   int64_t hv_lo, hv_hi;
   __device__ __forceinline__ bool hv_ok(const uint8_t* p) const {
@@ -163,7 +164,8 @@ struct SlotFn {
       if (valid[i]) {
         const uint8_t* p = slots + (uint64_t)row[i] * slot_bytes;
         if (key_bytes == 0) occ = true;
-        else if ((uint64_t)row[i] % (cap + 1) == cap) occ = side_used[(uint64_t)row[i] / (cap + 1)] != 0;
+        else if (nsub == 1 ? (uint64_t)row[i] == cap : (uint64_t)row[i] % (cap + 1) == cap)
+          occ = side_used[nsub == 1 ? 0 : (uint64_t)row[i] / (cap + 1)] != 0;
         else if (key_bytes == 4) occ = *(const unsigned*)p != 0u;
         else occ = *(const unsigned long long*)p != 0ull;
         occ = occ && hv_ok(p);
@@ -389,6 +391,7 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
     sf.slot_bytes = L.slot_bytes;
     sf.key_bytes = L.key_bytes;
     sf.side_used = side;
+    sf.nsub = nsub;
     sf.has_having = P.has_having;
     if (P.has_having) {
       int s = P.agg_state[P.hv.agg];
