@@ -200,6 +200,44 @@ sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_sort
 /* ---- materialization helper: out[i] = col[sel[i]] (any fixed-width type) ---- */
 sx_status sx_gather(sx_ctx* ctx, const sx_col* col, const sx_sel* sel, sx_col* out);
 
+/* ---- FINAL phase of a distributed aggregation (avg carried as sum+count) ----
+ * Groups partial rows (e.g. the allgathered outputs of sx_groupby_agg on every rank) by 1-2 key
+ * columns and combines each partial column exactly: ops[j] = SX_SUM (SX_I128 partial sums, int128
+ * add), SX_COUNT (SX_I64, add), SX_MIN / SX_MAX (SX_I64).  AVG: merge its SUM and COUNT, then sx_avg.
+ * Output types = input types; optional HAVING on a merged column; order unspecified.  Syncs once. */
+sx_status sx_groupby_merge(sx_ctx* ctx, const sx_col* keys, int nkeys, const sx_col* parts, const int32_t* ops,
+                           int nparts, const sx_having* having, int64_t groups_hint, sx_col* out_keys,
+                           sx_col* out_parts, int64_t* out_ngroups);
+/* avg = (double)sum / (double)count / 10^scale, element-wise (reading R3). */
+sx_status sx_avg(sx_ctx* ctx, const sx_col* sum /* SX_I128 */, const sx_col* count /* SX_I64 */, int scale,
+                 sx_col* out /* SX_F64 */);
+
+/* ---- H5/H10: partitioning and exchange across GPUs (NCCL over NVLink) ----------
+ * Destination rank of a key = ((hash64(key) >> 32) * nranks) >> 32 — the high hash bits, disjoint
+ * from the low bits that pick hash-table slots (reading R14); two 32-bit key columns are packed
+ * (k0 << 32) | k1 first.  sx_dest_rank is the host mirror of that function. */
+int sx_dest_rank(uint64_t key, int nranks);
+/* Regroup the selected rows by destination rank: out_cols[c] holds rank 0's rows, then rank 1's,
+ * ... (input order kept within each destination); counts[d] (host) = rows for rank d. */
+sx_status sx_partition_by_rank(sx_ctx* ctx, const sx_col* cols, int ncols, const int32_t* key_cols, int nkeys,
+                               const sx_sel* in_sel, int nranks, sx_col* out_cols, int64_t* counts /* host */);
+typedef struct sx_comm sx_comm;
+/* 128-byte NCCL unique id (host); create on one rank, distribute, then sx_comm_init on every rank. */
+sx_status sx_comm_unique_id(void* out);
+sx_status sx_comm_init(sx_ctx* ctx, const void* unique_id, int rank, int nranks, sx_comm** out);
+void sx_comm_destroy(sx_comm* comm);
+int sx_comm_rank(const sx_comm* comm);
+int sx_comm_size(const sx_comm* comm);
+/* Hash shuffle: every rank sends each selected row to sx_dest_rank(key) (partition + counts
+ * allgather + grouped ncclSend/ncclRecv).  out_cols: received rows, ordered by source rank.
+ * Syncs once (counts).  Collective: all ranks must call it. */
+sx_status sx_shuffle(sx_ctx* ctx, sx_comm* comm, const sx_col* cols, int ncols, const int32_t* key_cols, int nkeys,
+                     const sx_sel* in_sel, sx_col* out_cols, int64_t* out_rows /* host */);
+/* Broadcast/merge exchange: concatenation of every rank's columns in rank order (variable
+ * lengths).  Syncs once (lengths).  Collective. */
+sx_status sx_allgather(sx_ctx* ctx, sx_comm* comm, const sx_col* cols, int ncols, sx_col* out_cols,
+                       int64_t* out_rows /* host */);
+
 /* ---- fixed-plan executor: TPC-H Q1/Q3/Q6/Q9/Q18 ---------------------------------
  * Stands in for the Substrait consumer (north_star).  Columns are device
  * buffers as produced by gen/ (orderkey I32 or I64; decimals DEC64 scale 2;

@@ -230,6 +230,44 @@ class Ctx:
         self.check(self.L.sx_gather(self.h, C.byref(c), C.byref(s), C.byref(out)))
         return self.take_col(out)
 
+    def groupby_merge(self, keys, parts, ops, having=None, groups_hint=0):
+        """keys/parts: sx_col lists (partials); ops: 'sum'|'count'|'min'|'max' -> (keys, parts, n)"""
+        ka = (A.Col * len(keys))(*keys)
+        pa = (A.Col * max(len(parts), 1))(*parts)
+        oa = (C.c_int32 * max(len(ops), 1))(*[_AGGS[o] for o in ops])
+        hv = None
+        if having is not None:
+            hv = A.Having(having[0], _OPS[having[1]], int(having[2]), int(having[3]) if len(having) > 3 else 0)
+        ok = (A.Col * 2)()
+        op = (A.Col * max(len(parts), 1))()
+        ng = C.c_int64()
+        self.check(self.L.sx_groupby_merge(self.h, ka, len(keys), pa, oa, len(parts), C.byref(hv) if hv else None,
+                                           groups_hint, ok, op, C.byref(ng)))
+        return [self.take_col(ok[i]) for i in range(len(keys))], [self.take_col(op[i]) for i in range(len(parts))], ng.value
+
+    def avg(self, sum_col: A.Col, count_col: A.Col, scale: int):
+        out = A.Col()
+        self.check(self.L.sx_avg(self.h, C.byref(sum_col), C.byref(count_col), scale, C.byref(out)))
+        return self.take_col(out)
+
+    def partition_by_rank(self, cols, key_cols, nranks, in_sel=None):
+        """-> (partitioned tensors, counts list)"""
+        ca = (A.Col * len(cols))(*cols)
+        kc = (C.c_int32 * len(key_cols))(*key_cols)
+        outs = (A.Col * len(cols))()
+        cnt = (C.c_int64 * nranks)()
+        isel = self.sel(in_sel) if in_sel is not None else None
+        self.check(self.L.sx_partition_by_rank(self.h, ca, len(cols), kc, len(key_cols), C.byref(isel) if isel else None,
+                                               nranks, outs, cnt))
+        return [self.take_col(outs[i]) for i in range(len(cols))], [int(x) for x in cnt]
+
+    def copy_into(self, dst, dst_off: int, src, n: int):
+        """dst[dst_off:dst_off+n] = src[:n] (stream-ordered device copy; rows of any width)."""
+        if n <= 0:
+            return
+        w = src.element_size() * (src.shape[1] if src.dim() > 1 else 1)
+        self.check(self.L.sx_memcpy(self.h, C.c_void_p(dst.data_ptr() + dst_off * w), C.c_void_p(src.data_ptr()), n * w))
+
     # --------------------------------------------------------------- profiling
     def profile(self, on: bool = True):
         self.check(self.L.sx_profile_enable(self.h, 1 if on else 0))

@@ -115,7 +115,9 @@ class Q18Row(C.Structure):
 EXPORTS = ["sx_ctx_create", "sx_ctx_destroy", "sx_last_error", "sx_free", "sx_sync", "sx_memcpy", "sx_profile_enable",
            "sx_profile_read", "sx_launch_count", "sx_filter", "sx_groupby_agg", "sx_hash_build", "sx_hash_probe", "sx_ht_rows",
            "sx_ht_destroy", "sx_sort_topk", "sx_gather", "sx_tpch_default_params", "sx_tpch_q1", "sx_tpch_q6",
-           "sx_tpch_q3", "sx_tpch_q9", "sx_tpch_q18"]
+           "sx_tpch_q3", "sx_tpch_q9", "sx_tpch_q18", "sx_groupby_merge", "sx_avg", "sx_dest_rank",
+           "sx_partition_by_rank", "sx_comm_unique_id", "sx_comm_init", "sx_comm_destroy", "sx_comm_rank",
+           "sx_comm_size", "sx_shuffle", "sx_allgather"]
 
 
 def load(path: str = LIB_PATH):
@@ -154,4 +156,17 @@ def load(path: str = LIB_PATH):
     for q, row in (("q1", Q1Row), ("q3", Q3Row), ("q9", Q9Row), ("q18", Q18Row)):
         getattr(L, f"sx_tpch_{q}").argtypes = [vp, P(TpchTables), P(TpchParams), P(row), i64, P(C.c_int64)]
     L.sx_tpch_q6.argtypes = [vp, P(TpchTables), P(TpchParams), P(Q6Row), P(C.c_int64)]
+    L.sx_groupby_merge.argtypes = [vp, P(Col), i32, P(Col), vp, i32, P(Having), i64, P(Col), P(Col), P(C.c_int64)]
+    L.sx_avg.argtypes = [vp, P(Col), P(Col), i32, P(Col)]
+    L.sx_dest_rank.argtypes = [C.c_uint64, i32]
+    L.sx_dest_rank.restype = i32
+    L.sx_partition_by_rank.argtypes = [vp, P(Col), i32, vp, i32, P(Sel), i32, P(Col), vp]
+    L.sx_comm_unique_id.argtypes = [vp]
+    L.sx_comm_init.argtypes = [vp, vp, i32, i32, P(vp)]
+    L.sx_comm_destroy.argtypes = [vp]
+    L.sx_comm_destroy.restype = None
+    L.sx_comm_rank.argtypes = [vp]
+    L.sx_comm_size.argtypes = [vp]
+    L.sx_shuffle.argtypes = [vp, vp, P(Col), i32, vp, i32, P(Sel), P(Col), P(C.c_int64)]
+    L.sx_allgather.argtypes = [vp, vp, P(Col), i32, P(Col), P(C.c_int64)]
     return L

@@ -364,6 +364,8 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
           for (int a = 0; a < L.nst; ++a) {
             m.lo[a] = po.lo[a] + off;
             m.hi[a] = po.hi[a] ? po.hi[a] + off : nullptr;
+            m.lo_stride[a] = 1;
+            m.hi_stride[a] = 1;
           }
           m.n = cnt[q];
           Table tq{table + (uint64_t)q * (cap_p + 1) * L.slot_bytes, cap_p - 1, side + q, ctx->d_flags + 1};

@@ -484,10 +484,14 @@ __global__ void __launch_bounds__(kBlock, 1) k_gb_part(const __grid_constant__ P
 }
 
 // Phase B: merge partition p's records (partial states) into its L2-resident sub-table.
+// Also the FINAL phase of a distributed group-by (sx_groupby_merge): partial rows gathered from
+// all ranks are records too (I128 sums read with stride 2 / hi word at +8 bytes).
 struct MergeArgs {
   const unsigned long long* key;
   const unsigned long long* lo[kMaxStates];
   const int* hi[kMaxStates];
+  int lo_stride[kMaxStates];  // in u64 units (1: records, 2: SX_I128 columns)
+  int hi_stride[kMaxStates];  // in int units (1: records, 4: SX_I128 columns)
   int64_t n;
 };
 
@@ -497,9 +501,9 @@ static __global__ void __launch_bounds__(kBlock) k_gb_merge_records(const __grid
     uint8_t* p = find_or_insert(t, L, __ldg(m.key + r));
     if (!p) continue;
     for (int a = 0; a < L.nst; ++a) {
-      unsigned long long lo = __ldg(m.lo[a] + r);
+      unsigned long long lo = __ldg(m.lo[a] + r * m.lo_stride[a]);
       switch (L.kind[a]) {
-        case ST_SUM: atomic_add_sum96((unsigned long long*)(p + L.off8[a]), (int*)(p + L.off4[a]), (int64_t)lo, __ldg(m.hi[a] + r)); break;
+        case ST_SUM: atomic_add_sum96((unsigned long long*)(p + L.off8[a]), (int*)(p + L.off4[a]), (int64_t)lo, __ldg(m.hi[a] + r * m.hi_stride[a])); break;
         case ST_COUNT: atomicAdd((unsigned long long*)(p + L.off8[a]), lo); break;
         case ST_MIN: atomicMax((unsigned long long*)(p + L.off8[a]), ~order_u((int64_t)lo)); break;
         default: atomicMax((unsigned long long*)(p + L.off8[a]), order_u((int64_t)lo)); break;
