@@ -211,18 +211,37 @@ def main():
     from paper_2508_04701_b200 import tpch
 
     ctx = sx.Ctx(local)
-    # weak scaling: every rank holds its own SF-sized replica (the NCCL-sharded SF1000 path is
-    # DESIGN.md "next"); value is the whole-job aggregate.
-    tables = gen.gpu_tables(sf_milli, seed=args.seed, device=f"cuda:{local}")
-    T = tpch.Tpch(ctx, tables)
+    if world > 1:
+        # weak scaling: total SF = sf x world, rank r holds shard r of every table (orders and
+        # lineitem co-partitioned on orderkey); exchanges (allgather / shuffle) run over libsx's
+        # NCCL communicator; torch.distributed only distributes the NCCL unique id.
+        from paper_2508_04701_b200.sharded import NcclComm, ShardedTpch
+
+        uid = [NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = NcclComm(ctx, rank, world, uid[0])
+        sf_total = sf_milli * world
+        tables = gen.gpu_tables(sf_total, seed=args.seed, shard=(rank, world), device=f"cuda:{local}")
+        runner = ShardedTpch(ctx, comm, [tables])
+        run = runner.run
+    else:
+        sf_total = sf_milli
+        tables = gen.gpu_tables(sf_milli, seed=args.seed, device=f"cuda:{local}")
+        T = tpch.Tpch(ctx, tables)
+        run = T.run
     n = table_sizes(tables)
     qb = query_bytes(n)
     step_bytes = sum(qb.values())
+    job_bytes = step_bytes
+    if dist:
+        tb = torch.tensor([step_bytes], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tb)
+        job_bytes = float(tb.item())
 
     # parity at full size against the committed oracle answers (when present for this SF/seed)
     parity = "not checked (no committed answers for this SF/seed)"
-    ans_path = os.path.join(ROOT, "tests", "golden", f"answers_sf{sf_milli}_seed{args.seed}.json")
-    results = {q: T.run(q) for q in QUERIES}
+    ans_path = os.path.join(ROOT, "tests", "golden", f"answers_sf{sf_total}_seed{args.seed}.json")
+    results = {q: run(q) for q in QUERIES}
     if os.path.exists(ans_path):
         import oracle as _or  # test infrastructure: only the committed answer decoding is used here
         from tests.helpers import rows_equal
@@ -243,7 +262,7 @@ def main():
 
     for _ in range(args.warmup):
         for q in QUERIES:
-            T.run(q)
+            run(q)
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -258,7 +277,7 @@ def main():
         e0.record(stream)
         for _ in range(args.steps):
             for q in QUERIES:
-                T.run(q)
+                run(q)
         e1.record(stream)
         torch.cuda.synchronize()
         if dist:
@@ -271,7 +290,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = step_bytes * world / (ms / 1e3) / 1e9
+    value = job_bytes / (ms / 1e3) / 1e9
 
     # per-operator breakdown (query-level entries and operator entries in call order)
     per_q = {q.upper(): [] for q in QUERIES}
@@ -330,18 +349,18 @@ def main():
                 for cn, t in cols.items():
                     tables[tn][cn].copy_(t, non_blocking=True)
             for q in QUERIES:
-                r = T.run(q)  # results land in host memory inside the call
+                r = run(q)  # results land in host memory inside the call
                 d2h += 0
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1) / args.e2e_steps
         # result bytes per step (host row structs): Q1 4x, Q6 1x, Q3 10x, Q9 175x, Q18 100x rows
         d2h = 4 * 112 + 32 + 10 * 40 + 175 * 24 + 100 * 40
-        ev = step_bytes * world / (e_ms / 1e3) / 1e9
+        ev = job_bytes / (e_ms / 1e3) / 1e9
         if dist:
             t = torch.tensor([e_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ev = step_bytes * world / (float(t.item()) / 1e3) / 1e9
+            ev = job_bytes / (float(t.item()) / 1e3) / 1e9
         e2e = {"value": round(ev, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h,
                "ms_per_step": round(e_ms, 3)}
         del host
@@ -368,7 +387,9 @@ def main():
                        "sf": args.sf, "seed": args.seed, "rows_lineitem": n["l"],
                        "algorithmic_bytes_per_step": step_bytes, "query_bytes": qb,
                        "l2_note": "inputs (>30 GB) >> 126 MB L2; no flush needed",
-                       "parallelism": f"replicas x{world} (sharded exchange: next)"},
+                       "sf_total": sf_total / 1000, "job_bytes_per_step": job_bytes,
+                       "parallelism": (f"sharded x{world}: rank r holds shard r of SF{sf_total / 1000:g}; "
+                                       "allgather/shuffle over NCCL" if world > 1 else "single GPU")},
             "query_ms": q_ms, "operator_ms": op_ms, "parity": parity,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),

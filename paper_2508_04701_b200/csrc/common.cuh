@@ -47,6 +47,9 @@ struct sx_ht {
   uint64_t cap = 0;        // slots (power of two)
   void* slots = nullptr;
   int64_t rows = 0;        // inserted build rows
+  uint32_t* bm = nullptr;  // exact bitmap over [bm_min, bm_min + bm_bits) of the build keys (or null)
+  long long bm_min = 0;
+  unsigned long long bm_bits = 0;
 };
 
 namespace sx {

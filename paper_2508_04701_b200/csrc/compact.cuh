@@ -1,40 +1,36 @@
-// compact.cuh — ordered stream compaction skeleton (K2) with fused materialization (K3).
+// compact.cuh — ordered stream compaction skeleton (K2) + dense materialization (K3).
 //
-// One persistent pass: each CTA takes tiles of kBlock*ITEMS input positions
-// (virtual tile ids from an atomic counter => forward progress for the
-// look-back), evaluates a row functor for every position, ranks the survivors
-// with warp ballots + popc and a per-tile scan, obtains the tile's global
-// offset by decoupled look-back, and writes ascending row ids (+ an aux id and
-// gathered payload columns) at their final positions.  Inputs are read once;
-// outputs are written once.
+// Three barrier-light phases (a single-pass decoupled look-back serialised small tiles on the
+// look-back chain: ncu showed 60%+ of warp stalls at the tile barrier waiting for it):
+//   1. k_compact_local: every CTA takes tiles of kBlock*ITEMS input positions (grid-stride),
+//      evaluates the row functor for all of a thread's rows at once, ranks the survivors with
+//      warp ballots + popc and a per-tile scan of (item, warp) cells, and writes them compacted
+//      into a per-tile scratch region (row id, aux) plus the tile's count;
+//   2. scan of the tile counts (3 tiny kernels);
+//   3. k_compact_scatter: copies each tile's survivors to its final offset (coalesced), giving
+//      ascending row ids; payload columns are then gathered densely (k_gather_multi).
+// Inputs are read once; scratch traffic is 8 bytes per survivor each way.
 //
 // Functor interface:
 //   template <int ITEMS> __device__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS],
 //                                            bool (&alive)[ITEMS], int32_t (&aux)[ITEMS]) const;
-// The functor sees all of a thread's rows at once so it can issue their loads
-// back to back (memory-level parallelism), then evaluate.
 #pragma once
 #include "common.cuh"
 
 namespace sx {
 
 template <class F, bool HAS_SEL, int ITEMS>
-__global__ void __launch_bounds__(kBlock) k_compact(const __grid_constant__ F f, int64_t n, const int32_t* __restrict__ in_sel,
-                                                    int32_t* __restrict__ out_sel, int32_t* __restrict__ out_aux,
-                                                    const __grid_constant__ GatherSpec gs, unsigned long long* status,
-                                                    unsigned int* tile_ctr, int64_t ntiles) {
+__global__ void __launch_bounds__(kBlock) k_compact_local(const __grid_constant__ F f, int64_t n,
+                                                          const int32_t* __restrict__ in_sel,
+                                                          int32_t* __restrict__ s_row, int32_t* __restrict__ s_aux,
+                                                          int32_t* __restrict__ tile_cnt, int64_t ntiles) {
   constexpr int W = kBlock / 32;
   constexpr int NE = ITEMS * W;  // (item, warp) cells, scanned in that order
   static_assert(NE <= 64, "scan assumes <= 2 cells per lane");
-  __shared__ int64_t s_tile;
-  __shared__ int64_t s_excl;
   __shared__ int s_cnt[NE];
+  __shared__ int s_total;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  while (true) {
-    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(tile_ctr, 1u);
-    __syncthreads();
-    const int64_t tile = s_tile;
-    if (tile >= ntiles) break;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t base = tile * (int64_t)(kBlock * ITEMS);
     int32_t row[ITEMS];
     bool valid[ITEMS], alive[ITEMS];
@@ -69,25 +65,91 @@ __global__ void __launch_bounds__(kBlock) k_compact(const __grid_constant__ F f,
         if (lane >= o) { pa += ya; pb += yb; }
       }
       int half = __shfl_sync(kFull, pa, 31);
-      int total = half + __shfl_sync(kFull, pb, 31);
       if (lane < NE) s_cnt[lane] = pa - a;
       if (lane + 32 < NE) s_cnt[lane + 32] = half + pb - b;
-      int64_t excl = lookback_exclusive(status, tile, total);
-      if (lane == 0) s_excl = excl;
+      if (lane == 31) s_total = half + pb;
     }
     __syncthreads();
-    const int64_t excl = s_excl;
     const unsigned lt = lanemask_lt();
+    int32_t* tr = s_row + base;
+    int32_t* ta = s_aux ? s_aux + base : nullptr;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       if ((ball[i] >> lane) & 1u) {
-        int64_t pos = excl + s_cnt[i * W + w] + __popc(ball[i] & lt);
-        out_sel[pos] = (int32_t)row[i];
-        if (out_aux) out_aux[pos] = aux[i];
-        for (int g = 0; g < gs.n; ++g) gather_one(gs.g[g], pos, gs.g[g].by_aux ? (int64_t)aux[i] : row[i]);
+        int pos = s_cnt[i * W + w] + __popc(ball[i] & lt);
+        tr[pos] = row[i];
+        if (ta) ta[pos] = aux[i];
       }
     }
+    if (threadIdx.x == 0) tile_cnt[tile] = s_total;
     __syncthreads();
+  }
+}
+
+// exclusive scan of int32 tile counts into int64 offsets (offsets[ntiles] = total)
+static __global__ void __launch_bounds__(1024) k_scan_counts_local(const int32_t* __restrict__ cnt, int64_t n,
+                                                                   int64_t* __restrict__ off,
+                                                                   int64_t* __restrict__ block_sums) {
+  __shared__ int64_t wsum[32];
+  int64_t i = blockIdx.x * 1024ll + threadIdx.x;
+  int64_t v = i < n ? cnt[i] : 0;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t t = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(kFull, t, o);
+      if (lane >= o) t += y;
+    }
+    wsum[lane] = t;
+  }
+  __syncthreads();
+  int64_t incl = x + (w ? wsum[w - 1] : 0);
+  if (i < n) off[i] = incl - v;
+  if (threadIdx.x == 1023) block_sums[blockIdx.x] = incl;
+}
+
+static __global__ void k_scan_counts_sums(int64_t* __restrict__ sums, int64_t nb, int64_t* __restrict__ total) {
+  // one warp: sequential chunks of 32 (nb is ntiles / 1024, small)
+  const int lane = threadIdx.x;
+  int64_t run = 0;
+  for (int64_t b0 = 0; b0 < nb; b0 += 32) {
+    int64_t v = b0 + lane < nb ? sums[b0 + lane] : 0, x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (b0 + lane < nb) sums[b0 + lane] = run + x - v;
+    run += __shfl_sync(kFull, x, 31);
+  }
+  if (lane == 0) *total = run;
+}
+
+static __global__ void k_scan_counts_add(int64_t* __restrict__ off, int64_t n, const int64_t* __restrict__ sums) {
+  int64_t i = blockIdx.x * 1024ll + threadIdx.x;
+  if (i < n) off[i] += sums[blockIdx.x];
+}
+
+template <int TILE>
+__global__ void __launch_bounds__(kBlock) k_compact_scatter(const int32_t* __restrict__ s_row,
+                                                            const int32_t* __restrict__ s_aux,
+                                                            const int32_t* __restrict__ tile_cnt,
+                                                            const int64_t* __restrict__ tile_off, int64_t ntiles,
+                                                            int32_t* __restrict__ out_sel, int32_t* __restrict__ out_aux) {
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int c = tile_cnt[tile];
+    if (c == 0) continue;
+    const int64_t o = tile_off[tile], base = tile * (int64_t)TILE;
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+      out_sel[o + j] = __ldg(s_row + base + j);
+      if (out_aux) out_aux[o + j] = __ldg(s_aux + base + j);
+    }
   }
 }
 
@@ -108,27 +170,30 @@ sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel,
                       const GatherSpec& gs, int64_t* out_count) {
   *out_count = 0;
   if (n == 0) return SX_OK;
-  const int64_t tile_rows = (int64_t)kBlock * ITEMS;
-  const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
+  constexpr int TILE = kBlock * ITEMS;
+  const int64_t ntiles = (n + TILE - 1) / TILE;
   Scratch scr(ctx);
-  unsigned long long* status;
-  SX_TRY(scr.get(&status, (size_t)ntiles));
-  SX_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ntiles, ctx->stream));
-  unsigned int* ctr = ctx->d_counters;
-  SX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), ctx->stream));
+  int32_t *s_row, *s_aux = nullptr, *cnt;
+  int64_t *off, *bsum;
+  SX_TRY(scr.get(&s_row, (size_t)ntiles * TILE));
+  if (out_aux) SX_TRY(scr.get(&s_aux, (size_t)ntiles * TILE));
+  SX_TRY(scr.get(&cnt, (size_t)ntiles));
+  SX_TRY(scr.get(&off, (size_t)ntiles + 1));
+  const int64_t nb = (ntiles + 1023) / 1024;
+  SX_TRY(scr.get(&bsum, (size_t)nb + 1));
   unsigned grid = persistent_grid(ctx, 8, ntiles);
-  // Payload columns are gathered in a dense post-pass (one thread per output row) rather than
-  // inside the scan, where only the (few) surviving lanes of each warp would be active.
-  GatherSpec none;
-  none.n = 0;
   if (in_sel)
-    k_compact<F, true, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, out_sel, out_aux, none, status, ctr, ntiles);
+    k_compact_local<F, true, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, s_row, s_aux, cnt, ntiles);
   else
-    k_compact<F, false, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, out_sel, out_aux, none, status, ctr, ntiles);
+    k_compact_local<F, false, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, s_row, s_aux, cnt, ntiles);
   SX_CHECK_LAUNCH();
-  int64_t last;
-  SX_TRY(read_i64(ctx, status + (ntiles - 1), &last));
-  *out_count = (int64_t)((unsigned long long)last & ((1ull << 62) - 1));
+  k_scan_counts_local<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(cnt, ntiles, off, bsum);
+  k_scan_counts_sums<<<1, 32, 0, SX_STREAM(ctx)>>>(bsum, nb, off + ntiles);
+  k_scan_counts_add<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(off, ntiles, bsum);
+  k_compact_scatter<TILE><<<persistent_grid(ctx, 8, ntiles), kBlock, 0, SX_STREAM(ctx)>>>(s_row, s_aux, cnt, off, ntiles,
+                                                                                         out_sel, out_aux);
+  SX_CHECK_LAUNCH();
+  SX_TRY(read_i64(ctx, off + ntiles, out_count));
   if (gs.n > 0 && *out_count > 0) {
     k_gather_multi<<<persistent_grid(ctx, 8, (*out_count + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
         out_sel, out_aux, *out_count, gs);

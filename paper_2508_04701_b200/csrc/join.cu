@@ -30,14 +30,18 @@ struct BuildArgs {
   void* slots;
   uint64_t mask;
   unsigned long long* inserted;
+  long long* kmin;  // [0] min, [1] max of inserted single-column keys (bitmap filter range)
 };
 
 __global__ void __launch_bounds__(kBlock) k_build(const __grid_constant__ BuildArgs a) {
   int64_t cnt = 0;
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < a.n; idx += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = a.sel ? (int64_t)__ldg(a.sel + idx) : idx;
     if (!eval_conj(a.cols, a.preds, a.np, r)) continue;
     uint64_t key = key_of(a.cols, a.nkeys, a.kc0, a.kc1, r);
+    mn = min(mn, (long long)key);
+    mx = max(mx, (long long)key);
     uint64_t h = table_hash(key, a.key_bytes) & a.mask;
     if (a.key_bytes == 4) {
       unsigned long long* s = (unsigned long long*)a.slots;
@@ -50,9 +54,29 @@ __global__ void __launch_bounds__(kBlock) k_build(const __grid_constant__ BuildA
     }
     ++cnt;
   }
-  // warp-aggregated count of inserted rows
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
-  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(a.inserted, (unsigned long long)cnt);
+  // warp-aggregated count of inserted rows and key range
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(kFull, cnt, o);
+    mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+    mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd(a.inserted, (unsigned long long)cnt);
+    atomicMin(a.kmin, mn);
+    atomicMax(a.kmin + 1, mx);
+  }
+}
+
+// Exact key-range bitmap of the build keys (predicate transfer): bit (key - min).
+// Probes test it before touching the table, so misses cost one (L2-resident) word load.
+__global__ void __launch_bounds__(kBlock) k_bitmap_set(const __grid_constant__ BuildArgs a, uint32_t* bm,
+                                                       long long kmin) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < a.n; idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = a.sel ? (int64_t)__ldg(a.sel + idx) : idx;
+    if (!eval_conj(a.cols, a.preds, a.np, r)) continue;
+    uint64_t off = (uint64_t)((long long)key_of(a.cols, a.nkeys, a.kc0, a.kc1, r) - kmin);
+    atomicOr(bm + (off >> 5), 1u << (off & 31));
+  }
 }
 
 // Probe functor for the ordered compaction skeleton (semi / anti / inner on a unique build).
@@ -124,6 +148,9 @@ struct InnerArgs {
   int32_t* out_build;
   int64_t cap;
   unsigned long long* counter;
+  const uint32_t* bm;
+  long long bm_min;
+  unsigned long long bm_bits;
 };
 
 __global__ void __launch_bounds__(kBlock) k_probe_inner(const __grid_constant__ InnerArgs a,
@@ -143,6 +170,10 @@ __global__ void __launch_bounds__(kBlock) k_probe_inner(const __grid_constant__ 
     uint64_t key = alive ? key_of(a.cols, a.nkeys, a.kc0, a.kc1, r) : 0;
     uint64_t h = table_hash(key, a.key_bytes) & a.mask;
     bool pend = alive;
+    if (a.bm && pend) {
+      unsigned long long off = (unsigned long long)((long long)key - a.bm_min);
+      pend = off < a.bm_bits && ((__ldg(a.bm + (off >> 5)) >> (off & 31)) & 1u);
+    }
     while (__any_sync(kFull, pend)) {
       bool hit = false;
       int32_t brow = -1;
@@ -232,23 +263,52 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
     return s;
   }
   cudaMemsetAsync(ht->slots, 0xff, cap * slot_bytes, ctx->stream);
+  // counters: [0] inserted rows, [1] min key, [2] max key
   unsigned long long* ins = (unsigned long long*)ctx->d_counters;
-  cudaMemsetAsync(ins, 0, 8, ctx->stream);
+  int64_t* init = ctx->h_pinned + 8;
+  init[0] = 0;
+  init[1] = LLONG_MAX;
+  init[2] = LLONG_MIN;
+  cudaMemcpyAsync(ins, init, 3 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream);
   a.sel = in_sel ? in_sel->idx : nullptr;
   a.n = n;
   a.slots = ht->slots;
   a.mask = cap - 1;
   a.inserted = ins;
+  a.kmin = (long long*)(ins + 1);
   if (n > 0) k_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
   cudaError_t e = cudaGetLastError();
-  int64_t rows = 0;
-  if (e == cudaSuccess) s = read_i64(ctx, ins, &rows);
+  int64_t stats[3] = {0, 0, 0};
+  if (e == cudaSuccess) s = read_i64(ctx, ins, stats, 3);
   if (e != cudaSuccess || s != SX_OK) {
     dfree(ctx, ht->slots);
     delete ht;
     return e != cudaSuccess ? set_err(ctx, SX_ECUDA, "build: %s", cudaGetErrorString(e)) : s;
   }
-  ht->rows = rows;
+  ht->rows = stats[0];
+  // exact bitmap filter over the key range when it is small enough to stay cache-resident-ish
+  if (nkeys == 1 && stats[0] > 0) {
+    unsigned long long range = (unsigned long long)(stats[2] - stats[1]) + 1;
+    if (stats[2] >= stats[1] && range <= (1ull << 30)) {
+      size_t words = (size_t)((range + 31) / 32);
+      if (alloc(ctx, &ht->bm, words) == SX_OK) {
+        cudaMemsetAsync(ht->bm, 0, words * sizeof(uint32_t), ctx->stream);
+        ht->bm_min = stats[1];
+        ht->bm_bits = range;
+        k_bitmap_set<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a, ht->bm, stats[1]);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) {
+          dfree(ctx, ht->slots);
+          dfree(ctx, ht->bm);
+          delete ht;
+          return set_err(ctx, SX_ECUDA, "bitmap: %s", cudaGetErrorString(e));
+        }
+      } else {
+        ctx->err.clear();
+        ht->bm = nullptr;
+      }
+    }
+  }
   *out = ht;
   return SX_OK;
 }
@@ -257,7 +317,10 @@ SX_EXPORT int64_t sx_ht_rows(const sx_ht* ht) { return ht ? ht->rows : 0; }
 
 SX_EXPORT void sx_ht_destroy(sx_ctx* ctx, sx_ht* ht) {
   if (!ht) return;
-  if (ctx) dfree(ctx, ht->slots);
+  if (ctx) {
+    dfree(ctx, ht->slots);
+    dfree(ctx, ht->bm);
+  }
   delete ht;
 }
 
@@ -333,6 +396,10 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
       ft.slots = ht->slots;
       ft.mask = (uint32_t)(ht->cap - 1);
       ft.anti = join_type == SX_ANTI;
+      ft.member_only = join_type != SX_INNER;
+      ft.bm = ht->bm;
+      ft.bm_min = ht->bm_min;
+      ft.bm_bits = ht->bm_bits;
       return run_compact<decltype(ft), 4>(ctx, ft, n, isel, op, ob, gs, &count);
     };
     auto is32 = [&](int c) { int t = probe_cols[key_cols[c]].type; return t == SX_I32 || t == SX_DATE32; };
@@ -359,6 +426,9 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     a.slots = ht->slots;
     a.mask = ht->cap - 1;
     a.counter = (unsigned long long*)ctx->d_counters;
+    a.bm = ht->bm;
+    a.bm_min = ht->bm_min;
+    a.bm_bits = ht->bm_bits;
     int64_t cap = n > 1024 ? n : 1024;
     for (int attempt = 0; attempt < 2; ++attempt) {
       SX_TRY(scr.get(&op, (size_t)cap));

@@ -42,6 +42,10 @@ struct ProbeFnT {
   const void* slots;
   uint32_t mask;
   int anti;
+  int member_only;     // semi/anti: membership is the whole answer
+  const uint32_t* bm;  // optional exact key-range bitmap of the build side
+  long long bm_min;
+  unsigned long long bm_bits;
   template <int ITEMS>
   __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
                                        int32_t (&aux)[ITEMS]) const {
@@ -63,6 +67,23 @@ struct ProbeFnT {
       h[i] = (uint32_t)(KB == 4 ? hash32((uint32_t)key[i]) : hash64(key[i])) & mask;
       pend[i] = alive[i];
       found[i] = false;
+    }
+    if (bm) {  // exact pre-filter: keys absent from the build never touch the table
+      uint32_t w[ITEMS];
+      unsigned long long off[ITEMS];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        off[i] = (unsigned long long)((long long)key[i] - bm_min);
+        pend[i] = pend[i] && off[i] < bm_bits;
+        w[i] = pend[i] ? __ldg(bm + (off[i] >> 5)) : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) pend[i] = pend[i] && ((w[i] >> (off[i] & 31)) & 1u);
+      if (member_only) {  // semi / anti: the exact bitmap is the answer, the table is not needed
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) alive[i] = alive[i] && (anti ? !pend[i] : pend[i]);
+        return;
+      }
     }
     bool any = true;
     if (KB == 4) {
