@@ -82,8 +82,6 @@ SX_EXPORT sx_status sx_partition_by_rank(sx_ctx* ctx, const sx_col* cols, int nc
     if (!w) return set_err(ctx, SX_ETYPE, "column %d is not fixed-width", c);
     SX_TRY(scr.get((char**)&dst[c], (size_t)(n > 0 ? n : 1) * w));
   }
-  int32_t* sel;
-  SX_TRY(scr.get(&sel, (size_t)(n > 0 ? n : 1)));
   int64_t off = 0;
   for (int d = 0; d < nranks; ++d) {
     DestFn f{dc[key_cols[0]], dc[nkeys > 1 ? key_cols[1] : key_cols[0]], nkeys, nranks, d};
@@ -97,7 +95,9 @@ SX_EXPORT sx_status sx_partition_by_rank(sx_ctx* ctx, const sx_col* cols, int nc
       gs.g[c].width = w;
     }
     int64_t cnt = 0;
-    SX_TRY(run_compact(ctx, f, n, in_sel ? in_sel->idx : nullptr, sel + off, nullptr, gs, &cnt));
+    int32_t* sel = nullptr;  // destination d's row ids (temporary); payload lands at dst + off
+    SX_TRY(run_compact(ctx, f, n, in_sel ? in_sel->idx : nullptr, &sel, nullptr, gs, &cnt));
+    dfree(ctx, sel);
     counts[d] = cnt;
     off += cnt;
   }

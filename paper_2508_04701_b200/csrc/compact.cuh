@@ -164,12 +164,37 @@ static __global__ void __launch_bounds__(kBlock) k_gather_multi(const int32_t* _
 }
 
 // Host driver: runs the skeleton over n positions; returns the output count (one D2H read).
-// out_sel / out_aux / gather destinations must have capacity >= n.
+// Outputs are allocated here at the exact count (known after the scan): *out_sel always,
+// *out_aux when out_aux != nullptr, and every gs.g[g].dst that is nullptr (count * width bytes).
+// Ownership of all of them passes to the caller (also on error paths they are freed here).
 template <class F, int ITEMS = 8>
-sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel, int32_t* out_sel, int32_t* out_aux,
-                      const GatherSpec& gs, int64_t* out_count) {
+sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel, int32_t** out_sel,
+                      int32_t** out_aux, GatherSpec& gs, int64_t* out_count) {
   *out_count = 0;
-  if (n == 0) return SX_OK;
+  *out_sel = nullptr;
+  if (out_aux) *out_aux = nullptr;
+  bool owned[kMaxGather] = {};
+  for (int g = 0; g < gs.n; ++g) owned[g] = gs.g[g].dst == nullptr;
+  auto alloc_outputs = [&](int64_t cnt) -> sx_status {
+    size_t c = (size_t)(cnt > 0 ? cnt : 1);
+    SX_TRY(alloc(ctx, out_sel, c));
+    if (out_aux) {
+      sx_status s = alloc(ctx, out_aux, c);
+      if (s != SX_OK) { dfree(ctx, *out_sel); *out_sel = nullptr; return s; }
+    }
+    for (int g = 0; g < gs.n; ++g) {
+      if (!owned[g]) continue;
+      sx_status s = alloc(ctx, (char**)&gs.g[g].dst, c * gs.g[g].width);
+      if (s != SX_OK) {
+        for (int h = 0; h < g; ++h) if (owned[h]) { dfree(ctx, gs.g[h].dst); gs.g[h].dst = nullptr; }
+        dfree(ctx, *out_sel); *out_sel = nullptr;
+        if (out_aux) { dfree(ctx, *out_aux); *out_aux = nullptr; }
+        return s;
+      }
+    }
+    return SX_OK;
+  };
+  if (n == 0) return alloc_outputs(0);
   constexpr int TILE = kBlock * ITEMS;
   const int64_t ntiles = (n + TILE - 1) / TILE;
   Scratch scr(ctx);
@@ -190,14 +215,25 @@ sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel,
   k_scan_counts_local<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(cnt, ntiles, off, bsum);
   k_scan_counts_sums<<<1, 32, 0, SX_STREAM(ctx)>>>(bsum, nb, off + ntiles);
   k_scan_counts_add<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(off, ntiles, bsum);
-  k_compact_scatter<TILE><<<persistent_grid(ctx, 8, ntiles), kBlock, 0, SX_STREAM(ctx)>>>(s_row, s_aux, cnt, off, ntiles,
-                                                                                         out_sel, out_aux);
   SX_CHECK_LAUNCH();
-  SX_TRY(read_i64(ctx, off + ntiles, out_count));
-  if (gs.n > 0 && *out_count > 0) {
-    k_gather_multi<<<persistent_grid(ctx, 8, (*out_count + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
-        out_sel, out_aux, *out_count, gs);
-    SX_CHECK_LAUNCH();
+  int64_t count = 0;
+  SX_TRY(read_i64(ctx, off + ntiles, &count));
+  SX_TRY(alloc_outputs(count));
+  *out_count = count;
+  if (count > 0) {
+    k_compact_scatter<TILE><<<persistent_grid(ctx, 8, ntiles), kBlock, 0, SX_STREAM(ctx)>>>(
+        s_row, s_aux, cnt, off, ntiles, *out_sel, out_aux ? *out_aux : nullptr);
+    if (gs.n > 0)
+      k_gather_multi<<<persistent_grid(ctx, 8, (count + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+          *out_sel, out_aux ? *out_aux : nullptr, count, gs);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      dfree(ctx, *out_sel);
+      *out_sel = nullptr;
+      if (out_aux) { dfree(ctx, *out_aux); *out_aux = nullptr; }
+      for (int g = 0; g < gs.n; ++g) if (owned[g]) { dfree(ctx, gs.g[g].dst); gs.g[g].dst = nullptr; }
+      return set_err(ctx, SX_ECUDA, "compaction scatter: %s", cudaGetErrorString(e));
+    }
   }
   return SX_OK;
 }

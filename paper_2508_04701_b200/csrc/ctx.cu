@@ -1,4 +1,6 @@
 // ctx.cu — context lifecycle, stream-ordered pool, errors, profiling, sx_gather.
+#include <cstdlib>
+
 #include "common.cuh"
 
 using namespace sx;
@@ -26,6 +28,24 @@ SX_EXPORT sx_status sx_ctx_create(int device, void* stream, sx_ctx** out) {
   SX_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t thresh = UINT64_MAX;
   SX_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+  // Reserve the processing region up front ("pre-allocated in advance"): growing the pool
+  // later maps physical memory on the host timeline, inside whatever query first needs it.
+  {
+    const char* env = getenv("SX_POOL_RESERVE_GB");
+    double gb = env ? atof(env) : 48.0;
+    size_t freeb = 0, totalb = 0;
+    cudaMemGetInfo(&freeb, &totalb);
+    size_t want = (size_t)(gb * (1ull << 30));
+    if (want > freeb / 2) want = freeb / 2;
+    uint64_t reserved = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    if (want > reserved) {
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, want - reserved, ctx->stream) == cudaSuccess) cudaFreeAsync(p, ctx->stream);
+      cudaGetLastError();
+      cudaStreamSynchronize(ctx->stream);
+    }
+  }
   SX_CUDA(cudaMalloc((void**)&ctx->d_flags, 64 * sizeof(int)));
   SX_CUDA(cudaMemset(ctx->d_flags, 0, 64 * sizeof(int)));
   SX_CUDA(cudaMalloc((void**)&ctx->d_counters, 64 * sizeof(unsigned int)));

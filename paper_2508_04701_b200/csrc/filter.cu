@@ -46,10 +46,9 @@ sx_status filter_internal(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_p
     gs.g[g].src = dc[c];
     gs.g[g].by_aux = 0;
     gs.g[g].width = w;
-    SX_TRY(scr.get((char**)&gs.g[g].dst, (size_t)n * w));
+    gs.g[g].dst = nullptr;  // allocated by run_compact at the exact output count
   }
-  int32_t* sel;
-  SX_TRY(scr.get(&sel, (size_t)n));
+  int32_t* sel = nullptr;
   int64_t count = 0;
   const int32_t* isel = in_sel ? in_sel->idx : nullptr;
   if (ncontains) {
@@ -63,23 +62,21 @@ sx_status filter_internal(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_p
     f.chars = (const uint8_t*)c.data;
     f.plen = p.pattern_len;
     for (int i = 0; i < p.pattern_len; ++i) f.pat[i] = (uint8_t)p.pattern[i];
-    SX_TRY(run_compact(ctx, f, n, isel, sel, nullptr, gs, &count));
+    SX_TRY(run_compact(ctx, f, n, isel, &sel, nullptr, gs, &count));
   } else {
     ConjFn f;
     SX_TRY(check_preds(ctx, cols, ncols, conj, npred, f.preds));
     for (int i = 0; i < ncols; ++i) f.cols[i] = dc[i];
     f.np = npred;
-    SX_TRY(run_compact(ctx, f, n, isel, sel, nullptr, gs, &count));
+    SX_TRY(run_compact(ctx, f, n, isel, &sel, nullptr, gs, &count));
   }
   out_sel->len = count;
   out_sel->idx = sel;
-  scr.release(sel);
   for (int g = 0; g < ngather; ++g) {
     out_cols[g] = cols[gather_cols[g]];
     out_cols[g].len = count;
     out_cols[g].data = gs.g[g].dst;
     out_cols[g].offsets = nullptr;
-    scr.release(gs.g[g].dst);
   }
   return SX_OK;
 }

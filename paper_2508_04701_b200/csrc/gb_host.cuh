@@ -404,10 +404,10 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       sf.hv_lo = P.hv.lo;
       sf.hv_hi = P.hv.hi;
     }
-    SX_TRY(scr.get(&ids, nslots));
     GatherSpec none;
     none.n = 0;
-    SX_TRY(run_compact(ctx, sf, (int64_t)nslots, nullptr, ids, nullptr, none, &ng));
+    SX_TRY(run_compact(ctx, sf, (int64_t)nslots, nullptr, &ids, nullptr, none, &ng));
+    scr.ptrs.push_back(ids);
     SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
     if (flags[0]) return set_err(ctx, SX_EOVERFLOW, "a value expression left int64");
     if (!flags[1]) break;

@@ -8,6 +8,8 @@
 //   key_bytes 8: slot {u64 key; u32 row; u32 pad}, claimed by a 32-bit CAS on
 //                row, key stored after (probes run in a later kernel).
 // EMPTY: row word 0xFFFFFFFF (never a valid int32 row id).
+#include <algorithm>
+
 #include "compact.cuh"
 #include "filter.cuh"
 #include "join.cuh"
@@ -384,9 +386,8 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     f.anti = join_type == SX_ANTI;
     f.slots = ht->slots;
     f.mask = ht->cap - 1;
-    SX_TRY(scr.get(&op, (size_t)n));
-    if (join_type == SX_INNER) SX_TRY(scr.get(&ob, (size_t)n));
-    for (int g = 0; g < gs.n; ++g) SX_TRY(scr.get((char**)&gs.g[g].dst, (size_t)n * gs.g[g].width));
+    for (int g = 0; g < gs.n; ++g) gs.g[g].dst = nullptr;  // allocated at the exact output count
+    int32_t** pob = join_type == SX_INNER ? &ob : nullptr;
     auto run_t = [&](auto ft) -> sx_status {
       for (int i = 0; i < nprobe_cols; ++i) ft.cols[i] = pcols[i];
       for (int i = 0; i < nwhere; ++i) ft.preds[i] = preds[i];
@@ -400,7 +401,7 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
       ft.bm = ht->bm;
       ft.bm_min = ht->bm_min;
       ft.bm_bits = ht->bm_bits;
-      return run_compact<decltype(ft), 4>(ctx, ft, n, isel, op, ob, gs, &count);
+      return run_compact<decltype(ft), 4>(ctx, ft, n, isel, &op, pob, gs, &count);
     };
     auto is32 = [&](int c) { int t = probe_cols[key_cols[c]].type; return t == SX_I32 || t == SX_DATE32; };
     if (ht->cap <= (1ull << 32) && nkeys == 1 && kb == 4 && is32(0)) {
@@ -410,7 +411,7 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     } else if (ht->cap <= (1ull << 32) && nkeys == 2 && is32(0) && is32(1)) {
       SX_TRY(run_t(ProbeFnT<int32_t, 2, 8>{}));
     } else {
-      SX_TRY(run_compact(ctx, f, n, isel, op, ob, gs, &count));
+      SX_TRY(run_compact(ctx, f, n, isel, &op, pob, gs, &count));
     }
   } else {
     InnerArgs a{};
@@ -429,7 +430,8 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     a.bm = ht->bm;
     a.bm_min = ht->bm_min;
     a.bm_bits = ht->bm_bits;
-    int64_t cap = n > 1024 ? n : 1024;
+    // first guess: one output per build row (FK side built, PK side probed); exact retry if more
+    int64_t cap = std::max<int64_t>(std::min<int64_t>(n, std::max<int64_t>(ht->rows, n / 16)), 1024);
     for (int attempt = 0; attempt < 2; ++attempt) {
       SX_TRY(scr.get(&op, (size_t)cap));
       SX_TRY(scr.get(&ob, (size_t)cap));

@@ -144,11 +144,11 @@ SX_EXPORT sx_status sx_groupby_merge(sx_ctx* ctx, const sx_col* keys, int nkeys,
     sf.hv_hi = P.hv.hi;
   }
   int32_t* ids;
-  SX_TRY(scr.get(&ids, cap + 1));
   int64_t ng = 0;
   GatherSpec none;
   none.n = 0;
-  SX_TRY(run_compact(ctx, sf, (int64_t)(cap + 1), nullptr, ids, nullptr, none, &ng));
+  SX_TRY(run_compact(ctx, sf, (int64_t)(cap + 1), nullptr, &ids, nullptr, none, &ng));
+  scr.ptrs.push_back(ids);
   int flags[4];
   SX_CUDA(cudaMemcpy(flags, ctx->d_flags, sizeof flags, cudaMemcpyDeviceToHost));
   if (flags[1]) return set_err(ctx, SX_ENOMEM, "merge table full (groups_hint too small)");

@@ -366,13 +366,13 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
       psh = csh;
     }
     // all digits decided: the remaining active rows equal the k-th key exactly (unique keys) -> accepted
-    int32_t* winners;
-    SX_TRY(scr.get(&winners, (size_t)n));
+    int32_t* winners = nullptr;
     AcceptedFn af{flags};
     GatherSpec none;
     none.n = 0;
     int64_t m = 0;
-    SX_TRY(run_compact(ctx, af, n, nullptr, winners, nullptr, none, &m));
+    SX_TRY(run_compact(ctx, af, n, nullptr, &winners, nullptr, none, &m));
+    scr.ptrs.push_back(winners);
     if (m != outn) return set_err(ctx, SX_ECUDA, "radix select produced %lld of %lld rows", (long long)m, (long long)outn);
     size_t smem = (size_t)kBitonicMax * nwords * sizeof(uint32_t);
     SX_CUDA(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
