@@ -288,7 +288,66 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
   uint64_t cap_p = cap;  // slots per sub-table
   bool no_part = false;
   int nsub = 1;
-  for (int attempt = 0;; ++attempt) {
+  bool sorted_done = false;
+  // Sorted-input strategy (see k_runs_count): worth trying when the hash table would not be
+  // L2-resident; falls back to hashing if the key column turns out not to be non-decreasing.
+  if constexpr (Prog::kSortedOK) {
+    static const bool sorted_enabled = !(getenv("SX_GB_SORTED") && getenv("SX_GB_SORTED")[0] == '0');
+    if (sorted_enabled && !small && !keyless && P.nkeys == 1 && !sel && n > 0 && prog.no_filter() &&
+        cap * (uint64_t)L.slot_bytes > ctx->l2_bytes / 2) {
+      constexpr int RI = 4;
+      const int64_t ntiles = (n + (int64_t)kBlock * RI - 1) / ((int64_t)kBlock * RI);
+      int32_t* heads;
+      int64_t *first, *bsum;
+      SX_TRY(scr.get(&heads, (size_t)ntiles));
+      SX_TRY(scr.get(&first, (size_t)ntiles + 1));
+      const int64_t nb = (ntiles + 1023) / 1024;
+      SX_TRY(scr.get(&bsum, (size_t)nb + 1));
+      SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
+      unsigned grid = persistent_grid(ctx, 8, ntiles);
+      k_runs_count<Prog, RI><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(prog, n, heads, ntiles, ctx->d_flags + 3);
+      k_scan_counts_local<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(heads, ntiles, first, bsum);
+      k_scan_counts_sums<<<1, 32, 0, SX_STREAM(ctx)>>>(bsum, nb, first + ntiles);
+      k_scan_counts_add<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(first, ntiles, bsum);
+      SX_CHECK_LAUNCH();
+      int64_t G = 0;
+      SX_TRY(read_i64(ctx, first + ntiles, &G));
+      SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
+      if (!flags[3]) {
+        SX_TRY(scr.get(&table, (size_t)G * L.slot_bytes));
+        SX_CUDA(cudaMemsetAsync(table, 0, (size_t)G * L.slot_bytes, ctx->stream));
+        k_runs_agg<Prog, RI><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(prog, n, first, L, table, ntiles);
+        SX_CHECK_LAUNCH();
+        SlotFn sf;
+        std::memset(&sf, 0, sizeof sf);
+        sf.slots = table;
+        sf.cap = (uint64_t)G;
+        sf.slot_bytes = L.slot_bytes;
+        sf.key_bytes = 0;  // dense: every slot < G is a group
+        sf.nsub = 1;
+        sf.side_used = ctx->d_flags + 2;
+        sf.has_having = P.has_having;
+        if (P.has_having) {
+          int s = P.agg_state[P.hv.agg];
+          sf.hv_kind = L.kind[s];
+          sf.hv_off8 = L.off8[s];
+          sf.hv_off4 = L.off4[s];
+          sf.hv_op = P.hv.op;
+          sf.hv_lo = P.hv.lo;
+          sf.hv_hi = P.hv.hi;
+        }
+        GatherSpec none;
+        none.n = 0;
+        SX_TRY(run_compact(ctx, sf, G, nullptr, &ids, nullptr, none, &ng));
+        scr.ptrs.push_back(ids);
+        SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
+        if (flags[0]) return set_err(ctx, SX_EOVERFLOW, "a value expression left int64");
+        cap_p = (uint64_t)G;  // emit: no slot index equals G, so no side-slot key rewrite
+        sorted_done = true;
+      }
+    }
+  }
+  for (int attempt = 0; !sorted_done; ++attempt) {
     // partition when the table would not stay L2-resident
     int pbits = 0;
     // (opt-in until phase A beats the single HBM table: SX_GB_PARTITION=1)

@@ -170,9 +170,19 @@ struct InterpProg {
   GbArgs A;
   int* ovf_flag;
   static constexpr int kMaxNst = kMaxStates;
+  static constexpr bool kSortedOK = true;
   template <int ITEMS>
   struct Cache {};
+  bool no_filter() const { return A.np == 0; }
   __device__ __forceinline__ int kind(int a, const Layout& L) const { return L.kind[a]; }
+  template <int ITEMS>
+  __device__ __forceinline__ void keys_only(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS],
+                                            uint64_t (&key)[ITEMS]) const {
+    int64_t k0[ITEMS];
+    load_col<ITEMS>(A.cols[A.kc[0]], row, valid, k0);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = (uint64_t)(A.kfn[0] == SX_KEY_YEAR ? civil_year((int32_t)k0[i]) : k0[i]);
+  }
   template <int ITEMS>
   __device__ __forceinline__ void where_keys(const int32_t (&row)[ITEMS], bool (&alive)[ITEMS],
                                              uint64_t (&key)[ITEMS], Cache<ITEMS>&) const {
@@ -510,6 +520,170 @@ static __global__ void __launch_bounds__(kBlock) k_gb_merge_records(const __grid
       }
     }
   }
+}
+
+// ------------------------------------------------------------------------------ sorted-input K11
+// When the (single) group key column is non-decreasing in row order — e.g. lineitem clustered by
+// orderkey, as TPC-H data is generated — each group is one contiguous run, so a row's group id is
+// (number of key changes before it) and the aggregation state lives in a dense array indexed by it:
+// no hashing, no random table traffic.  Pass 1 counts key changes per tile and verifies the order
+// (any decrease raises *unsorted and the host falls back to hashing); a scan gives each tile its
+// first group id; pass 2 recomputes run boundaries, group ids by a tile-level scan, pre-reduces runs
+// across lanes and adds each run's partial state into its dense slot.  Programs opt in with
+// kSortedOK and provide keys_only<I>(row, valid, key) (no filter: runs are over all rows).
+template <class P, int ITEMS>
+__global__ void __launch_bounds__(kBlock) k_runs_count(const __grid_constant__ P prog, int64_t n, int32_t* tile_heads,
+                                                       int64_t ntiles, int* unsorted) {
+  __shared__ int s_heads[kBlock / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (*(volatile int*)unsorted) return;  // early exit: the hash path will run instead
+    const int64_t base = tile * (int64_t)(kBlock * ITEMS);
+    int32_t row[ITEMS], prow[ITEMS];
+    bool valid[ITEMS], pvalid[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
+      valid[i] = idx < n;
+      pvalid[i] = valid[i] && idx > 0;
+      row[i] = valid[i] ? (int32_t)idx : 0;
+      prow[i] = pvalid[i] ? (int32_t)(idx - 1) : 0;
+    }
+    uint64_t key[ITEMS], pkey[ITEMS];
+    prog.template keys_only<ITEMS>(row, valid, key);
+    prog.template keys_only<ITEMS>(prow, pvalid, pkey);
+    int h = 0;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      h += valid[i] && (!pvalid[i] || key[i] != pkey[i]);
+      bad |= pvalid[i] && (int64_t)key[i] < (int64_t)pkey[i];
+    }
+    if (bad) atomicExch(unsorted, 1);
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(kFull, h, o);
+    if (lane == 0) s_heads[w] = h;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int q = 0; q < kBlock / 32; ++q) t += s_heads[q];
+      tile_heads[tile] = t;
+    }
+    __syncthreads();
+  }
+}
+
+template <class P, int ITEMS>
+__global__ void __launch_bounds__(kBlock) k_runs_agg(const __grid_constant__ P prog, int64_t n,
+                                                     const int64_t* __restrict__ tile_first,
+                                                     const __grid_constant__ Layout L, uint8_t* __restrict__ dense,
+                                                     int64_t ntiles) {
+  constexpr int W = kBlock / 32;
+  constexpr int NE = ITEMS * W;
+  static_assert(NE <= 64, "scan assumes <= 2 cells per lane");
+  __shared__ int s_cnt[NE];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+  bool ovf = false;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * (int64_t)(kBlock * ITEMS);
+    int32_t row[ITEMS], prow[ITEMS];
+    bool valid[ITEMS], pvalid[ITEMS], alive[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
+      valid[i] = idx < n;
+      alive[i] = valid[i];
+      pvalid[i] = valid[i] && idx > 0;
+      row[i] = valid[i] ? (int32_t)idx : 0;
+      prow[i] = pvalid[i] ? (int32_t)(idx - 1) : 0;
+    }
+    uint64_t key[ITEMS], pkey[ITEMS];
+    typename P::template Cache<ITEMS> cache;
+    prog.template where_keys<ITEMS>(row, alive, key, cache);
+    prog.template keys_only<ITEMS>(prow, pvalid, pkey);
+    unsigned ball[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      ball[i] = __ballot_sync(kFull, valid[i] && (!pvalid[i] || key[i] != pkey[i]));
+      if (lane == 0) s_cnt[i * W + w] = __popc(ball[i]);
+    }
+    __syncthreads();
+    if (w == 0) {
+      int a = lane < NE ? s_cnt[lane] : 0;
+      int b = lane + 32 < NE ? s_cnt[lane + 32] : 0;
+      int pa = a, pb = b;
+      for (int o = 1; o < 32; o <<= 1) {
+        int ya = __shfl_up_sync(kFull, pa, o);
+        int yb = __shfl_up_sync(kFull, pb, o);
+        if (lane >= o) { pa += ya; pb += yb; }
+      }
+      int half = __shfl_sync(kFull, pa, 31);
+      if (lane < NE) s_cnt[lane] = pa - a;
+      if (lane + 32 < NE) s_cnt[lane + 32] = half + pb - b;
+    }
+    __syncthreads();
+    const int64_t first = tile_first[tile];
+    int64_t g[ITEMS];
+    unsigned seg_start[ITEMS];
+    bool tail[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      // group id = first id of the tile + heads up to and including this row - 1
+      g[i] = first + s_cnt[i * W + w] + __popc(ball[i] & (lt | (1u << lane))) - 1;
+      int64_t pg = __shfl_up_sync(kFull, g[i], 1);
+      bool pv = __shfl_up_sync(kFull, valid[i], 1);
+      bool head = !valid[i] || lane == 0 || !pv || pg != g[i];
+      unsigned heads = __ballot_sync(kFull, head);
+      int64_t ng = __shfl_down_sync(kFull, g[i], 1);
+      bool nv = __shfl_down_sync(kFull, valid[i], 1);
+      tail[i] = valid[i] && (lane == 31 || !nv || ng != g[i]);
+      seg_start[i] = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+      if (tail[i]) {
+        uint8_t* s = dense + g[i] * (int64_t)L.slot_bytes;
+        if (L.key_bytes == 4) *(unsigned*)s = (unsigned)key[i];
+        else *(unsigned long long*)s = key[i];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < P::kMaxNst; ++a) {
+      if (a >= L.nst) break;
+      const int kd = prog.kind(a, L);
+      int64_t v[ITEMS];
+      if (kd == ST_COUNT) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) v[i] = valid[i] ? 1 : 0;
+      } else {
+        prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
+      }
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        uint8_t* s = dense + g[i] * (int64_t)L.slot_bytes;
+        if (kd == ST_SUM || kd == ST_COUNT) {
+          unsigned long long l = valid[i] ? (unsigned long long)v[i] : 0;
+          int32_t h = (valid[i] && v[i] < 0) ? -1 : 0;
+          for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long l2 = __shfl_up_sync(kFull, l, o);
+            int32_t h2 = __shfl_up_sync(kFull, h, o);
+            if (lane - o >= (int)seg_start[i]) {
+              unsigned long long s2 = l + l2;
+              h += h2 + (s2 < l ? 1 : 0);
+              l = s2;
+            }
+          }
+          if (tail[i]) apply_state(s, L, a, l, h);
+        } else {
+          int64_t m = valid[i] ? v[i] : (kd == ST_MIN ? INT64_MAX : INT64_MIN);
+          for (int o = 1; o < 32; o <<= 1) {
+            int64_t m2 = __shfl_up_sync(kFull, m, o);
+            if (lane - o >= (int)seg_start[i]) m = (kd == ST_MIN) ? (m2 < m ? m2 : m) : (m2 > m ? m2 : m);
+          }
+          if (tail[i]) apply_state(s, L, a, (unsigned long long)m, 0);
+        }
+      }
+    }
+  }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
 }
 
 // ------------------------------------------------------------------------------ K9: small G

@@ -35,6 +35,10 @@ struct Q1Prog {
   int32_t ship_max;
   int* ovf_flag;
   static constexpr int kMaxNst = 6;
+  static constexpr bool kSortedOK = false;
+  bool no_filter() const { return false; }
+  template <int I>
+  __device__ __forceinline__ void keys_only(const int32_t (&)[I], const bool (&)[I], uint64_t (&)[I]) const {}
   template <int I>
   struct Cache { int64_t qty[I], ext[I], disc[I], tax[I]; };
   __device__ __forceinline__ int kind(int a, const Layout&) const { return a == 4 ? ST_COUNT : ST_SUM; }
@@ -82,6 +86,10 @@ struct Q6Prog {
   int64_t disc_lo, disc_hi, qty_lt;
   int* ovf_flag;
   static constexpr int kMaxNst = 2;
+  static constexpr bool kSortedOK = false;
+  bool no_filter() const { return false; }
+  template <int I>
+  __device__ __forceinline__ void keys_only(const int32_t (&)[I], const bool (&)[I], uint64_t (&)[I]) const {}
   template <int I>
   struct Cache { int64_t ext[I], disc[I]; };
   __device__ __forceinline__ int kind(int a, const Layout&) const { return a == 1 ? ST_COUNT : ST_SUM; }
@@ -122,6 +130,13 @@ struct Q18Prog {
   const long long* qty;
   int* ovf_flag;
   static constexpr int kMaxNst = 1;
+  static constexpr bool kSortedOK = true;
+  bool no_filter() const { return true; }
+  template <int I>
+  __device__ __forceinline__ void keys_only(const int32_t (&row)[I], const bool (&valid)[I], uint64_t (&key)[I]) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) key[i] = valid[i] ? (uint64_t)(int64_t)__ldg(okey + row[i]) : 0;
+  }
   template <int I>
   struct Cache { int64_t q[I]; };
   __device__ __forceinline__ int kind(int, const Layout&) const { return ST_SUM; }
