@@ -163,6 +163,24 @@ static __global__ void __launch_bounds__(kBlock) k_gather_multi(const int32_t* _
   }
 }
 
+// Exclusive scan of n int32 counts into off[0..n] (off[n] = total, read back into *total).
+inline sx_status scan_counts(sx_ctx* ctx, const int32_t* cnt, int64_t n, int64_t* off, int64_t* total) {
+  Scratch scr(ctx);
+  const int64_t nb = (n + 1023) / 1024;
+  int64_t* bsum;
+  SX_TRY(scr.get(&bsum, (size_t)nb + 1));
+  if (n > 0) {
+    k_scan_counts_local<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(cnt, n, off, bsum);
+    k_scan_counts_sums<<<1, 32, 0, SX_STREAM(ctx)>>>(bsum, nb, off + n);
+    k_scan_counts_add<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(off, n, bsum);
+    SX_CHECK_LAUNCH();
+    SX_TRY(read_i64(ctx, off + n, total));
+  } else {
+    *total = 0;
+  }
+  return SX_OK;
+}
+
 // Host driver: runs the skeleton over n positions; returns the output count (one D2H read).
 // Outputs are allocated here at the exact count (known after the scan): *out_sel always,
 // *out_aux when out_aux != nullptr, and every gs.g[g].dst that is nullptr (count * width bytes).

@@ -258,6 +258,9 @@ inline int agg_out_type(int op) {
   }
 }
 
+constexpr int64_t kSharedMaxGroups = 4096;      // K10 eligibility (hinted groups)
+constexpr uint64_t kSharedMaxBytes = 96u << 10;  // K10 per-CTA table bytes
+
 inline uint64_t pow2_at_least(uint64_t x) {
   uint64_t c = 16;
   while (c < x) c <<= 1;
@@ -292,20 +295,22 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
   // Sorted-input strategy (see k_runs_count): worth trying when the hash table would not be
   // L2-resident; falls back to hashing if the key column turns out not to be non-decreasing.
   if constexpr (Prog::kSortedOK) {
-    static const bool sorted_enabled = !(getenv("SX_GB_SORTED") && getenv("SX_GB_SORTED")[0] == '0');
-    if (sorted_enabled && !small && !keyless && P.nkeys == 1 && !sel && n > 0 && prog.no_filter() &&
-        cap * (uint64_t)L.slot_bytes > ctx->l2_bytes / 2) {
-      constexpr int RI = 4;
-      const int64_t ntiles = (n + (int64_t)kBlock * RI - 1) / ((int64_t)kBlock * RI);
+    // SX_GB_SORTED: 0 = never, 2 = whenever eligible regardless of table size (tests)
+    const char* env = getenv("SX_GB_SORTED");
+    const int mode = env ? atoi(env) : 1;
+    if (mode != 0 && !small && !keyless && P.nkeys == 1 && !sel && n > 0 && prog.no_filter() &&
+        (mode == 2 || cap * (uint64_t)L.slot_bytes > ctx->l2_bytes / 2)) {
+      const int64_t ntiles = (n + kRunTile - 1) / kRunTile;
       int32_t* heads;
-      int64_t *first, *bsum;
+      int64_t *first, *bsum, *carry_gid;
+      uint8_t* carry;
       SX_TRY(scr.get(&heads, (size_t)ntiles));
       SX_TRY(scr.get(&first, (size_t)ntiles + 1));
       const int64_t nb = (ntiles + 1023) / 1024;
       SX_TRY(scr.get(&bsum, (size_t)nb + 1));
       SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
-      unsigned grid = persistent_grid(ctx, 8, ntiles);
-      k_runs_count<Prog, RI><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(prog, n, heads, ntiles, ctx->d_flags + 3);
+      k_runs_count<Prog><<<persistent_grid(ctx, 8, ntiles), kBlock, 0, SX_STREAM(ctx)>>>(prog, n, heads, ntiles,
+                                                                                      ctx->d_flags + 3);
       k_scan_counts_local<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(heads, ntiles, first, bsum);
       k_scan_counts_sums<<<1, 32, 0, SX_STREAM(ctx)>>>(bsum, nb, first + ntiles);
       k_scan_counts_add<<<(unsigned)nb, 1024, 0, SX_STREAM(ctx)>>>(first, ntiles, bsum);
@@ -314,9 +319,18 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       SX_TRY(read_i64(ctx, first + ntiles, &G));
       SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
       if (!flags[3]) {
-        SX_TRY(scr.get(&table, (size_t)G * L.slot_bytes));
-        SX_CUDA(cudaMemsetAsync(table, 0, (size_t)G * L.slot_bytes, ctx->stream));
-        k_runs_agg<Prog, RI><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(prog, n, first, L, table, ntiles);
+        SX_TRY(scr.get(&table, (size_t)G * L.slot_bytes));  // every slot is written (no zero-fill)
+        SX_TRY(scr.get(&carry, (size_t)ntiles * L.slot_bytes));
+        SX_TRY(scr.get(&carry_gid, (size_t)ntiles));
+        const size_t smem = runs_smem_bytes(L.nst);
+        SX_CUDA(cudaFuncSetAttribute(k_runs_agg<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_runs_agg<Prog>, kBlock, smem));
+        if (per_sm < 1) return set_err(ctx, SX_ENOMEM, "sorted aggregation: %zu B shared memory per CTA", smem);
+        unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, ntiles);
+        k_runs_agg<Prog><<<grid, kBlock, smem, SX_STREAM(ctx)>>>(prog, n, first, L, table, carry, carry_gid, ntiles);
+        k_runs_fix<<<persistent_grid(ctx, 8, (ntiles + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+            L, table, carry, carry_gid, ntiles);
         SX_CHECK_LAUNCH();
         SlotFn sf;
         std::memset(&sf, 0, sizeof sf);
@@ -357,6 +371,12 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
     }
     nsub = 1 << pbits;
     cap_p = keyless ? 1 : cap >> pbits;
+    // K10 when a hinted group count fits a per-CTA shared-memory table at load <= 0.5
+    uint32_t shared_cap = 0;
+    if (!small && !keyless && attempt == 0 && groups_hint > 0 && groups_hint <= kSharedMaxGroups) {
+      uint64_t sc = pow2_at_least(2 * (uint64_t)groups_hint);
+      if ((sc + 1) * (uint64_t)L.slot_bytes <= kSharedMaxBytes) shared_cap = (uint32_t)sc;
+    }
     uint64_t nslots = keyless ? 1 : (uint64_t)nsub * (cap_p + 1);
     SX_TRY(scr.get(&table, nslots * L.slot_bytes));
     SX_CUDA(cudaMemsetAsync(table, 0, nslots * L.slot_bytes, ctx->stream));
@@ -374,6 +394,16 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       int64_t tiles = (n + (int64_t)kSmallThreads * 4 - 1) / ((int64_t)kSmallThreads * 4);
       unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, tiles);
       k_gb_small<Prog, 4><<<grid, kSmallThreads, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, t);
+      SX_CHECK_LAUNCH();
+    } else if (n > 0 && nsub == 1 && shared_cap) {
+      size_t smem = (size_t)(shared_cap + 1) * L.slot_bytes;
+      SX_CUDA(cudaFuncSetAttribute(k_gb_shared<Prog, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_shared<Prog, 4>, kBlock, smem));
+      if (per_sm < 1) per_sm = 1;
+      int64_t tiles = (n + (int64_t)kBlock * 4 - 1) / ((int64_t)kBlock * 4);
+      unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, tiles);
+      k_gb_shared<Prog, 4><<<grid, kBlock, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, t, shared_cap);
       SX_CHECK_LAUNCH();
     } else if (n > 0 && nsub == 1) {
       int64_t tiles = (n + 32 * 4 - 1) / (32 * 4) / (kBlock / 32) + 1;

@@ -170,6 +170,7 @@ struct InterpProg {
   GbArgs A;
   int* ovf_flag;
   static constexpr int kMaxNst = kMaxStates;
+  static constexpr int kUnrollStates = 1;  // runtime state list: keep the loop rolled (code size)
   static constexpr bool kSortedOK = true;
   template <int ITEMS>
   struct Cache {};
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_gb_global(const __grid_constant__
       seg_start[i] = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
       slot[i] = tail[i] ? find_or_insert(t, L, key[i]) : nullptr;
     }
-#pragma unroll
+#pragma unroll(P::kUnrollStates)
     for (int a = 0; a < P::kMaxNst; ++a) {
       if (a >= L.nst) break;
       const int kd = prog.kind(a, L);
@@ -323,6 +324,168 @@ __global__ void __launch_bounds__(kBlock, 3) k_gb_global(const __grid_constant__
     }
   }
   if (ovf) atomicExch(prog.ovf_flag, 1);
+}
+
+// Add one slot's encoded states (as stored: SUM {lo, hi}, COUNT, MIN ~u / MAX u) into another.
+__device__ __forceinline__ void merge_slot(uint8_t* dst, const uint8_t* src, const Layout& L) {
+  for (int a = 0; a < L.nst; ++a) {
+    unsigned long long u = *(const unsigned long long*)(src + L.off8[a]);
+    switch (L.kind[a]) {
+      case ST_SUM:
+        atomic_add_sum96((unsigned long long*)(dst + L.off8[a]), (int*)(dst + L.off4[a]), (int64_t)u,
+                         *(const int*)(src + L.off4[a]));
+        break;
+      case ST_COUNT: atomicAdd((unsigned long long*)(dst + L.off8[a]), u); break;
+      default: atomicMax((unsigned long long*)(dst + L.off8[a]), u); break;
+    }
+  }
+}
+
+// apply_state for a slot in shared memory, with native 32-bit shared atomics only (64-bit shared
+// add/max would compile to CAS spin loops): the 96-bit SUM {lo, hi} is updated word by word,
+// each word's carry-out (known from the returned old value) added into the next word; COUNT the
+// same without the top word; MIN/MAX by a compare-first CAS loop (most updates do not improve).
+__device__ __forceinline__ void apply_state_smem(uint8_t* s, const Layout& L, int a, unsigned long long lo, int32_t hi) {
+  const int kd = L.kind[a];
+  if (kd == ST_SUM || kd == ST_COUNT) {
+    unsigned* w = (unsigned*)(s + L.off8[a]);
+    const unsigned v0 = (unsigned)lo;
+    unsigned c1 = 0;
+    unsigned long long t = (unsigned long long)(unsigned)(lo >> 32);
+    if (v0) {
+      unsigned o0 = atomicAdd(w, v0);
+      t += (o0 + v0) < o0 ? 1u : 0u;
+    }
+    if ((unsigned)t) {
+      unsigned o1 = atomicAdd(w + 1, (unsigned)t);
+      c1 = (o1 + (unsigned)t) < o1 ? 1u : 0u;
+    }
+    c1 += (unsigned)(t >> 32);
+    if (kd == ST_SUM) {
+      int h = hi + (int)c1;
+      if (h) atomicAdd((int*)(s + L.off4[a]), h);
+    }
+  } else {
+    unsigned long long* p = (unsigned long long*)(s + L.off8[a]);
+    unsigned long long u = kd == ST_MIN ? ~order_u((int64_t)lo) : order_u((int64_t)lo);
+    unsigned long long cur = *(volatile unsigned long long*)p;
+    while (u > cur) {
+      unsigned long long old = atomicCAS(p, cur, u);
+      if (old == cur) break;
+      cur = old;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ K10: mid G
+// A few hundred to a few thousand groups (e.g. Q9's 175 (nation, year) pairs): hashing straight
+// into the global table serialises on a handful of L2 lines.  Each CTA instead aggregates into
+// its own shared-memory open-addressing table (same slot layout, shared-memory atomics; runs of
+// equal keys pre-reduced per warp as in K11) and adds its occupied slots to the global table once
+// at the end.  Should the CTA table fill up (bad hint), further new keys go to the global table.
+template <class P, int ITEMS>
+__global__ void __launch_bounds__(kBlock) k_gb_shared(const __grid_constant__ P prog, const int32_t* __restrict__ sel,
+                                                      int64_t n, const __grid_constant__ Layout L, Table t,
+                                                      uint32_t scap) {
+  extern __shared__ __align__(16) uint8_t sm_tab[];
+  __shared__ int s_side, s_full;
+  const int lane = threadIdx.x & 31;
+  const size_t bytes = (size_t)(scap + 1) * L.slot_bytes;
+  for (size_t j = threadIdx.x * 8; j < bytes; j += blockDim.x * 8) *(unsigned long long*)(sm_tab + j) = 0;
+  if (threadIdx.x == 0) { s_side = 0; s_full = 0; }
+  __syncthreads();
+  const Table st{sm_tab, scap - 1, &s_side, &s_full};
+  bool ovf = false;
+  const int64_t tile = (int64_t)kBlock * ITEMS;
+  const int w = threadIdx.x >> 5;
+  for (int64_t base = blockIdx.x * tile + (int64_t)w * 32 * ITEMS; base < n; base += (int64_t)gridDim.x * tile) {
+    int32_t row[ITEMS];
+    bool alive[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      int64_t idx = base + 32 * i + lane;
+      alive[i] = idx < n;
+      row[i] = alive[i] ? (sel ? __ldg(sel + idx) : (int32_t)idx) : 0;
+    }
+    uint64_t key[ITEMS];
+    typename P::template Cache<ITEMS> cache;
+    prog.template where_keys<ITEMS>(row, alive, key, cache);
+    unsigned seg_start[ITEMS];
+    int soff[ITEMS];        // byte offset of the row's CTA-table slot, -1 if none
+    uint8_t* gslot[ITEMS];  // global slot when the CTA table had no room
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      uint64_t pk = __shfl_up_sync(kFull, key[i], 1);
+      bool pa = __shfl_up_sync(kFull, alive[i], 1);
+      bool head = !alive[i] || lane == 0 || !pa || pk != key[i];
+      unsigned heads = __ballot_sync(kFull, head);
+      uint64_t nk = __shfl_down_sync(kFull, key[i], 1);
+      bool na = __shfl_down_sync(kFull, alive[i], 1);
+      bool tail = alive[i] && (lane == 31 || !na || nk != key[i]);
+      seg_start[i] = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+      soff[i] = -1;
+      gslot[i] = nullptr;
+      if (tail) {
+        uint8_t* p = nullptr;
+        if (!*(volatile int*)&s_full) p = find_or_insert(st, L, key[i]);
+        if (p) soff[i] = (int)(p - sm_tab);
+        else gslot[i] = find_or_insert(t, L, key[i]);
+      }
+    }
+#pragma unroll(P::kUnrollStates)
+    for (int a = 0; a < P::kMaxNst; ++a) {
+      if (a >= L.nst) break;
+      const int kd = prog.kind(a, L);
+      int64_t v[ITEMS];
+      if (kd == ST_COUNT) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) v[i] = alive[i] ? 1 : 0;
+      } else {
+        prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
+      }
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        if (kd == ST_SUM || kd == ST_COUNT) {
+          unsigned long long l = alive[i] ? (unsigned long long)v[i] : 0;
+          int32_t h = (alive[i] && v[i] < 0) ? -1 : 0;
+          for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long l2 = __shfl_up_sync(kFull, l, o);
+            int32_t h2 = __shfl_up_sync(kFull, h, o);
+            if (lane - o >= (int)seg_start[i]) {
+              unsigned long long s = l + l2;
+              h += h2 + (s < l ? 1 : 0);
+              l = s;
+            }
+          }
+          if (soff[i] >= 0) apply_state_smem(sm_tab + soff[i], L, a, l, h);
+          else if (gslot[i]) apply_state(gslot[i], L, a, l, h);
+        } else {
+          int64_t m = alive[i] ? v[i] : (kd == ST_MIN ? INT64_MAX : INT64_MIN);
+          for (int o = 1; o < 32; o <<= 1) {
+            int64_t m2 = __shfl_up_sync(kFull, m, o);
+            if (lane - o >= (int)seg_start[i]) m = (kd == ST_MIN) ? (m2 < m ? m2 : m) : (m2 > m ? m2 : m);
+          }
+          if (soff[i] >= 0) apply_state_smem(sm_tab + soff[i], L, a, (unsigned long long)m, 0);
+          else if (gslot[i]) apply_state(gslot[i], L, a, (unsigned long long)m, 0);
+        }
+      }
+    }
+  }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e <= scap; e += blockDim.x) {
+    const uint8_t* s = sm_tab + (size_t)e * L.slot_bytes;
+    uint64_t key;
+    if (e == scap) {
+      if (!s_side) continue;
+      key = 0;
+    } else {
+      key = L.key_bytes == 4 ? (uint64_t)*(const unsigned*)s : *(const unsigned long long*)s;
+      if (!key) continue;
+    }
+    uint8_t* p = find_or_insert(t, L, key);
+    if (p) merge_slot(p, s, L);
+  }
 }
 
 // ------------------------------------------------------------------------------ partitioned K11
@@ -412,7 +575,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_gb_part(const __grid_constant__ P
         }
       }
     }
-#pragma unroll
+#pragma unroll(P::kUnrollStates)
     for (int a = 0; a < P::kMaxNst; ++a) {
       if (a >= nst) break;
       const int kd = prog.kind(a, L);
@@ -526,164 +689,252 @@ static __global__ void __launch_bounds__(kBlock) k_gb_merge_records(const __grid
 // When the (single) group key column is non-decreasing in row order — e.g. lineitem clustered by
 // orderkey, as TPC-H data is generated — each group is one contiguous run, so a row's group id is
 // (number of key changes before it) and the aggregation state lives in a dense array indexed by it:
-// no hashing, no random table traffic.  Pass 1 counts key changes per tile and verifies the order
-// (any decrease raises *unsorted and the host falls back to hashing); a scan gives each tile its
-// first group id; pass 2 recomputes run boundaries, group ids by a tile-level scan, pre-reduces runs
-// across lanes and adds each run's partial state into its dense slot.  Programs opt in with
-// kSortedOK and provide keys_only<I>(row, valid, key) (no filter: runs are over all rows).
-template <class P, int ITEMS>
+// no hashing and no random table traffic.  Rows are blocked per thread (thread t of a tile owns
+// ITEMS consecutive rows), so a thread reduces its runs in registers, sequentially.
+//   k_runs_count: heads (key changes) per tile; any decrease raises *unsorted (host falls back to
+//                 hashing).  A scan of the counts gives each tile the id of its first head.
+//   k_runs_agg:   per tile, group slot j in [0, heads] in shared memory (j = 0: the group carried
+//                 over from the previous tile); each thread adds one partial per run it touches
+//                 (32-bit shared atomics, rarely contended: only runs crossing thread boundaries),
+//                 then the tile writes the groups whose head it holds into the dense array with
+//                 plain stores (every group has exactly one such tile, so no zero-fill) and the
+//                 carried-over partial into a per-tile record.
+//   k_runs_fix:   adds the per-tile carry records into their groups (atomics, after k_runs_agg).
+// Programs opt in with kSortedOK and provide keys_only<I>(row, valid, key) (runs are over all rows).
+constexpr int kRunItems = 8;
+constexpr int kRunTile = kBlock * kRunItems;
+
+// Block-wide exclusive scan of one int per thread; returns the prefix, *total = block sum.
+__device__ __forceinline__ int block_exclusive_scan(int x, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < kBlock / 32 ? s_warp[lane] : 0, vi = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(kFull, vi, o);
+      if (lane >= o) vi += y;
+    }
+    if (lane < kBlock / 32) s_warp[lane] = vi - v;
+    if (lane == kBlock / 32 - 1) s_warp[kBlock / 32] = vi;
+  }
+  __syncthreads();
+  int r = s_warp[w] + inc - x;
+  *total = s_warp[kBlock / 32];
+  return r;
+}
+
+template <class P>
 __global__ void __launch_bounds__(kBlock) k_runs_count(const __grid_constant__ P prog, int64_t n, int32_t* tile_heads,
                                                        int64_t ntiles, int* unsorted) {
-  __shared__ int s_heads[kBlock / 32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ int s_warp[kBlock / 32 + 1];
+  __shared__ int s_stop;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if (*(volatile int*)unsorted) return;  // early exit: the hash path will run instead
-    const int64_t base = tile * (int64_t)(kBlock * ITEMS);
-    int32_t row[ITEMS], prow[ITEMS];
-    bool valid[ITEMS], pvalid[ITEMS];
+    if (threadIdx.x == 0) s_stop = *(volatile int*)unsorted;
+    __syncthreads();
+    if (s_stop) return;  // the hash path will run instead (uniform per CTA)
+    const int64_t r0 = tile * (int64_t)kRunTile + (int64_t)threadIdx.x * kRunItems;
+    int32_t row[kRunItems];
+    bool valid[kRunItems];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
-      valid[i] = idx < n;
-      pvalid[i] = valid[i] && idx > 0;
-      row[i] = valid[i] ? (int32_t)idx : 0;
-      prow[i] = pvalid[i] ? (int32_t)(idx - 1) : 0;
+    for (int i = 0; i < kRunItems; ++i) {
+      valid[i] = r0 + i < n;
+      row[i] = valid[i] ? (int32_t)(r0 + i) : 0;
     }
-    uint64_t key[ITEMS], pkey[ITEMS];
-    prog.template keys_only<ITEMS>(row, valid, key);
-    prog.template keys_only<ITEMS>(prow, pvalid, pkey);
+    uint64_t key[kRunItems], pk[1];
+    prog.template keys_only<kRunItems>(row, valid, key);
+    int32_t prow[1] = {(int32_t)(r0 - 1)};
+    bool pv[1] = {r0 > 0 && r0 < n};
+    prog.template keys_only<1>(prow, pv, pk);
     int h = 0;
     bool bad = false;
+    uint64_t prev = pk[0];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      h += valid[i] && (!pvalid[i] || key[i] != pkey[i]);
-      bad |= pvalid[i] && (int64_t)key[i] < (int64_t)pkey[i];
+    for (int i = 0; i < kRunItems; ++i) {
+      const bool has_prev = i > 0 || pv[0];
+      h += valid[i] && (!has_prev || key[i] != prev);
+      bad |= valid[i] && has_prev && (int64_t)key[i] < (int64_t)prev;
+      prev = key[i];
     }
     if (bad) atomicExch(unsorted, 1);
-    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(kFull, h, o);
-    if (lane == 0) s_heads[w] = h;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int q = 0; q < kBlock / 32; ++q) t += s_heads[q];
-      tile_heads[tile] = t;
-    }
-    __syncthreads();
+    int total;
+    block_exclusive_scan(h, s_warp, &total);
+    if (threadIdx.x == 0) tile_heads[tile] = total;
   }
 }
 
-template <class P, int ITEMS>
+// Shared-memory accumulation of one partial (SoA arrays lo[S] / hi[S]), 32-bit atomics only.
+__device__ __forceinline__ void smem_add96(unsigned long long* lo_p, int* hi_p, unsigned long long lo, int32_t hi,
+                                           bool with_hi) {
+  unsigned* w = (unsigned*)lo_p;
+  const unsigned v0 = (unsigned)lo;
+  unsigned long long t = (unsigned long long)(unsigned)(lo >> 32);
+  unsigned c1 = 0;
+  if (v0) {
+    unsigned o0 = atomicAdd(w, v0);
+    t += (o0 + v0) < o0 ? 1u : 0u;
+  }
+  if ((unsigned)t) {
+    unsigned o1 = atomicAdd(w + 1, (unsigned)t);
+    c1 = (o1 + (unsigned)t) < o1 ? 1u : 0u;
+  }
+  c1 += (unsigned)(t >> 32);
+  if (with_hi) {
+    int h = hi + (int)c1;
+    if (h) atomicAdd(hi_p, h);
+  }
+}
+__device__ __forceinline__ void smem_max64(unsigned long long* p, unsigned long long u) {
+  unsigned long long cur = *(volatile unsigned long long*)p;
+  while (u > cur) {
+    unsigned long long old = atomicCAS(p, cur, u);
+    if (old == cur) break;
+    cur = old;
+  }
+}
+
+inline size_t runs_smem_bytes(int nst) {
+  return (size_t)(kRunTile + 1) * (8 * (size_t)nst + 8 + 4 * (size_t)nst) + 16;
+}
+
+template <class P>
 __global__ void __launch_bounds__(kBlock) k_runs_agg(const __grid_constant__ P prog, int64_t n,
                                                      const int64_t* __restrict__ tile_first,
                                                      const __grid_constant__ Layout L, uint8_t* __restrict__ dense,
+                                                     uint8_t* __restrict__ carry, int64_t* __restrict__ carry_gid,
                                                      int64_t ntiles) {
-  constexpr int W = kBlock / 32;
-  constexpr int NE = ITEMS * W;
-  static_assert(NE <= 64, "scan assumes <= 2 cells per lane");
-  __shared__ int s_cnt[NE];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned lt = lanemask_lt();
+  constexpr int S = kRunTile + 1;
+  extern __shared__ __align__(16) unsigned long long sm_runs[];
+  unsigned long long* s_lo = sm_runs;                 // [nst][S]
+  unsigned long long* s_key = sm_runs + (size_t)L.nst * S;  // [S]
+  int* s_hi = (int*)(s_key + S);                      // [nst][S]
+  __shared__ int s_warp[kBlock / 32 + 1];
+  __shared__ int s_first_head;
+  const int nst = L.nst;
   bool ovf = false;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t base = tile * (int64_t)(kBlock * ITEMS);
-    int32_t row[ITEMS], prow[ITEMS];
-    bool valid[ITEMS], pvalid[ITEMS], alive[ITEMS];
+    for (int j = threadIdx.x; j < nst * S; j += kBlock) {
+      s_lo[j] = 0;
+      s_hi[j] = 0;
+    }
+    const int64_t r0 = tile * (int64_t)kRunTile + (int64_t)threadIdx.x * kRunItems;
+    int32_t row[kRunItems];
+    bool valid[kRunItems], alive[kRunItems];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
-      valid[i] = idx < n;
+    for (int i = 0; i < kRunItems; ++i) {
+      valid[i] = r0 + i < n;
       alive[i] = valid[i];
-      pvalid[i] = valid[i] && idx > 0;
-      row[i] = valid[i] ? (int32_t)idx : 0;
-      prow[i] = pvalid[i] ? (int32_t)(idx - 1) : 0;
+      row[i] = valid[i] ? (int32_t)(r0 + i) : 0;
     }
-    uint64_t key[ITEMS], pkey[ITEMS];
-    typename P::template Cache<ITEMS> cache;
-    prog.template where_keys<ITEMS>(row, alive, key, cache);
-    prog.template keys_only<ITEMS>(prow, pvalid, pkey);
-    unsigned ball[ITEMS];
+    uint64_t key[kRunItems], pk[1];
+    typename P::template Cache<kRunItems> cache;
+    prog.template where_keys<kRunItems>(row, alive, key, cache);
+    int32_t prow[1] = {(int32_t)(r0 - 1)};
+    bool pv[1] = {r0 > 0 && r0 < n};
+    prog.template keys_only<1>(prow, pv, pk);
+    unsigned hd = 0;  // bit i: row i starts a group
+    {
+      uint64_t prev = pk[0];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      ball[i] = __ballot_sync(kFull, valid[i] && (!pvalid[i] || key[i] != pkey[i]));
-      if (lane == 0) s_cnt[i * W + w] = __popc(ball[i]);
-    }
-    __syncthreads();
-    if (w == 0) {
-      int a = lane < NE ? s_cnt[lane] : 0;
-      int b = lane + 32 < NE ? s_cnt[lane + 32] : 0;
-      int pa = a, pb = b;
-      for (int o = 1; o < 32; o <<= 1) {
-        int ya = __shfl_up_sync(kFull, pa, o);
-        int yb = __shfl_up_sync(kFull, pb, o);
-        if (lane >= o) { pa += ya; pb += yb; }
-      }
-      int half = __shfl_sync(kFull, pa, 31);
-      if (lane < NE) s_cnt[lane] = pa - a;
-      if (lane + 32 < NE) s_cnt[lane + 32] = half + pb - b;
-    }
-    __syncthreads();
-    const int64_t first = tile_first[tile];
-    int64_t g[ITEMS];
-    unsigned seg_start[ITEMS];
-    bool tail[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      // group id = first id of the tile + heads up to and including this row - 1
-      g[i] = first + s_cnt[i * W + w] + __popc(ball[i] & (lt | (1u << lane))) - 1;
-      int64_t pg = __shfl_up_sync(kFull, g[i], 1);
-      bool pv = __shfl_up_sync(kFull, valid[i], 1);
-      bool head = !valid[i] || lane == 0 || !pv || pg != g[i];
-      unsigned heads = __ballot_sync(kFull, head);
-      int64_t ng = __shfl_down_sync(kFull, g[i], 1);
-      bool nv = __shfl_down_sync(kFull, valid[i], 1);
-      tail[i] = valid[i] && (lane == 31 || !nv || ng != g[i]);
-      seg_start[i] = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
-      if (tail[i]) {
-        uint8_t* s = dense + g[i] * (int64_t)L.slot_bytes;
-        if (L.key_bytes == 4) *(unsigned*)s = (unsigned)key[i];
-        else *(unsigned long long*)s = key[i];
+      for (int i = 0; i < kRunItems; ++i) {
+        const bool has_prev = i > 0 || pv[0];
+        if (valid[i] && (!has_prev || key[i] != prev)) hd |= 1u << i;
+        prev = key[i];
       }
     }
-    __syncthreads();
+    if (threadIdx.x == 0) s_first_head = (int)(hd & 1u) | (r0 >= n ? 1 : 0);
+    int total;
+    const int pre = block_exclusive_scan(__popc(hd), s_warp, &total);  // (syncs: smem zeroed)
+    // slot of row i = pre + heads in rows [0, i]; a head stores its group's key
 #pragma unroll
+    for (int i = 0; i < kRunItems; ++i)
+      if ((hd >> i) & 1u) s_key[pre + __popc(hd & ((2u << i) - 1))] = key[i];
+#pragma unroll(P::kUnrollStates)
     for (int a = 0; a < P::kMaxNst; ++a) {
-      if (a >= L.nst) break;
+      if (a >= nst) break;
       const int kd = prog.kind(a, L);
-      int64_t v[ITEMS];
+      int64_t v[kRunItems];
       if (kd == ST_COUNT) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) v[i] = valid[i] ? 1 : 0;
+        for (int i = 0; i < kRunItems; ++i) v[i] = 1;
       } else {
-        prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
+        prog.template state<kRunItems>(a, row, alive, cache, v, ovf);
       }
+      unsigned long long* lo_a = s_lo + (size_t)a * S;
+      int* hi_a = s_hi + (size_t)a * S;
+      // sequential run reduction in registers; one shared-memory update per run
+      unsigned long long lo = 0, m = 0;
+      int32_t hi = 0;
+      int slot = pre;
+      bool any = false;
 #pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        uint8_t* s = dense + g[i] * (int64_t)L.slot_bytes;
+      for (int i = 0; i < kRunItems; ++i) {
+        if (!valid[i]) break;
+        if ((hd >> i) & 1u) {
+          if (any) {
+            if (kd == ST_SUM || kd == ST_COUNT) smem_add96(lo_a + slot, hi_a + slot, lo, hi, kd == ST_SUM);
+            else smem_max64(lo_a + slot, m);
+          }
+          ++slot;
+          lo = 0;
+          hi = 0;
+          m = 0;
+        }
+        any = true;
         if (kd == ST_SUM || kd == ST_COUNT) {
-          unsigned long long l = valid[i] ? (unsigned long long)v[i] : 0;
-          int32_t h = (valid[i] && v[i] < 0) ? -1 : 0;
-          for (int o = 1; o < 32; o <<= 1) {
-            unsigned long long l2 = __shfl_up_sync(kFull, l, o);
-            int32_t h2 = __shfl_up_sync(kFull, h, o);
-            if (lane - o >= (int)seg_start[i]) {
-              unsigned long long s2 = l + l2;
-              h += h2 + (s2 < l ? 1 : 0);
-              l = s2;
-            }
-          }
-          if (tail[i]) apply_state(s, L, a, l, h);
+          unsigned long long nl = lo + (unsigned long long)v[i];
+          bool cy = nl < lo, neg = v[i] < 0;
+          if (cy != neg) hi += cy ? 1 : -1;
+          lo = nl;
         } else {
-          int64_t m = valid[i] ? v[i] : (kd == ST_MIN ? INT64_MAX : INT64_MIN);
-          for (int o = 1; o < 32; o <<= 1) {
-            int64_t m2 = __shfl_up_sync(kFull, m, o);
-            if (lane - o >= (int)seg_start[i]) m = (kd == ST_MIN) ? (m2 < m ? m2 : m) : (m2 > m ? m2 : m);
-          }
-          if (tail[i]) apply_state(s, L, a, (unsigned long long)m, 0);
+          unsigned long long u = kd == ST_MIN ? ~order_u(v[i]) : order_u(v[i]);
+          m = u > m ? u : m;
         }
       }
+      if (any) {
+        if (kd == ST_SUM || kd == ST_COUNT) smem_add96(lo_a + slot, hi_a + slot, lo, hi, kd == ST_SUM);
+        else smem_max64(lo_a + slot, m);
+      }
     }
+    __syncthreads();
+    // write-out: slot j >= 1 is group first + j - 1 (head in this tile); slot 0 is the carry-in
+    const int64_t first = tile_first[tile];
+    for (int j = threadIdx.x; j <= total; j += kBlock) {
+      uint8_t* dst;
+      if (j == 0) {
+        if (s_first_head) {
+          carry_gid[tile] = -1;
+          continue;
+        }
+        carry_gid[tile] = first - 1;
+        dst = carry + (size_t)tile * L.slot_bytes;
+      } else {
+        dst = dense + (size_t)(first + j - 1) * L.slot_bytes;
+        if (L.key_bytes == 4) *(unsigned*)dst = (unsigned)s_key[j];
+        else *(unsigned long long*)dst = s_key[j];
+      }
+      for (int a = 0; a < nst; ++a) {
+        *(unsigned long long*)(dst + L.off8[a]) = s_lo[(size_t)a * S + j];
+        if (L.kind[a] == ST_SUM) *(int*)(dst + L.off4[a]) = s_hi[(size_t)a * S + j];
+      }
+    }
+    __syncthreads();
   }
   if (ovf) atomicExch(prog.ovf_flag, 1);
+}
+
+static __global__ void k_runs_fix(const __grid_constant__ Layout L, uint8_t* __restrict__ dense,
+                                  const uint8_t* __restrict__ carry, const int64_t* __restrict__ carry_gid,
+                                  int64_t ntiles) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = carry_gid[t];
+    if (g >= 0) merge_slot(dense + (size_t)g * L.slot_bytes, carry + (size_t)t * L.slot_bytes, L);
+  }
 }
 
 // ------------------------------------------------------------------------------ K9: small G
@@ -768,7 +1019,7 @@ __global__ void __launch_bounds__(kSmallThreads, (P::kMaxNst <= 2 ? 2 : 1)) k_gb
       cell0[i] = (alive[i] && s >= 0 ? s : kSmallSlots) * stride_slot + tid;  // kSmallSlots = trash
       slow |= alive[i] && s < 0;
     }
-#pragma unroll
+#pragma unroll(P::kUnrollStates)
     for (int a = 0; a < P::kMaxNst; ++a) {
       if (a >= nst) break;
       const int kd = prog.kind(a, L);

@@ -137,7 +137,51 @@ struct ProbeFn {
   }
 };
 
-// INNER join on a non-unique build: every match emitted; output slots by warp-aggregated atomics.
+// INNER join on a non-unique build, typed keys (count -> scan -> expand):
+//   1. ordered compaction with ProbeFnT{count_all}: the probe rows with >= 1 match, aux = count;
+//   2. exclusive scan of the counts -> each matched row's first output position;
+//   3. k_expand walks each matched row's chain again and writes its (probe row, build row)
+//      pairs at those positions; payload columns are then gathered densely.
+// Output order: probe order; a probe row's matches in table-chain order.
+template <typename KT, int NK, int KB>
+__global__ void __launch_bounds__(kBlock) k_expand(const __grid_constant__ ProbeFnT<KT, NK, KB> f,
+                                                   const int32_t* __restrict__ msel, const int64_t* __restrict__ offs,
+                                                   int64_t m, int32_t* __restrict__ op, int32_t* __restrict__ ob) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = __ldg(msel + j);
+    int64_t o = __ldg(offs + j);
+    uint64_t key = (uint64_t)(int64_t)__ldg(f.k0 + r);
+    if (NK == 2) key = (key << 32) | (uint32_t)__ldg(f.k1 + r);
+    uint32_t h = (uint32_t)(KB == 4 ? hash32((uint32_t)key) : hash64(key)) & f.mask;
+    if (KB == 4) {
+      bool first = (h & 1u) != 0;
+      h &= ~1u;
+      for (;;) {
+        ulonglong2 s = __ldg((const ulonglong2*)f.slots + (h >> 1));
+        uint32_t r0 = (uint32_t)(s.x >> 32), r1 = (uint32_t)(s.y >> 32);
+        if (!first) {
+          if (r0 == 0xffffffffu) break;
+          if ((uint32_t)s.x == (uint32_t)key) { op[o] = r; ob[o] = (int32_t)r0; ++o; }
+        }
+        if (r1 == 0xffffffffu) break;
+        if ((uint32_t)s.y == (uint32_t)key) { op[o] = r; ob[o] = (int32_t)r1; ++o; }
+        first = false;
+        h = (h + 2) & f.mask;
+      }
+    } else {
+      for (;;) {
+        longlong2 s = __ldg((const longlong2*)f.slots + h);
+        uint32_t rw = (uint32_t)(unsigned long long)s.y;
+        if (rw == 0xffffffffu) break;
+        if ((uint64_t)s.x == key) { op[o] = r; ob[o] = (int32_t)rw; ++o; }
+        h = (h + 1) & f.mask;
+      }
+    }
+  }
+}
+
+// INNER join on a non-unique build, generic keys: every match emitted; output slots by
+// warp-aggregated atomics (order not deterministic).
 struct InnerArgs {
   DCol cols[SX_MAX_COLS];
   DPred preds[SX_MAX_PREDS];
@@ -373,7 +417,61 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
   const int32_t* isel = in_sel ? in_sel->idx : nullptr;
   int64_t count = 0;
   int32_t *op = nullptr, *ob = nullptr;
-  if (join_type != SX_INNER || ht->unique) {
+  auto is32 = [&](int c) { int t = probe_cols[key_cols[c]].type; return t == SX_I32 || t == SX_DATE32; };
+  auto fill_t = [&](auto& ft) {
+    for (int i = 0; i < nprobe_cols; ++i) ft.cols[i] = pcols[i];
+    for (int i = 0; i < nwhere; ++i) ft.preds[i] = preds[i];
+    ft.np = nwhere;
+    ft.k0 = (decltype(ft.k0))probe_cols[key_cols[0]].data;
+    ft.k1 = nkeys > 1 ? (const int32_t*)probe_cols[key_cols[1]].data : nullptr;
+    ft.slots = ht->slots;
+    ft.mask = (uint32_t)(ht->cap - 1);
+    ft.anti = join_type == SX_ANTI;
+    ft.member_only = join_type != SX_INNER;
+    ft.count_all = 0;
+    ft.bm = ht->bm;
+    ft.bm_min = ht->bm_min;
+    ft.bm_bits = ht->bm_bits;
+  };
+  // non-unique INNER with typed keys: count -> scan -> expand (see k_expand)
+  auto run_expand = [&](auto ft) -> sx_status {
+    fill_t(ft);
+    ft.count_all = 1;
+    int32_t *msel = nullptr, *mcnt = nullptr;
+    int64_t m = 0;
+    GatherSpec none;
+    none.n = 0;
+    SX_TRY((run_compact<decltype(ft), 4>(ctx, ft, n, isel, &msel, &mcnt, none, &m)));
+    scr.ptrs.push_back(msel);
+    scr.ptrs.push_back(mcnt);
+    int64_t* offs;
+    SX_TRY(scr.get(&offs, (size_t)m + 1));
+    SX_TRY(scan_counts(ctx, mcnt, m, offs, &count));
+    if (count > INT32_MAX) return set_err(ctx, SX_EINDEX, "join output exceeds INT32_MAX rows");
+    const size_t c = (size_t)(count > 0 ? count : 1);
+    SX_TRY(scr.get(&op, c));
+    SX_TRY(scr.get(&ob, c));
+    for (int g = 0; g < gs.n; ++g) SX_TRY(scr.get((char**)&gs.g[g].dst, c * gs.g[g].width));
+    if (m > 0) {
+      k_expand<<<persistent_grid(ctx, 8, (m + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(ft, msel, offs, m, op,
+                                                                                                ob);
+      SX_CHECK_LAUNCH();
+    }
+    if (count > 0 && gs.n > 0) {
+      k_gather_multi<<<persistent_grid(ctx, 8, (count + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(op, ob,
+                                                                                                          count, gs);
+      SX_CHECK_LAUNCH();
+    }
+    return SX_OK;
+  };
+  const bool typed = ht->cap <= (1ull << 32) &&
+                     ((nkeys == 1 && kb == 4 && is32(0)) || (nkeys == 1 && kb == 8 && probe_cols[key_cols[0]].type == SX_I64) ||
+                      (nkeys == 2 && is32(0) && is32(1)));
+  if (join_type == SX_INNER && !ht->unique && typed) {
+    if (nkeys == 2) SX_TRY(run_expand(ProbeFnT<int32_t, 2, 8>{}));
+    else if (kb == 4) SX_TRY(run_expand(ProbeFnT<int32_t, 1, 4>{}));
+    else SX_TRY(run_expand(ProbeFnT<long long, 1, 8>{}));
+  } else if (join_type != SX_INNER || ht->unique) {
     // ordered compaction: each probe row emits at most one output
     ProbeFn f;
     for (int i = 0; i < nprobe_cols; ++i) f.cols[i] = pcols[i];
@@ -389,21 +487,9 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     for (int g = 0; g < gs.n; ++g) gs.g[g].dst = nullptr;  // allocated at the exact output count
     int32_t** pob = join_type == SX_INNER ? &ob : nullptr;
     auto run_t = [&](auto ft) -> sx_status {
-      for (int i = 0; i < nprobe_cols; ++i) ft.cols[i] = pcols[i];
-      for (int i = 0; i < nwhere; ++i) ft.preds[i] = preds[i];
-      ft.np = nwhere;
-      ft.k0 = (decltype(ft.k0))probe_cols[key_cols[0]].data;
-      ft.k1 = nkeys > 1 ? (const int32_t*)probe_cols[key_cols[1]].data : nullptr;
-      ft.slots = ht->slots;
-      ft.mask = (uint32_t)(ht->cap - 1);
-      ft.anti = join_type == SX_ANTI;
-      ft.member_only = join_type != SX_INNER;
-      ft.bm = ht->bm;
-      ft.bm_min = ht->bm_min;
-      ft.bm_bits = ht->bm_bits;
+      fill_t(ft);
       return run_compact<decltype(ft), 4>(ctx, ft, n, isel, &op, pob, gs, &count);
     };
-    auto is32 = [&](int c) { int t = probe_cols[key_cols[c]].type; return t == SX_I32 || t == SX_DATE32; };
     if (ht->cap <= (1ull << 32) && nkeys == 1 && kb == 4 && is32(0)) {
       SX_TRY(run_t(ProbeFnT<int32_t, 1, 4>{}));
     } else if (ht->cap <= (1ull << 32) && nkeys == 1 && kb == 8 && probe_cols[key_cols[0]].type == SX_I64) {

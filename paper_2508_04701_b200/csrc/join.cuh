@@ -43,6 +43,7 @@ struct ProbeFnT {
   uint32_t mask;
   int anti;
   int member_only;     // semi/anti: membership is the whole answer
+  int count_all;       // inner join on a non-unique build: aux = number of matches (scan to EMPTY)
   const uint32_t* bm;  // optional exact key-range bitmap of the build side
   long long bm_min;
   unsigned long long bm_bits;
@@ -55,8 +56,12 @@ struct ProbeFnT {
     uint64_t key[ITEMS];
     uint32_t h[ITEMS];
     bool pend[ITEMS], found[ITEMS];
+    uint32_t cnt[ITEMS];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) key[i] = alive[i] ? (uint64_t)(int64_t)__ldg(k0 + row[i]) : 0;
+    for (int i = 0; i < ITEMS; ++i) {
+      key[i] = alive[i] ? (uint64_t)(int64_t)__ldg(k0 + row[i]) : 0;
+      cnt[i] = 0;
+    }
     if (NK == 2) {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i)
@@ -107,12 +112,18 @@ struct ProbeFnT {
           if (!pend[i]) continue;
           uint32_t r0 = (uint32_t)(s[i].x >> 32), r1 = (uint32_t)(s[i].y >> 32);
           bool e0 = r0 == 0xffffffffu && !first[i], e1 = r1 == 0xffffffffu;
-          bool h0 = r0 != 0xffffffffu && !first[i] && (uint32_t)s[i].x == (uint32_t)key[i];
-          bool h1 = !e0 && !h0 && r1 != 0xffffffffu && (uint32_t)s[i].y == (uint32_t)key[i];
-          found[i] |= h0 || h1;
-          if (h0) aux[i] = (int32_t)r0;
-          if (h1) aux[i] = (int32_t)r1;
-          pend[i] = !(e0 || h0 || e1 || h1);
+          bool m0 = r0 != 0xffffffffu && !first[i] && (uint32_t)s[i].x == (uint32_t)key[i];
+          bool m1 = !e0 && r1 != 0xffffffffu && (uint32_t)s[i].y == (uint32_t)key[i];
+          if (count_all) {  // every match up to the first EMPTY slot
+            cnt[i] += (m0 ? 1 : 0) + (m1 ? 1 : 0);
+            pend[i] = !(e0 || e1);
+          } else {
+            bool h1 = m1 && !m0;
+            found[i] |= m0 || h1;
+            if (m0) aux[i] = (int32_t)r0;
+            if (h1) aux[i] = (int32_t)r1;
+            pend[i] = !(e0 || m0 || e1 || h1);
+          }
           first[i] = false;
           h[i] = (h[i] + 2) & mask;
           any |= pend[i];
@@ -131,13 +142,26 @@ struct ProbeFnT {
           if (!pend[i]) continue;
           uint32_t rw = (uint32_t)(unsigned long long)s[i].y;
           bool empty = rw == 0xffffffffu, hit = !empty && (uint64_t)s[i].x == key[i];
-          found[i] |= hit;
-          if (hit) aux[i] = (int32_t)rw;
-          pend[i] = !empty && !hit;
+          if (count_all) {
+            cnt[i] += hit ? 1 : 0;
+            pend[i] = !empty;
+          } else {
+            found[i] |= hit;
+            if (hit) aux[i] = (int32_t)rw;
+            pend[i] = !empty && !hit;
+          }
           h[i] = (h[i] + 1) & mask;
           any |= pend[i];
         }
       }
+    }
+    if (count_all) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        alive[i] = alive[i] && cnt[i] > 0;
+        aux[i] = (int32_t)cnt[i];
+      }
+      return;
     }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) alive[i] = alive[i] && (anti ? !found[i] : found[i]);

@@ -35,6 +35,7 @@ struct Q1Prog {
   int32_t ship_max;
   int* ovf_flag;
   static constexpr int kMaxNst = 6;
+  static constexpr int kUnrollStates = 6;
   static constexpr bool kSortedOK = false;
   bool no_filter() const { return false; }
   template <int I>
@@ -86,6 +87,7 @@ struct Q6Prog {
   int64_t disc_lo, disc_hi, qty_lt;
   int* ovf_flag;
   static constexpr int kMaxNst = 2;
+  static constexpr int kUnrollStates = 2;
   static constexpr bool kSortedOK = false;
   bool no_filter() const { return false; }
   template <int I>
@@ -130,6 +132,7 @@ struct Q18Prog {
   const long long* qty;
   int* ovf_flag;
   static constexpr int kMaxNst = 1;
+  static constexpr int kUnrollStates = 1;
   static constexpr bool kSortedOK = true;
   bool no_filter() const { return true; }
   template <int I>
@@ -154,6 +157,43 @@ struct Q18Prog {
                                         int64_t (&v)[I], bool&) const {
 #pragma unroll
     for (int i = 0; i < I; ++i) v[i] = c.q[i];
+  }
+};
+
+// Q9: key (nationkey, year(o_orderdate)); state 0 sum(ext*(100-disc) - supplycost*qty)
+struct Q9Prog {
+  const int32_t* nation;
+  const long long *cost, *qty, *ext, *disc;
+  const int32_t* odate;
+  int* ovf_flag;
+  static constexpr int kMaxNst = 1;
+  static constexpr int kUnrollStates = 1;
+  static constexpr bool kSortedOK = false;
+  bool no_filter() const { return true; }
+  template <int I>
+  __device__ __forceinline__ void keys_only(const int32_t (&)[I], const bool (&)[I], uint64_t (&)[I]) const {}
+  template <int I>
+  struct Cache {};
+  __device__ __forceinline__ int kind(int, const Layout&) const { return ST_SUM; }
+  template <int I>
+  __device__ __forceinline__ void where_keys(const int32_t (&row)[I], bool (&alive)[I], uint64_t (&key)[I],
+                                             Cache<I>&) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      uint32_t nk = alive[i] ? (uint32_t)__ldg(nation + row[i]) : 0u;
+      int32_t d = alive[i] ? __ldg(odate + row[i]) : 0;
+      key[i] = ((uint64_t)nk << 32) | (uint32_t)civil_year(d);
+    }
+  }
+  template <int I>
+  __device__ __forceinline__ void state(int, const int32_t (&row)[I], const bool (&alive)[I], const Cache<I>&,
+                                        int64_t (&v)[I], bool& ovf) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      int64_t e = alive[i] ? __ldg(ext + row[i]) : 0, d = alive[i] ? __ldg(disc + row[i]) : 0;
+      int64_t c = alive[i] ? __ldg(cost + row[i]) : 0, q = alive[i] ? __ldg(qty + row[i]) : 0;
+      v[i] = sub_ck(mul_ck(e, sub_ck(100, d, ovf), ovf), mul_ck(c, q, ovf), ovf);
+    }
   }
 };
 
@@ -545,7 +585,18 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   ga.value.t[1].f[1] = F(2);
   sx_col gok[2], goa[1];
   int64_t ng = 0;
-  SX_TRY(sx_groupby_agg(ctx, L5, 6, gk, 2, nullptr, nullptr, 0, &ga, 1, nullptr, 256, gok, goa, &ng));
+  if (w4(L5[0]) && w8(L5[1]) && w8(L5[2]) && w8(L5[3]) && w8(L5[4]) && w4(L5[5])) {
+    ProfScope pg(ctx, "groupby");
+    GbPlan plan;
+    SX_TRY(to_dcols_check(ctx, L5, 6));
+    SX_TRY(gb_plan(ctx, L5, 6, gk, 2, &ga, 1, nullptr, &plan));
+    SX_TRY(check_states(ctx, plan, {ST_SUM}));
+    Q9Prog prog{(const int32_t*)L5[0].data, (const long long*)L5[1].data, (const long long*)L5[2].data,
+                (const long long*)L5[3].data, (const long long*)L5[4].data, (const int32_t*)L5[5].data, ctx->d_flags};
+    SX_TRY(gb_run(ctx, prog, plan, nullptr, L5[0].len, 256, gok, goa, &ng));
+  } else {
+    SX_TRY(sx_groupby_agg(ctx, L5, 6, gk, 2, nullptr, nullptr, 0, &ga, 1, nullptr, 256, gok, goa, &ng));
+  }
   bag.keep(gok, 2);
   bag.keep(goa, 1);
   // 8. order by n_name asc (string order of the nation dimension), o_year desc

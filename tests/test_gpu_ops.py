@@ -107,7 +107,7 @@ AGGS = [("sum", [(1, [(2, 1, 0), (3, -1, 100)])]), ("count", []), ("min", [(1, [
 
 
 @pytest.mark.parametrize("n", SIZES)
-@pytest.mark.parametrize("ng,hint", [(3, 4), (4, 4), (300, 512), (5000, 0), (None, 0)])
+@pytest.mark.parametrize("ng,hint", [(3, 4), (4, 4), (300, 512), (175, 256), (3000, 100), (5000, 0), (None, 0)])
 def test_groupby_one_key(ctx, n, ng, hint):
     rng = np.random.default_rng(n + (ng or 0))
     dom = ng if ng else max(n, 1)
@@ -186,6 +186,33 @@ def test_groupby_having_and_sel(ctx):
     check_gb(canon(keys, outs, ["sum"]), want)
 
 
+@pytest.mark.parametrize("n", [1, 1023, 1024, 1025, 100_003])
+@pytest.mark.parametrize("order", ["sorted", "unsorted", "one_run"])
+def test_groupby_sorted_runs(ctx, monkeypatch, n, order):
+    """Sorted-input strategy (forced with SX_GB_SORTED=2): non-decreasing keys aggregate by runs
+    into a dense array; a decrease anywhere falls back to hashing.  Runs cross tile (1024 rows)
+    and warp boundaries; keys include 0 and negatives; HAVING applies at extraction."""
+    monkeypatch.setenv("SX_GB_SORTED", "2")
+    rng = np.random.default_rng(n + len(order))
+    if order == "one_run":
+        k = np.full(n, 7, np.int32)
+    else:
+        k = np.sort(rng.integers(-50, max(n // 3, 2), n)).astype(np.int32)
+        if order == "unsorted" and n > 1:
+            j = int(rng.integers(1, n))
+            k[j - 1], k[j] = k[j] + 1, k[j - 1]  # one descent (the last step, if j = n - 1)
+    v = rng.integers(-(10**12), 10**12, n).astype(np.int64)
+    w = rng.integers(0, 100, n).astype(np.int64)
+    cols = [c(dev(k)), c(dev(k)), c(dev(v)), c(dev(w))]
+    keys, aggs, g = ctx.groupby(cols, [(0, "id")], AGGS, groups_hint=n + 10)
+    want = oracle.groupby([k, k, v, w], [0], AGGS)
+    check_gb(canon(keys, aggs, [a[0] for a in AGGS]), want)
+    assert g == len(want)
+    keys, outs, g = ctx.groupby(cols, [(0, "id")], [("count", [])], having=(0, "ge", 3), groups_hint=n + 10)
+    want = [r for r in oracle.groupby([k, k, v, w], [0], [("count", [])]) if r[1] >= 3]
+    check_gb(canon(keys, outs, ["count"]), want)
+
+
 def test_groupby_expression_overflow_is_an_error(ctx):
     v = np.array([2**62, 3], np.int64)
     with pytest.raises(sx.SxError) as e:
@@ -195,7 +222,7 @@ def test_groupby_expression_overflow_is_an_error(ctx):
 
 # ------------------------------------------------------------------------------------- joins
 @pytest.mark.parametrize("nb,np_,dom", [(0, 100, 10), (1, 1, 1), (3000, 5000, 1000), (20_000, 100_003, 40_000),
-                                        (5000, 70_000, 2**40)])
+                                        (5000, 70_000, 2**40), (2000, 3000, 5)])
 def test_join_types(ctx, nb, np_, dom):
     rng = np.random.default_rng(nb + np_)
     dt = np.int64 if dom > 2**31 else np.int32
@@ -212,10 +239,37 @@ def test_join_types(ctx, nb, np_, dom):
     assert got == sorted(zip(wp.tolist(), wb.tolist()))
     pr, br = p.cpu().numpy(), b.cpu().numpy()
     assert np.array_equal(pay[0].cpu().numpy(), bpay[br]) and np.array_equal(pay[1].cpu().numpy(), ppay[pr])
+    assert np.all(np.diff(pr) >= 0)  # typed keys: count/scan/expand emits in probe order
     s, _, _ = ctx.hash_probe(ht, [c(tp)], [0], "semi")
     assert np.array_equal(s.cpu().numpy(), oracle.join(bk, pk, "semi"))
     a, _, _ = ctx.hash_probe(ht, [c(tp)], [0], "anti")
     assert np.array_equal(a.cpu().numpy(), oracle.join(bk, pk, "anti"))
+
+
+@pytest.mark.parametrize("kind", ["two_i32", "u8"])
+def test_join_non_unique_other_keys(ctx, kind):
+    """Non-unique INNER joins on packed two-column keys (typed expand path) and on u8 keys
+    (generic path): the multiset of (probe, build) pairs and the gathered payloads."""
+    rng = np.random.default_rng(17)
+    nb, n = 4000, 20_000
+    if kind == "two_i32":
+        b1, b2 = rng.integers(0, 30, nb).astype(np.int32), rng.integers(0, 20, nb).astype(np.int32)
+        p1, p2 = rng.integers(0, 35, n).astype(np.int32), rng.integers(0, 20, n).astype(np.int32)
+        bcols, pcols, keys = [c(dev(b1)), c(dev(b2))], [c(dev(p1)), c(dev(p2))], [0, 1]
+        bk = (b1.astype(np.int64) << 32) | b2
+        pk = (p1.astype(np.int64) << 32) | p2
+    else:
+        b1 = rng.integers(0, 200, nb).astype(np.uint8)
+        p1 = rng.integers(0, 256, n).astype(np.uint8)
+        bcols, pcols, keys = [c(dev(b1))], [c(dev(p1))], [0]
+        bk, pk = b1.astype(np.int64), p1.astype(np.int64)
+    bpay = rng.integers(0, 10**9, nb).astype(np.int64)
+    ht = ctx.hash_build(bcols + [c(dev(bpay))], keys)
+    p, b, pay = ctx.hash_probe(ht, pcols, keys, "inner", build_cols=bcols + [c(dev(bpay))], bp=[len(keys)])
+    wp, wb = oracle.join(bk, pk, "inner")
+    got = sorted(zip(p.cpu().numpy().tolist(), b.cpu().numpy().tolist()))
+    assert got == sorted(zip(wp.tolist(), wb.tolist()))
+    assert np.array_equal(pay[0].cpu().numpy(), bpay[b.cpu().numpy()])
 
 
 def test_join_unique_build_two_keys_where(ctx):

@@ -73,6 +73,19 @@ def test_query_params_vs_oracle(small):
     assert rows_equal(got, want), diff_rows(got, want)
 
 
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_q18_group_strategies(small, monkeypatch, mode):
+    """Q18's subquery group-by through the hash table (SX_GB_SORTED=0) and through the
+    sorted-run strategy forced at any table size (=2; by default it engages only when the
+    hash table would exceed half the L2, i.e. at the bench scale)."""
+    sfm, host, T = small
+    monkeypatch.setenv("SX_GB_SORTED", mode)
+    for over in ({}, dict(q18_qty_gt=20000)):
+        got = T.run("q18", tpch.default_params(**over))
+        want = oracle.run_query("q18", host, oracle.default_params(**over))
+        assert rows_equal(got, want), diff_rows(got, want)
+
+
 def test_gpu_generator_matches_cpu_generator():
     cpu = gen.cpu_tables(10, seed=42)
     g = gen.gpu_tables(10, seed=42)
