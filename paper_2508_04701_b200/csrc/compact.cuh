@@ -20,7 +20,7 @@
 namespace sx {
 
 template <class F, bool HAS_SEL, int ITEMS>
-__global__ void __launch_bounds__(kBlock) k_compact_local(const __grid_constant__ F f, int64_t n,
+__global__ void __launch_bounds__(kBlock, 4) k_compact_local(const __grid_constant__ F f, int64_t n,
                                                           const int32_t* __restrict__ in_sel,
                                                           int32_t* __restrict__ s_row, int32_t* __restrict__ s_aux,
                                                           int32_t* __restrict__ tile_cnt, int64_t ntiles) {

@@ -377,11 +377,13 @@ __device__ __forceinline__ void apply_state_smem(uint8_t* s, const Layout& L, in
   }
 }
 
+static __device__ __noinline__ void gb_row_to_global(const Table& t, const Layout& L, uint64_t key, int a, int64_t v);
+
 // ------------------------------------------------------------------------------ K10: mid G
 // A few hundred to a few thousand groups (e.g. Q9's 175 (nation, year) pairs): hashing straight
 // into the global table serialises on a handful of L2 lines.  Each CTA instead aggregates into
-// its own shared-memory open-addressing table (same slot layout, shared-memory atomics; runs of
-// equal keys pre-reduced per warp as in K11) and adds its occupied slots to the global table once
+// its own shared-memory open-addressing table (same slot layout, 32-bit shared-memory atomics)
+// and adds its occupied slots to the global table once
 // at the end.  Should the CTA table fill up (bad hint), further new keys go to the global table.
 template <class P, int ITEMS>
 __global__ void __launch_bounds__(kBlock) k_gb_shared(const __grid_constant__ P prog, const int32_t* __restrict__ sel,
@@ -410,26 +412,15 @@ __global__ void __launch_bounds__(kBlock) k_gb_shared(const __grid_constant__ P 
     uint64_t key[ITEMS];
     typename P::template Cache<ITEMS> cache;
     prog.template where_keys<ITEMS>(row, alive, key, cache);
-    unsigned seg_start[ITEMS];
-    int soff[ITEMS];        // byte offset of the row's CTA-table slot, -1 if none
-    uint8_t* gslot[ITEMS];  // global slot when the CTA table had no room
+    // per row: its CTA-table slot (no run pre-reduction: mid-G keys rarely repeat in a warp, and
+    // shared atomics are cheap), else the global table (cold, out of line)
+    int soff[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-      uint64_t pk = __shfl_up_sync(kFull, key[i], 1);
-      bool pa = __shfl_up_sync(kFull, alive[i], 1);
-      bool head = !alive[i] || lane == 0 || !pa || pk != key[i];
-      unsigned heads = __ballot_sync(kFull, head);
-      uint64_t nk = __shfl_down_sync(kFull, key[i], 1);
-      bool na = __shfl_down_sync(kFull, alive[i], 1);
-      bool tail = alive[i] && (lane == 31 || !na || nk != key[i]);
-      seg_start[i] = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
       soff[i] = -1;
-      gslot[i] = nullptr;
-      if (tail) {
-        uint8_t* p = nullptr;
-        if (!*(volatile int*)&s_full) p = find_or_insert(st, L, key[i]);
+      if (alive[i] && !*(volatile int*)&s_full) {
+        uint8_t* p = find_or_insert(st, L, key[i]);
         if (p) soff[i] = (int)(p - sm_tab);
-        else gslot[i] = find_or_insert(t, L, key[i]);
       }
     }
 #pragma unroll(P::kUnrollStates)
@@ -439,35 +430,16 @@ __global__ void __launch_bounds__(kBlock) k_gb_shared(const __grid_constant__ P 
       int64_t v[ITEMS];
       if (kd == ST_COUNT) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) v[i] = alive[i] ? 1 : 0;
+        for (int i = 0; i < ITEMS; ++i) v[i] = 1;
       } else {
         prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
       }
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
-        if (kd == ST_SUM || kd == ST_COUNT) {
-          unsigned long long l = alive[i] ? (unsigned long long)v[i] : 0;
-          int32_t h = (alive[i] && v[i] < 0) ? -1 : 0;
-          for (int o = 1; o < 32; o <<= 1) {
-            unsigned long long l2 = __shfl_up_sync(kFull, l, o);
-            int32_t h2 = __shfl_up_sync(kFull, h, o);
-            if (lane - o >= (int)seg_start[i]) {
-              unsigned long long s = l + l2;
-              h += h2 + (s < l ? 1 : 0);
-              l = s;
-            }
-          }
-          if (soff[i] >= 0) apply_state_smem(sm_tab + soff[i], L, a, l, h);
-          else if (gslot[i]) apply_state(gslot[i], L, a, l, h);
-        } else {
-          int64_t m = alive[i] ? v[i] : (kd == ST_MIN ? INT64_MAX : INT64_MIN);
-          for (int o = 1; o < 32; o <<= 1) {
-            int64_t m2 = __shfl_up_sync(kFull, m, o);
-            if (lane - o >= (int)seg_start[i]) m = (kd == ST_MIN) ? (m2 < m ? m2 : m) : (m2 > m ? m2 : m);
-          }
-          if (soff[i] >= 0) apply_state_smem(sm_tab + soff[i], L, a, (unsigned long long)m, 0);
-          else if (gslot[i]) apply_state(gslot[i], L, a, (unsigned long long)m, 0);
-        }
+        if (!alive[i]) continue;
+        if (soff[i] >= 0) apply_state_smem(sm_tab + soff[i], L, a, (unsigned long long)v[i],
+                                           (kd == ST_SUM && v[i] < 0) ? -1 : 0);
+        else gb_row_to_global(t, L, key[i], a, v[i]);
       }
     }
   }

@@ -144,7 +144,7 @@ struct ProbeFn {
 //      pairs at those positions; payload columns are then gathered densely.
 // Output order: probe order; a probe row's matches in table-chain order.
 template <typename KT, int NK, int KB>
-__global__ void __launch_bounds__(kBlock) k_expand(const __grid_constant__ ProbeFnT<KT, NK, KB> f,
+__global__ void __launch_bounds__(kBlock) k_expand(const __grid_constant__ ProbeFnT<KT, NK, KB, true> f,
                                                    const int32_t* __restrict__ msel, const int64_t* __restrict__ offs,
                                                    int64_t m, int32_t* __restrict__ op, int32_t* __restrict__ ob) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
@@ -428,7 +428,6 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     ft.mask = (uint32_t)(ht->cap - 1);
     ft.anti = join_type == SX_ANTI;
     ft.member_only = join_type != SX_INNER;
-    ft.count_all = 0;
     ft.bm = ht->bm;
     ft.bm_min = ht->bm_min;
     ft.bm_bits = ht->bm_bits;
@@ -436,7 +435,6 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
   // non-unique INNER with typed keys: count -> scan -> expand (see k_expand)
   auto run_expand = [&](auto ft) -> sx_status {
     fill_t(ft);
-    ft.count_all = 1;
     int32_t *msel = nullptr, *mcnt = nullptr;
     int64_t m = 0;
     GatherSpec none;
@@ -468,9 +466,9 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
                      ((nkeys == 1 && kb == 4 && is32(0)) || (nkeys == 1 && kb == 8 && probe_cols[key_cols[0]].type == SX_I64) ||
                       (nkeys == 2 && is32(0) && is32(1)));
   if (join_type == SX_INNER && !ht->unique && typed) {
-    if (nkeys == 2) SX_TRY(run_expand(ProbeFnT<int32_t, 2, 8>{}));
-    else if (kb == 4) SX_TRY(run_expand(ProbeFnT<int32_t, 1, 4>{}));
-    else SX_TRY(run_expand(ProbeFnT<long long, 1, 8>{}));
+    if (nkeys == 2) SX_TRY((run_expand(ProbeFnT<int32_t, 2, 8, true>{})));
+    else if (kb == 4) SX_TRY((run_expand(ProbeFnT<int32_t, 1, 4, true>{})));
+    else SX_TRY((run_expand(ProbeFnT<long long, 1, 8, true>{})));
   } else if (join_type != SX_INNER || ht->unique) {
     // ordered compaction: each probe row emits at most one output
     ProbeFn f;
@@ -497,7 +495,7 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     } else if (ht->cap <= (1ull << 32) && nkeys == 2 && is32(0) && is32(1)) {
       SX_TRY(run_t(ProbeFnT<int32_t, 2, 8>{}));
     } else {
-      SX_TRY(run_compact(ctx, f, n, isel, &op, pob, gs, &count));
+      SX_TRY((run_compact<ProbeFn, 4>(ctx, f, n, isel, &op, pob, gs, &count)));
     }
   } else {
     InnerArgs a{};

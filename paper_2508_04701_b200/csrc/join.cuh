@@ -32,7 +32,7 @@ __device__ __forceinline__ uint64_t table_hash(uint64_t key, int key_bytes) {
 // columns NK (2: two int32 columns packed (k0 << 32) | k1, reading R11) and the table layout KB.
 // All ITEMS key loads are issued back to back, then all first-slot loads, then the (rare) longer
 // chains; semi/anti/unique-inner emit at most one output per probe row (ordered compaction).
-template <typename KT, int NK, int KB>
+template <typename KT, int NK, int KB, bool CNT = false>
 struct ProbeFnT {
   DCol cols[SX_MAX_COLS];
   DPred preds[SX_MAX_PREDS];
@@ -43,7 +43,8 @@ struct ProbeFnT {
   uint32_t mask;
   int anti;
   int member_only;     // semi/anti: membership is the whole answer
-  int count_all;       // inner join on a non-unique build: aux = number of matches (scan to EMPTY)
+  // CNT: inner join on a non-unique build: aux = number of matches (scan to the first EMPTY)
+  static constexpr bool count_all = CNT;
   const uint32_t* bm;  // optional exact key-range bitmap of the build side
   long long bm_min;
   unsigned long long bm_bits;
@@ -114,7 +115,7 @@ struct ProbeFnT {
           bool e0 = r0 == 0xffffffffu && !first[i], e1 = r1 == 0xffffffffu;
           bool m0 = r0 != 0xffffffffu && !first[i] && (uint32_t)s[i].x == (uint32_t)key[i];
           bool m1 = !e0 && r1 != 0xffffffffu && (uint32_t)s[i].y == (uint32_t)key[i];
-          if (count_all) {  // every match up to the first EMPTY slot
+          if constexpr (CNT) {  // every match up to the first EMPTY slot
             cnt[i] += (m0 ? 1 : 0) + (m1 ? 1 : 0);
             pend[i] = !(e0 || e1);
           } else {
@@ -142,7 +143,7 @@ struct ProbeFnT {
           if (!pend[i]) continue;
           uint32_t rw = (uint32_t)(unsigned long long)s[i].y;
           bool empty = rw == 0xffffffffu, hit = !empty && (uint64_t)s[i].x == key[i];
-          if (count_all) {
+          if constexpr (CNT) {
             cnt[i] += hit ? 1 : 0;
             pend[i] = !empty;
           } else {
@@ -155,7 +156,7 @@ struct ProbeFnT {
         }
       }
     }
-    if (count_all) {
+    if constexpr (CNT) {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         alive[i] = alive[i] && cnt[i] > 0;
