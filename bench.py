@@ -70,17 +70,6 @@ def query_bytes(n: dict) -> dict:
     }
 
 
-# dominant-operator algorithmic bytes (per launch of that operator inside its query)
-def op_bytes(name: str, n: dict) -> int | None:
-    kb = n["kb"]
-    table = {
-        "Q1/groupby": n["l"] * 38,
-        "Q6/groupby": n["l"] * 28,
-        "Q18/groupby": n["l"] * (kb + 8) + 2 * n["o"] * (kb + 8),
-    }
-    return table.get(name)
-
-
 # ---------------------------------------------------------------------------------- clocks
 class ClockSampler:
     def __init__(self, gpu: int):
@@ -166,7 +155,8 @@ def main():
     ap.add_argument("--sf", type=float, default=100.0)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--impl", default="sx", choices=["sx", "reference"])
-    ap.add_argument("--cpu-sf", type=float, default=1.0, help="oracle sample scale factor")
+    ap.add_argument("--cpu-sf", type=float, default=10.0, help="oracle sample scale factor (cpu_baseline)")
+    ap.add_argument("--ref-sf", type=float, default=1.0, help="oracle sample scale factor per step (--impl reference)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -179,6 +169,8 @@ def main():
     cpu_milli = gen.sf_to_milli(args.cpu_sf)
 
     if args.impl == "reference":
+        cpu_milli = gen.sf_to_milli(args.ref_sf)
+        args.cpu_sf = args.ref_sf
         if rank != 0:
             return
         reps = args.warmup + args.steps
@@ -283,7 +275,7 @@ def main():
         if dist:
             dist.barrier()
     launches = sx.lib().sx_launch_count(ctx.h, 1)
-    prof = ctx.profile_read()
+    prof = ctx.profile_read(with_bytes=True)
     ctx.profile(False)
     ms = e0.elapsed_time(e1) / args.steps
     if dist:
@@ -292,45 +284,49 @@ def main():
         ms = float(t.item())
     value = job_bytes / (ms / 1e3) / 1e9
 
-    # per-operator breakdown (query-level entries and operator entries in call order)
+    # per-operator breakdown (query-level entries and operator entries in call order); every sx call
+    # reports its algorithmic bytes (SURVEY §8(d) definition 1) beside its CUDA-event time
     per_q = {q.upper(): [] for q in QUERIES}
-    ops = {}
+    ops, op_b = {}, {}
     cur = None
     # profile records are pushed at scope entry: query scope first, then its operator calls
-    for name, t in prof:
+    for name, t, b in prof:
         if name in per_q:
             per_q[name].append(t)
             cur = name
         else:
             key = f"{cur}/{name}"
             ops.setdefault(key, []).append(t)
+            op_b.setdefault(key, []).append(b)
     q_ms = {q: round(statistics.mean(v), 4) for q, v in per_q.items() if v}
     op_ms = {k: round(sum(v) / args.steps, 4) for k, v in ops.items()}
-    dom = max(op_ms, key=op_ms.get) if op_ms else None
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    peak_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "of fallback (B200_PROFILING.md 6.65 TB/s)"
+    # per-operator achieved algorithmic GB/s and fraction of the HBM peak
+    op_gbs = {k: {"ms": op_ms[k], "gb": round(sum(op_b[k]) / args.steps / 1e9, 4),
+                  "gbs": round(sum(op_b[k]) / (sum(ops[k]) / 1e3) / 1e9, 1) if sum(ops[k]) > 0 else None}
+              for k in ops}
+    for v in op_gbs.values():
+        v["frac"] = round(v["gbs"] / peak, 4) if v["gbs"] is not None else None
+    dom = max(op_ms, key=op_ms.get) if op_ms else None
     roof = None
     if dom:
-        ob = op_bytes(dom, n)
         calls = len(ops[dom]) / args.steps
         dur = op_ms[dom] / max(calls, 1)
+        ob = sum(op_b[dom]) / len(op_b[dom])
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get(dom)
-        if ob:
-            ach = ob / (dur / 1e3) / 1e9
-            roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(ach / peak, 4), "traffic": traffic, "algorithmic_bytes": ob,
-                    "ms_per_launch": round(dur, 4), "peak_source": peak_src}
-        else:
-            roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
-                    "traffic": traffic}
+        ach = ob / (dur / 1e3) / 1e9 if ob > 0 else None
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1) if ach else None, "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4) if ach else None, "traffic": traffic, "algorithmic_bytes": round(ob),
+                "ms_per_launch": round(dur, 4), "peak_source": peak_src}
 
     # e2e: public C-ABI call with host (pinned) inputs; H2D + queries + result D2H timed
     e2e = None
@@ -390,7 +386,7 @@ def main():
                        "sf_total": sf_total / 1000, "job_bytes_per_step": job_bytes,
                        "parallelism": (f"sharded x{world}: rank r holds shard r of SF{sf_total / 1000:g}; "
                                        "allgather/shuffle over NCCL" if world > 1 else "single GPU")},
-            "query_ms": q_ms, "operator_ms": op_ms, "parity": parity,
+            "query_ms": q_ms, "operator_ms": op_ms, "operator_roofline": op_gbs, "parity": parity,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

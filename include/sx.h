@@ -95,8 +95,10 @@ sx_status sx_memcpy(sx_ctx* ctx, void* dst, const void* src, size_t bytes);
 int64_t sx_launch_count(sx_ctx* ctx, int reset);
 /* Per-operator device timing (CUDA events around each sx_* call; Fig. 5 analog). */
 sx_status sx_profile_enable(sx_ctx* ctx, int on);
-/* Fills up to cap entries of (name, milliseconds) for calls since the last read; returns count in *n. */
-sx_status sx_profile_read(sx_ctx* ctx, char (*names)[32], float* ms, int cap, int* n);
+/* Fills up to cap entries of (name, milliseconds, algorithmic bytes) for calls since the last read
+ * (bytes: SURVEY §8(d) definition 1 — referenced input columns once at stored width + mandatory
+ * outputs once; 0 where a call does not define it; `bytes` may be NULL); returns count in *n. */
+sx_status sx_profile_read(sx_ctx* ctx, char (*names)[32], float* ms, double* bytes, int cap, int* n);
 
 /* ---- value expressions ------------------------------------------------------
  * value(r) = sum over t < nterms of coef_t * prod over f < nf_t of (mul_f * cols[col_f][r] + add_f).

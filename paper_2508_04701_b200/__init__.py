@@ -272,13 +272,16 @@ class Ctx:
     def profile(self, on: bool = True):
         self.check(self.L.sx_profile_enable(self.h, 1 if on else 0))
 
-    def profile_read(self):
+    def profile_read(self, with_bytes: bool = False):
+        """[(name, ms)] (or [(name, ms, algorithmic bytes)]) of the sx calls since the last read."""
         cap = 4096
         names = (C.c_char * 32 * cap)()
         ms = (C.c_float * cap)()
+        nb = (C.c_double * cap)()
         n = C.c_int()
-        self.check(self.L.sx_profile_read(self.h, names, ms, cap, C.byref(n)))
-        return [(bytes(names[i]).split(b"\0")[0].decode(), float(ms[i])) for i in range(n.value)]
+        self.check(self.L.sx_profile_read(self.h, names, ms, nb, cap, C.byref(n)))
+        out = [(bytes(names[i]).split(b"\0")[0].decode(), float(ms[i]), float(nb[i])) for i in range(n.value)]
+        return out if with_bytes else [o[:2] for o in out]
 
 
 class HashTable:

@@ -138,7 +138,7 @@ def load(path: str = LIB_PATH):
     L.sx_profile_enable.argtypes = [vp, i32]
     L.sx_launch_count.argtypes = [vp, i32]
     L.sx_launch_count.restype = i64
-    L.sx_profile_read.argtypes = [vp, vp, vp, i32, P(C.c_int)]
+    L.sx_profile_read.argtypes = [vp, vp, vp, vp, i32, P(C.c_int)]
     L.sx_filter.argtypes = [vp, P(Col), i32, P(Pred), i32, P(Sel), vp, i32, P(Sel), P(Col)]
     L.sx_groupby_agg.argtypes = [vp, P(Col), i32, P(Key), i32, P(Sel), P(Pred), i32, P(Agg), i32, P(Having), i64,
                                  P(Col), P(Col), P(C.c_int64)]

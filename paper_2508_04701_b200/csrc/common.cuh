@@ -35,7 +35,7 @@ struct sx_ctx {
   int64_t* h_pinned = nullptr;     // pinned host scratch for size reads (64 entries)
   bool profile = false;
   int64_t launches = 0;            // kernels launched by libsx on this ctx (sx_launch_count)
-  struct Prof { char name[32]; cudaEvent_t a, b; };
+  struct Prof { char name[32]; cudaEvent_t a, b; double bytes; };
   std::vector<Prof> prof;
 };
 
@@ -131,6 +131,7 @@ struct ProfScope {
     if (!c->profile) return;
     sx_ctx::Prof p;
     snprintf(p.name, sizeof p.name, "%s", name);
+    p.bytes = 0;
     cudaEventCreate(&p.a);
     cudaEventCreate(&p.b);
     cudaEventRecord(p.a, c->stream);
@@ -139,6 +140,11 @@ struct ProfScope {
   }
   ~ProfScope() {
     if (idx >= 0) cudaEventRecord(ctx->prof[idx].b, ctx->stream);
+  }
+  bool on() const { return idx >= 0; }
+  // Algorithmic bytes of this call (SURVEY §8(d) "Bytes definitions" 1).
+  void set_bytes(double b) {
+    if (idx >= 0) ctx->prof[idx].bytes = b;
   }
 };
 
@@ -151,6 +157,21 @@ inline int type_width(int t) {
     default: return 0;
   }
 }
+// Referenced-column set of one call, for its algorithmic bytes (SURVEY §8(d) definition 1:
+// each referenced input column read once at its stored width).
+struct RefCols {
+  bool used[SX_MAX_COLS] = {};
+  void add(int c) {
+    if (c >= 0 && c < SX_MAX_COLS) used[c] = true;
+  }
+  double row_bytes(const sx_col* cols, int ncols) const {
+    double b = 0;
+    for (int c = 0; c < ncols && c < SX_MAX_COLS; ++c)
+      if (used[c]) b += cols[c].type == SX_STR ? 8.0 : (double)type_width(cols[c].type);
+    return b;
+  }
+};
+
 inline bool is_int_type(int t) {
   return t == SX_U8 || t == SX_I32 || t == SX_DATE32 || t == SX_I64 || t == SX_DEC64;
 }

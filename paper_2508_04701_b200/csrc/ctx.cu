@@ -87,7 +87,7 @@ SX_EXPORT sx_status sx_profile_enable(sx_ctx* ctx, int on) {
   return SX_OK;
 }
 
-SX_EXPORT sx_status sx_profile_read(sx_ctx* ctx, char (*names)[32], float* ms, int cap, int* n) {
+SX_EXPORT sx_status sx_profile_read(sx_ctx* ctx, char (*names)[32], float* ms, double* bytes, int cap, int* n) {
   if (!ctx || !n) return SX_EINVAL;
   SX_CUDA(cudaStreamSynchronize(ctx->stream));
   int k = 0;
@@ -97,6 +97,7 @@ SX_EXPORT sx_status sx_profile_read(sx_ctx* ctx, char (*names)[32], float* ms, i
       cudaEventElapsedTime(&t, p.a, p.b);
       if (names) snprintf(names[k], 32, "%s", p.name);
       if (ms) ms[k] = t;
+      if (bytes) bytes[k] = p.bytes;
       ++k;
     }
     cudaEventDestroy(p.a);
@@ -143,6 +144,7 @@ SX_EXPORT sx_status sx_gather(sx_ctx* ctx, const sx_col* col, const sx_sel* sel,
   *out = *col;
   out->len = n;
   out->data = dst;
+  ps.set_bytes((4.0 + 2.0 * w) * n);  // selection + referenced rows read + output written
   return SX_OK;
 }
 

@@ -90,5 +90,23 @@ SX_EXPORT sx_status sx_filter(sx_ctx* ctx, const sx_col* cols, int ncols, const 
   *out_sel = sx_sel{0, nullptr};
   for (int g = 0; g < ngather && g < kMaxGather; ++g) out_cols[g] = sx_col{};
   ProfScope ps(ctx, "filter");
-  return filter_internal(ctx, cols, ncols, conj, npred, in_sel, gather_cols, ngather, out_sel, out_cols);
+  sx_status st = filter_internal(ctx, cols, ncols, conj, npred, in_sel, gather_cols, ngather, out_sel, out_cols);
+  if (st == SX_OK && ps.on()) {  // predicate columns + selection in + sel out (+ gathered, read and written)
+    int64_t n = in_sel ? in_sel->len : (npred > 0 ? cols[conj[0].col].len : (ncols > 0 ? cols[0].len : 0));
+    RefCols rc;
+    double b = in_sel ? 4.0 * n : 0.0;
+    for (int p = 0; p < npred; ++p) {
+      rc.add(conj[p].col);
+      const sx_col& c = cols[conj[p].col];
+      if (c.type == SX_STR && n > 0) {  // string bytes of the scanned rows
+        int64_t hi = 0;
+        cudaMemcpy(&hi, c.offsets + c.len, sizeof hi, cudaMemcpyDeviceToHost);
+        b += (double)hi * n / (double)(c.len > 0 ? c.len : 1);
+      }
+    }
+    b += rc.row_bytes(cols, ncols) * n + 4.0 * out_sel->len;
+    for (int g = 0; g < ngather; ++g) b += 2.0 * type_width(cols[gather_cols[g]].type) * out_sel->len;
+    ps.set_bytes(b);
+  }
+  return st;
 }

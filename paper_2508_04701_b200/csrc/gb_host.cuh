@@ -386,7 +386,27 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
     SX_CUDA(cudaMemsetAsync(side, 0, nsub * sizeof(int), ctx->stream));
     Table t{table, keyless ? 0 : cap_p - 1, side, ctx->d_flags + 1};
     bool part_overflow = false;
-    if (n > 0 && small) {
+    bool dense_done = false;
+    if constexpr (has_dense<Prog>::value) {
+      // K9d: dense input + vector-loading program (see k_gb_dense); the grid must keep every
+      // thread at <= 2^21 rows so that its int64 partial sums of |v| < 2^41 values cannot overflow
+      if (n > 0 && small && !sel && L.nst == Prog::kDenseNst) {
+        size_t smem = dense_smem_bytes<Prog::kDenseNst>();
+        SX_CUDA(cudaFuncSetAttribute(k_gb_dense<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_dense<Prog>, kDenseThreads, smem));
+        if (per_sm < 1) per_sm = 1;
+        int64_t groups = (n + Prog::kDenseRows - 1) / Prog::kDenseRows;
+        int64_t ctas = std::min<int64_t>((int64_t)ctx->num_sms * per_sm, (groups + kDenseThreads - 1) / kDenseThreads);
+        if ((groups + ctas * kDenseThreads - 1) / (ctas * kDenseThreads) * Prog::kDenseRows <= kDenseMaxRowsPerThread) {
+          k_gb_dense<Prog><<<(unsigned)ctas, kDenseThreads, smem, SX_STREAM(ctx)>>>(prog, n, L, t);
+          SX_CHECK_LAUNCH();
+          dense_done = true;
+        }
+      }
+    }
+    if (dense_done) {
+    } else if (n > 0 && small) {
       size_t smem = small_smem_bytes(L.nst);
       SX_CUDA(cudaFuncSetAttribute(k_gb_small<Prog, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0;

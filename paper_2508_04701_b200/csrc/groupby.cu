@@ -36,5 +36,19 @@ SX_EXPORT sx_status sx_groupby_agg(sx_ctx* ctx, const sx_col* cols, int ncols, c
   InterpProg prog;
   prog.A = A;
   prog.ovf_flag = ctx->d_flags;
-  return gb_run(ctx, prog, plan, in_sel ? in_sel->idx : nullptr, n, groups_hint, out_keys, out_aggs, out_ngroups);
+  sx_status st = gb_run(ctx, prog, plan, in_sel ? in_sel->idx : nullptr, n, groups_hint, out_keys, out_aggs, out_ngroups);
+  if (st == SX_OK && ps.on()) {  // referenced columns + selection once; the G output rows once
+    RefCols rc;
+    for (int k = 0; k < nkeys; ++k) rc.add(keys[k].col);
+    for (int p = 0; p < nwhere; ++p) rc.add(where[p].col);
+    for (int a = 0; a < naggs; ++a)
+      if (aggs[a].op != SX_COUNT)
+        for (int t = 0; t < aggs[a].value.nterms && t < 2; ++t)
+          for (int f = 0; f < aggs[a].value.t[t].nf && f < 3; ++f) rc.add(aggs[a].value.t[t].f[f].col);
+    double out_row = 0;
+    for (int k = 0; k < nkeys; ++k) out_row += type_width(out_keys[k].type);
+    for (int a = 0; a < naggs; ++a) out_row += type_width(out_aggs[a].type);
+    ps.set_bytes((rc.row_bytes(cols, ncols) + (in_sel ? 4.0 : 0.0)) * n + out_row * (double)*out_ngroups);
+  }
+  return st;
 }

@@ -1093,3 +1093,176 @@ __global__ void __launch_bounds__(kSmallThreads, (P::kMaxNst <= 2 ? 2 : 1)) k_gb
 }
 
 }  // namespace sx
+
+namespace sx {
+
+// ------------------------------------------------------------------------------ K9d: small G, dense
+// Small-G aggregation over a dense (selection-free) input for compiled row programs that can load
+// kDenseRows consecutive rows with 128-bit vector loads (P::dense).  Versus k_gb_small:
+//  * every column is read with a few wide loads per thread (ld.global.nc.v4), all issued before
+//    any use, instead of one scalar load per row and column;
+//  * the program guards each row group: when every value lies in |v| < 2^41 (TPC-H decimals are
+//    far below: ext < 2^24, discount/tax < 2^7), the products are exact 32x32->64 multiplies and
+//    a thread's private int64 partial sums cannot overflow (at most 2^21 rows per thread, checked
+//    on the host: 2^21 * 2^41 = 2^62), so the 96-bit carry tracking of k_gb_small disappears from
+//    the per-row loop;
+//  * a group that fails the guard takes the exact slow path (the program's checked per-row
+//    evaluation into the global table, as in k_gb_small).
+// Results are identical to k_gb_small's: integer sums are exact in either path.
+constexpr int kDenseThreads = 256;
+constexpr int64_t kDenseMaxRowsPerThread = 1 << 21;
+
+template <int NST>
+inline size_t dense_smem_bytes() {
+  return (size_t)(kSmallSlots + 1) * NST * kDenseThreads * sizeof(long long);
+}
+
+// Exact slow path for one row (checked arithmetic, global table); out of line.
+template <class P>
+static __device__ __noinline__ void gb_dense_slow_row(const P& prog, const Table& t, const Layout& L, int32_t r,
+                                                      bool& ovf) {
+  int32_t rr[1] = {r};
+  bool al[1] = {true};
+  uint64_t k[1];
+  typename P::template Cache<1> c;
+  prog.template where_keys<1>(rr, al, k, c);
+  if (!al[0]) return;
+  for (int a = 0; a < L.nst; ++a) {
+    int64_t v[1] = {1};
+    if (prog.kind(a, L) != ST_COUNT) prog.template state<1>(a, rr, al, c, v, ovf);
+    gb_row_to_global(t, L, k[0], a, v[0]);
+  }
+}
+
+template <class P>
+__global__ void __launch_bounds__(kDenseThreads, 2) k_gb_dense(const __grid_constant__ P prog, int64_t n,
+                                                               const __grid_constant__ Layout L, Table t) {
+  constexpr int NST = P::kDenseNst;
+  constexpr int R = P::kDenseRows;
+  extern __shared__ long long dacc[];  // [(kSmallSlots + 1) * NST][nthreads], lane-private columns
+  __shared__ unsigned long long ct_key[kCtaTable];
+  __shared__ int ct_used[kCtaTable];
+  __shared__ unsigned long long ct_lo[kCtaTable][NST];
+  __shared__ int ct_hi[kCtaTable][NST];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int j = 0; j < (kSmallSlots + 1) * NST; ++j) dacc[j * nt + tid] = 0;
+  for (int j = tid; j < kCtaTable; j += nt) {
+    ct_used[j] = 0;
+    ct_key[j] = 0;
+    for (int a = 0; a < NST; ++a) { ct_lo[j][a] = 0; ct_hi[j][a] = 0; }
+  }
+  uint64_t skey[kSmallSlots];
+  unsigned used = 0;
+#pragma unroll
+  for (int k = 0; k < kSmallSlots; ++k) skey[k] = 0;
+  bool ovf = false;
+  const int64_t ngroups = (n + R - 1) / R;
+  for (int64_t g = blockIdx.x * (int64_t)nt + tid; g < ngroups; g += (int64_t)gridDim.x * nt) {
+    const int64_t r0 = g * R;
+    bool alive[R];
+    uint64_t key[R];
+    int64_t v[R][NST];
+    bool fast = true;
+    prog.template dense<R>(r0, n, alive, key, v, fast);
+    if (!fast) {
+      for (int i = 0; i < R; ++i)
+        if (r0 + i < n) gb_dense_slow_row(prog, t, L, (int32_t)(r0 + i), ovf);
+      continue;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      int s = -1;
+#pragma unroll
+      for (int k = 0; k < kSmallSlots; ++k)
+        if (((used >> k) & 1u) && skey[k] == key[i]) s = k;
+      if (alive[i] && s < 0 && used != (1u << kSmallSlots) - 1) {
+        s = __ffs(~used) - 1;
+#pragma unroll
+        for (int k = 0; k < kSmallSlots; ++k)
+          if (k == s) skey[k] = key[i];
+        used |= 1u << s;
+      }
+      if (alive[i] && s < 0) {  // more distinct keys than register slots: exact global path
+        for (int a = 0; a < NST; ++a) gb_row_to_global(t, L, key[i], a, v[i][a]);
+        continue;
+      }
+      const int cell = (alive[i] ? s : kSmallSlots) * NST * nt + tid;
+#pragma unroll
+      for (int a = 0; a < NST; ++a) {
+        const int kd = prog.kind(a, L);
+        long long* p = dacc + cell + a * nt;
+        if (kd == ST_SUM || kd == ST_COUNT) {
+          *p += v[i][a];
+        } else {
+          unsigned long long u = kd == ST_MIN ? ~order_u(v[i][a]) : order_u(v[i][a]);
+          *p = (long long)(u > (unsigned long long)*p ? u : (unsigned long long)*p);
+        }
+      }
+    }
+  }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
+  __syncthreads();
+  // CTA merge (shared table, smem atomics; 96-bit sums), then one global update per CTA entry
+#pragma unroll
+  for (int k = 0; k < kSmallSlots; ++k) {
+    if (!((used >> k) & 1u)) continue;
+    uint64_t key = skey[k];
+    int e = (int)(hash64(key) & (kCtaTable - 1)), found = -1;
+    for (int probe = 0; probe < kCtaTable; ++probe) {
+      int u = atomicCAS(&ct_used[e], 0, 1);
+      if (u == 0) {
+        atomicExch(&ct_key[e], (unsigned long long)key);
+        atomicExch(&ct_used[e], 2);
+        found = e;
+        break;
+      }
+      while (*(volatile int*)&ct_used[e] == 1) {
+      }
+      if (*(volatile unsigned long long*)&ct_key[e] == key) { found = e; break; }
+      e = (e + 1) & (kCtaTable - 1);
+    }
+    for (int a = 0; a < NST; ++a) {
+      const long long sv = dacc[(k * NST + a) * nt + tid];
+      const unsigned long long val = (unsigned long long)sv;
+      const int kd = L.kind[a];
+      const int hv = (kd == ST_SUM && sv < 0) ? -1 : 0;
+      if (found < 0) {
+        uint8_t* p = find_or_insert(t, L, key);
+        if (!p) continue;
+        if (kd == ST_SUM || kd == ST_COUNT) apply_state(p, L, a, val, hv);
+        else atomicMax((unsigned long long*)(p + L.off8[a]), val);
+        continue;
+      }
+      if (kd == ST_SUM) {
+        unsigned long long old = atomicAdd(&ct_lo[found][a], val);
+        int h = hv + ((old + val) < old ? 1 : 0);
+        if (h) atomicAdd(&ct_hi[found][a], h);
+      } else if (kd == ST_COUNT) {
+        atomicAdd(&ct_lo[found][a], val);
+      } else {
+        atomicMax(&ct_lo[found][a], val);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < kCtaTable; e += nt) {
+    if (ct_used[e] != 2) continue;
+    uint8_t* p = find_or_insert(t, L, ct_key[e]);
+    if (!p) continue;
+    for (int a = 0; a < NST; ++a) {
+      const int kd = L.kind[a];
+      if (kd == ST_SUM) atomic_add_sum96((unsigned long long*)(p + L.off8[a]), (int*)(p + L.off4[a]),
+                                         (int64_t)ct_lo[e][a], ct_hi[e][a]);
+      else if (kd == ST_COUNT) atomicAdd((unsigned long long*)(p + L.off8[a]), ct_lo[e][a]);
+      else atomicMax((unsigned long long*)(p + L.off8[a]), ct_lo[e][a]);
+    }
+  }
+}
+
+// Detection of the dense interface (programs without it keep k_gb_small).
+template <class P, class = void>
+struct has_dense : std::false_type {};
+template <class P>
+struct has_dense<P, std::void_t<decltype(P::kDenseNst)>> : std::true_type {};
+
+}  // namespace sx

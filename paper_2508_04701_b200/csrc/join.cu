@@ -356,6 +356,12 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
     }
   }
   *out = ht;
+  if (ps.on()) {  // key (+ predicate) columns of the scanned rows, selection, one slot per inserted row
+    RefCols rc;
+    for (int k = 0; k < nkeys; ++k) rc.add(key_cols[k]);
+    for (int p = 0; p < nwhere; ++p) rc.add(where[p].col);
+    ps.set_bytes((rc.row_bytes(cols, ncols) + (in_sel ? 4.0 : 0.0)) * n + (double)slot_bytes * ht->rows);
+  }
   return SX_OK;
 }
 
@@ -551,6 +557,15 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     out_payload[g].data = gs.g[g].dst;
     out_payload[g].offsets = nullptr;
     scr.release(gs.g[g].dst);
+  }
+  if (ps.on()) {  // probe keys (+ predicate columns) + selection in; row ids out; payload read + written
+    RefCols rc;
+    for (int k = 0; k < nkeys; ++k) rc.add(key_cols[k]);
+    for (int p = 0; p < nwhere; ++p) rc.add(where[p].col);
+    double b = (rc.row_bytes(probe_cols, nprobe_cols) + (in_sel ? 4.0 : 0.0)) * n;
+    b += (join_type == SX_INNER ? 8.0 : 4.0) * count;
+    for (int g = 0; g < gs.n; ++g) b += 2.0 * gs.g[g].width * count;
+    ps.set_bytes(b);
   }
   return SX_OK;
 }

@@ -297,6 +297,11 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
   if (in_sel) n = in_sel->len;
   if (n > INT32_MAX) return set_err(ctx, SX_EINDEX, "sort input exceeds INT32_MAX rows");
   int64_t outn = (k < 0 || k > n) ? n : k;
+  if (ps.on()) {  // key columns (+ selection) read once, permutation written once
+    double kw = 0;
+    for (int c = 0; c < nkeys; ++c) kw += type_width(cols[keys[c].col].type);
+    ps.set_bytes((kw + (in_sel ? 4.0 : 0.0)) * n + 4.0 * outn);
+  }
   Scratch scr(ctx);
   int32_t* perm;
   SX_TRY(scr.get(&perm, (size_t)(outn > 0 ? outn : 1)));

@@ -61,6 +61,74 @@ struct Q1Prog {
       c.tax[i] = alive[i] ? __ldg(tax + row[i]) : 0;
     }
   }
+  // Dense interface (k_gb_dense): 4 consecutive rows with 128-bit loads.  Guard: qty, ext < 2^26 and
+  // 0 <= disc, tax < 2^7 make every state |v| < 2^41 and the products exact as 32x32->64 multiplies
+  // (|ext*(100-disc)| < 2^33, |.. *(100+tax)| < 2^41); a group failing it takes the checked path.
+  static constexpr int kDenseNst = 6;
+  static constexpr int kDenseRows = 4;
+  template <int R>
+  __device__ __forceinline__ void dense(int64_t r0, int64_t n, bool (&alive)[R], uint64_t (&key)[R],
+                                        int64_t (&v)[R][kDenseNst], bool& fast) const {
+    static_assert(R == 4, "Q1Prog::dense loads 4 rows");
+    int32_t sd[4];
+    uint32_t f[4], s[4];
+    long long q[4], e[4], d[4], x[4];
+    if (r0 + 4 <= n) {
+      const int4 a = __ldg((const int4*)(ship + r0));
+      const uint32_t fr = __ldg((const unsigned int*)(rf + r0)), lv = __ldg((const unsigned int*)(ls + r0));
+      longlong2 vq[2], ve[2], vd[2], vx[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        vq[j] = __ldg((const longlong2*)(qty + r0) + j);
+        ve[j] = __ldg((const longlong2*)(ext + r0) + j);
+        vd[j] = __ldg((const longlong2*)(disc + r0) + j);
+        vx[j] = __ldg((const longlong2*)(tax + r0) + j);
+      }
+      sd[0] = a.x; sd[1] = a.y; sd[2] = a.z; sd[3] = a.w;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        f[i] = (fr >> (8 * i)) & 0xffu;
+        s[i] = (lv >> (8 * i)) & 0xffu;
+        q[i] = (i & 1) ? vq[i >> 1].y : vq[i >> 1].x;
+        e[i] = (i & 1) ? ve[i >> 1].y : ve[i >> 1].x;
+        d[i] = (i & 1) ? vd[i >> 1].y : vd[i >> 1].x;
+        x[i] = (i & 1) ? vx[i >> 1].y : vx[i >> 1].x;
+        alive[i] = true;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        alive[i] = r0 + i < n;
+        const int64_t r = alive[i] ? r0 + i : r0;
+        sd[i] = alive[i] ? __ldg(ship + r) : 0;
+        f[i] = alive[i] ? __ldg(rf + r) : 0;
+        s[i] = alive[i] ? __ldg(ls + r) : 0;
+        q[i] = alive[i] ? __ldg(qty + r) : 0;
+        e[i] = alive[i] ? __ldg(ext + r) : 0;
+        d[i] = alive[i] ? __ldg(disc + r) : 0;
+        x[i] = alive[i] ? __ldg(tax + r) : 0;
+      }
+    }
+    unsigned long long u = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      alive[i] = alive[i] && sd[i] <= ship_max;
+      key[i] = ((uint64_t)f[i] << 32) | s[i];
+      u |= (((unsigned long long)q[i] | (unsigned long long)e[i]) >> 26) |
+           (((unsigned long long)d[i] | (unsigned long long)x[i]) >> 7);
+    }
+    fast = u == 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long dp = (long long)(int32_t)e[i] * (long long)(100 - (int32_t)d[i]);
+      v[i][0] = q[i];
+      v[i][1] = e[i];
+      v[i][2] = dp;
+      v[i][3] = dp * (long long)(100 + (int32_t)x[i]);
+      v[i][4] = 1;
+      v[i][5] = d[i];
+    }
+  }
   template <int I>
   __device__ __forceinline__ void state(int a, const int32_t (&)[I], const bool (&)[I], const Cache<I>& c,
                                         int64_t (&v)[I], bool& ovf) const {
@@ -122,6 +190,62 @@ struct Q6Prog {
                                         int64_t (&v)[I], bool& ovf) const {
 #pragma unroll
     for (int i = 0; i < I; ++i) v[i] = a == 0 ? mul_ck(c.ext[i], c.disc[i], ovf) : 1;
+  }
+  // Dense interface (k_gb_dense): shipdate for 8 rows first (2 x 128-bit); discount, quantity and
+  // extendedprice are then loaded per row pair only where a shipdate qualifies (one dependent
+  // level; ~15% of rows pass the date range).  Guard: ext < 2^26, 0 <= disc < 2^14 on qualifying
+  // rows make ext*disc < 2^40 an exact 32x32->64 product.
+  static constexpr int kDenseNst = 2;
+  static constexpr int kDenseRows = 8;
+  template <int R>
+  __device__ __forceinline__ void dense(int64_t r0, int64_t n, bool (&alive)[R], uint64_t (&key)[R],
+                                        int64_t (&v)[R][kDenseNst], bool& fast) const {
+    static_assert(R == 8, "Q6Prog::dense loads 8 rows");
+    int32_t sd[8];
+    long long q[8], e[8], d[8];
+    const bool full = r0 + 8 <= n;
+    if (full) {
+      const int4 a = __ldg((const int4*)(ship + r0)), b = __ldg((const int4*)(ship + r0 + 4));
+      sd[0] = a.x; sd[1] = a.y; sd[2] = a.z; sd[3] = a.w;
+      sd[4] = b.x; sd[5] = b.y; sd[6] = b.z; sd[7] = b.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) alive[i] = sd[i] >= date_lo && sd[i] < date_hi;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool need = alive[2 * j] || alive[2 * j + 1];
+        const longlong2 z = make_longlong2(0, 0);
+        const longlong2 dd = need ? __ldg((const longlong2*)(disc + r0) + j) : z;
+        const longlong2 qq = need ? __ldg((const longlong2*)(qty + r0) + j) : z;
+        const longlong2 ee = need ? __ldg((const longlong2*)(ext + r0) + j) : z;
+        d[2 * j] = dd.x; d[2 * j + 1] = dd.y;
+        q[2 * j] = qq.x; q[2 * j + 1] = qq.y;
+        e[2 * j] = ee.x; e[2 * j + 1] = ee.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool in = r0 + i < n;
+        const int64_t r = in ? r0 + i : r0;
+        sd[i] = in ? __ldg(ship + r) : 0;
+        alive[i] = in && sd[i] >= date_lo && sd[i] < date_hi;
+        d[i] = alive[i] ? __ldg(disc + r) : 0;
+        q[i] = alive[i] ? __ldg(qty + r) : 0;
+        e[i] = alive[i] ? __ldg(ext + r) : 0;
+      }
+    }
+    unsigned long long u = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      alive[i] = alive[i] && d[i] >= disc_lo && d[i] <= disc_hi && q[i] < qty_lt;
+      key[i] = 0;
+      u |= alive[i] ? ((unsigned long long)e[i] >> 26) | ((unsigned long long)d[i] >> 14) : 0ull;
+    }
+    fast = u == 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i][0] = (long long)(int32_t)e[i] * (long long)(int32_t)d[i];
+      v[i][1] = 1;
+    }
   }
 };
 
@@ -359,6 +483,7 @@ SX_EXPORT sx_status sx_tpch_q1(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
                 (const long long*)t->l_extendedprice.data, (const long long*)t->l_discount.data,
                 (const long long*)t->l_tax.data, p->q1_shipdate_max, ctx->d_flags};
     SX_TRY(gb_run(ctx, prog, plan, nullptr, t->l_shipdate.len, 4, ok, oa, &ng));
+    pg.set_bytes(38.0 * t->l_shipdate.len + (2 + 4 * 16 + 3 * 8 + 8) * (double)ng);  // 7 columns once + G rows
   } else {
     SX_TRY(sx_groupby_agg(ctx, cols, 7, keys, 2, nullptr, &where, 1, aggs, 8, nullptr, 4, ok, oa, &ng));
   }
@@ -415,6 +540,7 @@ SX_EXPORT sx_status sx_tpch_q6(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
                 (const long long*)t->l_quantity.data, (const long long*)t->l_extendedprice.data, p->q6_date_lo,
                 p->q6_date_hi, p->q6_disc_lo, p->q6_disc_hi, p->q6_qty_lt, ctx->d_flags};
     SX_TRY(gb_run(ctx, prog, plan, nullptr, t->l_shipdate.len, 1, nullptr, oa, &ng));
+    pg.set_bytes(28.0 * t->l_shipdate.len + 24.0);  // 4 columns once + the result
   } else {
     SX_TRY(sx_groupby_agg(ctx, cols, 4, nullptr, 0, nullptr, where, 4, aggs, 2, nullptr, 1, nullptr, oa, &ng));
   }
@@ -594,6 +720,7 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     Q9Prog prog{(const int32_t*)L5[0].data, (const long long*)L5[1].data, (const long long*)L5[2].data,
                 (const long long*)L5[3].data, (const long long*)L5[4].data, (const int32_t*)L5[5].data, ctx->d_flags};
     SX_TRY(gb_run(ctx, prog, plan, nullptr, L5[0].len, 256, gok, goa, &ng));
+    pg.set_bytes(40.0 * L5[0].len + 24.0 * ng);  // 6 columns once + G rows
   } else {
     SX_TRY(sx_groupby_agg(ctx, L5, 6, gk, 2, nullptr, nullptr, 0, &ga, 1, nullptr, 256, gok, goa, &ng));
   }
@@ -659,6 +786,9 @@ SX_EXPORT sx_status sx_tpch_q18(sx_ctx* ctx, const sx_tpch_tables* t, const sx_t
       Q18Prog<long long> prog{(const long long*)t->l_orderkey.data, (const long long*)t->l_quantity.data, ctx->d_flags};
       SX_TRY(gb_run(ctx, prog, plan, nullptr, t->l_orderkey.len, t->o_orderkey.len, gok, goa, &ng));
     }
+    // key + qty once, and the per-order state (one row per order: key + sum) written and read once
+    const double kw = type_width(t->l_orderkey.type);
+    pg.set_bytes((kw + 8) * t->l_orderkey.len + 2.0 * (kw + 8) * t->o_orderkey.len);
   } else {
     SX_TRY(sx_groupby_agg(ctx, lcols, 2, &gk, 1, nullptr, nullptr, 0, &ga, 1, &hv, t->o_orderkey.len, gok, goa, &ng));
   }

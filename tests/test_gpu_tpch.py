@@ -111,3 +111,32 @@ def test_query_vs_committed_answers(ctx, sfm):
             want = [(oracle.c_name(r[0]),) + tuple(r) for r in want]
         got = T.run(q)
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
+
+
+@pytest.mark.parametrize("trunc", [0, 3, 5])
+def test_q1_q6_dense_guard_and_tails(ctx, trunc):
+    """The dense small-G kernel (k_gb_dense) vs the oracle where its fast-path guard fails
+    (ext >= 2^26, negative discount, tax >= 2^7: exact slow path), where a 5th/6th group key
+    appears (more keys than register slots: global path), and for row counts that are not a
+    multiple of the 4/8-row vector groups (scalar tail)."""
+    host = gen.cpu_tables(10, seed=7)
+    li = {k: v.copy() for k, v in host["lineitem"].items()}
+    n = len(li["l_shipdate"]) - trunc
+    li = {k: v[:n].copy() for k, v in li.items()}
+    rng = np.random.default_rng(3)
+    for col, val in (("l_extendedprice", 1 << 40), ("l_discount", -5), ("l_tax", 200), ("l_quantity", 1 << 30)):
+        idx = rng.choice(n, 7, replace=False)
+        li[col][idx] = val
+    li["l_returnflag"][rng.choice(n, 5, replace=False)] = ord("Z")
+    li["l_linestatus"][rng.choice(n, 5, replace=False)] = ord("Q")
+    # Q6 rows that pass the date/discount/quantity ranges but carry a huge extendedprice
+    ok = np.nonzero((li["l_shipdate"] >= 8766) & (li["l_shipdate"] < 9131) & (li["l_discount"] >= 5) &
+                    (li["l_discount"] <= 7) & (li["l_quantity"] < 2400))[0]
+    li["l_extendedprice"][ok[:3]] = (1 << 27) + 11
+    host = dict(host)
+    host["lineitem"] = li
+    T = tpch.Tpch(ctx, to_dev(host))
+    for q in ("q1", "q6"):
+        want = oracle.run_query(q, host)
+        got = T.run(q)
+        assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
