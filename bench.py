@@ -160,6 +160,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--workload", default="tpch", choices=["tpch", "join", "join-zipf", "groupby", "sort"],
+                    help="tpch (default): Q1+Q6+Q3+Q9+Q18 step; others: operator µbenchmarks (mbench.py)")
+    ap.add_argument("--mb-build-log2", type=int, default=27)
+    ap.add_argument("--mb-probe-log2", type=int, default=30)
+    ap.add_argument("--mb-gb-log2", type=int, default=30)
+    ap.add_argument("--mb-groups", default="", help="comma list of G (default 2^2..2^26)")
+    ap.add_argument("--mb-sort-log2", type=int, default=28)
     args = ap.parse_args()
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
@@ -167,6 +174,19 @@ def main():
 
     sf_milli = gen.sf_to_milli(args.sf)
     cpu_milli = gen.sf_to_milli(args.cpu_sf)
+
+    if args.workload != "tpch" and args.impl == "sx":
+        import mbench
+
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "of fallback (B200_PROFILING.md 6.65 TB/s)"
+        mbench.run(args, METRIC, ClockSampler, peak, src)
+        return
 
     if args.impl == "reference":
         cpu_milli = gen.sf_to_milli(args.ref_sf)

@@ -245,3 +245,97 @@ def to_device(tables: dict, device="cuda") -> dict:
 
     return {t: {c: torch.from_numpy(np.ascontiguousarray(a)).to(device) for c, a in cols.items()}
             for t, cols in tables.items()}
+
+
+# ---------------------------------------------------------------------------- operator µbenchmarks
+# C5a join (build 2^27 int64 key mix64(i) + payload i; probe keys from a uniform
+# or Zipf(1.0) rank through an affine permutation, payload j), C5b group-by sweep (int64 key
+# mix64(g), g ~ U[0, G); DEC64 value), and our sort µbench (uniform int64 keys + int32 payload).
+# Readings R15-R17.  Host arrays (numpy) or device tensors; rows [r0, r1) of the
+# infinite counter-based stream, so shards are contiguous row ranges.
+
+def _mb_cpu():
+    lib = cpu_lib()
+    if not hasattr(lib, "_mb_ready"):
+        i64, u64, vp, ci = ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int
+        lib.sxg_cpu_fill_mb_build.argtypes = [i64, i64, vp, vp]
+        lib.sxg_cpu_fill_mb_probe.argtypes = [u64, i64, ci, i64, i64, vp, vp]
+        lib.sxg_cpu_fill_mb_groupby.argtypes = [u64, i64, i64, i64, vp, vp]
+        lib.sxg_cpu_fill_mb_sort.argtypes = [u64, i64, i64, vp, vp]
+        lib.sxg_cpu_mb_probe_rank.argtypes = [u64, i64, i64, ci]
+        lib.sxg_cpu_mb_probe_rank.restype = i64
+        lib._mb_ready = True
+    return lib
+
+
+def _mb_gpu():
+    lib = gpu_lib()
+    if not hasattr(lib, "_mb_ready"):
+        i64, u64, vp, ci = ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int
+        lib.sxg_gpu_fill_mb_build.argtypes = [i64, i64, vp, vp, vp]
+        lib.sxg_gpu_fill_mb_probe.argtypes = [u64, i64, ci, i64, i64, vp, vp, vp]
+        lib.sxg_gpu_fill_mb_groupby.argtypes = [u64, i64, i64, i64, vp, vp, vp]
+        lib.sxg_gpu_fill_mb_sort.argtypes = [u64, i64, i64, vp, vp, vp]
+        for f in ("sxg_gpu_fill_mb_build", "sxg_gpu_fill_mb_probe", "sxg_gpu_fill_mb_groupby", "sxg_gpu_fill_mb_sort"):
+            getattr(lib, f).restype = ci
+        lib._mb_ready = True
+    return lib
+
+
+def _mb_arrays(n, dtypes, device):
+    if device is None:
+        return [np.empty(int(n), dtype=d) for d in dtypes]
+    import torch
+
+    tm = {np.int64: torch.int64, np.int32: torch.int32}
+    return [torch.empty(int(n), dtype=tm[d], device=device) for d in dtypes]
+
+
+def _mb_ptr(a):
+    return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
+
+
+def _mb_call(device, cpu_fn, gpu_fn, args, outs):
+    if device is None:
+        getattr(_mb_cpu(), cpu_fn)(*args, *[_mb_ptr(o) for o in outs])
+    else:
+        import torch
+
+        rc = getattr(_mb_gpu(), gpu_fn)(*args, *[_mb_ptr(o) for o in outs], torch.cuda.current_stream(device).cuda_stream)
+        if rc != 0:
+            raise RuntimeError(f"generator CUDA error {rc}")
+        torch.cuda.current_stream(device).synchronize()
+    return outs
+
+
+def mb_join_build(nb: int, r0: int = 0, r1: int | None = None, device=None):
+    """Build side rows [r0, r1): (key int64 = mix64(i), payload int64 = i)."""
+    r1 = nb if r1 is None else r1
+    outs = _mb_arrays(r1 - r0, [np.int64, np.int64], device)
+    return _mb_call(device, "sxg_cpu_fill_mb_build", "sxg_gpu_fill_mb_build", (r0, r1), outs)
+
+
+def mb_join_probe(nb: int, nprobe: int, zipf: bool, seed: int = 42, r0: int = 0, r1: int | None = None, device=None):
+    """Probe side rows [r0, r1): (key int64, payload int64 = j); nb a power of two."""
+    assert nb >= 2 and nb & (nb - 1) == 0
+    r1 = nprobe if r1 is None else r1
+    outs = _mb_arrays(r1 - r0, [np.int64, np.int64], device)
+    return _mb_call(device, "sxg_cpu_fill_mb_probe", "sxg_gpu_fill_mb_probe", (seed, nb, 1 if zipf else 0, r0, r1), outs)
+
+
+def mb_probe_rank(j: int, nb: int, zipf: bool, seed: int = 42) -> int:
+    return int(_mb_cpu().sxg_cpu_mb_probe_rank(seed, j, nb, 1 if zipf else 0))
+
+
+def mb_groupby(n: int, G: int, seed: int = 42, r0: int = 0, r1: int | None = None, device=None):
+    """Rows [r0, r1): (key int64 = mix64(g), value int64 DEC64 scale 2)."""
+    r1 = n if r1 is None else r1
+    outs = _mb_arrays(r1 - r0, [np.int64, np.int64], device)
+    return _mb_call(device, "sxg_cpu_fill_mb_groupby", "sxg_gpu_fill_mb_groupby", (seed, G, r0, r1), outs)
+
+
+def mb_sort(n: int, seed: int = 42, r0: int = 0, r1: int | None = None, device=None):
+    """Rows [r0, r1): (key int64 uniform, payload int32 = i)."""
+    r1 = n if r1 is None else r1
+    outs = _mb_arrays(r1 - r0, [np.int64, np.int32], device)
+    return _mb_call(device, "sxg_cpu_fill_mb_sort", "sxg_gpu_fill_mb_sort", (seed, r0, r1), outs)

@@ -125,3 +125,33 @@ EXPORT void sxg_cpu_fill_orders_lineitem(
 
 /* For generator tests: the nation/segment dictionaries and the word list. */
 EXPORT const char* sxg_cpu_word(int w) { return sxg_word(w); }
+
+/* ---- operator micro-benchmarks (rows [r0, r1)) ---- */
+EXPORT void sxg_cpu_fill_mb_build(int64_t r0, int64_t r1, int64_t* key, int64_t* payload) {
+  for (int64_t i = r0; i < r1; ++i) {
+    if (key) key[i - r0] = (int64_t)sxg_mb_build_key(i);
+    if (payload) payload[i - r0] = i;
+  }
+}
+EXPORT void sxg_cpu_fill_mb_probe(uint64_t seed, int64_t nb, int zipf, int64_t r0, int64_t r1, int64_t* key,
+                                  int64_t* payload) {
+  for (int64_t j = r0; j < r1; ++j) {
+    if (key) key[j - r0] = (int64_t)sxg_mb_probe_key(seed, j, nb, zipf);
+    if (payload) payload[j - r0] = j;
+  }
+}
+EXPORT void sxg_cpu_fill_mb_groupby(uint64_t seed, int64_t G, int64_t r0, int64_t r1, int64_t* key, int64_t* value) {
+  for (int64_t i = r0; i < r1; ++i) {
+    if (key) key[i - r0] = (int64_t)sxg_mix64((uint64_t)sxg_mb_gb_group(seed, i, G));
+    if (value) value[i - r0] = sxg_mb_gb_value(seed, i);
+  }
+}
+EXPORT void sxg_cpu_fill_mb_sort(uint64_t seed, int64_t r0, int64_t r1, int64_t* key, int32_t* payload) {
+  for (int64_t i = r0; i < r1; ++i) {
+    if (key) key[i - r0] = sxg_mb_sort_key(seed, i);
+    if (payload) payload[i - r0] = (int32_t)i;
+  }
+}
+EXPORT int64_t sxg_cpu_mb_probe_rank(uint64_t seed, int64_t j, int64_t nb, int zipf) {
+  return sxg_mb_probe_rank(seed, j, nb, zipf);
+}

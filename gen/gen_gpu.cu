@@ -231,3 +231,50 @@ EXPORT int sxg_gpu_fill_orders_lineitem(uint64_t seed, int64_t sf_milli, int64_t
         (int32_t*)l_orderkey, l_partkey, l_suppkey, l_quantity, l_ext, l_disc, l_tax, l_rf, l_ls, l_ship);
   return (int)cudaGetLastError();
 }
+
+// ---- operator micro-benchmarks (rows [r0, r1)) ----
+namespace {
+__global__ void k_mb_build(int64_t r0, int64_t n, int64_t* key, int64_t* payload) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (key) key[t] = (int64_t)sxg_mb_build_key(r0 + t);
+    if (payload) payload[t] = r0 + t;
+  }
+}
+__global__ void k_mb_probe(uint64_t seed, int64_t nb, int zipf, int64_t r0, int64_t n, int64_t* key, int64_t* payload) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (key) key[t] = (int64_t)sxg_mb_probe_key(seed, r0 + t, nb, zipf);
+    if (payload) payload[t] = r0 + t;
+  }
+}
+__global__ void k_mb_groupby(uint64_t seed, int64_t G, int64_t r0, int64_t n, int64_t* key, int64_t* value) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (key) key[t] = (int64_t)sxg_mix64((uint64_t)sxg_mb_gb_group(seed, r0 + t, G));
+    if (value) value[t] = sxg_mb_gb_value(seed, r0 + t);
+  }
+}
+__global__ void k_mb_sort(uint64_t seed, int64_t r0, int64_t n, int64_t* key, int32_t* payload) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (key) key[t] = sxg_mb_sort_key(seed, r0 + t);
+    if (payload) payload[t] = (int32_t)(r0 + t);
+  }
+}
+}  // namespace
+
+EXPORT int sxg_gpu_fill_mb_build(int64_t r0, int64_t r1, int64_t* key, int64_t* payload, cudaStream_t s) {
+  if (r1 > r0) k_mb_build<<<grid_for(r1 - r0), kThreads, 0, s>>>(r0, r1 - r0, key, payload);
+  return (int)cudaGetLastError();
+}
+EXPORT int sxg_gpu_fill_mb_probe(uint64_t seed, int64_t nb, int zipf, int64_t r0, int64_t r1, int64_t* key,
+                                 int64_t* payload, cudaStream_t s) {
+  if (r1 > r0) k_mb_probe<<<grid_for(r1 - r0), kThreads, 0, s>>>(seed, nb, zipf, r0, r1 - r0, key, payload);
+  return (int)cudaGetLastError();
+}
+EXPORT int sxg_gpu_fill_mb_groupby(uint64_t seed, int64_t G, int64_t r0, int64_t r1, int64_t* key, int64_t* value,
+                                   cudaStream_t s) {
+  if (r1 > r0) k_mb_groupby<<<grid_for(r1 - r0), kThreads, 0, s>>>(seed, G, r0, r1 - r0, key, value);
+  return (int)cudaGetLastError();
+}
+EXPORT int sxg_gpu_fill_mb_sort(uint64_t seed, int64_t r0, int64_t r1, int64_t* key, int32_t* payload, cudaStream_t s) {
+  if (r1 > r0) k_mb_sort<<<grid_for(r1 - r0), kThreads, 0, s>>>(seed, r0, r1 - r0, key, payload);
+  return (int)cudaGetLastError();
+}

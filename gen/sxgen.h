@@ -221,4 +221,60 @@ SXG_HD int64_t sxg_line_price_term(const sxg_line* L) {
   return ((L->extendedprice * (100 - L->discount)) / 100) * (100 + L->tax) / 100;
 }
 
+/* ---- operator micro-benchmarks (SURVEY.md §8(d) C5a/C5b and "(ours) sort µbench";
+ *      readings R15-R17 in DESIGN.md).  Table ids 16.. are outside the TPC-H range. ---- */
+enum { SXG_T_MB_PROBE = 16, SXG_T_MB_GB = 17, SXG_T_MB_SORT = 18, SXG_T_MB_PERM = 19 };
+
+/* join build row i (0 <= i < nb): key mix64(i), payload i (R15: PK side, unique keys). */
+SXG_HD uint64_t sxg_mb_build_key(int64_t i) { return sxg_mix64((uint64_t)i); }
+
+/* affine permutation of [0, nb), nb a power of two: pi(r) = (a r + b) mod nb, a odd (R16: hot
+ * ranks scatter over the table). */
+SXG_HD int64_t sxg_mb_perm(uint64_t seed, int64_t r, int64_t nb) {
+  uint64_t a = sxg_rand(seed, SXG_T_MB_PERM, 1, 0) | 1ull, b = sxg_rand(seed, SXG_T_MB_PERM, 2, 0);
+  return (int64_t)((a * (uint64_t)r + b) & (uint64_t)(nb - 1));
+}
+
+/* 2^(m/16) in 16.16 fixed point, m = 0..16 (integer literals: identical on CPU and GPU). */
+#define SXG_EXP2_16THS_INIT {65536, 68438, 71468, 74632, 77936, 81386, 84990, 88752, 92682, 96785, \
+                             101070, 105545, 110218, 115098, 120194, 125515, 131072}
+
+/* probe row j's rank in [0, nb): uniform, or Zipf(1.0) (R16) sampled as a log-uniform over
+ * 16 x log2(nb) equal-probability cells (sub-octaves [2^(k+m/16), 2^(k+(m+1)/16)) of r+1), uniform
+ * inside a cell: density of r+1 proportional to 1/(r+1) up to the cell discretisation.  Integer
+ * arithmetic only, so CPU and GPU draw identical ranks.  nb a power of two, 2 <= nb <= 2^32. */
+SXG_HD int64_t sxg_mb_probe_rank(uint64_t seed, int64_t j, int64_t nb, int zipf) {
+  uint64_t r0 = sxg_rand(seed, SXG_T_MB_PROBE, 1, (uint64_t)j);
+  if (!zipf) return sxg_uniform(r0, 0, nb - 1);
+  const uint32_t B[17] = SXG_EXP2_16THS_INIT;
+  int L = 0;
+  while ((1ll << L) < nb) ++L;
+  uint64_t c = ((r0 >> 32) * (uint64_t)(16 * L)) >> 32; /* cell in [0, 16L) */
+  int k = (int)(c >> 4), m = (int)(c & 15);
+  uint64_t lo = ((uint64_t)B[m] << k) >> 16, hi = ((uint64_t)B[m + 1] << k) >> 16;
+  if (hi <= lo) hi = lo + 1;
+  uint64_t r1 = sxg_rand(seed, SXG_T_MB_PROBE, 2, (uint64_t)j);
+  int64_t v = (int64_t)lo + (int64_t)(((r1 >> 32) * (hi - lo)) >> 32); /* r + 1 in [lo, hi) */
+  int64_t r = v - 1;
+  return r < 0 ? 0 : (r >= nb ? nb - 1 : r);
+}
+/* probe row j: key = build key of pi(rank), payload j (every probe matches exactly one build row). */
+SXG_HD uint64_t sxg_mb_probe_key(uint64_t seed, int64_t j, int64_t nb, int zipf) {
+  return sxg_mb_build_key(sxg_mb_perm(seed, sxg_mb_probe_rank(seed, j, nb, zipf), nb));
+}
+
+/* group-by sweep row i (R17): group g ~ U[0, G), key mix64(g) (int64), value DEC64 scale 2
+ * uniform in [1.00, 100000.00]. */
+SXG_HD int64_t sxg_mb_gb_group(uint64_t seed, int64_t i, int64_t G) {
+  return sxg_uniform(sxg_rand(seed, SXG_T_MB_GB, 1, (uint64_t)i), 0, G - 1);
+}
+SXG_HD int64_t sxg_mb_gb_value(uint64_t seed, int64_t i) {
+  return sxg_uniform(sxg_rand(seed, SXG_T_MB_GB, 2, (uint64_t)i), 100, 10000000);
+}
+
+/* sort µbench row i: a uniform int64 key (all 64 bits), payload i. */
+SXG_HD int64_t sxg_mb_sort_key(uint64_t seed, int64_t i) {
+  return (int64_t)sxg_rand(seed, SXG_T_MB_SORT, 1, (uint64_t)i);
+}
+
 #endif /* SXGEN_H */

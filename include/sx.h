@@ -191,6 +191,37 @@ sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* probe_cols, 
 int64_t sx_ht_rows(const sx_ht* ht);  /* build rows inserted */
 void sx_ht_destroy(sx_ctx* ctx, sx_ht* ht);
 
+/* ---- H5: radix partitioning and the partitioned join ---------------------------------
+ * (north_star: "radix-partitioned joins when the build side exceeds L2"; SURVEY §8(a) H5;
+ * PAPER.md P:351 names GPU join algorithms as techniques Sirius can adopt.)
+ * Partition of a key = (hash64(key) >> 48) & (2^bits - 1): hash bits 48..57, disjoint from the
+ * table-slot bits (low) and the shard-rank bits (top; reading R14).  Two 32-bit key columns are
+ * packed (k0 << 32) | k1 first (reading R11).  sx_radix_of is the host mirror. */
+uint32_t sx_radix_of(uint64_t key, int bits);
+/* Regroup the selected rows (in_sel, else all) of every column by partition, 1 <= bits <= 10:
+ * out_cols[c] = cols[c] with rows partition-contiguous (partition p at rows
+ * offsets[p] .. offsets[p+1]); order inside a partition is unspecified.  offsets: HOST array of
+ * 2^bits + 1 entries.  out_rows (optional): the original row id of every output row.  Keys: one
+ * I32/DATE32/I64 column or two 32-bit columns; carried columns: fixed-width, at most 12.
+ * Syncs once (offsets). */
+sx_status sx_radix_partition(sx_ctx* ctx, const sx_col* cols, int ncols, const int32_t* key_cols, int nkeys,
+                             const sx_sel* in_sel, int bits, sx_col* out_cols, sx_sel* out_rows,
+                             int64_t* offsets /* host */);
+/* Build + probe in one call.  strategy 1 = flat (sx_hash_build + sx_hash_probe, semantics and
+ * output order as there); 2 = radix-partitioned; 0 = automatic: partitioned when the flat table
+ * (2^ceil(log2(2 n_build)) slots of 8/16 B) would exceed half the L2 and the join is INNER on a
+ * unique build (unique_hint, the PK side), else flat.  Partitioned: both sides are partitioned
+ * carrying their key and payload columns (sx_radix_partition), then the partitions are joined in
+ * waves whose tables together fit half the L2.  Outputs as sx_hash_probe: out_payload[0..nbp) =
+ * build_cols[bp[i]] at the matches, then out_payload[nbp..nbp+npp) = probe_cols[pp[j]];
+ * out_probe / out_build (row ids; each may be NULL = not produced).  Partitioned output order is
+ * unspecified (a multiset, reading R12).  *used_strategy (optional) = 1 or 2.  Syncs (counts). */
+sx_status sx_hash_join(sx_ctx* ctx, const sx_col* build_cols, int nbuild_cols, const int32_t* build_keys,
+                       const sx_sel* build_sel, int unique_hint, const sx_col* probe_cols, int nprobe_cols,
+                       const int32_t* probe_keys, const sx_sel* probe_sel, int nkeys, int join_type,
+                       const int32_t* bp, int nbp, const int32_t* pp, int npp, int strategy, sx_sel* out_probe,
+                       sx_sel* out_build, sx_col* out_payload, int* used_strategy);
+
 /* ---- H9: sort / top-k ---------------------------------------------------------
  * Stable sort of the selected rows by the keys (each ascending, or descending if
  * desc); out_perm = the first min(k, n) row ids (k < 0: all).  Ties keep input

@@ -146,6 +146,14 @@ def lib():
         L.or_sort.restype = C.c_int64
         L.or_civil_year.argtypes = [C.c_int32]
         L.or_civil_year.restype = C.c_int32
+        L.or_unmix64.argtypes = [C.c_uint64]
+        L.or_unmix64.restype = C.c_uint64
+        L.or_pair_mix.argtypes = [C.c_int64, C.c_int64]
+        L.or_pair_mix.restype = C.c_uint64
+        L.or_mb_join_closed.argtypes = [C.c_int64, C.c_int64, _VP, _VP, P(JoinSummary)]
+        L.or_mb_join_hash.argtypes = [C.c_int64, _VP, _VP, C.c_int64, _VP, _VP, P(JoinSummary)]
+        L.or_mb_groupby_direct.argtypes = [C.c_int64, _VP, _VP, C.c_int64, _VP, _VP, _VP, _VP]
+        L.or_mb_groupby_direct.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -310,7 +318,8 @@ def join(build_keys, probe_keys, jtype: str):
     b = _c(build_keys, np.int64)
     p = _c(probe_keys, np.int64)
     t = {"inner": 0, "semi": 1, "anti": 2}[jtype]
-    cap = len(p) if t else max(1, len(p) * max(1, len(b)))
+    mult = int(np.unique(b, return_counts=True)[1].max()) if len(b) else 1  # pairs <= probes x max multiplicity
+    cap = len(p) if t else max(1, len(p) * mult)
     cap = max(cap, 1)
     op = np.empty(cap, np.int32)
     ob = np.empty(cap, np.int32)
@@ -365,3 +374,53 @@ def sort(keys, desc, k: int = -1) -> np.ndarray:
 
 def civil_year(days: int) -> int:
     return lib().or_civil_year(days)
+
+
+# ---------------------------------------------------------------------------- operator µbenchmarks
+class JoinSummary(C.Structure):
+    _fields_ = [("count", C.c_int64), ("sum_build", I128), ("sum_probe", I128), ("pair_hash", C.c_uint64)]
+
+
+def _summary(s: JoinSummary) -> dict:
+    return {"count": int(s.count), "sum_build": i128_to_int(s.sum_build), "sum_probe": i128_to_int(s.sum_probe),
+            "pair_hash": int(s.pair_hash)}
+
+
+def unmix64(z: int) -> int:
+    return int(lib().or_unmix64(z & (2**64 - 1)))
+
+
+def pair_mix(b: int, p: int) -> int:
+    return int(lib().or_pair_mix(b, p))
+
+
+def mb_join_closed(nb: int, pkeys: np.ndarray, ppay: np.ndarray) -> dict:
+    """Join µbench result summary by the closed form (build rows (mix64(i), i), i < nb)."""
+    pk, pp = np.ascontiguousarray(pkeys, np.int64), np.ascontiguousarray(ppay, np.int64)
+    s = JoinSummary()
+    lib().or_mb_join_closed(nb, len(pk), pk.ctypes.data, pp.ctypes.data, C.byref(s))
+    return _summary(s)
+
+
+def mb_join_hash(bkeys, bpay, pkeys, ppay) -> dict:
+    """Join µbench result summary by brute force (std::unordered_multimap)."""
+    bk, bp = np.ascontiguousarray(bkeys, np.int64), np.ascontiguousarray(bpay, np.int64)
+    pk, pp = np.ascontiguousarray(pkeys, np.int64), np.ascontiguousarray(ppay, np.int64)
+    s = JoinSummary()
+    lib().or_mb_join_hash(len(bk), bk.ctypes.data, bp.ctypes.data, len(pk), pk.ctypes.data, pp.ctypes.data,
+                          C.byref(s))
+    return _summary(s)
+
+
+def mb_groupby_direct(keys, vals, G: int) -> dict:
+    """Group-by µbench by direct array over g = mix64^-1(key): {g: (sum, count, min, max)} for present g."""
+    k, v = np.ascontiguousarray(keys, np.int64), np.ascontiguousarray(vals, np.int64)
+    sm = (I128 * G)()
+    cnt = np.zeros(G, np.int64)
+    mn = np.zeros(G, np.int64)
+    mx = np.zeros(G, np.int64)
+    r = lib().or_mb_groupby_direct(len(k), k.ctypes.data, v.ctypes.data, G, sm, cnt.ctypes.data, mn.ctypes.data,
+                                   mx.ctypes.data)
+    if r < 0:
+        raise ValueError("a key is not mix64(g) for g < G")
+    return {g: (i128_to_int(sm[g]), int(cnt[g]), int(mn[g]), int(mx[g])) for g in range(G) if cnt[g]}

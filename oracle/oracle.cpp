@@ -379,4 +379,76 @@ int64_t or_sort(int64_t n, const or_i128* const* keys, int32_t nkeys, const int3
   return m;
 }
 
+// ---- operator µbenchmarks (SURVEY §8(c) "µbench join" / "µbench group-by") -----------------------
+// splitmix64 finalizer z -> (z ^ z>>30) * C1 -> (. ^ .>>27) * C2 -> . ^ .>>31 is a bijection; its
+// inverse undoes each step: x ^ x>>s is inverted by x ^ x>>s ^ x>>2s ^ ..., multiplication by an
+// odd constant by its inverse mod 2^64.
+uint64_t or_unmix64(uint64_t z) {
+  z = z ^ (z >> 31) ^ (z >> 62);
+  z *= 0x319642b2d24d8ec3ULL;  // C2^-1 mod 2^64
+  z = z ^ (z >> 27) ^ (z >> 54);
+  z *= 0x96de1b173f119089ULL;  // C1^-1 mod 2^64
+  z = z ^ (z >> 30) ^ (z >> 60);
+  return z;
+}
+
+uint64_t or_pair_mix(int64_t b, int64_t p) {
+  uint64_t z = (uint64_t)b * 0x9e3779b97f4a7c15ULL ^ (uint64_t)p;
+  z = (z ^ (z >> 32)) * 0xd6e8feb86659fd93ULL;
+  return z ^ (z >> 32);
+}
+
+static void summary_add(or_join_summary* s, i128& sb, i128& sp, int64_t b, int64_t p) {
+  s->count += 1;
+  sb += b;
+  sp += p;
+  s->pair_hash += or_pair_mix(b, p);
+}
+
+void or_mb_join_closed(int64_t nb, int64_t np, const int64_t* pkeys, const int64_t* ppay, or_join_summary* out) {
+  std::memset(out, 0, sizeof *out);
+  i128 sb = 0, sp = 0;
+  for (int64_t j = 0; j < np; ++j) {
+    uint64_t i = or_unmix64((uint64_t)pkeys[j]);
+    if (i < (uint64_t)nb) summary_add(out, sb, sp, (int64_t)i, ppay[j]);
+  }
+  out->sum_build = pack(sb);
+  out->sum_probe = pack(sp);
+}
+
+void or_mb_join_hash(int64_t nb, const int64_t* bkeys, const int64_t* bpay, int64_t np, const int64_t* pkeys,
+                     const int64_t* ppay, or_join_summary* out) {
+  std::memset(out, 0, sizeof *out);
+  std::unordered_multimap<int64_t, int64_t> m;
+  m.reserve((size_t)nb);
+  for (int64_t i = 0; i < nb; ++i) m.emplace(bkeys[i], bpay[i]);
+  i128 sb = 0, sp = 0;
+  for (int64_t j = 0; j < np; ++j) {
+    auto r = m.equal_range(pkeys[j]);
+    for (auto it = r.first; it != r.second; ++it) summary_add(out, sb, sp, it->second, ppay[j]);
+  }
+  out->sum_build = pack(sb);
+  out->sum_probe = pack(sp);
+}
+
+int64_t or_mb_groupby_direct(int64_t n, const int64_t* keys, const int64_t* vals, int64_t G, or_i128* sum,
+                             int64_t* cnt, int64_t* mn, int64_t* mx) {
+  std::vector<i128> s((size_t)G, 0);
+  for (int64_t g = 0; g < G; ++g) { cnt[g] = 0; mn[g] = INT64_MAX; mx[g] = INT64_MIN; }
+  for (int64_t r = 0; r < n; ++r) {
+    uint64_t g = or_unmix64((uint64_t)keys[r]);
+    if (g >= (uint64_t)G) return -1;
+    s[g] += vals[r];
+    cnt[g] += 1;
+    mn[g] = std::min(mn[g], vals[r]);
+    mx[g] = std::max(mx[g], vals[r]);
+  }
+  int64_t present = 0;
+  for (int64_t g = 0; g < G; ++g) {
+    sum[g] = pack(s[(size_t)g]);
+    present += cnt[g] > 0;
+  }
+  return present;
+}
+
 }  // extern "C"

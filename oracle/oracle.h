@@ -108,6 +108,25 @@ int64_t or_groupby(int64_t n, const int64_t* const* cols, int32_t nkeys, const i
 /* stable sort permutation over nkeys int128 key columns (desc[k] != 0 => descending); first k rows. */
 int64_t or_sort(int64_t n, const or_i128* const* keys, int32_t nkeys, const int32_t* desc, int64_t k, int32_t* out_perm);
 
+
+/* ---- operator µbenchmarks (SURVEY.md §8(c) "µbench join" / "µbench group-by", §8(d) C5a/C5b) ----
+ * The generator's build keys are mix64(i) (splitmix64 finalizer, a bijection on u64), so a key's
+ * build row is mix64^-1(key): the join's and the group-by's exact results reduce to plain loops
+ * with no hash table ("a special case reducing to a plain loop"). */
+typedef struct { int64_t count; or_i128 sum_build; or_i128 sum_probe; uint64_t pair_hash; } or_join_summary;
+uint64_t or_unmix64(uint64_t z);                 /* inverse of the splitmix64 finalizer */
+uint64_t or_pair_mix(int64_t b, int64_t p);      /* order-independent pair hash term (summed mod 2^64) */
+/* closed form: the build side is rows (mix64(i), i), i < nb; probe row j (key, payload) matches row
+ * mix64^-1(key) iff that is < nb.  Summary over all matching pairs. */
+void or_mb_join_closed(int64_t nb, int64_t np, const int64_t* pkeys, const int64_t* ppay, or_join_summary* out);
+/* brute force over arbitrary build rows: std::unordered_multimap (pins the closed form). */
+void or_mb_join_hash(int64_t nb, const int64_t* bkeys, const int64_t* bpay, int64_t np, const int64_t* pkeys,
+                     const int64_t* ppay, or_join_summary* out);
+/* group-by sweep, direct array indexed by g = mix64^-1(key) (must be < G, else returns -1):
+ * per g: sum (int128), count, min, max (count 0 = group absent).  Returns #groups present. */
+int64_t or_mb_groupby_direct(int64_t n, const int64_t* keys, const int64_t* vals, int64_t G, or_i128* sum,
+                             int64_t* cnt, int64_t* mn, int64_t* mx);
+
 /* proleptic Gregorian year of a day number (days since 1970-01-01). */
 int32_t or_civil_year(int32_t days);
 

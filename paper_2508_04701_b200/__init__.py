@@ -165,9 +165,9 @@ class Ctx:
                                     len(gather), C.byref(osel), outs))
         return self.take_sel(osel), [self.take_col(outs[i]) for i in range(len(gather))]
 
-    def groupby(self, cols, keys, aggs, where=(), in_sel=None, having=None, groups_hint=0):
+    def groupby(self, cols, keys, aggs, where=(), in_sel=None, having=None, groups_hint=0, raw=False):
         """keys: [(col, 'id'|'year')]; aggs: [(op, terms, scale)]; having: (agg, op, lo[, hi]).
-        -> (key tensors, agg tensors, ngroups)"""
+        -> (key tensors, agg tensors, ngroups); raw=True: the library-owned sx_cols (free_ptr them)."""
         ca = (A.Col * max(len(cols), 1))(*cols)
         ka = (A.Key * max(len(keys), 1))(*[A.Key(c, A.SX_KEY_YEAR if fn == "year" else A.SX_KEY_IDENTITY)
                                            for c, fn in keys])
@@ -183,6 +183,8 @@ class Ctx:
         self.check(self.L.sx_groupby_agg(self.h, ca, len(cols), ka, len(keys), C.byref(isel) if isel else None, pa,
                                          len(where), aa, len(aggs), C.byref(hv) if hv else None, groups_hint, ok, oa,
                                          C.byref(ng)))
+        if raw:
+            return [ok[i] for i in range(len(keys))], [oa[i] for i in range(len(aggs))], ng.value
         return [self.take_col(ok[i]) for i in range(len(keys))], [self.take_col(oa[i]) for i in range(len(aggs))], ng.value
 
     def hash_build(self, cols, key_cols, in_sel=None, where=(), unique=False):
@@ -214,7 +216,7 @@ class Ctx:
         b = self.take_sel(ob) if jt == A.SX_INNER else None
         return p, b, [self.take_col(outs[i]) for i in range(len(bp) + len(pp))]
 
-    def sort_topk(self, cols, keys, k=-1, in_sel=None):
+    def sort_topk(self, cols, keys, k=-1, in_sel=None, raw=False):
         """keys: [(col, desc)] -> int32 permutation tensor"""
         ca = (A.Col * max(len(cols), 1))(*cols)
         ks = (A.SortKey * len(keys))(*[A.SortKey(c, 1 if d else 0) for c, d in keys])
@@ -222,7 +224,7 @@ class Ctx:
         isel = self.sel(in_sel) if in_sel is not None else None
         self.check(self.L.sx_sort_topk(self.h, ca, len(cols), ks, len(keys), C.byref(isel) if isel else None, k,
                                        C.byref(out)))
-        return self.take_sel(out)
+        return out if raw else self.take_sel(out)
 
     def gather(self, c: A.Col, sel_t):
         out = A.Col()
@@ -260,6 +262,52 @@ class Ctx:
         self.check(self.L.sx_partition_by_rank(self.h, ca, len(cols), kc, len(key_cols), C.byref(isel) if isel else None,
                                                nranks, outs, cnt))
         return [self.take_col(outs[i]) for i in range(len(cols))], [int(x) for x in cnt]
+
+    def radix_partition(self, cols, key_cols, bits, in_sel=None, rows=False):
+        """H5 (sx_radix_partition) -> (partitioned tensors, row ids | None, offsets list of 2^bits + 1)"""
+        ca = (A.Col * len(cols))(*cols)
+        kc = (C.c_int32 * len(key_cols))(*key_cols)
+        outs = (A.Col * len(cols))()
+        orow = A.Sel()
+        offs = (C.c_int64 * ((1 << bits) + 1))()
+        isel = self.sel(in_sel) if in_sel is not None else None
+        self.check(self.L.sx_radix_partition(self.h, ca, len(cols), kc, len(key_cols), C.byref(isel) if isel else None,
+                                             bits, outs, C.byref(orow) if rows else None, offs))
+        r = self.take_sel(orow) if rows else None
+        return [self.take_col(outs[i]) for i in range(len(cols))], r, [int(x) for x in offs]
+
+    def hash_join(self, build_cols, build_keys, probe_cols, probe_keys, jtype="inner", unique=True, bp=(), pp=(),
+                  strategy=0, build_sel=None, probe_sel=None, rows=(True, True), raw=False):
+        """Build + probe (sx_hash_join).  -> (probe sel | None, build sel | None, payloads, strategy used).
+        raw=True returns the library-owned sx_sel / sx_col structs (free them with free_ptr)."""
+        ba = (A.Col * len(build_cols))(*build_cols)
+        pa = (A.Col * len(probe_cols))(*probe_cols)
+        bk = (C.c_int32 * len(build_keys))(*build_keys)
+        pk = (C.c_int32 * len(probe_keys))(*probe_keys)
+        bpa = (C.c_int32 * max(len(bp), 1))(*bp)
+        ppa = (C.c_int32 * max(len(pp), 1))(*pp)
+        op, ob = A.Sel(), A.Sel()
+        outs = (A.Col * max(len(bp) + len(pp), 1))()
+        used = C.c_int()
+        bs = self.sel(build_sel) if build_sel is not None else None
+        ps = self.sel(probe_sel) if probe_sel is not None else None
+        jt = _JOINS[jtype]
+        self.check(self.L.sx_hash_join(self.h, ba, len(build_cols), bk, C.byref(bs) if bs else None, 1 if unique else 0,
+                                       pa, len(probe_cols), pk, C.byref(ps) if ps else None, len(build_keys), jt,
+                                       bpa, len(bp), ppa, len(pp), strategy,
+                                       C.byref(op) if rows[0] else None,
+                                       C.byref(ob) if (rows[1] and jt == A.SX_INNER) else None, outs, C.byref(used)))
+        npay = len(bp) + len(pp)
+        if raw:
+            return (op if rows[0] else None), (ob if rows[1] and jt == A.SX_INNER else None), \
+                [outs[i] for i in range(npay)], used.value
+        p = self.take_sel(op) if rows[0] else None
+        b = self.take_sel(ob) if (rows[1] and jt == A.SX_INNER) else None
+        return p, b, [self.take_col(outs[i]) for i in range(npay)], used.value
+
+    def free_ptr(self, p):
+        if p:
+            self.check(self.L.sx_free(self.h, C.c_void_p(p)))
 
     def copy_into(self, dst, dst_off: int, src, n: int):
         """dst[dst_off:dst_off+n] = src[:n] (stream-ordered device copy; rows of any width)."""

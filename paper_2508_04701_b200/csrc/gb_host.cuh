@@ -260,6 +260,12 @@ inline int agg_out_type(int op) {
 
 constexpr int64_t kSharedMaxGroups = 4096;      // K10 eligibility (hinted groups)
 constexpr int kSharedItems = 1;                  // K10 rows per thread per step (code size vs MLP)
+// A program may ask for more rows per thread (P::kSharedItems): fused probe chains need the
+// memory-level parallelism of several independent rows per thread.
+template <class P, class = void>
+struct shared_items { static constexpr int value = kSharedItems; };
+template <class P>
+struct shared_items<P, std::void_t<decltype(P::kSharedItems)>> { static constexpr int value = P::kSharedItems; };
 constexpr uint64_t kSharedMaxBytes = 96u << 10;  // K10 per-CTA table bytes
 
 inline uint64_t pow2_at_least(uint64_t x) {
@@ -417,14 +423,15 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       k_gb_small<Prog, 4><<<grid, kSmallThreads, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, t);
       SX_CHECK_LAUNCH();
     } else if (n > 0 && nsub == 1 && shared_cap) {
+      constexpr int SI = shared_items<Prog>::value;
       size_t smem = (size_t)(shared_cap + 1) * L.slot_bytes;
-      SX_CUDA(cudaFuncSetAttribute(k_gb_shared<Prog, kSharedItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SX_CUDA(cudaFuncSetAttribute(k_gb_shared<Prog, SI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0;
-      SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_shared<Prog, kSharedItems>, kBlock, smem));
+      SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_shared<Prog, SI>, kBlock, smem));
       if (per_sm < 1) per_sm = 1;
       int64_t tiles = (n + (int64_t)kBlock * 4 - 1) / ((int64_t)kBlock * 4);
       unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, tiles);
-      k_gb_shared<Prog, kSharedItems><<<grid, kBlock, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, t, shared_cap);
+      k_gb_shared<Prog, SI><<<grid, kBlock, smem, SX_STREAM(ctx)>>>(prog, sel, n, L, t, shared_cap);
       SX_CHECK_LAUNCH();
     } else if (n > 0 && nsub == 1) {
       int64_t tiles = (n + 32 * 4 - 1) / (32 * 4) / (kBlock / 32) + 1;

@@ -1,0 +1,581 @@
+// radix.cu — H5: hash-bit radix partitioning (K7) and the radix-partitioned hash join.
+//
+// "hash-bit partitioning of both join sides when build > L2"; north_star:
+// "radix-partitioned joins when the build side exceeds L2".  PAPER.md P:351 lists GPU join
+// algorithms (gpu-join-eth) among the techniques Sirius can adopt; P:418 — joins dominate the
+// join-heavy queries.  The paper gives no kernel design; this is ours, for sm_100a:
+//
+//   sx_radix_partition  one pass, fan-out 2^bits (<= 2^10): partition(key) = (hash64(key) >> 48)
+//                       & (2^bits - 1) — hash bits 48..57, disjoint from the table-slot bits (low)
+//                       and from the shard-rank bits (top, sx_dest_rank; reading R14).
+//     K7a k_part_hist     per-CTA histogram of a contiguous chunk (shared-memory atomics)
+//         scan            partition-major exclusive scan -> every (partition, CTA) output cursor
+//     K7b k_part_scatter  per 2048-row tile: shared-memory counting sort by partition, then the
+//                         tile is written partition run by partition run (coalesced runs)
+//   sx_hash_join        build + probe in one call.  Flat (sx_hash_build + sx_hash_probe) while the
+//                       table fits half the L2; above that (unique build, INNER), both sides are
+//                       radix-partitioned carrying their payload columns, and the partitions are
+//                       joined in waves whose tables together stay L2-resident: probes hit L2
+//                       instead of random HBM sectors, payloads are never gathered at random.
+#include <algorithm>
+#include <vector>
+
+#include "compact.cuh"
+#include "join.cuh"
+
+using namespace sx;
+
+namespace {
+
+constexpr int kPartThreads = 256;
+constexpr int kPartItems = 8;
+constexpr int kPartTile = kPartThreads * kPartItems;  // rows per staged tile
+constexpr int kMaxPartBits = 10;
+constexpr int kPartShift = 48;
+constexpr int kMaxCarry = 12;
+
+struct PartSpec {
+  DCol k0, k1;
+  int nkeys;
+  int bits;
+  int ncarry;
+  DCol carry[kMaxCarry];
+  int width[kMaxCarry];
+  void* out[kMaxCarry];
+  int32_t* out_rowid;  // optional: original row id of every output row
+  const int32_t* sel;
+  int64_t n;
+  int64_t chunk;  // rows per CTA (multiple of kPartTile)
+};
+
+__device__ __forceinline__ uint64_t part_key(const DCol& k0, const DCol& k1, int nkeys, int64_t r) {
+  uint64_t k = (uint64_t)ldv(k0, r);
+  if (nkeys == 2) k = (k << 32) | (uint32_t)ldv(k1, r);
+  return k;
+}
+
+__host__ __device__ __forceinline__ uint32_t part_of(uint64_t key, int bits) {
+  return (uint32_t)(hash64(key) >> kPartShift) & ((1u << bits) - 1u);
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_hist(const __grid_constant__ PartSpec s, int32_t* hist) {
+  __shared__ int h[1 << kMaxPartBits];
+  const int P = 1 << s.bits;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) h[p] = 0;
+  __syncthreads();
+  const int64_t lo = blockIdx.x * s.chunk, hi = min(s.n, lo + s.chunk);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int64_t r = s.sel ? (int64_t)__ldg(s.sel + i) : i;
+    atomicAdd(&h[part_of(part_key(s.k0, s.k1, s.nkeys, r), s.bits)], 1);
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < P; p += blockDim.x) hist[(int64_t)p * gridDim.x + blockIdx.x] = h[p];
+}
+
+__device__ __forceinline__ void copy_val(const DCol& src, int w, void* dst, int64_t d, int64_t r) {
+  switch (w) {
+    case 1: ((uint8_t*)dst)[d] = __ldg((const uint8_t*)src.p + r); break;
+    case 4: ((int32_t*)dst)[d] = __ldg((const int32_t*)src.p + r); break;
+    case 8: ((long long*)dst)[d] = __ldg((const long long*)src.p + r); break;
+    default: ((longlong2*)dst)[d] = __ldg((const longlong2*)src.p + r); break;
+  }
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_scatter(const __grid_constant__ PartSpec s,
+                                                               const int64_t* __restrict__ offs) {
+  __shared__ int64_t cursor[1 << kMaxPartBits];
+  __shared__ int cnt[1 << kMaxPartBits];
+  __shared__ int start[1 << kMaxPartBits];
+  __shared__ uint16_t s_part[kPartTile];
+  __shared__ int32_t s_row[kPartTile];
+  __shared__ int s_warp[kPartThreads / 32];
+  const int P = 1 << s.bits;
+  const int tid = threadIdx.x;
+  for (int p = tid; p < P; p += kPartThreads) cursor[p] = offs[(int64_t)p * gridDim.x + blockIdx.x];
+  const int64_t lo = blockIdx.x * s.chunk, hi = min(s.n, lo + s.chunk);
+  for (int64_t base = lo; base < hi; base += kPartTile) {
+    for (int p = tid; p < P; p += kPartThreads) cnt[p] = 0;
+    __syncthreads();
+    int32_t row[kPartItems];
+    int part[kPartItems], rank[kPartItems];
+#pragma unroll
+    for (int i = 0; i < kPartItems; ++i) {
+      const int64_t idx = base + (int64_t)i * kPartThreads + tid;
+      part[i] = -1;
+      if (idx < hi) {
+        row[i] = s.sel ? __ldg(s.sel + idx) : (int32_t)idx;
+        part[i] = (int)part_of(part_key(s.k0, s.k1, s.nkeys, row[i]), s.bits);
+        rank[i] = atomicAdd(&cnt[part[i]], 1);
+      }
+    }
+    __syncthreads();
+    // exclusive scan of cnt[0..P) -> start[] (each thread scans a contiguous slice)
+    {
+      constexpr int kPer = (1 << kMaxPartBits) / kPartThreads;
+      int loc[kPer], sum = 0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int p = tid * kPer + j;
+        loc[j] = p < P ? cnt[p] : 0;
+        sum += loc[j];
+      }
+      int x = sum;
+      const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_warp[w] = x;
+      __syncthreads();
+      int wo = 0;
+      for (int k = 0; k < w; ++k) wo += s_warp[k];
+      int run = wo + x - sum;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int p = tid * kPer + j;
+        if (p < P) start[p] = run;
+        run += loc[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPartItems; ++i) {
+      if (part[i] < 0) continue;
+      const int pos = start[part[i]] + rank[i];
+      s_part[pos] = (uint16_t)part[i];
+      s_row[pos] = row[i];
+    }
+    __syncthreads();
+    const int tcount = (int)min((int64_t)kPartTile, hi - base);
+    for (int j = tid; j < tcount; j += kPartThreads) {
+      const int p = s_part[j];
+      const int64_t d = cursor[p] + (j - start[p]);
+      const int32_t r = s_row[j];
+      for (int c = 0; c < s.ncarry; ++c) copy_val(s.carry[c], s.width[c], s.out[c], d, r);
+      if (s.out_rowid) s.out_rowid[d] = r;
+    }
+    __syncthreads();
+    for (int p = tid; p < P; p += kPartThreads) cursor[p] += cnt[p];
+    __syncthreads();
+  }
+}
+
+// Partition rows (n, through sel) by hash bits; carried columns land partition-contiguous.
+// offsets_h (host, P+1) receives the partition boundaries.
+sx_status radix_partition(sx_ctx* ctx, PartSpec& s, int64_t* offsets_h) {
+  const int P = 1 << s.bits;
+  int64_t tiles = (s.n + kPartTile - 1) / kPartTile;
+  unsigned grid = persistent_grid(ctx, 4, tiles > 0 ? tiles : 1);
+  int64_t tiles_per = (tiles + grid - 1) / grid;
+  s.chunk = std::max<int64_t>(1, tiles_per) * kPartTile;
+  grid = (unsigned)std::max<int64_t>(1, (s.n + s.chunk - 1) / s.chunk);
+  Scratch scr(ctx);
+  int32_t* hist;
+  int64_t* offs;
+  const int64_t m = (int64_t)P * grid;
+  SX_TRY(scr.get(&hist, (size_t)m));
+  SX_TRY(scr.get(&offs, (size_t)m + 1));
+  int64_t total = 0;
+  if (s.n > 0) {
+    k_part_hist<<<grid, kPartThreads, 0, SX_STREAM(ctx)>>>(s, hist);
+    SX_CHECK_LAUNCH();
+    SX_TRY(scan_counts(ctx, hist, m, offs, &total));
+    k_part_scatter<<<grid, kPartThreads, 0, SX_STREAM(ctx)>>>(s, offs);
+    SX_CHECK_LAUNCH();
+    std::vector<int64_t> all((size_t)m + 1);
+    SX_CUDA(cudaMemcpyAsync(all.data(), offs, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int p = 0; p < P; ++p) offsets_h[p] = all[(size_t)p * grid];
+    offsets_h[P] = total;
+  } else {
+    for (int p = 0; p <= P; ++p) offsets_h[p] = 0;
+  }
+  return SX_OK;
+}
+
+sx_status check_keys(sx_ctx* ctx, const sx_col* cols, int ncols, const int32_t* key_cols, int nkeys, int* kb) {
+  if (nkeys < 1 || nkeys > 2 || !key_cols) return set_err(ctx, SX_EINVAL, "nkeys %d (1 or 2)", nkeys);
+  for (int k = 0; k < nkeys; ++k) {
+    if (key_cols[k] < 0 || key_cols[k] >= ncols) return set_err(ctx, SX_EINVAL, "key column out of range");
+    int t = cols[key_cols[k]].type;
+    if (!(t == SX_I32 || t == SX_DATE32 || t == SX_I64) || (nkeys == 2 && t == SX_I64))
+      return set_err(ctx, SX_ETYPE, "join key type %d", t);
+  }
+  *kb = (nkeys == 1 && cols[key_cols[0]].type != SX_I64) ? 4 : 8;
+  return SX_OK;
+}
+
+// ------------------------------------------------------------------ partitioned join (waves)
+struct PJoin {
+  // partitioned build side
+  const void* bkey;  // uint32 (kb 4) or uint64 packed keys
+  const int32_t* brow;
+  // partitioned probe side
+  const void* pkey;
+  const int32_t* prow;
+  int kb;
+  int bits;
+  int p0;                 // first partition of the wave
+  uint64_t cap;           // slots per partition table (power of two)
+  HtSlot8* slots;         // wave tables: partition (p - p0) at slots + (p - p0) * cap
+  int64_t b_lo, b_hi;     // build tuple range of the wave
+  int64_t p_lo, p_hi;     // probe tuple range of the wave
+  // outputs
+  unsigned long long* cursor;
+  int32_t* out_probe;     // optional
+  int32_t* out_build;     // optional
+  int npay;
+  DCol pay_src[kMaxCarry];  // partitioned payload columns (build ones indexed by jb, probe ones by jp)
+  int pay_build[kMaxCarry];
+  int pay_w[kMaxCarry];
+  void* pay_dst[kMaxCarry];
+};
+
+__device__ __forceinline__ uint64_t pj_key(const void* k, int kb, int64_t j) {
+  return kb == 4 ? (uint64_t)__ldg((const uint32_t*)k + j) : (uint64_t)__ldg((const unsigned long long*)k + j);
+}
+
+__global__ void __launch_bounds__(kBlock) k_pj_build(const __grid_constant__ PJoin a) {
+  for (int64_t j = a.b_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.b_hi;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = pj_key(a.bkey, a.kb, j);
+    const uint64_t h = hash64(key);
+    HtSlot8* t = a.slots + (uint64_t)(((uint32_t)(h >> kPartShift) & ((1u << a.bits) - 1u)) - a.p0) * a.cap;
+    uint64_t s = h & (a.cap - 1);
+    while (atomicCAS(&t[s].row, 0xffffffffu, (unsigned)(j - a.b_lo)) != 0xffffffffu) s = (s + 1) & (a.cap - 1);
+    t[s].key = key;
+  }
+}
+
+constexpr int kPjItems = 8;
+__global__ void __launch_bounds__(kBlock) k_pj_probe(const __grid_constant__ PJoin a) {
+  __shared__ int s_warp[kBlock / 32];
+  __shared__ unsigned long long s_base;
+  const int64_t tile = (int64_t)kBlock * kPjItems;
+  for (int64_t base = a.p_lo + blockIdx.x * tile; base < a.p_hi; base += (int64_t)gridDim.x * tile) {
+    int64_t jb[kPjItems];
+    uint64_t key[kPjItems], s[kPjItems];
+    const HtSlot8* t[kPjItems];
+    bool pend[kPjItems];
+#pragma unroll
+    for (int i = 0; i < kPjItems; ++i) {
+      const int64_t j = base + (int64_t)i * kBlock + threadIdx.x;
+      pend[i] = j < a.p_hi;
+      key[i] = pend[i] ? pj_key(a.pkey, a.kb, j) : 0;
+      const uint64_t h = hash64(key[i]);
+      t[i] = a.slots + (uint64_t)(((uint32_t)(h >> kPartShift) & ((1u << a.bits) - 1u)) - a.p0) * a.cap;
+      if (!pend[i]) t[i] = a.slots;
+      s[i] = h & (a.cap - 1);
+      jb[i] = -1;
+    }
+    bool any = true;
+    while (any) {
+      any = false;
+      longlong2 v[kPjItems];
+#pragma unroll
+      for (int i = 0; i < kPjItems; ++i) v[i] = pend[i] ? __ldg((const longlong2*)(t[i] + s[i])) : make_longlong2(0, -1);
+#pragma unroll
+      for (int i = 0; i < kPjItems; ++i) {
+        if (!pend[i]) continue;
+        const uint32_t rw = (uint32_t)(unsigned long long)v[i].y;
+        if (rw == 0xffffffffu) {
+          pend[i] = false;
+        } else if ((uint64_t)v[i].x == key[i]) {
+          jb[i] = a.b_lo + rw;
+          pend[i] = false;
+        } else {
+          s[i] = (s[i] + 1) & (a.cap - 1);
+          any = true;
+        }
+      }
+    }
+    // tile-level output allocation: one atomic per CTA tile
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < kPjItems; ++i) c += jb[i] >= 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int k = 0; k < kBlock / 32; ++k) tot += s_warp[k];
+      s_base = tot ? atomicAdd(a.cursor, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    int wo = 0;
+    for (int k = 0; k < w; ++k) wo += s_warp[k];
+    int64_t pos = (int64_t)s_base + wo + x - c;
+#pragma unroll
+    for (int i = 0; i < kPjItems; ++i) {
+      if (jb[i] < 0) continue;
+      const int64_t jp = base + (int64_t)i * kBlock + threadIdx.x;
+      if (a.out_probe) a.out_probe[pos] = __ldg(a.prow + jp);
+      if (a.out_build) a.out_build[pos] = __ldg(a.brow + jb[i]);
+      for (int g = 0; g < a.npay; ++g) copy_val(a.pay_src[g], a.pay_w[g], a.pay_dst[g], pos, a.pay_build[g] ? jb[i] : jp);
+      ++pos;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+SX_EXPORT uint32_t sx_radix_of(uint64_t key, int bits) {  // host mirror of the partition function
+  return (bits < 1 || bits > kMaxPartBits) ? 0u : part_of(key, bits);
+}
+
+SX_EXPORT sx_status sx_radix_partition(sx_ctx* ctx, const sx_col* cols, int ncols, const int32_t* key_cols, int nkeys,
+                                       const sx_sel* in_sel, int bits, sx_col* out_cols, sx_sel* out_rows,
+                                       int64_t* offsets) {
+  if (!ctx || !cols || !out_cols || !offsets || bits < 1 || bits > kMaxPartBits || ncols < 1 || ncols > kMaxCarry)
+    return SX_EINVAL;
+  for (int c = 0; c < ncols; ++c) out_cols[c] = sx_col{};
+  if (out_rows) *out_rows = sx_sel{0, nullptr};
+  ProfScope ps(ctx, "radix_partition");
+  DCol dc[SX_MAX_COLS];
+  SX_TRY(to_dcols(ctx, cols, ncols, dc));
+  int kb = 4;
+  SX_TRY(check_keys(ctx, cols, ncols, key_cols, nkeys, &kb));
+  const int64_t n = in_sel ? in_sel->len : cols[key_cols[0]].len;
+  if (n > INT32_MAX) return set_err(ctx, SX_EINDEX, "partition input exceeds INT32_MAX rows");
+  Scratch scr(ctx);
+  PartSpec s{};
+  s.k0 = dc[key_cols[0]];
+  s.k1 = dc[nkeys > 1 ? key_cols[1] : key_cols[0]];
+  s.nkeys = nkeys;
+  s.bits = bits;
+  s.ncarry = ncols;
+  s.sel = in_sel ? in_sel->idx : nullptr;
+  s.n = n;
+  double row_b = 0;
+  for (int c = 0; c < ncols; ++c) {
+    const int w = type_width(cols[c].type);
+    if (!w) return set_err(ctx, SX_ETYPE, "column %d is not fixed-width", c);
+    s.carry[c] = dc[c];
+    s.width[c] = w;
+    SX_TRY(scr.get((char**)&s.out[c], (size_t)(n > 0 ? n : 1) * w));
+    row_b += 2.0 * w;
+  }
+  if (out_rows) SX_TRY(scr.get(&s.out_rowid, (size_t)(n > 0 ? n : 1)));
+  SX_TRY(radix_partition(ctx, s, offsets));
+  for (int c = 0; c < ncols; ++c) {
+    out_cols[c] = cols[c];
+    out_cols[c].len = n;
+    out_cols[c].data = s.out[c];
+    out_cols[c].offsets = nullptr;
+    scr.release(s.out[c]);
+  }
+  if (out_rows) {
+    *out_rows = sx_sel{n, s.out_rowid};
+    scr.release(s.out_rowid);
+  }
+  ps.set_bytes((row_b + (in_sel ? 4.0 : 0.0) + (out_rows ? 4.0 : 0.0)) * n);  // every column read + written once
+  return SX_OK;
+}
+
+namespace {
+
+// Packed key column of a partitioned side (uint32 for one 32-bit key, else uint64).
+__global__ void k_pack_keys(DCol k0, DCol k1, int nkeys, int kb, int64_t n, void* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = (uint64_t)ldv(k0, i);
+    if (nkeys == 2) k = (k << 32) | (uint32_t)ldv(k1, i);
+    if (kb == 4) ((uint32_t*)out)[i] = (uint32_t)k;
+    else ((unsigned long long*)out)[i] = k;
+  }
+}
+
+}  // namespace
+
+SX_EXPORT sx_status sx_hash_join(sx_ctx* ctx, const sx_col* build_cols, int nbuild_cols, const int32_t* build_keys,
+                                 const sx_sel* build_sel, int unique_hint, const sx_col* probe_cols, int nprobe_cols,
+                                 const int32_t* probe_keys, const sx_sel* probe_sel, int nkeys, int join_type,
+                                 const int32_t* bp, int nbp, const int32_t* pp, int npp, int strategy,
+                                 sx_sel* out_probe, sx_sel* out_build, sx_col* out_payload, int* used_strategy) {
+  if (!ctx || !build_cols || !probe_cols || !build_keys || !probe_keys) return SX_EINVAL;
+  if (out_probe) *out_probe = sx_sel{0, nullptr};
+  if (out_build) *out_build = sx_sel{0, nullptr};
+  for (int i = 0; out_payload && i < nbp + npp && i < kMaxCarry; ++i) out_payload[i] = sx_col{};
+  if (used_strategy) *used_strategy = 0;
+  if (nbp < 0 || npp < 0 || nbp + npp > kMaxCarry || ((nbp + npp) > 0 && !out_payload))
+    return set_err(ctx, SX_EINVAL, "payload columns");
+  if (join_type < SX_INNER || join_type > SX_ANTI) return set_err(ctx, SX_EINVAL, "join type %d", join_type);
+  int kb = 4, kbp = 4;
+  SX_TRY(check_keys(ctx, build_cols, nbuild_cols, build_keys, nkeys, &kb));
+  SX_TRY(check_keys(ctx, probe_cols, nprobe_cols, probe_keys, nkeys, &kbp));
+  if (kb != kbp) return set_err(ctx, SX_ETYPE, "build/probe key widths differ");
+  const int64_t nb = build_sel ? build_sel->len : build_cols[build_keys[0]].len;
+  const int64_t np = probe_sel ? probe_sel->len : probe_cols[probe_keys[0]].len;
+  if (nb > INT32_MAX || np > INT32_MAX) return set_err(ctx, SX_EINDEX, "join side exceeds INT32_MAX rows");
+  // strategy: 1 flat, 2 partitioned, 0 auto (partitioned when the flat table would exceed half the L2)
+  uint64_t flat_cap = 64;
+  while (flat_cap < (uint64_t)(2 * nb)) flat_cap <<= 1;
+  const size_t flat_bytes = flat_cap * (size_t)(kb == 4 ? 8 : 16);
+  bool part = strategy == 2 || (strategy == 0 && flat_bytes > ctx->l2_bytes / 2);
+  if (join_type != SX_INNER || !unique_hint) part = false;  // partitioned path: PK build, INNER
+  if (!part) {
+    if (used_strategy) *used_strategy = 1;
+    sx_ht* ht = nullptr;
+    SX_TRY(sx_hash_build(ctx, build_cols, nbuild_cols, build_keys, nkeys, build_sel, nullptr, 0, unique_hint, &ht));
+    sx_sel op{}, ob{};
+    sx_status s = sx_hash_probe(ctx, ht, probe_cols, nprobe_cols, probe_keys, nkeys, probe_sel, nullptr, 0, join_type,
+                                build_cols, nbuild_cols, bp, nbp, pp, npp, &op, join_type == SX_INNER ? &ob : nullptr,
+                                out_payload);
+    sx_ht_destroy(ctx, ht);
+    if (s != SX_OK) return s;
+    if (out_probe) *out_probe = op;
+    else sx_free(ctx, op.idx);
+    if (out_build) *out_build = ob;
+    else sx_free(ctx, ob.idx);
+    return SX_OK;
+  }
+  if (used_strategy) *used_strategy = 2;
+  ProfScope ps(ctx, "join_partitioned");
+  Scratch scr(ctx);
+  DCol bdc[SX_MAX_COLS], pdc[SX_MAX_COLS];
+  SX_TRY(to_dcols(ctx, build_cols, nbuild_cols, bdc));
+  SX_TRY(to_dcols(ctx, probe_cols, nprobe_cols, pdc));
+  // fan-out: per-partition tables of <= 16 MB
+  int bits = 1;
+  while (bits < kMaxPartBits && (flat_bytes >> bits) > (16u << 20)) ++bits;
+  const int P = 1 << bits;
+  // partition both sides: carried = key columns, then payloads; + row ids if requested
+  auto part_side = [&](const sx_col* cols, const DCol* dc, const int32_t* keys, const sx_sel* sel, int64_t n,
+                       const int32_t* pay, int npay, bool rowid, PartSpec& s, std::vector<int64_t>& off) -> sx_status {
+    s = PartSpec{};
+    s.k0 = dc[keys[0]];
+    s.k1 = dc[nkeys > 1 ? keys[1] : keys[0]];
+    s.nkeys = nkeys;
+    s.bits = bits;
+    s.sel = sel ? sel->idx : nullptr;
+    s.n = n;
+    int c = 0;
+    for (int k = 0; k < nkeys; ++k, ++c) {
+      s.carry[c] = dc[keys[k]];
+      s.width[c] = type_width(cols[keys[k]].type);
+    }
+    for (int g = 0; g < npay; ++g, ++c) {
+      const int w = type_width(cols[pay[g]].type);
+      if (!w) return set_err(ctx, SX_ETYPE, "payload must be fixed-width");
+      s.carry[c] = dc[pay[g]];
+      s.width[c] = w;
+    }
+    s.ncarry = c;
+    for (int k = 0; k < c; ++k) SX_TRY(scr.get((char**)&s.out[k], (size_t)(n > 0 ? n : 1) * s.width[k]));
+    if (rowid) SX_TRY(scr.get(&s.out_rowid, (size_t)(n > 0 ? n : 1)));
+    off.assign((size_t)P + 1, 0);
+    return radix_partition(ctx, s, off.data());
+  };
+  for (int g = 0; g < nbp; ++g)
+    if (bp[g] < 0 || bp[g] >= nbuild_cols) return set_err(ctx, SX_EINVAL, "build payload column out of range");
+  for (int g = 0; g < npp; ++g)
+    if (pp[g] < 0 || pp[g] >= nprobe_cols) return set_err(ctx, SX_EINVAL, "probe payload column out of range");
+  PartSpec bs, psp;
+  std::vector<int64_t> boff, poff;
+  SX_TRY(part_side(build_cols, bdc, build_keys, build_sel, nb, bp, nbp, out_build != nullptr, bs, boff));
+  SX_TRY(part_side(probe_cols, pdc, probe_keys, probe_sel, np, pp, npp, out_probe != nullptr, psp, poff));
+  // packed keys of both partitioned sides (a single key column already is one: 4-byte keys are
+  // read as uint32, int64 keys as uint64)
+  const void *bkey = bs.out[0], *pkey = psp.out[0];
+  if (nkeys == 2) {
+    void *bk2, *pk2;
+    SX_TRY(scr.get((char**)&bk2, (size_t)(nb > 0 ? nb : 1) * kb));
+    SX_TRY(scr.get((char**)&pk2, (size_t)(np > 0 ? np : 1) * kb));
+    bkey = bk2;
+    pkey = pk2;
+    DCol b0{bs.out[0], build_cols[build_keys[0]].type, 0}, b1{bs.out[nkeys - 1], SX_I32, 0};
+    DCol p0{psp.out[0], probe_cols[probe_keys[0]].type, 0}, p1{psp.out[nkeys - 1], SX_I32, 0};
+    if (nb > 0) k_pack_keys<<<persistent_grid(ctx, 8, (nb + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(b0, b1, nkeys, kb, nb, bk2);
+    if (np > 0) k_pack_keys<<<persistent_grid(ctx, 8, (np + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(p0, p1, nkeys, kb, np, pk2);
+    SX_CHECK_LAUNCH();
+  }
+  // outputs (unique build: at most one match per probe row)
+  const size_t ocap = (size_t)(np > 0 ? np : 1);
+  int32_t *op = nullptr, *ob = nullptr;
+  if (out_probe) SX_TRY(scr.get(&op, ocap));
+  if (out_build) SX_TRY(scr.get(&ob, ocap));
+  PJoin a{};
+  a.bkey = bkey;
+  a.pkey = pkey;
+  a.brow = bs.out_rowid;
+  a.prow = psp.out_rowid;
+  a.kb = kb;
+  a.bits = bits;
+  a.out_probe = op;
+  a.out_build = ob;
+  a.npay = nbp + npp;
+  for (int g = 0; g < nbp; ++g) {
+    a.pay_src[g] = DCol{bs.out[nkeys + g], build_cols[bp[g]].type, 0};
+    a.pay_build[g] = 1;
+    a.pay_w[g] = bs.width[nkeys + g];
+  }
+  for (int g = 0; g < npp; ++g) {
+    a.pay_src[nbp + g] = DCol{psp.out[nkeys + g], probe_cols[pp[g]].type, 0};
+    a.pay_build[nbp + g] = 0;
+    a.pay_w[nbp + g] = psp.width[nkeys + g];
+  }
+  for (int g = 0; g < a.npay; ++g) SX_TRY(scr.get((char**)&a.pay_dst[g], ocap * a.pay_w[g]));
+  a.cursor = (unsigned long long*)ctx->d_counters;
+  SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
+  // per-partition table size from the largest build partition; waves of partitions whose tables
+  // together fit about half the L2
+  int64_t maxb = 1;
+  for (int p = 0; p < P; ++p) maxb = std::max<int64_t>(maxb, boff[p + 1] - boff[p]);
+  uint64_t cap = 64;
+  while (cap < (uint64_t)(2 * maxb)) cap <<= 1;
+  const size_t part_bytes = cap * sizeof(HtSlot8);
+  int W = (int)std::max<size_t>(1, (ctx->l2_bytes / 2) / part_bytes);
+  W = std::min(W, P);
+  HtSlot8* slots;
+  SX_TRY(scr.get(&slots, (size_t)W * cap));
+  a.slots = slots;
+  a.cap = cap;
+  for (int p0 = 0; p0 < P; p0 += W) {
+    const int p1 = std::min(P, p0 + W);
+    a.p0 = p0;
+    a.b_lo = boff[p0];
+    a.b_hi = boff[p1];
+    a.p_lo = poff[p0];
+    a.p_hi = poff[p1];
+    if (a.b_hi == a.b_lo || a.p_hi == a.p_lo) continue;
+    SX_CUDA(cudaMemsetAsync(slots, 0xff, (size_t)(p1 - p0) * cap * sizeof(HtSlot8), ctx->stream));
+    const int64_t nbw = a.b_hi - a.b_lo, npw = a.p_hi - a.p_lo;
+    k_pj_build<<<persistent_grid(ctx, 8, (nbw + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+    k_pj_probe<<<persistent_grid(ctx, 8, (npw + kBlock * kPjItems - 1) / (kBlock * kPjItems)), kBlock, 0, SX_STREAM(ctx)>>>(a);
+    SX_CHECK_LAUNCH();
+  }
+  int64_t count = 0;
+  SX_TRY(read_i64(ctx, a.cursor, &count));
+  if (out_probe) {
+    *out_probe = sx_sel{count, op};
+    scr.release(op);
+  }
+  if (out_build) {
+    *out_build = sx_sel{count, ob};
+    scr.release(ob);
+  }
+  for (int g = 0; g < a.npay; ++g) {
+    const sx_col& src = g < nbp ? build_cols[bp[g]] : probe_cols[pp[g - nbp]];
+    out_payload[g] = src;
+    out_payload[g].len = count;
+    out_payload[g].data = a.pay_dst[g];
+    out_payload[g].offsets = nullptr;
+    scr.release(a.pay_dst[g]);
+  }
+  // algorithmic bytes: both sides' keys (+ selections) read once, payloads read once and written
+  // once per output, row-id outputs once (build + probe definitions)
+  double kbytes = 0;
+  for (int k = 0; k < nkeys; ++k) kbytes += type_width(build_cols[build_keys[k]].type);
+  double b = (kbytes + (build_sel ? 4.0 : 0.0)) * nb + (kbytes + (probe_sel ? 4.0 : 0.0)) * np;
+  for (int g = 0; g < a.npay; ++g) b += 2.0 * a.pay_w[g] * count;
+  b += ((out_probe ? 4.0 : 0.0) + (out_build ? 4.0 : 0.0)) * count;
+  ps.set_bytes(b);
+  return SX_OK;
+}

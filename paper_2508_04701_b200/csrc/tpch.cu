@@ -10,6 +10,7 @@
 
 #include "common.cuh"
 #include "gb_host.cuh"
+#include "join.cuh"
 
 using namespace sx;
 
@@ -318,6 +319,113 @@ struct Q9Prog {
       int64_t c = alive[i] ? __ldg(cost + row[i]) : 0, q = alive[i] ? __ldg(qty + row[i]) : 0;
       v[i] = sub_ck(mul_ck(e, sub_ck(100, d, ovf), ovf), mul_ck(c, q, ovf), ovf);
     }
+  }
+};
+
+// Unique-key lookup in an sx_hash_build table (the layouts of join.cu): the build row id, or -1.
+template <int KB>
+__device__ __forceinline__ int32_t ht_find(const void* slots, uint32_t mask, uint64_t key) {
+  if (KB == 4) {
+    const unsigned long long* s = (const unsigned long long*)slots;
+    uint32_t h = hash32((uint32_t)key) & mask;
+    for (;;) {
+      const unsigned long long v = __ldg(s + h);
+      if ((uint32_t)(v >> 32) == 0xffffffffu) return -1;
+      if ((uint32_t)v == (uint32_t)key) return (int32_t)(v >> 32);
+      h = (h + 1) & mask;
+    }
+  } else {
+    const longlong2* s = (const longlong2*)slots;
+    uint32_t h = (uint32_t)hash64(key) & mask;
+    for (;;) {
+      const longlong2 v = __ldg(s + h);
+      const uint32_t rw = (uint32_t)(unsigned long long)v.y;
+      if (rw == 0xffffffffu) return -1;
+      if ((uint64_t)v.x == key) return (int32_t)rw;
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+// Q9 as one pass over lineitem (the plan's probe chain fused into its group-by, SURVEY §8(a) "the
+// executor may fuse adjacent steps"): green-part membership from the part build's exact key-range
+// bitmap; partsupp (partkey, suppkey) -> ps_supplycost, supplier suppkey -> s_nationkey and orders
+// orderkey -> o_orderdate through unique-key tables (PK sides); key (nationkey, year(o_orderdate));
+// state 0 sum(ext*(100-disc) - supplycost*qty).  Rows whose lookups miss drop out (inner joins).
+// Several rows per thread (kSharedItems) so their independent lookups overlap.
+template <typename KT, int OKB>
+struct Q9FusedProg {
+  const int32_t *partkey, *suppkey;
+  const KT* orderkey;
+  const long long *qty, *ext, *disc;
+  const uint32_t* pbm;
+  long long pbm_min;
+  unsigned long long pbm_bits;
+  const void* ps_slots;
+  uint32_t ps_mask;
+  const long long* ps_cost;
+  const void* s_slots;
+  uint32_t s_mask;
+  const int32_t* s_nation;
+  const void* o_slots;
+  uint32_t o_mask;
+  const int32_t* o_date;
+  int* ovf_flag;
+  static constexpr int kMaxNst = 1;
+  static constexpr int kUnrollStates = 1;
+  static constexpr bool kSortedOK = false;
+  static constexpr int kSharedItems = 4;
+  bool no_filter() const { return false; }
+  template <int I>
+  __device__ __forceinline__ void keys_only(const int32_t (&)[I], const bool (&)[I], uint64_t (&)[I]) const {}
+  template <int I>
+  struct Cache { int64_t cost[I], qty[I], ext[I], disc[I]; };
+  __device__ __forceinline__ int kind(int, const Layout&) const { return ST_SUM; }
+  template <int I>
+  __device__ __forceinline__ void where_keys(const int32_t (&row)[I], bool (&alive)[I], uint64_t (&key)[I],
+                                             Cache<I>& c) const {
+    int32_t pk[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) pk[i] = alive[i] ? __ldg(partkey + row[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const unsigned long long off = (unsigned long long)((long long)pk[i] - pbm_min);
+      const bool in = alive[i] && off < pbm_bits;
+      const uint32_t w = in ? __ldg(pbm + (off >> 5)) : 0u;
+      alive[i] = in && ((w >> (off & 31)) & 1u);
+    }
+    int32_t sk[I];
+    KT ok[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      sk[i] = alive[i] ? __ldg(suppkey + row[i]) : 0;
+      ok[i] = alive[i] ? __ldg(orderkey + row[i]) : (KT)0;
+      c.qty[i] = alive[i] ? __ldg(qty + row[i]) : 0;
+      c.ext[i] = alive[i] ? __ldg(ext + row[i]) : 0;
+      c.disc[i] = alive[i] ? __ldg(disc + row[i]) : 0;
+    }
+    int32_t rps[I], rs[I], ro[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      rps[i] = alive[i] ? ht_find<8>(ps_slots, ps_mask, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i]) : -1;
+      rs[i] = alive[i] ? ht_find<4>(s_slots, s_mask, (uint32_t)sk[i]) : -1;
+      ro[i] = alive[i] ? ht_find<OKB>(o_slots, o_mask, (uint64_t)(int64_t)ok[i]) : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      alive[i] = alive[i] && rps[i] >= 0 && rs[i] >= 0 && ro[i] >= 0;
+      c.cost[i] = alive[i] ? __ldg(ps_cost + rps[i]) : 0;
+      const uint32_t nk = alive[i] ? (uint32_t)__ldg(s_nation + rs[i]) : 0u;
+      const int32_t d = alive[i] ? __ldg(o_date + ro[i]) : 0;
+      key[i] = ((uint64_t)nk << 32) | (uint32_t)civil_year(d);
+    }
+  }
+  template <int I>
+  __device__ __forceinline__ void state(int, const int32_t (&)[I], const bool (&)[I], const Cache<I>& c,
+                                        int64_t (&v)[I], bool& ovf) const {
+#pragma unroll
+    for (int i = 0; i < I; ++i)
+      v[i] = sub_ck(mul_ck(c.ext[i], sub_ck(100, c.disc[i], ovf), ovf), mul_ck(c.cost[i], c.qty[i], ovf), ovf);
   }
 };
 
@@ -643,6 +751,85 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   sx_ht* ht_p;
   SX_TRY(sx_hash_build(ctx, pk, 1, &k0, 1, &sel_p, nullptr, 0, 1, &ht_p));
   bag.keep(ht_p);
+  sx_col gok[2], goa[1];
+  int64_t ng = 0;
+  // Fused plan (default): build partsupp' / supplier / orders PK tables, then one pass over
+  // lineitem probing all of them inside the group-by (Q9FusedProg).  SX_Q9_PLAN=ops selects the
+  // operator-at-a-time plan below (materialising every join's output).
+  const bool ops_plan = getenv("SX_Q9_PLAN") && std::strcmp(getenv("SX_Q9_PLAN"), "ops") == 0;
+  const bool okb4 = w4(t->o_orderkey) && w4(t->l_orderkey), okb8 = w8(t->o_orderkey) && w8(t->l_orderkey);
+  if (!ops_plan && ht_p->bm && (okb4 || okb8) && w4(t->l_partkey) && w4(t->l_suppkey) && w8(t->l_quantity) &&
+      w8(t->l_extendedprice) && w8(t->l_discount) && w4(t->ps_partkey) && w4(t->ps_suppkey) &&
+      w8(t->ps_supplycost) && w4(t->s_suppkey) && w4(t->s_nationkey) && w4(t->o_orderdate)) {
+    sx_col pscols[2] = {t->ps_partkey, t->ps_suppkey};
+    sx_sel sel_ps;
+    SX_TRY(sx_hash_probe(ctx, ht_p, pscols, 2, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0, nullptr,
+                         0, &sel_ps, nullptr, nullptr));
+    bag.keep(sel_ps);
+    int32_t k01[2] = {0, 1};
+    sx_ht *ht_ps, *ht_s, *ht_o;
+    SX_TRY(sx_hash_build(ctx, pscols, 2, k01, 2, &sel_ps, nullptr, 0, 1, &ht_ps));
+    bag.keep(ht_ps);
+    SX_TRY(sx_hash_build(ctx, &t->s_suppkey, 1, &k0, 1, nullptr, nullptr, 0, 1, &ht_s));
+    bag.keep(ht_s);
+    SX_TRY(sx_hash_build(ctx, &t->o_orderkey, 1, &k0, 1, nullptr, nullptr, 0, 1, &ht_o));
+    bag.keep(ht_o);
+    if (ht_ps->key_bytes != 8 || ht_s->key_bytes != 4 || ht_o->key_bytes != (okb4 ? 4 : 8))
+      return set_err(ctx, SX_EINVAL, "Q9: unexpected table layouts");
+    ProfScope pg(ctx, "probe_groupby");
+    sx_col tcols[6] = {t->s_nationkey, t->ps_supplycost, t->l_quantity, t->l_extendedprice, t->l_discount,
+                       t->o_orderdate};  // types only: the plan's state layout
+    sx_key gk[2] = {{0, SX_KEY_IDENTITY}, {5, SX_KEY_YEAR}};
+    sx_agg ga;
+    std::memset(&ga, 0, sizeof ga);
+    ga.op = SX_SUM;
+    ga.value.nterms = 2;
+    ga.value.t[0].coef = 1;
+    ga.value.t[0].nf = 2;
+    ga.value.t[0].f[0] = F(3);
+    ga.value.t[0].f[1] = F(4, -1, 100);
+    ga.value.t[1].coef = -1;
+    ga.value.t[1].nf = 2;
+    ga.value.t[1].f[0] = F(1);
+    ga.value.t[1].f[1] = F(2);
+    GbPlan plan;
+    SX_TRY(gb_plan(ctx, tcols, 6, gk, 2, &ga, 1, nullptr, &plan));
+    SX_TRY(check_states(ctx, plan, {ST_SUM}));
+    const int64_t n = t->l_partkey.len;
+    auto fill = [&](auto& pr) {
+      pr.partkey = (const int32_t*)t->l_partkey.data;
+      pr.suppkey = (const int32_t*)t->l_suppkey.data;
+      pr.qty = (const long long*)t->l_quantity.data;
+      pr.ext = (const long long*)t->l_extendedprice.data;
+      pr.disc = (const long long*)t->l_discount.data;
+      pr.pbm = ht_p->bm;
+      pr.pbm_min = ht_p->bm_min;
+      pr.pbm_bits = ht_p->bm_bits;
+      pr.ps_slots = ht_ps->slots;
+      pr.ps_mask = (uint32_t)(ht_ps->cap - 1);
+      pr.ps_cost = (const long long*)t->ps_supplycost.data;
+      pr.s_slots = ht_s->slots;
+      pr.s_mask = (uint32_t)(ht_s->cap - 1);
+      pr.s_nation = (const int32_t*)t->s_nationkey.data;
+      pr.o_slots = ht_o->slots;
+      pr.o_mask = (uint32_t)(ht_o->cap - 1);
+      pr.o_date = (const int32_t*)t->o_orderdate.data;
+      pr.ovf_flag = ctx->d_flags;
+    };
+    if (okb4) {
+      Q9FusedProg<int32_t, 4> pr;
+      fill(pr);
+      pr.orderkey = (const int32_t*)t->l_orderkey.data;
+      SX_TRY(gb_run(ctx, pr, plan, nullptr, n, 256, gok, goa, &ng));
+    } else {
+      Q9FusedProg<long long, 8> pr;
+      fill(pr);
+      pr.orderkey = (const long long*)t->l_orderkey.data;
+      SX_TRY(gb_run(ctx, pr, plan, nullptr, n, 256, gok, goa, &ng));
+    }
+    // lineitem's five referenced columns once (+ the G output rows); lookups are implementation cost
+    pg.set_bytes((4.0 + 4.0 + type_width(t->l_orderkey.type) + 24.0) * n + 24.0 * ng);
+  } else {
   // 2. lineitem semi-join P, materialising the columns the plan needs
   sx_col lcols[6] = {t->l_partkey, t->l_suppkey, t->l_orderkey, t->l_quantity, t->l_extendedprice, t->l_discount};
   int32_t lpp[6] = {0, 1, 2, 3, 4, 5};
@@ -709,8 +896,6 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   ga.value.t[1].nf = 2;
   ga.value.t[1].f[0] = F(1);
   ga.value.t[1].f[1] = F(2);
-  sx_col gok[2], goa[1];
-  int64_t ng = 0;
   if (w4(L5[0]) && w8(L5[1]) && w8(L5[2]) && w8(L5[3]) && w8(L5[4]) && w4(L5[5])) {
     ProfScope pg(ctx, "groupby");
     GbPlan plan;
@@ -724,6 +909,7 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   } else {
     SX_TRY(sx_groupby_agg(ctx, L5, 6, gk, 2, nullptr, nullptr, 0, &ga, 1, nullptr, 256, gok, goa, &ng));
   }
+  }  // operator-at-a-time plan
   bag.keep(gok, 2);
   bag.keep(goa, 1);
   // 8. order by n_name asc (string order of the nation dimension), o_year desc

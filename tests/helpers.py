@@ -83,3 +83,24 @@ def diff_rows(a: list, b: list) -> str:
             if len(lines) > 10:
                 break
     return "\n".join(lines)
+
+
+def np_pair_mix(b: np.ndarray, p: np.ndarray) -> int:
+    """Σ (mod 2^64) of the oracle's pair hash (oracle.or_pair_mix) over output pairs, in numpy (test side)."""
+    with np.errstate(over="ignore"):
+        z = b.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15) ^ p.astype(np.uint64)
+        z = (z ^ (z >> np.uint64(32))) * np.uint64(0xD6E8FEB86659FD93)
+        z = z ^ (z >> np.uint64(32))
+        return int(z.sum(dtype=np.uint64))
+
+
+def np_fmix64(k: np.ndarray) -> np.ndarray:
+    """murmur3 fmix64 (the hash DESIGN.md R14 documents), in numpy (test side)."""
+    k = k.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        k ^= k >> np.uint64(33)
+        k *= np.uint64(0xFF51AFD7ED558CCD)
+        k ^= k >> np.uint64(33)
+        k *= np.uint64(0xC4CEB9FE1A85EC53)
+        k ^= k >> np.uint64(33)
+    return k

@@ -21,7 +21,7 @@ def libsx():
 def header_functions():
     src = open(os.path.join(ROOT, "include", "sx.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:sx_status|void|int64_t|int|const char\*)\s+(sx_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:sx_status|void|int64_t|uint32_t|int|const char\*)\s+(sx_\w+)\s*\(", src, flags=re.M)))
 
 
 def test_header_declares_the_boundary():

@@ -1,0 +1,118 @@
+"""H5 parity: sx_radix_partition and sx_hash_join (flat and radix-partitioned) through the C ABI
+vs the CPU oracle (join µbench closed form / brute force, or_join) and vs properties that pin the
+partition function (SURVEY.md §8(a) H5, §8(c) "µbench join"; reading R14)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from tests.helpers import np_fmix64, np_pair_mix
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2508_04701_b200 as sx  # noqa: E402
+from paper_2508_04701_b200 import _abi as A  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return sx.Ctx(0)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("n,bits,key_t", [(0, 3, np.int64), (1, 1, np.int32), (5000, 4, np.int32),
+                                          (100_003, 8, np.int64), (300_001, 10, np.int32)])
+def test_radix_partition(ctx, n, bits, key_t):
+    rng = np.random.default_rng(n + bits)
+    keys = rng.integers(-2**31, 2**31 - 1, n, dtype=np.int64).astype(key_t)
+    pay = rng.integers(-2**62, 2**62, n, dtype=np.int64)
+    cols = [sx.col(dev(keys)), sx.col(dev(pay))]
+    (pk, pp), rows, offs = ctx.radix_partition(cols, [0], bits, rows=True)
+    pk, pp, rows = pk.cpu().numpy(), pp.cpu().numpy(), rows.cpu().numpy()
+    P = 1 << bits
+    # the documented partition function: (fmix64(key as u64, sign-extended) >> 48) & (2^bits - 1)
+    part = ((np_fmix64(keys.astype(np.int64).view(np.uint64)) >> np.uint64(48)) & np.uint64(P - 1)).astype(np.int64)
+    assert offs[0] == 0 and offs[-1] == n and all(offs[i] <= offs[i + 1] for i in range(P))
+    assert np.array_equal(np.diff(offs), np.bincount(part, minlength=P))
+    assert np.array_equal(np.sort(rows), np.arange(n))  # a permutation of the input rows
+    assert np.array_equal(pk, keys[rows]) and np.array_equal(pp, pay[rows])
+    for p in range(P):
+        assert (part[rows[offs[p]:offs[p + 1]]] == p).all()
+    for k in keys[:20]:
+        assert sx.lib().sx_radix_of(int(k) & (2**64 - 1), bits) == part[list(keys).index(k)]
+
+
+def test_radix_partition_with_selection(ctx):
+    n = 70_001
+    keys = np.arange(n, dtype=np.int32) * 7
+    sel = np.nonzero(keys % 3 == 1)[0].astype(np.int32)
+    (pk,), rows, offs = ctx.radix_partition([sx.col(dev(keys))], [0], 5, in_sel=dev(sel), rows=True)
+    rows = rows.cpu().numpy()
+    assert np.array_equal(np.sort(rows), sel)
+    assert np.array_equal(pk.cpu().numpy(), keys[rows])
+
+
+@pytest.mark.parametrize("zipf", [False, True])
+@pytest.mark.parametrize("strategy", [1, 2])
+def test_join_mbench_vs_closed_form(ctx, zipf, strategy):
+    nb, np_ = 1 << 16, (1 << 20) + 13
+    bk, bp = gen.mb_join_build(nb, device="cuda")
+    pk, pp = gen.mb_join_probe(nb, np_, zipf, seed=11, device="cuda")
+    want = oracle.mb_join_closed(nb, pk.cpu().numpy(), pp.cpu().numpy())
+    prow, brow, (gb, gp), used = ctx.hash_join([sx.col(bk), sx.col(bp)], [0], [sx.col(pk), sx.col(pp)], [0],
+                                               "inner", unique=True, bp=[1], pp=[1], strategy=strategy)
+    assert used == strategy
+    gb, gp = gb.cpu().numpy(), gp.cpu().numpy()
+    got = {"count": len(gb), "sum_build": int(gb.sum()), "sum_probe": int(gp.sum()), "pair_hash": np_pair_mix(gb, gp)}
+    assert got == want
+    # row ids are consistent with the payloads (payload = row id in this workload)
+    assert np.array_equal(prow.cpu().numpy().astype(np.int64), gp)
+    assert np.array_equal(brow.cpu().numpy().astype(np.int64), gb)
+
+
+@pytest.mark.parametrize("nkeys", [1, 2])
+def test_partitioned_join_vs_or_join(ctx, nkeys):
+    """Partitioned INNER join on a unique build with misses, int32 / packed two-key columns, a
+    selection on each side: the multiset of (probe row, build row) pairs equals or_join's."""
+    rng = np.random.default_rng(nkeys)
+    nb, np_ = 40_000, 250_003
+    if nkeys == 1:
+        bkey = rng.permutation(np.arange(-nb, nb * 3, dtype=np.int32))[:nb]
+        pkey = rng.integers(-nb * 2, nb * 4, np_, dtype=np.int64).astype(np.int32)
+        bcols, pcols = [sx.col(dev(bkey))], [sx.col(dev(pkey))]
+        bk64, pk64 = bkey.astype(np.int64), pkey.astype(np.int64)
+        keys = [0]
+    else:
+        u = rng.permutation(np.arange(nb * 2, dtype=np.int64))[:nb]
+        b0, b1 = (u // 7).astype(np.int32), (u % 7).astype(np.int32)
+        pu = rng.integers(0, nb * 3, np_, dtype=np.int64)
+        p0, p1 = (pu // 7).astype(np.int32), (pu % 7).astype(np.int32)
+        bcols, pcols = [sx.col(dev(b0)), sx.col(dev(b1))], [sx.col(dev(p0)), sx.col(dev(p1))]
+        bk64 = (b0.astype(np.int64) << 32) | b1.astype(np.int64)
+        pk64 = (p0.astype(np.int64) << 32) | p1.astype(np.int64)
+        keys = [0, 1]
+    bsel = np.nonzero(rng.random(nb) < 0.9)[0].astype(np.int32)
+    psel = np.nonzero(rng.random(np_) < 0.7)[0].astype(np.int32)
+    prow, brow, _, used = ctx.hash_join(bcols, keys, pcols, keys, "inner", unique=True, strategy=2,
+                                        build_sel=dev(bsel), probe_sel=dev(psel))
+    assert used == 2
+    got = sorted(zip(prow.cpu().numpy().tolist(), brow.cpu().numpy().tolist()))
+    op, ob = oracle.join(bk64[bsel], pk64[psel], "inner")
+    want = sorted(zip(psel[op].tolist(), bsel[ob].tolist()))
+    assert got == want
+
+
+def test_join_empty_sides(ctx):
+    e64 = dev(np.zeros(0, np.int64))
+    k = dev(np.arange(10, dtype=np.int64))
+    for b, p in ((e64, k), (k, e64), (e64, e64)):
+        for strategy in (1, 2):
+            prow, brow, _, _ = ctx.hash_join([sx.col(b)], [0], [sx.col(p)], [0], "inner", strategy=strategy)
+            assert len(prow) == 0 and len(brow) == 0

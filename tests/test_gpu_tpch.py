@@ -140,3 +140,15 @@ def test_q1_q6_dense_guard_and_tails(ctx, trunc):
         want = oracle.run_query(q, host)
         got = T.run(q)
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
+
+
+@pytest.mark.parametrize("plan", ["fused", "ops"])
+def test_q9_plans(small, monkeypatch, plan):
+    """Q9 through the fused probe-chain group-by (default) and the operator-at-a-time plan."""
+    sfm, host, T = small
+    if plan == "ops":
+        monkeypatch.setenv("SX_Q9_PLAN", "ops")
+    for over in ({}, dict(q9_color="blue")):
+        got = T.run("q9", tpch.default_params(**over))
+        want = oracle.run_query("q9", host, oracle.default_params(**over))
+        assert rows_equal(got, want), diff_rows(got, want)
