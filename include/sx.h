@@ -180,8 +180,14 @@ sx_status sx_groupby_agg(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_ke
  *   SX_ANTI:  each probe row with no match, once, ascending -> out_probe
  * Payload gather (fused materialization): out_payload[0..nbp) = build_cols[bp[i]]
  * at the matched build rows (INNER only), then out_payload[nbp..nbp+npp) =
- * probe_cols[pp[j]] at the output probe rows.  Syncs once (output length). */
+ * probe_cols[pp[j]] at the output probe rows.  Syncs once (output length). *
+ * unique_hint flags: SX_BUILD_UNIQUE (1) as above; SX_BUILD_MEMBERSHIP (2): only SEMI/ANTI probes
+ * will follow, so when the exact key-range bitmap exists (one key column, key range <= 2^30) the
+ * table itself is not built (probes answer from the bitmap); INNER probes of such a table return
+ * SX_EINVAL. */
 typedef enum { SX_INNER = 0, SX_SEMI = 1, SX_ANTI = 2 } sx_join;
+#define SX_BUILD_UNIQUE 1
+#define SX_BUILD_MEMBERSHIP 2
 sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, const int32_t* key_cols, int nkeys,
                         const sx_sel* in_sel, const sx_pred* where, int nwhere, int unique_hint, sx_ht** out);
 sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* probe_cols, int nprobe_cols,

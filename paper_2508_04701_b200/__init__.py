@@ -187,14 +187,14 @@ class Ctx:
             return [ok[i] for i in range(len(keys))], [oa[i] for i in range(len(aggs))], ng.value
         return [self.take_col(ok[i]) for i in range(len(keys))], [self.take_col(oa[i]) for i in range(len(aggs))], ng.value
 
-    def hash_build(self, cols, key_cols, in_sel=None, where=(), unique=False):
+    def hash_build(self, cols, key_cols, in_sel=None, where=(), unique=False, membership=False):
         ca = (A.Col * max(len(cols), 1))(*cols)
         kc = (C.c_int32 * len(key_cols))(*key_cols)
         pa, keep = preds(where)
         h = C.c_void_p()
         isel = self.sel(in_sel) if in_sel is not None else None
         self.check(self.L.sx_hash_build(self.h, ca, len(cols), kc, len(key_cols), C.byref(isel) if isel else None, pa,
-                                        len(where), 1 if unique else 0, C.byref(h)))
+                                        len(where), (1 if unique else 0) | (2 if membership else 0), C.byref(h)))
         return HashTable(self, h)
 
     def hash_probe(self, ht, cols, key_cols, jtype, in_sel=None, where=(), build_cols=(), bp=(), pp=()):

@@ -86,6 +86,62 @@ __global__ void __launch_bounds__(kBlock, 4) k_compact_local(const __grid_consta
   }
 }
 
+// Dense variant of phase 1 (no input selection; functors with eval_dense): thread t of a tile owns
+// ITEMS consecutive rows, which the functor reads with 128-bit vector loads and returns as a bit
+// mask; survivors are ranked by a block scan of the per-thread counts and written (ascending) to
+// the tile's scratch region.  Same scratch layout and phases 2-3 as k_compact_local.
+template <class F, int ITEMS>
+__global__ void __launch_bounds__(kBlock, 3) k_compact_dense(const __grid_constant__ F f, int64_t n,
+                                                          int32_t* __restrict__ s_row, int32_t* __restrict__ s_aux,
+                                                          int32_t* __restrict__ tile_cnt, int64_t ntiles) {
+  constexpr int W = kBlock / 32;
+  __shared__ int s_w[W];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * (int64_t)(kBlock * ITEMS);
+    const int64_t r0 = base + (int64_t)threadIdx.x * ITEMS;
+    uint32_t mask = 0;
+    int32_t aux[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) aux[i] = -1;
+    if (r0 < n) f.template eval_dense<ITEMS>(r0, n, mask, aux);
+    const int c = __popc(mask);
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    int wo = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const int v = s_w[q];
+      wo += q < w ? v : 0;
+      tot += v;
+    }
+    int pos = wo + x - c;
+    int32_t* tr = s_row + base;
+    int32_t* ta = s_aux ? s_aux + base : nullptr;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if ((mask >> i) & 1u) {
+        tr[pos] = (int32_t)(r0 + i);
+        if (ta) ta[pos] = aux[i];
+        ++pos;
+      }
+    }
+    if (threadIdx.x == 0) tile_cnt[tile] = tot;
+    __syncthreads();
+  }
+}
+
+template <class F, class = void>
+struct dense_items { static constexpr int value = 0; };
+template <class F>
+struct dense_items<F, std::void_t<decltype(F::kDenseItems)>> { static constexpr int value = F::kDenseItems; };
+
 // exclusive scan of int32 tile counts into int64 offsets (offsets[ntiles] = total)
 static __global__ void __launch_bounds__(1024) k_scan_counts_local(const int32_t* __restrict__ cnt, int64_t n,
                                                                    int64_t* __restrict__ off,
@@ -185,6 +241,11 @@ inline sx_status scan_counts(sx_ctx* ctx, const int32_t* cnt, int64_t n, int64_t
 // Outputs are allocated here at the exact count (known after the scan): *out_sel always,
 // *out_aux when out_aux != nullptr, and every gs.g[g].dst that is nullptr (count * width bytes).
 // Ownership of all of them passes to the caller (also on error paths they are freed here).
+template <class F, int ITEMS, bool DENSE, class AllocFn>
+sx_status run_compact_tiles(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel, int32_t** out_sel,
+                            int32_t** out_aux, GatherSpec& gs, int64_t* out_count, const bool* owned,
+                            AllocFn& alloc_outputs);
+
 template <class F, int ITEMS = 8>
 sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel, int32_t** out_sel,
                       int32_t** out_aux, GatherSpec& gs, int64_t* out_count) {
@@ -213,6 +274,18 @@ sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel,
     return SX_OK;
   };
   if (n == 0) return alloc_outputs(0);
+  constexpr int DI = dense_items<F>::value;
+  if constexpr (DI > 0) {
+    if (!in_sel) return run_compact_tiles<F, DI, true>(ctx, f, n, in_sel, out_sel, out_aux, gs, out_count, owned,
+                                                       alloc_outputs);
+  }
+  return run_compact_tiles<F, ITEMS, false>(ctx, f, n, in_sel, out_sel, out_aux, gs, out_count, owned, alloc_outputs);
+}
+
+template <class F, int ITEMS, bool DENSE, class AllocFn>
+sx_status run_compact_tiles(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel, int32_t** out_sel,
+                            int32_t** out_aux, GatherSpec& gs, int64_t* out_count, const bool* owned,
+                            AllocFn& alloc_outputs) {
   constexpr int TILE = kBlock * ITEMS;
   const int64_t ntiles = (n + TILE - 1) / TILE;
   Scratch scr(ctx);
@@ -225,7 +298,9 @@ sx_status run_compact(sx_ctx* ctx, const F& f, int64_t n, const int32_t* in_sel,
   const int64_t nb = (ntiles + 1023) / 1024;
   SX_TRY(scr.get(&bsum, (size_t)nb + 1));
   unsigned grid = persistent_grid(ctx, 8, ntiles);
-  if (in_sel)
+  if constexpr (DENSE)
+    k_compact_dense<F, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, s_row, s_aux, cnt, ntiles);
+  else if (in_sel)
     k_compact_local<F, true, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, s_row, s_aux, cnt, ntiles);
   else
     k_compact_local<F, false, ITEMS><<<grid, kBlock, 0, SX_STREAM(ctx)>>>(f, n, in_sel, s_row, s_aux, cnt, ntiles);

@@ -52,7 +52,88 @@ __device__ __forceinline__ void apply_pred(const DCol& c, const DPred& q, const 
   }
 }
 
+// ---- dense (selection-free) evaluation: a thread owns ITEMS consecutive rows r0.. (r0 % ITEMS == 0)
+// and loads each column with 128-bit vector loads (column buffers are 16-byte aligned) marked
+// streaming (ld.global.cs: evict-first, so scanned columns do not push the probed hash tables and
+// bitmaps out of L2); `full`
+// means all ITEMS rows exist (else the tail is loaded row by row).  Results are bit masks.
+template <int ITEMS>
+__device__ __forceinline__ void dense_load(const DCol& c, int64_t r0, int64_t n, bool full, int64_t (&x)[ITEMS]) {
+  static_assert(ITEMS % 4 == 0, "dense rows come in groups of 4");
+  if (full) {
+    switch (c.type) {
+      case SX_U8: {
+#pragma unroll
+        for (int j = 0; j < ITEMS / 4; ++j) {
+          const uint32_t v = __ldcs((const unsigned int*)((const uint8_t*)c.p + r0) + j);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) x[4 * j + b] = (int64_t)((v >> (8 * b)) & 0xffu);
+        }
+        return;
+      }
+      case SX_I32:
+      case SX_DATE32: {
+#pragma unroll
+        for (int j = 0; j < ITEMS / 4; ++j) {
+          const int4 v = __ldcs((const int4*)((const int32_t*)c.p + r0) + j);
+          x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+        }
+        return;
+      }
+      default: {
+#pragma unroll
+        for (int j = 0; j < ITEMS / 2; ++j) {
+          const longlong2 v = __ldcs((const longlong2*)((const long long*)c.p + r0) + j);
+          x[2 * j] = v.x; x[2 * j + 1] = v.y;
+        }
+        return;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) x[i] = r0 + i < n ? ldv(c, r0 + i) : 0;
+}
+
+template <int ITEMS>
+__device__ __forceinline__ uint32_t dense_valid(int64_t r0, int64_t n) {
+  const int64_t m = n - r0;
+  return m >= ITEMS ? (ITEMS == 32 ? 0xffffffffu : ((1u << ITEMS) - 1u)) : (m <= 0 ? 0u : ((1u << m) - 1u));
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void dense_pred(const DCol& c, const DPred& q, int64_t r0, int64_t n, bool full,
+                                           uint32_t& mask) {
+  int64_t x[ITEMS];
+  dense_load<ITEMS>(c, r0, n, full, x);
+  uint32_t m = 0;
+  const int64_t lo = q.lo, hi = q.hi;
+  switch (q.op) {  // uniform
+#define SX_DENSE(OPC, EXPR)                                                     \
+  case OPC:                                                                     \
+    _Pragma("unroll") for (int i = 0; i < ITEMS; ++i) m |= ((EXPR) ? 1u : 0u) << i; \
+    break;
+    SX_DENSE(SX_LT, x[i] < lo)
+    SX_DENSE(SX_LE, x[i] <= lo)
+    SX_DENSE(SX_GT, x[i] > lo)
+    SX_DENSE(SX_GE, x[i] >= lo)
+    SX_DENSE(SX_EQ, x[i] == lo)
+    SX_DENSE(SX_NE, x[i] != lo)
+    default:
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) m |= ((lo <= x[i] && x[i] <= hi) ? 1u : 0u) << i;
+#undef SX_DENSE
+  }
+  mask &= m;
+}
+
 struct ConjFn {
+  static constexpr int kDenseItems = 16;
+  template <int ITEMS>
+  __device__ __forceinline__ void eval_dense(int64_t r0, int64_t n, uint32_t& mask, int32_t (&)[ITEMS]) const {
+    const bool full = r0 + ITEMS <= n;
+    mask = dense_valid<ITEMS>(r0, n);
+    for (int p = 0; p < np; ++p) dense_pred<ITEMS>(cols[preds[p].col], preds[p], r0, n, full, mask);
+  }
   DCol cols[SX_MAX_COLS];
   DPred preds[SX_MAX_PREDS];
   int np;

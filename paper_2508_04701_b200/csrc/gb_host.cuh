@@ -175,6 +175,156 @@ struct SlotFn {
   }
 };
 
+// ------------------------------------------------------------------ K10r: owned runs + HAVING
+// Sorted-input group-by with the HAVING predicate pushed into the aggregation (Q18's subquery:
+// 1.5e8 orderkey runs of 1-7 lineitems, ~6.4e3 survive).  Each thread takes kRunItems consecutive
+// rows and OWNS the groups whose first row lies among them; it sums each owned group in registers
+// (96-bit), reading past its rows while the key continues (at most kRunAhead rows, else the host
+// falls back), applies HAVING and appends only the survivors (atomic cursor).  No per-group state
+// is written for the groups that fail HAVING and no group numbering pass is needed; a key that
+// decreases anywhere flags the input as unsorted (host falls back to hashing).
+constexpr int kRunAhead = 64;
+
+template <class P, class = void>
+struct runs_dense : std::false_type {};
+template <class P>
+struct runs_dense<P, std::void_t<decltype(P::kDenseRuns)>> : std::integral_constant<bool, P::kMaxNst == 1> {};
+
+template <class P>
+__device__ __forceinline__ void runs_acc(int kd, int64_t v, unsigned long long& lo, int32_t& hi) {
+  if (kd == ST_SUM || kd == ST_COUNT) {
+    const unsigned long long nl = lo + (unsigned long long)v;
+    const bool cy = nl < lo, neg = v < 0;
+    if (kd == ST_SUM && cy != neg) hi += cy ? 1 : -1;
+    lo = nl;
+  } else {
+    const unsigned long long u = kd == ST_MIN ? ~order_u(v) : order_u(v);
+    lo = u > lo ? u : lo;
+  }
+}
+
+template <class P>
+__global__ void __launch_bounds__(kBlock) k_runs_own(const __grid_constant__ P prog, int64_t n,
+                                                     const __grid_constant__ Layout L, const __grid_constant__ SlotFn hv,
+                                                     uint8_t* __restrict__ out, int64_t cap_out,
+                                                     unsigned long long* cursor, int* flags) {
+  constexpr int NST = P::kMaxNst;
+  constexpr int R = kRunItems;
+  static_assert(NST <= 2, "k_runs_own keeps every state of a group in registers");
+  bool ovf = false;
+  for (int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * R; r0 < n;
+       r0 += (int64_t)gridDim.x * blockDim.x * R) {
+    int32_t row[R];
+    bool valid[R], alive[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      valid[i] = r0 + i < n;
+      alive[i] = valid[i];
+      row[i] = valid[i] ? (int32_t)(r0 + i) : 0;
+    }
+    uint64_t key[R], pk[1];
+    int64_t v[NST][R];
+    if constexpr (runs_dense<P>::value) {  // one-state programs with 128-bit row loads
+      prog.template runs_dense<R>(r0, n, key, v[0]);
+    } else {
+      typename P::template Cache<R> cache;
+      prog.template where_keys<R>(row, alive, key, cache);
+#pragma unroll
+      for (int a = 0; a < NST; ++a) {
+        if (a >= L.nst) break;
+        if (prog.kind(a, L) == ST_COUNT) {
+#pragma unroll
+          for (int i = 0; i < R; ++i) v[a][i] = 1;
+        } else {
+          prog.template state<R>(a, row, alive, cache, v[a], ovf);
+        }
+      }
+    }
+    int32_t prow[1] = {(int32_t)(r0 - 1)};
+    bool pv[1] = {r0 > 0};
+    prog.template keys_only<1>(prow, pv, pk);
+    bool bad = false;
+    unsigned long long lo[NST];
+    int32_t hi[NST];
+    bool owned = false;
+    uint64_t gkey = 0;
+    uint64_t prev = pk[0];
+    bool has_prev = pv[0];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (!valid[i]) break;
+      const bool head = !has_prev || key[i] != prev;
+      bad |= has_prev && (int64_t)key[i] < (int64_t)prev;
+      if (head) {
+        owned = true;
+        gkey = key[i];
+#pragma unroll
+        for (int a = 0; a < NST; ++a) { lo[a] = 0; hi[a] = 0; }
+      }
+      if (owned) {
+#pragma unroll
+        for (int a = 0; a < NST; ++a)
+          if (a < L.nst) runs_acc<P>(prog.kind(a, L), v[a][i], lo[a], hi[a]);
+      }
+      prev = key[i];
+      has_prev = true;
+      // does the owned group end at row i?
+      bool ends;
+      if (i + 1 < R && valid[i + 1]) {
+        ends = key[i + 1] != key[i];
+      } else if (r0 + i + 1 >= n) {
+        ends = true;
+      } else if (owned) {  // read ahead into the following rows while the key continues
+        ends = true;
+        int64_t r = r0 + i + 1;
+        int steps = 0;
+        for (; r < n && steps < kRunAhead; ++r, ++steps) {
+          int32_t rr[1] = {(int32_t)r};
+          bool al[1] = {true};
+          uint64_t kk[1];
+          typename P::template Cache<1> c1;
+          prog.template where_keys<1>(rr, al, kk, c1);
+          if (kk[0] != gkey) {
+            bad |= (int64_t)kk[0] < (int64_t)gkey;
+            break;
+          }
+#pragma unroll
+          for (int a = 0; a < NST; ++a) {
+            if (a >= L.nst) break;
+            int64_t vv[1] = {1};
+            if (prog.kind(a, L) != ST_COUNT) prog.template state<1>(a, rr, al, c1, vv, ovf);
+            runs_acc<P>(prog.kind(a, L), vv[0], lo[a], hi[a]);
+          }
+        }
+        if (steps == kRunAhead && r < n) atomicExch(flags + 1, 1);  // a long run: host falls back
+      } else {
+        ends = false;
+      }
+      if (ends && owned) {
+        alignas(16) uint8_t buf[64];
+        if (L.key_bytes == 4) *(unsigned*)buf = (unsigned)gkey;
+        else *(unsigned long long*)buf = gkey;
+#pragma unroll
+        for (int a = 0; a < NST; ++a) {
+          if (a >= L.nst) break;
+          *(unsigned long long*)(buf + L.off8[a]) = lo[a];
+          if (L.kind[a] == ST_SUM) *(int*)(buf + L.off4[a]) = hi[a];
+        }
+        if (hv.hv_ok(buf)) {
+          const unsigned long long pos = atomicAdd(cursor, 1ull);
+          if ((int64_t)pos < cap_out) {
+            uint8_t* d = out + pos * L.slot_bytes;
+            for (int b = 0; b < L.slot_bytes; b += 4) *(unsigned*)(d + b) = *(const unsigned*)(buf + b);
+          }
+        }
+        owned = false;
+      }
+    }
+    if (bad) atomicExch(flags, 1);
+  }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
+}
+
 struct EmitArgs {
   const uint8_t* slots;
   const int32_t* ids;
@@ -305,7 +455,60 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
     // SX_GB_SORTED: 0 = never, 2 = whenever eligible regardless of table size (tests)
     const char* env = getenv("SX_GB_SORTED");
     const int mode = env ? atoi(env) : 1;
-    if (mode != 0 && !small && !keyless && P.nkeys == 1 && !sel && n > 0 && prog.no_filter() &&
+    bool own_done = false;
+    if constexpr (Prog::kMaxNst <= 2) {
+      // K10r: HAVING pushed into an owned-run aggregation (no per-group state written)
+      if (mode != 0 && !small && !keyless && P.nkeys == 1 && !sel && n > 0 && prog.no_filter() && P.has_having &&
+          L.slot_bytes <= 64 && (mode == 2 || cap * (uint64_t)L.slot_bytes > ctx->l2_bytes / 2)) {
+        SlotFn hv;
+        std::memset(&hv, 0, sizeof hv);
+        hv.has_having = 1;
+        const int sh = P.agg_state[P.hv.agg];
+        hv.hv_kind = L.kind[sh];
+        hv.hv_off8 = L.off8[sh];
+        hv.hv_off4 = L.off4[sh];
+        hv.hv_op = P.hv.op;
+        hv.hv_lo = P.hv.lo;
+        hv.hv_hi = P.hv.hi;
+        int64_t cap_out = std::max<int64_t>(1 << 16, n / 256);
+        unsigned long long* cursor = (unsigned long long*)ctx->d_counters;
+        for (int attempt = 0; attempt < 2 && !own_done; ++attempt) {
+          uint8_t* out;
+          SX_TRY(scr.get(&out, (size_t)cap_out * L.slot_bytes));
+          SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
+          SX_CUDA(cudaMemsetAsync(cursor, 0, 8, ctx->stream));
+          const int64_t threads = (n + kRunItems - 1) / kRunItems;
+          k_runs_own<Prog><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+              prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
+          SX_CHECK_LAUNCH();
+          int64_t cnt = 0;
+          SX_TRY(read_i64(ctx, cursor, &cnt));
+          SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
+          if (flags[2] || flags[3]) break;  // unsorted or a run longer than kRunAhead: other strategies
+          if (flags[0]) return set_err(ctx, SX_EOVERFLOW, "a value expression left int64");
+          if (cnt > cap_out) {
+            cap_out = cnt;
+            continue;
+          }
+          // the survivors form a dense table of cnt groups for the extraction below
+          SlotFn sf = hv;
+          sf.slots = out;
+          sf.cap = (uint64_t)cnt;
+          sf.slot_bytes = L.slot_bytes;
+          sf.key_bytes = 0;
+          sf.nsub = 1;
+          sf.side_used = ctx->d_flags + 2;
+          GatherSpec none;
+          none.n = 0;
+          SX_TRY(run_compact(ctx, sf, cnt, nullptr, &ids, nullptr, none, &ng));
+          scr.ptrs.push_back(ids);
+          table = out;
+          cap_p = (uint64_t)cnt;
+          sorted_done = own_done = true;
+        }
+      }
+    }
+    if (!own_done && mode != 0 && !small && !keyless && P.nkeys == 1 && !sel && n > 0 && prog.no_filter() &&
         (mode == 2 || cap * (uint64_t)L.slot_bytes > ctx->l2_bytes / 2)) {
       const int64_t ntiles = (n + kRunTile - 1) / kRunTile;
       int32_t* heads;

@@ -45,7 +45,8 @@ __global__ void __launch_bounds__(kBlock) k_build(const __grid_constant__ BuildA
     mn = min(mn, (long long)key);
     mx = max(mx, (long long)key);
     uint64_t h = table_hash(key, a.key_bytes) & a.mask;
-    if (a.key_bytes == 4) {
+    if (!a.slots) {  // membership-only build: count and key range only
+    } else if (a.key_bytes == 4) {
       unsigned long long* s = (unsigned long long*)a.slots;
       unsigned long long v = ((unsigned long long)(uint32_t)r << 32) | (uint32_t)key;
       while (atomicCAS(s + h, ~0ull, v) != ~0ull) h = (h + 1) & a.mask;
@@ -296,19 +297,25 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
   while (cap < (uint64_t)(2 * n)) cap <<= 1;
   size_t slot_bytes = a.key_bytes == 4 ? 8 : 16;
   if (cap * slot_bytes * 2 <= (32ull << 20)) cap <<= 1;  // small (L2-resident) tables: load <= 0.25
+  // unique_hint bit 1 (SX_BUILD_MEMBERSHIP): only semi/anti probes will follow; when the exact
+  // key-range bitmap can be built (one key column, range <= 2^30) the table itself is omitted
+  const bool membership = (unique_hint & 2) != 0 && nkeys == 1;
   sx_ht* ht = new sx_ht();
   ht->key_bytes = a.key_bytes;
   ht->key_types[0] = types[0];
   ht->key_types[1] = types[1];
   ht->nkeys = nkeys;
-  ht->unique = unique_hint != 0;
+  ht->unique = (unique_hint & 1) != 0;
   ht->cap = cap;
-  sx_status s = alloc(ctx, (char**)&ht->slots, cap * slot_bytes);
-  if (s != SX_OK) {
-    delete ht;
-    return s;
+  sx_status s = SX_OK;
+  if (!membership) {
+    s = alloc(ctx, (char**)&ht->slots, cap * slot_bytes);
+    if (s != SX_OK) {
+      delete ht;
+      return s;
+    }
+    cudaMemsetAsync(ht->slots, 0xff, cap * slot_bytes, ctx->stream);
   }
-  cudaMemsetAsync(ht->slots, 0xff, cap * slot_bytes, ctx->stream);
   // counters: [0] inserted rows, [1] min key, [2] max key
   unsigned long long* ins = (unsigned long long*)ctx->d_counters;
   int64_t* init = ctx->h_pinned + 8;
@@ -332,6 +339,21 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
     return e != cudaSuccess ? set_err(ctx, SX_ECUDA, "build: %s", cudaGetErrorString(e)) : s;
   }
   ht->rows = stats[0];
+  const bool bm_ok = nkeys == 1 && stats[0] > 0 && stats[2] >= stats[1] &&
+                     (unsigned long long)(stats[2] - stats[1]) + 1 <= (1ull << 30);
+  if (membership && !bm_ok && stats[0] > 0) {  // no bitmap possible: build the table after all
+    s = alloc(ctx, (char**)&ht->slots, cap * slot_bytes);
+    if (s != SX_OK) {
+      delete ht;
+      return s;
+    }
+    cudaMemsetAsync(ht->slots, 0xff, cap * slot_bytes, ctx->stream);
+    a.slots = ht->slots;
+    cudaMemcpyAsync(ins, init, 3 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream);
+    k_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+    SX_CHECK_LAUNCH();
+  }
+  if (membership && !ht->slots) ht->cap = 0;
   // exact bitmap filter over the key range when it is small enough to stay cache-resident-ish
   if (nkeys == 1 && stats[0] > 0) {
     unsigned long long range = (unsigned long long)(stats[2] - stats[1]) + 1;
@@ -388,6 +410,8 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
   ProfScope ps(ctx, join_type == SX_INNER ? "probe_inner" : (join_type == SX_SEMI ? "probe_semi" : "probe_anti"));
   if (join_type < SX_INNER || join_type > SX_ANTI) return set_err(ctx, SX_EINVAL, "join type %d", join_type);
   if (join_type == SX_INNER && !out_build) return set_err(ctx, SX_EINVAL, "INNER join needs out_build");
+  if (!ht->slots && (join_type == SX_INNER || !ht->bm))
+    return set_err(ctx, SX_EINVAL, "membership-only table: SEMI/ANTI probes only");
   if (join_type != SX_INNER && nbp > 0) return set_err(ctx, SX_EINVAL, "build payload only for INNER joins");
   if (nbp + npp > kMaxGather || nbp < 0 || npp < 0) return set_err(ctx, SX_EINVAL, "too many payload columns");
   if ((nbp + npp) > 0 && !out_payload) return set_err(ctx, SX_EINVAL, "out_payload is NULL");

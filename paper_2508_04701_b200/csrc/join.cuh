@@ -55,19 +55,51 @@ struct ProbeFnT {
     for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i];
     for (int p = 0; p < np; ++p) apply_pred<ITEMS>(cols[preds[p].col], preds[p], row, alive);
     uint64_t key[ITEMS];
-    uint32_t h[ITEMS];
-    bool pend[ITEMS], found[ITEMS];
-    uint32_t cnt[ITEMS];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      key[i] = alive[i] ? (uint64_t)(int64_t)__ldg(k0 + row[i]) : 0;
-      cnt[i] = 0;
-    }
+    for (int i = 0; i < ITEMS; ++i) key[i] = alive[i] ? (uint64_t)(int64_t)__ldg(k0 + row[i]) : 0;
     if (NK == 2) {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i)
         key[i] = (key[i] << 32) | (uint32_t)(alive[i] ? __ldg(k1 + row[i]) : 0);
     }
+    probe<ITEMS>(key, alive, aux);
+  }
+  // Dense path (no input selection): predicate and key columns of ITEMS consecutive rows with
+  // 128-bit vector loads, all issued before the bitmap / table lookups.
+  static constexpr int kDenseItems = 8;
+  template <int ITEMS>
+  __device__ __forceinline__ void eval_dense(int64_t r0, int64_t n, uint32_t& mask, int32_t (&aux)[ITEMS]) const {
+    const bool full = r0 + ITEMS <= n;
+    mask = dense_valid<ITEMS>(r0, n);
+    int64_t k[ITEMS];
+    dense_load<ITEMS>(DCol{k0, sizeof(KT) == 4 ? SX_I32 : SX_I64, 0}, r0, n, full, k);
+    for (int p = 0; p < np; ++p) dense_pred<ITEMS>(cols[preds[p].col], preds[p], r0, n, full, mask);
+    uint64_t key[ITEMS];
+    bool alive[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      alive[i] = (mask >> i) & 1u;
+      key[i] = (uint64_t)k[i];
+    }
+    if (NK == 2) {
+      int64_t k2[ITEMS];
+      dense_load<ITEMS>(DCol{k1, SX_I32, 0}, r0, n, full, k2);
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) key[i] = (key[i] << 32) | (uint32_t)k2[i];
+    }
+    probe<ITEMS>(key, alive, aux);
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) m |= (alive[i] ? 1u : 0u) << i;
+    mask = m;
+  }
+  template <int ITEMS>
+  __device__ __forceinline__ void probe(uint64_t (&key)[ITEMS], bool (&alive)[ITEMS], int32_t (&aux)[ITEMS]) const {
+    uint32_t h[ITEMS];
+    bool pend[ITEMS], found[ITEMS];
+    uint32_t cnt[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) cnt[i] = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       h[i] = (uint32_t)(KB == 4 ? hash32((uint32_t)key[i]) : hash64(key[i])) & mask;

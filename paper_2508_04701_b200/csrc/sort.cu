@@ -190,82 +190,129 @@ struct AcceptedFn {
 };
 
 // ---- LSD radix sort -----------------------------------------------------------------
-constexpr int kLsdTile = 256;
+// Per varying 8-bit digit (least significant first): K13a per-tile digit counts, a multi-block
+// exclusive scan of the digit-major count matrix, K13b stable scatter.  A tile is kLsdThreads x
+// ITEMS elements; warp w owns the contiguous sub-tile [w*32*ITEMS, (w+1)*32*ITEMS) in (item,
+// lane) order, so a per-warp running digit counter (match_any leaders) gives every element its
+// stable rank; the tile is then reordered in shared memory and written digit run by digit run
+// (coalesced).  Sorting is stable, so the position word is carried, never sorted on.
+constexpr int kLsdThreads = 256;
+constexpr int kLsdWarps = kLsdThreads / 32;
 
-__global__ void __launch_bounds__(kLsdTile) k_lsd_hist(const uint32_t* __restrict__ dw, int shift, int64_t n,
-                                                       unsigned* counts /* [256][ntiles] */, int64_t ntiles) {
-  __shared__ unsigned h[256];
+template <int ITEMS>
+__global__ void __launch_bounds__(kLsdThreads) k_lsd_count(const uint32_t* __restrict__ dw, int shift, int64_t n,
+                                                           int32_t* counts /* [256][ntiles] */, int64_t ntiles) {
+  __shared__ int h[256];
   h[threadIdx.x] = 0;
   __syncthreads();
-  int64_t i = blockIdx.x * (int64_t)kLsdTile + threadIdx.x;
-  if (i < n) atomicAdd(&h[(dw[i] >> shift) & 0xff], 1u);
+  const int64_t base = blockIdx.x * (int64_t)(kLsdThreads * ITEMS);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t e = base + (int64_t)i * kLsdThreads + threadIdx.x;
+    if (e < n) atomicAdd(&h[(__ldg(dw + e) >> shift) & 0xff], 1);
+  }
   __syncthreads();
   counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-// exclusive scan of counts in digit-major order (one CTA; the array is 256 * ntiles long)
-__global__ void __launch_bounds__(1024) k_lsd_scan(unsigned* counts, int64_t len) {
-  __shared__ unsigned long long carry;
-  __shared__ unsigned long long wsum[32];
-  if (threadIdx.x == 0) carry = 0;
+template <int ITEMS>
+__global__ void __launch_bounds__(kLsdThreads) k_lsd_scatter(const __grid_constant__ Words src,
+                                                             const __grid_constant__ Words dst, int dword, int shift,
+                                                             int64_t n, const int64_t* __restrict__ offs,
+                                                             int64_t ntiles) {
+  constexpr int T = kLsdThreads * ITEMS;
+  extern __shared__ uint32_t stage[];  // [nwords][T]
+  __shared__ int wcnt[kLsdWarps][256];
+  __shared__ int dstart[256];
+  __shared__ int s_warp[kLsdWarps];
+  __shared__ uint8_t sdig[T];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = src.nwords;
+  const int64_t base = blockIdx.x * (int64_t)T;
+  for (int j = threadIdx.x; j < kLsdWarps * 256; j += kLsdThreads) (&wcnt[0][0])[j] = 0;
   __syncthreads();
-  for (int64_t base = 0; base < len; base += blockDim.x) {
-    int64_t i = base + threadIdx.x;
-    unsigned long long v = i < len ? counts[i] : 0;
-    unsigned long long x = v;
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int dig[ITEMS], rank[ITEMS];
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t e = base + (int64_t)w * 32 * ITEMS + i * 32 + lane;
+    const bool v = e < n;
+    const int d = v ? (int)((__ldg(src.w[dword] + e) >> shift) & 0xff) : 256 + lane;
+    const unsigned peers = __match_any_sync(kFull, d);
+    const int leader = __ffs(peers) - 1;
+    int r = 0;
+    if (v) r = wcnt[w][d] + __popc(peers & lt);
+    __syncwarp();
+    if (v && lane == leader) wcnt[w][d] += __popc(peers);
+    __syncwarp();
+    dig[i] = v ? d : -1;
+    rank[i] = r;
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over warps (in place), tile total -> tile-local digit starts
+  {
+    const int d = threadIdx.x;  // kLsdThreads == 256 digits
+    int run = 0;
+#pragma unroll
+    for (int q = 0; q < kLsdWarps; ++q) {
+      const int c = wcnt[q][d];
+      wcnt[q][d] = run;
+      run += c;
+    }
+    int x = run;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      unsigned long long y = __shfl_up_sync(kFull, x, o);
+      const int y = __shfl_up_sync(kFull, x, o);
       if (lane >= o) x += y;
     }
-    if (lane == 31) wsum[w] = x;
+    if (lane == 31) s_warp[w] = x;
     __syncthreads();
-    if (w == 0) {
-      unsigned long long t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned long long y = __shfl_up_sync(kFull, t, o);
-        if (lane >= o) t += y;
-      }
-      wsum[lane] = t;
-    }
-    __syncthreads();
-    unsigned long long incl = x + (w ? wsum[w - 1] : 0) + carry;
-    if (i < len) counts[i] = (unsigned)(incl - v);
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = incl;
-    __syncthreads();
+    int wo = 0;
+    for (int q = 0; q < w; ++q) wo += s_warp[q];
+    dstart[d] = wo + x - run;
+  }
+  __syncthreads();
+  // reorder the tile in shared memory (all words), then write digit runs to their offsets
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (dig[i] < 0) continue;
+    const int64_t e = base + (int64_t)w * 32 * ITEMS + i * 32 + lane;
+    const int pos = dstart[dig[i]] + wcnt[w][dig[i]] + rank[i];
+    sdig[pos] = (uint8_t)dig[i];
+    for (int j = 0; j < nw; ++j) stage[j * T + pos] = __ldg(src.w[j] + e);
+  }
+  __syncthreads();
+  const int tcount = (int)min((int64_t)T, n - base);
+  for (int p = threadIdx.x; p < tcount; p += kLsdThreads) {
+    const int d = sdig[p];
+    const int64_t g = offs[(int64_t)d * ntiles + blockIdx.x] + (p - dstart[d]);
+    for (int j = 0; j < nw; ++j) dst.w[j][g] = stage[j * T + p];
   }
 }
 
-__global__ void __launch_bounds__(kLsdTile) k_lsd_scatter(const __grid_constant__ Words src, const __grid_constant__ Words dst,
-                                                          int dword, int shift, int64_t n, const unsigned* offsets,
-                                                          int64_t ntiles) {
-  __shared__ unsigned wc[kLsdTile / 32][256];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int d = threadIdx.x; d < 256; d += blockDim.x)
-    for (int q = 0; q < kLsdTile / 32; ++q) wc[q][d] = 0;
-  __syncthreads();
-  int64_t i = blockIdx.x * (int64_t)kLsdTile + threadIdx.x;
-  bool valid = i < n;
-  int d = valid ? (int)((src.w[dword][i] >> shift) & 0xff) : 256 + lane;  // unique dummy digits for invalid lanes
-  unsigned peers = __match_any_sync(kFull, d);
-  int rank = __popc(peers & lanemask_lt());
-  if (valid && rank == 0) wc[w][d] = __popc(peers);
-  __syncthreads();
-  // exclusive prefix over warps for each digit
-  if (threadIdx.x < 256) {
-    unsigned run = 0;
-    for (int q = 0; q < kLsdTile / 32; ++q) {
-      unsigned c = wc[q][threadIdx.x];
-      wc[q][threadIdx.x] = run;
-      run += c;
-    }
+template <int ITEMS>
+sx_status lsd_sort(sx_ctx* ctx, Scratch& scr, Words*& a, Words*& b, int nwords, int64_t n,
+                   const std::vector<std::pair<int, int>>& digits) {
+  constexpr int T = kLsdThreads * ITEMS;
+  const int64_t ntiles = (n + T - 1) / T;
+  int32_t* counts;
+  int64_t* offs;
+  SX_TRY(scr.get(&counts, (size_t)(256 * ntiles)));
+  SX_TRY(scr.get(&offs, (size_t)(256 * ntiles) + 1));
+  const size_t smem = (size_t)nwords * T * sizeof(uint32_t);
+  SX_CUDA(cudaFuncSetAttribute(k_lsd_scatter<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int p = (int)digits.size() - 1; p >= 0; --p) {
+    if (digits[p].first == nwords - 1) continue;  // position word: carried, not sorted on (stability)
+    int64_t total = 0;
+    k_lsd_count<ITEMS><<<(unsigned)ntiles, kLsdThreads, 0, SX_STREAM(ctx)>>>(a->w[digits[p].first], digits[p].second,
+                                                                              n, counts, ntiles);
+    SX_CHECK_LAUNCH();
+    SX_TRY(scan_counts(ctx, counts, 256 * ntiles, offs, &total));
+    k_lsd_scatter<ITEMS><<<(unsigned)ntiles, kLsdThreads, smem, SX_STREAM(ctx)>>>(*a, *b, digits[p].first,
+                                                                                 digits[p].second, n, offs, ntiles);
+    SX_CHECK_LAUNCH();
+    std::swap(a, b);
   }
-  __syncthreads();
-  if (valid) {
-    int64_t pos = (int64_t)offsets[(int64_t)d * ntiles + blockIdx.x] + wc[w][d] + rank;
-    for (int j = 0; j < src.nwords; ++j) dst.w[j][pos] = src.w[j][i];
-  }
+  return SX_OK;
 }
 
 }  // namespace
@@ -384,22 +431,15 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
     k_bitonic<<<1, 1024, smem, SX_STREAM(ctx)>>>(W, winners, m, outn, sel, perm);
     SX_CHECK_LAUNCH();
   } else {
-    // LSD radix sort over the varying digits, least significant first
+    // LSD radix sort over the varying key digits, least significant first
     Words W2{};
     W2.nwords = nwords;
     for (int j = 0; j < nwords; ++j) SX_TRY(scr.get(&W2.w[j], (size_t)n));
-    int64_t ntiles = (n + kLsdTile - 1) / kLsdTile;
-    unsigned* counts;
-    SX_TRY(scr.get(&counts, (size_t)(256 * ntiles)));
     Words* a = &W;
     Words* b = &W2;
-    for (int p = (int)digits.size() - 1; p >= 0; --p) {
-      k_lsd_hist<<<(unsigned)ntiles, kLsdTile, 0, SX_STREAM(ctx)>>>(a->w[digits[p].first], digits[p].second, n, counts, ntiles);
-      k_lsd_scan<<<1, 1024, 0, SX_STREAM(ctx)>>>(counts, 256 * ntiles);
-      k_lsd_scatter<<<(unsigned)ntiles, kLsdTile, 0, SX_STREAM(ctx)>>>(*a, *b, digits[p].first, digits[p].second, n, counts, ntiles);
-      SX_CHECK_LAUNCH();
-      std::swap(a, b);
-    }
+    if (nwords <= 3) SX_TRY(lsd_sort<16>(ctx, scr, a, b, nwords, n, digits));
+    else if (nwords <= 6) SX_TRY(lsd_sort<8>(ctx, scr, a, b, nwords, n, digits));
+    else SX_TRY(lsd_sort<4>(ctx, scr, a, b, nwords, n, digits));
     // positions (last word) of the first outn sorted rows -> row ids
     GatherSpec none;
     none.n = 0;

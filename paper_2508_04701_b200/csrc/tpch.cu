@@ -283,6 +283,40 @@ struct Q18Prog {
 #pragma unroll
     for (int i = 0; i < I; ++i) v[i] = c.q[i];
   }
+  // Dense rows for k_runs_own: R consecutive rows (r0 % R == 0) with 128-bit streaming loads.
+  static constexpr bool kDenseRuns = true;
+  template <int R>
+  __device__ __forceinline__ void runs_dense(int64_t r0, int64_t n, uint64_t (&key)[R], int64_t (&v)[R]) const {
+    static_assert(R % 4 == 0, "groups of 4 rows");
+    if (r0 + R <= n) {
+      if constexpr (sizeof(KT) == 4) {
+#pragma unroll
+        for (int j = 0; j < R / 4; ++j) {
+          const int4 k = __ldcs((const int4*)(okey + r0) + j);
+          key[4 * j] = (uint64_t)(int64_t)k.x; key[4 * j + 1] = (uint64_t)(int64_t)k.y;
+          key[4 * j + 2] = (uint64_t)(int64_t)k.z; key[4 * j + 3] = (uint64_t)(int64_t)k.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < R / 2; ++j) {
+          const longlong2 k = __ldcs((const longlong2*)(okey + r0) + j);
+          key[2 * j] = (uint64_t)k.x; key[2 * j + 1] = (uint64_t)k.y;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < R / 2; ++j) {
+        const longlong2 q = __ldcs((const longlong2*)(qty + r0) + j);
+        v[2 * j] = q.x; v[2 * j + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const bool in = r0 + i < n;
+        key[i] = in ? (uint64_t)(int64_t)__ldg(okey + r0 + i) : 0;
+        v[i] = in ? __ldg(qty + r0 + i) : 0;
+      }
+    }
+  }
 };
 
 // Q9: key (nationkey, year(o_orderdate)); state 0 sum(ext*(100-disc) - supplycost*qty)
@@ -387,12 +421,14 @@ struct Q9FusedProg {
     int32_t pk[I];
 #pragma unroll
     for (int i = 0; i < I; ++i) pk[i] = alive[i] ? __ldg(partkey + row[i]) : 0;
+    if (pbm) {  // rows not pre-selected by a semi-join: green-part membership here
 #pragma unroll
-    for (int i = 0; i < I; ++i) {
-      const unsigned long long off = (unsigned long long)((long long)pk[i] - pbm_min);
-      const bool in = alive[i] && off < pbm_bits;
-      const uint32_t w = in ? __ldg(pbm + (off >> 5)) : 0u;
-      alive[i] = in && ((w >> (off & 31)) & 1u);
+      for (int i = 0; i < I; ++i) {
+        const unsigned long long off = (unsigned long long)((long long)pk[i] - pbm_min);
+        const bool in = alive[i] && off < pbm_bits;
+        const uint32_t w = in ? __ldg(pbm + (off >> 5)) : 0u;
+        alive[i] = in && ((w >> (off & 31)) & 1u);
+      }
     }
     int32_t sk[I];
     KT ok[I];
@@ -753,26 +789,40 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   bag.keep(ht_p);
   sx_col gok[2], goa[1];
   int64_t ng = 0;
-  // Fused plan (default): build partsupp' / supplier / orders PK tables, then one pass over
-  // lineitem probing all of them inside the group-by (Q9FusedProg).  SX_Q9_PLAN=ops selects the
-  // operator-at-a-time plan below (materialising every join's output).
+  // Fused plan (default): lineitem semi-join green parts (selection only); PK tables for
+  // partsupp' (partkey, suppkey), supplier and the orders that have a green line (semi-join
+  // reduction through a membership-only build); then one group-by pass over the selected lineitem
+  // rows probing all three tables (Q9FusedProg).  SX_Q9_PLAN=ops: the operator-at-a-time plan below
+  // (every join output materialised).
   const bool ops_plan = getenv("SX_Q9_PLAN") && std::strcmp(getenv("SX_Q9_PLAN"), "ops") == 0;
   const bool okb4 = w4(t->o_orderkey) && w4(t->l_orderkey), okb8 = w8(t->o_orderkey) && w8(t->l_orderkey);
   if (!ops_plan && ht_p->bm && (okb4 || okb8) && w4(t->l_partkey) && w4(t->l_suppkey) && w8(t->l_quantity) &&
       w8(t->l_extendedprice) && w8(t->l_discount) && w4(t->ps_partkey) && w4(t->ps_suppkey) &&
       w8(t->ps_supplycost) && w4(t->s_suppkey) && w4(t->s_nationkey) && w4(t->o_orderdate)) {
+    // lineitem rows with a green part (exact bitmap semi-join; no columns materialised)
+    sx_sel sel_l;
+    SX_TRY(sx_hash_probe(ctx, ht_p, &t->l_partkey, 1, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0,
+                         nullptr, 0, &sel_l, nullptr, nullptr));
+    bag.keep(sel_l);
     sx_col pscols[2] = {t->ps_partkey, t->ps_suppkey};
     sx_sel sel_ps;
     SX_TRY(sx_hash_probe(ctx, ht_p, pscols, 2, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0, nullptr,
                          0, &sel_ps, nullptr, nullptr));
     bag.keep(sel_ps);
     int32_t k01[2] = {0, 1};
-    sx_ht *ht_ps, *ht_s, *ht_o;
-    SX_TRY(sx_hash_build(ctx, pscols, 2, k01, 2, &sel_ps, nullptr, 0, 1, &ht_ps));
+    sx_ht *ht_ps, *ht_s, *ht_lo, *ht_o;
+    SX_TRY(sx_hash_build(ctx, pscols, 2, k01, 2, &sel_ps, nullptr, 0, SX_BUILD_UNIQUE, &ht_ps));
     bag.keep(ht_ps);
-    SX_TRY(sx_hash_build(ctx, &t->s_suppkey, 1, &k0, 1, nullptr, nullptr, 0, 1, &ht_s));
+    SX_TRY(sx_hash_build(ctx, &t->s_suppkey, 1, &k0, 1, nullptr, nullptr, 0, SX_BUILD_UNIQUE, &ht_s));
     bag.keep(ht_s);
-    SX_TRY(sx_hash_build(ctx, &t->o_orderkey, 1, &k0, 1, nullptr, nullptr, 0, 1, &ht_o));
+    // orders semi-join reduction: only orders with a green line (their keys' bitmap) are built
+    SX_TRY(sx_hash_build(ctx, &t->l_orderkey, 1, &k0, 1, &sel_l, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
+    bag.keep(ht_lo);
+    sx_sel sel_o;
+    SX_TRY(sx_hash_probe(ctx, ht_lo, &t->o_orderkey, 1, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0,
+                         nullptr, 0, &sel_o, nullptr, nullptr));
+    bag.keep(sel_o);
+    SX_TRY(sx_hash_build(ctx, &t->o_orderkey, 1, &k0, 1, &sel_o, nullptr, 0, SX_BUILD_UNIQUE, &ht_o));
     bag.keep(ht_o);
     if (ht_ps->key_bytes != 8 || ht_s->key_bytes != 4 || ht_o->key_bytes != (okb4 ? 4 : 8))
       return set_err(ctx, SX_EINVAL, "Q9: unexpected table layouts");
@@ -795,16 +845,16 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     GbPlan plan;
     SX_TRY(gb_plan(ctx, tcols, 6, gk, 2, &ga, 1, nullptr, &plan));
     SX_TRY(check_states(ctx, plan, {ST_SUM}));
-    const int64_t n = t->l_partkey.len;
+    const int64_t n = sel_l.len;
     auto fill = [&](auto& pr) {
       pr.partkey = (const int32_t*)t->l_partkey.data;
       pr.suppkey = (const int32_t*)t->l_suppkey.data;
       pr.qty = (const long long*)t->l_quantity.data;
       pr.ext = (const long long*)t->l_extendedprice.data;
       pr.disc = (const long long*)t->l_discount.data;
-      pr.pbm = ht_p->bm;
-      pr.pbm_min = ht_p->bm_min;
-      pr.pbm_bits = ht_p->bm_bits;
+      pr.pbm = nullptr;  // rows come pre-selected (sel_l)
+      pr.pbm_min = 0;
+      pr.pbm_bits = 0;
       pr.ps_slots = ht_ps->slots;
       pr.ps_mask = (uint32_t)(ht_ps->cap - 1);
       pr.ps_cost = (const long long*)t->ps_supplycost.data;
@@ -820,15 +870,15 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       Q9FusedProg<int32_t, 4> pr;
       fill(pr);
       pr.orderkey = (const int32_t*)t->l_orderkey.data;
-      SX_TRY(gb_run(ctx, pr, plan, nullptr, n, 256, gok, goa, &ng));
+      SX_TRY(gb_run(ctx, pr, plan, sel_l.idx, n, 256, gok, goa, &ng));
     } else {
       Q9FusedProg<long long, 8> pr;
       fill(pr);
       pr.orderkey = (const long long*)t->l_orderkey.data;
-      SX_TRY(gb_run(ctx, pr, plan, nullptr, n, 256, gok, goa, &ng));
+      SX_TRY(gb_run(ctx, pr, plan, sel_l.idx, n, 256, gok, goa, &ng));
     }
-    // lineitem's five referenced columns once (+ the G output rows); lookups are implementation cost
-    pg.set_bytes((4.0 + 4.0 + type_width(t->l_orderkey.type) + 24.0) * n + 24.0 * ng);
+    // the selected lineitem rows' referenced columns once (+ selection, + the G output rows)
+    pg.set_bytes((4.0 + 4.0 + 4.0 + type_width(t->l_orderkey.type) + 24.0) * n + 24.0 * ng);
   } else {
   // 2. lineitem semi-join P, materialising the columns the plan needs
   sx_col lcols[6] = {t->l_partkey, t->l_suppkey, t->l_orderkey, t->l_quantity, t->l_extendedprice, t->l_discount};

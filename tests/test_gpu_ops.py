@@ -339,3 +339,26 @@ def test_gather(ctx):
     v = rng.integers(-5, 5, 10_000).astype(np.int64)
     s = rng.integers(0, 10_000, 777).astype(np.int32)
     assert np.array_equal(ctx.gather(c(dev(v)), dev(s)).cpu().numpy(), v[s])
+
+
+@pytest.mark.parametrize("span", [1000, 1 << 31])
+def test_membership_only_build(ctx, span):
+    """SX_BUILD_MEMBERSHIP: semi/anti probes equal those of a full build (bitmap when the key range
+    allows, else the table is built after all); INNER probes are refused when no table exists."""
+    rng = np.random.default_rng(9)
+    bk = rng.integers(-span // 2, span // 2, 5000, dtype=np.int64)
+    pk = rng.integers(-span // 2, span // 2, 20_011, dtype=np.int64)
+    bk[:100] = pk[:100]  # guaranteed matches
+    b, p = dev(bk), dev(pk)
+    ht = ctx.hash_build([c(b)], [0], membership=True)
+    for jt in ("semi", "anti"):
+        got, _, _ = ctx.hash_probe(ht, [c(p)], [0], jt)
+        want = oracle.join(bk, pk, jt)
+        assert np.array_equal(got.cpu().numpy(), want), jt
+    if span <= (1 << 30):
+        with pytest.raises(sx.SxError):
+            ctx.hash_probe(ht, [c(p)], [0], "inner")
+    else:
+        op, ob, _ = ctx.hash_probe(ht, [c(p)], [0], "inner")
+        wp, wb = oracle.join(bk, pk, "inner")
+        assert sorted(zip(op.cpu().numpy().tolist(), ob.cpu().numpy().tolist())) == sorted(zip(wp.tolist(), wb.tolist()))

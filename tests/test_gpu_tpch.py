@@ -148,6 +148,8 @@ def test_q9_plans(small, monkeypatch, plan):
     sfm, host, T = small
     if plan == "ops":
         monkeypatch.setenv("SX_Q9_PLAN", "ops")
+    else:
+        monkeypatch.setenv("SX_Q9_PLAN", "fused")
     for over in ({}, dict(q9_color="blue")):
         got = T.run("q9", tpch.default_params(**over))
         want = oracle.run_query("q9", host, oracle.default_params(**over))
