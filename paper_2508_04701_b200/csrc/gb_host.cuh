@@ -7,6 +7,7 @@
 
 #include "compact.cuh"
 #include "groupby.cuh"
+#include "radix.cuh"
 
 namespace sx {
 
@@ -134,6 +135,27 @@ struct SlotFn {
   int nsub;
   int has_having, hv_kind, hv_op, hv_off8, hv_off4;
   int64_t hv_lo, hv_hi;
+  // HAVING on a state given by value: SUM as {lo, hi} 96-bit, else the 8-byte slot word.
+  __device__ __forceinline__ bool hv_ok_state(unsigned long long lo, int32_t hi) const {
+    if (!has_having) return true;
+    if (hv_kind == ST_SUM) {
+      __int128 v = ((__int128)hi << 64) | (__int128)lo;
+      __int128 l = hv_lo, h = hv_hi;
+      switch (hv_op) {
+        case SX_LT: return v < l;
+        case SX_LE: return v <= l;
+        case SX_GT: return v > l;
+        case SX_GE: return v >= l;
+        case SX_EQ: return v == l;
+        case SX_NE: return v != l;
+        default: return l <= v && v <= h;
+      }
+    }
+    int64_t v = hv_kind == ST_COUNT ? (int64_t)lo
+              : hv_kind == ST_MAX ? (int64_t)(lo ^ 0x8000000000000000ull)
+                                  : (int64_t)(~lo ^ 0x8000000000000000ull);
+    return cmp(hv_op, v, hv_lo, hv_hi);
+  }
   __device__ __forceinline__ bool hv_ok(const uint8_t* p) const {
     if (!has_having) return true;
     if (hv_kind == ST_SUM) {
@@ -325,6 +347,130 @@ __global__ void __launch_bounds__(kBlock) k_runs_own(const __grid_constant__ P p
   if (ovf) atomicExch(prog.ovf_flag, 1);
 }
 
+// Dense variant of K10r for one-state programs with runs_dense (Q18): a thread loads its 8 rows
+// with 128-bit loads; the rows at its start that continue the previous thread's last group (its
+// "lead") are summed locally and handed to the previous lane with one shuffle, so a run that
+// crosses a thread boundary is finished without reloading rows (lane 31, and runs longer than the
+// next thread's 8 rows, read ahead row by row).
+template <class P>
+__global__ void __launch_bounds__(kBlock) k_runs_own_dense(const __grid_constant__ P prog, int64_t n,
+                                                           const __grid_constant__ Layout L,
+                                                           const __grid_constant__ SlotFn hv, uint8_t* __restrict__ out,
+                                                           int64_t cap_out, unsigned long long* cursor, int* flags) {
+  constexpr int R = kRunItems;
+  bool bad = false, ovf = false;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
+  // all lanes of a warp run the same number of iterations (shuffles below)
+  for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R; wbase < n; wbase += stride) {
+    const int64_t r0 = wbase + (int64_t)lane * R;
+    uint64_t key[R];
+    int64_t v[R];
+    prog.template runs_dense<R>(r0, n, key, v);
+    const int m = (int)max((int64_t)0, min((int64_t)R, n - r0));
+    uint64_t prev = 0;
+    const bool has_prev = r0 > 0 && r0 <= n;
+    if (has_prev) {
+      int32_t pr[1] = {(int32_t)(r0 - 1)};
+      bool pv[1] = {true};
+      uint64_t pk[1];
+      prog.template keys_only<1>(pr, pv, pk);
+      prev = pk[0];
+    }
+    // lead: leading rows continuing the previous thread's last group
+    unsigned long long lead_lo = 0;
+    int32_t lead_hi = 0;
+    int lead = 0;
+    bool in_lead = has_prev;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (i < m && in_lead && key[i] == prev) {
+        runs_acc<P>(ST_SUM, v[i], lead_lo, lead_hi);
+        ++lead;
+      } else {
+        in_lead = false;
+      }
+    }
+    // the next thread's lead continues my last group
+    const unsigned long long nx_lo = __shfl_down_sync(kFull, lead_lo, 1);
+    const int32_t nx_hi = __shfl_down_sync(kFull, lead_hi, 1);
+    const int nx_len = __shfl_down_sync(kFull, lead, 1);
+    // my groups: heads at rows i >= lead (a head: first row, or key change)
+    unsigned long long lo = 0;
+    int32_t hi = 0;
+    bool open = false;
+    uint64_t gk = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (i >= m || i < lead) continue;
+      const uint64_t pk = i > 0 ? key[i - 1] : prev;
+      const bool head = !(i > 0 || has_prev) || key[i] != pk;
+      bad |= (i > 0 || has_prev) && (int64_t)key[i] < (int64_t)pk;
+      if (head) {
+        if (open && hv.hv_ok_state(lo, hi)) {  // the previous owned group ended at row i - 1
+          const unsigned long long pos = atomicAdd(cursor, 1ull);
+          if ((int64_t)pos < cap_out) {
+            uint8_t* d = out + pos * L.slot_bytes;
+            if (L.key_bytes == 4) *(unsigned*)d = (unsigned)gk;
+            else *(unsigned long long*)d = gk;
+            *(unsigned long long*)(d + L.off8[0]) = lo;
+            *(int*)(d + L.off4[0]) = hi;
+          }
+        }
+        open = true;
+        gk = key[i];
+        lo = 0;
+        hi = 0;
+      }
+      runs_acc<P>(ST_SUM, v[i], lo, hi);
+    }
+    if (open) {  // my last owned group: finish it with the following rows
+      const int64_t nxt = r0 + R;  // first row of the next thread
+      if (nxt < n) {
+        bool more;
+        int64_t r;
+        if (lane < 31) {
+          // the next lane's lead (same warp) continues this group
+          const unsigned long long nl = lo + nx_lo;
+          const int carry = nl < lo ? 1 : 0;
+          hi += nx_hi + carry;
+          lo = nl;
+          more = nx_len == R;
+          r = nxt + R;
+        } else {
+          more = true;
+          r = nxt;
+        }
+        int steps = 0;
+        for (; more && r < n && steps < kRunAhead; ++r, ++steps) {  // rare: scalar continuation
+          int32_t rr[1] = {(int32_t)r};
+          bool al[1] = {true};
+          uint64_t kk[1];
+          typename P::template Cache<1> c1;
+          prog.template where_keys<1>(rr, al, kk, c1);
+          if (kk[0] != gk) break;
+          int64_t vv[1];
+          prog.template state<1>(0, rr, al, c1, vv, ovf);
+          runs_acc<P>(ST_SUM, vv[0], lo, hi);
+        }
+        if (more && steps == kRunAhead && r < n) atomicExch(flags + 1, 1);
+      }
+      if (hv.hv_ok_state(lo, hi)) {
+        const unsigned long long pos = atomicAdd(cursor, 1ull);
+        if ((int64_t)pos < cap_out) {
+          uint8_t* d = out + pos * L.slot_bytes;
+          if (L.key_bytes == 4) *(unsigned*)d = (unsigned)gk;
+          else *(unsigned long long*)d = gk;
+          *(unsigned long long*)(d + L.off8[0]) = lo;
+          *(int*)(d + L.off4[0]) = hi;
+        }
+      }
+    }
+  }
+  if (bad) atomicExch(flags, 1);
+  if (ovf) atomicExch(prog.ovf_flag, 1);
+}
+
 struct EmitArgs {
   const uint8_t* slots;
   const int32_t* ids;
@@ -409,6 +555,7 @@ inline int agg_out_type(int op) {
 }
 
 constexpr int64_t kSharedMaxGroups = 4096;      // K10 eligibility (hinted groups)
+constexpr uint64_t kRangesMaxBytes = 100u << 10; // K10p per-CTA table bytes (two CTAs per SM)
 constexpr int kSharedItems = 1;                  // K10 rows per thread per step (code size vs MLP)
 // A program may ask for more rows per thread (P::kSharedItems): fused probe chains need the
 // memory-level parallelism of several independent rows per thread.
@@ -428,6 +575,70 @@ inline uint64_t pow2_at_least(uint64_t x) {
 // Strategies: K9 (keyless / <= kSmallSlots groups), K11 into one table when it fits in half the
 // L2, otherwise partitioned K11 (records into 2^pbits hash partitions, each merged into an
 // L2-resident sub-table).  A table that fills up (bad hint) is resized and the step redone.
+// K10p host side: partition every column the program references (keys, predicates, expressions)
+// by the group key, remap the program onto the partitioned columns, cut each partition into row
+// ranges and aggregate the ranges in shared-memory tables (k_gb_ranges).
+inline sx_status gb_ranges(sx_ctx* ctx, const InterpProg& prog, const GbPlan& P, const int32_t* sel, int64_t n,
+                           int64_t groups_hint, const Layout& L, const Table& t, Scratch& scr) {
+  const GbArgs& A = prog.A;
+  bool used[SX_MAX_COLS] = {};
+  for (int k = 0; k < P.nkeys; ++k) used[A.kc[k]] = true;
+  for (int q = 0; q < A.np; ++q) used[A.preds[q].col] = true;
+  for (int a = 0; a < L.nst; ++a)
+    for (int tt = 0; tt < A.expr[a].nterms; ++tt)
+      for (int f = 0; f < A.expr[a].t[tt].nf; ++f) used[A.expr[a].t[tt].f[f].col] = true;
+  DCol carry[SX_MAX_COLS];
+  int width[SX_MAX_COLS], map[SX_MAX_COLS], nc = 0;
+  void* out[SX_MAX_COLS];
+  for (int c = 0; c < SX_MAX_COLS; ++c) {
+    map[c] = -1;
+    if (!used[c]) continue;
+    const int w = A.cols[c].type == SX_U8 ? 1 : (A.cols[c].type == SX_I32 || A.cols[c].type == SX_DATE32) ? 4 : 8;
+    carry[nc] = A.cols[c];
+    width[nc] = w;
+    SX_TRY(scr.get((char**)&out[nc], (size_t)n * w));
+    map[c] = nc++;
+  }
+  if (nc > 12) return set_err(ctx, SX_EINVAL, "group-by references too many columns for partitioning");
+  // the largest shared table that fits kRangesMaxBytes (two CTAs per SM); partitions sized so
+  // their expected group count fills at most half of it (load <= 0.5)
+  uint64_t scap = 1;
+  while ((2 * scap + 1) * (uint64_t)L.slot_bytes <= kRangesMaxBytes) scap <<= 1;
+  if (scap < 256) return SX_EUNSUPPORTED;
+  int bits = 1;
+  while (bits < 10 && (uint64_t)(groups_hint >> bits) > scap / 2) ++bits;
+  if ((uint64_t)(groups_hint >> bits) > scap / 2) return SX_EUNSUPPORTED;  // too many groups: other paths
+  std::vector<int64_t> off(((size_t)1 << bits) + 1);
+  const DCol k0 = A.cols[A.kc[0]], k1 = A.cols[P.nkeys > 1 ? A.kc[1] : A.kc[0]];
+  SX_TRY(radix_partition_carry(ctx, k0, k1, P.nkeys, carry, width, nc, sel, n, bits, out, off.data()));
+  InterpProg pp = prog;
+  for (int c = 0; c < SX_MAX_COLS; ++c)
+    if (map[c] >= 0) pp.A.cols[c].p = out[map[c]];
+  // row ranges: each partition cut into pieces of ~n / (4 x SMs) rows
+  const int64_t piece = std::max<int64_t>(1 << 16, n / (4 * (int64_t)ctx->num_sms));
+  std::vector<int64_t> items;
+  for (size_t p = 0; p + 1 < off.size(); ++p)
+    for (int64_t lo = off[p]; lo < off[p + 1]; lo += piece) {
+      items.push_back(lo);
+      items.push_back(std::min(off[p + 1], lo + piece));
+    }
+  const int64_t nitems = (int64_t)items.size() / 2;
+  int64_t* d_items;
+  SX_TRY(scr.get(&d_items, items.size() + 1));
+  SX_CUDA(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  const size_t smem = (size_t)(scap + 1) * L.slot_bytes;
+  SX_CUDA(cudaFuncSetAttribute(k_gb_ranges<InterpProg, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_ranges<InterpProg, 4>, kBlock, smem));
+  if (per_sm < 1) per_sm = 1;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * per_sm, nitems));
+  if (nitems > 0)
+    k_gb_ranges<InterpProg, 4><<<grid, kBlock, smem, SX_STREAM(ctx)>>>(pp, d_items, nitems, L, t, (uint32_t)scap);
+  SX_CHECK_LAUNCH();
+  // keep the partitioned columns alive until the kernel has run (Scratch frees stream-ordered)
+  return SX_OK;
+}
+
 template <class Prog>
 sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* sel, int64_t n,
                  int64_t groups_hint, sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups,
@@ -478,8 +689,17 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
           SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
           SX_CUDA(cudaMemsetAsync(cursor, 0, 8, ctx->stream));
           const int64_t threads = (n + kRunItems - 1) / kRunItems;
-          k_runs_own<Prog><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
-              prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
+          if constexpr (runs_dense<Prog>::value) {
+            if (L.nst == 1 && L.kind[0] == ST_SUM && L.slot_bytes <= 32)
+              k_runs_own_dense<Prog><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0,
+                                       SX_STREAM(ctx)>>>(prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
+            else
+              k_runs_own<Prog><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+                  prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
+          } else {
+            k_runs_own<Prog><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+                prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
+          }
           SX_CHECK_LAUNCH();
           int64_t cnt = 0;
           SX_TRY(read_i64(ctx, cursor, &cnt));
@@ -600,21 +820,51 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       // K9d: dense input + vector-loading program (see k_gb_dense); the grid must keep every
       // thread at <= 2^21 rows so that its int64 partial sums of |v| < 2^41 values cannot overflow
       if (n > 0 && small && !sel && L.nst == Prog::kDenseNst) {
-        size_t smem = dense_smem_bytes<Prog::kDenseNst>();
-        SX_CUDA(cudaFuncSetAttribute(k_gb_dense<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0;
-        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_dense<Prog>, kDenseThreads, smem));
-        if (per_sm < 1) per_sm = 1;
-        int64_t groups = (n + Prog::kDenseRows - 1) / Prog::kDenseRows;
-        int64_t ctas = std::min<int64_t>((int64_t)ctx->num_sms * per_sm, (groups + kDenseThreads - 1) / kDenseThreads);
-        if ((groups + ctas * kDenseThreads - 1) / (ctas * kDenseThreads) * Prog::kDenseRows <= kDenseMaxRowsPerThread) {
-          k_gb_dense<Prog><<<(unsigned)ctas, kDenseThreads, smem, SX_STREAM(ctx)>>>(prog, n, L, t);
-          SX_CHECK_LAUNCH();
-          dense_done = true;
+        bool staged = false;
+        if constexpr (has_bulk<Prog>::value) {
+          // K9s: bulk-staged (cp.async.bulk) tiles, one CTA per SM, when every column base is 16-B aligned
+          static const bool bulk_off = getenv("SX_BULK") && getenv("SX_BULK")[0] == '0';
+          bool aligned = true;
+          for (int c = 0; c < Prog::kBulkCols; ++c) aligned = aligned && ((uintptr_t)prog.bulk_col(c) % 16) == 0;
+          const int64_t rows_per_thread = (n + (int64_t)ctx->num_sms * kDenseThreads - 1) / ((int64_t)ctx->num_sms * kDenseThreads);
+          if (!bulk_off && aligned && n >= (int64_t)kBulkTile * ctx->num_sms && rows_per_thread <= kDenseMaxRowsPerThread) {
+            size_t smem = dense_smem_bytes<Prog::kDenseNst>() + 128 + (size_t)kBulkStages * bulk_stage_bytes<Prog>();
+            SX_CUDA(cudaFuncSetAttribute(k_gb_dense<Prog, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_gb_dense<Prog, true><<<(unsigned)ctx->num_sms, kDenseThreads, smem, SX_STREAM(ctx)>>>(prog, n, L, t);
+            SX_CHECK_LAUNCH();
+            staged = dense_done = true;
+          }
+        }
+        if (!staged) {
+          size_t smem = dense_smem_bytes<Prog::kDenseNst>();
+          SX_CUDA(cudaFuncSetAttribute(k_gb_dense<Prog, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          int per_sm = 0;
+          SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_dense<Prog, false>, kDenseThreads, smem));
+          if (per_sm < 1) per_sm = 1;
+          int64_t groups = (n + Prog::kDenseRows - 1) / Prog::kDenseRows;
+          int64_t ctas = std::min<int64_t>((int64_t)ctx->num_sms * per_sm, (groups + kDenseThreads - 1) / kDenseThreads);
+          if ((groups + ctas * kDenseThreads - 1) / (ctas * kDenseThreads) * Prog::kDenseRows <= kDenseMaxRowsPerThread) {
+            k_gb_dense<Prog, false><<<(unsigned)ctas, kDenseThreads, smem, SX_STREAM(ctx)>>>(prog, n, L, t);
+            SX_CHECK_LAUNCH();
+            dense_done = true;
+          }
         }
       }
     }
-    if (dense_done) {
+    bool ranges_done = false;
+    if constexpr (std::is_same<Prog, InterpProg>::value) {
+      // K10p: radix-partition the referenced columns on the group key, then per-range shared tables
+      static const bool ranges_off = getenv("SX_GB_RANGES") && getenv("SX_GB_RANGES")[0] == '0';
+      bool ident = true;
+      for (int k = 0; k < P.nkeys; ++k) ident = ident && P.key_fn[k] == SX_KEY_IDENTITY;
+      if (!ranges_off && n >= (1 << 22) && !small && !keyless && nsub == 1 && attempt == 0 && ident &&
+          groups_hint > kSharedMaxGroups) {
+        const sx_status rs = gb_ranges(ctx, prog, P, sel, n, groups_hint, L, t, scr);
+        if (rs == SX_OK) ranges_done = true;
+        else if (rs != SX_EUNSUPPORTED) return rs;
+      }
+    }
+    if (dense_done || ranges_done) {
     } else if (n > 0 && small) {
       size_t smem = small_smem_bytes(L.nst);
       SX_CUDA(cudaFuncSetAttribute(k_gb_small<Prog, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

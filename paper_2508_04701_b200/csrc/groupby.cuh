@@ -204,6 +204,9 @@ __device__ __forceinline__ uint8_t* slot_ptr(const Table& t, int slot_bytes, uin
 // Find or claim the slot of `key`; returns nullptr (and raises *full) if the table is full.
 __device__ __forceinline__ uint8_t* find_or_insert(const Table& t, const Layout& L, uint64_t key) {
   if (L.key_bytes == 0) return t.slots;
+  // 4-byte keys are hashed as stored (zero-extended): a key read back from a slot during a merge
+  // and the (possibly sign-extended) key of a row must land on the same slot
+  if (L.key_bytes == 4) key = (uint32_t)key;
   if (key == 0) {
     if (!*(volatile int*)t.side_used) atomicExch(t.side_used, 1);
     return slot_ptr(t, L.slot_bytes, t.mask + 1);
@@ -458,6 +461,86 @@ __global__ void __launch_bounds__(kBlock) k_gb_shared(const __grid_constant__ P 
     uint8_t* p = find_or_insert(t, L, key);
     if (p) merge_slot(p, s, L);
   }
+}
+
+// ------------------------------------------------------------------------------ K10p: ranges
+// Mid G (more groups than one shared-memory table holds): the input is radix-partitioned on the
+// group key first (H5), so each partition holds ~1/P of the groups; a CTA then aggregates one
+// row range of one partition at a time in a shared-memory table (as K10) and merges it into the
+// global table once per (range, group) instead of once per row.  items[2i], items[2i+1] = [lo, hi).
+template <class P, int ITEMS>
+__global__ void __launch_bounds__(kBlock) k_gb_ranges(const __grid_constant__ P prog, const int64_t* __restrict__ items,
+                                                      int64_t nitems, const __grid_constant__ Layout L, Table t,
+                                                      uint32_t scap) {
+  extern __shared__ __align__(16) uint8_t sm_tab[];
+  __shared__ int s_side, s_full;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const size_t bytes = (size_t)(scap + 1) * L.slot_bytes;
+  const Table st{sm_tab, scap - 1, &s_side, &s_full};
+  bool ovf = false;
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int64_t lo = __ldg(items + 2 * it), hi = __ldg(items + 2 * it + 1);
+    for (size_t j = threadIdx.x * 8; j < bytes; j += blockDim.x * 8) *(unsigned long long*)(sm_tab + j) = 0;
+    if (threadIdx.x == 0) { s_side = 0; s_full = 0; }
+    __syncthreads();
+    const int64_t tile = (int64_t)kBlock * ITEMS;
+    for (int64_t base = lo + (int64_t)w * 32 * ITEMS; base < hi; base += tile) {
+      int32_t row[ITEMS];
+      bool alive[ITEMS];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int64_t idx = base + 32 * i + lane;
+        alive[i] = idx < hi;
+        row[i] = alive[i] ? (int32_t)idx : 0;
+      }
+      uint64_t key[ITEMS];
+      typename P::template Cache<ITEMS> cache;
+      prog.template where_keys<ITEMS>(row, alive, key, cache);
+      int soff[ITEMS];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        soff[i] = -1;
+        if (alive[i] && !*(volatile int*)&s_full) {
+          uint8_t* p = find_or_insert(st, L, key[i]);
+          if (p) soff[i] = (int)(p - sm_tab);
+        }
+      }
+      for (int a = 0; a < L.nst; ++a) {
+        const int kd = prog.kind(a, L);
+        int64_t v[ITEMS];
+        if (kd == ST_COUNT) {
+#pragma unroll
+          for (int i = 0; i < ITEMS; ++i) v[i] = 1;
+        } else {
+          prog.template state<ITEMS>(a, row, alive, cache, v, ovf);
+        }
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          if (!alive[i]) continue;
+          if (soff[i] >= 0) apply_state_smem(sm_tab + soff[i], L, a, (unsigned long long)v[i],
+                                             (kd == ST_SUM && v[i] < 0) ? -1 : 0);
+          else gb_row_to_global(t, L, key[i], a, v[i]);
+        }
+      }
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e <= scap; e += blockDim.x) {
+      const uint8_t* sl = sm_tab + (size_t)e * L.slot_bytes;
+      uint64_t key;
+      if (e == scap) {
+        if (!s_side) continue;
+        key = 0;
+      } else {
+        key = L.key_bytes == 4 ? (uint64_t)*(const unsigned*)sl : *(const unsigned long long*)sl;
+        if (!key) continue;
+      }
+      uint8_t* p = find_or_insert(t, L, key);
+      if (p) merge_slot(p, sl, L);
+    }
+    __syncthreads();
+  }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
 }
 
 // ------------------------------------------------------------------------------ partitioned K11
@@ -1134,16 +1217,53 @@ static __device__ __noinline__ void gb_dense_slow_row(const P& prog, const Table
   }
 }
 
+// ---- bulk-staged variant (STAGED): cp.async.bulk (the TMA engine, 1-D bulk copies) moves whole
+// tiles of every referenced column into shared memory, kBulkStages deep, completion signalled on an
+// mbarrier per stage; the copies hold no registers, so the bytes in flight per SM are bounded by
+// shared memory instead of by the register file.
+constexpr int kBulkTile = 1024;   // rows per tile (x width: every column chunk is a multiple of 16 B)
+constexpr int kBulkStages = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 template <class P>
-__global__ void __launch_bounds__(kDenseThreads, 2) k_gb_dense(const __grid_constant__ P prog, int64_t n,
-                                                               const __grid_constant__ Layout L, Table t) {
+inline size_t bulk_stage_bytes() {
+  size_t b = 0;
+  for (int c = 0; c < P::kBulkCols; ++c) b += (size_t)kBulkTile * P::bulk_width(c);
+  return b;
+}
+
+template <class P, bool STAGED>
+__global__ void __launch_bounds__(kDenseThreads, STAGED ? 1 : 2) k_gb_dense(const __grid_constant__ P prog, int64_t n,
+                                                                            const __grid_constant__ Layout L, Table t) {
   constexpr int NST = P::kDenseNst;
   constexpr int R = P::kDenseRows;
-  extern __shared__ long long dacc[];  // [(kSmallSlots + 1) * NST][nthreads], lane-private columns
+  extern __shared__ __align__(128) long long dacc[];  // [(kSmallSlots + 1) * NST][nthreads], then stages
   __shared__ unsigned long long ct_key[kCtaTable];
   __shared__ int ct_used[kCtaTable];
   __shared__ unsigned long long ct_lo[kCtaTable][NST];
   __shared__ int ct_hi[kCtaTable][NST];
+  __shared__ __align__(8) uint64_t bars[kBulkStages];
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int j = 0; j < (kSmallSlots + 1) * NST; ++j) dacc[j * nt + tid] = 0;
   for (int j = tid; j < kCtaTable; j += nt) {
@@ -1156,18 +1276,11 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_gb_dense(const __grid_cons
 #pragma unroll
   for (int k = 0; k < kSmallSlots; ++k) skey[k] = 0;
   bool ovf = false;
-  const int64_t ngroups = (n + R - 1) / R;
-  for (int64_t g = blockIdx.x * (int64_t)nt + tid; g < ngroups; g += (int64_t)gridDim.x * nt) {
-    const int64_t r0 = g * R;
-    bool alive[R];
-    uint64_t key[R];
-    int64_t v[R][NST];
-    bool fast = true;
-    prog.template dense<R>(r0, n, alive, key, v, fast);
+  auto consume = [&](int64_t r0, bool (&alive)[R], uint64_t (&key)[R], int64_t (&v)[R][NST], bool fast) {
     if (!fast) {
       for (int i = 0; i < R; ++i)
         if (r0 + i < n) gb_dense_slow_row(prog, t, L, (int32_t)(r0 + i), ovf);
-      continue;
+      return;
     }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -1197,6 +1310,80 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_gb_dense(const __grid_cons
           unsigned long long u = kd == ST_MIN ? ~order_u(v[i][a]) : order_u(v[i][a]);
           *p = (long long)(u > (unsigned long long)*p ? u : (unsigned long long)*p);
         }
+      }
+    }
+  };
+  if constexpr (!STAGED) {
+    const int64_t ngroups = (n + R - 1) / R;
+    for (int64_t g = blockIdx.x * (int64_t)nt + tid; g < ngroups; g += (int64_t)gridDim.x * nt) {
+      const int64_t r0 = g * R;
+      bool alive[R];
+      uint64_t key[R];
+      int64_t v[R][NST];
+      bool fast = true;
+      prog.template dense<R>(r0, n, alive, key, v, fast);
+      consume(r0, alive, key, v, fast);
+    }
+  } else {
+    constexpr int C = P::kBulkCols;
+    uint8_t* stage0 = (uint8_t*)(dacc + (size_t)(kSmallSlots + 1) * NST * nt);
+    size_t stage_bytes = 0, col_off[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      col_off[c] = stage_bytes;
+      stage_bytes += (size_t)kBulkTile * P::bulk_width(c);
+    }
+    const int64_t ntiles = n / kBulkTile;  // full tiles; the tail goes through the global path
+    auto issue = [&](int64_t tile, int st) {
+      mbar_expect_tx(&bars[st], (uint32_t)stage_bytes);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int w = P::bulk_width(c);
+        bulk_g2s(stage0 + st * stage_bytes + col_off[c], (const uint8_t*)prog.bulk_col(c) + tile * kBulkTile * w,
+                 (uint32_t)(kBulkTile * w), &bars[st]);
+      }
+    };
+    if (tid == 0) {
+      for (int st = 0; st < kBulkStages; ++st) mbar_init(&bars[st], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int st = 0; st < kBulkStages; ++st) {
+        const int64_t tile = blockIdx.x + (int64_t)st * gridDim.x;
+        if (tile < ntiles) issue(tile, st);
+      }
+    int k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+      const int st = k % kBulkStages;
+      mbar_wait(&bars[st], (uint32_t)((k / kBulkStages) & 1));
+      const uint8_t* b[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) b[c] = stage0 + st * stage_bytes + col_off[c];
+      for (int j = tid * R; j < kBulkTile; j += nt * R) {
+        bool alive[R];
+        uint64_t key[R];
+        int64_t v[R][NST];
+        bool fast = true;
+        prog.template staged<R>(b, j, alive, key, v, fast);
+        consume(tile * kBulkTile + j, alive, key, v, fast);
+      }
+      __syncthreads();  // every thread is done with this stage
+      const int64_t nxt = tile + (int64_t)kBulkStages * gridDim.x;
+      if (tid == 0 && nxt < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nxt, st);
+      }
+    }
+    // tail rows (< one tile): the global-load path, block 0
+    if (blockIdx.x == 0) {
+      for (int64_t r0 = ntiles * kBulkTile + (int64_t)tid * R; r0 < n; r0 += (int64_t)nt * R) {
+        bool alive[R];
+        uint64_t key[R];
+        int64_t v[R][NST];
+        bool fast = true;
+        prog.template dense<R>(r0, n, alive, key, v, fast);
+        consume(r0, alive, key, v, fast);
       }
     }
   }
@@ -1260,6 +1447,11 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_gb_dense(const __grid_cons
 }
 
 // Detection of the dense interface (programs without it keep k_gb_small).
+template <class P, class = void>
+struct has_bulk : std::false_type {};
+template <class P>
+struct has_bulk<P, std::void_t<decltype(P::kBulkCols)>> : std::true_type {};
+
 template <class P, class = void>
 struct has_dense : std::false_type {};
 template <class P>

@@ -516,6 +516,24 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     int32_t** pob = join_type == SX_INNER ? &ob : nullptr;
     auto run_t = [&](auto ft) -> sx_status {
       fill_t(ft);
+      if (join_type == SX_INNER && ft.bm && ht->slots) {
+        // Two phases: the exact bitmap selects the matching probe rows (a streaming scan whose
+        // only lookups are bitmap words), then only those rows probe the table for their build
+        // row.  The scan's tiles never wait on a random HBM table access.
+        auto fm = ft;
+        fm.member_only = 1;
+        fm.anti = 0;
+        int32_t* cand = nullptr;
+        int64_t nc = 0;
+        GatherSpec none;
+        none.n = 0;
+        SX_TRY((run_compact<decltype(fm), 4>(ctx, fm, n, isel, &cand, nullptr, none, &nc)));
+        scr.ptrs.push_back(cand);
+        auto fl = ft;
+        fl.np = 0;  // predicates already applied
+        fl.bm = nullptr;
+        return run_compact<decltype(fl), 4>(ctx, fl, nc, cand, &op, pob, gs, &count);
+      }
       return run_compact<decltype(ft), 4>(ctx, ft, n, isel, &op, pob, gs, &count);
     };
     if (ht->cap <= (1ull << 32) && nkeys == 1 && kb == 4 && is32(0)) {
@@ -593,3 +611,112 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
   }
   return SX_OK;
 }
+
+// ------------------------------------------------------------------ payload tables (internal)
+namespace sx {
+namespace {
+struct PtArgs {
+  DCol k0, k1, pay;
+  int nkeys, kb, compact;
+  const int32_t* sel;
+  int64_t n;
+  ulonglong2* slots;
+  uint32_t mask;
+  int* bad;  // duplicate or reserved key
+};
+
+__global__ void __launch_bounds__(kBlock) k_pt_build(const __grid_constant__ PtArgs a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = a.sel ? (int64_t)__ldg(a.sel + i) : i;
+    uint64_t key = (uint64_t)ldv(a.k0, r);
+    if (a.nkeys == 2) key = (key << 32) | (uint32_t)ldv(a.k1, r);
+    const uint64_t x = a.kb == 4 ? (uint64_t)(uint32_t)key : key;
+    if (x == ~0ull) {
+      atomicExch(a.bad, 1);
+      continue;
+    }
+    uint32_t h = (uint32_t)(a.kb == 4 ? hash32((uint32_t)key) : hash64(key)) & a.mask;
+    if (a.compact) {  // 8-byte slots: (payload32 << 32) | key32 in one CAS
+      const unsigned long long e = ((unsigned long long)(uint32_t)ldv(a.pay, r) << 32) | (uint32_t)key;
+      if (e == ~0ull) {
+        atomicExch(a.bad, 1);
+        continue;
+      }
+      unsigned long long* sl = (unsigned long long*)a.slots;
+      for (;;) {
+        const unsigned long long old = atomicCAS(sl + h, ~0ull, e);
+        if (old == ~0ull) break;
+        if ((uint32_t)old == (uint32_t)key) {
+          atomicExch(a.bad, 1);
+          break;
+        }
+        h = (h + 1) & a.mask;
+      }
+      continue;
+    }
+    for (;;) {
+      const unsigned long long old = atomicCAS(&a.slots[h].x, ~0ull, (unsigned long long)x);
+      if (old == ~0ull) {
+        a.slots[h].y = (unsigned long long)ldv(a.pay, r);
+        break;
+      }
+      if (old == x) {  // a repeated key: not a PK side
+        atomicExch(a.bad, 1);
+        break;
+      }
+      h = (h + 1) & a.mask;
+    }
+  }
+}
+}  // namespace
+
+sx_status build_payload_table(sx_ctx* ctx, const sx_col* keys, int nkeys, const sx_col& pay, const sx_sel* sel,
+                              PayloadTable* out, bool allow_compact) {
+  *out = PayloadTable{};
+  if (nkeys < 1 || nkeys > 2) return set_err(ctx, SX_EINVAL, "payload table: nkeys %d", nkeys);
+  for (int k = 0; k < nkeys; ++k)
+    if (!(keys[k].type == SX_I32 || keys[k].type == SX_DATE32 || (nkeys == 1 && keys[k].type == SX_I64)))
+      return set_err(ctx, SX_ETYPE, "payload table: key type %d", keys[k].type);
+  if (!is_int_type(pay.type)) return set_err(ctx, SX_ETYPE, "payload table: payload type %d", pay.type);
+  const int64_t n = sel ? sel->len : keys[0].len;
+  uint64_t cap = 64;
+  while (cap < (uint64_t)(2 * n)) cap <<= 1;
+  if (cap > (1ull << 32)) return set_err(ctx, SX_EINDEX, "payload table too large");
+  PtArgs a{};
+  a.k0 = DCol{keys[0].data, keys[0].type, 0};
+  a.k1 = DCol{keys[nkeys - 1].data, keys[nkeys - 1].type, 0};
+  a.pay = DCol{pay.data, pay.type, 0};
+  a.nkeys = nkeys;
+  a.kb = (nkeys == 1 && keys[0].type != SX_I64) ? 4 : 8;
+  a.compact = allow_compact && a.kb == 4 && (pay.type == SX_I32 || pay.type == SX_DATE32 || pay.type == SX_U8);
+  a.sel = sel ? sel->idx : nullptr;
+  a.n = n;
+  a.mask = (uint32_t)(cap - 1);
+  a.bad = ctx->d_flags + 2;
+  const size_t sb = a.compact ? 8 : 16;
+  SX_TRY(alloc(ctx, (char**)&a.slots, (size_t)cap * sb));
+  SX_CUDA(cudaMemsetAsync(a.slots, 0xff, cap * sb, ctx->stream));
+  SX_CUDA(cudaMemsetAsync(a.bad, 0, sizeof(int), ctx->stream));
+  if (n > 0) k_pt_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+  cudaError_t e = cudaGetLastError();
+  int bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, a.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess || bad) {
+    dfree(ctx, a.slots);
+    return e != cudaSuccess ? set_err(ctx, SX_ECUDA, "payload table: %s", cudaGetErrorString(e))
+                            : set_err(ctx, SX_EINVAL, "payload table: repeated or reserved key");
+  }
+  out->slots = a.slots;
+  out->mask = a.mask;
+  out->kb = a.kb;
+  out->compact = a.compact;
+  out->rows = n;
+  return SX_OK;
+}
+
+void free_payload_table(sx_ctx* ctx, PayloadTable* t) {
+  if (t && t->slots) dfree(ctx, t->slots);
+  if (t) *t = PayloadTable{};
+}
+}  // namespace sx

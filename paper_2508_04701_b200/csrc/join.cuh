@@ -28,6 +28,57 @@ __device__ __forceinline__ uint64_t table_hash(uint64_t key, int key_bytes) {
   return key_bytes == 4 ? (uint64_t)hash32((uint32_t)key) : hash64(key);
 }
 
+// ---- payload tables (executor-internal): unique keys with an inline 8-byte payload -----------
+// 16-byte slots {x, y}: KB 4: x = key32 (high word 0) or ~0 = EMPTY; KB 8: x = key64 (~0 reserved
+// for EMPTY); y = the payload (any fixed-width integer column value, sign-extended).  A lookup is
+// one 16-byte load per probe step: the payload comes with the key, no second random access.
+// Compact form (32-bit key and a payload that fits 32 bits): 8-byte slots (payload32 << 32) | key32
+// claimed by one 64-bit CAS; ~0 = EMPTY (the entry key = payload = -1 is refused at build).
+struct PayloadTable {
+  ulonglong2* slots = nullptr;
+  uint32_t mask = 0;
+  int kb = 4;
+  int compact = 0;  // 8-byte slots
+  int64_t rows = 0;
+};
+
+__device__ __forceinline__ bool pt_find_compact(const unsigned long long* __restrict__ slots, uint32_t mask,
+                                                uint32_t key, int64_t& payload) {
+  uint32_t h = hash32(key) & mask;
+  for (;;) {
+    const unsigned long long v = __ldg(slots + h);
+    if (v == ~0ull) return false;
+    if ((uint32_t)v == key) {
+      payload = (int64_t)(int32_t)(v >> 32);
+      return true;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+template <int KB>
+__device__ __forceinline__ bool pt_find(const ulonglong2* __restrict__ slots, uint32_t mask, uint64_t key,
+                                        int64_t& payload) {
+  const uint64_t want = KB == 4 ? (uint64_t)(uint32_t)key : key;
+  uint32_t h = (uint32_t)(KB == 4 ? hash32((uint32_t)key) : hash64(key)) & mask;
+  for (;;) {
+    const ulonglong2 v = __ldg(slots + h);
+    if (v.x == ~0ull) return false;
+    if (v.x == want) {
+      payload = (int64_t)v.y;
+      return true;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// Builds a PayloadTable over the selected rows (sel or all n rows of the key columns): key = one
+// 32/64-bit column or two 32-bit columns packed (k0 << 32) | k1; payload = column `pay`.
+// SX_EINVAL if a key repeats (the table is for PK sides) or equals the reserved EMPTY value.
+sx_status build_payload_table(sx_ctx* ctx, const sx_col* keys, int nkeys, const sx_col& pay, const sx_sel* sel,
+                              PayloadTable* out, bool allow_compact = true);
+void free_payload_table(sx_ctx* ctx, PayloadTable* t);
+
 // Probe functor specialised on the key column type KT (int32_t / long long), the number of key
 // columns NK (2: two int32 columns packed (k0 << 32) | k1, reading R11) and the table layout KB.
 // All ITEMS key loads are issued back to back, then all first-slot loads, then the (rare) longer

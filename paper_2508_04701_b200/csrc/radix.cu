@@ -22,6 +22,7 @@
 
 #include "compact.cuh"
 #include "join.cuh"
+#include "radix.cuh"
 
 using namespace sx;
 
@@ -232,8 +233,19 @@ struct PJoin {
   void* pay_dst[kMaxCarry];
 };
 
+// Partitioned sides are streamed once per wave: evict-first loads (ld.global.cs) and stores
+// (st.global.cs) keep the wave's tables resident in L2.
 __device__ __forceinline__ uint64_t pj_key(const void* k, int kb, int64_t j) {
-  return kb == 4 ? (uint64_t)__ldg((const uint32_t*)k + j) : (uint64_t)__ldg((const unsigned long long*)k + j);
+  return kb == 4 ? (uint64_t)__ldcs((const uint32_t*)k + j) : (uint64_t)__ldcs((const unsigned long long*)k + j);
+}
+
+__device__ __forceinline__ void copy_val_cs(const DCol& src, int w, void* dst, int64_t d, int64_t r) {
+  switch (w) {
+    case 1: ((uint8_t*)dst)[d] = __ldcs((const uint8_t*)src.p + r); break;
+    case 4: __stcs((int32_t*)dst + d, __ldcs((const int32_t*)src.p + r)); break;
+    case 8: __stcs((long long*)dst + d, __ldcs((const long long*)src.p + r)); break;
+    default: __stcs((longlong2*)dst + d, __ldcs((const longlong2*)src.p + r)); break;
+  }
 }
 
 __global__ void __launch_bounds__(kBlock) k_pj_build(const __grid_constant__ PJoin a) {
@@ -316,9 +328,10 @@ __global__ void __launch_bounds__(kBlock) k_pj_probe(const __grid_constant__ PJo
     for (int i = 0; i < kPjItems; ++i) {
       if (jb[i] < 0) continue;
       const int64_t jp = base + (int64_t)i * kBlock + threadIdx.x;
-      if (a.out_probe) a.out_probe[pos] = __ldg(a.prow + jp);
-      if (a.out_build) a.out_build[pos] = __ldg(a.brow + jb[i]);
-      for (int g = 0; g < a.npay; ++g) copy_val(a.pay_src[g], a.pay_w[g], a.pay_dst[g], pos, a.pay_build[g] ? jb[i] : jp);
+      if (a.out_probe) __stcs(a.out_probe + pos, __ldcs(a.prow + jp));
+      if (a.out_build) __stcs(a.out_build + pos, __ldcs(a.brow + jb[i]));
+      for (int g = 0; g < a.npay; ++g)
+        copy_val_cs(a.pay_src[g], a.pay_w[g], a.pay_dst[g], pos, a.pay_build[g] ? jb[i] : jp);
       ++pos;
     }
     __syncthreads();
@@ -531,7 +544,7 @@ SX_EXPORT sx_status sx_hash_join(sx_ctx* ctx, const sx_col* build_cols, int nbui
   uint64_t cap = 64;
   while (cap < (uint64_t)(2 * maxb)) cap <<= 1;
   const size_t part_bytes = cap * sizeof(HtSlot8);
-  int W = (int)std::max<size_t>(1, (ctx->l2_bytes / 2) / part_bytes);
+  int W = (int)std::max<size_t>(1, (ctx->l2_bytes / 3) / part_bytes);
   W = std::min(W, P);
   HtSlot8* slots;
   SX_TRY(scr.get(&slots, (size_t)W * cap));
@@ -579,3 +592,25 @@ SX_EXPORT sx_status sx_hash_join(sx_ctx* ctx, const sx_col* build_cols, int nbui
   ps.set_bytes(b);
   return SX_OK;
 }
+
+namespace sx {
+sx_status radix_partition_carry(sx_ctx* ctx, DCol k0, DCol k1, int nkeys, const DCol* carry, const int* width,
+                                int ncarry, const int32_t* sel, int64_t n, int bits, void* const* out,
+                                int64_t* offsets_h) {
+  if (ncarry > kMaxCarry || bits < 1 || bits > kMaxPartBits) return set_err(ctx, SX_EINVAL, "radix partition spec");
+  PartSpec s{};
+  s.k0 = k0;
+  s.k1 = k1;
+  s.nkeys = nkeys;
+  s.bits = bits;
+  s.ncarry = ncarry;
+  for (int c = 0; c < ncarry; ++c) {
+    s.carry[c] = carry[c];
+    s.width[c] = width[c];
+    s.out[c] = out[c];
+  }
+  s.sel = sel;
+  s.n = n;
+  return radix_partition(ctx, s, offsets_h);
+}
+}  // namespace sx

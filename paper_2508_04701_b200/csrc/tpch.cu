@@ -68,6 +68,75 @@ struct Q1Prog {
   static constexpr int kDenseNst = 6;
   static constexpr int kDenseRows = 4;
   template <int R>
+  __device__ __forceinline__ void compute(const int32_t (&sd)[R], const uint32_t (&f)[R], const uint32_t (&s)[R],
+                                          const long long (&q)[R], const long long (&e)[R], const long long (&d)[R],
+                                          const long long (&x)[R], bool (&alive)[R], uint64_t (&key)[R],
+                                          int64_t (&v)[R][kDenseNst], bool& fast) const {
+    unsigned long long u = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      alive[i] = alive[i] && sd[i] <= ship_max;
+      key[i] = ((uint64_t)f[i] << 32) | s[i];
+      u |= (((unsigned long long)q[i] | (unsigned long long)e[i]) >> 26) |
+           (((unsigned long long)d[i] | (unsigned long long)x[i]) >> 7);
+    }
+    fast = u == 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const long long dp = (long long)(int32_t)e[i] * (long long)(100 - (int32_t)d[i]);
+      v[i][0] = q[i];
+      v[i][1] = e[i];
+      v[i][2] = dp;
+      v[i][3] = dp * (long long)(100 + (int32_t)x[i]);
+      v[i][4] = 1;
+      v[i][5] = d[i];
+    }
+  }
+  // 4 rows at row r0 from columns at (global or shared) base pointers; vector loads when `vec`
+  template <int R, bool GLOBAL>
+  __device__ __forceinline__ void load4(const int32_t* sp, const uint8_t* fp, const uint8_t* lp, const long long* qp,
+                                        const long long* ep, const long long* dp, const long long* xp, int32_t (&sd)[R],
+                                        uint32_t (&f)[R], uint32_t (&s)[R], long long (&q)[R], long long (&e)[R],
+                                        long long (&d)[R], long long (&x)[R]) const {
+    static_assert(R == 4, "4 rows");
+    int4 a;
+    uint32_t fr, lv;
+    longlong2 vq[2], ve[2], vd[2], vx[2];
+    if (GLOBAL) {
+      a = __ldcs((const int4*)sp);
+      fr = __ldcs((const unsigned int*)fp);
+      lv = __ldcs((const unsigned int*)lp);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        vq[j] = __ldcs((const longlong2*)qp + j);
+        ve[j] = __ldcs((const longlong2*)ep + j);
+        vd[j] = __ldcs((const longlong2*)dp + j);
+        vx[j] = __ldcs((const longlong2*)xp + j);
+      }
+    } else {
+      a = *(const int4*)sp;
+      fr = *(const unsigned int*)fp;
+      lv = *(const unsigned int*)lp;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        vq[j] = ((const longlong2*)qp)[j];
+        ve[j] = ((const longlong2*)ep)[j];
+        vd[j] = ((const longlong2*)dp)[j];
+        vx[j] = ((const longlong2*)xp)[j];
+      }
+    }
+    sd[0] = a.x; sd[1] = a.y; sd[2] = a.z; sd[3] = a.w;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[i] = (fr >> (8 * i)) & 0xffu;
+      s[i] = (lv >> (8 * i)) & 0xffu;
+      q[i] = (i & 1) ? vq[i >> 1].y : vq[i >> 1].x;
+      e[i] = (i & 1) ? ve[i >> 1].y : ve[i >> 1].x;
+      d[i] = (i & 1) ? vd[i >> 1].y : vd[i >> 1].x;
+      x[i] = (i & 1) ? vx[i >> 1].y : vx[i >> 1].x;
+    }
+  }
+  template <int R>
   __device__ __forceinline__ void dense(int64_t r0, int64_t n, bool (&alive)[R], uint64_t (&key)[R],
                                         int64_t (&v)[R][kDenseNst], bool& fast) const {
     static_assert(R == 4, "Q1Prog::dense loads 4 rows");
@@ -75,27 +144,9 @@ struct Q1Prog {
     uint32_t f[4], s[4];
     long long q[4], e[4], d[4], x[4];
     if (r0 + 4 <= n) {
-      const int4 a = __ldg((const int4*)(ship + r0));
-      const uint32_t fr = __ldg((const unsigned int*)(rf + r0)), lv = __ldg((const unsigned int*)(ls + r0));
-      longlong2 vq[2], ve[2], vd[2], vx[2];
+      load4<4, true>(ship + r0, rf + r0, ls + r0, qty + r0, ext + r0, disc + r0, tax + r0, sd, f, s, q, e, d, x);
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        vq[j] = __ldg((const longlong2*)(qty + r0) + j);
-        ve[j] = __ldg((const longlong2*)(ext + r0) + j);
-        vd[j] = __ldg((const longlong2*)(disc + r0) + j);
-        vx[j] = __ldg((const longlong2*)(tax + r0) + j);
-      }
-      sd[0] = a.x; sd[1] = a.y; sd[2] = a.z; sd[3] = a.w;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        f[i] = (fr >> (8 * i)) & 0xffu;
-        s[i] = (lv >> (8 * i)) & 0xffu;
-        q[i] = (i & 1) ? vq[i >> 1].y : vq[i >> 1].x;
-        e[i] = (i & 1) ? ve[i >> 1].y : ve[i >> 1].x;
-        d[i] = (i & 1) ? vd[i >> 1].y : vd[i >> 1].x;
-        x[i] = (i & 1) ? vx[i >> 1].y : vx[i >> 1].x;
-        alive[i] = true;
-      }
+      for (int i = 0; i < 4; ++i) alive[i] = true;
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -110,25 +161,35 @@ struct Q1Prog {
         x[i] = alive[i] ? __ldg(tax + r) : 0;
       }
     }
-    unsigned long long u = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      alive[i] = alive[i] && sd[i] <= ship_max;
-      key[i] = ((uint64_t)f[i] << 32) | s[i];
-      u |= (((unsigned long long)q[i] | (unsigned long long)e[i]) >> 26) |
-           (((unsigned long long)d[i] | (unsigned long long)x[i]) >> 7);
+    compute<4>(sd, f, s, q, e, d, x, alive, key, v, fast);
+  }
+  // Staged interface (k_gb_dense<P, true>): whole tiles of the 7 columns are copied into shared
+  // memory by bulk asynchronous copies (cp.async.bulk, the TMA engine); rows are read from there.
+  static constexpr int kBulkCols = 7;
+  __host__ __device__ static constexpr int bulk_width(int c) { return c == 0 ? 4 : (c <= 2 ? 1 : 8); }
+  __host__ __device__ const void* bulk_col(int c) const {
+    switch (c) {
+      case 0: return ship;
+      case 1: return rf;
+      case 2: return ls;
+      case 3: return qty;
+      case 4: return ext;
+      case 5: return disc;
+      default: return tax;
     }
-    fast = u == 0;
+  }
+  template <int R>
+  __device__ __forceinline__ void staged(const uint8_t* const (&b)[kBulkCols], int j, bool (&alive)[R],
+                                         uint64_t (&key)[R], int64_t (&v)[R][kDenseNst], bool& fast) const {
+    int32_t sd[4];
+    uint32_t f[4], s[4];
+    long long q[4], e[4], d[4], x[4];
+    load4<4, false>((const int32_t*)b[0] + j, b[1] + j, b[2] + j, (const long long*)b[3] + j,
+                    (const long long*)b[4] + j, (const long long*)b[5] + j, (const long long*)b[6] + j, sd, f, s, q,
+                    e, d, x);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const long long dp = (long long)(int32_t)e[i] * (long long)(100 - (int32_t)d[i]);
-      v[i][0] = q[i];
-      v[i][1] = e[i];
-      v[i][2] = dp;
-      v[i][3] = dp * (long long)(100 + (int32_t)x[i]);
-      v[i][4] = 1;
-      v[i][5] = d[i];
-    }
+    for (int i = 0; i < 4; ++i) alive[i] = true;
+    compute<4>(sd, f, s, q, e, d, x, alive, key, v, fast);
   }
   template <int I>
   __device__ __forceinline__ void state(int a, const int32_t (&)[I], const bool (&)[I], const Cache<I>& c,
@@ -395,15 +456,12 @@ struct Q9FusedProg {
   const uint32_t* pbm;
   long long pbm_min;
   unsigned long long pbm_bits;
-  const void* ps_slots;
+  const ulonglong2* ps;   // (partkey, suppkey) -> ps_supplycost
   uint32_t ps_mask;
-  const long long* ps_cost;
-  const void* s_slots;
-  uint32_t s_mask;
-  const int32_t* s_nation;
-  const void* o_slots;
-  uint32_t o_mask;
-  const int32_t* o_date;
+  const ulonglong2* sup;  // suppkey -> s_nationkey
+  uint32_t sup_mask;
+  const ulonglong2* ord;  // orderkey -> o_orderdate
+  uint32_t ord_mask;
   int* ovf_flag;
   static constexpr int kMaxNst = 1;
   static constexpr int kUnrollStates = 1;
@@ -440,20 +498,22 @@ struct Q9FusedProg {
       c.ext[i] = alive[i] ? __ldg(ext + row[i]) : 0;
       c.disc[i] = alive[i] ? __ldg(disc + row[i]) : 0;
     }
-    int32_t rps[I], rs[I], ro[I];
+    int64_t nk[I], d[I];
 #pragma unroll
     for (int i = 0; i < I; ++i) {
-      rps[i] = alive[i] ? ht_find<8>(ps_slots, ps_mask, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i]) : -1;
-      rs[i] = alive[i] ? ht_find<4>(s_slots, s_mask, (uint32_t)sk[i]) : -1;
-      ro[i] = alive[i] ? ht_find<OKB>(o_slots, o_mask, (uint64_t)(int64_t)ok[i]) : -1;
-    }
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-      alive[i] = alive[i] && rps[i] >= 0 && rs[i] >= 0 && ro[i] >= 0;
-      c.cost[i] = alive[i] ? __ldg(ps_cost + rps[i]) : 0;
-      const uint32_t nk = alive[i] ? (uint32_t)__ldg(s_nation + rs[i]) : 0u;
-      const int32_t d = alive[i] ? __ldg(o_date + ro[i]) : 0;
-      key[i] = ((uint64_t)nk << 32) | (uint32_t)civil_year(d);
+      bool f = alive[i];
+      c.cost[i] = 0;
+      nk[i] = 0;
+      d[i] = 0;
+      if (f) f = pt_find<8>(ps, ps_mask, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i], c.cost[i]);
+      if (f) f = pt_find_compact((const unsigned long long*)sup, sup_mask, (uint32_t)sk[i], nk[i]);
+      if constexpr (OKB == 4) {
+        if (f) f = pt_find_compact((const unsigned long long*)ord, ord_mask, (uint32_t)ok[i], d[i]);
+      } else {
+        if (f) f = pt_find<8>(ord, ord_mask, (uint64_t)(int64_t)ok[i], d[i]);
+      }
+      alive[i] = f;
+      key[i] = ((uint64_t)(uint32_t)nk[i] << 32) | (uint32_t)civil_year((int32_t)d[i]);
     }
   }
   template <int I>
@@ -809,12 +869,21 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     SX_TRY(sx_hash_probe(ctx, ht_p, pscols, 2, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0, nullptr,
                          0, &sel_ps, nullptr, nullptr));
     bag.keep(sel_ps);
-    int32_t k01[2] = {0, 1};
-    sx_ht *ht_ps, *ht_s, *ht_lo, *ht_o;
-    SX_TRY(sx_hash_build(ctx, pscols, 2, k01, 2, &sel_ps, nullptr, 0, SX_BUILD_UNIQUE, &ht_ps));
-    bag.keep(ht_ps);
-    SX_TRY(sx_hash_build(ctx, &t->s_suppkey, 1, &k0, 1, nullptr, nullptr, 0, SX_BUILD_UNIQUE, &ht_s));
-    bag.keep(ht_s);
+    // PK lookup tables with the looked-up value inline (PayloadTable: one random access each)
+    struct PtBag {
+      sx_ctx* c;
+      PayloadTable t[3];
+      ~PtBag() {
+        for (auto& x : t) free_payload_table(c, &x);
+      }
+    } pt{ctx, {}};
+    sx_ht* ht_lo;
+    {
+      ProfScope pb(ctx, "hash_build");
+      SX_TRY(build_payload_table(ctx, pscols, 2, t->ps_supplycost, &sel_ps, &pt.t[0]));
+      SX_TRY(build_payload_table(ctx, &t->s_suppkey, 1, t->s_nationkey, nullptr, &pt.t[1]));
+      pb.set_bytes((8.0 + 4.0 + 16.0) * sel_ps.len + (8.0 + 16.0) * t->s_suppkey.len);
+    }
     // orders semi-join reduction: only orders with a green line (their keys' bitmap) are built
     SX_TRY(sx_hash_build(ctx, &t->l_orderkey, 1, &k0, 1, &sel_l, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
     bag.keep(ht_lo);
@@ -822,9 +891,13 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     SX_TRY(sx_hash_probe(ctx, ht_lo, &t->o_orderkey, 1, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0,
                          nullptr, 0, &sel_o, nullptr, nullptr));
     bag.keep(sel_o);
-    SX_TRY(sx_hash_build(ctx, &t->o_orderkey, 1, &k0, 1, &sel_o, nullptr, 0, SX_BUILD_UNIQUE, &ht_o));
-    bag.keep(ht_o);
-    if (ht_ps->key_bytes != 8 || ht_s->key_bytes != 4 || ht_o->key_bytes != (okb4 ? 4 : 8))
+    {
+      ProfScope pb(ctx, "hash_build");
+      SX_TRY(build_payload_table(ctx, &t->o_orderkey, 1, t->o_orderdate, &sel_o, &pt.t[2]));
+      pb.set_bytes((4.0 + type_width(t->o_orderkey.type) + 4.0 + 16.0) * sel_o.len);
+    }
+    if (pt.t[0].kb != 8 || pt.t[1].kb != 4 || !pt.t[1].compact || pt.t[2].kb != (okb4 ? 4 : 8) ||
+        pt.t[2].compact != (okb4 ? 1 : 0))
       return set_err(ctx, SX_EINVAL, "Q9: unexpected table layouts");
     ProfScope pg(ctx, "probe_groupby");
     sx_col tcols[6] = {t->s_nationkey, t->ps_supplycost, t->l_quantity, t->l_extendedprice, t->l_discount,
@@ -855,15 +928,12 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       pr.pbm = nullptr;  // rows come pre-selected (sel_l)
       pr.pbm_min = 0;
       pr.pbm_bits = 0;
-      pr.ps_slots = ht_ps->slots;
-      pr.ps_mask = (uint32_t)(ht_ps->cap - 1);
-      pr.ps_cost = (const long long*)t->ps_supplycost.data;
-      pr.s_slots = ht_s->slots;
-      pr.s_mask = (uint32_t)(ht_s->cap - 1);
-      pr.s_nation = (const int32_t*)t->s_nationkey.data;
-      pr.o_slots = ht_o->slots;
-      pr.o_mask = (uint32_t)(ht_o->cap - 1);
-      pr.o_date = (const int32_t*)t->o_orderdate.data;
+      pr.ps = pt.t[0].slots;
+      pr.ps_mask = pt.t[0].mask;
+      pr.sup = pt.t[1].slots;
+      pr.sup_mask = pt.t[1].mask;
+      pr.ord = pt.t[2].slots;
+      pr.ord_mask = pt.t[2].mask;
       pr.ovf_flag = ctx->d_flags;
     };
     if (okb4) {

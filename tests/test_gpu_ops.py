@@ -362,3 +362,24 @@ def test_membership_only_build(ctx, span):
         op, ob, _ = ctx.hash_probe(ht, [c(p)], [0], "inner")
         wp, wb = oracle.join(bk, pk, "inner")
         assert sorted(zip(op.cpu().numpy().tolist(), ob.cpu().numpy().tolist())) == sorted(zip(wp.tolist(), wb.tolist()))
+
+
+@pytest.mark.parametrize("ng,hint,nkeys", [(50_000, 50_000, 1), (300_000, 400_000, 2), (9_000, 8_192, 1)])
+def test_groupby_partitioned_ranges(ctx, ng, hint, nkeys):
+    """K10p (mid G, >= 2^22 rows): radix partition on the group key + per-range shared tables,
+    with a where-predicate, keys 0/negative, two packed keys, and against the global-table path."""
+    rng = np.random.default_rng(ng)
+    n = (1 << 22) + 37
+    k = rng.integers(-(ng // 2), ng - ng // 2, n).astype(np.int32)
+    k2 = (rng.integers(0, 3, n)).astype(np.int32)
+    v = rng.integers(-(10**12), 10**12, n).astype(np.int64)
+    w = rng.integers(0, 100, n).astype(np.int64)
+    cols = [c(dev(k)), c(dev(k2)), c(dev(v)), c(dev(w))]
+    keys = [(0, "id")] + ([(1, "id")] if nkeys == 2 else [])
+    aggs = AGGS[:5]
+    got_keys, got_aggs, g = ctx.groupby(cols, keys, aggs, where=[(3, "lt", 90)], groups_hint=hint)
+    got = canon(got_keys, got_aggs, [a[0] for a in aggs])
+    m = w < 90
+    want = oracle.groupby([k[m], k2[m], v[m], w[m]], list(range(nkeys)), aggs)
+    check_gb(got, want)
+    assert g == len(want)
