@@ -823,7 +823,9 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
         bool staged = false;
         if constexpr (has_bulk<Prog>::value) {
           // K9s: bulk-staged (cp.async.bulk) tiles, one CTA per SM, when every column base is 16-B aligned
-          static const bool bulk_off = getenv("SX_BULK") && getenv("SX_BULK")[0] == '0';
+          // opt-in (SX_BULK=1): measured slower than K9d on Q1 at SF100 (6.1 vs 4.3 ms) — one 8-warp CTA
+          // per SM cannot hide the shared-memory latency of the per-row aggregation (profiles/)
+          const bool bulk_off = !(getenv("SX_BULK") && getenv("SX_BULK")[0] == '1');
           bool aligned = true;
           for (int c = 0; c < Prog::kBulkCols; ++c) aligned = aligned && ((uintptr_t)prog.bulk_col(c) % 16) == 0;
           const int64_t rows_per_thread = (n + (int64_t)ctx->num_sms * kDenseThreads - 1) / ((int64_t)ctx->num_sms * kDenseThreads);

@@ -142,15 +142,29 @@ def test_q1_q6_dense_guard_and_tails(ctx, trunc):
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
 
 
-@pytest.mark.parametrize("plan", ["fused", "ops"])
+@pytest.mark.parametrize("plan", ["fused", "fused-gather", "ops"])
 def test_q9_plans(small, monkeypatch, plan):
-    """Q9 through the fused probe-chain group-by (default) and the operator-at-a-time plan."""
+    """Q9 through the fused probe-chain group-by (default: dense scan; or gathering the semi-join's
+    rows) and the operator-at-a-time plan."""
     sfm, host, T = small
     if plan == "ops":
         monkeypatch.setenv("SX_Q9_PLAN", "ops")
     else:
         monkeypatch.setenv("SX_Q9_PLAN", "fused")
+        monkeypatch.setenv("SX_Q9_SCAN", "gather" if plan == "fused-gather" else "dense")
     for over in ({}, dict(q9_color="blue")):
         got = T.run("q9", tpch.default_params(**over))
         want = oracle.run_query("q9", host, oracle.default_params(**over))
         assert rows_equal(got, want), diff_rows(got, want)
+
+
+def test_q1_bulk_staged(ctx, monkeypatch):
+    """Q1 through the bulk-staged (cp.async.bulk + mbarrier) dense aggregation, SX_BULK=1: needs
+    >= 1024 rows per SM, so SF 0.1 (~600k rows, a ragged last tile)."""
+    monkeypatch.setenv("SX_BULK", "1")
+    host = gen.cpu_tables(100, seed=5)
+    T = tpch.Tpch(ctx, to_dev(host))
+    for q in ("q1", "q6"):
+        want = oracle.run_query(q, host)
+        got = T.run(q)
+        assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
