@@ -1253,8 +1253,24 @@ inline size_t bulk_stage_bytes() {
   return b;
 }
 
+template <class P, class = void>
+struct dense_min_blocks { static constexpr int value = 2; };
+template <class P>
+struct dense_min_blocks<P, std::void_t<decltype(P::kDenseMinBlocks)>> { static constexpr int value = P::kDenseMinBlocks; };
+
+template <class P, class = void>
+struct has_bulk : std::false_type {};
+template <class P>
+struct has_bulk<P, std::void_t<decltype(P::kBulkCols)>> : std::true_type {};
+
+template <class P, class = void>
+struct has_dense : std::false_type {};
+template <class P>
+struct has_dense<P, std::void_t<decltype(P::kDenseNst)>> : std::true_type {};
+
+
 template <class P, bool STAGED>
-__global__ void __launch_bounds__(kDenseThreads, STAGED ? 1 : 2) k_gb_dense(const __grid_constant__ P prog, int64_t n,
+__global__ void __launch_bounds__(kDenseThreads, STAGED ? 1 : dense_min_blocks<P>::value) k_gb_dense(const __grid_constant__ P prog, int64_t n,
                                                                             const __grid_constant__ Layout L, Table t) {
   constexpr int NST = P::kDenseNst;
   constexpr int R = P::kDenseRows;
@@ -1447,14 +1463,4 @@ __global__ void __launch_bounds__(kDenseThreads, STAGED ? 1 : 2) k_gb_dense(cons
 }
 
 // Detection of the dense interface (programs without it keep k_gb_small).
-template <class P, class = void>
-struct has_bulk : std::false_type {};
-template <class P>
-struct has_bulk<P, std::void_t<decltype(P::kBulkCols)>> : std::true_type {};
-
-template <class P, class = void>
-struct has_dense : std::false_type {};
-template <class P>
-struct has_dense<P, std::void_t<decltype(P::kDenseNst)>> : std::true_type {};
-
 }  // namespace sx

@@ -13,6 +13,7 @@
 #include "compact.cuh"
 #include "filter.cuh"
 #include "join.cuh"
+#include "radix.cuh"
 
 using namespace sx;
 
@@ -619,17 +620,19 @@ struct PtArgs {
   DCol k0, k1, pay;
   int nkeys, kb, compact;
   const int32_t* sel;
-  int64_t n;
+  int64_t lo, n;  // rows [lo, n) (of sel, else of the columns)
   ulonglong2* slots;
   uint32_t mask;
+  int pbits;
   int* bad;  // duplicate or reserved key
 };
 
 __global__ void __launch_bounds__(kBlock) k_pt_build(const __grid_constant__ PtArgs a) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = a.lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = a.sel ? (int64_t)__ldg(a.sel + i) : i;
     uint64_t key = (uint64_t)ldv(a.k0, r);
     if (a.nkeys == 2) key = (key << 32) | (uint32_t)ldv(a.k1, r);
+    const uint64_t base = pt_region_base(key, a.pbits, a.mask);
     const uint64_t x = a.kb == 4 ? (uint64_t)(uint32_t)key : key;
     if (x == ~0ull) {
       atomicExch(a.bad, 1);
@@ -642,7 +645,7 @@ __global__ void __launch_bounds__(kBlock) k_pt_build(const __grid_constant__ PtA
         atomicExch(a.bad, 1);
         continue;
       }
-      unsigned long long* sl = (unsigned long long*)a.slots;
+      unsigned long long* sl = (unsigned long long*)a.slots + base;
       for (;;) {
         const unsigned long long old = atomicCAS(sl + h, ~0ull, e);
         if (old == ~0ull) break;
@@ -654,10 +657,11 @@ __global__ void __launch_bounds__(kBlock) k_pt_build(const __grid_constant__ PtA
       }
       continue;
     }
+    ulonglong2* sl = a.slots + base;
     for (;;) {
-      const unsigned long long old = atomicCAS(&a.slots[h].x, ~0ull, (unsigned long long)x);
+      const unsigned long long old = atomicCAS(&sl[h].x, ~0ull, (unsigned long long)x);
       if (old == ~0ull) {
-        a.slots[h].y = (unsigned long long)ldv(a.pay, r);
+        sl[h].y = (unsigned long long)ldv(a.pay, r);
         break;
       }
       if (old == x) {  // a repeated key: not a PK side
@@ -694,10 +698,64 @@ sx_status build_payload_table(sx_ctx* ctx, const sx_col* keys, int nkeys, const 
   a.mask = (uint32_t)(cap - 1);
   a.bad = ctx->d_flags + 2;
   const size_t sb = a.compact ? 8 : 16;
+  Scratch scr(ctx);
+  // much larger than the L2: radix-partition (key, payload) and build region by region in waves
+  // that stay L2-resident (random CAS hits L2 instead of HBM)
+  // SX_PT_PARTITION: 0 never, 2 always (tests), else when the table exceeds half the L2
+  const char* pe = getenv("SX_PT_PARTITION");
+  const int pmode = pe ? pe[0] - '0' : 1;
+  std::vector<int64_t> off;
+  // (measured at SF100: 268 MB partsupp' table 0.35 -> 0.55 ms partitioned, 512 MB orders' 2.1 -> 1.9 ms:
+  // the partition pass pays off only well above the L2 size)
+  if (pmode != 0 && n > 0 && (pmode == 2 || cap * sb > 4 * ctx->l2_bytes)) {
+    int bits = 1;
+    while (bits < 10 && ((cap * sb) >> bits) > (8u << 20)) ++bits;
+    if (pmode == 2 && cap * sb <= (8u << 20)) bits = 3;  // forced: a few regions even for small tables
+    const int P = 1 << bits;
+    DCol carry[3];
+    int width[3];
+    void* outp[3];
+    int nc = 0;
+    for (int k = 0; k < nkeys; ++k) {
+      carry[nc] = DCol{keys[k].data, keys[k].type, 0};
+      width[nc] = type_width(keys[k].type);
+      ++nc;
+    }
+    carry[nc] = a.pay;
+    width[nc] = type_width(pay.type);
+    ++nc;
+    for (int c = 0; c < nc; ++c) SX_TRY(scr.get((char**)&outp[c], (size_t)n * width[c]));
+    off.assign((size_t)P + 1, 0);
+    SX_TRY(radix_partition_carry(ctx, a.k0, a.k1, nkeys, carry, width, nc, a.sel, n, bits, outp, off.data()));
+    int64_t maxp = 1;
+    for (int p = 0; p < P; ++p) maxp = std::max<int64_t>(maxp, off[p + 1] - off[p]);
+    uint64_t capp = 64;
+    while (capp < (uint64_t)(2 * maxp)) capp <<= 1;
+    a.pbits = bits;
+    a.mask = (uint32_t)(capp - 1);
+    cap = capp * P;
+    a.k0 = DCol{outp[0], keys[0].type, 0};
+    a.k1 = DCol{outp[nkeys - 1], keys[nkeys - 1].type, 0};
+    a.pay = DCol{outp[nc - 1], pay.type, 0};
+    a.sel = nullptr;
+  }
   SX_TRY(alloc(ctx, (char**)&a.slots, (size_t)cap * sb));
   SX_CUDA(cudaMemsetAsync(a.slots, 0xff, cap * sb, ctx->stream));
   SX_CUDA(cudaMemsetAsync(a.bad, 0, sizeof(int), ctx->stream));
-  if (n > 0) k_pt_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+  if (n > 0 && a.pbits == 0) {
+    k_pt_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+  } else if (n > 0) {
+    const int P = 1 << a.pbits;
+    const size_t region = ((size_t)a.mask + 1) * sb;
+    const int W = (int)std::max<size_t>(1, (ctx->l2_bytes / 3) / region);
+    for (int p0 = 0; p0 < P; p0 += W) {
+      const int p1 = std::min(P, p0 + W);
+      a.lo = off[p0];
+      a.n = off[p1];
+      if (a.n > a.lo)
+        k_pt_build<<<persistent_grid(ctx, 8, (a.n - a.lo + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+    }
+  }
   cudaError_t e = cudaGetLastError();
   int bad = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, a.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
@@ -709,6 +767,7 @@ sx_status build_payload_table(sx_ctx* ctx, const sx_col* keys, int nkeys, const 
   }
   out->slots = a.slots;
   out->mask = a.mask;
+  out->pbits = a.pbits;
   out->kb = a.kb;
   out->compact = a.compact;
   out->rows = n;

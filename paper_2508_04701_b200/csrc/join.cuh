@@ -34,19 +34,29 @@ __device__ __forceinline__ uint64_t table_hash(uint64_t key, int key_bytes) {
 // one 16-byte load per probe step: the payload comes with the key, no second random access.
 // Compact form (32-bit key and a payload that fits 32 bits): 8-byte slots (payload32 << 32) | key32
 // claimed by one 64-bit CAS; ~0 = EMPTY (the entry key = payload = -1 is refused at build).
+// Tables larger than L2 are built radix-partitioned (pbits > 0): region r = hash64(key) bits 48..
+// (the H5 partition function of the key as a signed 64-bit value) holds that partition's keys in
+// its own mask+1 slots, and each wave of regions is built while it is L2-resident.
 struct PayloadTable {
   ulonglong2* slots = nullptr;
-  uint32_t mask = 0;
+  uint32_t mask = 0;  // slots per region - 1
+  int pbits = 0;      // 0: one region
   int kb = 4;
-  int compact = 0;  // 8-byte slots
+  int compact = 0;    // 8-byte slots
   int64_t rows = 0;
 };
 
-__device__ __forceinline__ bool pt_find_compact(const unsigned long long* __restrict__ slots, uint32_t mask,
-                                                uint32_t key, int64_t& payload) {
+__device__ __forceinline__ uint64_t pt_region_base(uint64_t pkey, int pbits, uint32_t mask) {
+  return pbits ? (uint64_t)((uint32_t)(hash64(pkey) >> 48) & ((1u << pbits) - 1u)) * ((uint64_t)mask + 1) : 0ull;
+}
+
+// pkey: the key as a signed 64-bit value (region choice); key: the 32-bit key stored in the slot
+__device__ __forceinline__ bool pt_find_compact(const unsigned long long* __restrict__ slots, uint32_t mask, int pbits,
+                                                uint64_t pkey, uint32_t key, int64_t& payload) {
+  const unsigned long long* reg = slots + pt_region_base(pkey, pbits, mask);
   uint32_t h = hash32(key) & mask;
   for (;;) {
-    const unsigned long long v = __ldg(slots + h);
+    const unsigned long long v = __ldg(reg + h);
     if (v == ~0ull) return false;
     if ((uint32_t)v == key) {
       payload = (int64_t)(int32_t)(v >> 32);
@@ -57,12 +67,13 @@ __device__ __forceinline__ bool pt_find_compact(const unsigned long long* __rest
 }
 
 template <int KB>
-__device__ __forceinline__ bool pt_find(const ulonglong2* __restrict__ slots, uint32_t mask, uint64_t key,
+__device__ __forceinline__ bool pt_find(const ulonglong2* __restrict__ slots, uint32_t mask, int pbits, uint64_t key,
                                         int64_t& payload) {
   const uint64_t want = KB == 4 ? (uint64_t)(uint32_t)key : key;
+  const ulonglong2* reg = slots + pt_region_base(key, pbits, mask);
   uint32_t h = (uint32_t)(KB == 4 ? hash32((uint32_t)key) : hash64(key)) & mask;
   for (;;) {
-    const ulonglong2 v = __ldg(slots + h);
+    const ulonglong2 v = __ldg(reg + h);
     if (v.x == ~0ull) return false;
     if (v.x == want) {
       payload = (int64_t)v.y;

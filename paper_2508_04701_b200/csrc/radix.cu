@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(kBlock) k_pj_build(const __grid_constant__ PJo
   }
 }
 
-constexpr int kPjItems = 8;
-__global__ void __launch_bounds__(kBlock) k_pj_probe(const __grid_constant__ PJoin a) {
+constexpr int kPjItems = 4;
+__global__ void __launch_bounds__(kBlock, 4) k_pj_probe(const __grid_constant__ PJoin a) {
   __shared__ int s_warp[kBlock / 32];
   __shared__ unsigned long long s_base;
   const int64_t tile = (int64_t)kBlock * kPjItems;

@@ -259,6 +259,7 @@ struct Q6Prog {
   // rows make ext*disc < 2^40 an exact 32x32->64 product.
   static constexpr int kDenseNst = 2;
   static constexpr int kDenseRows = 8;
+  static constexpr int kDenseMinBlocks = 3;  // more rows in flight for the lazy (dependent) loads
   template <int R>
   __device__ __forceinline__ void dense(int64_t r0, int64_t n, bool (&alive)[R], uint64_t (&key)[R],
                                         int64_t (&v)[R][kDenseNst], bool& fast) const {
@@ -458,10 +459,13 @@ struct Q9FusedProg {
   unsigned long long pbm_bits;
   const ulonglong2* ps;   // (partkey, suppkey) -> ps_supplycost
   uint32_t ps_mask;
+  int ps_bits;
   const ulonglong2* sup;  // suppkey -> s_nationkey
   uint32_t sup_mask;
+  int sup_bits;
   const ulonglong2* ord;  // orderkey -> o_orderdate
   uint32_t ord_mask;
+  int ord_bits;
   int* ovf_flag;
   static constexpr int kMaxNst = 1;
   static constexpr int kUnrollStates = 1;
@@ -517,12 +521,16 @@ struct Q9FusedProg {
       c.cost[i] = 0;
       nk[i] = 0;
       d[i] = 0;
-      if (f) f = pt_find<8>(ps, ps_mask, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i], c.cost[i]);
-      if (f) f = pt_find_compact((const unsigned long long*)sup, sup_mask, (uint32_t)sk[i], nk[i]);
+      if (f) f = pt_find<8>(ps, ps_mask, ps_bits, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i], c.cost[i]);
+      if (f)
+        f = pt_find_compact((const unsigned long long*)sup, sup_mask, sup_bits, (uint64_t)(int64_t)sk[i],
+                            (uint32_t)sk[i], nk[i]);
       if constexpr (OKB == 4) {
-        if (f) f = pt_find_compact((const unsigned long long*)ord, ord_mask, (uint32_t)ok[i], d[i]);
+        if (f)
+          f = pt_find_compact((const unsigned long long*)ord, ord_mask, ord_bits, (uint64_t)(int64_t)ok[i],
+                              (uint32_t)ok[i], d[i]);
       } else {
-        if (f) f = pt_find<8>(ord, ord_mask, (uint64_t)(int64_t)ok[i], d[i]);
+        if (f) f = pt_find<8>(ord, ord_mask, ord_bits, (uint64_t)(int64_t)ok[i], d[i]);
       }
       alive[i] = f;
       key[i] = ((uint64_t)(uint32_t)nk[i] << 32) | (uint32_t)civil_year((int32_t)d[i]);
@@ -946,10 +954,13 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       pr.pbm_bits = ht_p->bm_bits;
       pr.ps = pt.t[0].slots;
       pr.ps_mask = pt.t[0].mask;
+      pr.ps_bits = pt.t[0].pbits;
       pr.sup = pt.t[1].slots;
       pr.sup_mask = pt.t[1].mask;
+      pr.sup_bits = pt.t[1].pbits;
       pr.ord = pt.t[2].slots;
       pr.ord_mask = pt.t[2].mask;
+      pr.ord_bits = pt.t[2].pbits;
       pr.ovf_flag = ctx->d_flags;
     };
     if (okb4) {

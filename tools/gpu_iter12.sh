@@ -1,0 +1,6 @@
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
+for q in q9 q18; do timeout 300 python tools/run_query.py --query $q --sf 100 --reps 3 > gpurun_out/rq_$q.txt 2>&1; done
+timeout 900 python bench.py --workload join --steps 2 --warmup 1 > gpurun_out/mb_join.json 2> gpurun_out/mb_join.err
+timeout 900 python bench.py --workload join-zipf --steps 2 --warmup 1 > gpurun_out/mb_join_zipf.json 2> gpurun_out/mb_join_zipf.err
+timeout 900 python bench.py --workload sort --steps 3 --warmup 1 > gpurun_out/mb_sort.json 2> gpurun_out/mb_sort.err
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
