@@ -515,8 +515,45 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     f.mask = ht->cap - 1;
     for (int g = 0; g < gs.n; ++g) gs.g[g].dst = nullptr;  // allocated at the exact output count
     int32_t** pob = join_type == SX_INNER ? &ob : nullptr;
+    // bitmap-only membership functor for one key column (semi/anti answer, or INNER phase 1)
+    auto make_bm = [&](auto* kt) {
+      using KT = std::remove_pointer_t<decltype(kt)>;
+      BitmapFn<KT> b;
+      for (int i = 0; i < nprobe_cols; ++i) b.cols[i] = pcols[i];
+      for (int i = 0; i < nwhere; ++i) b.preds[i] = preds[i];
+      b.np = nwhere;
+      b.k0 = (const KT*)probe_cols[key_cols[0]].data;
+      b.bm = ht->bm;
+      b.bm_min = ht->bm_min;
+      b.bm_bits = ht->bm_bits;
+      b.anti = join_type == SX_ANTI;
+      return b;
+    };
     auto run_t = [&](auto ft) -> sx_status {
       fill_t(ft);
+      if (ft.bm && nkeys == 1 && join_type != SX_INNER) {  // the exact bitmap is the answer
+        if (probe_cols[key_cols[0]].type == SX_I64)
+          return run_compact<BitmapFn<long long>, 8>(ctx, make_bm((long long*)nullptr), n, isel, &op, nullptr, gs,
+                                                     &count);
+        return run_compact<BitmapFn<int32_t>, 8>(ctx, make_bm((int32_t*)nullptr), n, isel, &op, nullptr, gs, &count);
+      }
+      if (join_type == SX_INNER && ft.bm && ht->slots && nkeys == 1) {
+        // Two phases: the exact bitmap selects the matching probe rows (a streaming scan whose
+        // only lookups are bitmap words), then only those rows probe the table for their build
+        // row.  The scan's tiles never wait on a random HBM table access.
+        int32_t* cand = nullptr;
+        int64_t nc = 0;
+        GatherSpec none;
+        none.n = 0;
+        auto bmf = make_bm((decltype(ft.k0))nullptr);
+        bmf.anti = 0;
+        SX_TRY((run_compact<decltype(bmf), 8>(ctx, bmf, n, isel, &cand, nullptr, none, &nc)));
+        scr.ptrs.push_back(cand);
+        auto fl = ft;
+        fl.np = 0;  // predicates already applied
+        fl.bm = nullptr;
+        return run_compact<decltype(fl), 4>(ctx, fl, nc, cand, &op, pob, gs, &count);
+      }
       if (join_type == SX_INNER && ft.bm && ht->slots) {
         // Two phases: the exact bitmap selects the matching probe rows (a streaming scan whose
         // only lookups are bitmap words), then only those rows probe the table for their build

@@ -90,6 +90,60 @@ sx_status build_payload_table(sx_ctx* ctx, const sx_col* keys, int nkeys, const 
                               PayloadTable* out, bool allow_compact = true);
 void free_payload_table(sx_ctx* ctx, PayloadTable* t);
 
+// Semi / anti membership through the build's exact key-range bitmap only (one key column of type
+// KT): no table code, so 16 rows per thread fit the registers and the scan keeps more loads in
+// flight.  Also phase 1 of the two-phase unique INNER probe.
+template <typename KT>
+struct BitmapFn {
+  DCol cols[SX_MAX_COLS];
+  DPred preds[SX_MAX_PREDS];
+  int np;
+  const KT* k0;
+  const uint32_t* bm;
+  long long bm_min;
+  unsigned long long bm_bits;
+  int anti;
+  static constexpr int kDenseItems = 16;
+  template <int ITEMS>
+  __device__ __forceinline__ bool hit(int64_t key, bool live) const {
+    const unsigned long long off = (unsigned long long)(key - bm_min);
+    const bool in = live && off < bm_bits;
+    const uint32_t w = in ? __ldg(bm + (off >> 5)) : 0u;
+    return in && ((w >> (off & 31)) & 1u);
+  }
+  template <int ITEMS>
+  __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
+                                       int32_t (&)[ITEMS]) const {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i];
+    for (int p = 0; p < np; ++p) apply_pred<ITEMS>(cols[preds[p].col], preds[p], row, alive);
+    int64_t key[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = alive[i] ? (int64_t)__ldg(k0 + row[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool h = hit<ITEMS>(key[i], alive[i]);
+      alive[i] = alive[i] && (anti ? !h : h);
+    }
+  }
+  template <int ITEMS>
+  __device__ __forceinline__ void eval_dense(int64_t r0, int64_t n, uint32_t& mask, int32_t (&)[ITEMS]) const {
+    const bool full = r0 + ITEMS <= n;
+    mask = dense_valid<ITEMS>(r0, n);
+    int64_t k[ITEMS];
+    dense_load<ITEMS>(DCol{k0, sizeof(KT) == 4 ? SX_I32 : SX_I64, 0}, r0, n, full, k);
+    for (int p = 0; p < np; ++p) dense_pred<ITEMS>(cols[preds[p].col], preds[p], r0, n, full, mask);
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool live = (mask >> i) & 1u;
+      const bool h = hit<ITEMS>(k[i], live);
+      m |= ((live && (anti ? !h : h)) ? 1u : 0u) << i;
+    }
+    mask = m;
+  }
+};
+
 // Probe functor specialised on the key column type KT (int32_t / long long), the number of key
 // columns NK (2: two int32 columns packed (k0 << 32) | k1, reading R11) and the table layout KB.
 // All ITEMS key loads are issued back to back, then all first-slot loads, then the (rare) longer
