@@ -48,6 +48,7 @@ struct sx_ht {
   void* slots = nullptr;
   int64_t rows = 0;        // inserted build rows
   uint32_t* bm = nullptr;  // exact bitmap over [bm_min, bm_min + bm_bits) of the build keys (or null)
+  int32_t* direct = nullptr;  // unique builds over a small key range: build row at [key - bm_min] (no table)
   long long bm_min = 0;
   unsigned long long bm_bits = 0;
 };

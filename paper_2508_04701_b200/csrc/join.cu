@@ -74,12 +74,13 @@ __global__ void __launch_bounds__(kBlock) k_build(const __grid_constant__ BuildA
 // Exact key-range bitmap of the build keys (predicate transfer): bit (key - min).
 // Probes test it before touching the table, so misses cost one (L2-resident) word load.
 __global__ void __launch_bounds__(kBlock) k_bitmap_set(const __grid_constant__ BuildArgs a, uint32_t* bm,
-                                                       long long kmin) {
+                                                       long long kmin, int32_t* direct) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < a.n; idx += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = a.sel ? (int64_t)__ldg(a.sel + idx) : idx;
     if (!eval_conj(a.cols, a.preds, a.np, r)) continue;
     uint64_t off = (uint64_t)((long long)key_of(a.cols, a.nkeys, a.kc0, a.kc1, r) - kmin);
     atomicOr(bm + (off >> 5), 1u << (off & 31));
+    if (direct) direct[off] = (int32_t)r;  // unique keys: one writer per entry
   }
 }
 
@@ -301,6 +302,12 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
   // unique_hint bit 1 (SX_BUILD_MEMBERSHIP): only semi/anti probes will follow; when the exact
   // key-range bitmap can be built (one key column, range <= 2^30) the table itself is omitted
   const bool membership = (unique_hint & 2) != 0 && nkeys == 1;
+  // a unique single-column build whose table would not be L2-resident may become a direct-address
+  // array (decided after the key range is known): bitmap + row per key, no table and no CAS
+  const bool direct_off = getenv("SX_DIRECT") && getenv("SX_DIRECT")[0] == '0';
+  const bool direct_cand = !direct_off && !membership && (unique_hint & 1) && nkeys == 1 &&
+                           (types[0] == SX_I32 || types[0] == SX_DATE32 || types[0] == SX_I64) &&
+                           cap * slot_bytes >= (8u << 20);
   sx_ht* ht = new sx_ht();
   ht->key_bytes = a.key_bytes;
   ht->key_types[0] = types[0];
@@ -309,7 +316,7 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
   ht->unique = (unique_hint & 1) != 0;
   ht->cap = cap;
   sx_status s = SX_OK;
-  if (!membership) {
+  if (!membership && !direct_cand) {
     s = alloc(ctx, (char**)&ht->slots, cap * slot_bytes);
     if (s != SX_OK) {
       delete ht;
@@ -342,7 +349,18 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
   ht->rows = stats[0];
   const bool bm_ok = nkeys == 1 && stats[0] > 0 && stats[2] >= stats[1] &&
                      (unsigned long long)(stats[2] - stats[1]) + 1 <= (1ull << 30);
-  if (membership && !bm_ok && stats[0] > 0) {  // no bitmap possible: build the table after all
+  const unsigned long long krange = bm_ok ? (unsigned long long)(stats[2] - stats[1]) + 1 : 0;
+  const bool use_direct = direct_cand && bm_ok && krange <= 64ull * (unsigned long long)stats[0] &&
+                          krange * 4 <= (4ull << 30);
+  if (use_direct) {
+    s = alloc(ctx, &ht->direct, (size_t)krange);
+    if (s != SX_OK) {
+      ctx->err.clear();
+      ht->direct = nullptr;
+    }
+  }
+  if ((membership || direct_cand) && !ht->direct && !(membership && bm_ok) && stats[0] > 0) {
+    // no bitmap / direct array possible: build the table after all
     s = alloc(ctx, (char**)&ht->slots, cap * slot_bytes);
     if (s != SX_OK) {
       delete ht;
@@ -354,7 +372,7 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
     k_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
     SX_CHECK_LAUNCH();
   }
-  if (membership && !ht->slots) ht->cap = 0;
+  if ((membership || ht->direct) && !ht->slots) ht->cap = 0;
   // exact bitmap filter over the key range when it is small enough to stay cache-resident-ish
   if (nkeys == 1 && stats[0] > 0) {
     unsigned long long range = (unsigned long long)(stats[2] - stats[1]) + 1;
@@ -364,7 +382,8 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
         cudaMemsetAsync(ht->bm, 0, words * sizeof(uint32_t), ctx->stream);
         ht->bm_min = stats[1];
         ht->bm_bits = range;
-        k_bitmap_set<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a, ht->bm, stats[1]);
+        k_bitmap_set<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a, ht->bm, stats[1],
+                                                                                                     ht->direct);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
           dfree(ctx, ht->slots);
@@ -375,6 +394,12 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
       } else {
         ctx->err.clear();
         ht->bm = nullptr;
+        if (ht->direct) {  // the direct array needs the bitmap
+          dfree(ctx, ht->direct);
+          dfree(ctx, ht->slots);
+          delete ht;
+          return set_err(ctx, SX_ENOMEM, "device pool exhausted (key bitmap)");
+        }
       }
     }
   }
@@ -395,6 +420,7 @@ SX_EXPORT void sx_ht_destroy(sx_ctx* ctx, sx_ht* ht) {
   if (ctx) {
     dfree(ctx, ht->slots);
     dfree(ctx, ht->bm);
+    dfree(ctx, ht->direct);
   }
   delete ht;
 }
@@ -411,7 +437,7 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
   ProfScope ps(ctx, join_type == SX_INNER ? "probe_inner" : (join_type == SX_SEMI ? "probe_semi" : "probe_anti"));
   if (join_type < SX_INNER || join_type > SX_ANTI) return set_err(ctx, SX_EINVAL, "join type %d", join_type);
   if (join_type == SX_INNER && !out_build) return set_err(ctx, SX_EINVAL, "INNER join needs out_build");
-  if (!ht->slots && (join_type == SX_INNER || !ht->bm))
+  if (!ht->slots && !ht->direct && (join_type == SX_INNER || !ht->bm))
     return set_err(ctx, SX_EINVAL, "membership-only table: SEMI/ANTI probes only");
   if (join_type != SX_INNER && nbp > 0) return set_err(ctx, SX_EINVAL, "build payload only for INNER joins");
   if (nbp + npp > kMaxGather || nbp < 0 || npp < 0) return set_err(ctx, SX_EINVAL, "too many payload columns");
@@ -462,6 +488,7 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
     ft.bm = ht->bm;
     ft.bm_min = ht->bm_min;
     ft.bm_bits = ht->bm_bits;
+    ft.direct = ht->direct;
   };
   // non-unique INNER with typed keys: count -> scan -> expand (see k_expand)
   auto run_expand = [&](auto ft) -> sx_status {
@@ -537,7 +564,7 @@ SX_EXPORT sx_status sx_hash_probe(sx_ctx* ctx, const sx_ht* ht, const sx_col* pr
                                                      &count);
         return run_compact<BitmapFn<int32_t>, 8>(ctx, make_bm((int32_t*)nullptr), n, isel, &op, nullptr, gs, &count);
       }
-      if (join_type == SX_INNER && ft.bm && ht->slots && nkeys == 1) {
+      if (join_type == SX_INNER && ft.bm && (ht->slots || ht->direct) && nkeys == 1) {
         // Two phases: the exact bitmap selects the matching probe rows (a streaming scan whose
         // only lookups are bitmap words), then only those rows probe the table for their build
         // row.  The scan's tiles never wait on a random HBM table access.

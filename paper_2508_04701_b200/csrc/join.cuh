@@ -164,6 +164,7 @@ struct ProbeFnT {
   const uint32_t* bm;  // optional exact key-range bitmap of the build side
   long long bm_min;
   unsigned long long bm_bits;
+  const int32_t* direct;  // unique direct-address build: row at [key - bm_min] (no table)
   template <int ITEMS>
   __device__ __forceinline__ void eval(const int32_t (&row)[ITEMS], const bool (&valid)[ITEMS], bool (&alive)[ITEMS],
                                        int32_t (&aux)[ITEMS]) const {
@@ -211,6 +212,22 @@ struct ProbeFnT {
   }
   template <int ITEMS>
   __device__ __forceinline__ void probe(uint64_t (&key)[ITEMS], bool (&alive)[ITEMS], int32_t (&aux)[ITEMS]) const {
+    if (direct) {  // bitmap word + one 4-byte read (candidates from a bitmap pass skip the bitmap)
+      bool hit[ITEMS];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const unsigned long long off = (unsigned long long)((long long)key[i] - bm_min);
+        hit[i] = alive[i] && off < bm_bits;
+        if (bm) {
+          const uint32_t w = hit[i] ? __ldg(bm + (off >> 5)) : 0u;
+          hit[i] = hit[i] && ((w >> (off & 31)) & 1u);
+        }
+        if (hit[i] && !member_only) aux[i] = __ldg(direct + off);
+      }
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) alive[i] = alive[i] && (anti ? !hit[i] : hit[i]);
+      return;
+    }
     uint32_t h[ITEMS];
     bool pend[ITEMS], found[ITEMS];
     uint32_t cnt[ITEMS];

@@ -449,6 +449,25 @@ __device__ __forceinline__ int32_t ht_find(const void* slots, uint32_t mask, uin
 // orderkey -> o_orderdate through unique-key tables (PK sides); key (nationkey, year(o_orderdate));
 // state 0 sum(ext*(100-disc) - supplycost*qty).  Rows whose lookups miss drop out (inner joins).
 // Several rows per thread (kSharedItems) so their independent lookups overlap.
+__device__ __forceinline__ bool direct_get(const uint32_t* __restrict__ bm, long long mn, unsigned long long nbits,
+                                           const int32_t* __restrict__ val, long long key, int64_t& out) {
+  const unsigned long long off = (unsigned long long)(key - mn);
+  if (!bm || off >= nbits || !((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u)) return false;
+  out = __ldg(val + off);
+  return true;
+}
+
+// val[key - min] = pay[r] for the rows whose key is in the bitmap (a PK side: one row per key)
+template <typename KT>
+__global__ void k_direct_fill(const KT* __restrict__ keys, const int32_t* __restrict__ pay, int64_t n,
+                              const uint32_t* __restrict__ bm, long long mn, unsigned long long nbits,
+                              int32_t* __restrict__ val) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long off = (unsigned long long)((long long)__ldg(keys + r) - mn);
+    if (off < nbits && ((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u)) val[off] = __ldg(pay + r);
+  }
+}
+
 template <typename KT, int OKB>
 struct Q9FusedProg {
   const int32_t *partkey, *suppkey;
@@ -460,12 +479,16 @@ struct Q9FusedProg {
   const ulonglong2* ps;   // (partkey, suppkey) -> ps_supplycost
   uint32_t ps_mask;
   int ps_bits;
-  const ulonglong2* sup;  // suppkey -> s_nationkey
-  uint32_t sup_mask;
-  int sup_bits;
-  const ulonglong2* ord;  // orderkey -> o_orderdate
-  uint32_t ord_mask;
-  int ord_bits;
+  // suppkey -> s_nationkey and orderkey -> o_orderdate: direct-address arrays over each key range,
+  // valid where the build's exact bitmap has the key (entries elsewhere are never read)
+  const uint32_t* sup_bm;
+  long long sup_min;
+  unsigned long long sup_n;
+  const int32_t* sup_val;
+  const uint32_t* ord_bm;
+  long long ord_min;
+  unsigned long long ord_n;
+  const int32_t* ord_val;
   int* ovf_flag;
   static constexpr int kMaxNst = 1;
   static constexpr int kUnrollStates = 1;
@@ -521,17 +544,9 @@ struct Q9FusedProg {
       c.cost[i] = 0;
       nk[i] = 0;
       d[i] = 0;
+      if (f) f = direct_get(sup_bm, sup_min, sup_n, sup_val, (long long)sk[i], nk[i]);
+      if (f) f = direct_get(ord_bm, ord_min, ord_n, ord_val, (long long)ok[i], d[i]);
       if (f) f = pt_find<8>(ps, ps_mask, ps_bits, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i], c.cost[i]);
-      if (f)
-        f = pt_find_compact((const unsigned long long*)sup, sup_mask, sup_bits, (uint64_t)(int64_t)sk[i],
-                            (uint32_t)sk[i], nk[i]);
-      if constexpr (OKB == 4) {
-        if (f)
-          f = pt_find_compact((const unsigned long long*)ord, ord_mask, ord_bits, (uint64_t)(int64_t)ok[i],
-                              (uint32_t)ok[i], d[i]);
-      } else {
-        if (f) f = pt_find<8>(ord, ord_mask, ord_bits, (uint64_t)(int64_t)ok[i], d[i]);
-      }
       alive[i] = f;
       key[i] = ((uint64_t)(uint32_t)nk[i] << 32) | (uint32_t)civil_year((int32_t)d[i]);
     }
@@ -879,16 +894,11 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   if (!ops_plan && ht_p->bm && (okb4 || okb8) && w4(t->l_partkey) && w4(t->l_suppkey) && w8(t->l_quantity) &&
       w8(t->l_extendedprice) && w8(t->l_discount) && w4(t->ps_partkey) && w4(t->ps_suppkey) &&
       w8(t->ps_supplycost) && w4(t->s_suppkey) && w4(t->s_nationkey) && w4(t->o_orderdate)) {
-    // SX_Q9_ORDERS=all: one PK table over every order (radix-partitioned build) and a dense pass
-    // over lineitem; default: semi-join reduction of orders through the green lineitems' keys
-    const bool orders_all = getenv("SX_Q9_ORDERS") && std::strcmp(getenv("SX_Q9_ORDERS"), "all") == 0;
     // lineitem rows with a green part (exact bitmap semi-join; no columns materialised)
     sx_sel sel_l{0, nullptr};
-    if (!orders_all) {
-      SX_TRY(sx_hash_probe(ctx, ht_p, &t->l_partkey, 1, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0,
-                           nullptr, 0, &sel_l, nullptr, nullptr));
-      bag.keep(sel_l);
-    }
+    SX_TRY(sx_hash_probe(ctx, ht_p, &t->l_partkey, 1, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0,
+                         nullptr, 0, &sel_l, nullptr, nullptr));
+    bag.keep(sel_l);
     sx_col pscols[2] = {t->ps_partkey, t->ps_suppkey};
     sx_sel sel_ps;
     SX_TRY(sx_hash_probe(ctx, ht_p, pscols, 2, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0, nullptr,
@@ -906,28 +916,49 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     {
       ProfScope pb(ctx, "hash_build");
       SX_TRY(build_payload_table(ctx, pscols, 2, t->ps_supplycost, &sel_ps, &pt.t[0]));
-      SX_TRY(build_payload_table(ctx, &t->s_suppkey, 1, t->s_nationkey, nullptr, &pt.t[1]));
-      pb.set_bytes((8.0 + 4.0 + 16.0) * sel_ps.len + (8.0 + 16.0) * t->s_suppkey.len);
+      pb.set_bytes((8.0 + 4.0 + 16.0) * sel_ps.len);
     }
-    if (orders_all) {
-      ProfScope pb(ctx, "hash_build");
-      SX_TRY(build_payload_table(ctx, &t->o_orderkey, 1, t->o_orderdate, nullptr, &pt.t[2]));
-      pb.set_bytes((type_width(t->o_orderkey.type) + 4.0 + 8.0) * t->o_orderkey.len);
-    } else {
-      // orders semi-join reduction: only orders with a green line (their keys' bitmap) are built
-      SX_TRY(sx_hash_build(ctx, &t->l_orderkey, 1, &k0, 1, &sel_l, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
-      bag.keep(ht_lo);
-      sx_sel sel_o;
-      SX_TRY(sx_hash_probe(ctx, ht_lo, &t->o_orderkey, 1, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr,
-                           0, nullptr, 0, &sel_o, nullptr, nullptr));
-      bag.keep(sel_o);
-      ProfScope pb(ctx, "hash_build");
-      SX_TRY(build_payload_table(ctx, &t->o_orderkey, 1, t->o_orderdate, &sel_o, &pt.t[2]));
-      pb.set_bytes((4.0 + type_width(t->o_orderkey.type) + 4.0 + 16.0) * sel_o.len);
+    // supplier: membership bitmap over the suppkey range + a direct nation array
+    sx_ht* ht_s;
+    SX_TRY(sx_hash_build(ctx, &t->s_suppkey, 1, &k0, 1, nullptr, nullptr, 0, SX_BUILD_UNIQUE | SX_BUILD_MEMBERSHIP, &ht_s));
+    bag.keep(ht_s);
+    int32_t* s_nat = nullptr;
+    if (!ht_s->bm && t->s_suppkey.len > 0) return set_err(ctx, SX_EUNSUPPORTED, "Q9: suppkey range too wide");
+    SX_TRY(alloc(ctx, &s_nat, (size_t)(ht_s->bm_bits > 0 ? ht_s->bm_bits : 1)));
+    bag.bufs.push_back(s_nat);
+    if (t->s_suppkey.len > 0) {
+      const int64_t ns = t->s_suppkey.len;
+      k_direct_fill<int32_t><<<persistent_grid(ctx, 8, (ns + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+          (const int32_t*)t->s_suppkey.data, (const int32_t*)t->s_nationkey.data, ns, ht_s->bm, ht_s->bm_min,
+          ht_s->bm_bits, s_nat);
+      SX_CHECK_LAUNCH();
     }
-    if (pt.t[0].kb != 8 || pt.t[1].kb != 4 || !pt.t[1].compact || pt.t[2].kb != (okb4 ? 4 : 8) ||
-        pt.t[2].compact != (okb4 ? 1 : 0))
-      return set_err(ctx, SX_EINVAL, "Q9: unexpected table layouts");
+    // orders semi-join reduction: the exact bitmap of the green lines' orderkeys; o_orderdate is
+    // then scattered into a direct array over that key range for exactly those orders (one pass
+    // over orders, no hash table: each later lookup is one bitmap word and one 4-byte read)
+    SX_TRY(sx_hash_build(ctx, &t->l_orderkey, 1, &k0, 1, &sel_l, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
+    bag.keep(ht_lo);
+    if (!ht_lo->bm && sel_l.len > 0) return set_err(ctx, SX_EUNSUPPORTED, "Q9: orderkey range too wide");
+    int32_t* o_date = nullptr;
+    SX_TRY(alloc(ctx, &o_date, (size_t)(ht_lo->bm_bits > 0 ? ht_lo->bm_bits : 1)));
+    bag.bufs.push_back(o_date);
+    {
+      ProfScope pb(ctx, "hash_build");
+      const int64_t no = t->o_orderkey.len;
+      if (no > 0 && ht_lo->bm) {
+        if (okb4)
+          k_direct_fill<int32_t><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+              (const int32_t*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, ht_lo->bm, ht_lo->bm_min,
+              ht_lo->bm_bits, o_date);
+        else
+          k_direct_fill<long long><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+              (const long long*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, ht_lo->bm,
+              ht_lo->bm_min, ht_lo->bm_bits, o_date);
+        SX_CHECK_LAUNCH();
+      }
+      pb.set_bytes((type_width(t->o_orderkey.type) + 4.0) * no);
+    }
+    if (pt.t[0].kb != 8) return set_err(ctx, SX_EINVAL, "Q9: unexpected table layouts");
     ProfScope pg(ctx, "probe_groupby");
     sx_col tcols[6] = {t->s_nationkey, t->ps_supplycost, t->l_quantity, t->l_extendedprice, t->l_discount,
                        t->o_orderdate};  // types only: the plan's state layout
@@ -949,7 +980,7 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     SX_TRY(check_states(ctx, plan, {ST_SUM}));
     // gather the semi-join's rows (default); SX_Q9_SCAN=dense scans every lineitem row instead
     // (measured 20.6 vs 6.4 ms at SF100: the dense pass is bound by its 6e8 bitmap lookups)
-    const bool gather = !orders_all && !(getenv("SX_Q9_SCAN") && std::strcmp(getenv("SX_Q9_SCAN"), "dense") == 0);
+    const bool gather = !(getenv("SX_Q9_SCAN") && std::strcmp(getenv("SX_Q9_SCAN"), "dense") == 0);
     const int64_t n = gather ? sel_l.len : t->l_partkey.len;
     const int32_t* gsel = gather ? sel_l.idx : nullptr;
     auto fill = [&](auto& pr) {
@@ -964,12 +995,14 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       pr.ps = pt.t[0].slots;
       pr.ps_mask = pt.t[0].mask;
       pr.ps_bits = pt.t[0].pbits;
-      pr.sup = pt.t[1].slots;
-      pr.sup_mask = pt.t[1].mask;
-      pr.sup_bits = pt.t[1].pbits;
-      pr.ord = pt.t[2].slots;
-      pr.ord_mask = pt.t[2].mask;
-      pr.ord_bits = pt.t[2].pbits;
+      pr.sup_bm = ht_s->bm;
+      pr.sup_min = ht_s->bm_min;
+      pr.sup_n = ht_s->bm_bits;
+      pr.sup_val = s_nat;
+      pr.ord_bm = ht_lo->bm;
+      pr.ord_min = ht_lo->bm_min;
+      pr.ord_n = ht_lo->bm_bits;
+      pr.ord_val = o_date;
       pr.ovf_flag = ctx->d_flags;
     };
     if (okb4) {

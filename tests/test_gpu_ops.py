@@ -383,3 +383,31 @@ def test_groupby_partitioned_ranges(ctx, ng, hint, nkeys):
     want = oracle.groupby([k[m], k2[m], v[m], w[m]], list(range(nkeys)), aggs)
     check_gb(got, want)
     assert g == len(want)
+
+
+@pytest.mark.parametrize("direct", ["1", "0"])
+def test_unique_build_direct_address(ctx, monkeypatch, direct):
+    """Unique single-key builds whose table would exceed 8 MB over a small key range become a
+    bitmap + direct row array (no hash table); SX_DIRECT=0 keeps the table.  INNER (with payload
+    gather and a probe predicate), SEMI and ANTI equal the oracle's either way."""
+    monkeypatch.setenv("SX_DIRECT", direct)
+    rng = np.random.default_rng(21)
+    nb = 700_001
+    bk = (rng.permutation(nb * 3)[:nb] - nb).astype(np.int32)  # unique, negatives included
+    bp = rng.integers(-10**9, 10**9, nb).astype(np.int64)
+    npr = 2_000_003
+    pk = rng.integers(-nb - 5, 2 * nb + 5, npr).astype(np.int32)
+    pw = rng.integers(0, 10, npr).astype(np.int32)
+    b, p = dev(bk), dev(pk)
+    ht = ctx.hash_build([c(b)], [0], unique=True)
+    op, ob, (pay,) = ctx.hash_probe(ht, [c(p), c(dev(pw))], [0], "inner", where=[(1, "lt", 7)],
+                                    build_cols=[c(b), c(dev(bp))], bp=[1])
+    m = pw < 7
+    wp, wb = oracle.join(bk, pk[m], "inner")
+    idx = np.nonzero(m)[0]
+    got = sorted(zip(op.cpu().numpy().tolist(), ob.cpu().numpy().tolist()))
+    assert got == sorted(zip(idx[wp].tolist(), wb.tolist()))
+    assert np.array_equal(pay.cpu().numpy(), bp[ob.cpu().numpy()])
+    for jt in ("semi", "anti"):
+        got, _, _ = ctx.hash_probe(ht, [c(p)], [0], jt)
+        assert np.array_equal(got.cpu().numpy(), oracle.join(bk, pk, jt)), jt
