@@ -170,3 +170,17 @@ def test_q1_bulk_staged(ctx, monkeypatch):
         want = oracle.run_query(q, host)
         got = T.run(q)
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
+
+
+def test_q9_q3_wide_orderkeys(ctx):
+    """int64 orderkeys spread over more than 2^30 (no exact bitmaps: Q9's fused plan falls back to the
+    operator-at-a-time plan, Q3's orders build keeps its hash table) still match the oracle."""
+    host = gen.cpu_tables(10, seed=3)
+    host = {t: dict(c) for t, c in host.items()}
+    for t, col in (("orders", "o_orderkey"), ("lineitem", "l_orderkey")):
+        host[t][col] = host[t][col].astype(np.int64) * (1 << 24) + 5
+    T = tpch.Tpch(ctx, to_dev(host))
+    for q in ("q9", "q3", "q18"):
+        want = oracle.run_query(q, host)
+        got = T.run(q)
+        assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
