@@ -361,6 +361,25 @@ __global__ void __launch_bounds__(kBlock) k_runs_own_dense(const __grid_constant
   bool bad = false, ovf = false;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
+  // HAVING and the slot layout in registers (not re-read from the parameter bank in every branch)
+  const int hv_op = hv.hv_op, kb = L.key_bytes, o8 = L.off8[0], o4 = L.off4[0], sb = L.slot_bytes;
+  const long long hv_lo = hv.hv_lo, hv_hi = hv.hv_hi;
+  const bool has_hv = hv.has_having != 0;
+  auto passes = [&](unsigned long long lo, int32_t hi) -> bool {
+    if (!has_hv) return true;
+    if (hi == ((long long)lo < 0 ? -1 : 0)) return cmp(hv_op, (long long)lo, hv_lo, hv_hi);  // fits int64
+    return hv.hv_ok_state(lo, hi);
+  };
+  auto emit = [&](uint64_t gk, unsigned long long lo, int32_t hi) {
+    const unsigned long long pos = atomicAdd(cursor, 1ull);
+    if ((int64_t)pos < cap_out) {
+      uint8_t* d = out + pos * sb;
+      if (kb == 4) *(unsigned*)d = (unsigned)gk;
+      else *(unsigned long long*)d = gk;
+      *(unsigned long long*)(d + o8) = lo;
+      *(int*)(d + o4) = hi;
+    }
+  };
   // all lanes of a warp run the same number of iterations (shuffles below)
   for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R; wbase < n; wbase += stride) {
     const int64_t r0 = wbase + (int64_t)lane * R;
@@ -431,16 +450,7 @@ __global__ void __launch_bounds__(kBlock) k_runs_own_dense(const __grid_constant
         if (open && small) {  // the int64 partial as 96 bits
           hi = (long long)lo < 0 ? -1 : 0;
         }
-        if (open && hv.hv_ok_state(lo, hi)) {  // the previous owned group ended at row i - 1
-          const unsigned long long pos = atomicAdd(cursor, 1ull);
-          if ((int64_t)pos < cap_out) {
-            uint8_t* d = out + pos * L.slot_bytes;
-            if (L.key_bytes == 4) *(unsigned*)d = (unsigned)gk;
-            else *(unsigned long long*)d = gk;
-            *(unsigned long long*)(d + L.off8[0]) = lo;
-            *(int*)(d + L.off4[0]) = hi;
-          }
-        }
+        if (open && passes(lo, hi)) emit(gk, lo, hi);  // the previous owned group ended at row i - 1
         open = true;
         gk = key[i];
         lo = 0;
@@ -481,16 +491,7 @@ __global__ void __launch_bounds__(kBlock) k_runs_own_dense(const __grid_constant
         }
         if (more && steps == kRunAhead && r < n) atomicExch(flags + 1, 1);
       }
-      if (hv.hv_ok_state(lo, hi)) {
-        const unsigned long long pos = atomicAdd(cursor, 1ull);
-        if ((int64_t)pos < cap_out) {
-          uint8_t* d = out + pos * L.slot_bytes;
-          if (L.key_bytes == 4) *(unsigned*)d = (unsigned)gk;
-          else *(unsigned long long*)d = gk;
-          *(unsigned long long*)(d + L.off8[0]) = lo;
-          *(int*)(d + L.off4[0]) = hi;
-        }
-      }
+      if (passes(lo, hi)) emit(gk, lo, hi);
     }
   }
   if (bad) atomicExch(flags, 1);
@@ -581,7 +582,7 @@ inline int agg_out_type(int op) {
 }
 
 constexpr int64_t kSharedMaxGroups = 4096;      // K10 eligibility (hinted groups)
-constexpr uint64_t kRangesMaxBytes = 100u << 10; // K10p per-CTA table bytes (two CTAs per SM)
+constexpr uint64_t kRangesMaxBytes = 100u << 10; // K10p per-CTA table bytes (at most; smaller when it suffices)
 constexpr int kSharedItems = 1;                  // K10 rows per thread per step (code size vs MLP)
 // A program may ask for more rows per thread (P::kSharedItems): fused probe chains need the
 // memory-level parallelism of several independent rows per thread.
@@ -628,12 +629,16 @@ inline sx_status gb_ranges(sx_ctx* ctx, const InterpProg& prog, const GbPlan& P,
   if (nc > 12) return set_err(ctx, SX_EINVAL, "group-by references too many columns for partitioning");
   // the largest shared table that fits kRangesMaxBytes (two CTAs per SM); partitions sized so
   // their expected group count fills at most half of it (load <= 0.5)
-  uint64_t scap = 1;
-  while ((2 * scap + 1) * (uint64_t)L.slot_bytes <= kRangesMaxBytes) scap <<= 1;
-  if (scap < 256) return SX_EUNSUPPORTED;
+  uint64_t smax = 1;
+  while ((2 * smax + 1) * (uint64_t)L.slot_bytes <= kRangesMaxBytes) smax <<= 1;
+  if (smax < 256) return SX_EUNSUPPORTED;
+  // partitions of ~512 groups (tables of 1024 slots: several CTAs per SM), more per partition
+  // only when the fan-out limit (2^10) forces it
   int bits = 1;
-  while (bits < 10 && (uint64_t)(groups_hint >> bits) > scap / 2) ++bits;
-  if ((uint64_t)(groups_hint >> bits) > scap / 2) return SX_EUNSUPPORTED;  // too many groups: other paths
+  while (bits < 10 && (uint64_t)(groups_hint >> bits) > 512) ++bits;
+  const uint64_t gpp = (uint64_t)(groups_hint >> bits) + 1;
+  uint64_t scap = pow2_at_least(gpp + gpp / 2);  // load <= 2/3
+  if (scap > smax) return SX_EUNSUPPORTED;  // too many groups per partition: other paths
   std::vector<int64_t> off(((size_t)1 << bits) + 1);
   const DCol k0 = A.cols[A.kc[0]], k1 = A.cols[P.nkeys > 1 ? A.kc[1] : A.kc[0]];
   SX_TRY(radix_partition_carry(ctx, k0, k1, P.nkeys, carry, width, nc, sel, n, bits, out, off.data()));
@@ -886,7 +891,7 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       bool ident = true;
       for (int k = 0; k < P.nkeys; ++k) ident = ident && P.key_fn[k] == SX_KEY_IDENTITY;
       if (!ranges_off && n >= (1 << 22) && !small && !keyless && nsub == 1 && attempt == 0 && ident &&
-          groups_hint > kSharedMaxGroups) {
+          shared_cap == 0 && groups_hint > 256) {  // (K10 covers what fits one shared table)
         const sx_status rs = gb_ranges(ctx, prog, P, sel, n, groups_hint, L, t, scr);
         if (rs == SX_OK) ranges_done = true;
         else if (rs != SX_EUNSUPPORTED) return rs;

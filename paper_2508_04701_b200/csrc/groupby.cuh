@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kBlock) k_gb_shared(const __grid_constant__ P 
 // row range of one partition at a time in a shared-memory table (as K10) and merges it into the
 // global table once per (range, group) instead of once per row.  items[2i], items[2i+1] = [lo, hi).
 template <class P, int ITEMS>
-__global__ void __launch_bounds__(kBlock) k_gb_ranges(const __grid_constant__ P prog, const int64_t* __restrict__ items,
+__global__ void __launch_bounds__(kBlock, 3) k_gb_ranges(const __grid_constant__ P prog, const int64_t* __restrict__ items,
                                                       int64_t nitems, const __grid_constant__ Layout L, Table t,
                                                       uint32_t scap) {
   extern __shared__ __align__(16) uint8_t sm_tab[];
