@@ -897,6 +897,21 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
         else if (rs != SX_EUNSUPPORTED) return rs;
       }
     }
+    if constexpr (has_dense_shared<Prog>::value) {
+      // K10d: dense vector-loading program into a per-CTA shared table (hinted mid G)
+      if (!dense_done && n > 0 && !sel && shared_cap && nsub == 1) {
+        size_t smem = (size_t)(shared_cap + 1) * L.slot_bytes;
+        SX_CUDA(cudaFuncSetAttribute(k_gb_dense_shared<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_dense_shared<Prog>, kBlock, smem));
+        if (per_sm < 1) per_sm = 1;
+        const int64_t groups = (n + Prog::kDenseRows - 1) / Prog::kDenseRows;
+        const unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, (groups + kBlock - 1) / kBlock);
+        k_gb_dense_shared<Prog><<<grid, kBlock, smem, SX_STREAM(ctx)>>>(prog, n, L, t, shared_cap);
+        SX_CHECK_LAUNCH();
+        dense_done = true;
+      }
+    }
     if (dense_done || ranges_done) {
     } else if (n > 0 && small) {
       size_t smem = small_smem_bytes(L.nst);

@@ -463,6 +463,61 @@ __global__ void __launch_bounds__(kBlock) k_gb_shared(const __grid_constant__ P 
   }
 }
 
+// ------------------------------------------------------------------------------ K10d: dense + shared
+// K10 with the dense front end of K9d: a program exposing dense<R>() (R consecutive rows with
+// 128-bit loads, e.g. a fused probe chain) aggregates into a per-CTA shared-memory table.  For
+// mid G over a full scan where gathers through a selection would move more sectors than a
+// streaming read of every column.
+template <class P>
+__global__ void __launch_bounds__(kBlock) k_gb_dense_shared(const __grid_constant__ P prog, int64_t n,
+                                                            const __grid_constant__ Layout L, Table t, uint32_t scap) {
+  constexpr int R = P::kDenseRows;
+  constexpr int NST = P::kDenseNst;
+  extern __shared__ __align__(16) uint8_t sm_tab[];
+  __shared__ int s_side, s_full;
+  const size_t bytes = (size_t)(scap + 1) * L.slot_bytes;
+  for (size_t j = threadIdx.x * 8; j < bytes; j += blockDim.x * 8) *(unsigned long long*)(sm_tab + j) = 0;
+  if (threadIdx.x == 0) { s_side = 0; s_full = 0; }
+  __syncthreads();
+  const Table st{sm_tab, scap - 1, &s_side, &s_full};
+  bool ovf = false;
+  const int64_t ngroups = (n + R - 1) / R;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * blockDim.x) {
+    bool alive[R];
+    uint64_t key[R];
+    int64_t v[R][NST];
+    bool fast = true;
+    prog.template dense<R>(g * R, n, alive, key, v, fast);
+    if (!fast) ovf = true;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (!alive[i]) continue;
+      uint8_t* sp = *(volatile int*)&s_full ? nullptr : find_or_insert(st, L, key[i]);
+#pragma unroll
+      for (int a = 0; a < NST; ++a) {
+        const int kd = prog.kind(a, L);
+        if (sp) apply_state_smem(sp, L, a, (unsigned long long)v[i][a], (kd == ST_SUM && v[i][a] < 0) ? -1 : 0);
+        else gb_row_to_global(t, L, key[i], a, v[i][a]);
+      }
+    }
+  }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e <= scap; e += blockDim.x) {
+    const uint8_t* sl = sm_tab + (size_t)e * L.slot_bytes;
+    uint64_t key;
+    if (e == scap) {
+      if (!s_side) continue;
+      key = 0;
+    } else {
+      key = L.key_bytes == 4 ? (uint64_t)*(const unsigned*)sl : *(const unsigned long long*)sl;
+      if (!key) continue;
+    }
+    uint8_t* p = find_or_insert(t, L, key);
+    if (p) merge_slot(p, sl, L);
+  }
+}
+
 // ------------------------------------------------------------------------------ K10p: ranges
 // Mid G (more groups than one shared-memory table holds): the input is radix-partitioned on the
 // group key first (H5), so each partition holds ~1/P of the groups; a CTA then aggregates one
@@ -1252,6 +1307,11 @@ inline size_t bulk_stage_bytes() {
   for (int c = 0; c < P::kBulkCols; ++c) b += (size_t)kBulkTile * P::bulk_width(c);
   return b;
 }
+
+template <class P, class = void>
+struct has_dense_shared : std::false_type {};
+template <class P>
+struct has_dense_shared<P, std::void_t<decltype(P::kDenseShared)>> : std::true_type {};
 
 template <class P, class = void>
 struct dense_min_blocks { static constexpr int value = 2; };

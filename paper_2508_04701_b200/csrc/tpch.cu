@@ -558,6 +558,45 @@ struct Q9FusedProg {
     for (int i = 0; i < I; ++i)
       v[i] = sub_ck(mul_ck(c.ext[i], sub_ck(100, c.disc[i], ovf), ovf), mul_ck(c.cost[i], c.qty[i], ovf), ovf);
   }
+  // Dense interface (K10d): 8 consecutive lineitem rows, all six columns with 128-bit streaming
+  // loads (every sector is read once: cheaper than gathering 5.4% of the rows' sectors), the
+  // green-part bitmap, then the three lookups for the green rows only.
+  static constexpr int kDenseNst = 1;
+  static constexpr int kDenseRows = 8;
+  static constexpr bool kDenseShared = true;
+  template <int R>
+  __device__ __forceinline__ void dense(int64_t r0, int64_t n, bool (&alive)[R], uint64_t (&key)[R],
+                                        int64_t (&v)[R][kDenseNst], bool& fast) const {
+    static_assert(R == 8, "8 rows");
+    int64_t pk[R], sk[R], ok[R], q[R], e[R], d[R];
+    const bool full = r0 + R <= n;
+    dense_load<R>(DCol{partkey, SX_I32, 0}, r0, n, full, pk);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const unsigned long long off = (unsigned long long)(pk[i] - pbm_min);
+      const bool in = r0 + i < n && off < pbm_bits;
+      const uint32_t w = in ? __ldg(pbm + (off >> 5)) : 0u;
+      alive[i] = in && ((w >> (off & 31)) & 1u);
+    }
+    dense_load<R>(DCol{suppkey, SX_I32, 0}, r0, n, full, sk);
+    dense_load<R>(DCol{orderkey, sizeof(KT) == 4 ? SX_I32 : SX_I64, 0}, r0, n, full, ok);
+    dense_load<R>(DCol{qty, SX_I64, 0}, r0, n, full, q);
+    dense_load<R>(DCol{ext, SX_I64, 0}, r0, n, full, e);
+    dense_load<R>(DCol{disc, SX_I64, 0}, r0, n, full, d);
+    bool ovf = false;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      bool f = alive[i];
+      int64_t cost = 0, nk = 0, dt = 0;
+      if (f) f = direct_get(sup_bm, sup_min, sup_n, sup_val, sk[i], nk);
+      if (f) f = direct_get(ord_bm, ord_min, ord_n, ord_val, ok[i], dt);
+      if (f) f = pt_find<8>(ps, ps_mask, ps_bits, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i], cost);
+      alive[i] = f;
+      key[i] = ((uint64_t)(uint32_t)nk << 32) | (uint32_t)civil_year((int32_t)dt);
+      v[i][0] = f ? sub_ck(mul_ck(e[i], sub_ck(100, d[i], ovf), ovf), mul_ck(cost, q[i], ovf), ovf) : 0;
+    }
+    fast = !ovf;
+  }
 };
 
 // Column width checks for the compiled plans (other layouts take the interpreted operator path).
@@ -894,11 +933,16 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   // the fused plan needs exact key-range bitmaps (key ranges <= 2^30); SX_EUNSUPPORTED from it
   // (e.g. SF1000's 64-bit orderkey range) falls back to the operator-at-a-time plan
   auto fused = [&]() -> sx_status {
+    // dense (default): one streaming pass over every lineitem column with the green-part test
+    // inside (K10d); SX_Q9_SCAN=gather: semi-join first, then gather the selected rows
+    const bool gather = getenv("SX_Q9_SCAN") && std::strcmp(getenv("SX_Q9_SCAN"), "gather") == 0;
     // lineitem rows with a green part (exact bitmap semi-join; no columns materialised)
     sx_sel sel_l{0, nullptr};
-    SX_TRY(sx_hash_probe(ctx, ht_p, &t->l_partkey, 1, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0,
-                         nullptr, 0, &sel_l, nullptr, nullptr));
-    bag.keep(sel_l);
+    if (gather) {
+      SX_TRY(sx_hash_probe(ctx, ht_p, &t->l_partkey, 1, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0,
+                           nullptr, 0, &sel_l, nullptr, nullptr));
+      bag.keep(sel_l);
+    }
     sx_col pscols[2] = {t->ps_partkey, t->ps_suppkey};
     sx_sel sel_ps;
     SX_TRY(sx_hash_probe(ctx, ht_p, pscols, 2, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0, nullptr,
@@ -933,13 +977,17 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
           ht_s->bm_bits, s_nat);
       SX_CHECK_LAUNCH();
     }
-    // orders semi-join reduction: the exact bitmap of the green lines' orderkeys (a membership-only
-    // build); o_orderdate is then scattered into a direct array over that key range for exactly
-    // those orders (one pass over orders, no hash table: each later lookup is one bitmap word and
-    // one 4-byte read).  (A bitmap of every orderkey measured 0.25 ms slower at SF100.)
-    SX_TRY(sx_hash_build(ctx, &t->l_orderkey, 1, &k0, 1, &sel_l, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
+    // orders: the exact bitmap of the orderkeys that can be looked up (gather mode: the green
+    // lines' keys, a semi-join reduction; dense mode: every orderkey), then o_orderdate scattered
+    // into a direct array over that key range (one pass over orders, no hash table: each later
+    // lookup is one bitmap word and one 4-byte read)
+    if (gather)
+      SX_TRY(sx_hash_build(ctx, &t->l_orderkey, 1, &k0, 1, &sel_l, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
+    else
+      SX_TRY(sx_hash_build(ctx, &t->o_orderkey, 1, &k0, 1, nullptr, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
     bag.keep(ht_lo);
-    if (!ht_lo->bm && sel_l.len > 0) return set_err(ctx, SX_EUNSUPPORTED, "Q9: orderkey range too wide");
+    if (!ht_lo->bm && (gather ? sel_l.len : t->o_orderkey.len) > 0)
+      return set_err(ctx, SX_EUNSUPPORTED, "Q9: orderkey range too wide");
     int32_t* o_date = nullptr;
     SX_TRY(alloc(ctx, &o_date, (size_t)(ht_lo->bm_bits > 0 ? ht_lo->bm_bits : 1)));
     bag.bufs.push_back(o_date);
@@ -979,9 +1027,6 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     GbPlan plan;
     SX_TRY(gb_plan(ctx, tcols, 6, gk, 2, &ga, 1, nullptr, &plan));
     SX_TRY(check_states(ctx, plan, {ST_SUM}));
-    // gather the semi-join's rows (default); SX_Q9_SCAN=dense scans every lineitem row instead
-    // (measured 20.6 vs 6.4 ms at SF100: the dense pass is bound by its 6e8 bitmap lookups)
-    const bool gather = !(getenv("SX_Q9_SCAN") && std::strcmp(getenv("SX_Q9_SCAN"), "dense") == 0);
     const int64_t n = gather ? sel_l.len : t->l_partkey.len;
     const int32_t* gsel = gather ? sel_l.idx : nullptr;
     auto fill = [&](auto& pr) {
