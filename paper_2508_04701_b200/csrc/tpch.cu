@@ -933,9 +933,10 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   // the fused plan needs exact key-range bitmaps (key ranges <= 2^30); SX_EUNSUPPORTED from it
   // (e.g. SF1000's 64-bit orderkey range) falls back to the operator-at-a-time plan
   auto fused = [&]() -> sx_status {
-    // dense (default): one streaming pass over every lineitem column with the green-part test
-    // inside (K10d); SX_Q9_SCAN=gather: semi-join first, then gather the selected rows
-    const bool gather = getenv("SX_Q9_SCAN") && std::strcmp(getenv("SX_Q9_SCAN"), "gather") == 0;
+    // gather (default): semi-join first, then gather the selected rows into the probe-chain
+    // group-by; SX_Q9_SCAN=dense: one streaming pass over every lineitem column with the
+    // green-part test inside (K10d; measured slower at SF100)
+    const bool gather = !(getenv("SX_Q9_SCAN") && std::strcmp(getenv("SX_Q9_SCAN"), "dense") == 0);
     // lineitem rows with a green part (exact bitmap semi-join; no columns materialised)
     sx_sel sel_l{0, nullptr};
     if (gather) {
