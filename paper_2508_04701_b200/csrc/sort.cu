@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(kLsdThreads) k_lsd_scatter(const __grid_consta
   extern __shared__ uint32_t stage[];  // [nwords][T]
   __shared__ int wcnt[kLsdWarps][256];
   __shared__ int dstart[256];
+  __shared__ int64_t s_off[256];  // this tile's global offset of each digit run
   __shared__ int s_warp[kLsdWarps];
   __shared__ uint8_t sdig[T];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = src.nwords;
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(kLsdThreads) k_lsd_scatter(const __grid_consta
     int wo = 0;
     for (int q = 0; q < w; ++q) wo += s_warp[q];
     dstart[d] = wo + x - run;
+    s_off[d] = offs[(int64_t)d * ntiles + blockIdx.x];
   }
   __syncthreads();
   // reorder the tile in shared memory (all words), then write digit runs to their offsets
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(kLsdThreads) k_lsd_scatter(const __grid_consta
   const int tcount = (int)min((int64_t)T, n - base);
   for (int p = threadIdx.x; p < tcount; p += kLsdThreads) {
     const int d = sdig[p];
-    const int64_t g = offs[(int64_t)d * ntiles + blockIdx.x] + (p - dstart[d]);
+    const int64_t g = s_off[d] + (p - dstart[d]);
     for (int j = 0; j < nw; ++j) dst.w[j][g] = stage[j * T + p];
   }
 }
