@@ -33,6 +33,8 @@ struct sx_ctx {
   int* d_flags = nullptr;          // [0] expression overflow, [1] table full, [2..] scratch
   unsigned int* d_counters = nullptr;  // tile counters etc. (64 entries)
   int64_t* h_pinned = nullptr;     // pinned host scratch for size reads (64 entries)
+  void* h_stage = nullptr;         // pinned host staging for result rows (grown on demand)
+  size_t h_stage_bytes = 0;
   bool profile = false;
   int64_t launches = 0;            // kernels launched by libsx on this ctx (sx_launch_count)
   struct Prof { char name[32]; cudaEvent_t a, b; double bytes; };

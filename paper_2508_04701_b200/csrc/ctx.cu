@@ -64,6 +64,7 @@ SX_EXPORT void sx_ctx_destroy(sx_ctx* ctx) {
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_counters);
   cudaFreeHost(ctx->h_pinned);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   delete ctx;
 }
 

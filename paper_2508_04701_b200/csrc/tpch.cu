@@ -683,16 +683,47 @@ sx_i128 i128_at(const std::vector<uint8_t>& v, int64_t i) {
 }
 
 // Gather `cols` by the permutation and copy them to host (one sync at the end).
+// The result rows: every output column gathered at the final permutation by ONE kernel into one
+// device buffer, then ONE copy into pinned host memory and one synchronisation.
 sx_status fetch_rows(sx_ctx* ctx, Bag& bag, const sx_col* cols, int n, const sx_sel& perm,
                      std::vector<std::vector<uint8_t>>& host) {
   host.assign(n, {});
+  if (n > kMaxGather) return set_err(ctx, SX_EINVAL, "fetch_rows: %d columns", n);
+  GatherSpec gs;
+  gs.n = n;
+  size_t off[kMaxGather + 1];
+  off[0] = 0;
   for (int i = 0; i < n; ++i) {
-    sx_col g;
-    SX_TRY(sx_gather(ctx, &cols[i], &perm, &g));
-    bag.keep(g);
-    SX_TRY(d2h(ctx, g, host[i]));
+    const int w = type_width(cols[i].type);
+    if (!w) return set_err(ctx, SX_ETYPE, "fetch_rows: column %d is not fixed-width", i);
+    gs.g[i].src = DCol{cols[i].data, cols[i].type, 0};
+    gs.g[i].by_aux = 0;
+    gs.g[i].width = w;
+    off[i + 1] = off[i] + (((size_t)perm.len * w + 15) & ~(size_t)15);
   }
+  uint8_t* dbuf;
+  SX_TRY(alloc(ctx, &dbuf, off[n] > 0 ? off[n] : 16));
+  bag.bufs.push_back(dbuf);
+  for (int i = 0; i < n; ++i) gs.g[i].dst = dbuf + off[i];
+  if (perm.len > 0) {
+    k_gather_multi<<<persistent_grid(ctx, 8, (perm.len + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+        perm.idx, nullptr, perm.len, gs);
+    SX_CHECK_LAUNCH();
+  }
+  if (ctx->h_stage_bytes < off[n]) {
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    ctx->h_stage = nullptr;
+    ctx->h_stage_bytes = 0;
+    SX_CUDA(cudaMallocHost(&ctx->h_stage, off[n] + (1 << 16)));
+    ctx->h_stage_bytes = off[n] + (1 << 16);
+  }
+  if (off[n]) SX_CUDA(cudaMemcpyAsync(ctx->h_stage, dbuf, off[n], cudaMemcpyDeviceToHost, ctx->stream));
   SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n; ++i) {
+    const size_t bytes = (size_t)perm.len * gs.g[i].width;
+    host[i].resize(bytes + 16);
+    std::memcpy(host[i].data(), (const uint8_t*)ctx->h_stage + off[i], bytes);
+  }
   return SX_OK;
 }
 
