@@ -205,6 +205,13 @@ SX_EXPORT sx_status sx_shuffle(sx_ctx* ctx, sx_comm* comm, const sx_col* cols, i
     out_cols[c].offsets = nullptr;
   }
   *out_rows = total;
+  if (ps.on()) {  // a shuffle's bytes are the bytes leaving this GPU
+    double w = 0, rows_out = 0;
+    for (int c = 0; c < ncols; ++c) w += type_width(cols[c].type);
+    for (int peer = 0; peer < g; ++peer)
+      if (peer != comm->rank) rows_out += (double)send[peer];
+    ps.set_bytes(w * rows_out);
+  }
   return SX_OK;
 }
 
@@ -238,5 +245,10 @@ SX_EXPORT sx_status sx_allgather(sx_ctx* ctx, sx_comm* comm, const sx_col* cols,
     out_cols[c].offsets = nullptr;
   }
   *out_rows = total;
+  if (ps.on()) {  // this rank's rows sent to every other rank
+    double w = 0;
+    for (int c = 0; c < ncols; ++c) w += type_width(cols[c].type);
+    ps.set_bytes(w * (double)n * (comm->nranks - 1));
+  }
   return SX_OK;
 }
