@@ -184,3 +184,30 @@ def test_q9_q3_wide_orderkeys(ctx):
         want = oracle.run_query(q, host)
         got = T.run(q)
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
+
+
+@pytest.mark.parametrize("empty", ["lineitem", "orders_lineitem", "part", "customer"])
+def test_queries_on_empty_tables(ctx, empty):
+    """Degenerate inputs: empty lineitem (and orders), no part, no customer — every plan returns
+    what the oracle returns (empty results, a NULL Q6, no groups)."""
+    host = gen.cpu_tables(10, seed=9)
+    host = {t: {c: a.copy() for c, a in cols.items()} for t, cols in host.items()}
+
+    def clear(t):
+        for c in list(host[t]):
+            if c == "p_name_offsets":
+                host[t][c] = host[t][c][:1].copy()
+                host[t][c][:] = 0
+            elif c == "p_name_chars":
+                host[t][c] = host[t][c][:0]
+            else:
+                host[t][c] = host[t][c][:0]
+
+    for t in {"lineitem": ["lineitem"], "orders_lineitem": ["orders", "lineitem"], "part": ["part"],
+              "customer": ["customer"]}[empty]:
+        clear(t)
+    T = tpch.Tpch(ctx, to_dev(host))
+    for q in QUERIES:
+        want = oracle.run_query(q, host)
+        got = T.run(q)
+        assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
