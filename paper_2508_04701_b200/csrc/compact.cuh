@@ -90,8 +90,13 @@ __global__ void __launch_bounds__(kBlock, 4) k_compact_local(const __grid_consta
 // ITEMS consecutive rows, which the functor reads with 128-bit vector loads and returns as a bit
 // mask; survivors are ranked by a block scan of the per-thread counts and written (ascending) to
 // the tile's scratch region.  Same scratch layout and phases 2-3 as k_compact_local.
+template <class F, class = void>
+struct dense_blocks { static constexpr int value = 3; };
+template <class F>
+struct dense_blocks<F, std::void_t<decltype(F::kMinBlocks)>> { static constexpr int value = F::kMinBlocks; };
+
 template <class F, int ITEMS>
-__global__ void __launch_bounds__(kBlock, 3) k_compact_dense(const __grid_constant__ F f, int64_t n,
+__global__ void __launch_bounds__(kBlock, dense_blocks<F>::value) k_compact_dense(const __grid_constant__ F f, int64_t n,
                                                           int32_t* __restrict__ s_row, int32_t* __restrict__ s_aux,
                                                           int32_t* __restrict__ tile_cnt, int64_t ntiles) {
   constexpr int W = kBlock / 32;

@@ -100,9 +100,84 @@ __device__ __forceinline__ uint32_t dense_valid(int64_t r0, int64_t n) {
   return m >= ITEMS ? (ITEMS == 32 ? 0xffffffffu : ((1u << ITEMS) - 1u)) : (m <= 0 ? 0u : ((1u << m) - 1u));
 }
 
+// 32-bit column values of ITEMS rows (kept 32-bit: half the registers, 32-bit compares)
+template <int ITEMS>
+__device__ __forceinline__ void dense_load32(const int32_t* p, int64_t r0, int64_t n, bool full, int32_t (&x)[ITEMS]) {
+  if (full) {
+#pragma unroll
+    for (int j = 0; j < ITEMS / 4; ++j) {
+      const int4 v = __ldcs((const int4*)(p + r0) + j);
+      x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) x[i] = r0 + i < n ? __ldg(p + r0 + i) : 0;
+}
+
+// A predicate on a 32-bit column with 32-bit compares: constants outside the int32 range make a
+// comparison uniformly true or false, else they are exact as int32.
+template <int ITEMS>
+__device__ __forceinline__ uint32_t dense_pred32(const int32_t (&x)[ITEMS], const DPred& q) {
+  const long long lo = q.lo, hi = q.hi;
+  const bool lo_big = lo > INT32_MAX, lo_small = lo < INT32_MIN;
+  const bool hi_big = hi > INT32_MAX, hi_small = hi < INT32_MIN;
+  const int32_t l = (int32_t)(lo_big ? INT32_MAX : lo_small ? INT32_MIN : lo);
+  const int32_t h = (int32_t)(hi_big ? INT32_MAX : hi_small ? INT32_MIN : hi);
+  constexpr uint32_t all = ITEMS == 32 ? 0xffffffffu : ((1u << ITEMS) - 1u);
+  uint32_t m = 0;
+  switch (q.op) {  // uniform
+    case SX_LT:
+      if (lo_big) return all;
+      if (lo_small) return 0;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) m |= (x[i] < l ? 1u : 0u) << i;
+      return m;
+    case SX_LE:
+      if (lo_big) return all;
+      if (lo_small) return 0;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) m |= (x[i] <= l ? 1u : 0u) << i;
+      return m;
+    case SX_GT:
+      if (lo_small) return all;
+      if (lo_big) return 0;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) m |= (x[i] > l ? 1u : 0u) << i;
+      return m;
+    case SX_GE:
+      if (lo_small) return all;
+      if (lo_big) return 0;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) m |= (x[i] >= l ? 1u : 0u) << i;
+      return m;
+    case SX_EQ:
+      if (lo_big || lo_small) return 0;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) m |= (x[i] == l ? 1u : 0u) << i;
+      return m;
+    case SX_NE:
+      if (lo_big || lo_small) return all;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) m |= (x[i] != l ? 1u : 0u) << i;
+      return m;
+    default:  // BETWEEN lo..hi
+      if (lo_big || hi_small || lo > hi) return 0;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) m |= (x[i] >= l && x[i] <= h ? 1u : 0u) << i;
+      return m;
+  }
+}
+
 template <int ITEMS>
 __device__ __forceinline__ void dense_pred(const DCol& c, const DPred& q, int64_t r0, int64_t n, bool full,
                                            uint32_t& mask) {
+  if (c.type == SX_I32 || c.type == SX_DATE32) {
+    int32_t x32[ITEMS];
+    dense_load32<ITEMS>((const int32_t*)c.p, r0, n, full, x32);
+    mask &= dense_pred32<ITEMS>(x32, q);
+    return;
+  }
   int64_t x[ITEMS];
   dense_load<ITEMS>(c, r0, n, full, x);
   uint32_t m = 0;

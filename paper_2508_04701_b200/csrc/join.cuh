@@ -104,6 +104,7 @@ struct BitmapFn {
   unsigned long long bm_bits;
   int anti;
   static constexpr int kDenseItems = 16;
+  static constexpr int kMinBlocks = 4;  // light functor: 4 CTAs (32 warps) per SM
   template <int ITEMS>
   __device__ __forceinline__ bool hit(int64_t key, bool live) const {
     const unsigned long long off = (unsigned long long)(key - bm_min);
@@ -130,15 +131,26 @@ struct BitmapFn {
   __device__ __forceinline__ void eval_dense(int64_t r0, int64_t n, uint32_t& mask, int32_t (&)[ITEMS]) const {
     const bool full = r0 + ITEMS <= n;
     mask = dense_valid<ITEMS>(r0, n);
-    int64_t k[ITEMS];
-    dense_load<ITEMS>(DCol{k0, sizeof(KT) == 4 ? SX_I32 : SX_I64, 0}, r0, n, full, k);
     for (int p = 0; p < np; ++p) dense_pred<ITEMS>(cols[preds[p].col], preds[p], r0, n, full, mask);
     uint32_t m = 0;
+    if constexpr (sizeof(KT) == 4) {  // 32-bit keys stay 32-bit until the bitmap offset
+      int32_t k[ITEMS];
+      dense_load32<ITEMS>((const int32_t*)k0, r0, n, full, k);
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const bool live = (mask >> i) & 1u;
-      const bool h = hit<ITEMS>(k[i], live);
-      m |= ((live && (anti ? !h : h)) ? 1u : 0u) << i;
+      for (int i = 0; i < ITEMS; ++i) {
+        const bool live = (mask >> i) & 1u;
+        const bool h = hit<ITEMS>((int64_t)k[i], live);
+        m |= ((live && (anti ? !h : h)) ? 1u : 0u) << i;
+      }
+    } else {
+      int64_t k[ITEMS];
+      dense_load<ITEMS>(DCol{k0, SX_I64, 0}, r0, n, full, k);
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const bool live = (mask >> i) & 1u;
+        const bool h = hit<ITEMS>(k[i], live);
+        m |= ((live && (anti ? !h : h)) ? 1u : 0u) << i;
+      }
     }
     mask = m;
   }

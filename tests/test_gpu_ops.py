@@ -411,3 +411,20 @@ def test_unique_build_direct_address(ctx, monkeypatch, direct):
     for jt in ("semi", "anti"):
         got, _, _ = ctx.hash_probe(ht, [c(p)], [0], jt)
         assert np.array_equal(got.cpu().numpy(), oracle.join(bk, pk, jt)), jt
+
+
+@pytest.mark.parametrize("op", ["lt", "le", "gt", "ge", "eq", "ne", "between"])
+def test_filter_int32_constants_beyond_int32(ctx, op):
+    """32-bit dense predicate path: constants outside the int32 range (uniformly true / false) and
+    at its edges, vs the oracle's int64 comparisons; a ragged tail."""
+    rng = np.random.default_rng(17)
+    n = 50_021
+    x = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+    x[:4] = [-2**31, 2**31 - 1, 0, -1]
+    t = dev(x)
+    for lo, hi in ((2**40, 2**41), (-2**40, 2**40), (-2**40, -2**39), (2**31 - 1, 2**31), (-2**31, -2**31),
+                   (5, 3), (-7, 2**35)):
+        pr = (0, op, lo, hi) if op == "between" else (0, op, lo)
+        sel, _ = ctx.filter([c(t)], [pr])
+        want = oracle.filter([x.astype(np.int64)], [pr])
+        assert np.array_equal(sel.cpu().numpy(), want), (op, lo, hi)
