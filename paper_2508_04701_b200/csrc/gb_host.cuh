@@ -899,7 +899,7 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
     }
     if constexpr (has_dense_shared<Prog>::value) {
       // K10d: dense vector-loading program into a per-CTA shared table (hinted mid G)
-      if (!dense_done && n > 0 && !sel && shared_cap && nsub == 1) {
+      if (!dense_done && n > 0 && !sel && shared_cap && nsub == 1 && prog.dense_ok()) {
         size_t smem = (size_t)(shared_cap + 1) * L.slot_bytes;
         SX_CUDA(cudaFuncSetAttribute(k_gb_dense_shared<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
