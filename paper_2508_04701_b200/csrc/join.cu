@@ -748,7 +748,7 @@ sx_status build_payload_table(sx_ctx* ctx, const sx_col* keys, int nkeys, const 
   if (!is_int_type(pay.type)) return set_err(ctx, SX_ETYPE, "payload table: payload type %d", pay.type);
   const int64_t n = sel ? sel->len : keys[0].len;
   uint64_t cap = 64;
-  while (cap < (uint64_t)(2 * n)) cap <<= 1;
+  while (cap < (uint64_t)(n + n / 2)) cap <<= 1;  // load <= 2/3: a smaller table stays more L2-resident
   if (cap > (1ull << 32)) return set_err(ctx, SX_EINDEX, "payload table too large");
   PtArgs a{};
   a.k0 = DCol{keys[0].data, keys[0].type, 0};

@@ -259,7 +259,7 @@ struct Q6Prog {
   // rows make ext*disc < 2^40 an exact 32x32->64 product.
   static constexpr int kDenseNst = 2;
   static constexpr int kDenseRows = 8;
-  static constexpr int kDenseMinBlocks = 3;  // more rows in flight for the lazy (dependent) loads
+  static constexpr int kDenseMinBlocks = 4;  // more rows in flight for the lazy (dependent) loads
   template <int R>
   __device__ __forceinline__ void dense(int64_t r0, int64_t n, bool (&alive)[R], uint64_t (&key)[R],
                                         int64_t (&v)[R][kDenseNst], bool& fast) const {
