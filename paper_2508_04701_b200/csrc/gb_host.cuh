@@ -206,6 +206,7 @@ struct SlotFn {
 // is written for the groups that fail HAVING and no group numbering pass is needed; a key that
 // decreases anywhere flags the input as unsorted (host falls back to hashing).
 constexpr int kRunAhead = 64;
+constexpr int kRunOwnRows = 8;   // rows per thread in k_runs_own_dense (16 measured slower: 4.35 vs 3.44 ms)
 
 template <class P, class = void>
 struct runs_dense : std::false_type {};
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(kBlock) k_runs_own_dense(const __grid_constant
                                                            const __grid_constant__ Layout L,
                                                            const __grid_constant__ SlotFn hv, uint8_t* __restrict__ out,
                                                            int64_t cap_out, unsigned long long* cursor, int* flags) {
-  constexpr int R = kRunItems;
+  constexpr int R = kRunOwnRows;
   bool bad = false, ovf = false;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
@@ -722,8 +723,8 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
           const int64_t threads = (n + kRunItems - 1) / kRunItems;
           if constexpr (runs_dense<Prog>::value) {
             if (L.nst == 1 && L.kind[0] == ST_SUM && L.slot_bytes <= 32)
-              k_runs_own_dense<Prog><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0,
-                                       SX_STREAM(ctx)>>>(prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
+              k_runs_own_dense<Prog><<<persistent_grid(ctx, 8, ((n + kRunOwnRows - 1) / kRunOwnRows + kBlock - 1) / kBlock),
+                                       kBlock, 0, SX_STREAM(ctx)>>>(prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
             else
               k_runs_own<Prog><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
                   prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
