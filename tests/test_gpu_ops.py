@@ -428,3 +428,32 @@ def test_filter_int32_constants_beyond_int32(ctx, op):
         sel, _ = ctx.filter([c(t)], [pr])
         want = oracle.filter([x.astype(np.int64)], [pr])
         assert np.array_equal(sel.cpu().numpy(), want), (op, lo, hi)
+
+
+@pytest.mark.parametrize("maxlen", [40, 300])
+def test_filter_contains_edges(ctx, maxlen):
+    """Warp-cooperative CONTAINS: empty strings, matches at the first / last byte, a pattern split
+    across two neighbouring strings (must not match), warps whose byte span exceeds the shared
+    stage (maxlen 300: per-lane fallback), a ragged last warp, and the empty pattern."""
+    rng = np.random.default_rng(maxlen)
+    n = 10_007
+    strs = []
+    for i in range(n):
+        L = int(rng.integers(0, maxlen))
+        s = bytes(rng.integers(97, 123, L, dtype=np.uint8))
+        r = i % 7
+        if r == 0 and L >= 5:
+            s = b"green" + s[5:]
+        elif r == 1 and L >= 5:
+            s = s[:-5] + b"green"
+        elif r == 2:
+            s = s + b"gre"          # and the next string starts with "en": no match across the boundary
+        elif r == 3:
+            s = b"en" + s
+        strs.append(s)
+    offs = np.zeros(n + 1, np.int64)
+    offs[1:] = np.cumsum([len(x) for x in strs])
+    chars = np.frombuffer(b"".join(strs), np.uint8).copy()
+    for pat in (b"green", b"gre", b"", b"q"):
+        sel, _ = ctx.filter([sx.col(dev(chars), A.SX_STR, offsets=dev(offs))], [(0, "contains", pat)])
+        assert np.array_equal(sel.cpu().numpy(), oracle.contains(offs, chars, pat)), pat
