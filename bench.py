@@ -9,8 +9,8 @@ hash build/probe, group-by, top-k: SURVEY.md §8(a) H1-H9) over the resident SF1
 value     = algorithmic bytes scanned per step (every referenced column read once at its
             stored width, + mandatory state; SURVEY §8(d) / DESIGN.md) / device time, GB/s,
             whole job (sum over ranks).  Inputs (36 GB at SF100) are >> L2 (126 MB): no flush needed.
-e2e       = the same metric through the public C-ABI call with HOST (pinned) inputs: the H2D copy
-            of every referenced column and the D2H of the results are inside the timed region.
+e2e       = the same metric through the public C ABI with HOST (pinned) inputs: sx_tpch_upload copies
+            every column H2D inside libsx, the plans' results are written to host memory; all timed.
 roofline  = the dominant operator (largest device time in the step, from sx per-call CUDA events
             on the launching stream), achieved algorithmic GB/s vs MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline = the CPU oracle (single thread) on a bounded sample (SF 1) on this host.
@@ -348,9 +348,10 @@ def main():
                 "frac": round(ach / peak, 4) if ach else None, "traffic": traffic, "algorithmic_bytes": round(ob),
                 "ms_per_launch": round(dur, 4), "peak_source": peak_src}
 
-    # e2e: public C-ABI call with host (pinned) inputs; H2D + queries + result D2H timed
+    # e2e: the public C ABI with HOST (pinned) inputs: sx_tpch_upload copies every column H2D inside
+    # the library, the five plans run, their results land in host memory; all of it timed per step
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         host = {tn: {cn: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for cn, t in cols.items()}
                 for tn, cols in tables.items()}
         for tn, cols in tables.items():
@@ -358,27 +359,45 @@ def main():
                 host[tn][cn].copy_(t)
         torch.cuda.synchronize()
         h2d = sum(t.numel() * t.element_size() for cols in host.values() for t in cols.values())
-        d2h = 0
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            for tn, cols in host.items():
-                for cn, t in cols.items():
-                    tables[tn][cn].copy_(t, non_blocking=True)
+            Te = tpch.Tpch.upload(ctx, host)
             for q in QUERIES:
-                r = run(q)  # results land in host memory inside the call
-                d2h += 0
+                Te.run(q)  # results land in host memory inside the call
+            Te.free()
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1) / args.e2e_steps
         # result bytes per step (host row structs): Q1 4x, Q6 1x, Q3 10x, Q9 175x, Q18 100x rows
         d2h = 4 * 112 + 32 + 10 * 40 + 175 * 24 + 100 * 40
         ev = job_bytes / (e_ms / 1e3) / 1e9
-        if dist:
-            t = torch.tensor([e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ev = job_bytes / (float(t.item()) / 1e3) / 1e9
         e2e = {"value": round(ev, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h,
-               "ms_per_step": round(e_ms, 3)}
+               "ms_per_step": round(e_ms, 3), "path": "sx_tpch_upload (host pinned -> device inside libsx) + sx_tpch_q*"}
+        del host
+    elif not args.no_e2e:
+        # sharded: every rank's shard copied from pinned host memory, then the sharded plans
+        host = {tn: {cn: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for cn, t in cols.items()}
+                for tn, cols in tables.items()}
+        for tn, cols in tables.items():
+            for cn, t in cols.items():
+                host[tn][cn].copy_(t)
+        torch.cuda.synchronize()
+        h2d = sum(t.numel() * t.element_size() for cols in host.values() for t in cols.values())
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            for tn, cols in host.items():
+                for cn, t in cols.items():
+                    tables[tn][cn].copy_(t, non_blocking=True)
+            for q in QUERIES:
+                run(q)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+        d2h = 4 * 112 + 32 + 10 * 40 + 175 * 24 + 100 * 40
+        e2e = {"value": round(job_bytes / (e_ms / 1e3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": d2h, "ms_per_step": round(e_ms, 3)}
         del host
 
     cpu = None

@@ -307,6 +307,13 @@ typedef struct {
 } sx_tpch_params;
 void sx_tpch_default_params(sx_tpch_params* p);
 
+/* End-to-end entry: `host` describes the same tables in HOST memory (pinned for full PCIe speed;
+ * SX_STR offsets are host too).  Every non-empty column is copied into a library-allocated device
+ * buffer (stream-ordered H2D copies, no sync) and `dev` receives the device description, to be
+ * passed to sx_tpch_q* and released with sx_tpch_tables_free. */
+sx_status sx_tpch_upload(sx_ctx* ctx, const sx_tpch_tables* host, sx_tpch_tables* dev);
+void sx_tpch_tables_free(sx_ctx* ctx, sx_tpch_tables* dev);
+
 typedef struct { uint64_t lo; int64_t hi; } sx_i128;
 typedef struct {
   uint8_t returnflag, linestatus, pad[6];

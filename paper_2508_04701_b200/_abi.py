@@ -117,7 +117,8 @@ EXPORTS = ["sx_ctx_create", "sx_ctx_destroy", "sx_last_error", "sx_free", "sx_sy
            "sx_ht_destroy", "sx_sort_topk", "sx_gather", "sx_tpch_default_params", "sx_tpch_q1", "sx_tpch_q6",
            "sx_tpch_q3", "sx_tpch_q9", "sx_tpch_q18", "sx_groupby_merge", "sx_avg", "sx_dest_rank",
            "sx_partition_by_rank", "sx_comm_unique_id", "sx_comm_init", "sx_comm_destroy", "sx_comm_rank",
-           "sx_comm_size", "sx_shuffle", "sx_allgather", "sx_radix_of", "sx_radix_partition", "sx_hash_join"]
+           "sx_comm_size", "sx_shuffle", "sx_allgather", "sx_radix_of", "sx_radix_partition", "sx_hash_join",
+           "sx_tpch_upload", "sx_tpch_tables_free"]
 
 
 def load(path: str = LIB_PATH):
@@ -169,6 +170,9 @@ def load(path: str = LIB_PATH):
     L.sx_comm_size.argtypes = [vp]
     L.sx_shuffle.argtypes = [vp, vp, P(Col), i32, vp, i32, P(Sel), P(Col), P(C.c_int64)]
     L.sx_allgather.argtypes = [vp, vp, P(Col), i32, P(Col), P(C.c_int64)]
+    L.sx_tpch_upload.argtypes = [vp, P(TpchTables), P(TpchTables)]
+    L.sx_tpch_tables_free.argtypes = [vp, P(TpchTables)]
+    L.sx_tpch_tables_free.restype = None
     L.sx_radix_of.argtypes = [C.c_uint64, i32]
     L.sx_radix_of.restype = C.c_uint32
     L.sx_radix_partition.argtypes = [vp, P(Col), i32, vp, i32, P(Sel), i32, P(Col), P(Sel), vp]

@@ -1321,3 +1321,52 @@ SX_EXPORT sx_status sx_tpch_q18(sx_ctx* ctx, const sx_tpch_tables* t, const sx_t
   *nrows = perm.len;
   return SX_OK;
 }
+
+// ------------------------------------------------------------------------------- host upload
+namespace {
+constexpr int kTpchCols = (int)(sizeof(sx_tpch_tables) / sizeof(sx_col));
+}
+
+SX_EXPORT sx_status sx_tpch_upload(sx_ctx* ctx, const sx_tpch_tables* host, sx_tpch_tables* dev) {
+  if (!ctx || !host || !dev) return SX_EINVAL;
+  std::memset(dev, 0, sizeof *dev);
+  const sx_col* hc = (const sx_col*)host;
+  sx_col* dc = (sx_col*)dev;
+  for (int i = 0; i < kTpchCols; ++i) {
+    const sx_col& h = hc[i];
+    sx_col& d = dc[i];
+    d = h;
+    d.data = nullptr;
+    d.offsets = nullptr;
+    if (h.len <= 0 && h.type != SX_STR) continue;
+    size_t bytes;
+    if (h.type == SX_STR) {
+      if (!h.offsets) continue;
+      bytes = (size_t)h.offsets[h.len];  // host offsets
+      int64_t* doff;
+      sx_status st = alloc(ctx, &doff, (size_t)h.len + 1);
+      if (st != SX_OK) { sx_tpch_tables_free(ctx, dev); return st; }
+      d.offsets = doff;
+      SX_CUDA(cudaMemcpyAsync(doff, h.offsets, sizeof(int64_t) * (h.len + 1), cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+      bytes = (size_t)h.len * type_width(h.type);
+    }
+    char* buf;
+    sx_status st = alloc(ctx, &buf, bytes + 16);
+    if (st != SX_OK) { sx_tpch_tables_free(ctx, dev); return st; }
+    d.data = buf;
+    if (bytes) SX_CUDA(cudaMemcpyAsync(buf, h.data, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return SX_OK;
+}
+
+SX_EXPORT void sx_tpch_tables_free(sx_ctx* ctx, sx_tpch_tables* dev) {
+  if (!ctx || !dev) return;
+  sx_col* dc = (sx_col*)dev;
+  for (int i = 0; i < kTpchCols; ++i) {
+    if (dc[i].data) dfree(ctx, (void*)dc[i].data);
+    if (dc[i].type == SX_STR && dc[i].offsets) dfree(ctx, (void*)dc[i].offsets);
+    dc[i].data = nullptr;
+    dc[i].offsets = nullptr;
+  }
+}

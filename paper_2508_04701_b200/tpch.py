@@ -76,6 +76,22 @@ class Tpch:
             setattr(T, name, A.Col(typ, scale, x.shape[0], x.data_ptr() if x.numel() else None, None, None))
         self.T = T
 
+    @classmethod
+    def upload(cls, ctx, host_tables: dict) -> "Tpch":
+        """Tables in host memory (CPU torch tensors, pinned for full PCIe speed) -> device copies made
+        by the library (sx_tpch_upload: stream-ordered H2D inside the C ABI).  free() releases them."""
+        h = cls(ctx, host_tables)
+        dev = A.TpchTables()
+        ctx.check(ctx.L.sx_tpch_upload(ctx.h, C.byref(h.T), C.byref(dev)))
+        obj = cls.__new__(cls)
+        obj.ctx, obj.tables, obj.T, obj._owned = ctx, host_tables, dev, True
+        return obj
+
+    def free(self):
+        if getattr(self, "_owned", False):
+            self.ctx.L.sx_tpch_tables_free(self.ctx.h, C.byref(self.T))
+            self._owned = False
+
     def run(self, q: str, params: A.TpchParams | None = None) -> list:
         c = self.ctx
         P = params or default_params()

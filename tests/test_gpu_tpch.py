@@ -211,3 +211,18 @@ def test_queries_on_empty_tables(ctx, empty):
         want = oracle.run_query(q, host)
         got = T.run(q)
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
+
+
+def test_upload_from_host_tables(ctx):
+    """sx_tpch_upload: tables in (pinned) host memory copied by the library, then the five plans."""
+    host = gen.cpu_tables(10, seed=4)
+    pinned = {t: {c: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for c, a in cols.items()}
+              for t, cols in host.items()}
+    T = tpch.Tpch.upload(ctx, pinned)
+    try:
+        for q in QUERIES:
+            want = oracle.run_query(q, host)
+            got = T.run(q)
+            assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
+    finally:
+        T.free()

@@ -13,10 +13,10 @@ timeout 600 python bench.py --sf 10 --no-e2e --no-cpu > gpurun_out/bench_sf10.js
 timeout 600 python bench.py --sf 0.01 --steps 20 --warmup 5 --no-e2e --no-cpu > gpurun_out/bench_sf001.json 2> gpurun_out/bench_sf001.err
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/bench_ncu.log 2>&1
 RQ="python tools/run_query.py --sf 100 --reps 1"
-cap g_q1 k_gb_dense 0 1 $RQ --query q1
-cap g_q6 k_gb_dense 0 1 $RQ --query q6
-cap g_q9_pg k_gb_shared 0 1 $RQ --query q9
-cap g_q9_semi k_compact_dense 0 1 $RQ --query q9
-cap g_q3 k_compact 2 4 $RQ --query q3
-cap g_q18 k_runs_own_dense 0 1 $RQ --query q18
+cap h_q1 k_gb_dense 0 1 $RQ --query q1
+cap h_q6 k_gb_dense 0 1 $RQ --query q6
+cap h_q9_pg k_gb_shared 0 1 $RQ --query q9
+cap h_q9_semi k_compact_dense 0 1 $RQ --query q9
+cap h_q3 k_compact 2 4 $RQ --query q3
+cap h_q18 k_runs_own_dense 0 1 $RQ --query q18
 du -sh gpurun_out
