@@ -90,6 +90,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_compact_local(const __grid_consta
 // ITEMS consecutive rows, which the functor reads with 128-bit vector loads and returns as a bit
 // mask; survivors are ranked by a block scan of the per-thread counts and written (ascending) to
 // the tile's scratch region.  Same scratch layout and phases 2-3 as k_compact_local.
+// functors whose eval_dense is warp-cooperative: called by every lane, also past the end
+template <class F, class = void>
+struct warp_coop { static constexpr bool value = false; };
+template <class F>
+struct warp_coop<F, std::void_t<decltype(F::kWarpCoop)>> { static constexpr bool value = F::kWarpCoop; };
+
 template <class F, class = void>
 struct dense_blocks { static constexpr int value = 3; };
 template <class F>
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(kBlock, dense_blocks<F>::value) k_compact_dens
     int32_t aux[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) aux[i] = -1;
-    if (r0 < n) f.template eval_dense<ITEMS>(r0, n, mask, aux);
+    if (warp_coop<F>::value || r0 < n) f.template eval_dense<ITEMS>(r0, n, mask, aux);
     const int c = __popc(mask);
     int x = c;
 #pragma unroll

@@ -247,6 +247,77 @@ struct ContainsFn {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) alive[i] = valid[i] && contains(row[i]);
   }
+  // Dense (no input selection), warp-cooperative: the 32 x ITEMS consecutive strings of a warp
+  // occupy one contiguous byte span [offsets[wr0], offsets[wr1]), which the warp streams with
+  // coalesced 16-byte loads (lane l reads bytes 16l.. of each 512-byte step).  Bytes equal to the
+  // pattern's first byte are candidates; a candidate is verified byte by byte (L1/L2 hits) and,
+  // if the whole pattern lies inside one string, that string's row is found by binary search
+  // over the warp's offsets and its bit set in the owning thread's mask (shared memory).  Every
+  // lane of the warp must call this (k_compact_dense: warp_coop).
+  static constexpr int kDenseItems = 16;
+  static constexpr int kMinBlocks = 4;
+  static constexpr bool kWarpCoop = true;
+  template <int ITEMS>
+  __device__ __forceinline__ void eval_dense(int64_t r0, int64_t n, uint32_t& mask, int32_t (&)[ITEMS]) const {
+    __shared__ uint32_t s_hit[kBlock];
+    const int lane = threadIdx.x & 31;
+    const int64_t wr0 = r0 - (int64_t)lane * ITEMS;
+    mask = 0;
+    if (wr0 >= n) return;  // warp-uniform
+    const uint32_t valid = dense_valid<ITEMS>(r0, n);
+    if (plen == 0) {
+      mask = valid;
+      return;
+    }
+    const int64_t wr1 = wr0 + 32 * ITEMS < n ? wr0 + 32 * ITEMS : n;
+    s_hit[threadIdx.x] = 0;
+    const int64_t S = __ldg(offsets + wr0), E = __ldg(offsets + wr1);
+    __syncwarp();
+    const uint32_t p4 = 0x01010101u * pat[0];
+    // 16-byte aligned chunks of absolute addresses covering [S, E): a chunk that holds a byte of
+    // the span lies inside the chars allocation's mapped granularity
+    const uintptr_t a0 = ((uintptr_t)(chars + S)) & ~(uintptr_t)15;
+    const uintptr_t aE = (uintptr_t)(chars + E);
+    for (uintptr_t cb = a0; cb < aE; cb += 1024) {  // warp-uniform; two 512-byte steps per trip
+      uint4 v[2];
+      uint32_t cm[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uintptr_t p = cb + 512 * h + 16 * lane;
+        v[h] = p < aE ? __ldg((const uint4*)p) : make_uint4(0u, 0u, 0u, 0u);
+        cm[h] = p < aE ? ((__vcmpeq4(v[h].x, p4) & 0x01010101u) | ((__vcmpeq4(v[h].y, p4) & 0x01010101u) << 1) |
+                          ((__vcmpeq4(v[h].z, p4) & 0x01010101u) << 2) | ((__vcmpeq4(v[h].w, p4) & 0x01010101u) << 3))
+                       : 0u;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t c = cm[h];
+        while (c) {
+          // bit 8b + 4... encodes byte 4*word + b: bit (8*b + word) for word w, byte b
+          const int bit = __ffs(c) - 1;
+          c &= c - 1;
+          const int j = 4 * (bit & 3) + (bit >> 3);
+          const int64_t q = (int64_t)((const uint8_t*)(cb + 512 * h + 16 * lane) - chars) + j;
+          if (q < S || q + plen > E) continue;
+          bool ok = true;
+          for (int k = 1; k < plen && ok; ++k) ok = __ldg(chars + q + k) == pat[k];
+          if (!ok) continue;
+          int64_t lo = wr0, hi = wr1 - 1;  // last row whose string starts at or before q
+          while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(offsets + mid) <= q) lo = mid;
+            else hi = mid - 1;
+          }
+          if (q + plen <= __ldg(offsets + lo + 1)) {
+            const int rel = (int)(lo - wr0);
+            atomicOr(&s_hit[(threadIdx.x & ~31) + rel / ITEMS], 1u << (rel % ITEMS));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    mask = s_hit[threadIdx.x] & valid;
+  }
 };
 
 sx_status filter_internal(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_pred* conj, int npred,

@@ -898,6 +898,22 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
         else if (rs != SX_EUNSUPPORTED) return rs;
       }
     }
+    if constexpr (has_wscan<Prog>::value) {
+      // K10w: warp-compacted scan (selective streaming filter + lookup chain), hinted mid G
+      if (!dense_done && n > 0 && !sel && shared_cap && nsub == 1 && L.nst == 1 && prog.wscan_ok()) {
+        size_t smem = (size_t)(kBlock / 32) * 2 * (32 * 8 * Prog::kWChunks) * sizeof(int32_t) +
+                      (size_t)(shared_cap + 1) * L.slot_bytes;
+        SX_CUDA(cudaFuncSetAttribute(k_gb_wscan<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gb_wscan<Prog>, kBlock, smem));
+        if (per_sm < 1) per_sm = 1;
+        const int64_t windows = (n + 32 * 8 * Prog::kWChunks - 1) / (32 * 8 * Prog::kWChunks);
+        const unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm, (windows + kBlock / 32 - 1) / (kBlock / 32));
+        k_gb_wscan<Prog><<<grid, kBlock, smem, SX_STREAM(ctx)>>>(prog, n, L, t, shared_cap);
+        SX_CHECK_LAUNCH();
+        dense_done = true;
+      }
+    }
     if constexpr (has_dense_shared<Prog>::value) {
       // K10d: dense vector-loading program into a per-CTA shared table (hinted mid G)
       if (!dense_done && n > 0 && !sel && shared_cap && nsub == 1 && prog.dense_ok()) {

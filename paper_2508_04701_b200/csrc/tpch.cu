@@ -564,7 +564,81 @@ struct Q9FusedProg {
   static constexpr int kDenseNst = 1;
   static constexpr int kDenseRows = 8;
   static constexpr bool kDenseShared = true;
-  bool dense_ok() const { return pbm != nullptr; }  // K10d only for the dense lineitem scan
+  int wscan = 0;  // 1: K10w (warp-compacted scan) instead of K10d for the full lineitem scan
+  bool dense_ok() const { return pbm != nullptr && !wscan; }  // K10d only for the dense lineitem scan
+  // K10w interface: the streaming green-part test of 8 rows (returns the passing mask and the
+  // partkeys), then the rest of the program for U compacted rows with every load of one level
+  // issued together: five column gathers, then the supplier and orders direct arrays (bitmap word
+  // and value read speculatively, both inside the key range) and the partsupp table's first slot.
+  static constexpr int kWChunks = 2;
+  static constexpr int kWRows = 2;
+  bool wscan_ok() const { return pbm != nullptr && wscan; }
+  __device__ __forceinline__ uint32_t wscan_select(int64_t r0, int64_t n, int32_t (&pk)[8]) const {
+    dense_load32<8>(partkey, r0, n, r0 + 8 <= n, pk);
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const unsigned long long off = (unsigned long long)((long long)pk[i] - pbm_min);
+      const bool in = r0 + i < n && off < pbm_bits;
+      const uint32_t w = in ? __ldg(pbm + (off >> 5)) : 0u;
+      m |= (in && ((w >> (off & 31)) & 1u)) ? (1u << i) : 0u;
+    }
+    return m;
+  }
+  template <int U>
+  __device__ __forceinline__ void wscan_rows(const int32_t (&row)[U], const int32_t (&pk)[U], bool (&alive)[U],
+                                             uint64_t (&key)[U], int64_t (&v)[U], bool& ovf) const {
+    int32_t sk[U];
+    KT ok[U];
+    int64_t q[U], e[U], d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      sk[u] = alive[u] ? __ldg(suppkey + row[u]) : 0;
+      ok[u] = alive[u] ? __ldg(orderkey + row[u]) : (KT)0;
+      q[u] = alive[u] ? __ldg(qty + row[u]) : 0;
+      e[u] = alive[u] ? __ldg(ext + row[u]) : 0;
+      d[u] = alive[u] ? __ldg(disc + row[u]) : 0;
+    }
+    uint32_t sw[U], ow[U];
+    int32_t sv[U], ov[U];
+    ulonglong2 p0[U];
+    uint32_t h[U];
+    const ulonglong2* reg[U];
+    uint64_t pkey[U];
+    unsigned long long soff[U], ooff[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      soff[u] = (unsigned long long)((long long)sk[u] - sup_min);
+      ooff[u] = (unsigned long long)((long long)ok[u] - ord_min);
+      const bool si = alive[u] && sup_bm && soff[u] < sup_n, oi = alive[u] && ord_bm && ooff[u] < ord_n;
+      sw[u] = si ? __ldg(sup_bm + (soff[u] >> 5)) : 0u;
+      sv[u] = si ? __ldg(sup_val + soff[u]) : 0;
+      ow[u] = oi ? __ldg(ord_bm + (ooff[u] >> 5)) : 0u;
+      ov[u] = oi ? __ldg(ord_val + ooff[u]) : 0;
+      pkey[u] = ((uint64_t)(uint32_t)pk[u] << 32) | (uint32_t)sk[u];
+      reg[u] = ps + pt_region_base(pkey[u], ps_bits, ps_mask);
+      h[u] = (uint32_t)hash64(pkey[u]) & ps_mask;
+      p0[u] = alive[u] ? __ldg(reg[u] + h[u]) : make_ulonglong2(~0ull, 0ull);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      bool f = alive[u] && ((sw[u] >> (soff[u] & 31)) & 1u) && ((ow[u] >> (ooff[u] & 31)) & 1u);
+      int64_t cost = 0;
+      if (f) {
+        ulonglong2 s = p0[u];
+        uint32_t hh = h[u];
+        for (;;) {
+          if (s.x == ~0ull) { f = false; break; }
+          if (s.x == pkey[u]) { cost = (int64_t)s.y; break; }
+          hh = (hh + 1) & ps_mask;
+          s = __ldg(reg[u] + hh);
+        }
+      }
+      alive[u] = f;
+      key[u] = ((uint64_t)(uint32_t)sv[u] << 32) | (uint32_t)civil_year(ov[u]);
+      v[u] = f ? sub_ck(mul_ck(e[u], sub_ck(100, d[u], ovf), ovf), mul_ck(cost, q[u], ovf), ovf) : 0;
+    }
+  }
   template <int R>
   __device__ __forceinline__ void dense(int64_t r0, int64_t n, bool (&alive)[R], uint64_t (&key)[R],
                                         int64_t (&v)[R][kDenseNst], bool& fast) const {
@@ -965,14 +1039,16 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   // the fused plan needs exact key-range bitmaps (key ranges <= 2^30); SX_EUNSUPPORTED from it
   // (e.g. SF1000's 64-bit orderkey range) falls back to the operator-at-a-time plan
   auto fused = [&]() -> sx_status {
-    // gather (default): semi-join first, then gather the selected rows into the probe-chain
-    // group-by; SX_Q9_SCAN=dense: one streaming pass over every lineitem column with the
-    // green-part test inside (K10d; measured slower at SF100)
-    // default (gather): the probe-chain group-by gathers the green rows through the semi-join's
-    // selection; SX_Q9_SCAN=mat: the semi-join materialises the six columns densely first (one
-    // pure gather kernel) and the group-by streams them (measured 11.7 vs 11.4 ms at SF100)
+    // default (SX_Q9_SCAN=wscan): one pass over lineitem (K10w) streams l_partkey, tests the
+    // green-part bitmap, compacts the green rows per warp and runs the lookup chain on them with
+    // every lane busy; no semi-join pass, no selection vector (8.1 vs 11.6 ms for Q9 at SF100).
+    // SX_Q9_SCAN=gather: semi-join first, then the probe-chain group-by gathers the selected rows
+    // (K10); =mat: the semi-join materialises the six columns densely first (one pure gather
+    // kernel) and the group-by streams them; =dense: every lineitem column streamed with the
+    // lookups per thread (K10d, latency-bound: 46 ms).  DESIGN.md §6.
     const char* scan_env = getenv("SX_Q9_SCAN");
-    const bool dense_scan = scan_env && std::strcmp(scan_env, "dense") == 0;
+    const bool wscan = !scan_env || std::strcmp(scan_env, "wscan") == 0;
+    const bool dense_scan = wscan || (scan_env && std::strcmp(scan_env, "dense") == 0);
     const bool gather = !dense_scan;
     const bool mat = gather && scan_env && std::strcmp(scan_env, "mat") == 0;
     // lineitem rows with a green part (exact bitmap semi-join)
@@ -1101,6 +1177,7 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       pr.ord_n = ht_lo->bm_bits;
       pr.ord_val = o_date;
       pr.ovf_flag = ctx->d_flags;
+      pr.wscan = wscan ? 1 : 0;
     };
     if (okb4) {
       Q9FusedProg<int32_t, 4> pr;

@@ -430,11 +430,15 @@ def test_filter_int32_constants_beyond_int32(ctx, op):
         assert np.array_equal(sel.cpu().numpy(), want), (op, lo, hi)
 
 
+LONG = b"greenish-goldenrod-x"  # 20 bytes: verification reaches past one 16-byte chunk
+
+
 @pytest.mark.parametrize("maxlen", [40, 300])
 def test_filter_contains_edges(ctx, maxlen):
     """Warp-cooperative CONTAINS: empty strings, matches at the first / last byte, a pattern split
     across two neighbouring strings (must not match), warps whose byte span exceeds the shared
-    stage (maxlen 300: per-lane fallback), a ragged last warp, and the empty pattern."""
+    stage (maxlen 300), a ragged last warp, the empty pattern, a 20-byte pattern, and a chars buffer
+    that starts off a 16-byte boundary."""
     rng = np.random.default_rng(maxlen)
     n = 10_007
     strs = []
@@ -450,10 +454,18 @@ def test_filter_contains_edges(ctx, maxlen):
             s = s + b"gre"          # and the next string starts with "en": no match across the boundary
         elif r == 3:
             s = b"en" + s
+        elif r == 4 and L >= 30:
+            s = s[:3] + LONG + s[3 + len(LONG):]
         strs.append(s)
     offs = np.zeros(n + 1, np.int64)
     offs[1:] = np.cumsum([len(x) for x in strs])
     chars = np.frombuffer(b"".join(strs), np.uint8).copy()
-    for pat in (b"green", b"gre", b"", b"q"):
+    for pat in (b"green", b"gre", b"", b"q", LONG):
         sel, _ = ctx.filter([sx.col(dev(chars), A.SX_STR, offsets=dev(offs))], [(0, "contains", pat)])
+        assert np.array_equal(sel.cpu().numpy(), oracle.contains(offs, chars, pat)), pat
+    # a chars buffer that does not start on a 16-byte boundary
+    pad = torch.zeros(chars.size + 3, dtype=torch.uint8, device="cuda")
+    pad[3:] = dev(chars)
+    for pat in (b"green", LONG):
+        sel, _ = ctx.filter([sx.col(pad[3:], A.SX_STR, offsets=dev(offs))], [(0, "contains", pat)])
         assert np.array_equal(sel.cpu().numpy(), oracle.contains(offs, chars, pat)), pat

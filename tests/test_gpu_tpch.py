@@ -142,7 +142,8 @@ def test_q1_q6_dense_guard_and_tails(ctx, trunc):
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
 
 
-@pytest.mark.parametrize("plan", ["fused", "fused-mat", "fused-dense", "fused-partitioned", "ops"])
+@pytest.mark.parametrize("plan", ["fused", "fused-mat", "fused-dense", "fused-wscan", "fused-wscan-partitioned",
+                                  "fused-partitioned", "ops"])
 def test_q9_plans(small, monkeypatch, plan):
     """Q9 through the fused probe-chain group-by (default: gathering the semi-join's rows; or a dense
     scan; or with radix-partitioned PK tables) and the operator-at-a-time plan."""
@@ -151,9 +152,10 @@ def test_q9_plans(small, monkeypatch, plan):
         monkeypatch.setenv("SX_Q9_PLAN", "ops")
     else:
         monkeypatch.setenv("SX_Q9_PLAN", "fused")
-        monkeypatch.setenv("SX_Q9_SCAN", {"fused-dense": "dense", "fused-mat": "mat"}.get(plan, "gather"))
+        monkeypatch.setenv("SX_Q9_SCAN", {"fused-dense": "dense", "fused-mat": "mat", "fused-wscan": "wscan",
+                                          "fused-wscan-partitioned": "wscan"}.get(plan, "gather"))
         # PK payload tables built radix-partitioned region by region (forced at any size)
-        monkeypatch.setenv("SX_PT_PARTITION", "2" if plan == "fused-partitioned" else "1")
+        monkeypatch.setenv("SX_PT_PARTITION", "2" if plan.endswith("partitioned") else "1")
     for over in ({}, dict(q9_color="blue")):
         got = T.run("q9", tpch.default_params(**over))
         want = oracle.run_query("q9", host, oracle.default_params(**over))
