@@ -272,6 +272,12 @@ struct ContainsFn {
     const int64_t wr1 = wr0 + 32 * ITEMS < n ? wr0 + 32 * ITEMS : n;
     s_hit[threadIdx.x] = 0;
     const int64_t S = __ldg(offsets + wr0), E = __ldg(offsets + wr1);
+    // the warp's string offsets relative to S, staged once with coalesced loads (the row search
+    // of each match then runs in shared memory instead of chasing offsets lines in HBM)
+    __shared__ int32_t s_off[kBlock / 32][32 * ITEMS + 1];
+    int32_t* wo = s_off[threadIdx.x >> 5];
+    const int nr = (int)(wr1 - wr0);
+    for (int k = lane; k <= nr; k += 32) wo[k] = (int32_t)(__ldg(offsets + wr0 + k) - S);
     __syncwarp();
     const uint32_t p4 = 0x01010101u * pat[0];
     // 16-byte aligned chunks of absolute addresses covering [S, E): a chunk that holds a byte of
@@ -302,16 +308,14 @@ struct ContainsFn {
           bool ok = true;
           for (int k = 1; k < plen && ok; ++k) ok = __ldg(chars + q + k) == pat[k];
           if (!ok) continue;
-          int64_t lo = wr0, hi = wr1 - 1;  // last row whose string starts at or before q
+          const int32_t qr = (int32_t)(q - S);
+          int lo = 0, hi = nr - 1;  // last row whose string starts at or before q
           while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if (__ldg(offsets + mid) <= q) lo = mid;
+            const int mid = (lo + hi + 1) >> 1;
+            if (wo[mid] <= qr) lo = mid;
             else hi = mid - 1;
           }
-          if (q + plen <= __ldg(offsets + lo + 1)) {
-            const int rel = (int)(lo - wr0);
-            atomicOr(&s_hit[(threadIdx.x & ~31) + rel / ITEMS], 1u << (rel % ITEMS));
-          }
+          if (qr + plen <= wo[lo + 1]) atomicOr(&s_hit[(threadIdx.x & ~31) + lo / ITEMS], 1u << (lo % ITEMS));
         }
       }
     }

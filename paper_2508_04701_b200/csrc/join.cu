@@ -71,6 +71,56 @@ __global__ void __launch_bounds__(kBlock) k_build(const __grid_constant__ BuildA
   }
 }
 
+// Membership builds of a plain key column (no predicate, no selection): count and key range
+// only, with 16-byte streaming loads (k_build's per-row interpreted path is 3x slower here).
+template <typename KT>
+__global__ void __launch_bounds__(kBlock) k_minmax(const KT* __restrict__ p, int64_t n, unsigned long long* inserted,
+                                                   long long* kmin) {
+  constexpr int V = 16 / sizeof(KT);
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  const int64_t head = (int64_t)(((16 - ((uintptr_t)p & 15)) & 15) / sizeof(KT)) < n
+                           ? (int64_t)(((16 - ((uintptr_t)p & 15)) & 15) / sizeof(KT)) : n;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  if (((uintptr_t)p % sizeof(KT)) == 0) {
+    for (int64_t i = tid; i < head; i += nt) {
+      const long long v = (long long)__ldg(p + i);
+      mn = min(mn, v);
+      mx = max(mx, v);
+    }
+    const int64_t nv = (n - head) / V;
+    const KT* q = p + head;
+    for (int64_t j = tid; j < nv; j += nt) {
+      KT x[V];
+      *(int4*)x = __ldcs((const int4*)q + j);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        mn = min(mn, (long long)x[k]);
+        mx = max(mx, (long long)x[k]);
+      }
+    }
+    for (int64_t i = head + nv * V + tid; i < n; i += nt) {
+      const long long v = (long long)__ldg(p + i);
+      mn = min(mn, v);
+      mx = max(mx, v);
+    }
+  } else {
+    for (int64_t i = tid; i < n; i += nt) {
+      const long long v = (long long)p[i];
+      mn = min(mn, v);
+      mx = max(mx, v);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+    mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0 && mn <= mx) {
+    atomicMin(kmin, mn);
+    atomicMax(kmin + 1, mx);
+  }
+  if (tid == 0) atomicAdd(inserted, (unsigned long long)n);
+}
+
 // Exact key-range bitmap of the build keys (predicate transfer): bit (key - min).
 // Probes test it before touching the table, so misses cost one (L2-resident) word load.
 __global__ void __launch_bounds__(kBlock) k_bitmap_set(const __grid_constant__ BuildArgs a, uint32_t* bm,
@@ -337,7 +387,15 @@ SX_EXPORT sx_status sx_hash_build(sx_ctx* ctx, const sx_col* cols, int ncols, co
   a.mask = cap - 1;
   a.inserted = ins;
   a.kmin = (long long*)(ins + 1);
-  if (n > 0) k_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+  const bool plain = !a.slots && a.np == 0 && !a.sel && nkeys == 1 && !cols[key_cols[0]].validity;
+  if (n > 0 && plain && (types[0] == SX_I32 || types[0] == SX_DATE32))
+    k_minmax<int32_t><<<persistent_grid(ctx, 8, (n / 4 + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+        (const int32_t*)cols[key_cols[0]].data, n, ins, a.kmin);
+  else if (n > 0 && plain && types[0] == SX_I64)
+    k_minmax<long long><<<persistent_grid(ctx, 8, (n / 2 + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+        (const long long*)cols[key_cols[0]].data, n, ins, a.kmin);
+  else if (n > 0)
+    k_build<<<persistent_grid(ctx, 8, (n + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
   cudaError_t e = cudaGetLastError();
   int64_t stats[3] = {0, 0, 0};
   if (e == cudaSuccess) s = read_i64(ctx, ins, stats, 3);

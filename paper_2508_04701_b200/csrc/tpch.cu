@@ -449,22 +449,29 @@ __device__ __forceinline__ int32_t ht_find(const void* slots, uint32_t mask, uin
 // orderkey -> o_orderdate through unique-key tables (PK sides); key (nationkey, year(o_orderdate));
 // state 0 sum(ext*(100-disc) - supplycost*qty).  Rows whose lookups miss drop out (inner joins).
 // Several rows per thread (kSharedItems) so their independent lookups overlap.
+template <typename V>
 __device__ __forceinline__ bool direct_get(const uint32_t* __restrict__ bm, long long mn, unsigned long long nbits,
-                                           const int32_t* __restrict__ val, long long key, int64_t& out) {
+                                           const V* __restrict__ val, long long key, int64_t& out) {
   const unsigned long long off = (unsigned long long)(key - mn);
   if (!bm || off >= nbits || !((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u)) return false;
   out = __ldg(val + off);
   return true;
 }
 
-// val[key - min] = pay[r] for the rows whose key is in the bitmap (a PK side: one row per key)
-template <typename KT>
+// val[key - min] = pay[r] for the rows whose key is in the bitmap (a PK side: one row per key;
+// bm == nullptr: every key of the column is in range, the bitmap was built from this column).
+// A narrower value type V sets *bad for a value it cannot hold (the plan then falls back).
+template <typename KT, typename V>
 __global__ void k_direct_fill(const KT* __restrict__ keys, const int32_t* __restrict__ pay, int64_t n,
                               const uint32_t* __restrict__ bm, long long mn, unsigned long long nbits,
-                              int32_t* __restrict__ val) {
+                              V* __restrict__ val, long long* bad) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long off = (unsigned long long)((long long)__ldg(keys + r) - mn);
-    if (off < nbits && ((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u)) val[off] = __ldg(pay + r);
+    if (off < nbits && (!bm || ((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u))) {
+      const int32_t x = __ldg(pay + r);
+      if (sizeof(V) < 4 && (int32_t)(V)x != x) *bad = 1;
+      val[off] = (V)x;
+    }
   }
 }
 
@@ -488,7 +495,7 @@ struct Q9FusedProg {
   const uint32_t* ord_bm;
   long long ord_min;
   unsigned long long ord_n;
-  const int32_t* ord_val;
+  const int16_t* ord_val;  // o_orderdate as int16 days (the plan checks the range)
   int* ovf_flag;
   static constexpr int kMaxNst = 1;
   static constexpr int kUnrollStates = 1;
@@ -1096,9 +1103,9 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     bag.bufs.push_back(s_nat);
     if (t->s_suppkey.len > 0) {
       const int64_t ns = t->s_suppkey.len;
-      k_direct_fill<int32_t><<<persistent_grid(ctx, 8, (ns + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
-          (const int32_t*)t->s_suppkey.data, (const int32_t*)t->s_nationkey.data, ns, ht_s->bm, ht_s->bm_min,
-          ht_s->bm_bits, s_nat);
+      k_direct_fill<int32_t, int32_t><<<persistent_grid(ctx, 8, (ns + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+          (const int32_t*)t->s_suppkey.data, (const int32_t*)t->s_nationkey.data, ns, nullptr, ht_s->bm_min,
+          ht_s->bm_bits, s_nat, nullptr);
       SX_CHECK_LAUNCH();
     }
     // orders: the exact bitmap of the orderkeys that can be looked up (gather mode: the green
@@ -1114,25 +1121,37 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     bag.keep(ht_lo);
     if (!ht_lo->bm && (gather ? sel_l.len : t->o_orderkey.len) > 0)
       return set_err(ctx, SX_EUNSUPPORTED, "Q9: orderkey range too wide");
-    int32_t* o_date = nullptr;
+    // o_orderdate as int16 days since 1970 (1880..2059; half the bytes of the direct array and of
+    // its lookups); a date outside that range makes the fused plan step aside (SX_EUNSUPPORTED)
+    int16_t* o_date = nullptr;
+    long long* d_bad = nullptr;
     SX_TRY(alloc(ctx, &o_date, (size_t)(ht_lo->bm_bits > 0 ? ht_lo->bm_bits : 1)));
     bag.bufs.push_back(o_date);
+    SX_TRY(alloc(ctx, &d_bad, 1));
+    bag.bufs.push_back(d_bad);
+    SX_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(long long), ctx->stream));
     {
       ProfScope pb(ctx, "hash_build");
       const int64_t no = t->o_orderkey.len;
+      // gather: the bitmap holds the green lines' orderkeys (test it); otherwise it was built
+      // from o_orderkey itself and every key is in it
+      const uint32_t* fbm = gather ? ht_lo->bm : nullptr;
       if (no > 0 && ht_lo->bm) {
         if (okb4)
-          k_direct_fill<int32_t><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
-              (const int32_t*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, ht_lo->bm, ht_lo->bm_min,
-              ht_lo->bm_bits, o_date);
+          k_direct_fill<int32_t, int16_t><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+              (const int32_t*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, fbm, ht_lo->bm_min,
+              ht_lo->bm_bits, o_date, d_bad);
         else
-          k_direct_fill<long long><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
-              (const long long*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, ht_lo->bm,
-              ht_lo->bm_min, ht_lo->bm_bits, o_date);
+          k_direct_fill<long long, int16_t><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+              (const long long*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, fbm,
+              ht_lo->bm_min, ht_lo->bm_bits, o_date, d_bad);
         SX_CHECK_LAUNCH();
       }
       pb.set_bytes((type_width(t->o_orderkey.type) + 4.0) * no);
     }
+    int64_t bad = 0;
+    SX_TRY(read_i64(ctx, d_bad, &bad));
+    if (bad) return set_err(ctx, SX_EUNSUPPORTED, "Q9: o_orderdate outside the int16 day range");
     if (pt.t[0].kb != 8) return set_err(ctx, SX_EINVAL, "Q9: unexpected table layouts");
     ProfScope pg(ctx, "probe_groupby");
     sx_col tcols[6] = {t->s_nationkey, t->ps_supplycost, t->l_quantity, t->l_extendedprice, t->l_discount,

@@ -228,3 +228,19 @@ def test_upload_from_host_tables(ctx):
             assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
     finally:
         T.free()
+
+
+@pytest.mark.parametrize("scan", ["wscan", "gather"])
+def test_q9_wide_orderdates_fall_back(ctx, monkeypatch, scan):
+    """The fused Q9 keeps o_orderdate as int16 days (1880..2059): an order dated outside that range
+    (here year 2100 and 1850) makes it step aside to the operator-at-a-time plan, still exact."""
+    monkeypatch.setenv("SX_Q9_SCAN", scan)
+    host = gen.cpu_tables(10, seed=5)
+    od = host["orders"]["o_orderdate"].copy()
+    od[::97] += 47000   # ~2100
+    od[1::97] -= 44000  # ~1850
+    host["orders"]["o_orderdate"] = od
+    T = tpch.Tpch(ctx, to_dev(host))
+    want = oracle.run_query("q9", host)
+    got = T.run("q9")
+    assert rows_equal(got, want), diff_rows(got, want)
