@@ -10,6 +10,7 @@
 //                        ordered compaction of the k winners, bitonic sort of those
 //   otherwise          : LSD radix sort (per pass: tile histograms, per-digit scan, stable scatter)
 #include "compact.cuh"
+#include <cstring>
 
 using namespace sx;
 
@@ -130,6 +131,42 @@ __global__ void __launch_bounds__(1024) k_bitonic(const __grid_constant__ Words 
     int64_t p = sm[i * nw + (nw - 1)];  // position word
     out_perm[i] = sel ? sel[p] : (int32_t)p;
   }
+}
+
+// Top-k tournament round: CTA c sorts rows [2048c, 2048c + 2048) of `pos` (or of 0..m-1) in
+// shared memory and keeps its first min(k, len) positions at pos_out[k c ..].  The union of the
+// chunks' top-k holds the global top-k (keys are unique: the position word breaks ties), so
+// rounds shrink m by >= 2x (k <= 1024) until one k_bitonic finishes; no host synchronisation.
+__global__ void __launch_bounds__(1024) k_topk_round(const __grid_constant__ Words W, const int32_t* pos, int64_t m,
+                                                     int64_t k, int32_t* pos_out) {
+  extern __shared__ uint32_t sm[];  // [N][nwords]
+  const int nw = W.nwords;
+  const int64_t c0 = (int64_t)blockIdx.x * kBitonicMax;
+  const int len = (int)min((int64_t)kBitonicMax, m - c0);
+  int N = 1;
+  while (N < len) N <<= 1;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const int64_t p = i < len ? (pos ? (int64_t)pos[c0 + i] : c0 + i) : -1;
+    for (int j = 0; j < nw; ++j) sm[i * nw + j] = p >= 0 ? W.w[j][p] : 0xffffffffu;
+  }
+  __syncthreads();
+  uint32_t ta[kMaxWords], tb[kMaxWords];
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        for (int j = 0; j < nw; ++j) { ta[j] = sm[lo * nw + j]; tb[j] = sm[hi * nw + j]; }
+        const bool sw = up ? key_less(tb, ta, nw) : key_less(ta, tb, nw);
+        if (sw)
+          for (int j = 0; j < nw; ++j) { sm[lo * nw + j] = tb[j]; sm[hi * nw + j] = ta[j]; }
+      }
+      __syncthreads();
+    }
+  }
+  const int keep = (int)min(k, (int64_t)len);
+  for (int i = threadIdx.x; i < keep; i += blockDim.x) pos_out[blockIdx.x * k + i] = (int32_t)sm[i * nw + (nw - 1)];
 }
 
 // ---- radix select -------------------------------------------------------------------
@@ -382,6 +419,36 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
     size_t smem = (size_t)kBitonicMax * nwords * sizeof(uint32_t);
     SX_CUDA(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_bitonic<<<1, 1024, smem, SX_STREAM(ctx)>>>(W, nullptr, n, outn, sel, perm);
+    SX_CHECK_LAUNCH();
+    out_perm->len = outn;
+    out_perm->idx = perm;
+    scr.release(perm);
+    return SX_OK;
+  }
+  // top-k (k <= 1024) by tournament rounds of per-chunk shared-memory sorts (default; the radix
+  // select below stays behind SX_TOPK=select)
+  const bool topk_select = getenv("SX_TOPK") && std::strcmp(getenv("SX_TOPK"), "select") == 0;
+  if (!topk_select && outn <= 1024 && outn < n) {
+    const size_t smem = (size_t)kBitonicMax * nwords * sizeof(uint32_t);
+    SX_CUDA(cudaFuncSetAttribute(k_topk_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SX_CUDA(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int32_t *pa = nullptr, *pb = nullptr;
+    const int64_t c1 = (n + kBitonicMax - 1) / kBitonicMax;
+    SX_TRY(scr.get(&pa, (size_t)(c1 * outn)));
+    SX_TRY(scr.get(&pb, (size_t)(c1 * outn)));
+    const int32_t* cur = nullptr;  // nullptr: rows 0..m-1
+    int64_t m = n;
+    int32_t* dst = pa;
+    while (m > kBitonicMax) {
+      const int64_t chunks = (m + kBitonicMax - 1) / kBitonicMax;
+      k_topk_round<<<(unsigned)chunks, 1024, smem, SX_STREAM(ctx)>>>(W, cur, m, outn, dst);
+      SX_CHECK_LAUNCH();
+      const int64_t last = m - (chunks - 1) * kBitonicMax;
+      m = (chunks - 1) * outn + std::min<int64_t>(outn, last);
+      cur = dst;
+      dst = dst == pa ? pb : pa;
+    }
+    k_bitonic<<<1, 1024, smem, SX_STREAM(ctx)>>>(W, cur, m, outn, sel, perm);
     SX_CHECK_LAUNCH();
     out_perm->len = outn;
     out_perm->idx = perm;

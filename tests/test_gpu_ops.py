@@ -324,6 +324,22 @@ def test_sort_topk(ctx, n, k):
         assert np.array_equal(perm.cpu().numpy(), want), keys
 
 
+@pytest.mark.parametrize("mode", ["tournament", "select"])
+def test_topk_paths(ctx, monkeypatch, mode):
+    """Top-k (k <= 1024) through the tournament rounds (default) and the radix select
+    (SX_TOPK=select), several rounds deep (n = 3e5, k = 1024 -> 150 chunks -> ... -> one CTA)."""
+    if mode == "select":
+        monkeypatch.setenv("SX_TOPK", "select")
+    rng = np.random.default_rng(11)
+    n = 300_000
+    v = rng.integers(-50, 50, n).astype(np.int64)  # heavy ties: the position word decides
+    w = rng.integers(0, 3, n).astype(np.int32)
+    for k in (1, 7, 1000, 1024):
+        perm = ctx.sort_topk([c(dev(v)), sx.col(dev(w), A.SX_I32)], [(0, 1), (1, 0)], k)
+        want = oracle.sort([v.tolist(), w.tolist()], [1, 0], k)
+        assert np.array_equal(perm.cpu().numpy(), want), k
+
+
 def test_sort_with_sel(ctx):
     rng = np.random.default_rng(8)
     n = 20_000
