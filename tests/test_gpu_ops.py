@@ -328,8 +328,7 @@ def test_sort_topk(ctx, n, k):
 def test_topk_paths(ctx, monkeypatch, mode):
     """Top-k (k <= 1024) through the tournament rounds (default) and the radix select
     (SX_TOPK=select), several rounds deep (n = 3e5, k = 1024 -> 150 chunks -> ... -> one CTA)."""
-    if mode == "select":
-        monkeypatch.setenv("SX_TOPK", "select")
+    monkeypatch.setenv("SX_TOPK", mode)
     rng = np.random.default_rng(11)
     n = 300_000
     v = rng.integers(-50, 50, n).astype(np.int64)  # heavy ties: the position word decides
