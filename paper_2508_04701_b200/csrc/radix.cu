@@ -456,7 +456,8 @@ SX_EXPORT sx_status sx_hash_join(sx_ctx* ctx, const sx_col* build_cols, int nbui
   SX_TRY(to_dcols(ctx, build_cols, nbuild_cols, bdc));
   SX_TRY(to_dcols(ctx, probe_cols, nprobe_cols, pdc));
   // fan-out: per-partition tables of <= SX_PJ_PART_MB (default 32) MB (join µbench: 52.8 ms at
-  // 32 MB, 59.0 at 16, 57.7 at 64, 70.8 at 8; 4096-tuple runs per partition and tile are longer)
+  // 32 MB, 59.0 at 16, 57.7 at 64, 70.8 at 8: fewer partitions give longer runs per partition in
+  // each scatter tile, so fewer partial-sector writes)
   const int part_mb = getenv("SX_PJ_PART_MB") ? std::max(1, atoi(getenv("SX_PJ_PART_MB"))) : 32;
   int bits = 1;
   while (bits < kMaxPartBits && (flat_bytes >> bits) > ((uint64_t)part_mb << 20)) ++bits;
