@@ -476,22 +476,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_runs_own_dense(const __grid_const
           more = nx_len == R;
           r = nxt + R;
         } else {
-          // lane 31: the next 8 rows belong to another warp; read them in one vector load
-          // instead of row by row (one round trip instead of one per continuing row)
-          uint64_t k2[R];
-          int64_t v2[R];
-          prog.template runs_dense<R>(nxt, n, k2, v2);
-          const int m2 = (int)min((int64_t)R, n - nxt);
-          int i2 = 0;
-#pragma unroll
-          for (int i = 0; i < R; ++i) {
-            if (i2 == i && i < m2 && k2[i] == gk) {
-              runs_acc<P>(ST_SUM, v2[i], lo, hi);
-              ++i2;
-            }
-          }
-          more = i2 == R;
-          r = nxt + R;
+          more = true;
+          r = nxt;
         }
         int steps = 0;
         for (; more && r < n && steps < kRunAhead; ++r, ++steps) {  // rare: scalar continuation
