@@ -244,3 +244,19 @@ def test_q9_wide_orderdates_fall_back(ctx, monkeypatch, scan):
     want = oracle.run_query("q9", host)
     got = T.run("q9")
     assert rows_equal(got, want), diff_rows(got, want)
+
+
+@pytest.mark.parametrize("nl", [1, 7, 511, 512, 513, 1025, 4099])
+def test_q9_wscan_window_edges(ctx, monkeypatch, nl):
+    """K10w (the default Q9 lineitem pass) on lineitem prefixes around its 512-row warp window and
+    the 8-row lane chunk: a single row, a partial chunk, one window +- 1, several windows + tail.
+    SF 0.01 tables (at SF 0.001 the generator's partsupp (partkey, suppkey) pairs can repeat,
+    SURVEY App. A, and the PK payload table refuses them)."""
+    monkeypatch.setenv("SX_Q9_SCAN", "wscan")
+    host = gen.cpu_tables(10, seed=3)
+    host["lineitem"] = {c: np.ascontiguousarray(a[:nl]) for c, a in host["lineitem"].items()}
+    T = tpch.Tpch(ctx, to_dev(host))
+    for over in ({}, dict(q9_color="blue")):
+        want = oracle.run_query("q9", host, oracle.default_params(**over))
+        got = T.run("q9", tpch.default_params(**over))
+        assert rows_equal(got, want), diff_rows(got, want)
