@@ -458,6 +458,29 @@ __device__ __forceinline__ bool direct_get(const uint32_t* __restrict__ bm, long
   return true;
 }
 
+// "no order" in the sentinel-initialised int16 date array (memset 0x80): a real date equal to it
+// is refused by the fill (the plan then falls back)
+constexpr int16_t kNoDate = (int16_t)0x8080;
+
+// [min, max] of a key column (d_mm preset to {LLONG_MAX, LLONG_MIN})
+template <typename KT>
+__global__ void k_key_range(const KT* __restrict__ keys, int64_t n, long long* d_mm) {
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const long long k = (long long)__ldcs(keys + r);
+    mn = min(mn, k);
+    mx = max(mx, k);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0 && mn <= mx) {
+    atomicMin(d_mm, mn);
+    atomicMax(d_mm + 1, mx);
+  }
+}
+
 // val[key - min] = pay[r] for the rows whose key is in the bitmap (a PK side: one row per key;
 // bm == nullptr: every key of the column is in range, the bitmap was built from this column).
 // A narrower value type V sets *bad for a value it cannot hold (the plan then falls back).
@@ -469,7 +492,7 @@ __global__ void k_direct_fill(const KT* __restrict__ keys, const int32_t* __rest
     const unsigned long long off = (unsigned long long)((long long)__ldg(keys + r) - mn);
     if (off < nbits && (!bm || ((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u))) {
       const int32_t x = __ldg(pay + r);
-      if (sizeof(V) < 4 && (int32_t)(V)x != x) *bad = 1;
+      if (sizeof(V) < 4 && ((int32_t)(V)x != x || (V)x == (V)kNoDate)) *bad = 1;
       val[off] = (V)x;
     }
   }
@@ -501,6 +524,17 @@ struct Q9FusedProg {
   static constexpr int kUnrollStates = 1;
   static constexpr bool kSortedOK = false;
   static constexpr int kSharedItems = 4;
+  // orderkey -> o_orderdate: bitmap-guarded (ord_bm) or, without a bitmap, the sentinel-initialised
+  // array itself tells which keys exist
+  __device__ __forceinline__ bool ord_get(long long key, int64_t& out) const {
+    if (ord_bm) return direct_get(ord_bm, ord_min, ord_n, ord_val, key, out);
+    const unsigned long long off = (unsigned long long)(key - ord_min);
+    if (off >= ord_n) return false;
+    const int16_t v = __ldg(ord_val + off);
+    if (v == kNoDate) return false;
+    out = v;
+    return true;
+  }
   bool no_filter() const { return false; }
   template <int I>
   __device__ __forceinline__ void keys_only(const int32_t (&)[I], const bool (&)[I], uint64_t (&)[I]) const {}
@@ -552,7 +586,7 @@ struct Q9FusedProg {
       nk[i] = 0;
       d[i] = 0;
       if (f) f = direct_get(sup_bm, sup_min, sup_n, sup_val, (long long)sk[i], nk[i]);
-      if (f) f = direct_get(ord_bm, ord_min, ord_n, ord_val, (long long)ok[i], d[i]);
+      if (f) f = ord_get((long long)ok[i], d[i]);
       if (f) f = pt_find<8>(ps, ps_mask, ps_bits, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i], c.cost[i]);
       alive[i] = f;
       key[i] = ((uint64_t)(uint32_t)nk[i] << 32) | (uint32_t)civil_year((int32_t)d[i]);
@@ -617,11 +651,11 @@ struct Q9FusedProg {
     for (int u = 0; u < U; ++u) {
       soff[u] = (unsigned long long)((long long)sk[u] - sup_min);
       ooff[u] = (unsigned long long)((long long)ok[u] - ord_min);
-      const bool si = alive[u] && sup_bm && soff[u] < sup_n, oi = alive[u] && ord_bm && ooff[u] < ord_n;
+      const bool si = alive[u] && sup_bm && soff[u] < sup_n, oi = alive[u] && ooff[u] < ord_n;
       sw[u] = si ? __ldg(sup_bm + (soff[u] >> 5)) : 0u;
       sv[u] = si ? __ldg(sup_val + soff[u]) : 0;
-      ow[u] = oi ? __ldg(ord_bm + (ooff[u] >> 5)) : 0u;
-      ov[u] = oi ? __ldg(ord_val + ooff[u]) : 0;
+      ow[u] = (oi && ord_bm) ? __ldg(ord_bm + (ooff[u] >> 5)) : 0u;
+      ov[u] = oi ? __ldg(ord_val + ooff[u]) : kNoDate;
       pkey[u] = ((uint64_t)(uint32_t)pk[u] << 32) | (uint32_t)sk[u];
       reg[u] = ps + pt_region_base(pkey[u], ps_bits, ps_mask);
       h[u] = (uint32_t)hash64(pkey[u]) & ps_mask;
@@ -629,7 +663,8 @@ struct Q9FusedProg {
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      bool f = alive[u] && ((sw[u] >> (soff[u] & 31)) & 1u) && ((ow[u] >> (ooff[u] & 31)) & 1u);
+      const bool of = ord_bm ? ((ow[u] >> (ooff[u] & 31)) & 1u) != 0 : ov[u] != kNoDate;
+      bool f = alive[u] && ((sw[u] >> (soff[u] & 31)) & 1u) && of;
       int64_t cost = 0;
       if (f) {
         ulonglong2 s = p0[u];
@@ -671,7 +706,7 @@ struct Q9FusedProg {
       bool f = alive[i];
       int64_t cost = 0, nk = 0, dt = 0;
       if (f) f = direct_get(sup_bm, sup_min, sup_n, sup_val, sk[i], nk);
-      if (f) f = direct_get(ord_bm, ord_min, ord_n, ord_val, ok[i], dt);
+      if (f) f = ord_get((long long)ok[i], dt);
       if (f) f = pt_find<8>(ps, ps_mask, ps_bits, ((uint64_t)(uint32_t)pk[i] << 32) | (uint32_t)sk[i], cost);
       alive[i] = f;
       key[i] = ((uint64_t)(uint32_t)nk << 32) | (uint32_t)civil_year((int32_t)dt);
@@ -1112,39 +1147,66 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     // lines' keys, a semi-join reduction; dense mode: every orderkey), then o_orderdate scattered
     // into a direct array over that key range (one pass over orders, no hash table: each later
     // lookup is one bitmap word and one 4-byte read)
-    if (mat)
-      SX_TRY(sx_hash_build(ctx, &LM[2], 1, &k0, 1, nullptr, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
-    else if (gather)
-      SX_TRY(sx_hash_build(ctx, &t->l_orderkey, 1, &k0, 1, &sel_l, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
-    else
-      SX_TRY(sx_hash_build(ctx, &t->o_orderkey, 1, &k0, 1, nullptr, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
-    bag.keep(ht_lo);
-    if (!ht_lo->bm && (gather ? sel_l.len : t->o_orderkey.len) > 0)
-      return set_err(ctx, SX_EUNSUPPORTED, "Q9: orderkey range too wide");
+    const int64_t no = t->o_orderkey.len;
+    long long o_min = 0;
+    unsigned long long o_n = 0;
+    const uint32_t* o_bm = nullptr;
+    if (gather) {
+      if (mat)
+        SX_TRY(sx_hash_build(ctx, &LM[2], 1, &k0, 1, nullptr, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
+      else
+        SX_TRY(sx_hash_build(ctx, &t->l_orderkey, 1, &k0, 1, &sel_l, nullptr, 0, SX_BUILD_MEMBERSHIP, &ht_lo));
+      bag.keep(ht_lo);
+      if (!ht_lo->bm && sel_l.len > 0) return set_err(ctx, SX_EUNSUPPORTED, "Q9: orderkey range too wide");
+      o_min = ht_lo->bm_min;
+      o_n = ht_lo->bm ? ht_lo->bm_bits : 0;
+      o_bm = ht_lo->bm;
+    } else if (no > 0) {
+      // every order: the key range only (no bitmap); the date array starts as "no order"
+      ProfScope pb(ctx, "hash_build");
+      long long* d_mm = nullptr;
+      SX_TRY(alloc(ctx, &d_mm, 2));
+      bag.bufs.push_back(d_mm);
+      const long long init[2] = {LLONG_MAX, LLONG_MIN};
+      SX_CUDA(cudaMemcpyAsync(d_mm, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+      if (okb4)
+        k_key_range<int32_t><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+            (const int32_t*)t->o_orderkey.data, no, d_mm);
+      else
+        k_key_range<long long><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+            (const long long*)t->o_orderkey.data, no, d_mm);
+      SX_CHECK_LAUNCH();
+      int64_t mm[2] = {0, 0};
+      SX_TRY(read_i64(ctx, d_mm, mm, 2));
+      if (mm[1] < mm[0] || (unsigned long long)(mm[1] - mm[0]) + 1 > (1ull << 30))
+        return set_err(ctx, SX_EUNSUPPORTED, "Q9: orderkey range too wide");
+      o_min = mm[0];
+      o_n = (unsigned long long)(mm[1] - mm[0]) + 1;
+      pb.set_bytes((double)type_width(t->o_orderkey.type) * no);
+    }
     // o_orderdate as int16 days since 1970 (1880..2059; half the bytes of the direct array and of
-    // its lookups); a date outside that range makes the fused plan step aside (SX_EUNSUPPORTED)
+    // its lookups); a date outside that range (or equal to the "no order" sentinel) makes the
+    // fused plan step aside (SX_EUNSUPPORTED)
     int16_t* o_date = nullptr;
     long long* d_bad = nullptr;
-    SX_TRY(alloc(ctx, &o_date, (size_t)(ht_lo->bm_bits > 0 ? ht_lo->bm_bits : 1)));
+    SX_TRY(alloc(ctx, &o_date, (size_t)(o_n > 0 ? o_n : 1)));
     bag.bufs.push_back(o_date);
     SX_TRY(alloc(ctx, &d_bad, 1));
     bag.bufs.push_back(d_bad);
     SX_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(long long), ctx->stream));
     {
       ProfScope pb(ctx, "hash_build");
-      const int64_t no = t->o_orderkey.len;
-      // gather: the bitmap holds the green lines' orderkeys (test it); otherwise it was built
-      // from o_orderkey itself and every key is in it
-      const uint32_t* fbm = gather ? ht_lo->bm : nullptr;
-      if (no > 0 && ht_lo->bm) {
+      if (!gather && o_n > 0) SX_CUDA(cudaMemsetAsync(o_date, 0x80, o_n * sizeof(int16_t), ctx->stream));
+      // gather: only the green lines' orderkeys (test the bitmap); otherwise every order
+      if (no > 0 && o_n > 0) {
         if (okb4)
           k_direct_fill<int32_t, int16_t><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
-              (const int32_t*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, fbm, ht_lo->bm_min,
-              ht_lo->bm_bits, o_date, d_bad);
+              (const int32_t*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, o_bm, o_min, o_n, o_date,
+              d_bad);
         else
           k_direct_fill<long long, int16_t><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
-              (const long long*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, fbm,
-              ht_lo->bm_min, ht_lo->bm_bits, o_date, d_bad);
+              (const long long*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, o_bm, o_min, o_n,
+              o_date, d_bad);
         SX_CHECK_LAUNCH();
       }
       pb.set_bytes((type_width(t->o_orderkey.type) + 4.0) * no);
@@ -1191,9 +1253,9 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       pr.sup_min = ht_s->bm_min;
       pr.sup_n = ht_s->bm_bits;
       pr.sup_val = s_nat;
-      pr.ord_bm = ht_lo->bm;
-      pr.ord_min = ht_lo->bm_min;
-      pr.ord_n = ht_lo->bm_bits;
+      pr.ord_bm = o_bm;
+      pr.ord_min = o_min;
+      pr.ord_n = o_n;
       pr.ord_val = o_date;
       pr.ovf_flag = ctx->d_flags;
       pr.wscan = wscan ? 1 : 0;
