@@ -52,6 +52,14 @@ def col(t, type: int | None = None, scale: int = 0, offsets=None) -> A.Col:
     if type is None:
         type = _DTYPE_TYPE[str(t.dtype)]
     n = t.shape[0] if type != A.SX_STR else offsets.shape[0] - 1
+    # sx.h: buffers are dense and 16-byte aligned (the kernels load 16 bytes at a time); a strided or
+    # offset view would be misread or fault, so it is rejected here rather than copied silently
+    for x in (t, offsets):
+        if x is not None and x.numel():
+            if not x.is_contiguous():
+                raise SxError(A.SX_EINVAL, "column tensor is not contiguous (pass .contiguous())")
+            if x.data_ptr() % (16 if x is t else 8):
+                raise SxError(A.SX_EINVAL, f"column tensor at {x.data_ptr():#x} is not 16-byte aligned (pass .clone())")
     c = A.Col(type, scale, n, t.data_ptr() if t.numel() else None,
               offsets.data_ptr() if offsets is not None else None, None)
     c._keep = (t, offsets)  # the struct borrows the tensors' memory: keep them alive with it

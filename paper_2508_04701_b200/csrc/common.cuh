@@ -355,11 +355,23 @@ inline unsigned persistent_grid(sx_ctx* ctx, int blocks_per_sm, int64_t work_til
   return (unsigned)(g < 1 ? 1 : g);
 }
 
+// The ABI's alignment rule (sx.h "Conventions"): the dense kernels load 16 bytes at a time
+// (Q1/Q6 programs, K10w, unselected compaction), so a misaligned buffer would fault (a sticky
+// error that kills the context) and a strided view would be misread: reject both up front.
+inline sx_status check_aligned(sx_ctx* ctx, const sx_col& c, int i) {
+  if (c.len > 0 && ((uintptr_t)c.data & 15u))
+    return set_err(ctx, SX_EINVAL, "column %d data %p is not 16-byte aligned", i, c.data);
+  if (c.type == SX_STR && c.offsets && ((uintptr_t)c.offsets & 7u))
+    return set_err(ctx, SX_EINVAL, "column %d offsets %p are not 8-byte aligned", i, (const void*)c.offsets);
+  return SX_OK;
+}
+
 // Validate a column array for device kernels; fills DCol[].
 inline sx_status to_dcols(sx_ctx* ctx, const sx_col* cols, int ncols, DCol* out) {
   if (ncols < 0 || ncols > SX_MAX_COLS) return set_err(ctx, SX_EINVAL, "ncols %d out of range", ncols);
   if (ncols > 0 && !cols) return set_err(ctx, SX_EINVAL, "cols is NULL");
   for (int i = 0; i < ncols; ++i) {
+    SX_TRY(check_aligned(ctx, cols[i], i));
     if (cols[i].validity) return set_err(ctx, SX_EUNSUPPORTED, "column %d has a validity bitmap (null-free v1)", i);
     if (cols[i].len > 0 && !cols[i].data) return set_err(ctx, SX_EINVAL, "column %d data is NULL", i);
     if (cols[i].len > INT32_MAX) return set_err(ctx, SX_EINDEX, "column %d has %lld rows > INT32_MAX", i, (long long)cols[i].len);

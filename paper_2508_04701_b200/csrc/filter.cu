@@ -27,6 +27,7 @@ sx_status filter_internal(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_p
   for (int i = 0; i < ncols; ++i) {
     if (cols[i].validity) return set_err(ctx, SX_EUNSUPPORTED, "column %d has a validity bitmap (null-free v1)", i);
     if (cols[i].len > INT32_MAX) return set_err(ctx, SX_EINDEX, "column %d has more than INT32_MAX rows", i);
+    SX_TRY(check_aligned(ctx, cols[i], i));
   }
   if (ncols > SX_MAX_COLS) return set_err(ctx, SX_EINVAL, "too many columns");
   for (int i = 0; i < ncols; ++i) dc[i] = DCol{cols[i].data, cols[i].type, 0};

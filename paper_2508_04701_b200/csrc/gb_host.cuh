@@ -676,6 +676,8 @@ template <class Prog>
 sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* sel, int64_t n,
                  int64_t groups_hint, sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups,
                  int force_small = -1) {
+  // row ids are int32 everywhere below (K10w compacts them, sel entries are int32): P:271
+  if (n > INT32_MAX) return set_err(ctx, SX_EINDEX, "group-by over %lld rows > INT32_MAX", (long long)n);
   Scratch scr(ctx);
   const Layout& L = P.L;
   bool keyless = P.nkeys == 0;

@@ -9,7 +9,8 @@ pipeline of sx_* operators plus exchange operators:
   supplier (Q9), Q18 candidates — and the partial aggregates / local top-k rows that every rank
   merges (sx_groupby_merge, sx_sort_topk);
 * shuffle (sx_shuffle, NCCL all-to-all): re-partitions orders and lineitem on hash(orderkey) when
-  they are not co-partitioned (Q3 with ``co_located=False``, the Doris plan of P:458).
+  they are not co-partitioned (``co_located=False``: Q3 — the Doris plan of P:458 — Q9's orders
+  join and Q18's group-by / orders join).
 
 Communicators: ``NcclComm`` (one process per GPU, libsx's NCCL exchange) and ``LoopbackComm``
 (g logical ranks inside one process on one GPU; the exchange is device-to-device copies) — the
@@ -291,9 +292,8 @@ class ShardedTpch:
         psall = self.comm.allgather(pss)
         supp = self.comm.allgather([[typed(t["supplier"]["s_suppkey"], A.SX_I32),
                                      typed(t["supplier"]["s_nationkey"], A.SX_I32)] for t in self.shards])
-        parts = []
+        l4s = []
         for r, t in zip(self.R, self.shards):
-            o = t["orders"]
             okt = l2s[r][2][1]
             ps_cols = [sxcol(x) for x in psall[r]]
             ht = c.hash_build(ps_cols, [0, 1], unique=True)
@@ -306,11 +306,19 @@ class ShardedTpch:
                    mkcol(l3[4], A.SX_DEC64), mkcol(l3[5], A.SX_DEC64)]
             _, _, l4 = c.hash_probe(ht, l3c, [1], "inner", build_cols=s_cols, bp=[1], pp=[0, 2, 3, 4, 5])
             ht.close()
-            l4c = [mkcol(l4[0], A.SX_I32), mkcol(l4[1], A.SX_DEC64), mkcol(l4[2], okt), mkcol(l4[3], A.SX_DEC64),
-                   mkcol(l4[4], A.SX_DEC64), mkcol(l4[5], A.SX_DEC64)]
+            l4s.append([typed(l4[0], A.SX_I32), typed(l4[1], A.SX_DEC64), typed(l4[2], okt), typed(l4[3], A.SX_DEC64),
+                        typed(l4[4], A.SX_DEC64), typed(l4[5], A.SX_DEC64)])
+        ords = [[typed(t["orders"]["o_orderkey"], _okt(t["orders"]["o_orderkey"])),
+                 typed(t["orders"]["o_orderdate"], A.SX_DATE32)] for t in self.shards]
+        if not self.co_located:  # the orders join needs both sides on the owner rank of orderkey
+            l4s = self.comm.shuffle(l4s, [2])
+            ords = self.comm.shuffle(ords, [0])
+        parts = []
+        for r in self.R:
+            l4c = [sxcol(x) for x in l4s[r]]
             ht = c.hash_build(l4c, [2])
-            _, _, l5 = c.hash_probe(ht, [mkcol(o["o_orderkey"], okt), mkcol(o["o_orderdate"], A.SX_DATE32)], [0],
-                                    "inner", build_cols=l4c, bp=[0, 1, 3, 4, 5], pp=[1])
+            _, _, l5 = c.hash_probe(ht, [sxcol(x) for x in ords[r]], [0], "inner", build_cols=l4c,
+                                    bp=[0, 1, 3, 4, 5], pp=[1])
             ht.close()
             gcols = [mkcol(l5[0], A.SX_I32), mkcol(l5[1], A.SX_DEC64), mkcol(l5[2], A.SX_DEC64),
                      mkcol(l5[3], A.SX_DEC64), mkcol(l5[4], A.SX_DEC64), mkcol(l5[5], A.SX_DATE32)]
@@ -335,18 +343,26 @@ class ShardedTpch:
     def q18(self, p=None):
         P = p or default_params()
         c = self.ctx
-        cands = []
+        lis, ords = [], []
         for t in self.shards:
             li, o = t["lineitem"], t["orders"]
             okt = _okt(o["o_orderkey"])
-            k, a, _ = c.groupby([mkcol(li["l_orderkey"], okt), mkcol(li["l_quantity"], A.SX_DEC64)], [(0, "id")],
+            lis.append([typed(li["l_orderkey"], okt), typed(li["l_quantity"], A.SX_DEC64)])
+            ords.append([typed(o["o_orderkey"], okt), typed(o["o_custkey"], A.SX_I32),
+                         typed(o["o_orderdate"], A.SX_DATE32), typed(o["o_totalprice"], A.SX_DEC64)])
+        if not self.co_located:  # the group-by and the orders join are complete per orderkey owner
+            lis = self.comm.shuffle(lis, [0])
+            ords = self.comm.shuffle(ords, [0])
+        cands = []
+        for r in self.R:
+            okt = ords[r][0][1]
+            k, a, _ = c.groupby([sxcol(x) for x in lis[r]], [(0, "id")],
                                 [("sum", [(1, [(1, 1, 0)])])], having=(0, "gt", P.q18_qty_gt),
-                                groups_hint=o["o_orderkey"].shape[0])
+                                groups_hint=max(1, ords[r][0][0].shape[0]))
             bcols = [mkcol(k[0], okt), mkcol(a[0], A.SX_I128)]
             ht = c.hash_build(bcols, [0], unique=True)
-            _, _, cc = c.hash_probe(ht, [mkcol(o["o_orderkey"], okt), mkcol(o["o_custkey"], A.SX_I32),
-                                         mkcol(o["o_orderdate"], A.SX_DATE32), mkcol(o["o_totalprice"], A.SX_DEC64)],
-                                    [0], "inner", build_cols=bcols, bp=[1], pp=[0, 1, 2, 3])
+            _, _, cc = c.hash_probe(ht, [sxcol(x) for x in ords[r]], [0], "inner", build_cols=bcols, bp=[1],
+                                    pp=[0, 1, 2, 3])
             ht.close()
             cands.append([typed(cc[0], A.SX_I128), typed(cc[1], okt), typed(cc[2], A.SX_I32),
                           typed(cc[3], A.SX_DATE32), typed(cc[4], A.SX_DEC64)])

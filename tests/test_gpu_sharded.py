@@ -42,20 +42,37 @@ def test_loopback_sharded_queries(ctx, oracle_answers, g):
 
 
 @pytest.mark.parametrize("g", [2, 4])
-def test_loopback_q3_with_shuffle(ctx, oracle_answers, g):
+@pytest.mark.parametrize("q", ["q3", "q9", "q18"])
+def test_loopback_with_shuffle(ctx, oracle_answers, g, q):
+    """co_located=False: every orderkey join / group-by goes through sx_partition_by_rank (the
+    shuffle's one-pass partition) before it runs, as on a cluster without co-partitioned tables."""
     shards = [gen.gpu_tables(100, seed=42, shard=(r, g)) for r in range(g)]
     st = ShardedTpch(ctx, LoopbackComm(ctx, g), shards, co_located=False)
-    got = st.run("q3")
-    assert rows_equal(got, oracle_answers["q3"]), diff_rows(got, oracle_answers["q3"])
+    got = st.run(q)
+    assert rows_equal(got, oracle_answers[q]), diff_rows(got, oracle_answers[q])
 
 
-def test_partition_by_rank_contract(ctx):
-    rng = np.random.default_rng(3)
-    n, g = 100_003, 5
+@pytest.mark.parametrize("n,g,with_sel", [(100_003, 5, False), (1, 3, False), (0, 2, False), (4096, 64, False),
+                                          (70_001, 8, True), (2047, 1, False)])
+def test_partition_by_rank_contract(ctx, n, g, with_sel):
+    """One pass (histogram, scan, stable scatter) over ragged tiles: counts = host histogram of
+    sx_dest_rank, and every destination segment keeps input order (bit-exact)."""
+    rng = np.random.default_rng(3 + n)
     k = rng.integers(-(2**40), 2**40, n).astype(np.int64)
     v = np.arange(n, dtype=np.int32)
-    parts, counts = ctx.partition_by_rank([sx.col(torch.from_numpy(k).cuda()), sx.col(torch.from_numpy(v).cuda())],
-                                          [0], g)
+    sel = None
+    if with_sel:
+        idx = np.sort(rng.choice(n, n // 3, replace=False)).astype(np.int32)
+        sel = torch.from_numpy(idx).cuda()
+        k, v = k[idx], v[idx]
+        kk = np.zeros(n, np.int64)
+        kk[idx] = k
+        vv = np.zeros(n, np.int32)
+        vv[idx] = v
+        dev = [sx.col(torch.from_numpy(kk).cuda()), sx.col(torch.from_numpy(vv).cuda())]
+    else:
+        dev = [sx.col(torch.from_numpy(k).cuda()), sx.col(torch.from_numpy(v).cuda())]
+    parts, counts = ctx.partition_by_rank(dev, [0], g, in_sel=sel)
     dest = np.array([sx.lib().sx_dest_rank(int(x) & ((1 << 64) - 1), g) for x in k])
     assert counts == [int((dest == d).sum()) for d in range(g)]
     pk, pv = parts[0].cpu().numpy(), parts[1].cpu().numpy()
