@@ -15,7 +15,8 @@
  *  - Data pointers in sx_col / sx_sel are DEVICE pointers (current ctx device)
  *    unless a comment says "host".  Layouts are Arrow little-endian; column
  *    buffers must be dense and 16-byte aligned (cudaMalloc / torch allocations
- *    are; string offsets 8-byte aligned): a misaligned buffer -> SX_EINVAL.
+ *    are; string offsets 8-byte aligned, string bytes unconstrained): a
+ *    misaligned buffer -> SX_EINVAL.
  *  - Inputs are borrowed for the duration of the call.  Outputs (selection
  *    vectors, output columns) are allocated by the library from its
  *    stream-ordered pool and released with sx_free(); hash tables with

@@ -58,7 +58,7 @@ def col(t, type: int | None = None, scale: int = 0, offsets=None) -> A.Col:
         if x is not None and x.numel():
             if not x.is_contiguous():
                 raise SxError(A.SX_EINVAL, "column tensor is not contiguous (pass .contiguous())")
-            if x.data_ptr() % (16 if x is t else 8):
+            if x.data_ptr() % (8 if x is offsets else (1 if type == A.SX_STR else 16)):
                 raise SxError(A.SX_EINVAL, f"column tensor at {x.data_ptr():#x} is not 16-byte aligned (pass .clone())")
     c = A.Col(type, scale, n, t.data_ptr() if t.numel() else None,
               offsets.data_ptr() if offsets is not None else None, None)

@@ -359,7 +359,8 @@ inline unsigned persistent_grid(sx_ctx* ctx, int blocks_per_sm, int64_t work_til
 // (Q1/Q6 programs, K10w, unselected compaction), so a misaligned buffer would fault (a sticky
 // error that kills the context) and a strided view would be misread: reject both up front.
 inline sx_status check_aligned(sx_ctx* ctx, const sx_col& c, int i) {
-  if (c.len > 0 && ((uintptr_t)c.data & 15u))
+  // (string bytes may start anywhere: the CONTAINS scan aligns its own windows)
+  if (c.len > 0 && c.type != SX_STR && ((uintptr_t)c.data & 15u))
     return set_err(ctx, SX_EINVAL, "column %d data %p is not 16-byte aligned", i, c.data);
   if (c.type == SX_STR && c.offsets && ((uintptr_t)c.offsets & 7u))
     return set_err(ctx, SX_EINVAL, "column %d offsets %p are not 8-byte aligned", i, (const void*)c.offsets);

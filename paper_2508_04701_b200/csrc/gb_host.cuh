@@ -8,6 +8,7 @@
 #include "compact.cuh"
 #include "groupby.cuh"
 #include "radix.cuh"
+#include "ring.cuh"
 
 namespace sx {
 
@@ -826,7 +827,9 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       }
     }
   }
+  bool ring_retry = false;  // K9r's per-CTA list of exact-path rows overflowed: redo with K9d
   for (int attempt = 0; !sorted_done; ++attempt) {
+    bool ring_used = false;
     // partition when the table would not stay L2-resident
     int pbits = 0;
     // (opt-in until phase A beats the single HBM table: SX_GB_PARTITION=1)
@@ -856,7 +859,19 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       // thread at <= 2^21 rows so that its int64 partial sums of |v| < 2^41 values cannot overflow
       if (n > 0 && small && !sel && L.nst == Prog::kDenseNst) {
         bool staged = false;
-        if constexpr (has_bulk<Prog>::value) {
+        if constexpr (has_ring<Prog>::value) {
+          // K9r (ring.cuh): producer warp + bulk-copy tile ring, one CTA per SM; every column base
+          // is 16-B aligned (to_dcols) and a tile's column chunks are multiples of 16 B.  SX_RING=0: K9d.
+          static const bool ring_off = getenv("SX_RING") && getenv("SX_RING")[0] == '0';
+          if (!ring_off && !ring_retry && n >= (int64_t)Prog::kRingTile * ctx->num_sms) {
+            const size_t smem = (size_t)Prog::kRingStages * ring_stage_bytes<Prog>();
+            SX_CUDA(cudaFuncSetAttribute(k_gb_ring<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_gb_ring<Prog><<<(unsigned)ctx->num_sms, (Prog::kRingConsumers + 1) * 32, smem, SX_STREAM(ctx)>>>(prog, n, L, t);
+            SX_CHECK_LAUNCH();
+            staged = dense_done = ring_used = true;
+          }
+        }
+        if constexpr (has_bulk<Prog>::value) if (!staged) {
           // K9s: bulk-staged (cp.async.bulk) tiles, one CTA per SM, when every column base is 16-B aligned
           // opt-in (SX_BULK=1): measured slower than K9d on Q1 at SF100 (6.1 vs 4.3 ms) — one 8-warp CTA
           // per SM cannot hide the shared-memory latency of the per-row aggregation (profiles/)
@@ -1048,6 +1063,13 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
     scr.ptrs.push_back(ids);
     SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
     if (flags[0]) return set_err(ctx, SX_EOVERFLOW, "a value expression left int64");
+    if (ring_used && flags[3]) {
+      if (attempt >= 2) return set_err(ctx, SX_ENOMEM, "ring aggregation retry failed");
+      dfree(ctx, table); scr.release(table);
+      dfree(ctx, ids); scr.release(ids);
+      ring_retry = true;
+      continue;
+    }
     if (!flags[1]) break;
     // table full: the hint was too small; retry at an upper bound (G <= n)
     if (attempt >= 2) return set_err(ctx, SX_ENOMEM, "aggregation table full after resizing");

@@ -191,6 +191,146 @@ struct Q1Prog {
     for (int i = 0; i < 4; ++i) alive[i] = true;
     compute<4>(sd, f, s, q, e, d, x, alive, key, v, fast);
   }
+  // Ring interface (K9r, ring.cuh): 1024-row tiles of the 7 columns (38.9 KB per stage), 5 stages,
+  // 16 consumer warps taking 2 consecutive rows per lane.  Per-thread exact accumulators in
+  // registers for the 6 (returnflag, linestatus) combinations {A,N,R} x {F,O}, 4 per group:
+  //   pk = sum(qty) | sum(disc) << 24 | count << 39  (packed), sum(ext), sum(dp), sum(charge).
+  // Fast-path guard per row: 0 <= qty < 2^13, 0 <= ext < 2^24, 0 <= disc, tax < 2^4.  Then dp =
+  // ext*(100-disc) < 2^31 and charge = dp*(100+tax) < 2^38 are exact 32x32->64 products, and over
+  // kRingFlush = 2048 rows per thread the packed fields (< 2^24, 2^15, 2^12) and the other sums
+  // (< 2^35, 2^42, 2^49) cannot overflow; every 2048 rows a warp-collective flush adds them into a
+  // per-CTA shared state (96-bit sums), merged into the global table once per CTA.  A row failing
+  // the guard, or with another flag value, takes the exact per-row path (gb_dense_slow_row).
+  static constexpr int kRingCols = 7;
+  static constexpr int kRingTile = 1024;
+  static constexpr int kRingStages = 5;
+  static constexpr int kRingConsumers = 16;
+  static constexpr int kRingLane = kRingTile / (kRingConsumers * 32);
+  static constexpr int kRingFlush = 2048;
+  static_assert(kRingLane == 2, "ring_consume reads 2 rows per lane");
+  __host__ __device__ static constexpr int ring_width(int c) { return bulk_width(c); }
+  __host__ __device__ const void* ring_col(int c) const { return bulk_col(c); }
+  struct RingAcc {
+    unsigned long long a[6][4];
+    int since;
+  };
+  static constexpr int kRingSlowCap = 2048;  // rows per CTA for the exact path (else the host reruns K9d)
+  struct RingShared {
+    unsigned long long lo[6][6];
+    int hi[6][6];
+    int nslow;
+    int32_t slow[kRingSlowCap];
+  };
+  __device__ __forceinline__ void ring_init(RingAcc& acc) const {
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc.a[k][j] = 0;
+    acc.since = 0;
+  }
+  __device__ __forceinline__ void ring_shared_init(RingShared& sh, int tid, int nt) const {
+    for (int j = tid; j < 36; j += nt) {
+      sh.lo[j / 6][j % 6] = 0;
+      sh.hi[j / 6][j % 6] = 0;
+    }
+    if (tid == 0) sh.nslow = 0;
+  }
+  __device__ __forceinline__ void ring_row(int32_t sd, uint32_t f, uint32_t s, long long q, long long e, long long d,
+                                           long long x, int64_t row, RingAcc& acc, RingShared& sh) const {
+    if (sd > ship_max) return;
+    const int fi = f == 'A' ? 0 : (f == 'N' ? 1 : (f == 'R' ? 2 : 3));
+    const int si = s == 'F' ? 0 : (s == 'O' ? 1 : 2);
+    const unsigned long long g = ((unsigned long long)q >> 13) | ((unsigned long long)e >> 24) |
+                                 ((unsigned long long)d >> 4) | ((unsigned long long)x >> 4);
+    if (fi == 3 || si == 2 || g != 0) {  // exact path after the stream (no call in the hot loop)
+      const int pos = atomicAdd(&sh.nslow, 1);
+      if (pos < kRingSlowCap) sh.slow[pos] = (int32_t)row;
+      else atomicExch(ovf_flag + 3, 1);
+      return;
+    }
+    const int slot = fi * 2 + si;
+    const uint32_t qq = (uint32_t)q, ee = (uint32_t)e, dd = (uint32_t)d, xx = (uint32_t)x;
+    const unsigned long long pk = (unsigned long long)(qq | (dd << 24)) + (1ull << 39);
+    const uint32_t dp = ee * (100u - dd);  // < 2^31
+    const unsigned long long ch = (unsigned long long)dp * (100u + xx);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      if (slot == k) {
+        acc.a[k][0] += pk;
+        acc.a[k][1] += ee;
+        acc.a[k][2] += dp;
+        acc.a[k][3] += ch;
+      }
+    }
+  }
+  // warp-collective (every lane of the warp calls it with the same acc.since)
+  __device__ __forceinline__ void ring_flush(RingAcc& acc, int lane, RingShared& sh) const {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      unsigned long long v[6];
+      v[0] = acc.a[k][0] & ((1ull << 24) - 1);          // sum(qty)
+      v[5] = (acc.a[k][0] >> 24) & ((1ull << 15) - 1);  // sum(disc)
+      v[4] = acc.a[k][0] >> 39;                         // count
+      v[1] = acc.a[k][1];
+      v[2] = acc.a[k][2];
+      v[3] = acc.a[k][3];
+      if (!__any_sync(kFull, v[4] != 0)) continue;
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[a] += __shfl_xor_sync(kFull, v[a], o);
+      if (lane == 0) {
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+          const unsigned long long old = atomicAdd(&sh.lo[k][a], v[a]);
+          if (old + v[a] < old) atomicAdd(&sh.hi[k][a], 1);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc.a[k][j] = 0;
+    }
+    acc.since = 0;
+  }
+  template <int C>
+  __device__ __forceinline__ void ring_consume(const uint8_t* const (&b)[C], int64_t row0, int cw, int lane,
+                                               RingAcc& acc, RingShared& sh, const Layout& L, const Table& t,
+                                               bool& ovf) const {
+    if (acc.since + kRingLane > kRingFlush) ring_flush(acc, lane, sh);
+    acc.since += kRingLane;
+    const int j = cw * (32 * kRingLane) + lane * kRingLane;
+    const int2 sd = *(const int2*)(b[0] + 4 * j);
+    const uint32_t f = *(const uint16_t*)(b[1] + j), sv = *(const uint16_t*)(b[2] + j);
+    const longlong2 q = *(const longlong2*)(b[3] + 8 * j), e = *(const longlong2*)(b[4] + 8 * j);
+    const longlong2 d = *(const longlong2*)(b[5] + 8 * j), x = *(const longlong2*)(b[6] + 8 * j);
+    ring_row(sd.x, f & 0xffu, sv & 0xffu, q.x, e.x, d.x, x.x, row0 + j, acc, sh);
+    ring_row(sd.y, f >> 8, sv >> 8, q.y, e.y, d.y, x.y, row0 + j + 1, acc, sh);
+  }
+  __device__ __forceinline__ void ring_tail(int64_t r0, int64_t n, int cw, int lane, RingAcc& acc, RingShared& sh,
+                                            const Layout& L, const Table& t, bool& ovf) const {
+    ring_flush(acc, lane, sh);  // <= kRingLane tail rows per lane follow
+    for (int64_t r = r0 + cw * 32 + lane; r < n; r += kRingConsumers * 32)
+      ring_row(__ldg(ship + r), __ldg(rf + r), __ldg(ls + r), __ldg(qty + r), __ldg(ext + r), __ldg(disc + r),
+               __ldg(tax + r), r, acc, sh);
+  }
+  __device__ __forceinline__ void ring_finish(RingShared& sh, int tid, int nt, const Layout& L, const Table& t) const {
+    bool ovf = false;
+    const int ns = min(sh.nslow, kRingSlowCap);
+    for (int i = tid; i < ns; i += nt) gb_dense_slow_row(*this, t, L, sh.slow[i], ovf);
+    if (ovf) atomicExch(ovf_flag, 1);
+    if (tid >= 6) return;
+    const int k = tid;
+    if (sh.lo[k][4] == 0 && sh.hi[k][4] == 0) return;  // no row of this group in the CTA
+    const uint64_t key = ((uint64_t)(k < 2 ? 'A' : (k < 4 ? 'N' : 'R')) << 32) | (uint64_t)((k & 1) ? 'O' : 'F');
+    uint8_t* p = find_or_insert(t, L, key);
+    if (!p) return;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      if (L.kind[a] == ST_SUM)
+        atomic_add_sum96((unsigned long long*)(p + L.off8[a]), (int*)(p + L.off4[a]), (int64_t)sh.lo[k][a], sh.hi[k][a]);
+      else
+        atomicAdd((unsigned long long*)(p + L.off8[a]), sh.lo[k][a]);
+    }
+  }
   template <int I>
   __device__ __forceinline__ void state(int a, const int32_t (&)[I], const bool (&)[I], const Cache<I>& c,
                                         int64_t (&v)[I], bool& ovf) const {

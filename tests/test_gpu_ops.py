@@ -484,3 +484,23 @@ def test_filter_contains_edges(ctx, maxlen):
     for pat in (b"green", LONG):
         sel, _ = ctx.filter([sx.col(pad[3:], A.SX_STR, offsets=dev(offs))], [(0, "contains", pat)])
         assert np.array_equal(sel.cpu().numpy(), oracle.contains(offs, chars, pat)), pat
+
+
+def test_misaligned_and_strided_columns_rejected(ctx):
+    """sx.h alignment rule: an offset or strided view is rejected by the binding, and a
+    misaligned pointer passed straight through the C ABI returns SX_EINVAL instead of faulting."""
+    import ctypes as C
+
+    x = torch.arange(1000, dtype=torch.int64, device="cuda")
+    with pytest.raises(sx.SxError):
+        sx.col(x[1:])
+    with pytest.raises(sx.SxError):
+        sx.col(x[::2])
+    raw = (A.Col * 1)(A.Col(A.SX_I64, 0, 999, x.data_ptr() + 8, None, None))
+    pred = (A.Pred * 1)(A.Pred(0, A.SX_LT, 5, 0, None, 0, 0))
+    out = A.Sel()
+    st = ctx.L.sx_filter(ctx.h, raw, 1, pred, 1, None, None, 0, C.byref(out), None)
+    assert st == A.SX_EINVAL
+    # the context is still healthy (no sticky fault): an aligned call succeeds
+    sel, _ = ctx.filter([sx.col(x)], [(0, "lt", 5)])
+    assert sel.cpu().tolist() == [0, 1, 2, 3, 4]

@@ -142,6 +142,33 @@ def test_q1_q6_dense_guard_and_tails(ctx, trunc):
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
 
 
+@pytest.mark.parametrize("case", ["tails", "guard", "overflow", "ring-off"])
+def test_q1_ring(ctx, monkeypatch, case):
+    """Q1 through K9r (producer warp + cp.async.bulk tile ring, >= 1024 rows per SM: SF 0.1): a
+    ragged last tile (global-load tail), rows failing the register fast path (exact per-CTA slow
+    list), a slow list that overflows (the host reruns K9d), and SX_RING=0 (K9d) on the same data."""
+    host = gen.cpu_tables(100, seed=11)
+    li = {k: v.copy() for k, v in host["lineitem"].items()}
+    n = len(li["l_shipdate"]) - (777 if case == "tails" else 0)
+    li = {k: v[:n].copy() for k, v in li.items()}
+    rng = np.random.default_rng(5)
+    if case == "guard":
+        for col, val in (("l_extendedprice", 1 << 40), ("l_discount", -5), ("l_tax", 17), ("l_quantity", 8192),
+                         ("l_discount", 16), ("l_extendedprice", 1 << 24)):
+            li[col][rng.choice(n, 9, replace=False)] = val
+        li["l_returnflag"][rng.choice(n, 9, replace=False)] = ord("Z")
+        li["l_linestatus"][rng.choice(n, 9, replace=False)] = ord("Q")
+    if case == "overflow":
+        li["l_returnflag"][rng.choice(n, n // 3, replace=False)] = ord("B")
+    if case == "ring-off":
+        monkeypatch.setenv("SX_RING", "0")
+    host = dict(host)
+    host["lineitem"] = li
+    want = oracle.run_query("q1", host)
+    got = tpch.Tpch(ctx, to_dev(host)).run("q1")
+    assert rows_equal(got, want), diff_rows(got, want)
+
+
 @pytest.mark.parametrize("plan", ["fused", "fused-mat", "fused-dense", "fused-wscan", "fused-wscan-partitioned",
                                   "fused-partitioned", "ops"])
 def test_q9_plans(small, monkeypatch, plan):
