@@ -864,7 +864,7 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
           // is 16-B aligned (to_dcols) and a tile's column chunks are multiples of 16 B.  SX_RING=0: K9d.
           static const bool ring_off = getenv("SX_RING") && getenv("SX_RING")[0] == '0';
           if (!ring_off && !ring_retry && n >= (int64_t)Prog::kRingTile * ctx->num_sms) {
-            const size_t smem = (size_t)Prog::kRingStages * ring_stage_bytes<Prog>();
+            const size_t smem = ring_smem_bytes<Prog>();
             SX_CUDA(cudaFuncSetAttribute(k_gb_ring<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             k_gb_ring<Prog><<<(unsigned)ctx->num_sms, (Prog::kRingConsumers + 1) * 32, smem, SX_STREAM(ctx)>>>(prog, n, L, t);
             SX_CHECK_LAUNCH();

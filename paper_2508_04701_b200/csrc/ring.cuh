@@ -13,12 +13,13 @@
 // whole tile go through the program's global-load tail path in the last CTA.  Program interface
 // (see Q1Prog in tpch.cu):
 //   kRingCols, kRingTile (rows per stage), kRingStages, kRingConsumers, ring_width(c), ring_col(c)
+//   kRingExtraBytes (dynamic shared memory after the ring, e.g. lane-private accumulators)
 //   struct RingAcc (per-thread registers), struct RingShared (per-CTA merge state)
-//   ring_shared_init(sh, tid, nthreads)            before the first barrier
-//   ring_consume(b[], row0, cw, lane, acc, sh, L, t, ovf)  one stage: cw-th slice of the tile
-//   ring_tail(r0, n, cw, lane, acc, sh, L, t, ovf) rows [r0, n) (< one tile), global loads
-//   ring_flush(acc, lane, sh)                      warp-collective: registers -> CTA state
-//   ring_finish(sh, tid, nthreads, L, t)           after the last barrier: CTA state -> table
+//   ring_shared_init(sh, x, tid, nthreads)          before the first barrier (x = extra smem)
+//   ring_consume(b[], row0, cw, lane, acc, sh, x)   one stage: cw-th slice of the tile
+//   ring_tail(r0, n, cw, lane, acc, sh, x)          rows [r0, n) (< one tile), global loads
+//   ring_flush(acc, cw, lane, sh, x)                warp-collective: per-thread -> CTA state
+//   ring_finish(sh, tid, nthreads, L, t)            after the last barrier: CTA state -> table
 #pragma once
 #include "groupby.cuh"
 
@@ -29,10 +30,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 template <class P>
+__host__ __device__ constexpr size_t ring_smem_bytes();
+template <class P>
 __host__ __device__ constexpr size_t ring_stage_bytes() {
   size_t b = 0;
   for (int c = 0; c < P::kRingCols; ++c) b += (size_t)P::kRingTile * P::ring_width(c);
   return b;
+}
+
+template <class P>
+__host__ __device__ constexpr size_t ring_smem_bytes() {
+  return (size_t)P::kRingStages * ring_stage_bytes<P>() + P::kRingExtraBytes;
 }
 
 template <class P, class = void>
@@ -59,7 +67,8 @@ __global__ void __launch_bounds__((P::kRingConsumers + 1) * 32, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  prog.ring_shared_init(sh, threadIdx.x, blockDim.x);
+  uint8_t* const xs = ring + (size_t)S * SB;  // the program's extra shared memory
+  prog.ring_shared_init(sh, xs, threadIdx.x, blockDim.x);
   __syncthreads();
   if (warp == NC) {  // producer: one elected lane issues every bulk copy
     if (lane == 0) {
@@ -81,7 +90,6 @@ __global__ void __launch_bounds__((P::kRingConsumers + 1) * 32, 1)
   } else {
     typename P::RingAcc acc;
     prog.ring_init(acc);
-    bool ovf = false;
     int64_t k = 0;
     for (int64_t tile = t0; tile < t1; ++tile, ++k) {
       const int s = (int)(k % S);
@@ -93,13 +101,12 @@ __global__ void __launch_bounds__((P::kRingConsumers + 1) * 32, 1)
         b[c] = ring + s * SB + off;
         off += (size_t)T * P::ring_width(c);
       }
-      prog.ring_consume(b, tile * (int64_t)T, warp, lane, acc, sh, L, t, ovf);
+      prog.ring_consume(b, tile * (int64_t)T, warp, lane, acc, sh, xs);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (blockIdx.x == gridDim.x - 1 && ntiles * T < n) prog.ring_tail(ntiles * T, n, warp, lane, acc, sh, L, t, ovf);
-    prog.ring_flush(acc, lane, sh);
-    if (ovf) atomicExch(prog.ovf_flag, 1);
+    if (blockIdx.x == gridDim.x - 1 && ntiles * T < n) prog.ring_tail(ntiles * T, n, warp, lane, acc, sh, xs);
+    prog.ring_flush(acc, warp, lane, sh, xs);
   }
   __syncthreads();
   prog.ring_finish(sh, threadIdx.x, blockDim.x, L, t);

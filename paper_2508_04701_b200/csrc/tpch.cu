@@ -191,27 +191,31 @@ struct Q1Prog {
     for (int i = 0; i < 4; ++i) alive[i] = true;
     compute<4>(sd, f, s, q, e, d, x, alive, key, v, fast);
   }
-  // Ring interface (K9r, ring.cuh): 1024-row tiles of the 7 columns (38.9 KB per stage), 5 stages,
-  // 16 consumer warps taking 2 consecutive rows per lane.  Per-thread exact accumulators in
-  // registers for the 6 (returnflag, linestatus) combinations {A,N,R} x {F,O}, 4 per group:
-  //   pk = sum(qty) | sum(disc) << 24 | count << 39  (packed), sum(ext), sum(dp), sum(charge).
+  // Ring interface (K9r, ring.cuh): 1024-row tiles of the 7 columns (38.9 KB per stage), 3 stages,
+  // 16 consumer warps taking 2 consecutive rows per lane.  Exact per-thread accumulators live in
+  // lane-private shared memory cells indexed by the row's group, so the group choice is an address,
+  // not a branch: the 6 (returnflag, linestatus) combinations {A,N,R} x {F,O}, 4 sums per group in
+  // two 16-byte cells: {pk, sum(ext)} and {sum(dp), sum(charge)}, where
+  //   pk = sum(qty) | sum(disc) << 24 | count << 39  (packed).
   // Fast-path guard per row: 0 <= qty < 2^13, 0 <= ext < 2^24, 0 <= disc, tax < 2^4.  Then dp =
   // ext*(100-disc) < 2^31 and charge = dp*(100+tax) < 2^38 are exact 32x32->64 products, and over
   // kRingFlush = 2048 rows per thread the packed fields (< 2^24, 2^15, 2^12) and the other sums
   // (< 2^35, 2^42, 2^49) cannot overflow; every 2048 rows a warp-collective flush adds them into a
   // per-CTA shared state (96-bit sums), merged into the global table once per CTA.  A row failing
-  // the guard, or with another flag value, takes the exact per-row path (gb_dense_slow_row).
+  // the guard, or with another flag value, goes to a per-CTA list for the exact per-row path
+  // (gb_dense_slow_row) after the stream; if that list overflows the host reruns K9d.
   static constexpr int kRingCols = 7;
   static constexpr int kRingTile = 1024;
-  static constexpr int kRingStages = 5;
+  static constexpr int kRingStages = 3;
   static constexpr int kRingConsumers = 16;
-  static constexpr int kRingLane = kRingTile / (kRingConsumers * 32);
+  static constexpr int kRingThreads = kRingConsumers * 32;
+  static constexpr int kRingLane = kRingTile / kRingThreads;
   static constexpr int kRingFlush = 2048;
+  static constexpr size_t kRingExtraBytes = (size_t)6 * 2 * kRingThreads * sizeof(ulonglong2);  // 96 KB
   static_assert(kRingLane == 2, "ring_consume reads 2 rows per lane");
   __host__ __device__ static constexpr int ring_width(int c) { return bulk_width(c); }
   __host__ __device__ const void* ring_col(int c) const { return bulk_col(c); }
   struct RingAcc {
-    unsigned long long a[6][4];
     int since;
   };
   static constexpr int kRingSlowCap = 2048;  // rows per CTA for the exact path (else the host reruns K9d)
@@ -221,96 +225,95 @@ struct Q1Prog {
     int nslow;
     int32_t slow[kRingSlowCap];
   };
-  __device__ __forceinline__ void ring_init(RingAcc& acc) const {
-#pragma unroll
-    for (int k = 0; k < 6; ++k)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc.a[k][j] = 0;
-    acc.since = 0;
+  __device__ __forceinline__ static ulonglong2* ring_cell(uint8_t* xs, int slot, int ct) {
+    return (ulonglong2*)xs + (slot * 2 * kRingThreads + ct);  // second cell at + kRingThreads
   }
-  __device__ __forceinline__ void ring_shared_init(RingShared& sh, int tid, int nt) const {
+  __device__ __forceinline__ void ring_init(RingAcc& acc) const { acc.since = 0; }
+  __device__ __forceinline__ void ring_shared_init(RingShared& sh, uint8_t* xs, int tid, int nt) const {
     for (int j = tid; j < 36; j += nt) {
       sh.lo[j / 6][j % 6] = 0;
       sh.hi[j / 6][j % 6] = 0;
     }
     if (tid == 0) sh.nslow = 0;
+    for (int j = tid; j < 6 * 2 * kRingThreads; j += nt) ((ulonglong2*)xs)[j] = make_ulonglong2(0, 0);
   }
   __device__ __forceinline__ void ring_row(int32_t sd, uint32_t f, uint32_t s, long long q, long long e, long long d,
-                                           long long x, int64_t row, RingAcc& acc, RingShared& sh) const {
-    if (sd > ship_max) return;
-    const int fi = f == 'A' ? 0 : (f == 'N' ? 1 : (f == 'R' ? 2 : 3));
-    const int si = s == 'F' ? 0 : (s == 'O' ? 1 : 2);
+                                           long long x, int64_t row, int ct, RingShared& sh, uint8_t* xs) const {
+    const bool fN = f == 'N', fR = f == 'R', sO = s == 'O';
+    const bool flags_ok = (f == 'A' || fN || fR) && (s == 'F' || sO);
     const unsigned long long g = ((unsigned long long)q >> 13) | ((unsigned long long)e >> 24) |
                                  ((unsigned long long)d >> 4) | ((unsigned long long)x >> 4);
-    if (fi == 3 || si == 2 || g != 0) {  // exact path after the stream (no call in the hot loop)
+    const bool alive = sd <= ship_max, fast = flags_ok && g == 0;
+    if (alive && !fast) {  // exact path after the stream (no call in the hot loop)
       const int pos = atomicAdd(&sh.nslow, 1);
       if (pos < kRingSlowCap) sh.slow[pos] = (int32_t)row;
       else atomicExch(ovf_flag + 3, 1);
-      return;
     }
-    const int slot = fi * 2 + si;
-    const uint32_t qq = (uint32_t)q, ee = (uint32_t)e, dd = (uint32_t)d, xx = (uint32_t)x;
-    const unsigned long long pk = (unsigned long long)(qq | (dd << 24)) + (1ull << 39);
-    const uint32_t dp = ee * (100u - dd);  // < 2^31
-    const unsigned long long ch = (unsigned long long)dp * (100u + xx);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      if (slot == k) {
-        acc.a[k][0] += pk;
-        acc.a[k][1] += ee;
-        acc.a[k][2] += dp;
-        acc.a[k][3] += ch;
-      }
+    if (alive && fast) {
+      const int slot = ((int)fN + 2 * (int)fR) * 2 + (int)sO;
+      const uint32_t qq = (uint32_t)q, ee = (uint32_t)e, dd = (uint32_t)d, xx = (uint32_t)x;
+      const uint32_t dp = ee * (100u - dd);  // < 2^31
+      ulonglong2* c = ring_cell(xs, slot, ct);
+      ulonglong2 a = c[0], b = c[kRingThreads];
+      a.x += (unsigned long long)(qq | (dd << 24)) + (1ull << 39);
+      a.y += ee;
+      b.x += dp;
+      b.y += (unsigned long long)dp * (100u + xx);
+      c[0] = a;
+      c[kRingThreads] = b;
     }
   }
-  // warp-collective (every lane of the warp calls it with the same acc.since)
-  __device__ __forceinline__ void ring_flush(RingAcc& acc, int lane, RingShared& sh) const {
-#pragma unroll
+  // warp-collective (every lane of the warp calls it at the same point)
+  __device__ __forceinline__ void ring_flush(RingAcc& acc, int cw, int lane, RingShared& sh, uint8_t* xs) const {
+    const int ct = cw * 32 + lane;
+#pragma unroll 1
     for (int k = 0; k < 6; ++k) {
+      ulonglong2* c = ring_cell(xs, k, ct);
+      const ulonglong2 a = c[0], b = c[kRingThreads];
       unsigned long long v[6];
-      v[0] = acc.a[k][0] & ((1ull << 24) - 1);          // sum(qty)
-      v[5] = (acc.a[k][0] >> 24) & ((1ull << 15) - 1);  // sum(disc)
-      v[4] = acc.a[k][0] >> 39;                         // count
-      v[1] = acc.a[k][1];
-      v[2] = acc.a[k][2];
-      v[3] = acc.a[k][3];
+      v[0] = a.x & ((1ull << 24) - 1);          // sum(qty)
+      v[5] = (a.x >> 24) & ((1ull << 15) - 1);  // sum(disc)
+      v[4] = a.x >> 39;                         // count
+      v[1] = a.y;
+      v[2] = b.x;
+      v[3] = b.y;
       if (!__any_sync(kFull, v[4] != 0)) continue;
+      c[0] = make_ulonglong2(0, 0);
+      c[kRingThreads] = make_ulonglong2(0, 0);
 #pragma unroll
-      for (int a = 0; a < 6; ++a)
+      for (int j = 0; j < 6; ++j)
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[a] += __shfl_xor_sync(kFull, v[a], o);
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(kFull, v[j], o);
       if (lane == 0) {
 #pragma unroll
-        for (int a = 0; a < 6; ++a) {
-          const unsigned long long old = atomicAdd(&sh.lo[k][a], v[a]);
-          if (old + v[a] < old) atomicAdd(&sh.hi[k][a], 1);
+        for (int j = 0; j < 6; ++j) {
+          const unsigned long long old = atomicAdd(&sh.lo[k][j], v[j]);
+          if (old + v[j] < old) atomicAdd(&sh.hi[k][j], 1);
         }
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc.a[k][j] = 0;
     }
     acc.since = 0;
   }
   template <int C>
   __device__ __forceinline__ void ring_consume(const uint8_t* const (&b)[C], int64_t row0, int cw, int lane,
-                                               RingAcc& acc, RingShared& sh, const Layout& L, const Table& t,
-                                               bool& ovf) const {
-    if (acc.since + kRingLane > kRingFlush) ring_flush(acc, lane, sh);
+                                               RingAcc& acc, RingShared& sh, uint8_t* xs) const {
+    if (acc.since + kRingLane > kRingFlush) ring_flush(acc, cw, lane, sh, xs);
     acc.since += kRingLane;
-    const int j = cw * (32 * kRingLane) + lane * kRingLane;
+    const int ct = cw * 32 + lane, j = ct * kRingLane;
     const int2 sd = *(const int2*)(b[0] + 4 * j);
     const uint32_t f = *(const uint16_t*)(b[1] + j), sv = *(const uint16_t*)(b[2] + j);
     const longlong2 q = *(const longlong2*)(b[3] + 8 * j), e = *(const longlong2*)(b[4] + 8 * j);
     const longlong2 d = *(const longlong2*)(b[5] + 8 * j), x = *(const longlong2*)(b[6] + 8 * j);
-    ring_row(sd.x, f & 0xffu, sv & 0xffu, q.x, e.x, d.x, x.x, row0 + j, acc, sh);
-    ring_row(sd.y, f >> 8, sv >> 8, q.y, e.y, d.y, x.y, row0 + j + 1, acc, sh);
+    ring_row(sd.x, f & 0xffu, sv & 0xffu, q.x, e.x, d.x, x.x, row0 + j, ct, sh, xs);
+    ring_row(sd.y, f >> 8, sv >> 8, q.y, e.y, d.y, x.y, row0 + j + 1, ct, sh, xs);
   }
   __device__ __forceinline__ void ring_tail(int64_t r0, int64_t n, int cw, int lane, RingAcc& acc, RingShared& sh,
-                                            const Layout& L, const Table& t, bool& ovf) const {
-    ring_flush(acc, lane, sh);  // <= kRingLane tail rows per lane follow
-    for (int64_t r = r0 + cw * 32 + lane; r < n; r += kRingConsumers * 32)
+                                            uint8_t* xs) const {
+    ring_flush(acc, cw, lane, sh, xs);  // <= kRingLane tail rows per lane follow
+    const int ct = cw * 32 + lane;
+    for (int64_t r = r0 + ct; r < n; r += kRingThreads)
       ring_row(__ldg(ship + r), __ldg(rf + r), __ldg(ls + r), __ldg(qty + r), __ldg(ext + r), __ldg(disc + r),
-               __ldg(tax + r), r, acc, sh);
+               __ldg(tax + r), r, ct, sh, xs);
   }
   __device__ __forceinline__ void ring_finish(RingShared& sh, int tid, int nt, const Layout& L, const Table& t) const {
     bool ovf = false;
