@@ -49,27 +49,27 @@ template <class P>
 struct has_ring<P, std::void_t<decltype(P::kRingCols)>> : std::true_type {};
 
 template <class P>
-__global__ void __launch_bounds__((P::kRingConsumers + 1) * 32, 1)
-    k_gb_ring(const __grid_constant__ P prog, int64_t n, const __grid_constant__ Layout L, Table t) {
-  constexpr int C = P::kRingCols, S = P::kRingStages, T = P::kRingTile, NC = P::kRingConsumers;
-  constexpr size_t SB = ring_stage_bytes<P>();
-  extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t full[S];
-  __shared__ __align__(8) uint64_t empty[S];
-  __shared__ typename P::RingShared sh;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ntiles = n / T;
-  const int64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
+__device__ __forceinline__ void ring_init_bars(uint64_t* full, uint64_t* empty) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
+    for (int s = 0; s < P::kRingStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NC);
+      mbar_init(&empty[s], P::kRingConsumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  uint8_t* const xs = ring + (size_t)S * SB;  // the program's extra shared memory
-  prog.ring_shared_init(sh, xs, threadIdx.x, blockDim.x);
-  __syncthreads();
+}
+
+// The pipeline after ring_init_bars + a __syncthreads: warp kRingConsumers produces, the others
+// call consume(b[], row0, cw, lane) once per tile of this CTA's chunk [t0, t1) of n / kRingTile
+// whole tiles.  Returns true on consumer threads.
+template <class P, class F>
+__device__ __forceinline__ bool ring_pipeline(const P& prog, int64_t n, uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                              F&& consume) {
+  constexpr int C = P::kRingCols, S = P::kRingStages, T = P::kRingTile, NC = P::kRingConsumers;
+  constexpr size_t SB = ring_stage_bytes<P>();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = n / T;
+  const int64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
   if (warp == NC) {  // producer: one elected lane issues every bulk copy
     if (lane == 0) {
       int64_t k = 0;
@@ -87,24 +87,46 @@ __global__ void __launch_bounds__((P::kRingConsumers + 1) * 32, 1)
         }
       }
     }
-  } else {
-    typename P::RingAcc acc;
-    prog.ring_init(acc);
-    int64_t k = 0;
-    for (int64_t tile = t0; tile < t1; ++tile, ++k) {
-      const int s = (int)(k % S);
-      mbar_wait(&full[s], (uint32_t)((k / S) & 1));
-      const uint8_t* b[C];
-      size_t off = 0;
+    return false;
+  }
+  int64_t k = 0;
+  for (int64_t tile = t0; tile < t1; ++tile, ++k) {
+    const int s = (int)(k % S);
+    mbar_wait(&full[s], (uint32_t)((k / S) & 1));
+    const uint8_t* b[C];
+    size_t off = 0;
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        b[c] = ring + s * SB + off;
-        off += (size_t)T * P::ring_width(c);
-      }
-      prog.ring_consume(b, tile * (int64_t)T, warp, lane, acc, sh, xs);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+    for (int c = 0; c < C; ++c) {
+      b[c] = ring + s * SB + off;
+      off += (size_t)T * P::ring_width(c);
     }
+    consume(b, tile * (int64_t)T, warp, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  return true;
+}
+
+template <class P>
+__global__ void __launch_bounds__((P::kRingConsumers + 1) * 32, 1)
+    k_gb_ring(const __grid_constant__ P prog, int64_t n, const __grid_constant__ Layout L, Table t) {
+  constexpr int S = P::kRingStages, T = P::kRingTile;
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[S];
+  __shared__ __align__(8) uint64_t empty[S];
+  __shared__ typename P::RingShared sh;
+  ring_init_bars<P>(full, empty);
+  uint8_t* const xs = ring + (size_t)S * ring_stage_bytes<P>();  // the program's extra shared memory
+  prog.ring_shared_init(sh, xs, threadIdx.x, blockDim.x);
+  __syncthreads();
+  typename P::RingAcc acc;
+  prog.ring_init(acc);
+  const bool consumer = ring_pipeline(prog, n, ring, full, empty, [&](const uint8_t* const* b, int64_t row0, int cw, int lane) {
+    prog.ring_consume(b, row0, cw, lane, acc, sh, xs);
+  });
+  if (consumer) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntiles = n / T;
     if (blockIdx.x == gridDim.x - 1 && ntiles * T < n) prog.ring_tail(ntiles * T, n, warp, lane, acc, sh, xs);
     prog.ring_flush(acc, warp, lane, sh, xs);
   }
