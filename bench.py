@@ -147,6 +147,16 @@ def run_oracle(sf_milli: int, reps: int) -> list[float]:
 
 
 # ---------------------------------------------------------------------------------- main
+def bench_config(args, world: int) -> dict:
+    """The workload a bench line is quoted on; identical in the sx and the reference arm."""
+    sf_total = args.sf * world
+    return {"workload": f"TPC-H Q1+Q6+Q3+Q9+Q18 SF{args.sf:g} (one step = all five plans)",
+            "sf": args.sf, "seed": args.seed,
+            "l2_note": "inputs (>30 GB) >> 126 MB L2; no flush needed",
+            "parallelism": (f"sharded x{world}: rank r holds shard r of SF{sf_total:g}; "
+                            "allgather/shuffle over NCCL" if world > 1 else "single GPU")}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -198,14 +208,16 @@ def main():
         b = oracle_bytes(cpu_milli)
         t = statistics.mean(secs)
         v = b / t / 1e9
-        sample = (f"TPC-H Q1+Q6+Q3+Q9+Q18 at SF {args.cpu_sf:g} ({b / 1e9:.2f} GB algorithmic), materialised host "
+        sample = (f"bounded sample of the SF{args.sf * args.gpus:g} workload: the same five plans at SF "
+                  f"{args.cpu_sf:g} per step ({b / 1e9:.2f} GB algorithmic), materialised host "
                   "columns, generation excluded, single-threaded C++ oracle")
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded TPC-H-shaped generator)",
-            "config": {"workload": f"TPC-H Q1+Q6+Q3+Q9+Q18 SF{args.cpu_sf:g} CPU oracle sample", "sf": args.cpu_sf,
-                       "seed": args.seed},
+            # the same config as the sx arm's line (the workload this arm samples); the sample itself
+            # is described in cpu_baseline.sample
+            "config": bench_config(args, args.gpus),
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }))
@@ -427,13 +439,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (seeded TPC-H-shaped generator, generated in HBM; decimals scaled int64)",
-            "config": {"workload": f"TPC-H Q1+Q6+Q3+Q9+Q18 SF{args.sf:g} (one step = all five plans)",
-                       "sf": args.sf, "seed": args.seed, "rows_lineitem": n["l"],
-                       "algorithmic_bytes_per_step": step_bytes, "query_bytes": qb,
-                       "l2_note": "inputs (>30 GB) >> 126 MB L2; no flush needed",
-                       "sf_total": sf_total / 1000, "job_bytes_per_step": job_bytes,
-                       "parallelism": (f"sharded x{world}: rank r holds shard r of SF{sf_total / 1000:g}; "
-                                       "allgather/shuffle over NCCL" if world > 1 else "single GPU")},
+            "config": bench_config(args, world),
+            "workload_detail": {"rows_lineitem": n["l"], "algorithmic_bytes_per_step": step_bytes,
+                                "query_bytes": qb, "sf_total": sf_total / 1000, "job_bytes_per_step": job_bytes},
             "query_ms": q_ms, "operator_ms": op_ms, "operator_roofline": op_gbs, "parity": parity,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
