@@ -501,187 +501,6 @@ __global__ void __launch_bounds__(kBlock, 4) k_runs_own_dense(const __grid_const
   if (ovf) atomicExch(prog.ovf_flag, 1);
 }
 
-// K10rr: K10r (owned runs, HAVING pushed down) over the tile ring (ring.cuh).  The key and value
-// columns stream into shared memory through cp.async.bulk; each consumer warp takes 128
-// consecutive rows of a tile (4 per lane).  A lane's head rows (first row, or a key change) are
-// the groups it owns; the rows at its start that continue the previous lane's group (its "lead")
-// are handed backwards by an affine suffix scan over the warp — S(L) = lead(L) + headless(L) *
-// S(L+1) — so every owned group collects its continuation through any number of headless lanes
-// in 5 shuffle steps; lane 31 reads the rows after the warp's 128 (shared memory within the tile,
-// global memory past it) while the key continues.  Values must satisfy |v| < 2^40 (sums over a
-// group of <= 128 + kRunAhead rows are then exact in int64): otherwise, for runs longer than
-// kRunAhead past a warp, or for an unsorted key column, flags[1]/flags[0] send the host to
-// the other strategies.  Rows after the last whole tile form one more (global-load) tile.
-template <class P>
-__global__ void __launch_bounds__((P::kRingConsumers + 1) * 32, 1)
-    k_runs_ring(const __grid_constant__ P prog, int64_t n, const __grid_constant__ Layout L,
-                const __grid_constant__ SlotFn hv, uint8_t* __restrict__ out, int64_t cap_out,
-                unsigned long long* cursor, int* flags) {
-  using KT = typename P::KeyT;
-  constexpr int S = P::kRingStages, T = P::kRingTile, NC = P::kRingConsumers, R = T / (NC * 32);
-  static_assert(R == 4, "4 rows per lane");
-  extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t full[S];
-  __shared__ __align__(8) uint64_t empty[S];
-  ring_init_bars<P>(full, empty);
-  __syncthreads();
-  bool bad = false, big = false, longrun = false;
-  const int hv_op = hv.hv_op, kb = L.key_bytes, o8 = L.off8[0], o4 = L.off4[0], sb = L.slot_bytes;
-  const long long hv_lo = hv.hv_lo, hv_hi = hv.hv_hi;
-  const bool has_hv = hv.has_having != 0;
-  // one warp segment: rows j0 + 4*lane + i of a tile starting at global row row0 holding m rows;
-  // FROM_SMEM: the tile is in the ring (b), else read from global memory
-  auto segment = [&](const uint8_t* const* b, bool from_smem, int64_t row0, int m, int cw, int lane) {
-    const int j0 = cw * (32 * R), j = j0 + lane * R;
-    uint64_t k[R];
-    long long v[R];
-    bool val[R];
-    if (from_smem) {
-      if constexpr (sizeof(KT) == 4) {
-        const int4 kk = *(const int4*)(b[0] + 4 * j);
-        k[0] = (uint64_t)(int64_t)kk.x; k[1] = (uint64_t)(int64_t)kk.y;
-        k[2] = (uint64_t)(int64_t)kk.z; k[3] = (uint64_t)(int64_t)kk.w;
-      } else {
-        const longlong2 k01 = *(const longlong2*)(b[0] + 8 * j), k23 = *(const longlong2*)(b[0] + 8 * j + 16);
-        k[0] = (uint64_t)k01.x; k[1] = (uint64_t)k01.y; k[2] = (uint64_t)k23.x; k[3] = (uint64_t)k23.y;
-      }
-      const longlong2 v01 = *(const longlong2*)(b[1] + 8 * j), v23 = *(const longlong2*)(b[1] + 8 * j + 16);
-      v[0] = v01.x; v[1] = v01.y; v[2] = v23.x; v[3] = v23.y;
-#pragma unroll
-      for (int i = 0; i < R; ++i) val[i] = true;
-    } else {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        val[i] = j + i < m;
-        k[i] = val[i] ? (uint64_t)(int64_t)__ldg(prog.okey + row0 + j + i) : 0;
-        v[i] = val[i] ? __ldg(prog.qty + row0 + j + i) : 0;
-      }
-    }
-    auto key_at = [&](int64_t r) -> uint64_t {  // global row r (r - row0 < T: from the tile)
-      const int64_t jj = r - row0;
-      if (from_smem && jj >= 0 && jj < T) return (uint64_t)(int64_t)((const KT*)b[0])[jj];
-      return (uint64_t)(int64_t)__ldg(prog.okey + r);
-    };
-    auto val_at = [&](int64_t r) -> long long {
-      const int64_t jj = r - row0;
-      if (from_smem && jj >= 0 && jj < T) return ((const long long*)b[1])[jj];
-      return __ldg(prog.qty + r);
-    };
-    unsigned long long mag = 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) mag |= (unsigned long long)(v[i] < 0 ? -v[i] : v[i]);
-    big |= (mag >> 40) != 0;
-    // previous row's key (lane 0: the row before this warp's segment)
-    uint64_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
-    bool pv = true;
-    if (lane == 0) {
-      const int64_t r = row0 + j0 - 1;
-      pv = r >= 0;
-      if (pv) pk = key_at(r);
-    }
-    bool head[R];
-    long long lead = 0;
-    bool nohead = true;
-    {
-      uint64_t prev = pk;
-      bool hp = pv;
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        head[i] = val[i] && (!hp || k[i] != prev);
-        bad |= val[i] && hp && (int64_t)k[i] < (int64_t)prev;
-        nohead = nohead && !head[i];
-        if (val[i] && nohead) lead += v[i];
-        prev = k[i];
-        hp = hp || val[i];
-      }
-    }
-    // suffix affine scan: (a, hb) of lanes [L, 32): S(L) = a + hb * S(32)
-    long long a = lead;
-    bool hb = nohead && val[R - 1];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const long long a2 = __shfl_down_sync(kFull, a, d);
-      const bool b2 = __shfl_down_sync(kFull, (int)hb, d) != 0;
-      if (lane + d < 32) {
-        if (hb) a += a2;
-        hb = hb && b2;
-      }
-    }
-    long long ca = __shfl_down_sync(kFull, a, 1);
-    bool cb = __shfl_down_sync(kFull, (int)hb, 1) != 0;
-    if (lane == 31) {
-      ca = 0;
-      cb = true;
-    }
-    // S(32): lane 31 continues the group of the segment's last row past the segment
-    long long ext = 0;
-    if (lane == 31 && val[R - 1]) {
-      const uint64_t K = k[R - 1];
-      int64_t r = row0 + j0 + 32 * R;
-      int steps = 0;
-      for (; r < n && steps < kRunAhead; ++r, ++steps) {
-        if (key_at(r) != K) break;
-        const long long x = val_at(r);
-        big |= ((unsigned long long)(x < 0 ? -x : x) >> 40) != 0;
-        ext += x;
-      }
-      if (steps == kRunAhead && r < n && key_at(r) == K) longrun = true;
-    }
-    ext = __shfl_sync(kFull, ext, 31);
-    // owned groups: every head row; the last one in the lane takes the continuation
-    long long acc = 0;
-    bool open = false;
-    uint64_t gk = 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      if (!val[i]) break;
-      if (head[i]) {
-        if (open) {
-          const int32_t hi = acc < 0 ? -1 : 0;
-          if (!has_hv || (hi == (acc < 0 ? -1 : 0) && cmp(hv_op, acc, hv_lo, hv_hi))) {
-            const unsigned long long pos = atomicAdd(cursor, 1ull);
-            if ((int64_t)pos < cap_out) {
-              uint8_t* d = out + pos * sb;
-              if (kb == 4) *(unsigned*)d = (unsigned)gk;
-              else *(unsigned long long*)d = gk;
-              *(unsigned long long*)(d + o8) = (unsigned long long)acc;
-              *(int*)(d + o4) = hi;
-            }
-          }
-        }
-        open = true;
-        gk = k[i];
-        acc = 0;
-      }
-      if (open) acc += v[i];
-    }
-    if (open) {
-      acc += ca + (cb ? ext : 0);
-      const int32_t hi = acc < 0 ? -1 : 0;
-      if (!has_hv || cmp(hv_op, acc, hv_lo, hv_hi)) {
-        const unsigned long long pos = atomicAdd(cursor, 1ull);
-        if ((int64_t)pos < cap_out) {
-          uint8_t* d = out + pos * sb;
-          if (kb == 4) *(unsigned*)d = (unsigned)gk;
-          else *(unsigned long long*)d = gk;
-          *(unsigned long long*)(d + o8) = (unsigned long long)acc;
-          *(int*)(d + o4) = hi;
-        }
-      }
-    }
-  };
-  const bool consumer = ring_pipeline(prog, n, ring, full, empty, [&](const uint8_t* const* b, int64_t row0, int cw, int lane) {
-    segment(b, true, row0, T, cw, lane);
-  });
-  if (consumer) {
-    const int64_t ntiles = n / T;
-    if (blockIdx.x == gridDim.x - 1 && ntiles * T < n)
-      segment(nullptr, false, ntiles * T, (int)(n - ntiles * T), threadIdx.x >> 5, threadIdx.x & 31);
-  }
-  if (bad) atomicExch(flags, 1);
-  if (big || longrun) atomicExch(flags + 1, 1);
-}
-
 struct EmitArgs {
   const uint8_t* slots;
   const int32_t* ids;
@@ -900,29 +719,13 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
         hv.hv_hi = P.hv.hi;
         int64_t cap_out = std::max<int64_t>(1 << 16, n / 256);
         unsigned long long* cursor = (unsigned long long*)ctx->d_counters;
-        bool ring_failed = false;
         for (int attempt = 0; attempt < 2 && !own_done; ++attempt) {
           uint8_t* out;
           SX_TRY(scr.get(&out, (size_t)cap_out * L.slot_bytes));
           SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
           SX_CUDA(cudaMemsetAsync(cursor, 0, 8, ctx->stream));
           const int64_t threads = (n + kRunItems - 1) / kRunItems;
-          bool ring_launched = false;
-          if constexpr (has_ring<Prog>::value) {
-            // K10rr (tile ring) first; a flagged run (|v| >= 2^40, a run past kRunAhead, unsorted)
-            // retries below with K10r, which decides between its own checks and hashing
-            static const bool ring_off = getenv("SX_RING") && getenv("SX_RING")[0] == '0';
-            if (!ring_off && attempt == 0 && !ring_failed && L.nst == 1 && L.kind[0] == ST_SUM && L.slot_bytes <= 32 &&
-                n >= (int64_t)Prog::kRingTile * ctx->num_sms) {
-              const size_t smem = ring_smem_bytes<Prog>();
-              SX_CUDA(cudaFuncSetAttribute(k_runs_ring<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-              k_runs_ring<Prog><<<(unsigned)ctx->num_sms, (Prog::kRingConsumers + 1) * 32, smem, SX_STREAM(ctx)>>>(
-                  prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
-              ring_launched = true;
-            }
-          }
-          if (ring_launched) {
-          } else if constexpr (runs_dense<Prog>::value) {
+          if constexpr (runs_dense<Prog>::value) {
             if (L.nst == 1 && L.kind[0] == ST_SUM && L.slot_bytes <= 32)
               k_runs_own_dense<Prog><<<persistent_grid(ctx, 8, ((n + kRunOwnRows - 1) / kRunOwnRows + kBlock - 1) / kBlock),
                                        kBlock, 0, SX_STREAM(ctx)>>>(prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
@@ -937,11 +740,6 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
           int64_t cnt = 0;
           SX_TRY(read_i64(ctx, cursor, &cnt));
           SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
-          if (ring_launched && (flags[2] || flags[3])) {  // let K10r decide
-            ring_failed = true;
-            --attempt;
-            continue;
-          }
           if (flags[2] || flags[3]) break;  // unsorted or a run longer than kRunAhead: other strategies
           if (flags[0]) return set_err(ctx, SX_EOVERFLOW, "a value expression left int64");
           if (cnt > cap_out) {
@@ -1064,7 +862,7 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
         if constexpr (has_ring<Prog>::value) {
           // K9r (ring.cuh): producer warp + bulk-copy tile ring, one CTA per SM; every column base
           // is 16-B aligned (to_dcols) and a tile's column chunks are multiples of 16 B.  SX_RING=0: K9d.
-          static const bool ring_off = getenv("SX_RING") && getenv("SX_RING")[0] == '0';
+          const bool ring_off = getenv("SX_RING") && getenv("SX_RING")[0] == '0';
           if (!ring_off && !ring_retry && n >= (int64_t)Prog::kRingTile * ctx->num_sms) {
             const size_t smem = ring_smem_bytes<Prog>();
             SX_CUDA(cudaFuncSetAttribute(k_gb_ring<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

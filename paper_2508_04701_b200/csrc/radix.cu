@@ -18,6 +18,7 @@
 //                       joined in waves whose tables together stay L2-resident: probes hit L2
 //                       instead of random HBM sectors, payloads are never gathered at random.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "compact.cuh"
@@ -65,9 +66,16 @@ __global__ void __launch_bounds__(kPartThreads) k_part_hist(const __grid_constan
   for (int p = threadIdx.x; p < P; p += blockDim.x) h[p] = 0;
   __syncthreads();
   const int64_t lo = blockIdx.x * s.chunk, hi = min(s.n, lo + s.chunk);
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const int64_t r = s.sel ? (int64_t)__ldg(s.sel + i) : i;
-    atomicAdd(&h[part_of(part_key(s.k0, s.k1, s.nkeys, r), s.bits)], 1);
+  const int lane = threadIdx.x & 31;
+  // warp-aggregated: one shared atomic per distinct partition per warp (the loop trip count is
+  // warp-uniform: chunk bounds are CTA-uniform)
+  for (int64_t b = lo; b < hi; b += blockDim.x) {
+    const int64_t i = b + threadIdx.x;
+    const bool v = i < hi;
+    const int64_t r = v ? (s.sel ? (int64_t)__ldg(s.sel + i) : i) : 0;
+    const int p = v ? (int)part_of(part_key(s.k0, s.k1, s.nkeys, r), s.bits) : (1 << kMaxPartBits) + lane;
+    const unsigned peers = __match_any_sync(kFull, p);
+    if (v && lane == __ffs(peers) - 1) atomicAdd(&h[p], __popc(peers));
   }
   __syncthreads();
   for (int p = threadIdx.x; p < P; p += blockDim.x) hist[(int64_t)p * gridDim.x + blockIdx.x] = h[p];
@@ -162,14 +170,138 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(const __grid_cons
   }
 }
 
+// K7b' (default): 4096-row tiles; ranks within a partition come from warp-aggregated shared
+// counters (__match_any_sync leaders: one shared atomic per distinct partition per warp instead of
+// one per row), and every carried column is staged in shared memory in partition order — loaded
+// coalesced at the tile's own rows, written as partition runs (~32 rows of each column per
+// partition per tile at fan-out 128) — instead of re-gathering each value by row id at write
+// time.  One column at a time, so the staging buffer is 16 B x 4096 at most.
+constexpr int kVsItems = 16;
+constexpr int kVsTile = kPartThreads * kVsItems;
+
+__device__ __forceinline__ void stage_val(const DCol& src, int w, uint8_t* sb, int pos, int64_t r) {
+  switch (w) {
+    case 1: sb[pos] = __ldcs((const uint8_t*)src.p + r); break;
+    case 4: ((int32_t*)sb)[pos] = __ldcs((const int32_t*)src.p + r); break;
+    case 8: ((long long*)sb)[pos] = __ldcs((const long long*)src.p + r); break;
+    default: ((longlong2*)sb)[pos] = __ldcs((const longlong2*)src.p + r); break;
+  }
+}
+__device__ __forceinline__ void emit_val(int w, const uint8_t* sb, int j, void* dst, int64_t d) {
+  switch (w) {
+    case 1: ((uint8_t*)dst)[d] = sb[j]; break;
+    case 4: ((int32_t*)dst)[d] = ((const int32_t*)sb)[j]; break;
+    case 8: ((long long*)dst)[d] = ((const long long*)sb)[j]; break;
+    default: ((longlong2*)dst)[d] = ((const longlong2*)sb)[j]; break;
+  }
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_scatter_v(const __grid_constant__ PartSpec s,
+                                                                 const int64_t* __restrict__ offs, int max_w) {
+  extern __shared__ __align__(16) uint8_t sbuf[];  // kVsTile * max_w
+  __shared__ int64_t cursor[1 << kMaxPartBits];
+  __shared__ int cnt[1 << kMaxPartBits];
+  __shared__ int start[1 << kMaxPartBits];
+  __shared__ uint16_t s_part[kVsTile];
+  __shared__ int s_warp[kPartThreads / 32];
+  const int P = 1 << s.bits;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned lt = lanemask_lt();
+  for (int p = tid; p < P; p += kPartThreads) cursor[p] = offs[(int64_t)p * gridDim.x + blockIdx.x];
+  const int64_t lo = blockIdx.x * s.chunk, hi = min(s.n, lo + s.chunk);
+  for (int64_t base = lo; base < hi; base += kVsTile) {
+    for (int p = tid; p < P; p += kPartThreads) cnt[p] = 0;
+    __syncthreads();
+    int32_t row[kVsItems];
+    int part[kVsItems], rank[kVsItems];
+#pragma unroll
+    for (int i = 0; i < kVsItems; ++i) {
+      const int64_t idx = base + (int64_t)i * kPartThreads + tid;
+      const bool v = idx < hi;
+      row[i] = v ? (s.sel ? __ldg(s.sel + idx) : (int32_t)idx) : 0;
+      const int p = v ? (int)part_of(part_key(s.k0, s.k1, s.nkeys, row[i]), s.bits) : (1 << kMaxPartBits) + lane;
+      const unsigned peers = __match_any_sync(kFull, p);
+      const int leader = __ffs(peers) - 1;
+      int b = 0;
+      if (v && lane == leader) b = atomicAdd(&cnt[p], __popc(peers));
+      b = __shfl_sync(kFull, b, leader);
+      part[i] = v ? p : -1;
+      rank[i] = b + __popc(peers & lt);
+    }
+    __syncthreads();
+    {
+      constexpr int kPer = (1 << kMaxPartBits) / kPartThreads;
+      int loc[kPer], sum = 0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int p = tid * kPer + j;
+        loc[j] = p < P ? cnt[p] : 0;
+        sum += loc[j];
+      }
+      int x = sum;
+      const int w = tid >> 5;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_warp[w] = x;
+      __syncthreads();
+      int wo = 0;
+      for (int k = 0; k < w; ++k) wo += s_warp[k];
+      int run = wo + x - sum;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int p = tid * kPer + j;
+        if (p < P) start[p] = run;
+        run += loc[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kVsItems; ++i) {
+      if (part[i] < 0) continue;
+      rank[i] += start[part[i]];  // now the tile-local position
+      s_part[rank[i]] = (uint16_t)part[i];
+    }
+    const int tcount = (int)min((int64_t)kVsTile, hi - base);
+    const int ncols = s.ncarry + (s.out_rowid ? 1 : 0);
+    for (int c = 0; c < ncols; ++c) {
+      const bool rid = c == s.ncarry;
+      const int w = rid ? 4 : s.width[c];
+#pragma unroll
+      for (int i = 0; i < kVsItems; ++i) {
+        if (part[i] < 0) continue;
+        if (rid) ((int32_t*)sbuf)[rank[i]] = row[i];
+        else stage_val(s.carry[c], w, sbuf, rank[i], row[i]);
+      }
+      __syncthreads();
+      void* dst = rid ? (void*)s.out_rowid : s.out[c];
+      for (int j = tid; j < tcount; j += kPartThreads) {
+        const int p = s_part[j];
+        emit_val(w, sbuf, j, dst, cursor[p] + (j - start[p]));
+      }
+      __syncthreads();
+    }
+    for (int p = tid; p < P; p += kPartThreads) cursor[p] += cnt[p];
+    __syncthreads();
+  }
+}
+
 // Partition rows (n, through sel) by hash bits; carried columns land partition-contiguous.
 // offsets_h (host, P+1) receives the partition boundaries.
 sx_status radix_partition(sx_ctx* ctx, PartSpec& s, int64_t* offsets_h) {
   const int P = 1 << s.bits;
-  int64_t tiles = (s.n + kPartTile - 1) / kPartTile;
+  // SX_PART_SCATTER=rowid: the round-1 scatter (row ids staged, values re-gathered at write time)
+  const bool v2 = !(getenv("SX_PART_SCATTER") && std::strcmp(getenv("SX_PART_SCATTER"), "rowid") == 0);
+  const int tile_rows = v2 ? kVsTile : kPartTile;
+  int max_w = 4;
+  for (int c = 0; c < s.ncarry; ++c) max_w = std::max(max_w, s.width[c]);
+  const size_t vsmem = (size_t)kVsTile * max_w;
+  int64_t tiles = (s.n + tile_rows - 1) / tile_rows;
   unsigned grid = persistent_grid(ctx, 4, tiles > 0 ? tiles : 1);
   int64_t tiles_per = (tiles + grid - 1) / grid;
-  s.chunk = std::max<int64_t>(1, tiles_per) * kPartTile;
+  s.chunk = std::max<int64_t>(1, tiles_per) * tile_rows;
   grid = (unsigned)std::max<int64_t>(1, (s.n + s.chunk - 1) / s.chunk);
   Scratch scr(ctx);
   int32_t* hist;
@@ -182,7 +314,12 @@ sx_status radix_partition(sx_ctx* ctx, PartSpec& s, int64_t* offsets_h) {
     k_part_hist<<<grid, kPartThreads, 0, SX_STREAM(ctx)>>>(s, hist);
     SX_CHECK_LAUNCH();
     SX_TRY(scan_counts(ctx, hist, m, offs, &total));
-    k_part_scatter<<<grid, kPartThreads, 0, SX_STREAM(ctx)>>>(s, offs);
+    if (v2) {
+      SX_CUDA(cudaFuncSetAttribute(k_part_scatter_v, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsmem));
+      k_part_scatter_v<<<grid, kPartThreads, vsmem, SX_STREAM(ctx)>>>(s, offs, max_w);
+    } else {
+      k_part_scatter<<<grid, kPartThreads, 0, SX_STREAM(ctx)>>>(s, offs);
+    }
     SX_CHECK_LAUNCH();
     std::vector<int64_t> all((size_t)m + 1);
     SX_CUDA(cudaMemcpyAsync(all.data(), offs, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, ctx->stream));
@@ -333,6 +470,156 @@ __global__ void __launch_bounds__(kBlock, 4) k_pj_probe(const __grid_constant__ 
       for (int g = 0; g < a.npay; ++g)
         copy_val_cs(a.pay_src[g], a.pay_w[g], a.pay_dst[g], pos, a.pay_build[g] ? jb[i] : jp);
       ++pos;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- inline-value partitioned join (K8i) ---------------------------------------------------
+// When each side carries at most ONE value to the output (a payload column of width <= 8, or the
+// row id), the build value lives in the slot beside its key — {key64, value} — so a probe is one
+// 16-byte L2 load and the output needs no second (dependent) access into the build side.  The key
+// ~0 is the EMPTY marker; a build key equal to ~0 is kept in a side cell instead.  Output:
+// per-CTA tile of kPiTile probes, hits staged in shared memory in probe order and written as one
+// contiguous run claimed with a single atomic per tile (join output order is unspecified, R12).
+struct PJoinI {
+  const void* bkey;
+  const void* pkey;
+  int kb;
+  int bits;
+  int p0;
+  uint64_t cap;
+  ulonglong2* slots;
+  int64_t b_lo, b_hi, p_lo, p_hi;
+  DCol bval;  // partitioned build value (width <= 8), or row ids
+  DCol pval;  // partitioned probe value, or row ids; p == nullptr: none
+  int bw, pw;  // output widths (0: not produced)
+  unsigned long long* cursor;
+  unsigned long long* side;  // [0] 1 when the key ~0 is in the build, [1] its value
+  void* out_b;
+  void* out_p;
+};
+
+__device__ __forceinline__ int64_t ld_val_cs(const DCol& c, int64_t j) {
+  switch (c.type) {
+    case SX_U8: return (int64_t)__ldcs((const uint8_t*)c.p + j);
+    case SX_I64:
+    case SX_DEC64:
+      return (int64_t)__ldcs((const long long*)c.p + j);
+    default: return (int64_t)__ldcs((const int32_t*)c.p + j);
+  }
+}
+__device__ __forceinline__ void st_val(void* dst, int w, int64_t d, int64_t v) {
+  switch (w) {
+    case 1: ((uint8_t*)dst)[d] = (uint8_t)v; break;
+    case 4: __stcs((int32_t*)dst + d, (int32_t)v); break;
+    default: __stcs((long long*)dst + d, (long long)v); break;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_pji_build(const __grid_constant__ PJoinI a) {
+  for (int64_t j = a.b_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.b_hi;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = pj_key(a.bkey, a.kb, j);
+    const int64_t val = ld_val_cs(a.bval, j);
+    if (key == ~0ull) {
+      a.side[1] = (unsigned long long)val;
+      a.side[0] = 1ull;
+      continue;
+    }
+    const uint64_t h = hash64(key);
+    ulonglong2* t = a.slots + (uint64_t)(((uint32_t)(h >> kPartShift) & ((1u << a.bits) - 1u)) - a.p0) * a.cap;
+    uint64_t s = h & (a.cap - 1);
+    while (atomicCAS(&t[s].x, ~0ull, key) != ~0ull) s = (s + 1) & (a.cap - 1);
+    t[s].y = (unsigned long long)val;
+  }
+}
+
+constexpr int kPiItems = 8;
+constexpr int kPiTile = kBlock * kPiItems;
+__global__ void __launch_bounds__(kBlock, 2) k_pji_probe(const __grid_constant__ PJoinI a) {
+  __shared__ long long s_b[kPiTile];
+  __shared__ long long s_p[kPiTile];
+  __shared__ int s_warp[kBlock / 32];
+  __shared__ unsigned long long s_base;
+  __shared__ int s_tot;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool side_on = a.side[0] != 0;
+  const long long side_v = (long long)a.side[1];
+  for (int64_t base = a.p_lo + blockIdx.x * (int64_t)kPiTile; base < a.p_hi; base += (int64_t)gridDim.x * kPiTile) {
+    // idx: global slot index (region base | in-region slot; regions are cap-aligned)
+    uint64_t key[kPiItems], idx[kPiItems];
+    long long pv[kPiItems], bv[kPiItems];
+    bool pend[kPiItems], hit[kPiItems];
+    const uint64_t m = a.cap - 1;
+#pragma unroll
+    for (int i = 0; i < kPiItems; ++i) {
+      const int64_t j = base + (int64_t)i * kBlock + threadIdx.x;
+      const bool v = j < a.p_hi;
+      key[i] = v ? pj_key(a.pkey, a.kb, j) : ~0ull;
+      pv[i] = (v && a.pw) ? ld_val_cs(a.pval, j) : 0;
+      const uint64_t h = hash64(key[i]);
+      idx[i] = (uint64_t)(((uint32_t)(h >> kPartShift) & ((1u << a.bits) - 1u)) - a.p0) * a.cap + (h & m);
+      hit[i] = v && key[i] == ~0ull && side_on;
+      bv[i] = side_v;
+      pend[i] = v && key[i] != ~0ull;
+      if (!pend[i]) idx[i] = 0;
+    }
+    bool any = true;
+    while (any) {
+      any = false;
+      ulonglong2 sv[kPiItems];
+#pragma unroll
+      for (int i = 0; i < kPiItems; ++i) sv[i] = pend[i] ? __ldg(a.slots + idx[i]) : make_ulonglong2(~0ull, 0ull);
+#pragma unroll
+      for (int i = 0; i < kPiItems; ++i) {
+        if (!pend[i]) continue;
+        if (sv[i].x == key[i]) {
+          hit[i] = true;
+          bv[i] = (long long)sv[i].y;
+          pend[i] = false;
+        } else if (sv[i].x == ~0ull) {
+          pend[i] = false;
+        } else {
+          idx[i] = (idx[i] & ~m) | ((idx[i] + 1) & m);
+          any = true;
+        }
+      }
+    }
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < kPiItems; ++i) c += hit[i];
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int k = 0; k < kBlock / 32; ++k) tot += s_warp[k];
+      s_base = tot ? atomicAdd(a.cursor, (unsigned long long)tot) : 0ull;
+      s_tot = tot;
+    }
+    int wo = 0;
+    for (int k = 0; k < w; ++k) wo += s_warp[k];
+    __syncthreads();
+    const int tot = s_tot;
+    int pos = wo + x - c;
+#pragma unroll
+    for (int i = 0; i < kPiItems; ++i) {
+      if (!hit[i]) continue;
+      s_b[pos] = bv[i];
+      s_p[pos] = pv[i];
+      ++pos;
+    }
+    __syncthreads();
+    const int64_t ob = (int64_t)s_base;
+    for (int k = threadIdx.x; k < tot; k += kBlock) {
+      if (a.bw) st_val(a.out_b, a.bw, ob + k, s_b[k]);
+      if (a.pw) st_val(a.out_p, a.pw, ob + k, s_p[k]);
     }
     __syncthreads();
   }
@@ -514,6 +801,103 @@ SX_EXPORT sx_status sx_hash_join(sx_ctx* ctx, const sx_col* build_cols, int nbui
   }
   // outputs (unique build: at most one match per probe row)
   const size_t ocap = (size_t)(np > 0 ? np : 1);
+  // inline-value path (K8i): each side carries at most one value of width <= 8 (a payload column
+  // or its row ids); SX_PJ_INLINE=0 forces the row-id path below
+  auto carry_ok = [&](int npay, const sx_col* cols, const int32_t* pay, bool rows) {
+    if (npay == 0) return true;
+    return npay == 1 && !rows && type_width(cols[pay[0]].type) <= 8;
+  };
+  const bool inline_off = getenv("SX_PJ_INLINE") && getenv("SX_PJ_INLINE")[0] == '0';
+  if (!inline_off && carry_ok(nbp, build_cols, bp, out_build != nullptr) &&
+      carry_ok(npp, probe_cols, pp, out_probe != nullptr)) {
+    PJoinI a{};
+    a.bkey = bkey;
+    a.pkey = pkey;
+    a.kb = kb;
+    a.bits = bits;
+    void* ob_out = nullptr;
+    void* op_out = nullptr;
+    if (nbp == 1) {
+      a.bval = DCol{bs.out[nkeys], build_cols[bp[0]].type, 0};
+      a.bw = bs.width[nkeys];
+    } else if (out_build) {
+      a.bval = DCol{bs.out_rowid, SX_I32, 0};
+      a.bw = 4;
+    }
+    if (npp == 1) {
+      a.pval = DCol{psp.out[nkeys], probe_cols[pp[0]].type, 0};
+      a.pw = psp.width[nkeys];
+    } else if (out_probe) {
+      a.pval = DCol{psp.out_rowid, SX_I32, 0};
+      a.pw = 4;
+    }
+    if (a.bw) SX_TRY(scr.get((char**)&ob_out, ocap * a.bw));
+    if (a.pw) SX_TRY(scr.get((char**)&op_out, ocap * a.pw));
+    a.out_b = ob_out;
+    a.out_p = op_out;
+    unsigned long long* side;
+    SX_TRY(scr.get(&side, 2));
+    SX_CUDA(cudaMemsetAsync(side, 0, 16, ctx->stream));
+    a.side = side;
+    a.cursor = (unsigned long long*)ctx->d_counters;
+    SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
+    int64_t maxb = 1;
+    for (int p = 0; p < P; ++p) maxb = std::max<int64_t>(maxb, boff[p + 1] - boff[p]);
+    uint64_t cap = 64;
+    while (cap < (uint64_t)(2 * maxb)) cap <<= 1;
+    const size_t part_bytes = cap * sizeof(ulonglong2);
+    const int l2div = getenv("SX_PJ_L2DIV") ? std::max(1, atoi(getenv("SX_PJ_L2DIV"))) : 3;
+    int W = (int)std::max<size_t>(1, (ctx->l2_bytes / l2div) / part_bytes);
+    W = std::min(W, P);
+    ulonglong2* slots;
+    SX_TRY(scr.get(&slots, (size_t)W * cap));
+    a.slots = slots;
+    a.cap = cap;
+    for (int p0 = 0; p0 < P; p0 += W) {
+      const int p1 = std::min(P, p0 + W);
+      a.p0 = p0;
+      a.b_lo = boff[p0];
+      a.b_hi = boff[p1];
+      a.p_lo = poff[p0];
+      a.p_hi = poff[p1];
+      if (a.b_hi == a.b_lo || a.p_hi == a.p_lo) continue;
+      SX_CUDA(cudaMemsetAsync(slots, 0xff, (size_t)(p1 - p0) * cap * sizeof(ulonglong2), ctx->stream));
+      const int64_t nbw = a.b_hi - a.b_lo, npw = a.p_hi - a.p_lo;
+      k_pji_build<<<persistent_grid(ctx, 8, (nbw + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+      k_pji_probe<<<persistent_grid(ctx, 4, (npw + kPiTile - 1) / kPiTile), kBlock, 0, SX_STREAM(ctx)>>>(a);
+      SX_CHECK_LAUNCH();
+      SX_CUDA(cudaMemsetAsync(side, 0, 16, ctx->stream));  // the side cell belongs to one wave
+    }
+    int64_t count = 0;
+    SX_TRY(read_i64(ctx, a.cursor, &count));
+    if (nbp == 1) {
+      out_payload[0] = build_cols[bp[0]];
+      out_payload[0].len = count;
+      out_payload[0].data = ob_out;
+      out_payload[0].offsets = nullptr;
+      scr.release(ob_out);
+    } else if (out_build) {
+      *out_build = sx_sel{count, (int32_t*)ob_out};
+      scr.release(ob_out);
+    }
+    if (npp == 1) {
+      out_payload[nbp] = probe_cols[pp[0]];
+      out_payload[nbp].len = count;
+      out_payload[nbp].data = op_out;
+      out_payload[nbp].offsets = nullptr;
+      scr.release(op_out);
+    } else if (out_probe) {
+      *out_probe = sx_sel{count, (int32_t*)op_out};
+      scr.release(op_out);
+    }
+    double kbytes = 0;
+    for (int k = 0; k < nkeys; ++k) kbytes += type_width(build_cols[build_keys[k]].type);
+    double b = (kbytes + (build_sel ? 4.0 : 0.0)) * nb + (kbytes + (probe_sel ? 4.0 : 0.0)) * np;
+    b += 2.0 * (nbp ? a.bw : 0) * count + 2.0 * (npp ? a.pw : 0) * count;
+    b += ((out_probe ? 4.0 : 0.0) + (out_build ? 4.0 : 0.0)) * count;
+    ps.set_bytes(b);
+    return SX_OK;
+  }
   int32_t *op = nullptr, *ob = nullptr;
   if (out_probe) SX_TRY(scr.get(&op, ocap));
   if (out_build) SX_TRY(scr.get(&ob, ocap));

@@ -336,6 +336,214 @@ __global__ void __launch_bounds__(kLsdThreads) k_lsd_scatter(const __grid_consta
   }
 }
 
+// ---- onesweep LSD radix sort (K13o) ---------------------------------------------------
+// One histogram pass over every varying digit up front (K13h), a 256-way exclusive scan per
+// digit, then ONE kernel per digit pass (K13s): a CTA claims the next tile (atomic ticket, so
+// every predecessor is already resident), ranks its rows exactly as k_lsd_scatter does, publishes
+// its per-digit counts and resolves its per-digit global offsets by decoupled look-back over the
+// predecessors' published counts (Merrill & Garland's chained scan, per digit), then scatters.
+// No count pass and no separate scan per digit pass: each pass reads the words once and writes
+// them once.  Status words are [63:32] tag | [31:0] count, tag = 2q+1 (aggregate) / 2q+2
+// (inclusive prefix) for pass q, so one zero-fill serves every pass of a sort.
+constexpr int kOsMaxDigits = 32;
+struct OsHist {
+  const uint32_t* w[kOsMaxDigits];
+  int shift[kOsMaxDigits];
+  int ndig;
+  int64_t n;
+  unsigned* hist;  // [ndig][256]
+};
+
+__global__ void __launch_bounds__(kLsdThreads) k_os_hist(const __grid_constant__ OsHist a) {
+  extern __shared__ unsigned h[];  // [ndig][256]
+  for (int i = threadIdx.x; i < a.ndig * 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t* pw = nullptr;
+    uint32_t v = 0;
+    for (int d = 0; d < a.ndig; ++d) {
+      if (a.w[d] != pw) {
+        pw = a.w[d];
+        v = __ldcs(pw + i);
+      }
+      atomicAdd(&h[d * 256 + ((v >> a.shift[d]) & 0xff)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.ndig * 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&a.hist[i], h[i]);
+}
+
+// exclusive scan of each digit's 256 counts (one CTA per digit)
+__global__ void __launch_bounds__(256) k_os_scan(unsigned* hist) {
+  __shared__ unsigned s[256];
+  unsigned* hd = hist + blockIdx.x * 256;
+  const int t = threadIdx.x;
+  const unsigned v = hd[t];
+  s[t] = v;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const unsigned x = t >= o ? s[t - o] : 0u;
+    __syncthreads();
+    s[t] += x;
+    __syncthreads();
+  }
+  hd[t] = s[t] - v;
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kLsdThreads) k_onesweep(const __grid_constant__ Words src,
+                                                          const __grid_constant__ Words dst, int dword, int shift,
+                                                          int64_t n, const unsigned* __restrict__ dbase,
+                                                          unsigned long long* status, unsigned* ticket, unsigned pass,
+                                                          int pos_only) {
+  constexpr int T = kLsdThreads * ITEMS;
+  extern __shared__ uint32_t stage[];  // [nwords][T]
+  __shared__ int wcnt[kLsdWarps][256];
+  __shared__ int dstart[256];
+  __shared__ int64_t s_off[256];
+  __shared__ int s_warp[kLsdWarps];
+  __shared__ uint8_t sdig[T];
+  __shared__ unsigned s_tile;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = src.nwords;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  for (int j = threadIdx.x; j < kLsdWarps * 256; j += kLsdThreads) (&wcnt[0][0])[j] = 0;
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * (int64_t)T;
+  int dig[ITEMS], rank[ITEMS];
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t e = base + (int64_t)w * 32 * ITEMS + i * 32 + lane;
+    const bool v = e < n;
+    const int d = v ? (int)((__ldg(src.w[dword] + e) >> shift) & 0xff) : 256 + lane;
+    const unsigned peers = __match_any_sync(kFull, d);
+    const int leader = __ffs(peers) - 1;
+    int r = 0;
+    if (v) r = wcnt[w][d] + __popc(peers & lt);
+    __syncwarp();
+    if (v && lane == leader) wcnt[w][d] += __popc(peers);
+    __syncwarp();
+    dig[i] = v ? d : -1;
+    rank[i] = r;
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;  // kLsdThreads == 256 digits
+    int run = 0;
+#pragma unroll
+    for (int q = 0; q < kLsdWarps; ++q) {
+      const int c = wcnt[q][d];
+      wcnt[q][d] = run;
+      run += c;
+    }
+    // publish this tile's count of digit d (inclusive already for tile 0)
+    const unsigned long long agg_tag = (unsigned long long)(2u * pass + 1u) << 32;
+    const unsigned long long inc_tag = (unsigned long long)(2u * pass + 2u) << 32;
+    unsigned long long* st = status + tile * 256 + d;
+    st_relaxed(st, (tile == 0 ? inc_tag : agg_tag) | (unsigned)run);
+    int x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    int wo = 0;
+    for (int q = 0; q < w; ++q) wo += s_warp[q];
+    dstart[d] = wo + x - run;
+    // look-back over the predecessors' counts of digit d
+    int64_t excl = 0;
+    if (tile > 0) {
+      for (int64_t j = tile - 1;; --j) {
+        unsigned long long sw;
+        do {
+          sw = ld_relaxed(status + j * 256 + d);
+        } while ((sw >> 32) < (2u * pass + 1u));
+        excl += (uint32_t)sw;
+        if ((sw >> 32) == (2u * pass + 2u)) break;
+      }
+      st_relaxed(st, inc_tag | (unsigned)(excl + run));
+    }
+    s_off[d] = (int64_t)dbase[d] + excl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (dig[i] < 0) continue;
+    const int64_t e = base + (int64_t)w * 32 * ITEMS + i * 32 + lane;
+    const int pos = dstart[dig[i]] + wcnt[w][dig[i]] + rank[i];
+    sdig[pos] = (uint8_t)dig[i];
+    if (pos_only) {
+      stage[pos] = __ldg(src.w[nw - 1] + e);
+    } else {
+      for (int j = 0; j < nw; ++j) stage[j * T + pos] = __ldg(src.w[j] + e);
+    }
+  }
+  __syncthreads();
+  const int tcount = (int)min((int64_t)T, n - base);
+  if (pos_only) {
+    for (int p = threadIdx.x; p < tcount; p += kLsdThreads) {
+      const int d = sdig[p];
+      __stcs(dst.w[nw - 1] + s_off[d] + (p - dstart[d]), stage[p]);
+    }
+  } else {
+    for (int p = threadIdx.x; p < tcount; p += kLsdThreads) {
+      const int d = sdig[p];
+      const int64_t g = s_off[d] + (p - dstart[d]);
+      for (int j = 0; j < nw; ++j) __stcs(dst.w[j] + g, stage[j * T + p]);
+    }
+  }
+}
+
+template <int ITEMS>
+sx_status onesweep_sort(sx_ctx* ctx, Scratch& scr, Words*& a, Words*& b, int nwords, int64_t n,
+                        const std::vector<std::pair<int, int>>& digits) {
+  constexpr int T = kLsdThreads * ITEMS;
+  const int64_t ntiles = (n + T - 1) / T;
+  // sort digits, least significant first (the position word is carried, never sorted on)
+  std::vector<std::pair<int, int>> pass;
+  for (int p = (int)digits.size() - 1; p >= 0; --p)
+    if (digits[p].first != nwords - 1) pass.push_back(digits[p]);
+  const int np = (int)pass.size();
+  if (np == 0) return SX_OK;
+  if (np > kOsMaxDigits) return set_err(ctx, SX_EINVAL, "sort key has %d digits", np);
+  unsigned* hist;
+  unsigned long long* status;
+  unsigned* tickets;
+  SX_TRY(scr.get(&hist, (size_t)np * 256));
+  SX_TRY(scr.get(&status, (size_t)ntiles * 256));
+  SX_TRY(scr.get(&tickets, (size_t)np));
+  SX_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned) * np * 256, ctx->stream));
+  SX_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ntiles * 256, ctx->stream));
+  SX_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * np, ctx->stream));
+  OsHist h{};
+  for (int q = 0; q < np; ++q) {
+    h.w[q] = a->w[pass[q].first];
+    h.shift[q] = pass[q].second;
+  }
+  h.ndig = np;
+  h.n = n;
+  h.hist = hist;
+  const size_t hsm = (size_t)np * 256 * sizeof(unsigned);
+  k_os_hist<<<persistent_grid(ctx, 4, (n + kLsdThreads - 1) / kLsdThreads), kLsdThreads, hsm, SX_STREAM(ctx)>>>(h);
+  SX_CHECK_LAUNCH();
+  k_os_scan<<<np, 256, 0, SX_STREAM(ctx)>>>(hist);
+  SX_CHECK_LAUNCH();
+  const size_t smem = (size_t)nwords * T * sizeof(uint32_t);
+  SX_CUDA(cudaFuncSetAttribute(k_onesweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int q = 0; q < np; ++q) {
+    const int pos_only = q == np - 1;  // the last pass only needs the positions in order
+    k_onesweep<ITEMS><<<(unsigned)ntiles, kLsdThreads, smem, SX_STREAM(ctx)>>>(
+        *a, *b, pass[q].first, pass[q].second, n, hist + q * 256, status, tickets + q, (unsigned)q, pos_only);
+    SX_CHECK_LAUNCH();
+    std::swap(a, b);
+  }
+  return SX_OK;
+}
+
 template <int ITEMS>
 sx_status lsd_sort(sx_ctx* ctx, Scratch& scr, Words*& a, Words*& b, int nwords, int64_t n,
                    const std::vector<std::pair<int, int>>& digits) {
@@ -519,9 +727,17 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
     for (int j = 0; j < nwords; ++j) SX_TRY(scr.get(&W2.w[j], (size_t)n));
     Words* a = &W;
     Words* b = &W2;
-    if (nwords <= 3) SX_TRY(lsd_sort<16>(ctx, scr, a, b, nwords, n, digits));
-    else if (nwords <= 6) SX_TRY(lsd_sort<8>(ctx, scr, a, b, nwords, n, digits));
-    else SX_TRY(lsd_sort<4>(ctx, scr, a, b, nwords, n, digits));
+    // onesweep (default) or the count + scan + scatter LSD passes (SX_SORT=lsd, kept for A/B)
+    const bool lsd = getenv("SX_SORT") && std::strcmp(getenv("SX_SORT"), "lsd") == 0;
+    if (lsd) {
+      if (nwords <= 3) SX_TRY(lsd_sort<16>(ctx, scr, a, b, nwords, n, digits));
+      else if (nwords <= 6) SX_TRY(lsd_sort<8>(ctx, scr, a, b, nwords, n, digits));
+      else SX_TRY(lsd_sort<4>(ctx, scr, a, b, nwords, n, digits));
+    } else {
+      if (nwords <= 3) SX_TRY(onesweep_sort<16>(ctx, scr, a, b, nwords, n, digits));
+      else if (nwords <= 6) SX_TRY(onesweep_sort<8>(ctx, scr, a, b, nwords, n, digits));
+      else SX_TRY(onesweep_sort<4>(ctx, scr, a, b, nwords, n, digits));
+    }
     // positions (last word) of the first outn sorted rows -> row ids
     GatherSpec none;
     none.n = 0;

@@ -487,16 +487,6 @@ struct Q18Prog {
 #pragma unroll
     for (int i = 0; i < I; ++i) v[i] = c.q[i];
   }
-  // Ring interface (K10rr, k_runs_ring): 2048-row tiles of (l_orderkey, l_quantity), 6 stages
-  // (147 KB with int32 keys), 16 consumer warps x 128 rows.
-  using KeyT = KT;
-  static constexpr int kRingCols = 2;
-  static constexpr int kRingTile = 2048;
-  static constexpr int kRingStages = 6;
-  static constexpr int kRingConsumers = 16;
-  static constexpr size_t kRingExtraBytes = 0;
-  __host__ __device__ static constexpr int ring_width(int c) { return c == 0 ? (int)sizeof(KT) : 8; }
-  __host__ __device__ const void* ring_col(int c) const { return c == 0 ? (const void*)okey : (const void*)qty; }
   // Dense rows for k_runs_own: R consecutive rows (r0 % R == 0) with 128-bit streaming loads.
   static constexpr bool kDenseRuns = true;
   template <int R>

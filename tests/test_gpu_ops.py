@@ -339,6 +339,22 @@ def test_topk_paths(ctx, monkeypatch, mode):
         assert np.array_equal(perm.cpu().numpy(), want), k
 
 
+@pytest.mark.parametrize("mode", ["onesweep", "lsd"])
+def test_sort_many_tiles(ctx, monkeypatch, mode):
+    """Full sorts spanning ~500 onesweep tiles (decoupled look-back chains across many CTAs):
+    full-range int64 keys (all 8 digits vary), and heavy ties resolved by stability."""
+    if mode == "lsd":
+        monkeypatch.setenv("SX_SORT", "lsd")
+    rng = np.random.default_rng(21)
+    n = 2_000_003
+    v = rng.integers(-(2**63), 2**63 - 1, n, dtype=np.int64)
+    perm = ctx.sort_topk([c(dev(v))], [(0, 0)], -1)
+    assert np.array_equal(perm.cpu().numpy(), oracle.sort([v.tolist()], [0], -1))
+    t = rng.integers(0, 3, n).astype(np.int32)
+    perm = ctx.sort_topk([sx.col(dev(t), A.SX_I32)], [(0, 1)], -1)
+    assert np.array_equal(perm.cpu().numpy(), oracle.sort([t.tolist()], [1], -1))
+
+
 def test_sort_with_sel(ctx):
     rng = np.random.default_rng(8)
     n = 20_000

@@ -86,38 +86,6 @@ def test_q18_group_strategies(small, monkeypatch, mode):
         assert rows_equal(got, want), diff_rows(got, want)
 
 
-@pytest.mark.parametrize("case", ["tails", "run60", "run200", "big", "unsorted", "ring-off"])
-def test_q18_ring(ctx, monkeypatch, case):
-    """Q18's owned-run aggregation over the tile ring (K10rr, forced with SX_GB_SORTED=2 at SF 0.1 so
-    that >= 2048 rows per SM stream): a ragged last tile, a 60-row run crossing warps (suffix scan
-    + lane 31's continuation), a 200-row run (past kRunAhead: the host retries with K10r), a
-    quantity >= 2^40 (int64 fast path refused), an unsorted key column (hashing), and SX_RING=0."""
-    monkeypatch.setenv("SX_GB_SORTED", "2")
-    if case == "ring-off":
-        monkeypatch.setenv("SX_RING", "0")
-    host = gen.cpu_tables(100, seed=13)
-    li = {k: v.copy() for k, v in host["lineitem"].items()}
-    n = len(li["l_orderkey"]) - (1111 if case == "tails" else 0)
-    li = {k: v[:n].copy() for k, v in li.items()}
-    ok = li["l_orderkey"]
-    if case in ("run60", "run200"):
-        L = 60 if case == "run60" else 200
-        for start in (4096 * 7 + 100, 2048 * 40 - 30, n - L):  # inside a tile, across tiles, at the end
-            ok[start:start + L] = ok[start]
-    if case == "big":
-        li["l_quantity"][[5, 70_000, n - 1]] = 1 << 41
-    if case == "unsorted":
-        ok[[1000, 1001]] = ok[[1001, 1000]] if ok[1000] != ok[1001] else (ok[1000], ok[1000] - 1)
-        ok[300_000], ok[300_001] = ok[300_001], ok[300_000]
-    host = dict(host)
-    host["lineitem"] = li
-    T = tpch.Tpch(ctx, to_dev(host))
-    for over in ({}, dict(q18_qty_gt=15000)):
-        got = T.run("q18", tpch.default_params(**over))
-        want = oracle.run_query("q18", host, oracle.default_params(**over))
-        assert rows_equal(got, want), diff_rows(got, want)
-
-
 def test_gpu_generator_matches_cpu_generator():
     cpu = gen.cpu_tables(10, seed=42)
     g = gen.gpu_tables(10, seed=42)
