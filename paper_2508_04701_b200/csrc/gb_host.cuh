@@ -501,6 +501,94 @@ __global__ void __launch_bounds__(kBlock, 4) k_runs_own_dense(const __grid_const
   if (ovf) atomicExch(prog.ovf_flag, 1);
 }
 
+// K10l: lean owned runs for 32-bit keys and one int64 SUM whose values are < 2^40 in magnitude
+// (programs with kLeanRuns: Q18).  Same ownership rule as K10r (a thread owns the groups whose
+// first row lies among its 8 rows; the next lane's leading rows finish its last group), but the
+// per-row work is branch-free 32-bit key compares and selects with int64 run sums: K10r's
+// generic form executes ~100 instructions per row (round-1 ncu: 1.93e9 warp instructions for
+// 6e8 rows, issue-bound at 2.8 ms).  The previous key comes from the neighbouring lane.  Rare
+// cases go to flags: flags[0] a decreasing key (unsorted: host hashes), flags[1] a value >= 2^40
+// or a run longer than kRunAhead rows past its thread (host reruns K10r).
+template <class P, class = void>
+struct has_lean_runs : std::false_type {};
+template <class P>
+struct has_lean_runs<P, std::void_t<decltype(P::kLeanRuns)>> : std::integral_constant<bool, P::kLeanRuns> {};
+
+template <class P>
+__global__ void __launch_bounds__(kBlock, 4) k_runs_lean(const __grid_constant__ P prog, int64_t n,
+                                                      const __grid_constant__ Layout L,
+                                                      const __grid_constant__ SlotFn hv, uint8_t* __restrict__ out,
+                                                      int64_t cap_out, unsigned long long* cursor, int* flags) {
+  constexpr int R = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
+  const int hv_op = hv.hv_op, o8 = L.off8[0], o4 = L.off4[0], sb = L.slot_bytes;
+  const long long hv_lo = hv.hv_lo, hv_hi = hv.hv_hi;
+  unsigned bad = 0, wide = 0;
+  auto emit = [&](int32_t gk, long long s) {
+    if (!cmp(hv_op, s, hv_lo, hv_hi)) return;
+    const unsigned long long pos = atomicAdd(cursor, 1ull);
+    if ((int64_t)pos < cap_out) {
+      uint8_t* d = out + pos * sb;
+      *(int32_t*)d = gk;
+      *(long long*)(d + o8) = s;
+      *(int*)(d + o4) = s < 0 ? -1 : 0;
+    }
+  };
+  for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R; wbase < n; wbase += stride) {
+    const int64_t r0 = wbase + (int64_t)lane * R;
+    int32_t k[R];
+    long long v[R];
+    prog.lean_load(r0, n, k, v);  // rows >= n: v = 0, k = 0 (masked by m below)
+    const int m = (int)max((int64_t)0, min((int64_t)R, n - r0));
+    int32_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
+    if (lane == 0 && r0 > 0 && r0 <= n) pk = prog.lean_key(r0 - 1);
+    const bool has_prev = r0 > 0;
+    long long lead = 0, s = 0;
+    int lead_len = 0;
+    bool open = false;
+    int32_t ck = 0, prev = pk;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const bool in = i < m;
+      wide |= in ? (unsigned)((int32_t)(v[i] >> 32) + 256) >> 9 : 0u;  // |v| >= 2^40
+      const bool head = in && (k[i] != prev || (i == 0 && !has_prev));
+      bad |= (in && (i > 0 || has_prev) && k[i] < prev) ? 1u : 0u;
+      if (head && open) emit(ck, s);
+      open = open || head;
+      lead += (in && !open) ? v[i] : 0;
+      lead_len += (in && !open) ? 1 : 0;
+      s = head ? v[i] : s + v[i];
+      ck = head ? k[i] : ck;
+      prev = in ? k[i] : prev;
+    }
+    // the next lane's leading rows continue my last group
+    const long long nx_lead = __shfl_down_sync(kFull, lead, 1);
+    const int nx_len = __shfl_down_sync(kFull, lead_len, 1);
+    if (open) {
+      const int64_t nxt = r0 + R;
+      bool more = true;
+      int64_t r = nxt;
+      if (lane < 31 && nxt < n) {
+        s += nx_lead;
+        more = nx_len == R;
+        r = nxt + R;
+      }
+      int steps = 0;
+      for (; more && r < n && steps < kRunAhead; ++r, ++steps) {  // rare: scalar continuation
+        if (prog.lean_key(r) != ck) break;
+        const long long x = prog.lean_val(r);
+        wide |= (unsigned)((int32_t)(x >> 32) + 256) >> 9;
+        s += x;
+      }
+      if (more && steps == kRunAhead && r < n) wide = 1;
+      emit(ck, s);
+    }
+  }
+  if (bad) atomicExch(flags, 1);
+  if (wide) atomicExch(flags + 1, 1);
+}
+
 struct EmitArgs {
   const uint8_t* slots;
   const int32_t* ids;
@@ -719,13 +807,25 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
         hv.hv_hi = P.hv.hi;
         int64_t cap_out = std::max<int64_t>(1 << 16, n / 256);
         unsigned long long* cursor = (unsigned long long*)ctx->d_counters;
+        bool lean_failed = false;
         for (int attempt = 0; attempt < 2 && !own_done; ++attempt) {
           uint8_t* out;
           SX_TRY(scr.get(&out, (size_t)cap_out * L.slot_bytes));
           SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(int), ctx->stream));
           SX_CUDA(cudaMemsetAsync(cursor, 0, 8, ctx->stream));
           const int64_t threads = (n + kRunItems - 1) / kRunItems;
-          if constexpr (runs_dense<Prog>::value) {
+          bool lean = false;
+          if constexpr (has_lean_runs<Prog>::value) {
+            // K10l first (SX_RUNS_LEAN=0: K10r); a wide value or a long run retries with K10r
+            const bool lean_off = getenv("SX_RUNS_LEAN") && getenv("SX_RUNS_LEAN")[0] == '0';
+            lean = !lean_off && !lean_failed && L.nst == 1 && L.kind[0] == ST_SUM && L.key_bytes == 4 &&
+                   L.slot_bytes <= 32;
+            if (lean)
+              k_runs_lean<Prog><<<persistent_grid(ctx, 8, ((n + 7) / 8 + kBlock - 1) / kBlock), kBlock, 0,
+                                  SX_STREAM(ctx)>>>(prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
+          }
+          if (lean) {
+          } else if constexpr (runs_dense<Prog>::value) {
             if (L.nst == 1 && L.kind[0] == ST_SUM && L.slot_bytes <= 32)
               k_runs_own_dense<Prog><<<persistent_grid(ctx, 8, ((n + kRunOwnRows - 1) / kRunOwnRows + kBlock - 1) / kBlock),
                                        kBlock, 0, SX_STREAM(ctx)>>>(prog, n, L, hv, out, cap_out, cursor, ctx->d_flags + 2);
@@ -740,6 +840,11 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
           int64_t cnt = 0;
           SX_TRY(read_i64(ctx, cursor, &cnt));
           SX_CUDA(cudaMemcpy(flags, ctx->d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost));
+          if (lean && !flags[2] && flags[3]) {  // |v| >= 2^40 or a long run: K10r decides
+            lean_failed = true;
+            --attempt;
+            continue;
+          }
           if (flags[2] || flags[3]) break;  // unsorted or a run longer than kRunAhead: other strategies
           if (flags[0]) return set_err(ctx, SX_EOVERFLOW, "a value expression left int64");
           if (cnt > cap_out) {

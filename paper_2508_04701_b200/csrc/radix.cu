@@ -66,16 +66,10 @@ __global__ void __launch_bounds__(kPartThreads) k_part_hist(const __grid_constan
   for (int p = threadIdx.x; p < P; p += blockDim.x) h[p] = 0;
   __syncthreads();
   const int64_t lo = blockIdx.x * s.chunk, hi = min(s.n, lo + s.chunk);
-  const int lane = threadIdx.x & 31;
-  // warp-aggregated: one shared atomic per distinct partition per warp (the loop trip count is
-  // warp-uniform: chunk bounds are CTA-uniform)
-  for (int64_t b = lo; b < hi; b += blockDim.x) {
-    const int64_t i = b + threadIdx.x;
-    const bool v = i < hi;
-    const int64_t r = v ? (s.sel ? (int64_t)__ldg(s.sel + i) : i) : 0;
-    const int p = v ? (int)part_of(part_key(s.k0, s.k1, s.nkeys, r), s.bits) : (1 << kMaxPartBits) + lane;
-    const unsigned peers = __match_any_sync(kFull, p);
-    if (v && lane == __ffs(peers) - 1) atomicAdd(&h[p], __popc(peers));
+  // plain shared atomics (a __match_any_sync-aggregated variant measured 2.5x slower on B200)
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int64_t r = s.sel ? (int64_t)__ldg(s.sel + i) : i;
+    atomicAdd(&h[part_of(part_key(s.k0, s.k1, s.nkeys, r), s.bits)], 1);
   }
   __syncthreads();
   for (int p = threadIdx.x; p < P; p += blockDim.x) hist[(int64_t)p * gridDim.x + blockIdx.x] = h[p];
@@ -170,9 +164,8 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(const __grid_cons
   }
 }
 
-// K7b' (default): 4096-row tiles; ranks within a partition come from warp-aggregated shared
-// counters (__match_any_sync leaders: one shared atomic per distinct partition per warp instead of
-// one per row), and every carried column is staged in shared memory in partition order — loaded
+// K7b' (default): 4096-row tiles; ranks within a partition from shared atomics, and every
+// carried column is staged in shared memory in partition order — loaded
 // coalesced at the tile's own rows, written as partition runs (~32 rows of each column per
 // partition per tile at fan-out 128) — instead of re-gathering each value by row id at write
 // time.  One column at a time, so the staging buffer is 16 B x 4096 at most.
@@ -196,7 +189,7 @@ __device__ __forceinline__ void emit_val(int w, const uint8_t* sb, int j, void* 
   }
 }
 
-__global__ void __launch_bounds__(kPartThreads) k_part_scatter_v(const __grid_constant__ PartSpec s,
+__global__ void __launch_bounds__(kPartThreads, 3) k_part_scatter_v(const __grid_constant__ PartSpec s,
                                                                  const int64_t* __restrict__ offs, int max_w) {
   extern __shared__ __align__(16) uint8_t sbuf[];  // kVsTile * max_w
   __shared__ int64_t cursor[1 << kMaxPartBits];
@@ -206,27 +199,23 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter_v(const __grid_co
   __shared__ int s_warp[kPartThreads / 32];
   const int P = 1 << s.bits;
   const int tid = threadIdx.x, lane = tid & 31;
-  const unsigned lt = lanemask_lt();
   for (int p = tid; p < P; p += kPartThreads) cursor[p] = offs[(int64_t)p * gridDim.x + blockIdx.x];
   const int64_t lo = blockIdx.x * s.chunk, hi = min(s.n, lo + s.chunk);
   for (int64_t base = lo; base < hi; base += kVsTile) {
     for (int p = tid; p < P; p += kPartThreads) cnt[p] = 0;
     __syncthreads();
-    int32_t row[kVsItems];
-    int part[kVsItems], rank[kVsItems];
+    // pr[i] = partition << 16 | rank within the partition (tile-local position after the scan);
+    // -1 past the end.  Row ids are recomputed (or re-read from the selection) when staging.
+    int pr[kVsItems];
 #pragma unroll
     for (int i = 0; i < kVsItems; ++i) {
       const int64_t idx = base + (int64_t)i * kPartThreads + tid;
-      const bool v = idx < hi;
-      row[i] = v ? (s.sel ? __ldg(s.sel + idx) : (int32_t)idx) : 0;
-      const int p = v ? (int)part_of(part_key(s.k0, s.k1, s.nkeys, row[i]), s.bits) : (1 << kMaxPartBits) + lane;
-      const unsigned peers = __match_any_sync(kFull, p);
-      const int leader = __ffs(peers) - 1;
-      int b = 0;
-      if (v && lane == leader) b = atomicAdd(&cnt[p], __popc(peers));
-      b = __shfl_sync(kFull, b, leader);
-      part[i] = v ? p : -1;
-      rank[i] = b + __popc(peers & lt);
+      pr[i] = -1;
+      if (idx < hi) {
+        const int32_t row = s.sel ? __ldg(s.sel + idx) : (int32_t)idx;
+        const int p = (int)part_of(part_key(s.k0, s.k1, s.nkeys, row), s.bits);
+        pr[i] = (p << 16) | atomicAdd(&cnt[p], 1);  // order within a partition is free (R12)
+      }
     }
     __syncthreads();
     {
@@ -260,9 +249,10 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter_v(const __grid_co
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kVsItems; ++i) {
-      if (part[i] < 0) continue;
-      rank[i] += start[part[i]];  // now the tile-local position
-      s_part[rank[i]] = (uint16_t)part[i];
+      if (pr[i] < 0) continue;
+      const int p = pr[i] >> 16;
+      pr[i] = start[p] + (pr[i] & 0xffff);  // now the tile-local position
+      s_part[pr[i]] = (uint16_t)p;
     }
     const int tcount = (int)min((int64_t)kVsTile, hi - base);
     const int ncols = s.ncarry + (s.out_rowid ? 1 : 0);
@@ -271,9 +261,11 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter_v(const __grid_co
       const int w = rid ? 4 : s.width[c];
 #pragma unroll
       for (int i = 0; i < kVsItems; ++i) {
-        if (part[i] < 0) continue;
-        if (rid) ((int32_t*)sbuf)[rank[i]] = row[i];
-        else stage_val(s.carry[c], w, sbuf, rank[i], row[i]);
+        if (pr[i] < 0) continue;
+        const int64_t idx = base + (int64_t)i * kPartThreads + tid;
+        const int32_t row = s.sel ? __ldg(s.sel + idx) : (int32_t)idx;
+        if (rid) ((int32_t*)sbuf)[pr[i]] = row;
+        else stage_val(s.carry[c], w, sbuf, pr[i], row);
       }
       __syncthreads();
       void* dst = rid ? (void*)s.out_rowid : s.out[c];
@@ -535,29 +527,25 @@ __global__ void __launch_bounds__(kBlock) k_pji_build(const __grid_constant__ PJ
   }
 }
 
-constexpr int kPiItems = 8;
+constexpr int kPiItems = 4;
 constexpr int kPiTile = kBlock * kPiItems;
-__global__ void __launch_bounds__(kBlock, 2) k_pji_probe(const __grid_constant__ PJoinI a) {
-  __shared__ long long s_b[kPiTile];
-  __shared__ long long s_p[kPiTile];
+__global__ void __launch_bounds__(kBlock, 4) k_pji_probe(const __grid_constant__ PJoinI a) {
   __shared__ int s_warp[kBlock / 32];
   __shared__ unsigned long long s_base;
-  __shared__ int s_tot;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool side_on = a.side[0] != 0;
   const long long side_v = (long long)a.side[1];
+  const uint64_t m = a.cap - 1;
   for (int64_t base = a.p_lo + blockIdx.x * (int64_t)kPiTile; base < a.p_hi; base += (int64_t)gridDim.x * kPiTile) {
     // idx: global slot index (region base | in-region slot; regions are cap-aligned)
     uint64_t key[kPiItems], idx[kPiItems];
-    long long pv[kPiItems], bv[kPiItems];
+    long long bv[kPiItems];
     bool pend[kPiItems], hit[kPiItems];
-    const uint64_t m = a.cap - 1;
 #pragma unroll
     for (int i = 0; i < kPiItems; ++i) {
       const int64_t j = base + (int64_t)i * kBlock + threadIdx.x;
       const bool v = j < a.p_hi;
       key[i] = v ? pj_key(a.pkey, a.kb, j) : ~0ull;
-      pv[i] = (v && a.pw) ? ld_val_cs(a.pval, j) : 0;
       const uint64_t h = hash64(key[i]);
       idx[i] = (uint64_t)(((uint32_t)(h >> kPartShift) & ((1u << a.bits) - 1u)) - a.p0) * a.cap + (h & m);
       hit[i] = v && key[i] == ~0ull && side_on;
@@ -586,6 +574,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_pji_probe(const __grid_constant__
         }
       }
     }
+    // one atomic per CTA tile for the output run; a thread's hits land consecutively
     int c = 0;
 #pragma unroll
     for (int i = 0; i < kPiItems; ++i) c += hit[i];
@@ -601,25 +590,18 @@ __global__ void __launch_bounds__(kBlock, 2) k_pji_probe(const __grid_constant__
       int tot = 0;
       for (int k = 0; k < kBlock / 32; ++k) tot += s_warp[k];
       s_base = tot ? atomicAdd(a.cursor, (unsigned long long)tot) : 0ull;
-      s_tot = tot;
     }
     int wo = 0;
     for (int k = 0; k < w; ++k) wo += s_warp[k];
     __syncthreads();
-    const int tot = s_tot;
-    int pos = wo + x - c;
+    int64_t pos = (int64_t)s_base + wo + x - c;
 #pragma unroll
     for (int i = 0; i < kPiItems; ++i) {
       if (!hit[i]) continue;
-      s_b[pos] = bv[i];
-      s_p[pos] = pv[i];
+      const int64_t j = base + (int64_t)i * kBlock + threadIdx.x;
+      if (a.bw) st_val(a.out_b, a.bw, pos, bv[i]);
+      if (a.pw) st_val(a.out_p, a.pw, pos, ld_val_cs(a.pval, j));
       ++pos;
-    }
-    __syncthreads();
-    const int64_t ob = (int64_t)s_base;
-    for (int k = threadIdx.x; k < tot; k += kBlock) {
-      if (a.bw) st_val(a.out_b, a.bw, ob + k, s_b[k]);
-      if (a.pw) st_val(a.out_p, a.pw, ob + k, s_p[k]);
     }
     __syncthreads();
   }

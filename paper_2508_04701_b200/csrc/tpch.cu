@@ -487,6 +487,29 @@ struct Q18Prog {
 #pragma unroll
     for (int i = 0; i < I; ++i) v[i] = c.q[i];
   }
+  // K10l (k_runs_lean): 32-bit keys; 8 rows per thread with 128-bit streaming loads
+  static constexpr bool kLeanRuns = sizeof(KT) == 4;
+  __device__ __forceinline__ void lean_load(int64_t r0, int64_t n, int32_t (&k)[8], long long (&v)[8]) const {
+    if (r0 + 8 <= n) {
+      const int4 a = __ldcs((const int4*)(okey + r0)), b = __ldcs((const int4*)(okey + r0) + 1);
+      k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w; k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const longlong2 q = __ldcs((const longlong2*)(qty + r0) + j);
+        v[2 * j] = q.x;
+        v[2 * j + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool in = r0 + i < n;
+        k[i] = in ? (int32_t)__ldg(okey + r0 + i) : 0;
+        v[i] = in ? __ldg(qty + r0 + i) : 0;
+      }
+    }
+  }
+  __device__ __forceinline__ int32_t lean_key(int64_t r) const { return (int32_t)__ldg(okey + r); }
+  __device__ __forceinline__ long long lean_val(int64_t r) const { return __ldg(qty + r); }
   // Dense rows for k_runs_own: R consecutive rows (r0 % R == 0) with 128-bit streaming loads.
   static constexpr bool kDenseRuns = true;
   template <int R>
@@ -994,6 +1017,135 @@ __global__ void k_lookup_rank(const int32_t* __restrict__ keys, int64_t n, const
   }
 }
 
+// Q3 fused lineitem pass (K10q; SURVEY §8(a) Q3 step 3 probe + step 4 group-by, adjacent steps
+// fused by the executor): lineitem is read once — l_shipdate and l_orderkey streamed with 128-bit
+// loads, 8 consecutive rows per thread — rows with shipdate > DATE are tested against the exact
+// key-range bitmap of the qualifying orders (the orders build), l_extendedprice/l_discount are
+// loaded only for the ~0.5% rows that join, and revenue = ext*(100-disc) is summed per orderkey
+// run (owned runs as K10l: a thread owns the groups starting among its rows; the next lane's
+// leading rows finish its last group).  One (orderkey, revenue) per order with >= 1 joined row is
+// appended (atomic cursor; group order is unspecified, R13).  flags: [0] a decreasing orderkey,
+// [1] a revenue term >= 2^40 in magnitude or a run past kRunAhead rows, [2] ext*(100-disc) left
+// int64 — the host then runs the operator-at-a-time plan, which decides.
+struct Q3Fused {
+  const int32_t* okey;
+  const int32_t* ship;
+  const long long* ext;
+  const long long* disc;
+  int32_t date;
+  const uint32_t* bm;
+  long long bm_min;
+  unsigned long long bm_bits;
+  int32_t* out_key;
+  longlong2* out_rev;
+  int64_t cap;
+  unsigned long long* cursor;
+  int* flags;
+  __device__ __forceinline__ bool joins(int32_t key, int32_t sd) const {
+    const unsigned long long off = (unsigned long long)((long long)key - bm_min);
+    if (!(sd > date) || off >= bm_bits) return false;
+    return (__ldg(bm + (off >> 5)) >> (off & 31)) & 1u;
+  }
+  __device__ __forceinline__ long long term(int64_t r, bool& ovf) const {
+    return mul_ck(__ldg(ext + r), 100 - __ldg(disc + r), ovf);
+  }
+};
+
+__global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n) {
+  constexpr int R = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
+  unsigned bad = 0, wide = 0;
+  bool ovf = false;
+  auto emit = [&](int32_t gk, long long s) {
+    const unsigned long long pos = atomicAdd(a.cursor, 1ull);
+    if ((int64_t)pos < a.cap) {
+      a.out_key[pos] = gk;
+      a.out_rev[pos] = make_longlong2(s, s < 0 ? -1 : 0);
+    }
+  };
+  for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R; wbase < n; wbase += stride) {
+    const int64_t r0 = wbase + (int64_t)lane * R;
+    int32_t k[R], sd[R];
+    if (r0 + R <= n) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int4 x = __ldcs((const int4*)(a.okey + r0) + j), y = __ldcs((const int4*)(a.ship + r0) + j);
+        k[4 * j] = x.x; k[4 * j + 1] = x.y; k[4 * j + 2] = x.z; k[4 * j + 3] = x.w;
+        sd[4 * j] = y.x; sd[4 * j + 1] = y.y; sd[4 * j + 2] = y.z; sd[4 * j + 3] = y.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const bool in = r0 + i < n;
+        k[i] = in ? __ldg(a.okey + r0 + i) : 0;
+        sd[i] = in ? __ldg(a.ship + r0 + i) : 0;
+      }
+    }
+    const int m = (int)max((int64_t)0, min((int64_t)R, n - r0));
+    // the bitmap words of the shipdate survivors (sorted keys: mostly the same word)
+    bool q[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) q[i] = i < m && a.joins(k[i], sd[i]);
+    long long v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = q[i] ? a.term(r0 + i, ovf) : 0;
+    int32_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
+    if (lane == 0 && r0 > 0 && r0 <= n) pk = __ldg(a.okey + r0 - 1);
+    const bool has_prev = r0 > 0;
+    long long lead = 0, s = 0;
+    int lead_len = 0, lead_c = 0, c = 0;
+    bool open = false;
+    int32_t ck = 0, prev = pk;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const bool in = i < m;
+      wide |= q[i] ? (unsigned)((int32_t)(v[i] >> 32) + 256) >> 9 : 0u;
+      const bool head = in && (k[i] != prev || (i == 0 && !has_prev));
+      bad |= (in && (i > 0 || has_prev) && k[i] < prev) ? 1u : 0u;
+      if (head && open && c > 0) emit(ck, s);
+      open = open || head;
+      lead += (in && !open) ? v[i] : 0;
+      lead_c += (in && !open && q[i]) ? 1 : 0;
+      lead_len += (in && !open) ? 1 : 0;
+      s = head ? v[i] : s + v[i];
+      c = head ? (int)q[i] : c + (int)q[i];
+      ck = head ? k[i] : ck;
+      prev = in ? k[i] : prev;
+    }
+    const long long nx_lead = __shfl_down_sync(kFull, lead, 1);
+    const int nx_c = __shfl_down_sync(kFull, lead_c, 1);
+    const int nx_len = __shfl_down_sync(kFull, lead_len, 1);
+    if (open) {
+      const int64_t nxt = r0 + R;
+      bool more = true;
+      int64_t r = nxt;
+      if (lane < 31 && nxt < n) {
+        s += nx_lead;
+        c += nx_c;
+        more = nx_len == R;
+        r = nxt + R;
+      }
+      int steps = 0;
+      for (; more && r < n && steps < kRunAhead; ++r, ++steps) {  // rare: scalar continuation
+        const int32_t kr = __ldg(a.okey + r);
+        if (kr != ck) break;
+        if (a.joins(kr, __ldg(a.ship + r))) {
+          const long long x = a.term(r, ovf);
+          wide |= (unsigned)((int32_t)(x >> 32) + 256) >> 9;
+          s += x;
+          ++c;
+        }
+      }
+      if (more && steps == kRunAhead && r < n) wide = 1;
+      if (c > 0) emit(ck, s);
+    }
+  }
+  if (bad) atomicExch(a.flags, 1);
+  if (wide) atomicExch(a.flags + 1, 1);
+  if (ovf) atomicExch(a.flags + 2, 1);
+}
+
 static const char* kNation[25] = {"ALGERIA", "ARGENTINA", "BRAZIL", "CANADA", "EGYPT", "ETHIOPIA", "FRANCE",
                                   "GERMANY", "INDIA", "INDONESIA", "IRAN", "IRAQ", "JAPAN", "JORDAN", "KENYA",
                                   "MOROCCO", "MOZAMBIQUE", "PERU", "CHINA", "ROMANIA", "SAUDI ARABIA", "VIETNAM",
@@ -1152,6 +1304,84 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   sx_ht* ht_o;
   SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, 1, &ht_o));
   bag.keep(ht_o);
+  // 3+4 fused (default; SX_Q3_PLAN=ops forces the operator-at-a-time steps below): one pass over
+  // lineitem probes the orders bitmap and sums revenue per orderkey run (k_q3_fused), then the
+  // groups' o_orderdate / o_shippriority come from a probe of the orders build with the group keys.
+  const bool ops_plan = getenv("SX_Q3_PLAN") && std::strcmp(getenv("SX_Q3_PLAN"), "ops") == 0;
+  if (!ops_plan && ht_o->bm && ht_o->nkeys == 1 && ht_o->key_bytes == 4 && w4(t->l_orderkey) &&
+      w4(t->l_shipdate) && w8(t->l_extendedprice) && w8(t->l_discount) &&
+      t->l_shipdate.len == t->l_orderkey.len && t->l_extendedprice.len == t->l_orderkey.len &&
+      t->l_discount.len == t->l_orderkey.len && t->l_orderkey.len > 0) {
+    const int64_t n = t->l_orderkey.len;
+    const int64_t gcap = std::max<int64_t>(1, ht_o->rows);
+    int32_t* gk;
+    longlong2* grev;
+    SX_TRY(alloc(ctx, &gk, (size_t)gcap));
+    bag.bufs.push_back(gk);
+    SX_TRY(alloc(ctx, &grev, (size_t)gcap));
+    bag.bufs.push_back(grev);
+    Q3Fused a{};
+    a.okey = (const int32_t*)t->l_orderkey.data;
+    a.ship = (const int32_t*)t->l_shipdate.data;
+    a.ext = (const long long*)t->l_extendedprice.data;
+    a.disc = (const long long*)t->l_discount.data;
+    a.date = (int32_t)std::max<int64_t>(INT32_MIN, std::min<int64_t>(INT32_MAX, p->q3_date));
+    a.bm = ht_o->bm;
+    a.bm_min = ht_o->bm_min;
+    a.bm_bits = ht_o->bm_bits;
+    a.out_key = gk;
+    a.out_rev = grev;
+    a.cap = gcap;
+    a.cursor = (unsigned long long*)ctx->d_counters;
+    a.flags = ctx->d_flags;
+    int64_t cnt = 0;
+    int fl[3] = {0, 0, 0};
+    {
+      ProfScope pg(ctx, "probe_groupby");
+      SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
+      SX_CUDA(cudaMemsetAsync(a.flags, 0, 3 * sizeof(int), ctx->stream));
+      k_q3_fused<<<persistent_grid(ctx, 8, ((n + 7) / 8 + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a, n);
+      SX_CHECK_LAUNCH();
+      SX_TRY(read_i64(ctx, a.cursor, &cnt));
+      SX_CUDA(cudaMemcpy(fl, a.flags, sizeof fl, cudaMemcpyDeviceToHost));
+      // algorithmic bytes: l_orderkey + l_shipdate once, ext + disc of the joined rows, the groups
+      pg.set_bytes(8.0 * n + 16.0 * cnt * 2.0 + 20.0 * cnt);
+    }
+    if (!fl[0] && !fl[1] && !fl[2] && cnt <= gcap) {
+      sx_col gkc{SX_I32, 0, cnt, gk, nullptr, nullptr};
+      sx_col grc{SX_I128, 4, cnt, grev, nullptr, nullptr};
+      sx_col bcols[2] = {t->o_orderdate, t->o_shippriority};
+      int32_t bp[2] = {0, 1};
+      sx_sel jp, jb;
+      sx_col pay[2];
+      SX_TRY(sx_hash_probe(ctx, ht_o, &gkc, 1, &k0, 1, nullptr, nullptr, 0, SX_INNER, bcols, 2, bp, 2, nullptr, 0, &jp,
+                           &jb, pay));
+      bag.keep(jp);
+      bag.keep(jb);
+      bag.keep(pay, 2);
+      if (jp.len != cnt) return set_err(ctx, SX_ECUDA, "Q3: %lld of %lld groups found their order", (long long)jp.len,
+                                        (long long)cnt);
+      // unique build: probe output in probe order, so pay[] aligns with the groups
+      sx_col scols[3] = {grc, pay[0], gkc};
+      sx_sortkey sks[3] = {{0, 1}, {1, 0}, {2, 0}};
+      sx_sel perm;
+      SX_TRY(sx_sort_topk(ctx, scols, 3, sks, 3, nullptr, p->q3_limit, &perm));
+      bag.keep(perm);
+      sx_col all[4] = {gkc, grc, pay[0], pay[1]};
+      std::vector<std::vector<uint8_t>> h;
+      SX_TRY(fetch_rows(ctx, bag, all, 4, perm, h));
+      if (perm.len > cap) return set_err(ctx, SX_EINVAL, "Q3: %lld rows > cap", (long long)perm.len);
+      for (int64_t i = 0; i < perm.len; ++i) {
+        out[i].l_orderkey = key_at(h[0], SX_I32, i);
+        out[i].revenue = i128_at(h[1], i);
+        out[i].o_orderdate = (int32_t)key_at(h[2], pay[0].type, i);
+        out[i].o_shippriority = (int32_t)key_at(h[3], pay[1].type, i);
+      }
+      *nrows = perm.len;
+      return SX_OK;
+    }
+    // unsorted lineitem, a wide revenue term or an overflow: the operator plan below decides
+  }
   // 3. lineitem with l_shipdate > DATE joined to those orders (unique build: ordered output)
   sx_col lcols[4] = {t->l_orderkey, t->l_shipdate, t->l_extendedprice, t->l_discount};
   sx_pred lship = P(1, SX_GT, p->q3_date);

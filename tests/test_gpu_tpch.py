@@ -86,6 +86,70 @@ def test_q18_group_strategies(small, monkeypatch, mode):
         assert rows_equal(got, want), diff_rows(got, want)
 
 
+@pytest.mark.parametrize("case", ["tails", "run20", "run60", "run200", "big", "unsorted", "lean-off"])
+def test_q18_owned_runs(ctx, monkeypatch, case):
+    """Q18's owned-run aggregation (K10l lean kernel, else K10r; forced with SX_GB_SORTED=2 at SF 0.1):
+    a ragged tail, runs of 20 / 60 rows crossing lanes and warps (lead hand-off, scalar
+    continuation), a 200-row run (past kRunAhead: K10r, then hashing), a quantity >= 2^40 (K10l
+    refuses: K10r), an unsorted key column (hashing), and SX_RUNS_LEAN=0 (K10r) on the same data."""
+    monkeypatch.setenv("SX_GB_SORTED", "2")
+    if case == "lean-off":
+        monkeypatch.setenv("SX_RUNS_LEAN", "0")
+    host = gen.cpu_tables(100, seed=13)
+    li = {k: v.copy() for k, v in host["lineitem"].items()}
+    n = len(li["l_orderkey"]) - (1111 if case == "tails" else 0)
+    li = {k: v[:n].copy() for k, v in li.items()}
+    ok = li["l_orderkey"]
+    if case in ("run20", "run60", "run200"):
+        L = {"run20": 20, "run60": 60, "run200": 200}[case]
+        for start in (4096 * 7 + 100, 2048 * 40 - 30, 256 * 100 - 3, n - L):  # inside, across tiles/warps, at the end
+            ok[start:start + L] = ok[start]
+    if case == "big":
+        li["l_quantity"][[5, 70_000, n - 1]] = 1 << 41
+    if case == "unsorted":
+        ok[[1000, 1001]] = ok[[1001, 1000]] if ok[1000] != ok[1001] else (ok[1000], ok[1000] - 1)
+        ok[300_000], ok[300_001] = ok[300_001], ok[300_000]
+    host = dict(host)
+    host["lineitem"] = li
+    T = tpch.Tpch(ctx, to_dev(host))
+    for over in ({}, dict(q18_qty_gt=15000)):
+        got = T.run("q18", tpch.default_params(**over))
+        want = oracle.run_query("q18", host, oracle.default_params(**over))
+        assert rows_equal(got, want), diff_rows(got, want)
+
+
+
+@pytest.mark.parametrize("case", ["fused", "ops", "tails", "run30", "unsorted", "wide"])
+def test_q3_plans(ctx, monkeypatch, case):
+    """Q3 through the fused lineitem pass (K10q, default) and the operator-at-a-time plan
+    (SX_Q3_PLAN=ops), at SF 0.1: a ragged tail, 30-row orderkey runs crossing lanes/warps, an
+    unsorted l_orderkey (fused pass refuses: ops plan), and an extendedprice >= 2^40 / 100 (a
+    revenue term >= 2^40: fused pass refuses) — every case against the oracle."""
+    if case == "ops":
+        monkeypatch.setenv("SX_Q3_PLAN", "ops")
+    host = gen.cpu_tables(100, seed=17)
+    li = {k: v.copy() for k, v in host["lineitem"].items()}
+    n = len(li["l_orderkey"]) - (777 if case == "tails" else 0)
+    li = {k: v[:n].copy() for k, v in li.items()}
+    ok = li["l_orderkey"]
+    if case == "run30":
+        for start in (4096 * 5 + 11, 256 * 77 - 5, n - 30):
+            ok[start:start + 30] = ok[start]
+            li["l_shipdate"][start:start + 30] = 9300  # after the Q3 date: every row of the run joins if its order does
+    if case == "unsorted":
+        ok[[2000, 2001]] = ok[[2001, 2000]] if ok[2000] != ok[2001] else (ok[2000], ok[2000] - 1)
+    if case == "wide":
+        li["l_extendedprice"][[3, n // 2]] = 1 << 40
+    host = dict(host)
+    host["lineitem"] = li
+    T = tpch.Tpch(ctx, to_dev(host))
+    for over in ({}, dict(q3_limit=1000)):
+        got = T.run("q3", tpch.default_params(**over))
+        want = oracle.run_query("q3", host, oracle.default_params(**over))
+        assert rows_equal(got, want), diff_rows(got, want)
+
+
+
 def test_gpu_generator_matches_cpu_generator():
     cpu = gen.cpu_tables(10, seed=42)
     g = gen.gpu_tables(10, seed=42)
