@@ -46,6 +46,14 @@ SX_EXPORT sx_status sx_ctx_create(int device, void* stream, sx_ctx** out) {
       cudaStreamSynchronize(ctx->stream);
     }
   }
+  // L2 fetch granularity (bytes per DRAM fetch on an L2 miss; SX_L2_FETCH = 32 / 64 / 128): the
+  // hot path's sparse gathers (K10w's green rows, probe lookups) touch one 32-byte sector per
+  // line, so a larger fetch moves bytes nobody reads.  Unset: the driver default.
+  if (const char* fe = getenv("SX_L2_FETCH")) {
+    const size_t g = (size_t)atoi(fe);
+    if (g == 32 || g == 64 || g == 128) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g);
+    cudaGetLastError();
+  }
   SX_CUDA(cudaMalloc((void**)&ctx->d_flags, 64 * sizeof(int)));
   SX_CUDA(cudaMemset(ctx->d_flags, 0, 64 * sizeof(int)));
   SX_CUDA(cudaMalloc((void**)&ctx->d_counters, 64 * sizeof(unsigned int)));

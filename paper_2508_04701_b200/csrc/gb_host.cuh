@@ -664,6 +664,11 @@ static __global__ void k_gb_emit(const __grid_constant__ EmitArgs a) {
   }
 }
 
+// K18 (gbsimple.cu): the plain-shape fast path; SX_EUNSUPPORTED when the call is not of that shape
+sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* keys, int nkeys, const sx_sel* in_sel,
+                    int nwhere, const sx_agg* aggs, int naggs, const sx_having* having, int64_t groups_hint,
+                    sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups);
+
 inline int agg_out_type(int op) {
   switch (op) {
     case SX_SUM: return SX_I128;

@@ -1,0 +1,558 @@
+// gbsimple.cu — K18: the plain-shape fast path of sx_groupby_agg (H7).
+//
+// group-by is substantial where few groups cause memory contention (Q1) and where
+// many groups need a large table (Q10/Q18); SURVEY §8(d) C5b sweeps G = 2^2 .. 2^26.  For the plain
+// shape — one integer key column (identity), no WHERE / selection / HAVING, every aggregate a
+// COUNT or SUM / MIN / MAX / AVG of one integer column — the aggregation runs in shared memory
+// for every G the partitioner can split down to a shared table:
+//
+//   K18s (hinted G <= 1024): each CTA aggregates a contiguous chunk of rows into R replicas of a
+//        shared-memory hash table (lane l uses replica l % R, so small G does not serialise on a
+//        few shared addresses), then merges its replicas into a global table (one atomic per
+//        group and state per CTA) from which the groups are emitted;
+//   K18p (hinted G <= 2^21): the key and value columns are radix-partitioned on hash bits 48..
+//        (K7, the join's partitioner) into P partitions of <= ~1024 expected groups; one CTA per
+//        partition aggregates it in a shared table and writes its groups straight to the output
+//        (partitions hold disjoint keys, so no merge).
+//
+// Exactness (readings R2/R3): shared partial sums are int64 while every value is < 2^40 in
+// magnitude and a CTA sums < 2^23 rows (checked: a row outside takes an exact global 96-bit
+// atomic instead); global sums are 96-bit; AVG = (double)sum / (double)count / 10^scale exactly
+// as the generic path.  Anything else returns SX_EUNSUPPORTED and sx_groupby_agg takes the generic
+// path.  Output group order is unspecified (R13).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "gb_host.cuh"
+#include "radix.cuh"
+
+using namespace sx;
+
+namespace {
+
+constexpr int kGsThreads = 512;
+constexpr int kGsMaxStates = 6;
+constexpr int kGsMaxVals = 4;
+constexpr long long kEmptyKey = LLONG_MIN;  // shared / global EMPTY marker; the real key goes to the side slot
+constexpr int kGsPartSlots = 4096;          // K18p shared table (<= ~2048 groups per partition)
+
+struct GsSpec {
+  const void* key;
+  int key_bytes;  // 4 or 8
+  int key_type;
+  int nv;
+  const void* val[kGsMaxVals];
+  int vbytes[kGsMaxVals];
+  int nst;
+  int kind[kGsMaxStates];  // ST_SUM / ST_COUNT / ST_MIN / ST_MAX
+  int vc[kGsMaxStates];    // value column of the state (-1: COUNT)
+  // outputs
+  int naggs;
+  int agg_op[SX_MAX_AGGS];
+  int agg_state[SX_MAX_AGGS];
+  int agg_scale[SX_MAX_AGGS];
+  int count_state;
+  void* out_key;
+  void* out_agg[SX_MAX_AGGS];
+  int64_t out_cap;
+  unsigned long long* out_cursor;
+  int* flags;  // [0] a shared table filled up
+};
+
+// global merge table (K18s): keys[C + 1] (side slot C for kEmptyKey), per state C + 1 u64 (+ hi)
+struct GsGlobal {
+  unsigned long long* keys;
+  int* used;  // per slot: 1 once claimed (the side slot's marker)
+  unsigned long long* st[kGsMaxStates];
+  int* hi[kGsMaxStates];
+  uint64_t mask;
+};
+
+__device__ __forceinline__ long long ld_key(const GsSpec& s, int64_t r) {
+  return s.key_bytes == 4 ? (long long)__ldcs((const int32_t*)s.key + r) : __ldcs((const long long*)s.key + r);
+}
+__device__ __forceinline__ long long ld_v(const GsSpec& s, int c, int64_t r) {
+  return s.vbytes[c] == 4 ? (long long)__ldcs((const int32_t*)s.val[c] + r) : __ldcs((const long long*)s.val[c] + r);
+}
+__device__ __forceinline__ long long pick(const long long (&v)[kGsMaxVals], int c) {
+  return c == 0 ? v[0] : c == 1 ? v[1] : c == 2 ? v[2] : v[3];  // (no dynamic register indexing)
+}
+__device__ __forceinline__ bool small_v(long long v) { return ((unsigned)((int32_t)(v >> 32) + 256) >> 9) == 0; }
+
+// shared table: keys[S + 1] then nst arrays of S + 1 u64 (slot S = side slot for kEmptyKey)
+struct STab {
+  long long* keys;
+  unsigned long long* st;  // [nst][S + 1]
+  uint32_t S;
+  __device__ __forceinline__ unsigned long long* state(int a, uint32_t slot) const { return st + (size_t)a * (S + 1) + slot; }
+};
+
+__device__ __forceinline__ void stab_init(const STab& t, const GsSpec& s, int tid, int nt) {
+  for (uint32_t i = tid; i <= t.S; i += nt) {
+    t.keys[i] = kEmptyKey;
+    for (int a = 0; a < s.nst; ++a)
+      *t.state(a, i) = s.kind[a] == ST_MIN ? (unsigned long long)LLONG_MAX
+                       : s.kind[a] == ST_MAX ? (unsigned long long)LLONG_MIN : 0ull;
+  }
+}
+
+// slot of `k` in t (inserting it); S + 1 when the table is full
+__device__ __forceinline__ uint32_t stab_slot(const STab& t, long long k) {
+  if (k == kEmptyKey) return t.S;
+  uint32_t h = (uint32_t)hash64((uint64_t)k) & (t.S - 1);
+  for (uint32_t probes = 0; probes < t.S; ++probes) {
+    const long long cur = t.keys[h];
+    if (cur == k) return h;
+    if (cur == kEmptyKey) {
+      const long long old = (long long)atomicCAS((unsigned long long*)&t.keys[h], (unsigned long long)kEmptyKey,
+                                                 (unsigned long long)k);
+      if (old == kEmptyKey || old == k) return h;
+    }
+    h = (h + 1) & (t.S - 1);
+  }
+  return t.S + 1;
+}
+
+__device__ __forceinline__ void stab_update(const STab& t, const GsSpec& s, uint32_t slot, const long long (&v)[kGsMaxVals]) {
+#pragma unroll
+  for (int a = 0; a < kGsMaxStates; ++a) {
+    if (a >= s.nst) break;
+    unsigned long long* p = t.state(a, slot);
+    switch (s.kind[a]) {
+      case ST_SUM: atomicAdd(p, (unsigned long long)pick(v, s.vc[a])); break;
+      case ST_COUNT: atomicAdd(p, 1ull); break;
+      case ST_MIN: atomicMin((long long*)p, pick(v, s.vc[a])); break;
+      default: atomicMax((long long*)p, pick(v, s.vc[a])); break;
+    }
+  }
+}
+
+// ---- global merge table --------------------------------------------------------------------
+__device__ __forceinline__ uint64_t g_slot(const GsGlobal& g, long long k, int* flags) {
+  if (k == kEmptyKey) {
+    g.used[g.mask + 1] = 1;
+    return g.mask + 1;
+  }
+  uint64_t h = hash64((uint64_t)k) & g.mask;
+  for (uint64_t probes = 0; probes <= g.mask; ++probes) {
+    const unsigned long long old = atomicCAS(&g.keys[h], (unsigned long long)kEmptyKey, (unsigned long long)k);
+    if (old == (unsigned long long)kEmptyKey || old == (unsigned long long)k) return h;
+    h = (h + 1) & g.mask;
+  }
+  atomicExch(flags, 1);  // more groups than the hint allowed for: the host takes the generic path
+  return g.mask + 1;
+}
+
+__device__ __forceinline__ void g_add(const GsGlobal& g, const GsSpec& s, uint64_t slot, int a, unsigned long long x,
+                                      bool x_is_sum) {
+  switch (s.kind[a]) {
+    case ST_SUM:
+      if (x_is_sum) atomic_add_i64_to_sum96(g.st[a] + slot, g.hi[a] + slot, (long long)x);
+      break;
+    case ST_COUNT: atomicAdd(g.st[a] + slot, x); break;
+    case ST_MIN: atomicMin((long long*)g.st[a] + slot, (long long)x); break;
+    default: atomicMax((long long*)g.st[a] + slot, (long long)x); break;
+  }
+}
+
+// exact single-row update of the global table (a value >= 2^40: not summed in shared memory)
+__device__ __forceinline__ void g_row(const GsGlobal& g, const GsSpec& s, long long k, const long long (&v)[kGsMaxVals]) {
+  const uint64_t slot = g_slot(g, k, s.flags);
+  for (int a = 0; a < s.nst; ++a)
+    g_add(g, s, slot, a, s.kind[a] == ST_COUNT ? 1ull : (unsigned long long)pick(v, s.vc[a]), true);
+}
+
+// ---- K18s ----------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kGsThreads) k_gbs_local(const __grid_constant__ GsSpec s, int64_t n, int64_t chunk,
+                                                          uint32_t S, int R, const __grid_constant__ GsGlobal g) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const size_t tab_bytes = (size_t)(S + 1) * 8 * (1 + s.nst);
+  const int lane = threadIdx.x & 31;
+  STab t;
+  t.S = S;
+  t.keys = (long long*)(smem + (size_t)(lane % R) * tab_bytes);
+  t.st = (unsigned long long*)(t.keys + (S + 1));
+  for (int r = 0; r < R; ++r) {
+    STab x;
+    x.S = S;
+    x.keys = (long long*)(smem + (size_t)r * tab_bytes);
+    x.st = (unsigned long long*)(x.keys + (S + 1));
+    stab_init(x, s, threadIdx.x, blockDim.x);
+  }
+  __syncthreads();
+  const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  bool full = false;
+  constexpr int U = 4;
+  for (int64_t b = lo; b < hi; b += (int64_t)U * blockDim.x) {
+    long long k[U], v[U][kGsMaxVals];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = b + (int64_t)u * blockDim.x + threadIdx.x;
+      const bool in = r < hi;
+      k[u] = in ? ld_key(s, r) : 0;
+#pragma unroll
+      for (int c = 0; c < kGsMaxVals; ++c) v[u][c] = (in && c < s.nv) ? ld_v(s, c, r) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = b + (int64_t)u * blockDim.x + threadIdx.x;
+      if (r >= hi) continue;
+      bool sm = true;
+#pragma unroll
+      for (int c = 0; c < kGsMaxVals; ++c) sm = sm && (c >= s.nv || small_v(v[u][c]));
+      if (!sm) {
+        g_row(g, s, k[u], v[u]);
+        continue;
+      }
+      const uint32_t slot = stab_slot(t, k[u]);
+      if (slot > S) {
+        full = true;
+        continue;
+      }
+      stab_update(t, s, slot, v[u]);
+    }
+  }
+  if (full) atomicExch(s.flags, 1);
+  __syncthreads();
+  // merge every replica into the global table
+  for (int r = 0; r < R; ++r) {
+    STab x;
+    x.S = S;
+    x.keys = (long long*)(smem + (size_t)r * tab_bytes);
+    x.st = (unsigned long long*)(x.keys + (S + 1));
+    for (uint32_t i = threadIdx.x; i <= S; i += blockDim.x) {
+      const long long key = x.keys[i];
+      // (the side slot holds the key kEmptyKey; its count tells whether it was used)
+      const bool used = i < S ? key != kEmptyKey : *x.state(s.count_state, i) != 0;
+      if (!used) continue;
+      const uint64_t gs = g_slot(g, i < S ? key : kEmptyKey, s.flags);
+      for (int a = 0; a < s.nst; ++a) g_add(g, s, gs, a, *x.state(a, i), true);
+    }
+  }
+}
+
+__global__ void k_gbs_init(const __grid_constant__ GsSpec s, const __grid_constant__ GsGlobal g) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= g.mask + 1; i += (uint64_t)gridDim.x * blockDim.x) {
+    g.keys[i] = (unsigned long long)kEmptyKey;
+    g.used[i] = 0;
+    for (int a = 0; a < s.nst; ++a) {
+      g.st[a][i] = s.kind[a] == ST_MIN ? (unsigned long long)LLONG_MAX
+                   : s.kind[a] == ST_MAX ? (unsigned long long)LLONG_MIN : 0ull;
+      if (g.hi[a]) g.hi[a][i] = 0;
+    }
+  }
+}
+
+__device__ __forceinline__ void put_out_key(const GsSpec& s, int64_t i, long long k) {
+  if (s.key_bytes == 4) ((int32_t*)s.out_key)[i] = (int32_t)k;
+  else ((long long*)s.out_key)[i] = k;
+}
+
+// one output row from states (lo, hi per state)
+__device__ __forceinline__ void put_out_aggs(const GsSpec& s, int64_t i, const unsigned long long (&lo)[kGsMaxStates],
+                                             const long long (&hi)[kGsMaxStates]) {
+  const unsigned long long count = s.count_state >= 0 ? lo[s.count_state] : 0;
+  for (int j = 0; j < s.naggs; ++j) {
+    const int a = s.agg_state[j];
+    switch (s.agg_op[j]) {
+      case SX_SUM: ((longlong2*)s.out_agg[j])[i] = make_longlong2((long long)lo[a], hi[a]); break;
+      case SX_COUNT: ((long long*)s.out_agg[j])[i] = (long long)count; break;
+      case SX_MIN:
+      case SX_MAX: ((long long*)s.out_agg[j])[i] = (long long)lo[a]; break;
+      default: {  // AVG = (double)sum / (double)count / 10^scale (reading R3)
+        double sc = 1.0;
+        for (int q = 0; q < s.agg_scale[j]; ++q) sc *= 10.0;
+        ((double*)s.out_agg[j])[i] = i128_to_double(lo[a], hi[a]) / (double)count / sc;
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_gbs_emit(const __grid_constant__ GsSpec s, const __grid_constant__ GsGlobal g) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= g.mask + 1; i += (uint64_t)gridDim.x * blockDim.x) {
+    const bool used = i <= g.mask ? g.keys[i] != (unsigned long long)kEmptyKey : g.used[i] != 0;
+    if (!used) continue;
+    const unsigned long long pos = atomicAdd(s.out_cursor, 1ull);
+    if ((int64_t)pos >= s.out_cap) continue;
+    unsigned long long lo[kGsMaxStates];
+    long long hi[kGsMaxStates];
+    for (int a = 0; a < kGsMaxStates; ++a) {
+      lo[a] = a < s.nst ? g.st[a][i] : 0;
+      hi[a] = (a < s.nst && s.kind[a] == ST_SUM) ? (long long)g.hi[a][i] : 0;
+    }
+    put_out_key(s, (int64_t)pos, i <= g.mask ? (long long)g.keys[i] : kEmptyKey);
+    put_out_aggs(s, (int64_t)pos, lo, hi);
+  }
+}
+
+// ---- K18p ----------------------------------------------------------------------------------
+// One CTA per partition (grid-stride over partitions): shared table of kGsPartSlots slots, the
+// partition's rows [off[p], off[p+1]) of the partitioned key/value columns, then its groups are
+// appended to the output (one atomic per CTA).
+__global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__ GsSpec s, const int64_t* __restrict__ off,
+                                                         int P, const __grid_constant__ GsGlobal g) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_cnt;
+  __shared__ unsigned long long s_base;
+  STab t;
+  t.S = kGsPartSlots;
+  t.keys = (long long*)smem;
+  t.st = (unsigned long long*)(t.keys + (t.S + 1));
+  for (int p = blockIdx.x; p < P; p += gridDim.x) {
+    stab_init(t, s, threadIdx.x, blockDim.x);
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const int64_t lo = off[p], hi = off[p + 1];
+    bool full = false;
+    constexpr int U = 4;
+    for (int64_t b = lo; b < hi; b += (int64_t)U * blockDim.x) {
+      long long k[U], v[U][kGsMaxVals];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = b + (int64_t)u * blockDim.x + threadIdx.x;
+        const bool in = r < hi;
+        k[u] = in ? ld_key(s, r) : 0;
+#pragma unroll
+        for (int c = 0; c < kGsMaxVals; ++c) v[u][c] = (in && c < s.nv) ? ld_v(s, c, r) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = b + (int64_t)u * blockDim.x + threadIdx.x;
+        if (r >= hi) continue;
+        bool sm = true;
+#pragma unroll
+        for (int c = 0; c < kGsMaxVals; ++c) sm = sm && (c >= s.nv || small_v(v[u][c]));
+        if (!sm) {
+          full = true;  // exactness needs the 96-bit path: the host reruns generically
+          continue;
+        }
+        const uint32_t slot = stab_slot(t, k[u]);
+        if (slot > t.S) {
+          full = true;
+          continue;
+        }
+        stab_update(t, s, slot, v[u]);
+      }
+    }
+    if (full) atomicExch(s.flags, 1);
+    __syncthreads();
+    // count used slots, claim an output run, write the groups
+    for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) {
+      const bool used = i < t.S ? t.keys[i] != kEmptyKey : *t.state(s.count_state, i) != 0;
+      if (used) atomicAdd(&s_cnt, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = atomicAdd(s.out_cursor, (unsigned long long)s_cnt);
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) {
+      const bool used = i < t.S ? t.keys[i] != kEmptyKey : *t.state(s.count_state, i) != 0;
+      if (!used) continue;
+      const int64_t pos = (int64_t)s_base + atomicAdd(&s_cnt, 1);
+      if (pos >= s.out_cap) continue;
+      unsigned long long lo[kGsMaxStates];
+      long long hi[kGsMaxStates];
+      for (int a = 0; a < kGsMaxStates; ++a) {
+        lo[a] = a < s.nst ? *t.state(a, i) : 0;
+        hi[a] = (a < s.nst && s.kind[a] == ST_SUM) ? ((long long)lo[a] < 0 ? -1 : 0) : 0;
+      }
+      put_out_key(s, pos, i < t.S ? t.keys[i] : kEmptyKey);
+      put_out_aggs(s, pos, lo, hi);
+    }
+    __syncthreads();
+  }
+  (void)g;
+}
+
+bool plain_col_expr(const sx_expr& e, int* col) {
+  if (e.nterms != 1 || e.t[0].coef != 1 || e.t[0].nf != 1) return false;
+  const auto& f = e.t[0].f[0];
+  if (f.mul != 1 || f.add != 0) return false;
+  *col = f.col;
+  return true;
+}
+
+}  // namespace
+
+namespace sx {
+
+sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* keys, int nkeys, const sx_sel* in_sel,
+                    int nwhere, const sx_agg* aggs, int naggs, const sx_having* having, int64_t groups_hint,
+                    sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups) {
+  const bool off = getenv("SX_GB_SIMPLE") && getenv("SX_GB_SIMPLE")[0] == '0';
+  if (off || nkeys != 1 || in_sel || nwhere || having || naggs < 1 || naggs > SX_MAX_AGGS || groups_hint < 1 ||
+      groups_hint > (1 << 21))
+    return SX_EUNSUPPORTED;
+  if (keys[0].fn != SX_KEY_IDENTITY || keys[0].col < 0 || keys[0].col >= ncols) return SX_EUNSUPPORTED;
+  const sx_col& kc = cols[keys[0].col];
+  const int kt = kc.type;
+  if (!(kt == SX_I32 || kt == SX_DATE32 || kt == SX_I64) || kc.validity) return SX_EUNSUPPORTED;
+  const int64_t n = kc.len;
+  if (n < (1 << 20) || n > INT32_MAX) return SX_EUNSUPPORTED;
+  GsSpec s{};
+  s.key = kc.data;
+  s.key_bytes = kt == SX_I64 ? 8 : 4;
+  s.key_type = kt;
+  s.count_state = -1;
+  int vcol_of[kGsMaxVals];
+  auto vslot = [&](int col) -> int {
+    for (int c = 0; c < s.nv; ++c)
+      if (vcol_of[c] == col) return c;
+    if (s.nv == kGsMaxVals) return -1;
+    const sx_col& vc = cols[col];
+    if (vc.len != n || vc.validity) return -1;
+    const int w = (vc.type == SX_I64 || vc.type == SX_DEC64) ? 8 : (vc.type == SX_I32 || vc.type == SX_DATE32) ? 4 : 0;
+    if (!w) return -1;
+    vcol_of[s.nv] = col;
+    s.val[s.nv] = vc.data;
+    s.vbytes[s.nv] = w;
+    return s.nv++;
+  };
+  auto state = [&](int kind, int vc) -> int {
+    for (int a = 0; a < s.nst; ++a)
+      if (s.kind[a] == kind && s.vc[a] == vc) return a;
+    if (s.nst == kGsMaxStates) return -1;
+    s.kind[s.nst] = kind;
+    s.vc[s.nst] = vc;
+    return s.nst++;
+  };
+  s.naggs = naggs;
+  s.count_state = state(ST_COUNT, -1);  // always kept: it marks the side slot (key kEmptyKey) as used
+  for (int j = 0; j < naggs; ++j) {
+    const int op = aggs[j].op;
+    s.agg_op[j] = op;
+    s.agg_scale[j] = aggs[j].scale;
+    if (op == SX_COUNT) {
+      s.agg_state[j] = s.count_state;
+      continue;
+    }
+    int col = -1;
+    if (!plain_col_expr(aggs[j].value, &col) || col < 0 || col >= ncols) return SX_EUNSUPPORTED;
+    const int vc = vslot(col);
+    if (vc < 0) return SX_EUNSUPPORTED;
+    const int kind = (op == SX_SUM || op == SX_AVG) ? ST_SUM : op == SX_MIN ? ST_MIN : op == SX_MAX ? ST_MAX : -1;
+    if (kind < 0) return SX_EUNSUPPORTED;
+    const int a = state(kind, vc);
+    if (a < 0) return SX_EUNSUPPORTED;
+    s.agg_state[j] = a;
+  }
+  for (int c = 0; c < s.nv; ++c)
+    if ((uintptr_t)s.val[c] % 16) return SX_EUNSUPPORTED;
+  if ((uintptr_t)s.key % 16) return SX_EUNSUPPORTED;
+  Scratch scr(ctx);
+  // outputs (capacity from the hint; rerun with the exact count if it was low)
+  int64_t cap = std::min<int64_t>(n, 2 * groups_hint + 1024);
+  unsigned long long* cursor = (unsigned long long*)ctx->d_counters;
+  s.out_cursor = cursor;
+  s.flags = ctx->d_flags;
+  const bool part = groups_hint > 1024;
+  // K18p partitioning (once, outside the capacity retry)
+  int bits = 0;
+  std::vector<int64_t> offs;
+  int64_t* d_off = nullptr;
+  if (part) {
+    // fan-out 1024 (the partitioner's maximum): <= 2048 expected groups per shared table, and
+    // enough partitions to spread over every SM whatever G is
+    bits = 10;
+    if ((groups_hint >> bits) > 2048) return SX_EUNSUPPORTED;
+    const int P = 1 << bits;
+    DCol kd{kc.data, kt, 0};
+    DCol carry[1 + kGsMaxVals];
+    int width[1 + kGsMaxVals];
+    void* outp[1 + kGsMaxVals];
+    carry[0] = kd;
+    width[0] = s.key_bytes;
+    for (int c = 0; c < s.nv; ++c) {
+      carry[1 + c] = DCol{s.val[c], cols[vcol_of[c]].type, 0};
+      width[1 + c] = s.vbytes[c];
+    }
+    for (int c = 0; c <= s.nv; ++c) SX_TRY(scr.get((char**)&outp[c], (size_t)n * width[c]));
+    offs.assign((size_t)P + 1, 0);
+    SX_TRY(radix_partition_carry(ctx, kd, kd, 1, carry, width, 1 + s.nv, nullptr, n, bits, outp, offs.data()));
+    // a partition sums in one CTA with int64 partials: <= 2^23 rows of |v| < 2^40 (skewed keys
+    // beyond that take the generic path)
+    for (int p = 0; p < P; ++p)
+      if (offs[p + 1] - offs[p] > (1 << 23)) return SX_EUNSUPPORTED;
+    s.key = outp[0];
+    for (int c = 0; c < s.nv; ++c) s.val[c] = outp[1 + c];
+    SX_TRY(scr.get(&d_off, (size_t)P + 1));
+    SX_CUDA(cudaMemcpyAsync(d_off, offs.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    void* okey;
+    void* oagg[SX_MAX_AGGS];
+    SX_TRY(scr.get((char**)&okey, (size_t)std::max<int64_t>(cap, 1) * s.key_bytes));
+    for (int j = 0; j < naggs; ++j) SX_TRY(scr.get((char**)&oagg[j], (size_t)std::max<int64_t>(cap, 1) * type_width(agg_out_type(aggs[j].op))));
+    s.out_key = okey;
+    for (int j = 0; j < naggs; ++j) s.out_agg[j] = oagg[j];
+    s.out_cap = cap;
+    SX_CUDA(cudaMemsetAsync(cursor, 0, 8, ctx->stream));
+    SX_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(int), ctx->stream));
+    GsGlobal g{};
+    if (part) {
+      const int P = 1 << bits;
+      const size_t smem = (size_t)(kGsPartSlots + 1) * 8 * (1 + s.nst);
+      SX_CUDA(cudaFuncSetAttribute(k_gbs_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbs_part, kGsThreads, smem));
+      const unsigned grid = (unsigned)std::min<int64_t>(P, (int64_t)ctx->num_sms * std::max(1, per_sm));
+      k_gbs_part<<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, d_off, P, g);
+      SX_CHECK_LAUNCH();
+    } else {
+      // global merge table: load <= 0.5
+      uint64_t C = 64;
+      while (C < (uint64_t)(2 * groups_hint)) C <<= 1;
+      SX_TRY(scr.get(&g.keys, C + 1));
+      SX_TRY(scr.get(&g.used, C + 1));
+      for (int a = 0; a < s.nst; ++a) {
+        SX_TRY(scr.get(&g.st[a], C + 1));
+        g.hi[a] = nullptr;
+        if (s.kind[a] == ST_SUM) SX_TRY(scr.get(&g.hi[a], C + 1));
+      }
+      g.mask = C - 1;
+      k_gbs_init<<<persistent_grid(ctx, 4, (C + kBlock) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(s, g);
+      // shared table: S slots (load <= 0.5 at the hint), R replicas in <= 96 KB
+      uint32_t S = 16;
+      while (S < (uint32_t)(2 * groups_hint)) S <<= 1;
+      const size_t tab = (size_t)(S + 1) * 8 * (1 + s.nst);
+      int R = (int)std::max<size_t>(1, std::min<size_t>(32, (96u << 10) / tab));
+      while (32 % R) --R;
+      const size_t smem = tab * R;
+      SX_CUDA(cudaFuncSetAttribute(k_gbs_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbs_local, kGsThreads, smem));
+      const int64_t ctas = (int64_t)ctx->num_sms * std::max(1, per_sm);
+      // every CTA sums < 2^23 rows (int64 partial sums of |v| < 2^40 values cannot overflow)
+      int64_t chunk = (n + ctas - 1) / ctas;
+      chunk = std::min<int64_t>(chunk, 1 << 22);
+      const unsigned grid = (unsigned)((n + chunk - 1) / chunk);
+      k_gbs_local<<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, n, chunk, S, R, g);
+      SX_CHECK_LAUNCH();
+      k_gbs_emit<<<persistent_grid(ctx, 4, (C + kBlock) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(s, g);
+      SX_CHECK_LAUNCH();
+    }
+    int64_t ng = 0;
+    SX_TRY(read_i64(ctx, cursor, &ng));
+    int fl = 0;
+    SX_CUDA(cudaMemcpy(&fl, s.flags, sizeof(int), cudaMemcpyDeviceToHost));
+    if (fl) return SX_EUNSUPPORTED;  // a shared table filled up / a wide value in K18p: generic path
+    if (ng > cap) {
+      if (!part) return SX_EUNSUPPORTED;  // (the global table was sized from the hint: generic path)
+      cap = ng;
+      continue;
+    }
+    out_keys[0] = sx_col{kt, kc.scale, ng, okey, nullptr, nullptr};
+    scr.release(okey);
+    for (int j = 0; j < naggs; ++j) {
+      out_aggs[j] = sx_col{agg_out_type(aggs[j].op), 0, ng, oagg[j], nullptr, nullptr};
+      scr.release(oagg[j]);
+    }
+    *out_ngroups = ng;
+    return SX_OK;
+  }
+  return SX_EUNSUPPORTED;
+}
+
+}  // namespace sx

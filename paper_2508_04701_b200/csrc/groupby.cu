@@ -19,6 +19,22 @@ SX_EXPORT sx_status sx_groupby_agg(sx_ctx* ctx, const sx_col* cols, int ncols, c
   for (int i = 0; i < nkeys && i < 2; ++i) out_keys[i] = sx_col{};
   for (int i = 0; i < naggs && i < SX_MAX_AGGS; ++i) out_aggs[i] = sx_col{};
   ProfScope ps(ctx, "groupby");
+  // K18: the plain shape (one integer key, plain-column aggregates, no filter) in shared memory
+  sx_status st = gb_simple(ctx, cols, ncols, keys, nkeys, in_sel, nwhere, aggs, naggs, having, groups_hint, out_keys,
+                           out_aggs, out_ngroups);
+  if (st != SX_EUNSUPPORTED) {
+    if (st == SX_OK && ps.on()) {  // key + value columns once; the G output rows once
+      RefCols rc;
+      rc.add(keys[0].col);
+      for (int a = 0; a < naggs; ++a)
+        if (aggs[a].op != SX_COUNT) rc.add(aggs[a].value.t[0].f[0].col);
+      double out_row = type_width(out_keys[0].type);
+      for (int a = 0; a < naggs; ++a) out_row += type_width(out_aggs[a].type);
+      ps.set_bytes(rc.row_bytes(cols, ncols) * (double)cols[keys[0].col].len + out_row * (double)*out_ngroups);
+    }
+    return st;
+  }
+  ctx->err.clear();
   GbPlan plan;
   SX_TRY(gb_plan(ctx, cols, ncols, keys, nkeys, aggs, naggs, having, &plan));
   GbArgs A;
@@ -36,7 +52,7 @@ SX_EXPORT sx_status sx_groupby_agg(sx_ctx* ctx, const sx_col* cols, int ncols, c
   InterpProg prog;
   prog.A = A;
   prog.ovf_flag = ctx->d_flags;
-  sx_status st = gb_run(ctx, prog, plan, in_sel ? in_sel->idx : nullptr, n, groups_hint, out_keys, out_aggs, out_ngroups);
+  st = gb_run(ctx, prog, plan, in_sel ? in_sel->idx : nullptr, n, groups_hint, out_keys, out_aggs, out_ngroups);
   if (st == SX_OK && ps.on()) {  // referenced columns + selection once; the G output rows once
     RefCols rc;
     for (int k = 0; k < nkeys; ++k) rc.add(keys[k].col);

@@ -663,6 +663,42 @@ __global__ void k_direct_fill(const KT* __restrict__ keys, const int32_t* __rest
   }
 }
 
+// Orders stored in strictly increasing orderkey order (checked here; TPC-H's orders are): ONE pass
+// writes the whole int16 date array over [min, max] — thread t takes orders [4t, 4t + 4) and owns
+// the entries from its first key up to the next thread's first key, writing the dates at the keys
+// and the "no order" sentinel in the gaps — instead of a sentinel memset, then scattered 2-byte
+// writes into the (then DRAM-resident) array (read-modify-write of every sector).  bad[0]: a date
+// outside int16 (plan falls back); bad[1]: keys not strictly increasing (host reruns the scatter).
+template <typename KT>
+__global__ void k_date_fill_sorted(const KT* __restrict__ keys, const int32_t* __restrict__ dates, int64_t n,
+                                   long long mn, unsigned long long nbits, int16_t* __restrict__ val, long long* bad) {
+  constexpr int K = 4;
+  bool wide = false, unsorted = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t * K < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o0 = t * K, o1 = min(n, o0 + K);
+    long long prev = o0 > 0 ? (long long)__ldg(keys + o0 - 1) : mn - 1;
+    const long long nb = (long long)nbits;
+    const long long end = o1 < n ? min(nb, (long long)__ldg(keys + o1) - mn) : nb;
+    long long pos = o0 > 0 ? (long long)__ldg(keys + o0) - mn : 0;
+    for (int64_t o = o0; o < o1; ++o) {
+      const long long k = (long long)__ldg(keys + o);
+      const long long off = k - mn;
+      if (k <= prev || off < pos || off >= nb) {
+        unsorted = true;
+        break;
+      }
+      prev = k;
+      for (; pos < off; ++pos) val[pos] = kNoDate;
+      const int32_t x = __ldg(dates + o);
+      wide |= (int32_t)(int16_t)x != x || (int16_t)x == kNoDate;
+      val[pos++] = (int16_t)x;
+    }
+    for (; !unsorted && pos < end; ++pos) val[pos] = kNoDate;
+  }
+  if (wide) atomicExch((unsigned long long*)bad, 1ull);
+  if (unsorted) atomicExch((unsigned long long*)bad + 1, 1ull);
+}
+
 template <typename KT, int OKB>
 struct Q9FusedProg {
   const int32_t *partkey, *suppkey;
@@ -1051,18 +1087,44 @@ struct Q3Fused {
   }
 };
 
+// Groups are staged per warp in shared memory and appended kQ3Flush at a time (one global atomic
+// per flush): 1.13e6 groups appended one atomic each serialise on the cursor (measured 3.16 ms
+// for the pass vs 1.65 + 0.29 ms for the operator plan's probe + group-by).
+constexpr int kQ3Buf = 448, kQ3Flush = 160;  // a warp iteration appends <= 8 * 32 + 32 = 288 groups
 __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n) {
   constexpr int R = 8;
-  const int lane = threadIdx.x & 31;
+  __shared__ int32_t s_key[kBlock / 32][kQ3Buf];
+  __shared__ long long s_rev[kBlock / 32][kQ3Buf];
+  __shared__ int s_cnt[kBlock / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
   unsigned bad = 0, wide = 0;
   bool ovf = false;
+  if (lane == 0) s_cnt[w] = 0;
+  __syncwarp();
   auto emit = [&](int32_t gk, long long s) {
-    const unsigned long long pos = atomicAdd(a.cursor, 1ull);
-    if ((int64_t)pos < a.cap) {
-      a.out_key[pos] = gk;
-      a.out_rev[pos] = make_longlong2(s, s < 0 ? -1 : 0);
+    const int pos = atomicAdd(&s_cnt[w], 1);
+    s_key[w][pos] = gk;
+    s_rev[w][pos] = s;
+  };
+  auto flush = [&](int min_count) {  // warp-collective
+    __syncwarp();
+    const int c = s_cnt[w];
+    if (c < min_count || c == 0) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(a.cursor, (unsigned long long)c);
+    base = __shfl_sync(kFull, base, 0);
+    for (int i = lane; i < c; i += 32) {
+      const int64_t pos = (int64_t)base + i;
+      if (pos < a.cap) {
+        a.out_key[pos] = s_key[w][i];
+        const long long sv = s_rev[w][i];
+        a.out_rev[pos] = make_longlong2(sv, sv < 0 ? -1 : 0);
+      }
     }
+    __syncwarp();
+    if (lane == 0) s_cnt[w] = 0;
+    __syncwarp();
   };
   for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R; wbase < n; wbase += stride) {
     const int64_t r0 = wbase + (int64_t)lane * R;
@@ -1140,7 +1202,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
       if (more && steps == kRunAhead && r < n) wide = 1;
       if (c > 0) emit(ck, s);
     }
+    flush(kQ3Flush);
   }
+  flush(1);
   if (bad) atomicExch(a.flags, 1);
   if (wide) atomicExch(a.flags + 1, 1);
   if (ovf) atomicExch(a.flags + 2, 1);
@@ -1533,13 +1597,54 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       o_min = ht_lo->bm_min;
       o_n = ht_lo->bm ? ht_lo->bm_bits : 0;
       o_bm = ht_lo->bm;
-    } else if (no > 0) {
+    }
+    int16_t* o_date = nullptr;
+    long long* d_bad = nullptr;
+    SX_TRY(alloc(ctx, &d_bad, 2));
+    bag.bufs.push_back(d_bad);
+    SX_CUDA(cudaMemsetAsync(d_bad, 0, 2 * sizeof(long long), ctx->stream));
+    bool filled = false;
+    if (!gather && no > 0) {
+      // orders in key order (the common case): the range from the end keys, one fill pass
+      ProfScope pb(ctx, "hash_build");
+      long long ends[2];
+      const size_t kw = type_width(t->o_orderkey.type);
+      int64_t* hp = ctx->h_pinned + 16;
+      SX_CUDA(cudaMemcpyAsync(hp, t->o_orderkey.data, kw, cudaMemcpyDeviceToHost, ctx->stream));
+      SX_CUDA(cudaMemcpyAsync(hp + 1, (const uint8_t*)t->o_orderkey.data + (no - 1) * kw, kw, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      SX_CUDA(cudaStreamSynchronize(ctx->stream));
+      ends[0] = kw == 4 ? (long long)*(const int32_t*)hp : (long long)hp[0];
+      ends[1] = kw == 4 ? (long long)*(const int32_t*)(hp + 1) : (long long)hp[1];
+      const bool sorted_shape = ends[1] >= ends[0] && (unsigned long long)(ends[1] - ends[0]) + 1 <= (1ull << 30) &&
+                                (unsigned long long)(ends[1] - ends[0]) + 1 >= (unsigned long long)no;
+      if (sorted_shape) {
+        o_min = ends[0];
+        o_n = (unsigned long long)(ends[1] - ends[0]) + 1;
+        SX_TRY(alloc(ctx, &o_date, (size_t)o_n));
+        bag.bufs.push_back(o_date);
+        const int64_t threads = (no + 3) / 4;
+        if (okb4)
+          k_date_fill_sorted<int32_t><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+              (const int32_t*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, o_min, o_n, o_date, d_bad);
+        else
+          k_date_fill_sorted<long long><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+              (const long long*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, o_min, o_n, o_date, d_bad);
+        SX_CHECK_LAUNCH();
+        int64_t bb[2] = {0, 0};
+        SX_TRY(read_i64(ctx, d_bad, bb, 2));
+        filled = bb[1] == 0;  // else: not in key order, the scatter below
+        if (!filled) SX_CUDA(cudaMemsetAsync(d_bad, 0, 2 * sizeof(long long), ctx->stream));
+        pb.set_bytes((type_width(t->o_orderkey.type) + 4.0) * no + 2.0 * o_n);
+      }
+    }
+    if (!gather && no > 0 && !filled) {
       // every order: the key range only (no bitmap); the date array starts as "no order"
       ProfScope pb(ctx, "hash_build");
       long long* d_mm = nullptr;
       SX_TRY(alloc(ctx, &d_mm, 2));
       bag.bufs.push_back(d_mm);
-      const long long init[2] = {LLONG_MAX, LLONG_MIN};
+      long long init[2] = {LLONG_MAX, LLONG_MIN};
       SX_CUDA(cudaMemcpyAsync(d_mm, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
       if (okb4)
         k_key_range<int32_t><<<persistent_grid(ctx, 8, (no + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
@@ -1559,14 +1664,9 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     // o_orderdate as int16 days since 1970 (1880..2059; half the bytes of the direct array and of
     // its lookups); a date outside that range (or equal to the "no order" sentinel) makes the
     // fused plan step aside (SX_EUNSUPPORTED)
-    int16_t* o_date = nullptr;
-    long long* d_bad = nullptr;
-    SX_TRY(alloc(ctx, &o_date, (size_t)(o_n > 0 ? o_n : 1)));
-    bag.bufs.push_back(o_date);
-    SX_TRY(alloc(ctx, &d_bad, 1));
-    bag.bufs.push_back(d_bad);
-    SX_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(long long), ctx->stream));
-    {
+    if (!filled) {
+      SX_TRY(alloc(ctx, &o_date, (size_t)(o_n > 0 ? o_n : 1)));
+      bag.bufs.push_back(o_date);
       ProfScope pb(ctx, "hash_build");
       if (!gather && o_n > 0) SX_CUDA(cudaMemsetAsync(o_date, 0x80, o_n * sizeof(int16_t), ctx->stream));
       // gather: only the green lines' orderkeys (test the bitmap); otherwise every order

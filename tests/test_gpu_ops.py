@@ -122,6 +122,34 @@ def test_groupby_one_key(ctx, n, ng, hint):
     assert g == len(want)
 
 
+SIMPLE_AGGS = [("sum", [(1, [(1, 1, 0)])]), ("count", []), ("min", [(1, [(1, 1, 0)])]), ("max", [(1, [(1, 1, 0)])]),
+               ("avg", [(1, [(1, 1, 0)])], 2), ("max", [(1, [(2, 1, 0)])])]
+
+
+@pytest.mark.parametrize("G,hint,wide", [(4, 4, False), (100, 128, False), (1000, 1024, True), (5000, 5000, False),
+                                         (200_000, 200_000, False), (3000, 1500, False), (300, 0, False)])
+def test_groupby_plain_shape(ctx, G, hint, wide):
+    """K18 (the plain shape: one int64 key, plain-column aggregates; >= 2^20 rows): shared replicas
+    (hint <= 1024), partitioned shared tables (hint > 1024), an under-hinted G (falls back), the
+    key INT64_MIN (the shared tables' EMPTY marker: side slot), values >= 2^40 (exact global
+    path in K18s), an int32 value column — against the oracle."""
+    rng = np.random.default_rng(G)
+    n = (1 << 20) + 12_345
+    keys = np.unique(rng.integers(-(2**63), 2**63 - 1, G * 2, dtype=np.int64))[:G]
+    keys[0] = -(2**63)
+    k = keys[rng.integers(0, G, n)]
+    v = rng.integers(-(10**9), 10**9, n).astype(np.int64)
+    if wide:
+        v[rng.integers(0, n, 50)] = 2**61
+    w = rng.integers(-(2**31), 2**31 - 1, n).astype(np.int32)
+    cols = [sx.col(dev(k)), sx.col(dev(v), A.SX_DEC64, 2), sx.col(dev(w), A.SX_I32)]
+    keys_o, aggs_o, g = ctx.groupby(cols, [(0, "id")], SIMPLE_AGGS, groups_hint=hint)
+    got = canon(keys_o, aggs_o, [a[0] for a in SIMPLE_AGGS])
+    want = oracle.groupby([k, v, w], [0], SIMPLE_AGGS)
+    check_gb(got, want)
+    assert g == len(want)
+
+
 @pytest.mark.parametrize("hint", [4, 64])
 def test_groupby_two_u8_keys_where(ctx, hint):
     rng = np.random.default_rng(11)
