@@ -15,8 +15,8 @@
 //        partition aggregates it in a shared table and writes its groups straight to the output
 //        (partitions hold disjoint keys, so no merge).
 //
-// Exactness (readings R2/R3): shared partial sums are int64 while every value is < 2^40 in
-// magnitude and a CTA sums < 2^23 rows (checked: a row outside takes an exact global 96-bit
+// Exactness (readings R2/R3): shared partial sums are exact while every value is < 2^40 in
+// magnitude and a CTA sums <= 2^22 rows (checked: a row outside takes an exact global 96-bit
 // atomic instead); global sums are 96-bit; AVG = (double)sum / (double)count / 10^scale exactly
 // as the generic path.  Anything else returns SX_EUNSUPPORTED and sx_groupby_agg takes the generic
 // path.  Output group order is unspecified (R13).
@@ -114,18 +114,56 @@ __device__ __forceinline__ uint32_t stab_slot(const STab& t, long long k) {
   return t.S + 1;
 }
 
+// Shared-memory state updates with 32-bit atomics: on sm_100a a 64-bit shared atomicAdd / Min /
+// Max compiles to a CAS spin loop (SASS ATOMS.CAST.SPIN.64).  SUM keeps {u32 lo, i32 hi} in the
+// state word (v = hi * 2^32 + lo for |v| < 2^40; the carry of lo goes into hi; |sum| < 2^62 for
+// <= 2^22 rows), COUNT a u32 in the low word, MIN/MAX the 64-bit value updated by CAS only when
+// the row improves on the value read (rare after the first rows of a group).
 __device__ __forceinline__ void stab_update(const STab& t, const GsSpec& s, uint32_t slot, const long long (&v)[kGsMaxVals]) {
 #pragma unroll
   for (int a = 0; a < kGsMaxStates; ++a) {
     if (a >= s.nst) break;
     unsigned long long* p = t.state(a, slot);
     switch (s.kind[a]) {
-      case ST_SUM: atomicAdd(p, (unsigned long long)pick(v, s.vc[a])); break;
-      case ST_COUNT: atomicAdd(p, 1ull); break;
-      case ST_MIN: atomicMin((long long*)p, pick(v, s.vc[a])); break;
-      default: atomicMax((long long*)p, pick(v, s.vc[a])); break;
+      case ST_SUM: {
+        const long long x = pick(v, s.vc[a]);
+        const unsigned lo = (unsigned)x;
+        const int hi = (int)(x >> 32);
+        const unsigned old = atomicAdd((unsigned*)p, lo);
+        const int h = hi + (old + lo < old ? 1 : 0);
+        if (h) atomicAdd((int*)p + 1, h);
+        break;
+      }
+      case ST_COUNT: atomicAdd((unsigned*)p, 1u); break;
+      case ST_MIN: {
+        const long long x = pick(v, s.vc[a]);
+        long long cur = *(volatile long long*)p;
+        while (x < cur) {
+          const long long old = (long long)atomicCAS(p, (unsigned long long)cur, (unsigned long long)x);
+          if (old == cur) break;
+          cur = old;
+        }
+        break;
+      }
+      default: {
+        const long long x = pick(v, s.vc[a]);
+        long long cur = *(volatile long long*)p;
+        while (x > cur) {
+          const long long old = (long long)atomicCAS(p, (unsigned long long)cur, (unsigned long long)x);
+          if (old == cur) break;
+          cur = old;
+        }
+        break;
+      }
     }
   }
+}
+
+// a shared state word as its value (SUM: hi * 2^32 + lo; COUNT: the low word; MIN/MAX as stored)
+__device__ __forceinline__ unsigned long long stab_value(int kind, unsigned long long w) {
+  if (kind == ST_SUM) return (unsigned long long)(((long long)(int)(w >> 32) << 32) + (long long)(unsigned)w);
+  if (kind == ST_COUNT) return (unsigned long long)(unsigned)w;
+  return w;
 }
 
 // ---- global merge table --------------------------------------------------------------------
@@ -224,10 +262,10 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_local(const __grid_constant_
     for (uint32_t i = threadIdx.x; i <= S; i += blockDim.x) {
       const long long key = x.keys[i];
       // (the side slot holds the key kEmptyKey; its count tells whether it was used)
-      const bool used = i < S ? key != kEmptyKey : *x.state(s.count_state, i) != 0;
+      const bool used = i < S ? key != kEmptyKey : (unsigned)*x.state(s.count_state, i) != 0;
       if (!used) continue;
       const uint64_t gs = g_slot(g, i < S ? key : kEmptyKey, s.flags);
-      for (int a = 0; a < s.nst; ++a) g_add(g, s, gs, a, *x.state(a, i), true);
+      for (int a = 0; a < s.nst; ++a) g_add(g, s, gs, a, stab_value(s.kind[a], *x.state(a, i)), true);
     }
   }
 }
@@ -340,7 +378,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
     __syncthreads();
     // count used slots, claim an output run, write the groups
     for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) {
-      const bool used = i < t.S ? t.keys[i] != kEmptyKey : *t.state(s.count_state, i) != 0;
+      const bool used = i < t.S ? t.keys[i] != kEmptyKey : (unsigned)*t.state(s.count_state, i) != 0;
       if (used) atomicAdd(&s_cnt, 1);
     }
     __syncthreads();
@@ -348,14 +386,14 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) {
-      const bool used = i < t.S ? t.keys[i] != kEmptyKey : *t.state(s.count_state, i) != 0;
+      const bool used = i < t.S ? t.keys[i] != kEmptyKey : (unsigned)*t.state(s.count_state, i) != 0;
       if (!used) continue;
       const int64_t pos = (int64_t)s_base + atomicAdd(&s_cnt, 1);
       if (pos >= s.out_cap) continue;
       unsigned long long lo[kGsMaxStates];
       long long hi[kGsMaxStates];
       for (int a = 0; a < kGsMaxStates; ++a) {
-        lo[a] = a < s.nst ? *t.state(a, i) : 0;
+        lo[a] = a < s.nst ? stab_value(s.kind[a], *t.state(a, i)) : 0;
         hi[a] = (a < s.nst && s.kind[a] == ST_SUM) ? ((long long)lo[a] < 0 ? -1 : 0) : 0;
       }
       put_out_key(s, pos, i < t.S ? t.keys[i] : kEmptyKey);
@@ -471,10 +509,10 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
     for (int c = 0; c <= s.nv; ++c) SX_TRY(scr.get((char**)&outp[c], (size_t)n * width[c]));
     offs.assign((size_t)P + 1, 0);
     SX_TRY(radix_partition_carry(ctx, kd, kd, 1, carry, width, 1 + s.nv, nullptr, n, bits, outp, offs.data()));
-    // a partition sums in one CTA with int64 partials: <= 2^23 rows of |v| < 2^40 (skewed keys
+    // a partition sums in one CTA in the shared SUM words: <= 2^22 rows of |v| < 2^40 (skewed keys
     // beyond that take the generic path)
     for (int p = 0; p < P; ++p)
-      if (offs[p + 1] - offs[p] > (1 << 23)) return SX_EUNSUPPORTED;
+      if (offs[p + 1] - offs[p] > (1 << 22)) return SX_EUNSUPPORTED;
     s.key = outp[0];
     for (int c = 0; c < s.nv; ++c) s.val[c] = outp[1 + c];
     SX_TRY(scr.get(&d_off, (size_t)P + 1));
@@ -526,7 +564,7 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
       const int64_t ctas = (int64_t)ctx->num_sms * std::max(1, per_sm);
       // every CTA sums < 2^23 rows (int64 partial sums of |v| < 2^40 values cannot overflow)
       int64_t chunk = (n + ctas - 1) / ctas;
-      chunk = std::min<int64_t>(chunk, 1 << 22);
+      chunk = std::min<int64_t>(chunk, 1 << 22);  // (<= 2^22 rows per CTA: the shared SUM words)
       const unsigned grid = (unsigned)((n + chunk - 1) / chunk);
       k_gbs_local<<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, n, chunk, S, R, g);
       SX_CHECK_LAUNCH();

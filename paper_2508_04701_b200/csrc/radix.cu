@@ -280,13 +280,137 @@ __global__ void __launch_bounds__(kPartThreads, 3) k_part_scatter_v(const __grid
   }
 }
 
+// K7r: the common case — <= 3 carried columns of 4 or 8 bytes whose first nkeys ARE the key
+// columns, no selection, no row ids.  Every carried value of the tile is loaded into registers
+// when the tile starts (one memory round trip per tile; the staged variant above loads each
+// column after the ranking, one round trip per column: ncu long-scoreboard bound at ~1.4 TB/s),
+// the partition is computed from the loaded key, ranks come from shared atomics, and each column
+// then goes through shared memory to its partition runs.  512 threads x 8 rows = 4096-row tiles.
+constexpr int kRsThreads = 512;
+constexpr int kRsItems = 8;
+constexpr int kRsTile = kRsThreads * kRsItems;
+
+template <int NC>
+__global__ void __launch_bounds__(kRsThreads, 2) k_part_scatter_r(const __grid_constant__ PartSpec s,
+                                                                  const int64_t* __restrict__ offs) {
+  extern __shared__ __align__(16) unsigned char rs_dyn[];
+  unsigned long long* sbuf = (unsigned long long*)rs_dyn;  // [kRsTile]
+  __shared__ int64_t cursor[1 << kMaxPartBits];
+  __shared__ int cnt[1 << kMaxPartBits];
+  __shared__ int start[1 << kMaxPartBits];
+  __shared__ uint16_t s_part[kRsTile];
+  __shared__ int s_warp[kRsThreads / 32];
+  const int P = 1 << s.bits;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int p = tid; p < P; p += kRsThreads) cursor[p] = offs[(int64_t)p * gridDim.x + blockIdx.x];
+  const int64_t lo = blockIdx.x * s.chunk, hi = min(s.n, lo + s.chunk);
+  for (int64_t base = lo; base < hi; base += kRsTile) {
+    for (int p = tid; p < P; p += kRsThreads) cnt[p] = 0;
+    // every carried value of my rows (as 64-bit; 4-byte columns sign-extended like ldv)
+    unsigned long long v[NC][kRsItems];
+#pragma unroll
+    for (int i = 0; i < kRsItems; ++i) {
+      const int64_t idx = base + (int64_t)i * kRsThreads + tid;
+      const bool in = idx < hi;
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        v[c][i] = !in ? 0ull
+                  : s.width[c] == 8 ? (unsigned long long)__ldcs((const long long*)s.carry[c].p + idx)
+                                    : (unsigned long long)(long long)__ldcs((const int32_t*)s.carry[c].p + idx);
+    }
+    __syncthreads();  // cnt[] cleared
+    int pr[kRsItems];  // partition << 16 | rank
+#pragma unroll
+    for (int i = 0; i < kRsItems; ++i) {
+      const int64_t idx = base + (int64_t)i * kRsThreads + tid;
+      pr[i] = -1;
+      if (idx < hi) {
+        uint64_t k = v[0][i];
+        if (NC >= 2 && s.nkeys == 2) k = (k << 32) | (uint32_t)v[NC >= 2 ? 1 : 0][i];
+        const int p = (int)part_of(k, s.bits);
+        pr[i] = (p << 16) | atomicAdd(&cnt[p], 1);  // order within a partition is free (R12)
+      }
+    }
+    __syncthreads();
+    {
+      constexpr int kPer = (1 << kMaxPartBits) / kRsThreads;
+      int loc[kPer], sum = 0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int p = tid * kPer + j;
+        loc[j] = p < P ? cnt[p] : 0;
+        sum += loc[j];
+      }
+      int x = sum;
+      const int w = tid >> 5;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_warp[w] = x;
+      __syncthreads();
+      int wo = 0;
+      for (int k = 0; k < w; ++k) wo += s_warp[k];
+      int run = wo + x - sum;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int p = tid * kPer + j;
+        if (p < P) start[p] = run;
+        run += loc[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kRsItems; ++i) {
+      if (pr[i] < 0) continue;
+      const int p = pr[i] >> 16;
+      pr[i] = start[p] + (pr[i] & 0xffff);
+      s_part[pr[i]] = (uint16_t)p;
+    }
+    const int tcount = (int)min((int64_t)kRsTile, hi - base);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      __syncthreads();  // s_part complete / the previous column's reads done
+#pragma unroll
+      for (int i = 0; i < kRsItems; ++i)
+        if (pr[i] >= 0) sbuf[pr[i]] = v[c][i];
+      __syncthreads();
+      if (s.width[c] == 8) {
+        long long* dst = (long long*)s.out[c];
+        for (int j = tid; j < tcount; j += kRsThreads) {
+          const int p = s_part[j];
+          __stcs(dst + cursor[p] + (j - start[p]), (long long)sbuf[j]);
+        }
+      } else {
+        int32_t* dst = (int32_t*)s.out[c];
+        for (int j = tid; j < tcount; j += kRsThreads) {
+          const int p = s_part[j];
+          __stcs(dst + cursor[p] + (j - start[p]), (int32_t)sbuf[j]);
+        }
+      }
+    }
+    __syncthreads();
+    for (int p = tid; p < P; p += kRsThreads) cursor[p] += cnt[p];
+    __syncthreads();
+  }
+}
+
 // Partition rows (n, through sel) by hash bits; carried columns land partition-contiguous.
 // offsets_h (host, P+1) receives the partition boundaries.
 sx_status radix_partition(sx_ctx* ctx, PartSpec& s, int64_t* offsets_h) {
   const int P = 1 << s.bits;
   // SX_PART_SCATTER=rowid: the round-1 scatter (row ids staged, values re-gathered at write time)
-  const bool v2 = !(getenv("SX_PART_SCATTER") && std::strcmp(getenv("SX_PART_SCATTER"), "rowid") == 0);
-  const int tile_rows = v2 ? kVsTile : kPartTile;
+  const char* mode = getenv("SX_PART_SCATTER");
+  const bool v2 = !(mode && std::strcmp(mode, "rowid") == 0);
+  // K7r when every carried column is 4 or 8 bytes wide, the keys are carried first, <= 3 columns
+  bool reg = v2 && !(mode && std::strcmp(mode, "staged") == 0) && !s.sel && !s.out_rowid && s.ncarry >= s.nkeys &&
+             s.ncarry <= 3;
+  for (int c = 0; reg && c < s.ncarry; ++c) reg = s.width[c] == 4 || s.width[c] == 8;
+  reg = reg && s.carry[0].p == s.k0.p && (s.nkeys == 1 || s.carry[1].p == s.k1.p);
+  reg = reg && (s.nkeys == 1 ? (s.width[0] == 8 || s.k0.type == SX_I32 || s.k0.type == SX_DATE32)
+                             : (s.width[0] == 4 && s.width[1] == 4));
+  const int tile_rows = reg ? kRsTile : v2 ? kVsTile : kPartTile;
   int max_w = 4;
   for (int c = 0; c < s.ncarry; ++c) max_w = std::max(max_w, s.width[c]);
   const size_t vsmem = (size_t)kVsTile * max_w;
@@ -306,7 +430,23 @@ sx_status radix_partition(sx_ctx* ctx, PartSpec& s, int64_t* offsets_h) {
     k_part_hist<<<grid, kPartThreads, 0, SX_STREAM(ctx)>>>(s, hist);
     SX_CHECK_LAUNCH();
     SX_TRY(scan_counts(ctx, hist, m, offs, &total));
-    if (v2) {
+    if (reg) {
+      const size_t rsm = (size_t)kRsTile * sizeof(unsigned long long);
+      switch (s.ncarry) {
+        case 1:
+          SX_CUDA(cudaFuncSetAttribute(k_part_scatter_r<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+          k_part_scatter_r<1><<<grid, kRsThreads, rsm, SX_STREAM(ctx)>>>(s, offs);
+          break;
+        case 2:
+          SX_CUDA(cudaFuncSetAttribute(k_part_scatter_r<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+          k_part_scatter_r<2><<<grid, kRsThreads, rsm, SX_STREAM(ctx)>>>(s, offs);
+          break;
+        default:
+          SX_CUDA(cudaFuncSetAttribute(k_part_scatter_r<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+          k_part_scatter_r<3><<<grid, kRsThreads, rsm, SX_STREAM(ctx)>>>(s, offs);
+          break;
+      }
+    } else if (v2) {
       SX_CUDA(cudaFuncSetAttribute(k_part_scatter_v, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsmem));
       k_part_scatter_v<<<grid, kPartThreads, vsmem, SX_STREAM(ctx)>>>(s, offs, max_w);
     } else {

@@ -11,6 +11,7 @@
 //   otherwise          : LSD radix sort (per pass: tile histograms, per-digit scan, stable scatter)
 #include "compact.cuh"
 #include <cstring>
+#include <type_traits>
 
 using namespace sx;
 
@@ -248,6 +249,14 @@ __device__ __forceinline__ unsigned digit_peers(int d, bool v) {
   return peers;
 }
 
+template <int J, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (J < N) {
+    f(std::integral_constant<int, J>{});
+    static_for<J + 1, N>(f);
+  }
+}
+
 // ---- LSD radix sort -----------------------------------------------------------------
 // Per varying 8-bit digit (least significant first): K13a per-tile digit counts, a multi-block
 // exclusive scan of the digit-major count matrix, K13b stable scatter.  A tile is kLsdThreads x
@@ -405,14 +414,18 @@ __global__ void __launch_bounds__(256) k_os_scan(unsigned* hist) {
   hd[t] = s[t] - v;
 }
 
-template <int ITEMS>
-__global__ void __launch_bounds__(kLsdThreads, 3) k_onesweep(const __grid_constant__ Words src,
+// NW (words per row, the position word last) and ITEMS are compile-time: every word of every row
+// is loaded into registers at the start of the tile (one round trip; ncu on the first version,
+// which re-read the words from global memory after ranking: 52% long-scoreboard stalls, 1.4 TB/s),
+// then each word is staged through shared memory in sorted order and written out.
+template <int ITEMS, int NW>
+__global__ void __launch_bounds__(kLsdThreads, ITEMS * NW > 40 ? 2 : 3) k_onesweep(const __grid_constant__ Words src,
                                                           const __grid_constant__ Words dst, int dword, int shift,
                                                           int64_t n, const unsigned* __restrict__ dbase,
                                                           unsigned long long* status, unsigned* ticket, unsigned pass,
                                                           int pos_only) {
   constexpr int T = kLsdThreads * ITEMS;
-  extern __shared__ uint32_t stage[];  // [nwords][T]
+  extern __shared__ uint32_t stage[];  // [T]
   __shared__ int wcnt[kLsdWarps][256];
   __shared__ int hcnt[256];
   __shared__ int dstart[256];
@@ -420,7 +433,7 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_onesweep(const __grid_consta
   __shared__ int s_warp[kLsdWarps];
   __shared__ uint8_t sdig[T];
   __shared__ unsigned s_tile;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = src.nwords;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   for (int j = threadIdx.x; j < kLsdWarps * 256; j += kLsdThreads) (&wcnt[0][0])[j] = 0;
   hcnt[threadIdx.x] = 0;
@@ -429,26 +442,40 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_onesweep(const __grid_consta
   const int64_t base = tile * (int64_t)T;
   const unsigned long long agg_tag = (unsigned long long)(2u * pass + 1u) << 32;
   const unsigned long long inc_tag = (unsigned long long)(2u * pass + 2u) << 32;
-  // 1. the tile's digits (all loads in flight together) and its digit counts, published before the
-  //    (longer) stable ranking so that successors' look-backs find them early
-  int dig[ITEMS], rank[ITEMS];
+  // 1. every word of the tile's rows (the last pass needs only the digit and position words)
+  // dr[i] = digit << 16 | rank (rank: within the warp, then within the tile); -1 past the end.
+  // The digit word is picked with masks, not a select on `dword`, which the compiler turns into a
+  // dynamic index of val[] and moves val[] to local memory.
+  uint32_t val[NW][ITEMS];
+  int dr[ITEMS];
+  uint32_t dmask[NW];
+#pragma unroll
+  for (int j = 0; j < NW; ++j) dmask[j] = 0u - (uint32_t)(j == dword);
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int64_t e = base + (int64_t)w * 32 * ITEMS + i * 32 + lane;
-    dig[i] = e < n ? (int)((__ldcs(src.w[dword] + e) >> shift) & 0xff) : -1;
+    const bool in = e < n;
+    uint32_t dw = 0;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      val[j][i] = (in && (!pos_only || dmask[j] || j == NW - 1)) ? __ldcs(src.w[j] + e) : 0u;
+      dw |= val[j][i] & dmask[j];
+    }
+    dr[i] = in ? (int)((dw >> shift) & 0xff) << 16 : -1;
   }
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i)
-    if (dig[i] >= 0) atomicAdd(&hcnt[dig[i]], 1);
+    if (dr[i] >= 0) atomicAdd(&hcnt[dr[i] >> 16], 1);
   __syncthreads();
+  // the tile's digit counts, published before the (longer) stable ranking
   const int tcnt = hcnt[threadIdx.x];
   st_relaxed(status + tile * 256 + threadIdx.x, (tile == 0 ? inc_tag : agg_tag) | (unsigned)tcnt);
   // 2. stable ranks: per-warp running digit counters over (item, lane) order
   const unsigned lt = lanemask_lt();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const bool v = dig[i] >= 0;
-    const int d = v ? dig[i] : 0;
+    const bool v = dr[i] >= 0;
+    const int d = v ? dr[i] >> 16 : 0;
     const unsigned peers = digit_peers(d, v);
     const int leader = __ffs(peers) - 1;
     int r = 0;
@@ -456,7 +483,7 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_onesweep(const __grid_consta
     __syncwarp();
     if (v && lane == leader) wcnt[w][d] += __popc(peers);
     __syncwarp();
-    rank[i] = r;
+    if (v) dr[i] |= r;
   }
   __syncthreads();
   {
@@ -489,10 +516,12 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_onesweep(const __grid_consta
 #pragma unroll
         for (int q = 0; q < 4; ++q) sw[q] = j - q >= 0 ? ld_relaxed(status + (j - q) * 256 + d) : inc_tag;
 #pragma unroll
-        for (int q = 0; q < 4 && !done; ++q) {
-          while ((sw[q] >> 32) < (2u * pass + 1u)) sw[q] = ld_relaxed(status + (j - q) * 256 + d);
-          if (j - q >= 0) excl += (uint32_t)sw[q];
-          if ((sw[q] >> 32) == (2u * pass + 2u)) done = true;
+        for (int q = 0; q < 4; ++q) {
+          if (!done) {
+            while ((sw[q] >> 32) < (2u * pass + 1u)) sw[q] = ld_relaxed(status + (j - q) * 256 + d);
+            if (j - q >= 0) excl += (uint32_t)sw[q];
+            if ((sw[q] >> 32) == (2u * pass + 2u)) done = true;
+          }
         }
         j -= 4;
       }
@@ -501,37 +530,35 @@ __global__ void __launch_bounds__(kLsdThreads, 3) k_onesweep(const __grid_consta
     s_off[d] = (int64_t)dbase[d] + excl;
   }
   __syncthreads();
+  // 4. sorted positions; then each word through shared memory to its digit run
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    if (dig[i] < 0) continue;
-    const int64_t e = base + (int64_t)w * 32 * ITEMS + i * 32 + lane;
-    const int pos = dstart[dig[i]] + wcnt[w][dig[i]] + rank[i];
-    sdig[pos] = (uint8_t)dig[i];
-    if (pos_only) {
-      stage[pos] = __ldg(src.w[nw - 1] + e);
-    } else {
-      for (int j = 0; j < nw; ++j) stage[j * T + pos] = __ldg(src.w[j] + e);
-    }
+    if (dr[i] < 0) continue;
+    const int d = dr[i] >> 16;
+    dr[i] = (d << 16) | ((dr[i] & 0xffff) + dstart[d] + wcnt[w][d]);
+    sdig[dr[i] & 0xffff] = (uint8_t)d;
   }
-  __syncthreads();
   const int tcount = (int)min((int64_t)T, n - base);
-  if (pos_only) {
+  static_for<0, NW>([&](auto jc) {  // compile-time word index: val stays in registers
+    constexpr int j = decltype(jc)::value;
+    if (pos_only && j != NW - 1) return;
+    __syncthreads();  // (first word: sdig complete; later words: the previous word's reads done)
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (dr[i] >= 0) stage[dr[i] & 0xffff] = val[j][i];
+    __syncthreads();
+    uint32_t* out = dst.w[j];
     for (int p = threadIdx.x; p < tcount; p += kLsdThreads) {
       const int d = sdig[p];
-      __stcs(dst.w[nw - 1] + s_off[d] + (p - dstart[d]), stage[p]);
+      __stcs(out + s_off[d] + (p - dstart[d]), stage[p]);
     }
-  } else {
-    for (int p = threadIdx.x; p < tcount; p += kLsdThreads) {
-      const int d = sdig[p];
-      const int64_t g = s_off[d] + (p - dstart[d]);
-      for (int j = 0; j < nw; ++j) __stcs(dst.w[j] + g, stage[j * T + p]);
-    }
-  }
+  });
 }
 
-template <int ITEMS>
+template <int ITEMS, int NW>
 sx_status onesweep_sort(sx_ctx* ctx, Scratch& scr, Words*& a, Words*& b, int nwords, int64_t n,
                         const std::vector<std::pair<int, int>>& digits) {
+  if (nwords != NW) return set_err(ctx, SX_EINVAL, "onesweep: %d words", nwords);
   constexpr int T = kLsdThreads * ITEMS;
   const int64_t ntiles = (n + T - 1) / T;
   // sort digits, least significant first (the position word is carried, never sorted on)
@@ -563,11 +590,11 @@ sx_status onesweep_sort(sx_ctx* ctx, Scratch& scr, Words*& a, Words*& b, int nwo
   SX_CHECK_LAUNCH();
   k_os_scan<<<np, 256, 0, SX_STREAM(ctx)>>>(hist);
   SX_CHECK_LAUNCH();
-  const size_t smem = (size_t)nwords * T * sizeof(uint32_t);
-  SX_CUDA(cudaFuncSetAttribute(k_onesweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = (size_t)T * sizeof(uint32_t);
+  SX_CUDA(cudaFuncSetAttribute(k_onesweep<ITEMS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int q = 0; q < np; ++q) {
     const int pos_only = q == np - 1;  // the last pass only needs the positions in order
-    k_onesweep<ITEMS><<<(unsigned)ntiles, kLsdThreads, smem, SX_STREAM(ctx)>>>(
+    k_onesweep<ITEMS, NW><<<(unsigned)ntiles, kLsdThreads, smem, SX_STREAM(ctx)>>>(
         *a, *b, pass[q].first, pass[q].second, n, hist + q * 256, status, tickets + q, (unsigned)q, pos_only);
     SX_CHECK_LAUNCH();
     std::swap(a, b);
@@ -765,9 +792,16 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
       else if (nwords <= 6) SX_TRY(lsd_sort<8>(ctx, scr, a, b, nwords, n, digits));
       else SX_TRY(lsd_sort<4>(ctx, scr, a, b, nwords, n, digits));
     } else {
-      if (nwords <= 3) SX_TRY(onesweep_sort<16>(ctx, scr, a, b, nwords, n, digits));
-      else if (nwords <= 6) SX_TRY(onesweep_sort<8>(ctx, scr, a, b, nwords, n, digits));
-      else SX_TRY(onesweep_sort<4>(ctx, scr, a, b, nwords, n, digits));
+      switch (nwords) {  // registers: ITEMS x NW words per thread
+        case 2: SX_TRY((onesweep_sort<16, 2>(ctx, scr, a, b, nwords, n, digits))); break;
+        case 3: SX_TRY((onesweep_sort<16, 3>(ctx, scr, a, b, nwords, n, digits))); break;
+        case 4: SX_TRY((onesweep_sort<12, 4>(ctx, scr, a, b, nwords, n, digits))); break;
+        case 5: SX_TRY((onesweep_sort<8, 5>(ctx, scr, a, b, nwords, n, digits))); break;
+        case 6: SX_TRY((onesweep_sort<8, 6>(ctx, scr, a, b, nwords, n, digits))); break;
+        case 7: SX_TRY((onesweep_sort<6, 7>(ctx, scr, a, b, nwords, n, digits))); break;
+        case 8: SX_TRY((onesweep_sort<6, 8>(ctx, scr, a, b, nwords, n, digits))); break;
+        default: SX_TRY((onesweep_sort<5, 9>(ctx, scr, a, b, nwords, n, digits))); break;
+      }
     }
     // positions (last word) of the first outn sorted rows -> row ids
     GatherSpec none;

@@ -664,36 +664,52 @@ __global__ void k_direct_fill(const KT* __restrict__ keys, const int32_t* __rest
 }
 
 // Orders stored in strictly increasing orderkey order (checked here; TPC-H's orders are): ONE pass
-// writes the whole int16 date array over [min, max] — thread t takes orders [4t, 4t + 4) and owns
-// the entries from its first key up to the next thread's first key, writing the dates at the keys
-// and the "no order" sentinel in the gaps — instead of a sentinel memset, then scattered 2-byte
-// writes into the (then DRAM-resident) array (read-modify-write of every sector).  bad[0]: a date
-// outside int16 (plan falls back); bad[1]: keys not strictly increasing (host reruns the scatter).
+// writes the whole int16 date array over [min, max].  A warp takes 256 consecutive orders and owns
+// the array entries from their first key up to the next warp's first key: it fills them with the
+// "no order" sentinel using 16-byte stores, then (after __syncwarp) writes each order's date at its
+// key.  This replaces a sentinel memset followed by scattered 2-byte writes into the (then
+// DRAM-resident) array — read-modify-write of every sector — and a per-thread gap-filling
+// version (2-byte stores 32 sectors apart per warp instruction: 4.2 ms).  bad[0]: a date outside
+// int16 (plan falls back); bad[1]: keys not strictly increasing (host reruns the scatter fill).
 template <typename KT>
 __global__ void k_date_fill_sorted(const KT* __restrict__ keys, const int32_t* __restrict__ dates, int64_t n,
                                    long long mn, unsigned long long nbits, int16_t* __restrict__ val, long long* bad) {
-  constexpr int K = 4;
+  constexpr int K = 8, W = 32 * K;
+  const int lane = threadIdx.x & 31;
   bool wide = false, unsorted = false;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t * K < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o0 = t * K, o1 = min(n, o0 + K);
-    long long prev = o0 > 0 ? (long long)__ldg(keys + o0 - 1) : mn - 1;
-    const long long nb = (long long)nbits;
-    const long long end = o1 < n ? min(nb, (long long)__ldg(keys + o1) - mn) : nb;
-    long long pos = o0 > 0 ? (long long)__ldg(keys + o0) - mn : 0;
-    for (int64_t o = o0; o < o1; ++o) {
-      const long long k = (long long)__ldg(keys + o);
-      const long long off = k - mn;
-      if (k <= prev || off < pos || off >= nb) {
+  const long long nb = (long long)nbits;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c * W < n; c += warps) {
+    const int64_t o0 = c * W, o1 = min(n, o0 + W);
+    const long long p0 = o0 > 0 ? (long long)__ldg(keys + o0) - mn : 0;
+    const long long p1 = o1 < n ? (long long)__ldg(keys + o1) - mn : nb;
+    if (p0 < 0 || p1 > nb || p1 < p0) {
+      unsorted = true;
+      continue;
+    }
+    // 1. sentinel over [p0, p1): scalar head and tail, 8 entries per 16-byte store between
+    const long long a = min(p1, (p0 + 7) & ~7ll), b = max(a, p1 & ~7ll);
+    if (p0 + lane < a) val[p0 + lane] = kNoDate;
+    if (b + lane < p1) val[b + lane] = kNoDate;
+    const uint4 sent = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+    for (long long u = a / 8 + lane; u < b / 8; u += 32) __stcs((uint4*)val + u, sent);
+    __syncwarp();
+    // 2. the dates at the keys (and the order check)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t o = o0 + k * 32 + lane;
+      if (o >= o1) continue;
+      const long long key = (long long)__ldg(keys + o);
+      const long long prev = o > 0 ? (long long)__ldg(keys + o - 1) : mn - 1;
+      const long long off = key - mn;
+      if (key <= prev || off < p0 || off >= p1) {
         unsorted = true;
-        break;
+        continue;
       }
-      prev = k;
-      for (; pos < off; ++pos) val[pos] = kNoDate;
       const int32_t x = __ldg(dates + o);
       wide |= (int32_t)(int16_t)x != x || (int16_t)x == kNoDate;
-      val[pos++] = (int16_t)x;
+      val[off] = (int16_t)x;
     }
-    for (; !unsorted && pos < end; ++pos) val[pos] = kNoDate;
   }
   if (wide) atomicExch((unsigned long long*)bad, 1ull);
   if (unsorted) atomicExch((unsigned long long*)bad + 1, 1ull);
@@ -1210,6 +1226,28 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
   if (ovf) atomicExch(a.flags + 2, 1);
 }
 
+// Q3 carries of each group: the order with that key by binary search of o_orderkey (orders in
+// strictly increasing key order — any key not found sets *notfound and the plan steps aside).
+__global__ void k_q3_carry(const int32_t* __restrict__ gk, int64_t ng, const int32_t* __restrict__ okey, int64_t no,
+                           const int32_t* __restrict__ odate, const int32_t* __restrict__ oprio, int32_t* out_date,
+                           int32_t* out_prio, int* notfound) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ng; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = gk[i];
+    int64_t lo = 0, hi = no;  // first position with okey >= k
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(okey + mid) < k) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < no && __ldg(okey + lo) == k) {
+      out_date[i] = __ldg(odate + lo);
+      out_prio[i] = __ldg(oprio + lo);
+    } else {
+      atomicExch(notfound, 1);
+    }
+  }
+}
+
 static const char* kNation[25] = {"ALGERIA", "ARGENTINA", "BRAZIL", "CANADA", "EGYPT", "ETHIOPIA", "FRANCE",
                                   "GERMANY", "INDIA", "INDONESIA", "IRAN", "IRAQ", "JAPAN", "JORDAN", "KENYA",
                                   "MOROCCO", "MOZAMBIQUE", "PERU", "CHINA", "ROMANIA", "SAUDI ARABIA", "VIETNAM",
@@ -1366,13 +1404,26 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   bag.keep(sel_o);
   sx_col okey[1] = {t->o_orderkey};
   sx_ht* ht_o;
-  SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, 1, &ht_o));
-  bag.keep(ht_o);
   // 3+4 fused (default; SX_Q3_PLAN=ops forces the operator-at-a-time steps below): one pass over
-  // lineitem probes the orders bitmap and sums revenue per orderkey run (k_q3_fused), then the
-  // groups' o_orderdate / o_shippriority come from a probe of the orders build with the group keys.
+  // lineitem probes the orders' exact key bitmap (a membership-only build: no table, no direct
+  // array) and sums revenue per orderkey run (k_q3_fused); the groups' o_orderdate /
+  // o_shippriority then come from a binary search of o_orderkey (orders in key order; any key not
+  // found there sends the plan to the operator steps, which build the full table).
   const bool ops_plan = getenv("SX_Q3_PLAN") && std::strcmp(getenv("SX_Q3_PLAN"), "ops") == 0;
-  if (!ops_plan && ht_o->bm && ht_o->nkeys == 1 && ht_o->key_bytes == 4 && w4(t->l_orderkey) &&
+  const bool fused_shape = !ops_plan && w4(t->o_orderkey) && w4(t->o_orderdate) && w4(t->o_shippriority);
+  SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, fused_shape ? (SX_BUILD_UNIQUE | SX_BUILD_MEMBERSHIP) : 1,
+                       &ht_o));
+  bag.keep(ht_o);
+  auto full_build = [&]() -> sx_status {  // the operator plan needs the probe-able build
+    if (ht_o->slots || ht_o->direct) return SX_OK;
+    sx_ht_destroy(ctx, ht_o);
+    bag.hts.pop_back();
+    ht_o = nullptr;
+    SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, 1, &ht_o));
+    bag.keep(ht_o);
+    return SX_OK;
+  };
+  if (fused_shape && ht_o->bm && ht_o->nkeys == 1 && ht_o->key_bytes == 4 && w4(t->l_orderkey) &&
       w4(t->l_shipdate) && w8(t->l_extendedprice) && w8(t->l_discount) &&
       t->l_shipdate.len == t->l_orderkey.len && t->l_extendedprice.len == t->l_orderkey.len &&
       t->l_discount.len == t->l_orderkey.len && t->l_orderkey.len > 0) {
@@ -1411,21 +1462,32 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       // algorithmic bytes: l_orderkey + l_shipdate once, ext + disc of the joined rows, the groups
       pg.set_bytes(8.0 * n + 16.0 * cnt * 2.0 + 20.0 * cnt);
     }
+    bool carried = false;
+    sx_col pay[2];
     if (!fl[0] && !fl[1] && !fl[2] && cnt <= gcap) {
+      ProfScope pc(ctx, "probe_inner");
+      int32_t *cd, *cp;
+      SX_TRY(alloc(ctx, &cd, (size_t)std::max<int64_t>(cnt, 1)));
+      bag.bufs.push_back(cd);
+      SX_TRY(alloc(ctx, &cp, (size_t)std::max<int64_t>(cnt, 1)));
+      bag.bufs.push_back(cp);
+      SX_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(int), ctx->stream));
+      if (cnt > 0) {
+        k_q3_carry<<<persistent_grid(ctx, 8, (cnt + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+            gk, cnt, (const int32_t*)t->o_orderkey.data, t->o_orderkey.len, (const int32_t*)t->o_orderdate.data,
+            (const int32_t*)t->o_shippriority.data, cd, cp, a.flags);
+        SX_CHECK_LAUNCH();
+      }
+      int nf = 0;
+      SX_CUDA(cudaMemcpy(&nf, a.flags, sizeof(int), cudaMemcpyDeviceToHost));
+      carried = nf == 0;
+      pay[0] = sx_col{t->o_orderdate.type, 0, cnt, cd, nullptr, nullptr};
+      pay[1] = sx_col{t->o_shippriority.type, 0, cnt, cp, nullptr, nullptr};
+      pc.set_bytes(4.0 * cnt * 3 + 8.0 * cnt);
+    }
+    if (carried) {
       sx_col gkc{SX_I32, 0, cnt, gk, nullptr, nullptr};
       sx_col grc{SX_I128, 4, cnt, grev, nullptr, nullptr};
-      sx_col bcols[2] = {t->o_orderdate, t->o_shippriority};
-      int32_t bp[2] = {0, 1};
-      sx_sel jp, jb;
-      sx_col pay[2];
-      SX_TRY(sx_hash_probe(ctx, ht_o, &gkc, 1, &k0, 1, nullptr, nullptr, 0, SX_INNER, bcols, 2, bp, 2, nullptr, 0, &jp,
-                           &jb, pay));
-      bag.keep(jp);
-      bag.keep(jb);
-      bag.keep(pay, 2);
-      if (jp.len != cnt) return set_err(ctx, SX_ECUDA, "Q3: %lld of %lld groups found their order", (long long)jp.len,
-                                        (long long)cnt);
-      // unique build: probe output in probe order, so pay[] aligns with the groups
       sx_col scols[3] = {grc, pay[0], gkc};
       sx_sortkey sks[3] = {{0, 1}, {1, 0}, {2, 0}};
       sx_sel perm;
@@ -1444,8 +1506,9 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       *nrows = perm.len;
       return SX_OK;
     }
-    // unsorted lineitem, a wide revenue term or an overflow: the operator plan below decides
+    // unsorted lineitem or orders, a wide revenue term or an overflow: the operator plan decides
   }
+  SX_TRY(full_build());
   // 3. lineitem with l_shipdate > DATE joined to those orders (unique build: ordered output)
   sx_col lcols[4] = {t->l_orderkey, t->l_shipdate, t->l_extendedprice, t->l_discount};
   sx_pred lship = P(1, SX_GT, p->q3_date);
@@ -1623,7 +1686,7 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
         o_n = (unsigned long long)(ends[1] - ends[0]) + 1;
         SX_TRY(alloc(ctx, &o_date, (size_t)o_n));
         bag.bufs.push_back(o_date);
-        const int64_t threads = (no + 3) / 4;
+        const int64_t threads = (no + 255) / 256 * 32;  // one warp per 256 orders
         if (okb4)
           k_date_fill_sorted<int32_t><<<persistent_grid(ctx, 8, (threads + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
               (const int32_t*)t->o_orderkey.data, (const int32_t*)t->o_orderdate.data, no, o_min, o_n, o_date, d_bad);
