@@ -159,6 +159,55 @@ __device__ __forceinline__ void stab_update(const STab& t, const GsSpec& s, uint
   }
 }
 
+// Compile-time state signature for the common one-value-column shape: states in the canonical
+// order COUNT, [SUM], [MIN], [MAX] of value column 0 (straight-line per-row code); SigRt runs the
+// runtime state list.
+struct SigRt {
+  static constexpr bool kFixed = false;
+};
+template <bool SUM, bool MIN, bool MAX>
+struct SigFix {
+  static constexpr bool kFixed = true, kHasSum = SUM, kHasMin = MIN, kHasMax = MAX;
+  static constexpr int kSum = 1, kMin = 1 + SUM, kMax = 1 + SUM + MIN;
+};
+
+__device__ __forceinline__ void sh_sum(unsigned long long* p, long long x) {
+  const unsigned lo = (unsigned)x;
+  const int hi = (int)(x >> 32);
+  const unsigned old = atomicAdd((unsigned*)p, lo);
+  const int h = hi + (old + lo < old ? 1 : 0);
+  if (h) atomicAdd((int*)p + 1, h);
+}
+__device__ __forceinline__ void sh_min(unsigned long long* p, long long x) {
+  long long cur = *(volatile long long*)p;
+  while (x < cur) {
+    const long long old = (long long)atomicCAS(p, (unsigned long long)cur, (unsigned long long)x);
+    if (old == cur) break;
+    cur = old;
+  }
+}
+__device__ __forceinline__ void sh_max(unsigned long long* p, long long x) {
+  long long cur = *(volatile long long*)p;
+  while (x > cur) {
+    const long long old = (long long)atomicCAS(p, (unsigned long long)cur, (unsigned long long)x);
+    if (old == cur) break;
+    cur = old;
+  }
+}
+
+template <class SIG>
+__device__ __forceinline__ void stab_update_t(const STab& t, const GsSpec& s, uint32_t slot,
+                                              const long long (&v)[kGsMaxVals]) {
+  if constexpr (SIG::kFixed) {
+    atomicAdd((unsigned*)t.state(0, slot), 1u);
+    if constexpr (SIG::kHasSum) sh_sum(t.state(SIG::kSum, slot), v[0]);
+    if constexpr (SIG::kHasMin) sh_min(t.state(SIG::kMin, slot), v[0]);
+    if constexpr (SIG::kHasMax) sh_max(t.state(SIG::kMax, slot), v[0]);
+  } else {
+    stab_update(t, s, slot, v);
+  }
+}
+
 // a shared state word as its value (SUM: hi * 2^32 + lo; COUNT: the low word; MIN/MAX as stored)
 __device__ __forceinline__ unsigned long long stab_value(int kind, unsigned long long w) {
   if (kind == ST_SUM) return (unsigned long long)(((long long)(int)(w >> 32) << 32) + (long long)(unsigned)w);
@@ -202,6 +251,7 @@ __device__ __forceinline__ void g_row(const GsGlobal& g, const GsSpec& s, long l
 }
 
 // ---- K18s ----------------------------------------------------------------------------------
+template <class SIG>
 __global__ void __launch_bounds__(kGsThreads) k_gbs_local(const __grid_constant__ GsSpec s, int64_t n, int64_t chunk,
                                                           uint32_t S, int R, const __grid_constant__ GsGlobal g) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -230,7 +280,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_local(const __grid_constant_
       const bool in = r < hi;
       k[u] = in ? ld_key(s, r) : 0;
 #pragma unroll
-      for (int c = 0; c < kGsMaxVals; ++c) v[u][c] = (in && c < s.nv) ? ld_v(s, c, r) : 0;
+      for (int c = 0; c < kGsMaxVals; ++c) v[u][c] = (in && c < (SIG::kFixed ? 1 : s.nv)) ? ld_v(s, c, r) : 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -238,7 +288,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_local(const __grid_constant_
       if (r >= hi) continue;
       bool sm = true;
 #pragma unroll
-      for (int c = 0; c < kGsMaxVals; ++c) sm = sm && (c >= s.nv || small_v(v[u][c]));
+      for (int c = 0; c < kGsMaxVals; ++c) sm = sm && (c >= (SIG::kFixed ? 1 : s.nv) || small_v(v[u][c]));
       if (!sm) {
         g_row(g, s, k[u], v[u]);
         continue;
@@ -248,7 +298,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_local(const __grid_constant_
         full = true;
         continue;
       }
-      stab_update(t, s, slot, v[u]);
+      stab_update_t<SIG>(t, s, slot, v[u]);
     }
   }
   if (full) atomicExch(s.flags, 1);
@@ -329,6 +379,7 @@ __global__ void k_gbs_emit(const __grid_constant__ GsSpec s, const __grid_consta
 // One CTA per partition (grid-stride over partitions): shared table of kGsPartSlots slots, the
 // partition's rows [off[p], off[p+1]) of the partitioned key/value columns, then its groups are
 // appended to the output (one atomic per CTA).
+template <class SIG>
 __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__ GsSpec s, const int64_t* __restrict__ off,
                                                          int P, const __grid_constant__ GsGlobal g) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -353,7 +404,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
         const bool in = r < hi;
         k[u] = in ? ld_key(s, r) : 0;
 #pragma unroll
-        for (int c = 0; c < kGsMaxVals; ++c) v[u][c] = (in && c < s.nv) ? ld_v(s, c, r) : 0;
+        for (int c = 0; c < kGsMaxVals; ++c) v[u][c] = (in && c < (SIG::kFixed ? 1 : s.nv)) ? ld_v(s, c, r) : 0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -361,7 +412,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
         if (r >= hi) continue;
         bool sm = true;
 #pragma unroll
-        for (int c = 0; c < kGsMaxVals; ++c) sm = sm && (c >= s.nv || small_v(v[u][c]));
+        for (int c = 0; c < kGsMaxVals; ++c) sm = sm && (c >= (SIG::kFixed ? 1 : s.nv) || small_v(v[u][c]));
         if (!sm) {
           full = true;  // exactness needs the 96-bit path: the host reruns generically
           continue;
@@ -371,7 +422,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
           full = true;
           continue;
         }
-        stab_update(t, s, slot, v[u]);
+        stab_update_t<SIG>(t, s, slot, v[u]);
       }
     }
     if (full) atomicExch(s.flags, 1);
@@ -402,6 +453,21 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
     __syncthreads();
   }
   (void)g;
+}
+
+template <class F>
+sx_status with_sig(int sig, F&& f) {
+  switch (sig) {
+    case 0: return f(SigFix<false, false, false>{});
+    case 1: return f(SigFix<true, false, false>{});
+    case 2: return f(SigFix<false, true, false>{});
+    case 3: return f(SigFix<true, true, false>{});
+    case 4: return f(SigFix<false, false, true>{});
+    case 5: return f(SigFix<true, false, true>{});
+    case 6: return f(SigFix<false, true, true>{});
+    case 7: return f(SigFix<true, true, true>{});
+    default: return f(SigRt{});
+  }
 }
 
 bool plain_col_expr(const sx_expr& e, int* col) {
@@ -476,6 +542,31 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
     if (a < 0) return SX_EUNSUPPORTED;
     s.agg_state[j] = a;
   }
+  // the fixed signature (one value column; COUNT, SUM, MIN, MAX at most once each): states in the
+  // canonical order COUNT, SUM, MIN, MAX
+  int sig = -1;  // bit 0 SUM, bit 1 MIN, bit 2 MAX
+  if (s.nv == 1) {
+    int seen[4] = {0, 0, 0, 0}, remap[kGsMaxStates];
+    bool ok = true;
+    for (int a = 0; a < s.nst; ++a) ok = ok && ++seen[s.kind[a]] == 1;
+    if (ok) {
+      const bool hs = seen[ST_SUM], hm = seen[ST_MIN], hx = seen[ST_MAX];
+      const int idx[4] = {1, 0, 1 + hs, 1 + hs + hm};  // by kind: SUM, COUNT, MIN, MAX
+      int kind[kGsMaxStates], vc[kGsMaxStates];
+      for (int a = 0; a < s.nst; ++a) {
+        remap[a] = idx[s.kind[a]];
+        kind[remap[a]] = s.kind[a];
+        vc[remap[a]] = s.vc[a];
+      }
+      for (int a = 0; a < s.nst; ++a) {
+        s.kind[a] = kind[a];
+        s.vc[a] = vc[a];
+      }
+      for (int j = 0; j < naggs; ++j) s.agg_state[j] = remap[s.agg_state[j]];
+      s.count_state = 0;
+      sig = (hs ? 1 : 0) | (hm ? 2 : 0) | (hx ? 4 : 0);
+    }
+  }
   for (int c = 0; c < s.nv; ++c)
     if ((uintptr_t)s.val[c] % 16) return SX_EUNSUPPORTED;
   if ((uintptr_t)s.key % 16) return SX_EUNSUPPORTED;
@@ -532,12 +623,16 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
     if (part) {
       const int P = 1 << bits;
       const size_t smem = (size_t)(kGsPartSlots + 1) * 8 * (1 + s.nst);
-      SX_CUDA(cudaFuncSetAttribute(k_gbs_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int per_sm = 0;
-      SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbs_part, kGsThreads, smem));
-      const unsigned grid = (unsigned)std::min<int64_t>(P, (int64_t)ctx->num_sms * std::max(1, per_sm));
-      k_gbs_part<<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, d_off, P, g);
-      SX_CHECK_LAUNCH();
+      SX_TRY(with_sig(sig, [&](auto sg) -> sx_status {
+        using SIG = decltype(sg);
+        SX_CUDA(cudaFuncSetAttribute(k_gbs_part<SIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbs_part<SIG>, kGsThreads, smem));
+        const unsigned grid = (unsigned)std::min<int64_t>(P, (int64_t)ctx->num_sms * std::max(1, per_sm));
+        k_gbs_part<SIG><<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, d_off, P, g);
+        SX_CHECK_LAUNCH();
+        return SX_OK;
+      }));
     } else {
       // global merge table: load <= 0.5
       uint64_t C = 64;
@@ -558,16 +653,19 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
       int R = (int)std::max<size_t>(1, std::min<size_t>(32, (96u << 10) / tab));
       while (32 % R) --R;
       const size_t smem = tab * R;
-      SX_CUDA(cudaFuncSetAttribute(k_gbs_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int per_sm = 0;
-      SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbs_local, kGsThreads, smem));
-      const int64_t ctas = (int64_t)ctx->num_sms * std::max(1, per_sm);
-      // every CTA sums < 2^23 rows (int64 partial sums of |v| < 2^40 values cannot overflow)
-      int64_t chunk = (n + ctas - 1) / ctas;
-      chunk = std::min<int64_t>(chunk, 1 << 22);  // (<= 2^22 rows per CTA: the shared SUM words)
-      const unsigned grid = (unsigned)((n + chunk - 1) / chunk);
-      k_gbs_local<<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, n, chunk, S, R, g);
-      SX_CHECK_LAUNCH();
+      SX_TRY(with_sig(sig, [&](auto sg) -> sx_status {
+        using SIG = decltype(sg);
+        SX_CUDA(cudaFuncSetAttribute(k_gbs_local<SIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbs_local<SIG>, kGsThreads, smem));
+        const int64_t ctas = (int64_t)ctx->num_sms * std::max(1, per_sm);
+        int64_t chunk = (n + ctas - 1) / ctas;
+        chunk = std::min<int64_t>(chunk, 1 << 22);  // (<= 2^22 rows per CTA: the shared SUM words)
+        const unsigned grid = (unsigned)((n + chunk - 1) / chunk);
+        k_gbs_local<SIG><<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, n, chunk, S, R, g);
+        SX_CHECK_LAUNCH();
+        return SX_OK;
+      }));
       k_gbs_emit<<<persistent_grid(ctx, 4, (C + kBlock) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(s, g);
       SX_CHECK_LAUNCH();
     }

@@ -358,6 +358,7 @@ struct Q6Prog {
   int32_t date_lo, date_hi;
   int64_t disc_lo, disc_hi, qty_lt;
   int* ovf_flag;
+  int lazy3;  // 1: discount first, quantity/price only where the discount qualifies (3 levels)
   static constexpr int kMaxNst = 2;
   static constexpr int kUnrollStates = 2;
   static constexpr bool kSortedOK = false;
@@ -415,16 +416,38 @@ struct Q6Prog {
       sd[4] = b.x; sd[5] = b.y; sd[6] = b.z; sd[7] = b.w;
 #pragma unroll
       for (int i = 0; i < 8; ++i) alive[i] = sd[i] >= date_lo && sd[i] < date_hi;
+      if (lazy3) {
+        // discount pairs where a shipdate qualifies (~28% of pairs), then quantity / price pairs
+        // only where date and discount qualify (~8%): fewer sectors than loading all three
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool need = alive[2 * j] || alive[2 * j + 1];
-        const longlong2 z = make_longlong2(0, 0);
-        const longlong2 dd = need ? __ldg((const longlong2*)(disc + r0) + j) : z;
-        const longlong2 qq = need ? __ldg((const longlong2*)(qty + r0) + j) : z;
-        const longlong2 ee = need ? __ldg((const longlong2*)(ext + r0) + j) : z;
-        d[2 * j] = dd.x; d[2 * j + 1] = dd.y;
-        q[2 * j] = qq.x; q[2 * j + 1] = qq.y;
-        e[2 * j] = ee.x; e[2 * j + 1] = ee.y;
+        for (int j = 0; j < 4; ++j) {
+          const bool need = alive[2 * j] || alive[2 * j + 1];
+          const longlong2 dd = need ? __ldg((const longlong2*)(disc + r0) + j) : make_longlong2(0, 0);
+          d[2 * j] = dd.x; d[2 * j + 1] = dd.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) alive[i] = alive[i] && d[i] >= disc_lo && d[i] <= disc_hi;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool need = alive[2 * j] || alive[2 * j + 1];
+          const longlong2 z = make_longlong2(0, 0);
+          const longlong2 qq = need ? __ldg((const longlong2*)(qty + r0) + j) : z;
+          const longlong2 ee = need ? __ldg((const longlong2*)(ext + r0) + j) : z;
+          q[2 * j] = qq.x; q[2 * j + 1] = qq.y;
+          e[2 * j] = ee.x; e[2 * j + 1] = ee.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool need = alive[2 * j] || alive[2 * j + 1];
+          const longlong2 z = make_longlong2(0, 0);
+          const longlong2 dd = need ? __ldg((const longlong2*)(disc + r0) + j) : z;
+          const longlong2 qq = need ? __ldg((const longlong2*)(qty + r0) + j) : z;
+          const longlong2 ee = need ? __ldg((const longlong2*)(ext + r0) + j) : z;
+          d[2 * j] = dd.x; d[2 * j + 1] = dd.y;
+          q[2 * j] = qq.x; q[2 * j + 1] = qq.y;
+          e[2 * j] = ee.x; e[2 * j + 1] = ee.y;
+        }
       }
     } else {
 #pragma unroll
@@ -1161,10 +1184,34 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
       }
     }
     const int m = (int)max((int64_t)0, min((int64_t)R, n - r0));
-    // the bitmap words of the shipdate survivors (sorted keys: mostly the same word)
+    // the bitmap words of the 8 rows: keys are sorted, so they lie in the words of the first and
+    // the last row (2 loads for 8 rows; a wider span — or unsorted keys — loads per row)
     bool q[R];
+    {
+      const uint32_t kmin = (uint32_t)a.bm_min, bits = (uint32_t)a.bm_bits;  // (bm_bits <= 2^30)
+      uint32_t off[R];
+      bool cand[R];
 #pragma unroll
-    for (int i = 0; i < R; ++i) q[i] = i < m && a.joins(k[i], sd[i]);
+      for (int i = 0; i < R; ++i) {
+        off[i] = (uint32_t)k[i] - kmin;
+        cand[i] = i < m && sd[i] > a.date && off[i] < bits;
+      }
+      const uint32_t w0 = off[0] >> 5, w1 = off[R - 1] >> 5;  // (used only when m == R)
+      bool anyc = false;
+#pragma unroll
+      for (int i = 0; i < R; ++i) anyc |= cand[i];
+      if (anyc && m == R && off[0] < bits && off[R - 1] < bits && w1 - w0 <= 1) {
+        const uint32_t b0 = __ldg(a.bm + w0), b1 = __ldg(a.bm + w1);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const uint32_t wd = (off[i] >> 5) == w0 ? b0 : b1;
+          q[i] = cand[i] && ((wd >> (off[i] & 31)) & 1u);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < R; ++i) q[i] = cand[i] && ((__ldg(a.bm + (off[i] >> 5)) >> (off[i] & 31)) & 1u);
+      }
+    }
     long long v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) v[i] = q[i] ? a.term(r0 + i, ovf) : 0;
@@ -1360,7 +1407,8 @@ SX_EXPORT sx_status sx_tpch_q6(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     SX_TRY(check_states(ctx, plan, {ST_SUM, ST_COUNT}));
     Q6Prog prog{(const int32_t*)t->l_shipdate.data, (const long long*)t->l_discount.data,
                 (const long long*)t->l_quantity.data, (const long long*)t->l_extendedprice.data, p->q6_date_lo,
-                p->q6_date_hi, p->q6_disc_lo, p->q6_disc_hi, p->q6_qty_lt, ctx->d_flags};
+                p->q6_date_hi, p->q6_disc_lo, p->q6_disc_hi, p->q6_qty_lt, ctx->d_flags,
+                getenv("SX_Q6_LAZY3") && getenv("SX_Q6_LAZY3")[0] == '1' ? 1 : 0};
     SX_TRY(gb_run(ctx, prog, plan, nullptr, t->l_shipdate.len, 1, nullptr, oa, &ng));
     pg.set_bytes(28.0 * t->l_shipdate.len + 24.0);  // 4 columns once + the result
   } else {
@@ -1423,7 +1471,8 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     bag.keep(ht_o);
     return SX_OK;
   };
-  if (fused_shape && ht_o->bm && ht_o->nkeys == 1 && ht_o->key_bytes == 4 && w4(t->l_orderkey) &&
+  if (fused_shape && ht_o->bm && ht_o->bm_bits <= (1ull << 30) && ht_o->bm_min >= INT32_MIN &&
+      ht_o->bm_min <= INT32_MAX && ht_o->nkeys == 1 && ht_o->key_bytes == 4 && w4(t->l_orderkey) &&
       w4(t->l_shipdate) && w8(t->l_extendedprice) && w8(t->l_discount) &&
       t->l_shipdate.len == t->l_orderkey.len && t->l_extendedprice.len == t->l_orderkey.len &&
       t->l_discount.len == t->l_orderkey.len && t->l_orderkey.len > 0) {

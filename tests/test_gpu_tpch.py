@@ -143,9 +143,9 @@ def test_q3_plans(ctx, monkeypatch, case):
     host = dict(host)
     host["lineitem"] = li
     T = tpch.Tpch(ctx, to_dev(host))
-    for over in ({}, dict(q3_limit=1000)):
-        got = T.run("q3", tpch.default_params(**over))
-        want = oracle.run_query("q3", host, oracle.default_params(**over))
+    for lim in (10, 1000):
+        got = T.run("q3", tpch.default_params(q3_limit=lim))
+        want = oracle.run_query("q3", host, limit=lim)
         assert rows_equal(got, want), diff_rows(got, want)
 
 
@@ -163,6 +163,26 @@ def test_orders_not_in_key_order(ctx):
         got = T.run(q)
         want = oracle.run_query(q, host)
         assert rows_equal(got, want), f"{q}: " + diff_rows(got, want)
+
+
+
+@pytest.mark.parametrize("lazy3", ["0", "1"])
+def test_q6_lazy_levels(ctx, monkeypatch, lazy3):
+    """Q6's dense program with two lazy levels (shipdate, then discount/quantity/price) and three
+    (SX_Q6_LAZY3=1: discount gates quantity/price), with boundary values of every predicate."""
+    monkeypatch.setenv("SX_Q6_LAZY3", lazy3)
+    host = gen.cpu_tables(100, seed=23)
+    li = {k: v.copy() for k, v in host["lineitem"].items()}
+    n = len(li["l_shipdate"]) - 5
+    li = {k: v[:n].copy() for k, v in li.items()}
+    rng = np.random.default_rng(2)
+    for col, vals in (("l_shipdate", [8765, 8766, 9130, 9131]), ("l_discount", [4, 5, 7, 8]), ("l_quantity", [2399, 2400])):
+        li[col][rng.choice(n, 2000, replace=False)] = rng.choice(vals, 2000)
+    host = dict(host)
+    host["lineitem"] = li
+    got = tpch.Tpch(ctx, to_dev(host)).run("q6")
+    want = oracle.run_query("q6", host)
+    assert rows_equal(got, want), diff_rows(got, want)
 
 
 
