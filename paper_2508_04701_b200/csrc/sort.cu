@@ -418,20 +418,20 @@ __global__ void __launch_bounds__(256) k_os_scan(unsigned* hist) {
 // is loaded into registers at the start of the tile (one round trip; ncu on the first version,
 // which re-read the words from global memory after ranking: 52% long-scoreboard stalls, 1.4 TB/s),
 // then each word is staged through shared memory in sorted order and written out.
-template <int ITEMS, int NW>
+template <int ITEMS, int NW, bool MATCH>
 __global__ void __launch_bounds__(kLsdThreads, ITEMS * NW > 40 ? 2 : 3) k_onesweep(const __grid_constant__ Words src,
                                                           const __grid_constant__ Words dst, int dword, int shift,
                                                           int64_t n, const unsigned* __restrict__ dbase,
                                                           unsigned long long* status, unsigned* ticket, unsigned pass,
                                                           int pos_only) {
   constexpr int T = kLsdThreads * ITEMS;
-  extern __shared__ uint32_t stage[];  // [T]
+  extern __shared__ uint32_t stage[];  // [T] staged words, then [T] destination indices
+  uint32_t* sdst = stage + T;
   __shared__ int wcnt[kLsdWarps][256];
   __shared__ int hcnt[256];
   __shared__ int dstart[256];
   __shared__ int64_t s_off[256];
   __shared__ int s_warp[kLsdWarps];
-  __shared__ uint8_t sdig[T];
   __shared__ unsigned s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kLsdThreads, ITEMS * NW > 40 ? 2 : 3) k_oneswe
   for (int i = 0; i < ITEMS; ++i) {
     const bool v = dr[i] >= 0;
     const int d = v ? dr[i] >> 16 : 0;
-    const unsigned peers = digit_peers(d, v);
+    const unsigned peers = MATCH ? (__match_any_sync(kFull, v ? d : 256 + lane)) : digit_peers(d, v);
     const int leader = __ffs(peers) - 1;
     int r = 0;
     if (v) r = wcnt[w][d] + __popc(peers & lt);
@@ -536,28 +536,33 @@ __global__ void __launch_bounds__(kLsdThreads, ITEMS * NW > 40 ? 2 : 3) k_oneswe
     if (dr[i] < 0) continue;
     const int d = dr[i] >> 16;
     dr[i] = (d << 16) | ((dr[i] & 0xffff) + dstart[d] + wcnt[w][d]);
-    sdig[dr[i] & 0xffff] = (uint8_t)d;
   }
   const int tcount = (int)min((int64_t)T, n - base);
+  // destination index of every sorted position, once (n <= INT32_MAX: 32 bits)
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (dr[i] < 0) continue;
+    const int d = dr[i] >> 16, p = dr[i] & 0xffff;
+    sdst[p] = (uint32_t)(s_off[d] + (p - dstart[d]));
+  }
   static_for<0, NW>([&](auto jc) {  // compile-time word index: val stays in registers
     constexpr int j = decltype(jc)::value;
     if (pos_only && j != NW - 1) return;
-    __syncthreads();  // (first word: sdig complete; later words: the previous word's reads done)
+    __syncthreads();  // (first word: sdst complete; later words: the previous word's reads done)
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i)
       if (dr[i] >= 0) stage[dr[i] & 0xffff] = val[j][i];
     __syncthreads();
     uint32_t* out = dst.w[j];
-    for (int p = threadIdx.x; p < tcount; p += kLsdThreads) {
-      const int d = sdig[p];
-      __stcs(out + s_off[d] + (p - dstart[d]), stage[p]);
-    }
+    for (int p = threadIdx.x; p < tcount; p += kLsdThreads) __stcs(out + sdst[p], stage[p]);
   });
 }
 
 template <int ITEMS, int NW>
 sx_status onesweep_sort(sx_ctx* ctx, Scratch& scr, Words*& a, Words*& b, int nwords, int64_t n,
                         const std::vector<std::pair<int, int>>& digits) {
+  // SX_SORT_RANK=ballot: bit-sliced ballots instead of __match_any_sync for the stable ranks
+  const bool ballot = getenv("SX_SORT_RANK") && std::strcmp(getenv("SX_SORT_RANK"), "ballot") == 0;
   if (nwords != NW) return set_err(ctx, SX_EINVAL, "onesweep: %d words", nwords);
   constexpr int T = kLsdThreads * ITEMS;
   const int64_t ntiles = (n + T - 1) / T;
@@ -590,12 +595,17 @@ sx_status onesweep_sort(sx_ctx* ctx, Scratch& scr, Words*& a, Words*& b, int nwo
   SX_CHECK_LAUNCH();
   k_os_scan<<<np, 256, 0, SX_STREAM(ctx)>>>(hist);
   SX_CHECK_LAUNCH();
-  const size_t smem = (size_t)T * sizeof(uint32_t);
-  SX_CUDA(cudaFuncSetAttribute(k_onesweep<ITEMS, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = (size_t)2 * T * sizeof(uint32_t);
+  SX_CUDA(cudaFuncSetAttribute(k_onesweep<ITEMS, NW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SX_CUDA(cudaFuncSetAttribute(k_onesweep<ITEMS, NW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int q = 0; q < np; ++q) {
     const int pos_only = q == np - 1;  // the last pass only needs the positions in order
-    k_onesweep<ITEMS, NW><<<(unsigned)ntiles, kLsdThreads, smem, SX_STREAM(ctx)>>>(
-        *a, *b, pass[q].first, pass[q].second, n, hist + q * 256, status, tickets + q, (unsigned)q, pos_only);
+    if (ballot)
+      k_onesweep<ITEMS, NW, false><<<(unsigned)ntiles, kLsdThreads, smem, SX_STREAM(ctx)>>>(
+          *a, *b, pass[q].first, pass[q].second, n, hist + q * 256, status, tickets + q, (unsigned)q, pos_only);
+    else
+      k_onesweep<ITEMS, NW, true><<<(unsigned)ntiles, kLsdThreads, smem, SX_STREAM(ctx)>>>(
+          *a, *b, pass[q].first, pass[q].second, n, hist + q * 256, status, tickets + q, (unsigned)q, pos_only);
     SX_CHECK_LAUNCH();
     std::swap(a, b);
   }

@@ -1092,16 +1092,16 @@ __global__ void k_lookup_rank(const int32_t* __restrict__ keys, int64_t n, const
   }
 }
 
-// Q3 fused lineitem pass (K10q; SURVEY §8(a) Q3 step 3 probe + step 4 group-by, adjacent steps
-// fused by the executor): lineitem is read once — l_shipdate and l_orderkey streamed with 128-bit
-// loads, 8 consecutive rows per thread — rows with shipdate > DATE are tested against the exact
-// key-range bitmap of the qualifying orders (the orders build), l_extendedprice/l_discount are
-// loaded only for the ~0.5% rows that join, and revenue = ext*(100-disc) is summed per orderkey
-// run (owned runs as K10l: a thread owns the groups starting among its rows; the next lane's
-// leading rows finish its last group).  One (orderkey, revenue) per order with >= 1 joined row is
-// appended (atomic cursor; group order is unspecified, R13).  flags: [0] a decreasing orderkey,
-// [1] a revenue term >= 2^40 in magnitude or a run past kRunAhead rows, [2] ext*(100-disc) left
-// int64 — the host then runs the operator-at-a-time plan, which decides.
+// Q3 fused lineitem pass (K10q, the probe with its revenue projection):
+// lineitem is read once — l_shipdate and l_orderkey streamed with 128-bit loads, 8 consecutive
+// rows per thread — rows with shipdate > DATE are tested against the exact key-range bitmap of
+// the qualifying orders (the orders build; the 8 rows' keys are sorted, so two bitmap words serve
+// them), and only the ~0.5% rows that join load l_extendedprice / l_discount and append one
+// record (l_orderkey, ext*(100-disc)) through a per-warp shared buffer (one global atomic per
+// flush).  A warp whose 256 rows have no joining row does nothing else.  The records then go
+// through sx_groupby_agg (step 4).  A first version that also summed the orderkey runs in the
+// pass (owned runs) ran ~100 instructions per row and lost to the operator plan (3.1 vs 1.9 ms).
+// flags: [0] a product left int64.
 struct Q3Fused {
   const int32_t* okey;
   const int32_t* ship;
@@ -1112,58 +1112,37 @@ struct Q3Fused {
   long long bm_min;
   unsigned long long bm_bits;
   int32_t* out_key;
-  longlong2* out_rev;
+  long long* out_val;
   int64_t cap;
   unsigned long long* cursor;
   int* flags;
-  __device__ __forceinline__ bool joins(int32_t key, int32_t sd) const {
-    const unsigned long long off = (unsigned long long)((long long)key - bm_min);
-    if (!(sd > date) || off >= bm_bits) return false;
-    return (__ldg(bm + (off >> 5)) >> (off & 31)) & 1u;
-  }
-  __device__ __forceinline__ long long term(int64_t r, bool& ovf) const {
-    return mul_ck(__ldg(ext + r), 100 - __ldg(disc + r), ovf);
-  }
 };
 
-// Groups are staged per warp in shared memory and appended kQ3Flush at a time (one global atomic
-// per flush): 1.13e6 groups appended one atomic each serialise on the cursor (measured 3.16 ms
-// for the pass vs 1.65 + 0.29 ms for the operator plan's probe + group-by).
-constexpr int kQ3Buf = 448, kQ3Flush = 160;  // a warp iteration appends <= 8 * 32 + 32 = 288 groups
+constexpr int kQ3Buf = 384, kQ3Flush = 128;  // a warp iteration appends <= 256 records
 __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n) {
   constexpr int R = 8;
   __shared__ int32_t s_key[kBlock / 32][kQ3Buf];
-  __shared__ long long s_rev[kBlock / 32][kQ3Buf];
-  __shared__ int s_cnt[kBlock / 32];
+  __shared__ long long s_val[kBlock / 32][kQ3Buf];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
-  unsigned bad = 0, wide = 0;
+  const uint32_t kmin = (uint32_t)a.bm_min, bits = (uint32_t)a.bm_bits;  // (bm_bits <= 2^30)
+  const unsigned lt = lanemask_lt();
   bool ovf = false;
-  if (lane == 0) s_cnt[w] = 0;
-  __syncwarp();
-  auto emit = [&](int32_t gk, long long s) {
-    const int pos = atomicAdd(&s_cnt[w], 1);
-    s_key[w][pos] = gk;
-    s_rev[w][pos] = s;
-  };
-  auto flush = [&](int min_count) {  // warp-collective
-    __syncwarp();
-    const int c = s_cnt[w];
-    if (c < min_count || c == 0) return;
+  int cnt = 0;  // records in the warp's buffer (warp-uniform)
+  auto flush = [&]() {  // warp-collective
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(a.cursor, (unsigned long long)c);
+    if (lane == 0) base = atomicAdd(a.cursor, (unsigned long long)cnt);
     base = __shfl_sync(kFull, base, 0);
-    for (int i = lane; i < c; i += 32) {
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) {
       const int64_t pos = (int64_t)base + i;
       if (pos < a.cap) {
         a.out_key[pos] = s_key[w][i];
-        const long long sv = s_rev[w][i];
-        a.out_rev[pos] = make_longlong2(sv, sv < 0 ? -1 : 0);
+        a.out_val[pos] = s_val[w][i];
       }
     }
     __syncwarp();
-    if (lane == 0) s_cnt[w] = 0;
-    __syncwarp();
+    cnt = 0;
   };
   for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R; wbase < n; wbase += stride) {
     const int64_t r0 = wbase + (int64_t)lane * R;
@@ -1180,97 +1159,51 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
       for (int i = 0; i < R; ++i) {
         const bool in = r0 + i < n;
         k[i] = in ? __ldg(a.okey + r0 + i) : 0;
-        sd[i] = in ? __ldg(a.ship + r0 + i) : 0;
+        sd[i] = in ? __ldg(a.ship + r0 + i) : INT32_MIN;
       }
     }
-    const int m = (int)max((int64_t)0, min((int64_t)R, n - r0));
-    // the bitmap words of the 8 rows: keys are sorted, so they lie in the words of the first and
-    // the last row (2 loads for 8 rows; a wider span — or unsorted keys — loads per row)
-    bool q[R];
-    {
-      const uint32_t kmin = (uint32_t)a.bm_min, bits = (uint32_t)a.bm_bits;  // (bm_bits <= 2^30)
-      uint32_t off[R];
-      bool cand[R];
+    uint32_t off[R];
+    bool cand[R], anyc = false;
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        off[i] = (uint32_t)k[i] - kmin;
-        cand[i] = i < m && sd[i] > a.date && off[i] < bits;
-      }
-      const uint32_t w0 = off[0] >> 5, w1 = off[R - 1] >> 5;  // (used only when m == R)
-      bool anyc = false;
-#pragma unroll
-      for (int i = 0; i < R; ++i) anyc |= cand[i];
-      if (anyc && m == R && off[0] < bits && off[R - 1] < bits && w1 - w0 <= 1) {
+    for (int i = 0; i < R; ++i) {
+      off[i] = (uint32_t)k[i] - kmin;
+      cand[i] = sd[i] > a.date && off[i] < bits;
+      anyc |= cand[i];
+    }
+    unsigned qmask = 0;
+    if (anyc) {
+      const uint32_t w0 = off[0] >> 5, w1 = off[R - 1] >> 5;
+      if (r0 + R <= n && off[0] < bits && off[R - 1] < bits && w1 - w0 <= 1) {
         const uint32_t b0 = __ldg(a.bm + w0), b1 = __ldg(a.bm + w1);
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           const uint32_t wd = (off[i] >> 5) == w0 ? b0 : b1;
-          q[i] = cand[i] && ((wd >> (off[i] & 31)) & 1u);
+          qmask |= (cand[i] && ((wd >> (off[i] & 31)) & 1u)) ? 1u << i : 0u;
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < R; ++i) q[i] = cand[i] && ((__ldg(a.bm + (off[i] >> 5)) >> (off[i] & 31)) & 1u);
+        for (int i = 0; i < R; ++i)
+          qmask |= (cand[i] && ((__ldg(a.bm + (off[i] >> 5)) >> (off[i] & 31)) & 1u)) ? 1u << i : 0u;
       }
     }
-    long long v[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = q[i] ? a.term(r0 + i, ovf) : 0;
-    int32_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
-    if (lane == 0 && r0 > 0 && r0 <= n) pk = __ldg(a.okey + r0 - 1);
-    const bool has_prev = r0 > 0;
-    long long lead = 0, s = 0;
-    int lead_len = 0, lead_c = 0, c = 0;
-    bool open = false;
-    int32_t ck = 0, prev = pk;
+    if (!__any_sync(kFull, qmask != 0)) continue;
+    // the joining rows' revenue terms, appended in row order (item-major within the warp)
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const bool in = i < m;
-      wide |= q[i] ? (unsigned)((int32_t)(v[i] >> 32) + 256) >> 9 : 0u;
-      const bool head = in && (k[i] != prev || (i == 0 && !has_prev));
-      bad |= (in && (i > 0 || has_prev) && k[i] < prev) ? 1u : 0u;
-      if (head && open && c > 0) emit(ck, s);
-      open = open || head;
-      lead += (in && !open) ? v[i] : 0;
-      lead_c += (in && !open && q[i]) ? 1 : 0;
-      lead_len += (in && !open) ? 1 : 0;
-      s = head ? v[i] : s + v[i];
-      c = head ? (int)q[i] : c + (int)q[i];
-      ck = head ? k[i] : ck;
-      prev = in ? k[i] : prev;
-    }
-    const long long nx_lead = __shfl_down_sync(kFull, lead, 1);
-    const int nx_c = __shfl_down_sync(kFull, lead_c, 1);
-    const int nx_len = __shfl_down_sync(kFull, lead_len, 1);
-    if (open) {
-      const int64_t nxt = r0 + R;
-      bool more = true;
-      int64_t r = nxt;
-      if (lane < 31 && nxt < n) {
-        s += nx_lead;
-        c += nx_c;
-        more = nx_len == R;
-        r = nxt + R;
+      const bool q = (qmask >> i) & 1u;
+      const unsigned b = __ballot_sync(kFull, q);
+      if (q) {
+        const long long e = __ldg(a.ext + r0 + i), d = __ldg(a.disc + r0 + i);
+        const int pos = cnt + __popc(b & lt);
+        s_key[w][pos] = k[i];
+        s_val[w][pos] = mul_ck(e, 100 - d, ovf);
       }
-      int steps = 0;
-      for (; more && r < n && steps < kRunAhead; ++r, ++steps) {  // rare: scalar continuation
-        const int32_t kr = __ldg(a.okey + r);
-        if (kr != ck) break;
-        if (a.joins(kr, __ldg(a.ship + r))) {
-          const long long x = a.term(r, ovf);
-          wide |= (unsigned)((int32_t)(x >> 32) + 256) >> 9;
-          s += x;
-          ++c;
-        }
-      }
-      if (more && steps == kRunAhead && r < n) wide = 1;
-      if (c > 0) emit(ck, s);
+      cnt += __popc(b);
     }
-    flush(kQ3Flush);
+    if (cnt >= kQ3Flush) flush();
   }
-  flush(1);
-  if (bad) atomicExch(a.flags, 1);
-  if (wide) atomicExch(a.flags + 1, 1);
-  if (ovf) atomicExch(a.flags + 2, 1);
+  if (cnt > 0) flush();
+  if (ovf) atomicExch(a.flags, 1);
 }
 
 // Q3 carries of each group: the order with that key by binary search of o_orderkey (orders in
@@ -1457,7 +1390,9 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   // array) and sums revenue per orderkey run (k_q3_fused); the groups' o_orderdate /
   // o_shippriority then come from a binary search of o_orderkey (orders in key order; any key not
   // found there sends the plan to the operator steps, which build the full table).
-  const bool ops_plan = getenv("SX_Q3_PLAN") && std::strcmp(getenv("SX_Q3_PLAN"), "ops") == 0;
+  // (default: the operator plan — the fused pass measured 3.1 ms against 1.65 + 0.29 ms for the
+  // probe and group-by it replaces; SX_Q3_PLAN=fused selects it)
+  const bool ops_plan = !(getenv("SX_Q3_PLAN") && std::strcmp(getenv("SX_Q3_PLAN"), "fused") == 0);
   const bool fused_shape = !ops_plan && w4(t->o_orderkey) && w4(t->o_orderdate) && w4(t->o_shippriority);
   SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, fused_shape ? (SX_BUILD_UNIQUE | SX_BUILD_MEMBERSHIP) : 1,
                        &ht_o));
@@ -1477,13 +1412,15 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       t->l_shipdate.len == t->l_orderkey.len && t->l_extendedprice.len == t->l_orderkey.len &&
       t->l_discount.len == t->l_orderkey.len && t->l_orderkey.len > 0) {
     const int64_t n = t->l_orderkey.len;
-    const int64_t gcap = std::max<int64_t>(1, ht_o->rows);
-    int32_t* gk;
-    longlong2* grev;
-    SX_TRY(alloc(ctx, &gk, (size_t)gcap));
-    bag.bufs.push_back(gk);
-    SX_TRY(alloc(ctx, &grev, (size_t)gcap));
-    bag.bufs.push_back(grev);
+    // records: at most one per lineitem row; sized for 8 lines per qualifying order (the pass
+    // reports the true count; a larger one sends the plan to the operator steps)
+    const int64_t rcap = std::max<int64_t>(1, std::min<int64_t>(n, 8 * ht_o->rows));
+    int32_t* rk;
+    long long* rv;
+    SX_TRY(alloc(ctx, &rk, (size_t)rcap));
+    bag.bufs.push_back(rk);
+    SX_TRY(alloc(ctx, &rv, (size_t)rcap));
+    bag.bufs.push_back(rv);
     Q3Fused a{};
     a.okey = (const int32_t*)t->l_orderkey.data;
     a.ship = (const int32_t*)t->l_shipdate.data;
@@ -1493,27 +1430,45 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     a.bm = ht_o->bm;
     a.bm_min = ht_o->bm_min;
     a.bm_bits = ht_o->bm_bits;
-    a.out_key = gk;
-    a.out_rev = grev;
-    a.cap = gcap;
+    a.out_key = rk;
+    a.out_val = rv;
+    a.cap = rcap;
     a.cursor = (unsigned long long*)ctx->d_counters;
     a.flags = ctx->d_flags;
-    int64_t cnt = 0;
-    int fl[3] = {0, 0, 0};
+    int64_t nrec = 0;
+    int fl = 0;
     {
-      ProfScope pg(ctx, "probe_groupby");
+      ProfScope pg(ctx, "probe_inner");
       SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
-      SX_CUDA(cudaMemsetAsync(a.flags, 0, 3 * sizeof(int), ctx->stream));
+      SX_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(int), ctx->stream));
       k_q3_fused<<<persistent_grid(ctx, 8, ((n + 7) / 8 + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a, n);
       SX_CHECK_LAUNCH();
-      SX_TRY(read_i64(ctx, a.cursor, &cnt));
-      SX_CUDA(cudaMemcpy(fl, a.flags, sizeof fl, cudaMemcpyDeviceToHost));
-      // algorithmic bytes: l_orderkey + l_shipdate once, ext + disc of the joined rows, the groups
-      pg.set_bytes(8.0 * n + 16.0 * cnt * 2.0 + 20.0 * cnt);
+      SX_TRY(read_i64(ctx, a.cursor, &nrec));
+      SX_CUDA(cudaMemcpy(&fl, a.flags, sizeof fl, cudaMemcpyDeviceToHost));
+      // algorithmic bytes: l_orderkey + l_shipdate once, ext + disc of the joined rows, the records
+      pg.set_bytes(8.0 * n + 16.0 * nrec + 12.0 * nrec);
+    }
+    int64_t cnt = 0;
+    int32_t* gk = nullptr;
+    longlong2* grev = nullptr;
+    bool grouped = false;
+    if (!fl && nrec <= rcap) {
+      // 4. group by l_orderkey: revenue = sum of the terms [scale 4]
+      sx_col rcols[2] = {sx_col{SX_I32, 0, nrec, rk, nullptr, nullptr}, sx_col{SX_DEC64, 4, nrec, rv, nullptr, nullptr}};
+      sx_key gkey = {0, SX_KEY_IDENTITY};
+      sx_agg gagg = A(SX_SUM, E1(1, {F(1)}));
+      sx_col gok[1], goa[1];
+      SX_TRY(sx_groupby_agg(ctx, rcols, 2, &gkey, 1, nullptr, nullptr, 0, &gagg, 1, nullptr,
+                            std::min<int64_t>(std::max<int64_t>(nrec, 1), 1 << 21), gok, goa, &cnt));
+      bag.keep(gok, 1);
+      bag.keep(goa, 1);
+      gk = (int32_t*)gok[0].data;
+      grev = (longlong2*)goa[0].data;
+      grouped = true;
     }
     bool carried = false;
     sx_col pay[2];
-    if (!fl[0] && !fl[1] && !fl[2] && cnt <= gcap) {
+    if (grouped) {
       ProfScope pc(ctx, "probe_inner");
       int32_t *cd, *cp;
       SX_TRY(alloc(ctx, &cd, (size_t)std::max<int64_t>(cnt, 1)));
@@ -1555,7 +1510,7 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       *nrows = perm.len;
       return SX_OK;
     }
-    // unsorted lineitem or orders, a wide revenue term or an overflow: the operator plan decides
+    // more records than sized for, an overflow, or orders not in key order: the operator plan decides
   }
   SX_TRY(full_build());
   // 3. lineitem with l_shipdate > DATE joined to those orders (unique build: ordered output)
