@@ -1462,6 +1462,7 @@ __global__ void __launch_bounds__(kDenseThreads, STAGED ? 1 : dense_min_blocks<P
     }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
+      if (!alive[i]) continue;  // (Q6: ~98% of rows; no shared read-modify-write for them)
       int s = -1;
 #pragma unroll
       for (int k = 0; k < kSmallSlots; ++k)

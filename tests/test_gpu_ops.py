@@ -367,14 +367,14 @@ def test_topk_paths(ctx, monkeypatch, mode):
         assert np.array_equal(perm.cpu().numpy(), want), k
 
 
-@pytest.mark.parametrize("mode", ["onesweep", "onesweep-ballot", "lsd"])
+@pytest.mark.parametrize("mode", ["onesweep", "onesweep-match", "lsd"])
 def test_sort_many_tiles(ctx, monkeypatch, mode):
     """Full sorts spanning ~500 onesweep tiles (decoupled look-back chains across many CTAs):
     full-range int64 keys (all 8 digits vary), and heavy ties resolved by stability."""
     if mode == "lsd":
         monkeypatch.setenv("SX_SORT", "lsd")
-    if mode == "onesweep-ballot":
-        monkeypatch.setenv("SX_SORT_RANK", "ballot")
+    if mode == "onesweep-match":
+        monkeypatch.setenv("SX_SORT_RANK", "match")
     rng = np.random.default_rng(21)
     n = 2_000_003
     v = rng.integers(-(2**63), 2**63 - 1, n, dtype=np.int64)
