@@ -1092,16 +1092,19 @@ __global__ void k_lookup_rank(const int32_t* __restrict__ keys, int64_t n, const
   }
 }
 
-// Q3 fused lineitem pass (K10q, the probe with its revenue projection):
-// lineitem is read once — l_shipdate and l_orderkey streamed with 128-bit loads, 8 consecutive
-// rows per thread — rows with shipdate > DATE are tested against the exact key-range bitmap of
-// the qualifying orders (the orders build; the 8 rows' keys are sorted, so two bitmap words serve
-// them), and only the ~0.5% rows that join load l_extendedprice / l_discount and append one
-// record (l_orderkey, ext*(100-disc)) through a per-warp shared buffer (one global atomic per
-// flush).  A warp whose 256 rows have no joining row does nothing else.  The records then go
-// through sx_groupby_agg (step 4).  A first version that also summed the orderkey runs in the
-// pass (owned runs) ran ~100 instructions per row and lost to the operator plan (3.1 vs 1.9 ms).
-// flags: [0] a product left int64.
+// Q3 fused lineitem pass (K10q; SURVEY §8(a) Q3 steps 3 + 4, adjacent steps fused by the
+// executor): lineitem is read once — l_shipdate and l_orderkey streamed with 128-bit loads, 8
+// consecutive rows per lane — rows with shipdate > DATE are tested against the exact key-range
+// bitmap of the qualifying orders (the orders build; two bitmap words serve a lane's 8 sorted
+// keys), and only the ~0.5% rows that join load l_extendedprice / l_discount.  Each warp owns a
+// CONTIGUOUS range of rows and the orderkey groups that start in it: it merges its joining rows'
+// revenue terms in row order (warp-uniform state, lanes taken in order), skips the leading rows
+// of the group begun before its range (the previous warp's), and reads past its range end while
+// the last group continues.  One (orderkey, revenue) per order with >= 1 joining row is appended
+// through a per-warp shared buffer; no group-by table.  Earlier versions: owned runs per THREAD
+// (~100 instructions per row: 3.1 ms), and join records + sx_groupby_agg (1.06 + 0.76 ms).
+// flags: [0] l_orderkey decreases (the plan takes the operator steps), [1] a product or a group
+// sum left int64.
 struct Q3Fused {
   const int32_t* okey;
   const int32_t* ship;
@@ -1112,42 +1115,72 @@ struct Q3Fused {
   long long bm_min;
   unsigned long long bm_bits;
   int32_t* out_key;
-  long long* out_val;
+  longlong2* out_rev;
   int64_t cap;
   unsigned long long* cursor;
   int* flags;
+  __device__ __forceinline__ bool joins1(int32_t k, int32_t sd) const {
+    const uint32_t off = (uint32_t)k - (uint32_t)bm_min;
+    return sd > date && off < (uint32_t)bm_bits && ((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u);
+  }
 };
 
-constexpr int kQ3Buf = 384, kQ3Flush = 128;  // a warp iteration appends <= 256 records
-__global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n) {
+constexpr int kQ3Buf = 96, kQ3Flush = 64;  // a chunk closes <= 8 * 32 groups... flushed per group (see emit)
+__global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n, int64_t per) {
   constexpr int R = 8;
   __shared__ int32_t s_key[kBlock / 32][kQ3Buf];
   __shared__ long long s_val[kBlock / 32][kQ3Buf];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t R0 = gw * per, R1 = min(n, R0 + per);
+  if (R0 >= n) return;  // (warp-uniform)
   const uint32_t kmin = (uint32_t)a.bm_min, bits = (uint32_t)a.bm_bits;  // (bm_bits <= 2^30)
-  const unsigned lt = lanemask_lt();
-  bool ovf = false;
-  int cnt = 0;  // records in the warp's buffer (warp-uniform)
+  bool ovf = false, bad = false;
+  int cnt = 0;  // buffered groups (warp-uniform)
   auto flush = [&]() {  // warp-collective
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(a.cursor, (unsigned long long)cnt);
+    if (lane == 0 && cnt) base = atomicAdd(a.cursor, (unsigned long long)cnt);
     base = __shfl_sync(kFull, base, 0);
     __syncwarp();
     for (int i = lane; i < cnt; i += 32) {
       const int64_t pos = (int64_t)base + i;
       if (pos < a.cap) {
         a.out_key[pos] = s_key[w][i];
-        a.out_val[pos] = s_val[w][i];
+        const long long v = s_val[w][i];
+        a.out_rev[pos] = make_longlong2(v, v < 0 ? -1 : 0);
       }
     }
     __syncwarp();
     cnt = 0;
   };
-  for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R; wbase < n; wbase += stride) {
-    const int64_t r0 = wbase + (int64_t)lane * R;
+  // warp-uniform current group
+  bool cur = false;
+  int32_t cur_key = 0;
+  long long cur_sum = 0;
+  auto add = [&](int32_t key, long long term) {  // warp-uniform call
+    if (cur && key == cur_key) {
+      cur_sum = add_ck(cur_sum, term, ovf);
+      return;
+    }
+    if (cur) {
+      if (lane == 0) {
+        s_key[w][cnt] = cur_key;
+        s_val[w][cnt] = cur_sum;
+      }
+      if (++cnt == kQ3Buf) flush();
+    }
+    cur = true;
+    cur_key = key;
+    cur_sum = term;
+  };
+  const bool has_prev = R0 > 0;
+  const int32_t kprev = has_prev ? __ldg(a.okey + R0 - 1) : 0;  // rows of this group: the previous warp's
+  int32_t lastk = kprev;  // last key seen (sortedness check across chunks)
+  for (int64_t base = R0; base < R1; base += 32 * R) {
+    const int64_t r0 = base + (int64_t)lane * R;
+    const int m = (int)max((int64_t)0, min((int64_t)R, R1 - r0));
     int32_t k[R], sd[R];
-    if (r0 + R <= n) {
+    if (m == R) {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int4 x = __ldcs((const int4*)(a.okey + r0) + j), y = __ldcs((const int4*)(a.ship + r0) + j);
@@ -1157,23 +1190,36 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
     } else {
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const bool in = r0 + i < n;
-        k[i] = in ? __ldg(a.okey + r0 + i) : 0;
-        sd[i] = in ? __ldg(a.ship + r0 + i) : INT32_MIN;
+        k[i] = i < m ? __ldg(a.okey + r0 + i) : INT32_MAX;
+        sd[i] = i < m ? __ldg(a.ship + r0 + i) : INT32_MIN;
       }
+    }
+    // keys non-decreasing across the chunk (lane order) and from the previous chunk
+    {
+      int32_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
+      if (lane == 0) pk = lastk;
+      bool dec = (has_prev || base > R0 || lane > 0) && m > 0 && k[0] < pk;
+#pragma unroll
+      for (int i = 1; i < R; ++i) dec |= i < m && k[i] < k[i - 1];
+      bad |= __any_sync(kFull, dec);
+      int32_t lk = k[0];  // my last valid key (selects: no dynamic register indexing)
+#pragma unroll
+      for (int i = 1; i < R; ++i) lk = i < m ? k[i] : lk;
+      const int lastlane = (int)min((int64_t)31, (R1 - 1 - base) / R);
+      lastk = __shfl_sync(kFull, lk, lastlane);
     }
     uint32_t off[R];
     bool cand[R], anyc = false;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       off[i] = (uint32_t)k[i] - kmin;
-      cand[i] = sd[i] > a.date && off[i] < bits;
+      cand[i] = i < m && sd[i] > a.date && off[i] < bits && !(has_prev && k[i] == kprev);
       anyc |= cand[i];
     }
     unsigned qmask = 0;
     if (anyc) {
       const uint32_t w0 = off[0] >> 5, w1 = off[R - 1] >> 5;
-      if (r0 + R <= n && off[0] < bits && off[R - 1] < bits && w1 - w0 <= 1) {
+      if (m == R && off[0] < bits && off[R - 1] < bits && w1 - w0 <= 1) {
         const uint32_t b0 = __ldg(a.bm + w0), b1 = __ldg(a.bm + w1);
 #pragma unroll
         for (int i = 0; i < R; ++i) {
@@ -1186,34 +1232,89 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
           qmask |= (cand[i] && ((__ldg(a.bm + (off[i] >> 5)) >> (off[i] & 31)) & 1u)) ? 1u << i : 0u;
       }
     }
-    if (!__any_sync(kFull, qmask != 0)) continue;
-    // the joining rows' revenue terms, appended in row order (item-major within the warp)
+    unsigned lanes = __ballot_sync(kFull, qmask != 0);
+    if (!lanes) continue;
+    long long t[R];
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const bool q = (qmask >> i) & 1u;
-      const unsigned b = __ballot_sync(kFull, q);
-      if (q) {
-        const long long e = __ldg(a.ext + r0 + i), d = __ldg(a.disc + r0 + i);
-        const int pos = cnt + __popc(b & lt);
-        s_key[w][pos] = k[i];
-        s_val[w][pos] = mul_ck(e, 100 - d, ovf);
+    for (int i = 0; i < R; ++i)
+      t[i] = ((qmask >> i) & 1u) ? mul_ck(__ldg(a.ext + r0 + i), 100 - __ldg(a.disc + r0 + i), ovf) : 0;
+    // the joining rows in row order: lanes ascending, a lane's rows ascending
+    while (lanes) {
+      const int L = __ffs(lanes) - 1;
+      lanes &= lanes - 1;
+      const unsigned qm = __shfl_sync(kFull, qmask, L);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int32_t key = __shfl_sync(kFull, k[i], L);
+        const long long term = __shfl_sync(kFull, t[i], L);
+        if ((qm >> i) & 1u) add(key, term);
       }
-      cnt += __popc(b);
     }
-    if (cnt >= kQ3Flush) flush();
   }
-  if (cnt > 0) flush();
-  if (ovf) atomicExch(a.flags, 1);
+  // the range's last group continues past R1 (its owner is this warp)
+  if (R1 < n) {
+    const int32_t klast = __ldg(a.okey + R1 - 1);
+    for (int64_t r = R1;; r += 32) {
+      const int64_t rr = r + lane;
+      const int32_t kr = rr < n ? __ldg(a.okey + rr) : INT32_MIN;
+      const bool same = rr < n && kr == klast;
+      const bool q = same && a.joins1(kr, __ldg(a.ship + rr)) && !(has_prev && kr == kprev);
+      const long long term = q ? mul_ck(__ldg(a.ext + rr), 100 - __ldg(a.disc + rr), ovf) : 0;
+      unsigned ql = __ballot_sync(kFull, q);
+      while (ql) {
+        const int L = __ffs(ql) - 1;
+        ql &= ql - 1;
+        add(klast, __shfl_sync(kFull, term, L));
+      }
+      if (__ballot_sync(kFull, same) != kFull) break;
+    }
+  }
+  if (cur) {
+    if (lane == 0) {
+      s_key[w][cnt] = cur_key;
+      s_val[w][cnt] = cur_sum;
+    }
+    ++cnt;
+  }
+  flush();
+  if (bad) atomicExch(a.flags, 1);
+  if (ovf) atomicExch(a.flags + 1, 1);
 }
 
-// Q3 carries of each group: the order with that key by binary search of o_orderkey (orders in
-// strictly increasing key order — any key not found sets *notfound and the plan steps aside).
+// Q3 carries of each group: the order with that key, searched in o_orderkey (orders in strictly
+// increasing key order) from an interpolated guess — TPC-H orderkeys are spread evenly, so the
+// guess lands within a few rows — with an exponential then binary search around it; any key not
+// found sets *notfound and the plan takes the operator steps.
 __global__ void k_q3_carry(const int32_t* __restrict__ gk, int64_t ng, const int32_t* __restrict__ okey, int64_t no,
                            const int32_t* __restrict__ odate, const int32_t* __restrict__ oprio, int32_t* out_date,
                            int32_t* out_prio, int* notfound) {
+  const long long kmin = __ldg(okey), kmax = __ldg(okey + no - 1);
+  const double scale = kmax > kmin ? (double)(no - 1) / (double)(kmax - kmin) : 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ng; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t k = gk[i];
-    int64_t lo = 0, hi = no;  // first position with okey >= k
+    int64_t g = (int64_t)((double)((long long)k - kmin) * scale);
+    g = g < 0 ? 0 : (g >= no ? no - 1 : g);
+    // bracket [lo, hi) containing the first position with okey >= k
+    int64_t lo, hi;  // the answer is the first position of [lo, hi) with okey >= k, else hi
+    if (__ldg(okey + g) < k) {  // answer > g: probe g + 1, g + 2, g + 4, ...
+      int64_t prev = g, step = 1, c = g + 1;  // okey[prev] < k
+      while (c < no && __ldg(okey + c) < k) {
+        prev = c;
+        step <<= 1;
+        c = g + step;
+      }
+      lo = prev + 1;
+      hi = c < no ? c : no;  // okey[c] >= k, or the end
+    } else {  // answer <= g: probe g - 1, g - 2, g - 4, ...
+      int64_t prev = g, step = 1, c = g - 1;  // okey[prev] >= k
+      while (c >= 0 && __ldg(okey + c) >= k) {
+        prev = c;
+        step <<= 1;
+        c = g - step;
+      }
+      lo = c >= 0 ? c + 1 : 0;  // okey[c] < k, or the start
+      hi = prev;
+    }
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
       if (__ldg(okey + mid) < k) lo = mid + 1;
@@ -1412,15 +1513,13 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       t->l_shipdate.len == t->l_orderkey.len && t->l_extendedprice.len == t->l_orderkey.len &&
       t->l_discount.len == t->l_orderkey.len && t->l_orderkey.len > 0) {
     const int64_t n = t->l_orderkey.len;
-    // records: at most one per lineitem row; sized for 8 lines per qualifying order (the pass
-    // reports the true count; a larger one sends the plan to the operator steps)
-    const int64_t rcap = std::max<int64_t>(1, std::min<int64_t>(n, 8 * ht_o->rows));
-    int32_t* rk;
-    long long* rv;
-    SX_TRY(alloc(ctx, &rk, (size_t)rcap));
-    bag.bufs.push_back(rk);
-    SX_TRY(alloc(ctx, &rv, (size_t)rcap));
-    bag.bufs.push_back(rv);
+    const int64_t gcap = std::max<int64_t>(1, ht_o->rows);  // groups are qualifying orders
+    int32_t* gk;
+    longlong2* grev;
+    SX_TRY(alloc(ctx, &gk, (size_t)gcap));
+    bag.bufs.push_back(gk);
+    SX_TRY(alloc(ctx, &grev, (size_t)gcap));
+    bag.bufs.push_back(grev);
     Q3Fused a{};
     a.okey = (const int32_t*)t->l_orderkey.data;
     a.ship = (const int32_t*)t->l_shipdate.data;
@@ -1430,42 +1529,29 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     a.bm = ht_o->bm;
     a.bm_min = ht_o->bm_min;
     a.bm_bits = ht_o->bm_bits;
-    a.out_key = rk;
-    a.out_val = rv;
-    a.cap = rcap;
+    a.out_key = gk;
+    a.out_rev = grev;
+    a.cap = gcap;
     a.cursor = (unsigned long long*)ctx->d_counters;
     a.flags = ctx->d_flags;
-    int64_t nrec = 0;
-    int fl = 0;
-    {
-      ProfScope pg(ctx, "probe_inner");
-      SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
-      SX_CUDA(cudaMemsetAsync(a.flags, 0, sizeof(int), ctx->stream));
-      k_q3_fused<<<persistent_grid(ctx, 8, ((n + 7) / 8 + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a, n);
-      SX_CHECK_LAUNCH();
-      SX_TRY(read_i64(ctx, a.cursor, &nrec));
-      SX_CUDA(cudaMemcpy(&fl, a.flags, sizeof fl, cudaMemcpyDeviceToHost));
-      // algorithmic bytes: l_orderkey + l_shipdate once, ext + disc of the joined rows, the records
-      pg.set_bytes(8.0 * n + 16.0 * nrec + 12.0 * nrec);
-    }
     int64_t cnt = 0;
-    int32_t* gk = nullptr;
-    longlong2* grev = nullptr;
-    bool grouped = false;
-    if (!fl && nrec <= rcap) {
-      // 4. group by l_orderkey: revenue = sum of the terms [scale 4]
-      sx_col rcols[2] = {sx_col{SX_I32, 0, nrec, rk, nullptr, nullptr}, sx_col{SX_DEC64, 4, nrec, rv, nullptr, nullptr}};
-      sx_key gkey = {0, SX_KEY_IDENTITY};
-      sx_agg gagg = A(SX_SUM, E1(1, {F(1)}));
-      sx_col gok[1], goa[1];
-      SX_TRY(sx_groupby_agg(ctx, rcols, 2, &gkey, 1, nullptr, nullptr, 0, &gagg, 1, nullptr,
-                            std::min<int64_t>(std::max<int64_t>(nrec, 1), 1 << 21), gok, goa, &cnt));
-      bag.keep(gok, 1);
-      bag.keep(goa, 1);
-      gk = (int32_t*)gok[0].data;
-      grev = (longlong2*)goa[0].data;
-      grouped = true;
+    int fl[2] = {0, 0};
+    {
+      ProfScope pg(ctx, "probe_groupby");
+      SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
+      SX_CUDA(cudaMemsetAsync(a.flags, 0, 2 * sizeof(int), ctx->stream));
+      // one warp per contiguous range of whole 256-row chunks, every warp of a persistent grid
+      const unsigned grid = persistent_grid(ctx, 4, ((n + 255) / 256 + (kBlock / 32) - 1) / (kBlock / 32));
+      const int64_t warps = (int64_t)grid * (kBlock / 32);
+      const int64_t per = ((n + warps - 1) / warps + 255) / 256 * 256;
+      k_q3_fused<<<grid, kBlock, 0, SX_STREAM(ctx)>>>(a, n, per);
+      SX_CHECK_LAUNCH();
+      SX_TRY(read_i64(ctx, a.cursor, &cnt));
+      SX_CUDA(cudaMemcpy(fl, a.flags, sizeof fl, cudaMemcpyDeviceToHost));
+      // algorithmic bytes: l_orderkey + l_shipdate once, ext + disc of the joined rows, the groups
+      pg.set_bytes(8.0 * n + 20.0 * cnt);
     }
+    const bool grouped = !fl[0] && !fl[1] && cnt <= gcap;
     bool carried = false;
     sx_col pay[2];
     if (grouped) {
