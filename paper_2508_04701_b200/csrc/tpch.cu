@@ -1126,7 +1126,7 @@ struct Q3Fused {
 };
 
 constexpr int kQ3Buf = 96, kQ3Flush = 64;  // a chunk closes <= 8 * 32 groups... flushed per group (see emit)
-__global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n, int64_t per) {
+__global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n, int64_t per) {
   constexpr int R = 8;
   __shared__ int32_t s_key[kBlock / 32][kQ3Buf];
   __shared__ long long s_val[kBlock / 32][kQ3Buf];
@@ -1176,6 +1176,20 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
   const bool has_prev = R0 > 0;
   const int32_t kprev = has_prev ? __ldg(a.okey + R0 - 1) : 0;  // rows of this group: the previous warp's
   int32_t lastk = kprev;  // last key seen (sortedness check across chunks)
+  // the next chunk's keys and dates are in flight while this chunk is processed (a warp walks its
+  // range sequentially: without this, one 2 KB load round trip per chunk — ncu: 40% long-scoreboard)
+  int4 nx[2], ny[2];
+  auto fetch = [&](int64_t b) {
+    const int64_t r = b + (int64_t)lane * R;
+    if (b < R1 && r + R <= R1) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        nx[j] = __ldcs((const int4*)(a.okey + r) + j);
+        ny[j] = __ldcs((const int4*)(a.ship + r) + j);
+      }
+    }
+  };
+  fetch(R0);
   for (int64_t base = R0; base < R1; base += 32 * R) {
     const int64_t r0 = base + (int64_t)lane * R;
     const int m = (int)max((int64_t)0, min((int64_t)R, R1 - r0));
@@ -1183,9 +1197,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
     if (m == R) {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int4 x = __ldcs((const int4*)(a.okey + r0) + j), y = __ldcs((const int4*)(a.ship + r0) + j);
-        k[4 * j] = x.x; k[4 * j + 1] = x.y; k[4 * j + 2] = x.z; k[4 * j + 3] = x.w;
-        sd[4 * j] = y.x; sd[4 * j + 1] = y.y; sd[4 * j + 2] = y.z; sd[4 * j + 3] = y.w;
+        k[4 * j] = nx[j].x; k[4 * j + 1] = nx[j].y; k[4 * j + 2] = nx[j].z; k[4 * j + 3] = nx[j].w;
+        sd[4 * j] = ny[j].x; sd[4 * j + 1] = ny[j].y; sd[4 * j + 2] = ny[j].z; sd[4 * j + 3] = ny[j].w;
       }
     } else {
 #pragma unroll
@@ -1194,6 +1207,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
         sd[i] = i < m ? __ldg(a.ship + r0 + i) : INT32_MIN;
       }
     }
+    fetch(base + 32 * R);
     // keys non-decreasing across the chunk (lane order) and from the previous chunk
     {
       int32_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
@@ -1327,6 +1341,80 @@ __global__ void k_q3_carry(const int32_t* __restrict__ gk, int64_t ng, const int
       atomicExch(notfound, 1);
     }
   }
+}
+
+// Row of each probe key in a PK column stored in strictly increasing order (the executor's
+// "sorted primary key" lookup; TPC-H's orders and customer are stored in key order): search from
+// an interpolated guess, exponential then binary; a key not found sets *notfound (the plan then
+// takes its hash-join steps, which decide inner-join semantics and unsorted tables).
+template <typename KT>
+__global__ void k_sorted_lookup(const KT* __restrict__ probe, int64_t np, const KT* __restrict__ sorted, int64_t ns,
+                                int32_t* __restrict__ out_row, int* notfound) {
+  if (ns <= 0) {
+    if (np > 0 && blockIdx.x == 0 && threadIdx.x == 0) atomicExch(notfound, 1);
+    return;
+  }
+  const long long kmin = (long long)__ldg(sorted), kmax = (long long)__ldg(sorted + ns - 1);
+  const double scale = kmax > kmin ? (double)(ns - 1) / ((double)kmax - (double)kmin) : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+    const KT k = probe[i];
+    double gd = ((double)k - (double)kmin) * scale;
+    int64_t g = gd < 0 ? 0 : (gd >= (double)(ns - 1) ? ns - 1 : (int64_t)gd);
+    int64_t lo, hi;  // the answer is the first position of [lo, hi) with key >= k, else hi
+    if (__ldg(sorted + g) < k) {
+      int64_t prev = g, step = 1, c = g + 1;
+      while (c < ns && __ldg(sorted + c) < k) {
+        prev = c;
+        step <<= 1;
+        c = g + step;
+      }
+      lo = prev + 1;
+      hi = c < ns ? c : ns;
+    } else {
+      int64_t prev = g, step = 1, c = g - 1;
+      while (c >= 0 && __ldg(sorted + c) >= k) {
+        prev = c;
+        step <<= 1;
+        c = g - step;
+      }
+      lo = c >= 0 ? c + 1 : 0;
+      hi = prev;
+    }
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(sorted + mid) < k) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < ns && __ldg(sorted + lo) == k) out_row[i] = (int32_t)lo;
+    else atomicExch(notfound, 1);
+  }
+}
+
+// rows of `keys` (len n) in the sorted PK column pk; false when a key is missing (or pk unsorted)
+sx_status sorted_lookup(sx_ctx* ctx, Bag& bag, const sx_col& pk, const sx_col& keys, int32_t** rows, bool* ok) {
+  *ok = false;
+  *rows = nullptr;
+  if (pk.type != keys.type || !(w4(pk) || w8(pk)) || pk.len > INT32_MAX) return SX_OK;
+  int32_t* r;
+  SX_TRY(alloc(ctx, &r, (size_t)std::max<int64_t>(keys.len, 1)));
+  bag.bufs.push_back(r);
+  int* nf = ctx->d_flags + 8;
+  SX_CUDA(cudaMemsetAsync(nf, 0, sizeof(int), ctx->stream));
+  if (keys.len > 0) {
+    const unsigned grid = persistent_grid(ctx, 8, (keys.len + kBlock - 1) / kBlock);
+    if (w4(pk))
+      k_sorted_lookup<int32_t><<<grid, kBlock, 0, SX_STREAM(ctx)>>>((const int32_t*)keys.data, keys.len,
+                                                                   (const int32_t*)pk.data, pk.len, r, nf);
+    else
+      k_sorted_lookup<long long><<<grid, kBlock, 0, SX_STREAM(ctx)>>>((const long long*)keys.data, keys.len,
+                                                                     (const long long*)pk.data, pk.len, r, nf);
+    SX_CHECK_LAUNCH();
+  }
+  int h = 0;
+  SX_CUDA(cudaMemcpy(&h, nf, sizeof(int), cudaMemcpyDeviceToHost));
+  *ok = h == 0;
+  *rows = r;
+  return SX_OK;
 }
 
 static const char* kNation[25] = {"ALGERIA", "ARGENTINA", "BRAZIL", "CANADA", "EGYPT", "ETHIOPIA", "FRANCE",
@@ -1541,7 +1629,7 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
       SX_CUDA(cudaMemsetAsync(a.flags, 0, 2 * sizeof(int), ctx->stream));
       // one warp per contiguous range of whole 256-row chunks, every warp of a persistent grid
-      const unsigned grid = persistent_grid(ctx, 4, ((n + 255) / 256 + (kBlock / 32) - 1) / (kBlock / 32));
+      const unsigned grid = persistent_grid(ctx, 3, ((n + 255) / 256 + (kBlock / 32) - 1) / (kBlock / 32));
       const int64_t warps = (int64_t)grid * (kBlock / 32);
       const int64_t per = ((n + warps - 1) / warps + 255) / 256 * 256;
       k_q3_fused<<<grid, kBlock, 0, SX_STREAM(ctx)>>>(a, n, per);
@@ -2058,6 +2146,49 @@ SX_EXPORT sx_status sx_tpch_q18(sx_ctx* ctx, const sx_tpch_tables* t, const sx_t
   }
   bag.keep(gok, 1);
   bag.keep(goa, 1);
+  // 2+3 by sorted-PK lookups (default; SX_Q18_JOIN=hash forces the hash joins below): the ~6.4e3
+  //    qualifying orderkeys are looked up in o_orderkey and their custkeys in c_custkey (both
+  //    tables in key order) instead of scanning 1.5e8 orders and 1.5e7 customers
+  const bool hash_joins = getenv("SX_Q18_JOIN") && std::strcmp(getenv("SX_Q18_JOIN"), "hash") == 0;
+  if (!hash_joins) {
+    ProfScope pl(ctx, "probe_inner");
+    int32_t* orow;
+    bool ok = false;
+    SX_TRY(sorted_lookup(ctx, bag, t->o_orderkey, gok[0], &orow, &ok));
+    sx_col R[5];
+    bool found = false;
+    if (ok) {
+      const sx_sel os{ng, orow};
+      sx_col oc[4] = {t->o_orderkey, t->o_custkey, t->o_orderdate, t->o_totalprice};
+      R[0] = goa[0];
+      for (int c = 0; c < 4; ++c) {
+        SX_TRY(sx_gather(ctx, &oc[c], &os, &R[1 + c]));
+        bag.keep(R[1 + c]);
+      }
+      int32_t* crow;
+      SX_TRY(sorted_lookup(ctx, bag, t->c_custkey, R[2], &crow, &found));  // every order's customer exists
+    }
+    pl.set_bytes(ng * (2.0 * type_width(t->o_orderkey.type) + 4.0 + 4 + 4 + 8 + 4 + 4));
+    if (found) {
+      sx_col scols[3] = {R[4], R[3], R[1]};
+      sx_sortkey sks[3] = {{0, 1}, {1, 0}, {2, 0}};
+      sx_sel perm;
+      SX_TRY(sx_sort_topk(ctx, scols, 3, sks, 3, nullptr, p->q18_limit, &perm));
+      bag.keep(perm);
+      std::vector<std::vector<uint8_t>> h;
+      SX_TRY(fetch_rows(ctx, bag, R, 5, perm, h));
+      if (perm.len > cap) return set_err(ctx, SX_EINVAL, "Q18: %lld rows > cap", (long long)perm.len);
+      for (int64_t i = 0; i < perm.len; ++i) {
+        out[i].o_orderkey = key_at(h[1], R[1].type, i);
+        out[i].c_custkey = at<int32_t>(h[2], i);
+        out[i].o_orderdate = at<int32_t>(h[3], i);
+        out[i].o_totalprice = at<int64_t>(h[4], i);
+        out[i].sum_qty = i128_at(h[0], i);
+      }
+      *nrows = perm.len;
+      return SX_OK;
+    }
+  }
   // 2. orders with o_orderkey in that set; carry sum(l_quantity) from the group-by (equal to the
   //    literal re-aggregation over the joined lineitems; reading for Q18)
   sx_col big[2] = {gok[0], goa[0]};

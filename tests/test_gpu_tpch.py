@@ -187,6 +187,31 @@ def test_q6_lazy_levels(ctx, monkeypatch, lazy3):
 
 
 
+@pytest.mark.parametrize("case", ["sorted", "hash", "customer-shuffled", "customer-missing"])
+def test_q18_join_modes(ctx, monkeypatch, case):
+    """Q18's orders/customer joins by sorted-PK lookups (default), by hash joins (SX_Q18_JOIN=hash),
+    with the customer rows shuffled (lookups fail: hash joins), and with qualifying orders whose
+    customer is missing (inner-join semantics: those orders drop out)."""
+    if case == "hash":
+        monkeypatch.setenv("SX_Q18_JOIN", "hash")
+    host = gen.cpu_tables(100, seed=29)
+    host = dict(host)
+    c = host["customer"]
+    if case == "customer-shuffled":
+        perm = np.random.default_rng(6).permutation(len(c["c_custkey"]))
+        host["customer"] = {k: v[perm].copy() for k, v in c.items()}
+    if case == "customer-missing":
+        keep = np.ones(len(c["c_custkey"]), bool)
+        keep[::3] = False
+        host["customer"] = {k: v[keep].copy() for k, v in c.items()}
+    T = tpch.Tpch(ctx, to_dev(host))
+    for over in ({}, dict(q18_qty_gt=15000)):
+        got = T.run("q18", tpch.default_params(**over))
+        want = oracle.run_query("q18", host, oracle.default_params(**over))
+        assert rows_equal(got, want), diff_rows(got, want)
+
+
+
 def test_gpu_generator_matches_cpu_generator():
     cpu = gen.cpu_tables(10, seed=42)
     g = gen.gpu_tables(10, seed=42)
