@@ -593,6 +593,150 @@ __global__ void __launch_bounds__(kBlock, 4) k_runs_lean(const __grid_constant__
   if (wide) atomicExch(flags + 1, 1);
 }
 
+// K10wr: K10w's selective scan fed by the tile ring (ring.cuh) instead of per-lane loads and
+// gathers (programs with kWRing: Q9).  One producer warp bulk-copies whole tiles of every column
+// the pass reads (partkey, suppkey, orderkey, quantity, price, discount: 36 B/row streamed once at
+// full bandwidth, no 128-byte line over-fetch from gathering the 5.4% green rows) into a 3-stage
+// shared ring; each of the 16 consumer warps tests its 64 rows of a tile against the green-part
+// bitmap, copies the green rows' values into a per-warp buffer, and once 32 are buffered every
+// lane runs one row's three lookups (the program's lookups<1>) and aggregates into the per-CTA
+// shared table, exactly as K10w.  Rows after the last whole tile: global loads, same path.
+template <class P, class = void>
+struct has_wring : std::false_type {};
+template <class P>
+struct has_wring<P, std::void_t<decltype(P::kWRing)>> : std::true_type {};
+
+constexpr int kWrBuf = 96;  // per-warp buffered green rows (<= 31 left + 64 new)
+
+template <class P>
+__host__ __device__ constexpr size_t wring_buf_bytes() {
+  return (size_t)kWrBuf * (4 + 4 + sizeof(typename P::KeyT) + 8 + 8 + 8);
+}
+
+template <class P>
+__global__ void __launch_bounds__((P::RingCols::kRingConsumers + 1) * 32, 1)
+    k_gb_wring(const __grid_constant__ P prog, const __grid_constant__ typename P::RingCols rc, int64_t n,
+               const __grid_constant__ Layout L, Table t, uint32_t scap) {
+  using RC = typename P::RingCols;
+  using KT = typename P::KeyT;
+  constexpr int S = RC::kRingStages, T = RC::kRingTile, NC = RC::kRingConsumers, SL = T / NC;
+  static_assert(SL % 32 == 0, "a consumer warp's slice is whole 32-row groups");
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[S];
+  __shared__ __align__(8) uint64_t empty[S];
+  __shared__ int s_side, s_full;
+  uint8_t* const wbufs = ring + (size_t)S * ring_stage_bytes<RC>();
+  uint8_t* const sm_tab = wbufs + (size_t)NC * wring_buf_bytes<P>();
+  const size_t tbytes = (size_t)(scap + 1) * L.slot_bytes;
+  for (size_t j = threadIdx.x * 8; j < tbytes; j += blockDim.x * 8) *(unsigned long long*)(sm_tab + j) = 0;
+  if (threadIdx.x == 0) { s_side = 0; s_full = 0; }
+  ring_init_bars<RC>(full, empty);
+  __syncthreads();
+  const Table st{sm_tab, scap - 1, &s_side, &s_full};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // this warp's buffer (consumers only)
+  uint8_t* wb = wbufs + (size_t)(warp < NC ? warp : 0) * wring_buf_bytes<P>();
+  int32_t* b_pk = (int32_t*)wb;
+  int32_t* b_sk = b_pk + kWrBuf;
+  KT* b_ok = (KT*)(b_sk + kWrBuf);
+  long long* b_q = (long long*)(wb + (size_t)kWrBuf * (8 + sizeof(KT)));
+  long long* b_e = b_q + kWrBuf;
+  long long* b_d = b_e + kWrBuf;
+  bool ovf = false;
+  int cnt = 0;  // buffered green rows (warp-uniform)
+  const unsigned lt = lanemask_lt();
+  auto process = [&](int m) {  // entries [0, m), m <= 32: lane i takes entry i
+    bool alive[1] = {lane < m};
+    const int i = alive[0] ? lane : 0;
+    int32_t pk[1] = {b_pk[i]}, sk[1] = {b_sk[i]};
+    KT ok[1] = {b_ok[i]};
+    int64_t q[1] = {b_q[i]}, e[1] = {b_e[i]}, d[1] = {b_d[i]};
+    uint64_t key[1];
+    int64_t v[1];
+    prog.template lookups<1>(pk, sk, ok, q, e, d, alive, key, v, ovf);
+    if (alive[0]) {
+      uint8_t* sp = *(volatile int*)&s_full ? nullptr : find_or_insert(st, L, key[0]);
+      if (sp) apply_state_smem(sp, L, 0, (unsigned long long)v[0], v[0] < 0 ? -1 : 0);
+      else gb_row_to_global(t, L, key[0], 0, v[0]);
+    }
+    __syncwarp();
+    // move the entries past m (<= 63 of them) to the front: read both into registers, then write
+    const int rem = cnt - m;
+    int32_t mp[2], ms[2];
+    KT mo[2];
+    long long mq[2], me[2], md[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = m + h * 32 + lane;
+      const bool in = h * 32 + lane < rem;
+      mp[h] = in ? b_pk[j] : 0; ms[h] = in ? b_sk[j] : 0; mo[h] = in ? b_ok[j] : (KT)0;
+      mq[h] = in ? b_q[j] : 0; me[h] = in ? b_e[j] : 0; md[h] = in ? b_d[j] : 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = h * 32 + lane;
+      if (j < rem) {
+        b_pk[j] = mp[h]; b_sk[j] = ms[h]; b_ok[j] = mo[h]; b_q[j] = mq[h]; b_e[j] = me[h]; b_d[j] = md[h];
+      }
+    }
+    __syncwarp();
+    cnt = rem;
+  };
+  // append one row (all lanes call; `green` per lane), values given
+  auto append = [&](bool green, int32_t pk, int32_t sk, KT ok, long long q, long long e, long long d) {
+    const unsigned bal = __ballot_sync(kFull, green);
+    if (green) {
+      const int pos = cnt + __popc(bal & lt);
+      b_pk[pos] = pk; b_sk[pos] = sk; b_ok[pos] = ok; b_q[pos] = q; b_e[pos] = e; b_d[pos] = d;
+    }
+    cnt += __popc(bal);
+    __syncwarp();
+  };
+  const bool consumer = ring_pipeline(rc, n, ring, full, empty, [&](const uint8_t* const* b, int64_t, int cw, int ln) {
+#pragma unroll
+    for (int j = 0; j < SL / 32; ++j) {
+      const int idx = cw * SL + j * 32 + ln;
+      const int32_t pk = ((const int32_t*)b[0])[idx];
+      const bool green = prog.wring_green(pk);
+      append(green, pk, ((const int32_t*)b[1])[idx], ((const KT*)b[2])[idx], ((const long long*)b[3])[idx],
+             ((const long long*)b[4])[idx], ((const long long*)b[5])[idx]);
+    }
+    while (cnt >= 32) process(32);
+  });
+  if (consumer) {
+    const int64_t ntiles = n / T;
+    if (blockIdx.x == gridDim.x - 1) {  // rows after the last whole tile
+      for (int64_t r0 = ntiles * T + (int64_t)warp * 32; r0 < n; r0 += (int64_t)NC * 32) {
+        const int64_t r = r0 + lane;
+        const bool in = r < n;
+        const int32_t pk = in ? __ldg((const int32_t*)rc.ring_col(0) + r) : 0;
+        const bool green = in && prog.wring_green(pk);
+        append(green, pk, green ? __ldg((const int32_t*)rc.ring_col(1) + r) : 0,
+               green ? __ldg((const KT*)rc.ring_col(2) + r) : (KT)0, green ? __ldg((const long long*)rc.ring_col(3) + r) : 0,
+               green ? __ldg((const long long*)rc.ring_col(4) + r) : 0, green ? __ldg((const long long*)rc.ring_col(5) + r) : 0);
+        while (cnt >= 32) process(32);
+      }
+    }
+    while (cnt > 0) process(cnt < 32 ? cnt : 32);
+  }
+  if (ovf) atomicExch(prog.ovf_flag, 1);
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e <= scap; e += blockDim.x) {
+    const uint8_t* sl = sm_tab + (size_t)e * L.slot_bytes;
+    uint64_t key;
+    if (e == scap) {
+      if (!s_side) continue;
+      key = 0;
+    } else {
+      key = L.key_bytes == 4 ? (uint64_t)*(const unsigned*)sl : *(const unsigned long long*)sl;
+      if (!key) continue;
+    }
+    uint8_t* p = find_or_insert(t, L, key);
+    if (p) merge_slot(p, sl, L);
+  }
+}
+
 struct EmitArgs {
   const uint8_t* slots;
   const int32_t* ids;
@@ -1028,6 +1172,24 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
         const sx_status rs = gb_ranges(ctx, prog, P, sel, n, groups_hint, L, t, scr);
         if (rs == SX_OK) ranges_done = true;
         else if (rs != SX_EUNSUPPORTED) return rs;
+      }
+    }
+    if constexpr (has_wring<Prog>::value) {
+      // K10wr: the selective scan fed by the tile ring (SX_Q9_RING=0: K10w); one CTA per SM
+      using RC = typename Prog::RingCols;
+      const bool ring_off = getenv("SX_Q9_RING") && getenv("SX_Q9_RING")[0] == '0';
+      const typename Prog::RingCols rc = prog.ring_cols();
+      bool aligned = true;
+      for (int c = 0; c < RC::kRingCols; ++c) aligned = aligned && ((uintptr_t)rc.ring_col(c) % 16) == 0;
+      if (!ring_off && aligned && !dense_done && n >= (int64_t)RC::kRingTile * ctx->num_sms && !sel && shared_cap &&
+          nsub == 1 && L.nst == 1 && prog.wscan_ok()) {
+        const size_t smem = (size_t)RC::kRingStages * ring_stage_bytes<RC>() + (size_t)RC::kRingConsumers * wring_buf_bytes<Prog>() +
+                            (size_t)(shared_cap + 1) * L.slot_bytes;
+        SX_CUDA(cudaFuncSetAttribute(k_gb_wring<Prog>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_gb_wring<Prog><<<(unsigned)ctx->num_sms, (RC::kRingConsumers + 1) * 32, smem, SX_STREAM(ctx)>>>(
+            prog, rc, n, L, t, shared_cap);
+        SX_CHECK_LAUNCH();
+        dense_done = true;
       }
     }
     if constexpr (has_wscan<Prog>::value) {

@@ -853,6 +853,20 @@ struct Q9FusedProg {
   // and value read speculatively, both inside the key range) and the partsupp table's first slot.
   static constexpr int kWChunks = 2;
   static constexpr int kWRows = 2;
+  // K10wr interface (gb_host.cuh): the six lineitem columns through the tile ring
+  static constexpr bool kWRing = true;
+  using KeyT = KT;
+  struct RingCols {
+    const void* col[6];  // partkey, suppkey, orderkey, quantity, extendedprice, discount
+    static constexpr int kRingCols = 6, kRingTile = 1024, kRingStages = 3, kRingConsumers = 16;
+    __host__ __device__ static constexpr int ring_width(int c) { return c == 2 ? (int)sizeof(KT) : (c < 2 ? 4 : 8); }
+    __host__ __device__ const void* ring_col(int c) const { return col[c]; }
+  };
+  RingCols ring_cols() const { return RingCols{{partkey, suppkey, orderkey, qty, ext, disc}}; }
+  __device__ __forceinline__ bool wring_green(int32_t pk) const {
+    const unsigned long long off = (unsigned long long)((long long)pk - pbm_min);
+    return off < pbm_bits && ((__ldg(pbm + (off >> 5)) >> (off & 31)) & 1u);
+  }
   bool wscan_ok() const { return pbm != nullptr && wscan; }
   __device__ __forceinline__ uint32_t wscan_select(int64_t r0, int64_t n, int32_t (&pk)[8]) const {
     dense_load32<8>(partkey, r0, n, r0 + 8 <= n, pk);
@@ -880,6 +894,14 @@ struct Q9FusedProg {
       e[u] = alive[u] ? __ldg(ext + row[u]) : 0;
       d[u] = alive[u] ? __ldg(disc + row[u]) : 0;
     }
+    lookups<U>(pk, sk, ok, q, e, d, alive, key, v, ovf);
+  }
+  // the three lookups (supplier nation, order date, partsupp cost) and the profit of U green rows,
+  // every load of one level issued together
+  template <int U>
+  __device__ __forceinline__ void lookups(const int32_t (&pk)[U], const int32_t (&sk)[U], const KT (&ok)[U],
+                                          const int64_t (&q)[U], const int64_t (&e)[U], const int64_t (&d)[U],
+                                          bool (&alive)[U], uint64_t (&key)[U], int64_t (&v)[U], bool& ovf) const {
     uint32_t sw[U], ow[U];
     int32_t sv[U], ov[U];
     ulonglong2 p0[U];

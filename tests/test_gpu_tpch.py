@@ -212,6 +212,27 @@ def test_q18_join_modes(ctx, monkeypatch, case):
 
 
 
+@pytest.mark.parametrize("ring", ["1", "0"])
+@pytest.mark.parametrize("trim", [0, 777])
+def test_q9_ring(ctx, monkeypatch, ring, trim):
+    """Q9's lineitem pass fed by the tile ring (K10wr, default at >= 1024 rows per SM) and by
+    per-lane loads (K10w, SX_Q9_RING=0), with whole tiles only and with a ragged tail (global-load
+    path in the last CTA) — against the oracle, also for another colour."""
+    monkeypatch.setenv("SX_Q9_RING", ring)
+    host = gen.cpu_tables(200, seed=31)
+    li = host["lineitem"]
+    n = len(li["l_orderkey"])
+    n = n - n % 1024 - trim if trim == 0 else n - trim
+    host = dict(host)
+    host["lineitem"] = {k: v[:n].copy() for k, v in li.items()}
+    T = tpch.Tpch(ctx, to_dev(host))
+    for color in ("green", "blue"):
+        got = T.run("q9", tpch.default_params(q9_color=color))
+        want = oracle.run_query("q9", host, oracle.default_params(q9_color=color))
+        assert rows_equal(got, want), diff_rows(got, want)
+
+
+
 def test_gpu_generator_matches_cpu_generator():
     cpu = gen.cpu_tables(10, seed=42)
     g = gen.gpu_tables(10, seed=42)
