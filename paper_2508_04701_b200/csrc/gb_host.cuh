@@ -1175,9 +1175,11 @@ sx_status gb_run(sx_ctx* ctx, const Prog& prog, const GbPlan& P, const int32_t* 
       }
     }
     if constexpr (has_wring<Prog>::value) {
-      // K10wr: the selective scan fed by the tile ring (SX_Q9_RING=0: K10w); one CTA per SM
+      // K10wr: the selective scan fed by the tile ring; one CTA per SM.  Opt-in (SX_Q9_RING=1):
+      // measured 8.6 vs 4.3 ms for K10w at SF100 — its 16 consumer warps per SM cannot hide the
+      // latency of the green rows' lookups (ncu: 69% long-scoreboard stalls, 3.2 TB/s)
       using RC = typename Prog::RingCols;
-      const bool ring_off = getenv("SX_Q9_RING") && getenv("SX_Q9_RING")[0] == '0';
+      const bool ring_off = !(getenv("SX_Q9_RING") && getenv("SX_Q9_RING")[0] == '1');
       const typename Prog::RingCols rc = prog.ring_cols();
       bool aligned = true;
       for (int c = 0; c < RC::kRingCols; ++c) aligned = aligned && ((uintptr_t)rc.ring_col(c) % 16) == 0;

@@ -1148,7 +1148,7 @@ struct Q3Fused {
 };
 
 constexpr int kQ3Buf = 96, kQ3Flush = 64;  // a chunk closes <= 8 * 32 groups... flushed per group (see emit)
-__global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n, int64_t per) {
+__global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n, int64_t per) {
   constexpr int R = 8;
   __shared__ int32_t s_key[kBlock / 32][kQ3Buf];
   __shared__ long long s_val[kBlock / 32][kQ3Buf];
@@ -1198,20 +1198,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ 
   const bool has_prev = R0 > 0;
   const int32_t kprev = has_prev ? __ldg(a.okey + R0 - 1) : 0;  // rows of this group: the previous warp's
   int32_t lastk = kprev;  // last key seen (sortedness check across chunks)
-  // the next chunk's keys and dates are in flight while this chunk is processed (a warp walks its
-  // range sequentially: without this, one 2 KB load round trip per chunk — ncu: 40% long-scoreboard)
-  int4 nx[2], ny[2];
-  auto fetch = [&](int64_t b) {
-    const int64_t r = b + (int64_t)lane * R;
-    if (b < R1 && r + R <= R1) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        nx[j] = __ldcs((const int4*)(a.okey + r) + j);
-        ny[j] = __ldcs((const int4*)(a.ship + r) + j);
-      }
-    }
-  };
-  fetch(R0);
+  // (prefetching the next chunk into registers measured slower: 2.05 vs 1.87 ms at 3 CTAs/SM)
   for (int64_t base = R0; base < R1; base += 32 * R) {
     const int64_t r0 = base + (int64_t)lane * R;
     const int m = (int)max((int64_t)0, min((int64_t)R, R1 - r0));
@@ -1219,8 +1206,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ 
     if (m == R) {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        k[4 * j] = nx[j].x; k[4 * j + 1] = nx[j].y; k[4 * j + 2] = nx[j].z; k[4 * j + 3] = nx[j].w;
-        sd[4 * j] = ny[j].x; sd[4 * j + 1] = ny[j].y; sd[4 * j + 2] = ny[j].z; sd[4 * j + 3] = ny[j].w;
+        const int4 x = __ldcs((const int4*)(a.okey + r0) + j), y = __ldcs((const int4*)(a.ship + r0) + j);
+        k[4 * j] = x.x; k[4 * j + 1] = x.y; k[4 * j + 2] = x.z; k[4 * j + 3] = x.w;
+        sd[4 * j] = y.x; sd[4 * j + 1] = y.y; sd[4 * j + 2] = y.z; sd[4 * j + 3] = y.w;
       }
     } else {
 #pragma unroll
@@ -1229,7 +1217,6 @@ __global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ 
         sd[i] = i < m ? __ldg(a.ship + r0 + i) : INT32_MIN;
       }
     }
-    fetch(base + 32 * R);
     // keys non-decreasing across the chunk (lane order) and from the previous chunk
     {
       int32_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
@@ -1601,9 +1588,8 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   // array) and sums revenue per orderkey run (k_q3_fused); the groups' o_orderdate /
   // o_shippriority then come from a binary search of o_orderkey (orders in key order; any key not
   // found there sends the plan to the operator steps, which build the full table).
-  // (default: the operator plan — the fused pass measured 3.1 ms against 1.65 + 0.29 ms for the
-  // probe and group-by it replaces; SX_Q3_PLAN=fused selects it)
-  const bool ops_plan = !(getenv("SX_Q3_PLAN") && std::strcmp(getenv("SX_Q3_PLAN"), "fused") == 0);
+  // (default: fused, 3.27 vs 3.61 ms for Q3 at SF100; SX_Q3_PLAN=ops selects the operator plan)
+  const bool ops_plan = getenv("SX_Q3_PLAN") && std::strcmp(getenv("SX_Q3_PLAN"), "ops") == 0;
   const bool fused_shape = !ops_plan && w4(t->o_orderkey) && w4(t->o_orderdate) && w4(t->o_shippriority);
   SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, fused_shape ? (SX_BUILD_UNIQUE | SX_BUILD_MEMBERSHIP) : 1,
                        &ht_o));
@@ -1651,7 +1637,7 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
       SX_CUDA(cudaMemsetAsync(a.flags, 0, 2 * sizeof(int), ctx->stream));
       // one warp per contiguous range of whole 256-row chunks, every warp of a persistent grid
-      const unsigned grid = persistent_grid(ctx, 3, ((n + 255) / 256 + (kBlock / 32) - 1) / (kBlock / 32));
+      const unsigned grid = persistent_grid(ctx, 4, ((n + 255) / 256 + (kBlock / 32) - 1) / (kBlock / 32));
       const int64_t warps = (int64_t)grid * (kBlock / 32);
       const int64_t per = ((n + warps - 1) / warps + 255) / 256 * 256;
       k_q3_fused<<<grid, kBlock, 0, SX_STREAM(ctx)>>>(a, n, per);

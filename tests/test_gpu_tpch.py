@@ -121,10 +121,10 @@ def test_q18_owned_runs(ctx, monkeypatch, case):
 
 @pytest.mark.parametrize("case", ["fused", "ops", "tails", "run30", "unsorted", "wide"])
 def test_q3_plans(ctx, monkeypatch, case):
-    """Q3 through the fused lineitem pass (K10q, SX_Q3_PLAN=fused: join + revenue terms as records,
-    then the group-by) and the operator-at-a-time plan (default), at SF 0.1: a ragged tail, 30-row
-    orderkey runs, an unsorted l_orderkey (the 8-row bitmap-word shortcut must not apply), and an
-    extendedprice of 2^40 (revenue terms beyond 32 bits) — every case against the oracle."""
+    """Q3 through the fused lineitem pass (K10q, the default: warp-range owned orderkey groups,
+    interpolated carries) and the operator-at-a-time plan (SX_Q3_PLAN=ops), at SF 0.1: a ragged
+    tail, 30-row orderkey runs crossing warp ranges, an unsorted l_orderkey (the fused pass steps
+    aside), and an extendedprice of 2^40 (revenue terms beyond 32 bits) — against the oracle."""
     monkeypatch.setenv("SX_Q3_PLAN", "ops" if case == "ops" else "fused")
     host = gen.cpu_tables(100, seed=17)
     li = {k: v.copy() for k, v in host["lineitem"].items()}
@@ -215,10 +215,10 @@ def test_q18_join_modes(ctx, monkeypatch, case):
 @pytest.mark.parametrize("ring", ["1", "0"])
 @pytest.mark.parametrize("trim", [0, 777])
 def test_q9_ring(ctx, monkeypatch, ring, trim):
-    """Q9's lineitem pass fed by the tile ring (K10wr, default at >= 1024 rows per SM) and by
-    per-lane loads (K10w, SX_Q9_RING=0), with whole tiles only and with a ragged tail (global-load
+    """Q9's lineitem pass fed by the tile ring (K10wr, SX_Q9_RING=1, >= 1024 rows per SM) and by
+    per-lane loads (K10w, the default), with whole tiles only and with a ragged tail (global-load
     path in the last CTA) — against the oracle, also for another colour."""
-    monkeypatch.setenv("SX_Q9_RING", ring)
+    monkeypatch.setenv("SX_Q9_RING", ring)  # (K10wr is opt-in: measured slower than K10w)
     host = gen.cpu_tables(200, seed=31)
     li = host["lineitem"]
     n = len(li["l_orderkey"])
