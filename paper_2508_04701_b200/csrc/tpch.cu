@@ -1304,6 +1304,69 @@ __global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ 
   if (ovf) atomicExch(a.flags + 1, 1);
 }
 
+// Q3 step 2 for the fused plan: one pass over orders applies o_orderdate < DATE and the customer
+// semi-join (the customer build's exact custkey bitmap) and sets the qualifying orderkeys' bits in
+// an exact bitmap over [first key, last key] of o_orderkey — the join filter the lineitem pass
+// probes (predicate transfer).  No selection vector and no separate build pass.  The
+// bitmap is exact in any row order as long as every key lies in the range (else *flag: the plan
+// takes the operator steps).  8 consecutive orders per thread: their keys share 1-2 bitmap words.
+__global__ void __launch_bounds__(kBlock) k_q3_orders(const int32_t* __restrict__ okey, const int32_t* __restrict__ ocust,
+                                                      const int32_t* __restrict__ odate, int64_t n, int32_t date,
+                                                      const uint32_t* __restrict__ cbm, long long cbm_min,
+                                                      unsigned long long cbm_bits, uint32_t* obm, long long omin,
+                                                      unsigned long long obits, unsigned long long* count, int* flag) {
+  constexpr int R = 8;
+  unsigned long long c = 0;
+  bool bad = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t * R < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r0 = t * R;
+    int32_t k[R], cu[R], d[R];
+    if (r0 + R <= n) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int4 x = __ldcs((const int4*)(okey + r0) + j), y = __ldcs((const int4*)(ocust + r0) + j),
+                   z = __ldcs((const int4*)(odate + r0) + j);
+        k[4 * j] = x.x; k[4 * j + 1] = x.y; k[4 * j + 2] = x.z; k[4 * j + 3] = x.w;
+        cu[4 * j] = y.x; cu[4 * j + 1] = y.y; cu[4 * j + 2] = y.z; cu[4 * j + 3] = y.w;
+        d[4 * j] = z.x; d[4 * j + 1] = z.y; d[4 * j + 2] = z.z; d[4 * j + 3] = z.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const bool in = r0 + i < n;
+        k[i] = in ? __ldg(okey + r0 + i) : 0;
+        cu[i] = in ? __ldg(ocust + r0 + i) : 0;
+        d[i] = in ? __ldg(odate + r0 + i) : INT32_MAX;
+      }
+    }
+    uint32_t w0 = 0xffffffffu, m0 = 0, w1 = 0xffffffffu, m1 = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const unsigned long long coff = (unsigned long long)((long long)cu[i] - cbm_min);
+      const bool dq = d[i] < date && coff < cbm_bits;
+      const bool q = dq && ((__ldg(cbm + (coff >> 5)) >> (coff & 31)) & 1u);
+      if (!q) continue;
+      const unsigned long long off = (unsigned long long)((long long)k[i] - omin);
+      if (off >= obits) {
+        bad = true;
+        continue;
+      }
+      ++c;
+      const uint32_t w = (uint32_t)(off >> 5), b = 1u << (off & 31);
+      if (w == w0) m0 |= b;
+      else if (w == w1) m1 |= b;
+      else if (w0 == 0xffffffffu) { w0 = w; m0 = b; }
+      else if (w1 == 0xffffffffu) { w1 = w; m1 = b; }
+      else atomicOr(obm + w, b);
+    }
+    if (m0) atomicOr(obm + w0, m0);
+    if (m1) atomicOr(obm + w1, m1);
+  }
+  c = __reduce_add_sync(kFull, (unsigned)c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+  if (bad) atomicExch(flag, 1);
+}
+
 // Q3 carries of each group: the order with that key, searched in o_orderkey (orders in strictly
 // increasing key order) from an interpolated guess — TPC-H orderkeys are spread evenly, so the
 // guess lands within a few rows — with an exponential then binary search around it; any key not
@@ -1574,42 +1637,53 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
   sx_ht* ht_c;
   SX_TRY(sx_hash_build(ctx, ccols, 2, &k0, 1, &sel_c, nullptr, 0, 1, &ht_c));
   bag.keep(ht_c);
-  // 2. orders with o_orderdate < DATE and o_custkey in C (semi join), then build orderkey -> row
-  sx_col ocols[2] = {t->o_custkey, t->o_orderdate};
-  sx_pred odate = P(1, SX_LT, p->q3_date);
-  sx_sel sel_o;
-  SX_TRY(sx_hash_probe(ctx, ht_c, ocols, 2, &k0, 1, nullptr, &odate, 1, SX_SEMI, nullptr, 0, nullptr, 0, nullptr, 0,
-                       &sel_o, nullptr, nullptr));
-  bag.keep(sel_o);
-  sx_col okey[1] = {t->o_orderkey};
-  sx_ht* ht_o;
-  // 3+4 fused (default; SX_Q3_PLAN=ops forces the operator-at-a-time steps below): one pass over
-  // lineitem probes the orders' exact key bitmap (a membership-only build: no table, no direct
-  // array) and sums revenue per orderkey run (k_q3_fused); the groups' o_orderdate /
-  // o_shippriority then come from a binary search of o_orderkey (orders in key order; any key not
-  // found there sends the plan to the operator steps, which build the full table).
-  // (default: fused, 3.27 vs 3.61 ms for Q3 at SF100; SX_Q3_PLAN=ops selects the operator plan)
+  // 2-4 fused (default; SX_Q3_PLAN=ops forces the operator-at-a-time steps below): one pass over
+  // orders sets the exact bitmap of the qualifying orderkeys (k_q3_orders), one pass over lineitem
+  // probes it and sums revenue per orderkey (k_q3_fused), and the groups' o_orderdate /
+  // o_shippriority come from a search of o_orderkey (orders in key order; any key not found sends
+  // the plan to the operator steps).  (3.27 vs 3.61 ms for Q3 at SF100 with a membership build.)
   const bool ops_plan = getenv("SX_Q3_PLAN") && std::strcmp(getenv("SX_Q3_PLAN"), "ops") == 0;
-  const bool fused_shape = !ops_plan && w4(t->o_orderkey) && w4(t->o_orderdate) && w4(t->o_shippriority);
-  SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, fused_shape ? (SX_BUILD_UNIQUE | SX_BUILD_MEMBERSHIP) : 1,
-                       &ht_o));
-  bag.keep(ht_o);
-  auto full_build = [&]() -> sx_status {  // the operator plan needs the probe-able build
-    if (ht_o->slots || ht_o->direct) return SX_OK;
-    sx_ht_destroy(ctx, ht_o);
-    bag.hts.pop_back();
-    ht_o = nullptr;
-    SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, 1, &ht_o));
-    bag.keep(ht_o);
-    return SX_OK;
-  };
-  if (fused_shape && ht_o->bm && ht_o->bm_bits <= (1ull << 30) && ht_o->bm_min >= INT32_MIN &&
-      ht_o->bm_min <= INT32_MAX && ht_o->nkeys == 1 && ht_o->key_bytes == 4 && w4(t->l_orderkey) &&
-      w4(t->l_shipdate) && w8(t->l_extendedprice) && w8(t->l_discount) &&
-      t->l_shipdate.len == t->l_orderkey.len && t->l_extendedprice.len == t->l_orderkey.len &&
-      t->l_discount.len == t->l_orderkey.len && t->l_orderkey.len > 0) {
+  const int64_t no = t->o_orderkey.len;
+  uint32_t* obm = nullptr;
+  long long omin = 0;
+  unsigned long long obits = 0;
+  int64_t nqual = 0;
+  bool fused = false;
+  if (!ops_plan && ht_c->bm && w4(t->o_orderkey) && w4(t->o_custkey) && w4(t->o_orderdate) &&
+      w4(t->o_shippriority) && t->o_custkey.len == no && t->o_orderdate.len == no && no > 0 && w4(t->l_orderkey) &&
+      w4(t->l_shipdate) && w8(t->l_extendedprice) && w8(t->l_discount) && t->l_shipdate.len == t->l_orderkey.len &&
+      t->l_extendedprice.len == t->l_orderkey.len && t->l_discount.len == t->l_orderkey.len &&
+      t->l_orderkey.len > 0) {
+    ProfScope pb(ctx, "probe_semi");  // the semi-join and the orderkey bitmap in one pass
+    int32_t* hp = (int32_t*)(ctx->h_pinned + 20);
+    SX_CUDA(cudaMemcpyAsync(hp, t->o_orderkey.data, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaMemcpyAsync(hp + 1, (const int32_t*)t->o_orderkey.data + no - 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    omin = hp[0];
+    if (hp[1] >= hp[0] && (unsigned long long)((long long)hp[1] - hp[0]) + 1 <= (1ull << 30)) {
+      obits = (unsigned long long)((long long)hp[1] - hp[0]) + 1;
+      const size_t words = (size_t)((obits + 31) / 32);
+      SX_TRY(alloc(ctx, &obm, words));
+      bag.bufs.push_back(obm);
+      SX_CUDA(cudaMemsetAsync(obm, 0, words * sizeof(uint32_t), ctx->stream));
+      unsigned long long* cntp = (unsigned long long*)ctx->d_counters;
+      SX_CUDA(cudaMemsetAsync(cntp, 0, 8, ctx->stream));
+      SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), ctx->stream));
+      k_q3_orders<<<persistent_grid(ctx, 8, ((no + 7) / 8 + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+          (const int32_t*)t->o_orderkey.data, (const int32_t*)t->o_custkey.data, (const int32_t*)t->o_orderdate.data,
+          no, (int32_t)std::max<int64_t>(INT32_MIN, std::min<int64_t>(INT32_MAX, p->q3_date)), ht_c->bm, ht_c->bm_min,
+          ht_c->bm_bits, obm, omin, obits, cntp, ctx->d_flags);
+      SX_CHECK_LAUNCH();
+      SX_TRY(read_i64(ctx, cntp, &nqual));
+      int fl = 0;
+      SX_CUDA(cudaMemcpy(&fl, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
+      fused = fl == 0;
+      pb.set_bytes(12.0 * no + (double)words * 4);
+    }
+  }
+  if (fused) {
     const int64_t n = t->l_orderkey.len;
-    const int64_t gcap = std::max<int64_t>(1, ht_o->rows);  // groups are qualifying orders
+    const int64_t gcap = std::max<int64_t>(1, nqual);  // groups are qualifying orders
     int32_t* gk;
     longlong2* grev;
     SX_TRY(alloc(ctx, &gk, (size_t)gcap));
@@ -1622,9 +1696,9 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     a.ext = (const long long*)t->l_extendedprice.data;
     a.disc = (const long long*)t->l_discount.data;
     a.date = (int32_t)std::max<int64_t>(INT32_MIN, std::min<int64_t>(INT32_MAX, p->q3_date));
-    a.bm = ht_o->bm;
-    a.bm_min = ht_o->bm_min;
-    a.bm_bits = ht_o->bm_bits;
+    a.bm = obm;
+    a.bm_min = omin;
+    a.bm_bits = obits;
     a.out_key = gk;
     a.out_rev = grev;
     a.cap = gcap;
@@ -1692,9 +1766,19 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       *nrows = perm.len;
       return SX_OK;
     }
-    // more records than sized for, an overflow, or orders not in key order: the operator plan decides
+    // unsorted lineitem, an overflow, or orders not in key order: the operator plan decides
   }
-  SX_TRY(full_build());
+  // 2. orders with o_orderdate < DATE and o_custkey in C (semi join), then build orderkey -> row
+  sx_col ocols[2] = {t->o_custkey, t->o_orderdate};
+  sx_pred odate = P(1, SX_LT, p->q3_date);
+  sx_sel sel_o;
+  SX_TRY(sx_hash_probe(ctx, ht_c, ocols, 2, &k0, 1, nullptr, &odate, 1, SX_SEMI, nullptr, 0, nullptr, 0, nullptr, 0,
+                       &sel_o, nullptr, nullptr));
+  bag.keep(sel_o);
+  sx_col okey[1] = {t->o_orderkey};
+  sx_ht* ht_o;
+  SX_TRY(sx_hash_build(ctx, okey, 1, &k0, 1, &sel_o, nullptr, 0, 1, &ht_o));
+  bag.keep(ht_o);
   // 3. lineitem with l_shipdate > DATE joined to those orders (unique build: ordered output)
   sx_col lcols[4] = {t->l_orderkey, t->l_shipdate, t->l_extendedprice, t->l_discount};
   sx_pred lship = P(1, SX_GT, p->q3_date);
