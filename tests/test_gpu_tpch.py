@@ -233,6 +233,25 @@ def test_q9_ring(ctx, monkeypatch, ring, trim):
 
 
 
+@pytest.mark.parametrize("psw", ["1", "0", "wide-cost"])
+def test_q9_partsupp_index(ctx, monkeypatch, psw):
+    """Q9's partsupp lookups through the index by green-bitmap word (default), through the payload
+    hash table (SX_Q9_PSW=0), and with a supplycost beyond int32 (the index refuses: the table)."""
+    monkeypatch.setenv("SX_Q9_PSW", "0" if psw == "0" else "1")
+    host = gen.cpu_tables(200, seed=37)
+    if psw == "wide-cost":
+        host = dict(host)
+        ps = {k: v.copy() for k, v in host["partsupp"].items()}
+        ps["ps_supplycost"][::97] = 1 << 33
+        host["partsupp"] = ps
+    T = tpch.Tpch(ctx, to_dev(host))
+    for color in ("green", "red"):
+        got = T.run("q9", tpch.default_params(q9_color=color))
+        want = oracle.run_query("q9", host, oracle.default_params(q9_color=color))
+        assert rows_equal(got, want), diff_rows(got, want)
+
+
+
 def test_gpu_generator_matches_cpu_generator():
     cpu = gen.cpu_tables(10, seed=42)
     g = gen.gpu_tables(10, seed=42)
