@@ -233,6 +233,19 @@ def test_q9_ring(ctx, monkeypatch, ring, trim):
 
 
 
+@pytest.mark.parametrize("psw", ["1", "0"])
+def test_q9_repeated_partsupp_pair_fails(ctx, monkeypatch, psw):
+    """A repeated (ps_partkey, ps_suppkey) pair — the fused plan relies on it being a key — fails
+    loudly in both partsupp structures (DESIGN §3 reading) instead of picking one cost."""
+    monkeypatch.setenv("SX_Q9_PSW", psw)
+    host = dict(gen.cpu_tables(200, seed=37))
+    ps = {k: v.copy() for k, v in host["partsupp"].items()}
+    ps["ps_suppkey"][1::4] = ps["ps_suppkey"][0::4]
+    host["partsupp"] = ps
+    with pytest.raises(Exception, match="repeated"):
+        tpch.Tpch(ctx, to_dev(host)).run("q9")
+
+
 @pytest.mark.parametrize("psw", ["1", "0", "wide-cost"])
 def test_q9_partsupp_index(ctx, monkeypatch, psw):
     """Q9's partsupp lookups through the index by green-bitmap word (default), through the payload
