@@ -170,6 +170,87 @@ __global__ void __launch_bounds__(1024) k_topk_round(const __grid_constant__ Wor
   for (int i = threadIdx.x; i < keep; i += blockDim.x) pos_out[blockIdx.x * k + i] = (int32_t)sm[i * nw + (nw - 1)];
 }
 
+// ---- warp top-k (K14w, k <= 32) --------------------------------------------------------
+// Each warp scans a contiguous block of >= k rows keeping its k best composite keys sorted across
+// its lanes (lane i: the i-th best, all words in registers).  A row enters only if it beats the
+// current k-th best (rare after the first rows: ~k ln(rows/k) insertions per warp), by a
+// warp-wide shift.  The warps' lists (warps x k positions) then go through the tournament rounds.
+// One pass over the encoded words instead of one radix-select pass per varying digit (Q3's top-10
+// of 1.13e6 rows x 7 words: 14 digits, ~30 launches).
+__global__ void __launch_bounds__(256) k_topk_warp(const __grid_constant__ Words W, int64_t n, int k, int64_t per,
+                                                   int32_t* __restrict__ out_pos) {
+  const int lane = threadIdx.x & 31;
+  const int nw = W.nwords;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t lo = gw * per, hi = min(n, lo + per);
+  if (lo >= n) return;  // (warp-uniform)
+  uint32_t mine[kMaxWords];  // my list entry (lane < cnt)
+#pragma unroll
+  for (int j = 0; j < kMaxWords; ++j) mine[j] = 0xffffffffu;
+  int cnt = 0;  // warp-uniform list length
+  for (int64_t b = lo; b < hi; b += 32) {
+    const int64_t r = b + lane;
+    uint32_t w[kMaxWords];
+    const bool in = r < hi;
+#pragma unroll
+    for (int j = 0; j < kMaxWords; ++j) w[j] = (in && j < nw) ? __ldg(W.w[j] + r) : 0xffffffffu;
+    // the current k-th best (lane k-1) when the list is full
+    bool cand = in;
+    if (cnt == k) {
+      bool less = false, decided = false;
+#pragma unroll
+      for (int j = 0; j < kMaxWords; ++j) {
+        const uint32_t kj = __shfl_sync(kFull, mine[j], k - 1);
+        if (j < nw && !decided && w[j] != kj) {
+          less = w[j] < kj;
+          decided = true;
+        }
+      }
+      cand = in && less;
+    }
+    unsigned cb = __ballot_sync(kFull, cand);
+    while (cb) {
+      const int src = __ffs(cb) - 1;
+      cb &= cb - 1;
+      uint32_t nwv[kMaxWords];
+#pragma unroll
+      for (int j = 0; j < kMaxWords; ++j) nwv[j] = __shfl_sync(kFull, w[j], src);
+      // does it still beat the k-th best?  (position among the list: entries less than it)
+      bool my_less = false, decided = false;  // is my entry < new?
+#pragma unroll
+      for (int j = 0; j < kMaxWords; ++j) {
+        if (j < nw && !decided && mine[j] != nwv[j]) {
+          my_less = mine[j] < nwv[j];
+          decided = true;
+        }
+      }
+      const unsigned lb = __ballot_sync(kFull, lane < cnt && my_less);
+      const int pos = __popc(lb);  // list entries before the new one (they are a prefix)
+      if (pos >= k) continue;  // not better than the k-th best any more
+#pragma unroll
+      for (int j = 0; j < kMaxWords; ++j) {
+        const uint32_t up = __shfl_up_sync(kFull, mine[j], 1);
+        if (lane > pos) mine[j] = up;
+        else if (lane == pos) mine[j] = nwv[j];
+      }
+      cnt = min(cnt + 1, k);
+    }
+  }
+  uint32_t mpos = 0;  // my entry's position word (the last word; selects, no dynamic index)
+#pragma unroll
+  for (int j = 0; j < kMaxWords; ++j) mpos = j == nw - 1 ? mine[j] : mpos;
+  if (lane < k) out_pos[gw * k + lane] = lane < cnt ? (int32_t)mpos : -1;
+}
+
+// compact the warp lists' positions (drop -1 entries of short lists), keep order irrelevant
+__global__ void k_topk_compact(const int32_t* __restrict__ in, int64_t m, int32_t* __restrict__ out,
+                               unsigned long long* count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = in[i];
+    if (v >= 0) out[atomicAdd(count, 1ull)] = v;
+  }
+}
+
 // ---- radix select -------------------------------------------------------------------
 struct SelState {
   unsigned long long k_rem;
@@ -715,7 +796,30 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
   // key words (Q3's 1.1e6 rows x 7 words: 0.35 ms vs 2.0 ms for 552 chunk sorts).
   // SX_TOPK=select / =tournament force either path.
   const char* topk_env = getenv("SX_TOPK");
-  const bool topk_tour = topk_env ? std::strcmp(topk_env, "tournament") == 0 : n <= 32 * (int64_t)kBitonicMax;
+  // K14w for k <= 32 over many rows (SX_TOPK=warp forces it at any size), then the rounds below
+  const bool topk_warp = outn <= 32 && outn < n &&
+                         (topk_env ? std::strcmp(topk_env, "warp") == 0 : n > 32 * (int64_t)kBitonicMax);
+  const int32_t* warp_pos = nullptr;
+  int64_t warp_m = 0;
+  if (topk_warp) {
+    // warps with >= k rows each (so lists fill), at most ~4 per SM-thread-slot
+    int64_t warps = std::min<int64_t>((int64_t)ctx->num_sms * 64, std::max<int64_t>(1, n / (32 * outn)));
+    const int64_t per = (n + warps - 1) / warps;
+    warps = (n + per - 1) / per;
+    int32_t *lists, *cpos;
+    SX_TRY(scr.get(&lists, (size_t)(warps * outn)));
+    SX_TRY(scr.get(&cpos, (size_t)(warps * outn)));
+    k_topk_warp<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, SX_STREAM(ctx)>>>(W, n, (int)outn, per, lists);
+    SX_CHECK_LAUNCH();
+    unsigned long long* cntp = (unsigned long long*)ctx->d_counters;
+    SX_CUDA(cudaMemsetAsync(cntp, 0, 8, ctx->stream));
+    k_topk_compact<<<persistent_grid(ctx, 4, (warps * outn + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
+        lists, warps * outn, cpos, cntp);
+    SX_CHECK_LAUNCH();
+    SX_TRY(read_i64(ctx, cntp, &warp_m));
+    warp_pos = cpos;
+  }
+  const bool topk_tour = topk_warp || (topk_env ? std::strcmp(topk_env, "tournament") == 0 : n <= 32 * (int64_t)kBitonicMax);
   if (topk_tour && outn <= 1024 && outn < n) {
     const size_t smem = (size_t)kBitonicMax * nwords * sizeof(uint32_t);
     SX_CUDA(cudaFuncSetAttribute(k_topk_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -724,8 +828,8 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
     const int64_t c1 = (n + kBitonicMax - 1) / kBitonicMax;
     SX_TRY(scr.get(&pa, (size_t)(c1 * outn)));
     SX_TRY(scr.get(&pb, (size_t)(c1 * outn)));
-    const int32_t* cur = nullptr;  // nullptr: rows 0..m-1
-    int64_t m = n;
+    const int32_t* cur = warp_pos;  // nullptr: rows 0..m-1 (K14w: its candidate positions)
+    int64_t m = warp_pos ? warp_m : n;
     int32_t* dst = pa;
     while (m > kBitonicMax) {
       const int64_t chunks = (m + kBitonicMax - 1) / kBitonicMax;

@@ -352,16 +352,17 @@ def test_sort_topk(ctx, n, k):
         assert np.array_equal(perm.cpu().numpy(), want), keys
 
 
-@pytest.mark.parametrize("mode", ["tournament", "select"])
+@pytest.mark.parametrize("mode", ["tournament", "select", "warp"])
 def test_topk_paths(ctx, monkeypatch, mode):
-    """Top-k (k <= 1024) through the tournament rounds (default) and the radix select
-    (SX_TOPK=select), several rounds deep (n = 3e5, k = 1024 -> 150 chunks -> ... -> one CTA)."""
+    """Top-k (k <= 1024) through the tournament rounds, the radix select (SX_TOPK=select) and the
+    warp lists (K14w, SX_TOPK=warp, k <= 32), several rounds deep (n = 3e5, k = 1024 -> 150 chunks
+    -> ... -> one CTA)."""
     monkeypatch.setenv("SX_TOPK", mode)
     rng = np.random.default_rng(11)
     n = 300_000
     v = rng.integers(-50, 50, n).astype(np.int64)  # heavy ties: the position word decides
     w = rng.integers(0, 3, n).astype(np.int32)
-    for k in (1, 7, 1000, 1024):
+    for k in (1, 7, 32, 1000, 1024):
         perm = ctx.sort_topk([c(dev(v)), sx.col(dev(w), A.SX_I32)], [(0, 1), (1, 0)], k)
         want = oracle.sort([v.tolist(), w.tolist()], [1, 0], k)
         assert np.array_equal(perm.cpu().numpy(), want), k
