@@ -1948,12 +1948,13 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       }
     } pt{ctx, {}};
     sx_ht* ht_lo;
-    // partsupp: the index by green-bitmap word (dense scans; SX_Q9_PSW=0: the table), else the
-    // semi-join + payload table
+    // partsupp: the semi-join + payload table; or (opt-in, SX_Q9_PSW=1, K10w only) the index by
+    // green-bitmap word — measured slower: 5.16 vs 4.35 ms for the lineitem pass and 0.87 vs
+    // 0.54 ms to build (the per-lookup entry scan is a chain of dependent L2 reads)
     int64_t* psw_off = nullptr;
     uint2* psw_ent = nullptr;
-    const bool psw_off_env = getenv("SX_Q9_PSW") && getenv("SX_Q9_PSW")[0] == '0';
-    if (!gather && !psw_off_env && ht_p->bm && w4(t->ps_partkey) && w4(t->ps_suppkey) && w8(t->ps_supplycost) &&
+    const bool psw_on = getenv("SX_Q9_PSW") && getenv("SX_Q9_PSW")[0] == '1';
+    if (!gather && wscan && psw_on && ht_p->bm && w4(t->ps_partkey) && w4(t->ps_suppkey) && w8(t->ps_supplycost) &&
         t->ps_suppkey.len == t->ps_partkey.len && t->ps_supplycost.len == t->ps_partkey.len) {
       ProfScope pb(ctx, "hash_build");
       const int64_t nps = t->ps_partkey.len;

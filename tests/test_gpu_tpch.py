@@ -248,8 +248,8 @@ def test_q9_repeated_partsupp_pair_fails(ctx, monkeypatch, psw):
 
 @pytest.mark.parametrize("psw", ["1", "0", "wide-cost"])
 def test_q9_partsupp_index(ctx, monkeypatch, psw):
-    """Q9's partsupp lookups through the index by green-bitmap word (default), through the payload
-    hash table (SX_Q9_PSW=0), and with a supplycost beyond int32 (the index refuses: the table)."""
+    """Q9's partsupp lookups through the index by green-bitmap word (SX_Q9_PSW=1), through the
+    payload hash table (the default), and with a supplycost beyond int32 (the index refuses)."""
     monkeypatch.setenv("SX_Q9_PSW", "0" if psw == "0" else "1")
     host = gen.cpu_tables(200, seed=37)
     if psw == "wide-cost":
