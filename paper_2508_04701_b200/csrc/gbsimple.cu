@@ -455,6 +455,50 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
   (void)g;
 }
 
+// K18p2's second level: each CTA takes whole level-1 partitions (contiguous rows) and splits each
+// into kSub sub-partitions by hash bits 43..47 (disjoint from the level-1 bits 48..57 and the
+// shared-table slot bits 0..11): a shared histogram, its scan (the sub-partitions' offsets), then a
+// scatter of the key and value columns inside the partition's own range of the output.
+constexpr int kSubBits = 5, kSub = 1 << kSubBits;
+__global__ void __launch_bounds__(kGsThreads) k_gbs_subpart(const __grid_constant__ GsSpec s,
+                                                            const int64_t* __restrict__ off1, int P1, int nv,
+                                                            const __grid_constant__ GsSpec d, int64_t* __restrict__ off2) {
+  __shared__ int cnt[kSub];
+  __shared__ int64_t start[kSub];
+  __shared__ int cur[kSub];
+  for (int p = blockIdx.x; p < P1; p += gridDim.x) {
+    const int64_t lo = off1[p], hi = off1[p + 1];
+    if (threadIdx.x < kSub) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x)
+      atomicAdd(&cnt[(hash64((uint64_t)ld_key(s, r)) >> 43) & (kSub - 1)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t run = lo;
+      for (int b = 0; b < kSub; ++b) {
+        start[b] = run;
+        off2[(int64_t)p * kSub + b] = run;
+        run += cnt[b];
+        cur[b] = 0;
+      }
+      if (p == P1 - 1) off2[(int64_t)P1 * kSub] = run;
+    }
+    __syncthreads();
+    for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+      const long long k = ld_key(s, r);
+      const int b = (int)((hash64((uint64_t)k) >> 43) & (kSub - 1));
+      const int64_t pos = start[b] + atomicAdd(&cur[b], 1);
+      if (s.key_bytes == 4) ((int32_t*)d.key)[pos] = (int32_t)k;
+      else ((long long*)d.key)[pos] = k;
+      for (int c = 0; c < nv; ++c) {
+        if (s.vbytes[c] == 4) ((int32_t*)d.val[c])[pos] = __ldcs((const int32_t*)s.val[c] + r);
+        else ((long long*)d.val[c])[pos] = __ldcs((const long long*)s.val[c] + r);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <class F>
 sx_status with_sig(int sig, F&& f) {
   switch (sig) {
@@ -487,7 +531,7 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
                     sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups) {
   const bool off = getenv("SX_GB_SIMPLE") && getenv("SX_GB_SIMPLE")[0] == '0';
   if (off || nkeys != 1 || in_sel || nwhere || having || naggs < 1 || naggs > SX_MAX_AGGS || groups_hint < 1 ||
-      groups_hint > (1 << 21))
+      groups_hint > (1 << 27))
     return SX_EUNSUPPORTED;
   if (keys[0].fn != SX_KEY_IDENTITY || keys[0].col < 0 || keys[0].col >= ncols) return SX_EUNSUPPORTED;
   const sx_col& kc = cols[keys[0].col];
@@ -581,11 +625,14 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
   int bits = 0;
   std::vector<int64_t> offs;
   int64_t* d_off = nullptr;
+  int Pn = 0;  // partitions the shared tables aggregate
   if (part) {
     // fan-out 1024 (the partitioner's maximum): <= 2048 expected groups per shared table, and
-    // enough partitions to spread over every SM whatever G is
+    // enough partitions to spread over every SM whatever G is; above 2^21 groups a second level
+    // (K18p2) splits every partition 32 ways
     bits = 10;
-    if ((groups_hint >> bits) > 2048) return SX_EUNSUPPORTED;
+    const bool two = (groups_hint >> bits) > 2048;
+    if (two && (groups_hint >> (bits + kSubBits)) > 2048) return SX_EUNSUPPORTED;
     const int P = 1 << bits;
     DCol kd{kc.data, kt, 0};
     DCol carry[1 + kGsMaxVals];
@@ -608,6 +655,22 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
     for (int c = 0; c < s.nv; ++c) s.val[c] = outp[1 + c];
     SX_TRY(scr.get(&d_off, (size_t)P + 1));
     SX_CUDA(cudaMemcpyAsync(d_off, offs.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, ctx->stream));
+    Pn = P;
+    if (two) {
+      GsSpec d2 = s;
+      void* o2[1 + kGsMaxVals];
+      for (int c = 0; c <= s.nv; ++c) SX_TRY(scr.get((char**)&o2[c], (size_t)n * width[c]));
+      d2.key = o2[0];
+      for (int c = 0; c < s.nv; ++c) d2.val[c] = o2[1 + c];
+      int64_t* d_off2;
+      SX_TRY(scr.get(&d_off2, (size_t)P * kSub + 1));
+      k_gbs_subpart<<<persistent_grid(ctx, 2, P), kGsThreads, 0, SX_STREAM(ctx)>>>(s, d_off, P, s.nv, d2, d_off2);
+      SX_CHECK_LAUNCH();
+      s.key = d2.key;
+      for (int c = 0; c < s.nv; ++c) s.val[c] = d2.val[c];
+      d_off = d_off2;
+      Pn = P * kSub;
+    }
   }
   for (int attempt = 0; attempt < 2; ++attempt) {
     void* okey;
@@ -621,7 +684,7 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
     SX_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(int), ctx->stream));
     GsGlobal g{};
     if (part) {
-      const int P = 1 << bits;
+      const int P = Pn;
       const size_t smem = (size_t)(kGsPartSlots + 1) * 8 * (1 + s.nst);
       SX_TRY(with_sig(sig, [&](auto sg) -> sx_status {
         using SIG = decltype(sg);

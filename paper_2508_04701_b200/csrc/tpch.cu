@@ -978,13 +978,23 @@ struct Q9FusedProg {
       bool f = alive[u] && ((sw[u] >> (soff[u] & 31)) & 1u) && of;
       int64_t cost = 0;
       if (f && psw_off) {
+        // the word's block: 8 entries loaded together (one round trip), the rare rest in a loop
+        const int64_t lo = (int64_t)p0[u].x, hi = (int64_t)p0[u].y;
         bool hit = false;
-        for (int64_t e = (int64_t)p0[u].x; e < (int64_t)p0[u].y; ++e) {
-          const uint2 en = __ldg(psw_ent + e);
-          if (en.x == h[u]) {
-            cost = (int64_t)(int32_t)en.y;
+        uint2 en[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) en[q] = lo + q < hi ? __ldg(psw_ent + lo + q) : make_uint2(0xffffffffu, 0u);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (!hit && en[q].x == h[u]) {
+            cost = (int64_t)(int32_t)en[q].y;
             hit = true;
-            break;
+          }
+        for (int64_t e = lo + 8; !hit && e < hi; ++e) {
+          const uint2 x = __ldg(psw_ent + e);
+          if (x.x == h[u]) {
+            cost = (int64_t)(int32_t)x.y;
+            hit = true;
           }
         }
         f = hit;

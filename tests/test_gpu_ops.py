@@ -127,10 +127,12 @@ SIMPLE_AGGS = [("sum", [(1, [(1, 1, 0)])]), ("count", []), ("min", [(1, [(1, 1, 
 
 
 @pytest.mark.parametrize("G,hint,wide", [(4, 4, False), (100, 128, False), (1000, 1024, True), (5000, 5000, False),
-                                         (200_000, 200_000, False), (3000, 1500, False), (300, 0, False)])
+                                         (200_000, 200_000, False), (3000, 1500, False), (300, 0, False),
+                                         (3_000_000, 3_000_000, False)])
 def test_groupby_plain_shape(ctx, G, hint, wide):
     """K18 (the plain shape: one int64 key, plain-column aggregates; >= 2^20 rows): shared replicas
-    (hint <= 1024), partitioned shared tables (hint > 1024), an under-hinted G (falls back), the
+    (hint <= 1024), partitioned shared tables (hint > 1024; two partition levels above 2^21),
+    an under-hinted G (falls back), the
     key INT64_MIN (the shared tables' EMPTY marker: side slot), values >= 2^40 (exact global
     path in K18s), an int32 value column — against the oracle."""
     rng = np.random.default_rng(G)
