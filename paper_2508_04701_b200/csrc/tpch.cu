@@ -738,45 +738,6 @@ __global__ void k_date_fill_sorted(const KT* __restrict__ keys, const int32_t* _
   if (unsorted) atomicExch((unsigned long long*)bad + 1, 1ull);
 }
 
-// Q9's partsupp index (executor-internal, replaces the payload hash table when it applies): the
-// partsupp rows of green parts grouped by the 32-bit word of the green-part bitmap holding their
-// partkey's bit — word w's entries at [woff[w], woff[w+1]), each {bit | suppkey << 5, cost} in 8
-// bytes.  A lookup of (partkey, suppkey) reads woff[w..w+1] and scans ~7 entries (one or two
-// sectors): two dependent L2 reads into a ~40 MB structure, instead of one random DRAM line of a
-// 134 MB table (the green-part bitmap's density, 5.4%, keeps the blocks short).  Needs suppkey <
-// 2^27 and costs within int32 (flags[0] else; the plan then builds the payload table), and
-// flags[1] a repeated (partkey, suppkey) pair (PK side: the plan fails, as the table build does).
-__global__ void k_psw_count(const int32_t* __restrict__ pk, int64_t n, const uint32_t* __restrict__ bm, long long bmin,
-                            unsigned long long bbits, int32_t* __restrict__ wcount) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long off = (unsigned long long)((long long)__ldcs(pk + r) - bmin);
-    if (off < bbits && ((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u)) atomicAdd(wcount + (off >> 5), 1);
-  }
-}
-__global__ void k_psw_fill(const int32_t* __restrict__ pk, const int32_t* __restrict__ sk,
-                           const long long* __restrict__ cost, int64_t n, const uint32_t* __restrict__ bm, long long bmin,
-                           unsigned long long bbits, const int64_t* __restrict__ woff, int32_t* __restrict__ wcur,
-                           uint2* __restrict__ ent, int* flags) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long off = (unsigned long long)((long long)__ldcs(pk + r) - bmin);
-    if (!(off < bbits && ((__ldg(bm + (off >> 5)) >> (off & 31)) & 1u))) continue;
-    const int32_t s = __ldg(sk + r);
-    const long long c = __ldg(cost + r);
-    if (s < 0 || s >= (1 << 27) || c != (long long)(int32_t)c) atomicExch(flags, 1);
-    const int64_t pos = woff[off >> 5] + atomicAdd(wcur + (off >> 5), 1);
-    ent[pos] = make_uint2((uint32_t)(off & 31) | ((uint32_t)s << 5), (uint32_t)(int32_t)c);
-  }
-}
-__global__ void k_psw_dupcheck(const int64_t* __restrict__ woff, const uint2* __restrict__ ent, int64_t nwords,
-                               int* flags) {
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t lo = woff[w], hi = woff[w + 1];
-    for (int64_t i = lo; i < hi; ++i)
-      for (int64_t j = i + 1; j < hi; ++j)
-        if (ent[i].x == ent[j].x) atomicExch(flags + 1, 1);
-  }
-}
-
 template <typename KT, int OKB>
 struct Q9FusedProg {
   const int32_t *partkey, *suppkey;
@@ -788,8 +749,6 @@ struct Q9FusedProg {
   const ulonglong2* ps;   // (partkey, suppkey) -> ps_supplycost
   uint32_t ps_mask;
   int ps_bits;
-  const int64_t* psw_off;  // partsupp index by green-bitmap word (k_psw_*), or null: the table
-  const uint2* psw_ent;
   // suppkey -> s_nationkey and orderkey -> o_orderdate: direct-address arrays over each key range,
   // valid where the build's exact bitmap has the key (entries elsewhere are never read)
   const uint32_t* sup_bm;
@@ -960,45 +919,16 @@ struct Q9FusedProg {
       ow[u] = (oi && ord_bm) ? __ldg(ord_bm + (ooff[u] >> 5)) : 0u;
       ov[u] = oi ? __ldg(ord_val + ooff[u]) : kNoDate;
       pkey[u] = ((uint64_t)(uint32_t)pk[u] << 32) | (uint32_t)sk[u];
-      if (psw_off) {  // index by bitmap word: its entry range (scanned below)
-        const unsigned long long poff = (unsigned long long)((long long)pk[u] - pbm_min);
-        p0[u] = alive[u] ? make_ulonglong2(__ldg(psw_off + (poff >> 5)), __ldg(psw_off + (poff >> 5) + 1))
-                         : make_ulonglong2(0ull, 0ull);
-        h[u] = (uint32_t)(poff & 31) | ((uint32_t)sk[u] << 5);
-        reg[u] = nullptr;
-      } else {
-        reg[u] = ps + pt_region_base(pkey[u], ps_bits, ps_mask);
-        h[u] = (uint32_t)hash64(pkey[u]) & ps_mask;
-        p0[u] = alive[u] ? __ldg(reg[u] + h[u]) : make_ulonglong2(~0ull, 0ull);
-      }
+      reg[u] = ps + pt_region_base(pkey[u], ps_bits, ps_mask);
+      h[u] = (uint32_t)hash64(pkey[u]) & ps_mask;
+      p0[u] = alive[u] ? __ldg(reg[u] + h[u]) : make_ulonglong2(~0ull, 0ull);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool of = ord_bm ? ((ow[u] >> (ooff[u] & 31)) & 1u) != 0 : ov[u] != kNoDate;
       bool f = alive[u] && ((sw[u] >> (soff[u] & 31)) & 1u) && of;
       int64_t cost = 0;
-      if (f && psw_off) {
-        // the word's block: 8 entries loaded together (one round trip), the rare rest in a loop
-        const int64_t lo = (int64_t)p0[u].x, hi = (int64_t)p0[u].y;
-        bool hit = false;
-        uint2 en[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) en[q] = lo + q < hi ? __ldg(psw_ent + lo + q) : make_uint2(0xffffffffu, 0u);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (!hit && en[q].x == h[u]) {
-            cost = (int64_t)(int32_t)en[q].y;
-            hit = true;
-          }
-        for (int64_t e = lo + 8; !hit && e < hi; ++e) {
-          const uint2 x = __ldg(psw_ent + e);
-          if (x.x == h[u]) {
-            cost = (int64_t)(int32_t)x.y;
-            hit = true;
-          }
-        }
-        f = hit;
-      } else if (f) {
+      if (f) {
         ulonglong2 s = p0[u];
         uint32_t hh = h[u];
         for (;;) {
@@ -1958,50 +1888,7 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       }
     } pt{ctx, {}};
     sx_ht* ht_lo;
-    // partsupp: the semi-join + payload table; or (opt-in, SX_Q9_PSW=1, K10w only) the index by
-    // green-bitmap word — measured slower: 5.16 vs 4.35 ms for the lineitem pass and 0.87 vs
-    // 0.54 ms to build (the per-lookup entry scan is a chain of dependent L2 reads)
-    int64_t* psw_off = nullptr;
-    uint2* psw_ent = nullptr;
-    const bool psw_on = getenv("SX_Q9_PSW") && getenv("SX_Q9_PSW")[0] == '1';
-    if (!gather && wscan && psw_on && ht_p->bm && w4(t->ps_partkey) && w4(t->ps_suppkey) && w8(t->ps_supplycost) &&
-        t->ps_suppkey.len == t->ps_partkey.len && t->ps_supplycost.len == t->ps_partkey.len) {
-      ProfScope pb(ctx, "hash_build");
-      const int64_t nps = t->ps_partkey.len;
-      const int64_t nwords = (int64_t)((ht_p->bm_bits + 31) / 32);
-      int32_t *wcount, *wcur;
-      SX_TRY(alloc(ctx, &wcount, (size_t)nwords));
-      bag.bufs.push_back(wcount);
-      SX_TRY(alloc(ctx, &wcur, (size_t)nwords));
-      bag.bufs.push_back(wcur);
-      SX_TRY(alloc(ctx, &psw_off, (size_t)nwords + 1));
-      bag.bufs.push_back(psw_off);
-      SX_CUDA(cudaMemsetAsync(wcount, 0, nwords * sizeof(int32_t), ctx->stream));
-      SX_CUDA(cudaMemsetAsync(wcur, 0, nwords * sizeof(int32_t), ctx->stream));
-      SX_CUDA(cudaMemsetAsync(ctx->d_flags, 0, 2 * sizeof(int), ctx->stream));
-      const unsigned g = persistent_grid(ctx, 8, (nps + kBlock - 1) / kBlock);
-      if (nps > 0)
-        k_psw_count<<<g, kBlock, 0, SX_STREAM(ctx)>>>((const int32_t*)t->ps_partkey.data, nps, ht_p->bm, ht_p->bm_min,
-                                                      ht_p->bm_bits, wcount);
-      SX_CHECK_LAUNCH();
-      int64_t nent = 0;
-      SX_TRY(scan_counts(ctx, wcount, nwords, psw_off, &nent));
-      SX_TRY(alloc(ctx, &psw_ent, (size_t)std::max<int64_t>(nent, 1)));
-      bag.bufs.push_back(psw_ent);
-      if (nps > 0)
-        k_psw_fill<<<g, kBlock, 0, SX_STREAM(ctx)>>>((const int32_t*)t->ps_partkey.data, (const int32_t*)t->ps_suppkey.data,
-                                                     (const long long*)t->ps_supplycost.data, nps, ht_p->bm,
-                                                     ht_p->bm_min, ht_p->bm_bits, psw_off, wcur, psw_ent, ctx->d_flags);
-      k_psw_dupcheck<<<persistent_grid(ctx, 8, (nwords + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(
-          psw_off, psw_ent, nwords, ctx->d_flags);
-      SX_CHECK_LAUNCH();
-      int fl[2] = {0, 0};
-      SX_CUDA(cudaMemcpy(fl, ctx->d_flags, sizeof fl, cudaMemcpyDeviceToHost));
-      if (fl[1]) return set_err(ctx, SX_EINVAL, "Q9: payload table: repeated or reserved key (ps_partkey, ps_suppkey)");
-      if (fl[0]) psw_off = nullptr;  // a suppkey or cost outside the packed entry: the table below
-      pb.set_bytes(4.0 * nps + 16.0 * nent + 8.0 * nwords);
-    }
-    if (!psw_off) {
+    {
       sx_sel sel_ps;
       SX_TRY(sx_hash_probe(ctx, ht_p, pscols, 2, &k0, 1, nullptr, nullptr, 0, SX_SEMI, nullptr, 0, nullptr, 0, nullptr,
                            0, &sel_ps, nullptr, nullptr));
@@ -2132,7 +2019,7 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
     int64_t bad = 0;
     SX_TRY(read_i64(ctx, d_bad, &bad));
     if (bad) return set_err(ctx, SX_EUNSUPPORTED, "Q9: o_orderdate outside the int16 day range");
-    if (!psw_off && pt.t[0].kb != 8) return set_err(ctx, SX_EINVAL, "Q9: unexpected table layouts");
+    if (pt.t[0].kb != 8) return set_err(ctx, SX_EINVAL, "Q9: unexpected table layouts");
     ProfScope pg(ctx, "probe_groupby");
     sx_col tcols[6] = {t->s_nationkey, t->ps_supplycost, t->l_quantity, t->l_extendedprice, t->l_discount,
                        t->o_orderdate};  // types only: the plan's state layout
@@ -2167,8 +2054,6 @@ SX_EXPORT sx_status sx_tpch_q9(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       pr.ps = pt.t[0].slots;
       pr.ps_mask = pt.t[0].mask;
       pr.ps_bits = pt.t[0].pbits;
-      pr.psw_off = psw_off;
-      pr.psw_ent = psw_ent;
       pr.sup_bm = ht_s->bm;
       pr.sup_min = ht_s->bm_min;
       pr.sup_n = ht_s->bm_bits;

@@ -233,35 +233,15 @@ def test_q9_ring(ctx, monkeypatch, ring, trim):
 
 
 
-@pytest.mark.parametrize("psw", ["1", "0"])
-def test_q9_repeated_partsupp_pair_fails(ctx, monkeypatch, psw):
+def test_q9_repeated_partsupp_pair_fails(ctx):
     """A repeated (ps_partkey, ps_suppkey) pair — the fused plan relies on it being a key — fails
-    loudly in both partsupp structures (DESIGN §3 reading) instead of picking one cost."""
-    monkeypatch.setenv("SX_Q9_PSW", psw)
+    loudly (DESIGN §3 reading) instead of picking one cost."""
     host = dict(gen.cpu_tables(200, seed=37))
     ps = {k: v.copy() for k, v in host["partsupp"].items()}
     ps["ps_suppkey"][1::4] = ps["ps_suppkey"][0::4]
     host["partsupp"] = ps
     with pytest.raises(Exception, match="repeated"):
         tpch.Tpch(ctx, to_dev(host)).run("q9")
-
-
-@pytest.mark.parametrize("psw", ["1", "0", "wide-cost"])
-def test_q9_partsupp_index(ctx, monkeypatch, psw):
-    """Q9's partsupp lookups through the index by green-bitmap word (SX_Q9_PSW=1), through the
-    payload hash table (the default), and with a supplycost beyond int32 (the index refuses)."""
-    monkeypatch.setenv("SX_Q9_PSW", "0" if psw == "0" else "1")
-    host = gen.cpu_tables(200, seed=37)
-    if psw == "wide-cost":
-        host = dict(host)
-        ps = {k: v.copy() for k, v in host["partsupp"].items()}
-        ps["ps_supplycost"][::97] = 1 << 33
-        host["partsupp"] = ps
-    T = tpch.Tpch(ctx, to_dev(host))
-    for color in ("green", "red"):
-        got = T.run("q9", tpch.default_params(q9_color=color))
-        want = oracle.run_query("q9", host, oracle.default_params(q9_color=color))
-        assert rows_equal(got, want), diff_rows(got, want)
 
 
 
