@@ -6,14 +6,15 @@
 // COUNT or SUM / MIN / MAX / AVG of one integer column — the aggregation runs in shared memory
 // for every G the partitioner can split down to a shared table:
 //
-//   K18s (hinted G <= 1024): each CTA aggregates a contiguous chunk of rows into R replicas of a
-//        shared-memory hash table (lane l uses replica l % R, so small G does not serialise on a
-//        few shared addresses), then merges its replicas into a global table (one atomic per
-//        group and state per CTA) from which the groups are emitted;
-//   K18p (hinted G <= 2^21): the key and value columns are radix-partitioned on hash bits 48..
-//        (K7, the join's partitioner) into P partitions of <= ~1024 expected groups; one CTA per
-//        partition aggregates it in a shared table and writes its groups straight to the output
-//        (partitions hold disjoint keys, so no merge).
+//   K18s (a 2 x hint-slot table fits ~200 KB, G <~ 2500): each CTA aggregates a contiguous chunk
+//        of rows into R replicas of a shared-memory hash table (lane l uses replica l % R, so
+//        small G does not serialise on a few shared addresses), then merges its replicas into a
+//        global table (one atomic per group and state per CTA) from which the groups are emitted;
+//   K18p (hinted G <= 2^26): the key and value columns are radix-partitioned on hash bits 48..
+//        (K7, the join's partitioner) into 1024 partitions — above 2^21 groups each is split 32
+//        ways more by bits 43..47 (K18p2, segment-local) — and one CTA per partition aggregates
+//        it in a shared table and writes its groups straight to the output (partitions hold
+//        disjoint keys, so no merge).
 //
 // Exactness (readings R2/R3): shared partial sums are exact while every value is < 2^40 in
 // magnitude and a CTA sums <= 2^22 rows (checked: a row outside takes an exact global 96-bit
@@ -620,7 +621,12 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
   unsigned long long* cursor = (unsigned long long*)ctx->d_counters;
   s.out_cursor = cursor;
   s.flags = ctx->d_flags;
-  const bool part = groups_hint > 1024;
+  // K18s while one CTA's replicated tables fit ~200 KB of shared memory (S = 2 x hint slots; the
+  // partitioned path leaves 1-4 groups per partition for G ~ 2048-4096: every thread of the CTA
+  // on the same few shared addresses, 172 ms for G = 2048), else K18p
+  uint32_t S_loc = 16;
+  while (S_loc < (uint32_t)(2 * groups_hint)) S_loc <<= 1;
+  const bool part = (size_t)(S_loc + 1) * 8 * (1 + s.nst) > (200u << 10);
   // K18p partitioning (once, outside the capacity retry)
   int bits = 0;
   std::vector<int64_t> offs;
@@ -709,9 +715,9 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
       }
       g.mask = C - 1;
       k_gbs_init<<<persistent_grid(ctx, 4, (C + kBlock) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(s, g);
-      // shared table: S slots (load <= 0.5 at the hint), R replicas in <= 96 KB
-      uint32_t S = 16;
-      while (S < (uint32_t)(2 * groups_hint)) S <<= 1;
+      // shared table: S slots (load <= 0.5 at the hint), R replicas in <= 96 KB (one table up to
+      // ~200 KB)
+      const uint32_t S = S_loc;
       const size_t tab = (size_t)(S + 1) * 8 * (1 + s.nst);
       int R = (int)std::max<size_t>(1, std::min<size_t>(32, (96u << 10) / tab));
       while (32 % R) --R;

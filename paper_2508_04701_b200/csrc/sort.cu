@@ -796,9 +796,9 @@ SX_EXPORT sx_status sx_sort_topk(sx_ctx* ctx, const sx_col* cols, int ncols, con
   // key words (Q3's 1.1e6 rows x 7 words: 0.35 ms vs 2.0 ms for 552 chunk sorts).
   // SX_TOPK=select / =tournament force either path.
   const char* topk_env = getenv("SX_TOPK");
-  // K14w for k <= 32 over many rows (SX_TOPK=warp forces it at any size), then the rounds below
-  const bool topk_warp = outn <= 32 && outn < n &&
-                         (topk_env ? std::strcmp(topk_env, "warp") == 0 : n > 32 * (int64_t)kBitonicMax);
+  // K14w for k <= 32 (opt-in, SX_TOPK=warp): measured slower than the radix select on Q3's
+  // top-10 of 1.13e6 rows (0.40 / 0.37 vs 0.28 ms: the serial per-warp insertions and the rounds)
+  const bool topk_warp = outn <= 32 && outn < n && topk_env && std::strcmp(topk_env, "warp") == 0;
   const int32_t* warp_pos = nullptr;
   int64_t warp_m = 0;
   if (topk_warp) {
