@@ -1148,7 +1148,7 @@ struct Q3Fused {
 };
 
 constexpr int kQ3Buf = 96, kQ3Flush = 64;  // a chunk closes <= 8 * 32 groups... flushed per group (see emit)
-__global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n, int64_t per) {
+__global__ void __launch_bounds__(kBlock, 4) k_q3_fused(const __grid_constant__ Q3Fused a, int64_t n, int64_t per) {
   constexpr int R = 8;
   __shared__ int32_t s_key[kBlock / 32][kQ3Buf];
   __shared__ long long s_val[kBlock / 32][kQ3Buf];
@@ -1199,10 +1199,24 @@ __global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ 
   const int32_t kprev = has_prev ? __ldg(a.okey + R0 - 1) : 0;  // rows of this group: the previous warp's
   int32_t lastk = kprev;  // last key seen (sortedness check across chunks)
   // (prefetching the next chunk into registers measured slower: 2.05 vs 1.87 ms at 3 CTAs/SM)
-  // one chunk (32 lanes x R rows) of the range, its keys and dates already loaded
-  auto chunk = [&](int64_t base, const int32_t (&k)[R], const int32_t (&sd)[R]) {
+  for (int64_t base = R0; base < R1; base += 32 * R) {
     const int64_t r0 = base + (int64_t)lane * R;
     const int m = (int)max((int64_t)0, min((int64_t)R, R1 - r0));
+    int32_t k[R], sd[R];
+    if (m == R) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int4 x = __ldcs((const int4*)(a.okey + r0) + j), y = __ldcs((const int4*)(a.ship + r0) + j);
+        k[4 * j] = x.x; k[4 * j + 1] = x.y; k[4 * j + 2] = x.z; k[4 * j + 3] = x.w;
+        sd[4 * j] = y.x; sd[4 * j + 1] = y.y; sd[4 * j + 2] = y.z; sd[4 * j + 3] = y.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        k[i] = i < m ? __ldg(a.okey + r0 + i) : INT32_MAX;
+        sd[i] = i < m ? __ldg(a.ship + r0 + i) : INT32_MIN;
+      }
+    }
     // keys non-decreasing across the chunk (lane order) and from the previous chunk
     {
       int32_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
@@ -1242,7 +1256,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ 
       }
     }
     unsigned lanes = __ballot_sync(kFull, qmask != 0);
-    if (!lanes) return;
+    if (!lanes) continue;
     long long t[R];
 #pragma unroll
     for (int i = 0; i < R; ++i)
@@ -1259,33 +1273,6 @@ __global__ void __launch_bounds__(kBlock, 3) k_q3_fused(const __grid_constant__ 
         if ((qm >> i) & 1u) add(key, term);
       }
     }
-    };
-  auto load = [&](int64_t base, int32_t (&k)[R], int32_t (&sd)[R]) {
-    const int64_t r0 = base + (int64_t)lane * R;
-    const int m = (int)max((int64_t)0, min((int64_t)R, R1 - r0));
-    if (m == R) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int4 x = __ldcs((const int4*)(a.okey + r0) + j), y = __ldcs((const int4*)(a.ship + r0) + j);
-        k[4 * j] = x.x; k[4 * j + 1] = x.y; k[4 * j + 2] = x.z; k[4 * j + 3] = x.w;
-        sd[4 * j] = y.x; sd[4 * j + 1] = y.y; sd[4 * j + 2] = y.z; sd[4 * j + 3] = y.w;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        k[i] = i < m ? __ldg(a.okey + r0 + i) : INT32_MAX;
-        sd[i] = i < m ? __ldg(a.ship + r0 + i) : INT32_MIN;
-      }
-    }
-  };
-  // two chunks' loads in flight per iteration (4 KB per warp round trip; one chunk: 2.8 TB/s)
-  for (int64_t base = R0; base < R1; base += 2 * 32 * R) {
-    int32_t ka[R], sa[R], kb[R], sb[R];
-    load(base, ka, sa);
-    const bool two = base + 32 * R < R1;
-    if (two) load(base + 32 * R, kb, sb);
-    chunk(base, ka, sa);
-    if (two) chunk(base + 32 * R, kb, sb);
   }
   // the range's last group continues past R1 (its owner is this warp)
   if (R1 < n) {
@@ -1724,7 +1711,7 @@ SX_EXPORT sx_status sx_tpch_q3(sx_ctx* ctx, const sx_tpch_tables* t, const sx_tp
       SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
       SX_CUDA(cudaMemsetAsync(a.flags, 0, 2 * sizeof(int), ctx->stream));
       // one warp per contiguous range of whole 256-row chunks, every warp of a persistent grid
-      const unsigned grid = persistent_grid(ctx, 3, ((n + 255) / 256 + (kBlock / 32) - 1) / (kBlock / 32));
+      const unsigned grid = persistent_grid(ctx, 4, ((n + 255) / 256 + (kBlock / 32) - 1) / (kBlock / 32));
       const int64_t warps = (int64_t)grid * (kBlock / 32);
       const int64_t per = ((n + warps - 1) / warps + 255) / 256 * 256;
       k_q3_fused<<<grid, kBlock, 0, SX_STREAM(ctx)>>>(a, n, per);
