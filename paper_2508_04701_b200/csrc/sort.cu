@@ -506,8 +506,8 @@ __global__ void __launch_bounds__(kLsdThreads, ITEMS * NW > 40 ? 2 : 3) k_oneswe
                                                           unsigned long long* status, unsigned* ticket, unsigned pass,
                                                           int pos_only) {
   constexpr int T = kLsdThreads * ITEMS;
-  extern __shared__ uint32_t stage[];  // [T] staged words, then [T] destination indices
-  uint32_t* sdst = stage + T;
+  extern __shared__ uint32_t stage[];  // [T + 1] staged words (T: dump slot), then [T] destinations
+  uint32_t* sdst = stage + T + 1;
   __shared__ int wcnt[kLsdWarps][256];
   __shared__ int hcnt[256];
   __shared__ int dstart[256];
@@ -619,9 +619,12 @@ __global__ void __launch_bounds__(kLsdThreads, ITEMS * NW > 40 ? 2 : 3) k_oneswe
     dr[i] = (d << 16) | ((dr[i] & 0xffff) + dstart[d] + wcnt[w][d]);
   }
   const int tcount = (int)min((int64_t)T, n - base);
-  // destination index of every sorted position, once (n <= INT32_MAX: 32 bits)
+  // destination index of every sorted position, once (n <= INT32_MAX: 32 bits); sp[i]: the item's
+  // shared slot, or the dump slot T past the end (no predicate in the per-word staging below)
+  int sp[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
+    sp[i] = dr[i] >= 0 ? (dr[i] & 0xffff) : T;
     if (dr[i] < 0) continue;
     const int d = dr[i] >> 16, p = dr[i] & 0xffff;
     sdst[p] = (uint32_t)(s_off[d] + (p - dstart[d]));
@@ -631,11 +634,15 @@ __global__ void __launch_bounds__(kLsdThreads, ITEMS * NW > 40 ? 2 : 3) k_oneswe
     if (pos_only && j != NW - 1) return;
     __syncthreads();  // (first word: sdst complete; later words: the previous word's reads done)
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i)
-      if (dr[i] >= 0) stage[dr[i] & 0xffff] = val[j][i];
+    for (int i = 0; i < ITEMS; ++i) stage[sp[i]] = val[j][i];
     __syncthreads();
     uint32_t* out = dst.w[j];
-    for (int p = threadIdx.x; p < tcount; p += kLsdThreads) __stcs(out + sdst[p], stage[p]);
+    if (tcount == T) {
+#pragma unroll 4
+      for (int p = threadIdx.x; p < T; p += kLsdThreads) __stcs(out + sdst[p], stage[p]);
+    } else {
+      for (int p = threadIdx.x; p < tcount; p += kLsdThreads) __stcs(out + sdst[p], stage[p]);
+    }
   });
 }
 
@@ -677,7 +684,7 @@ sx_status onesweep_sort(sx_ctx* ctx, Scratch& scr, Words*& a, Words*& b, int nwo
   SX_CHECK_LAUNCH();
   k_os_scan<<<np, 256, 0, SX_STREAM(ctx)>>>(hist);
   SX_CHECK_LAUNCH();
-  const size_t smem = (size_t)2 * T * sizeof(uint32_t);
+  const size_t smem = (size_t)(2 * T + 1) * sizeof(uint32_t);
   SX_CUDA(cudaFuncSetAttribute(k_onesweep<ITEMS, NW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SX_CUDA(cudaFuncSetAttribute(k_onesweep<ITEMS, NW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int q = 0; q < np; ++q) {
