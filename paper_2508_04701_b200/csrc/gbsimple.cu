@@ -381,17 +381,27 @@ __global__ void k_gbs_emit(const __grid_constant__ GsSpec s, const __grid_consta
 // partition's rows [off[p], off[p+1]) of the partitioned key/value columns, then its groups are
 // appended to the output (one atomic per CTA).
 template <class SIG>
+// R replicas of an S-slot table per CTA (warp w uses replica w % R): with few groups per partition
+// (e.g. 64 for G = 2^16 over 1024 partitions) one table put 512 threads on the same few shared
+// words (ncu: 38% barrier/serialisation stalls).  The replicas are merged into replica 0 (shared
+// atomics) before its groups are written.
 __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__ GsSpec s, const int64_t* __restrict__ off,
-                                                         int P, const __grid_constant__ GsGlobal g) {
+                                                         int P, uint32_t S, int R, const __grid_constant__ GsGlobal g) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_cnt;
   __shared__ unsigned long long s_base;
-  STab t;
-  t.S = kGsPartSlots;
-  t.keys = (long long*)smem;
-  t.st = (unsigned long long*)(t.keys + (t.S + 1));
+  const size_t tab_bytes = (size_t)(S + 1) * 8 * (1 + s.nst);
+  auto rep = [&](int r) {
+    STab x;
+    x.S = S;
+    x.keys = (long long*)(smem + (size_t)r * tab_bytes);
+    x.st = (unsigned long long*)(x.keys + (S + 1));
+    return x;
+  };
+  STab t = rep((threadIdx.x >> 5) % R);
+  const STab t0 = rep(0);
   for (int p = blockIdx.x; p < P; p += gridDim.x) {
-    stab_init(t, s, threadIdx.x, blockDim.x);
+    for (int r = 0; r < R; ++r) stab_init(rep(r), s, threadIdx.x, blockDim.x);
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     const int64_t lo = off[p], hi = off[p + 1];
@@ -426,9 +436,33 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
         stab_update_t<SIG>(t, s, slot, v[u]);
       }
     }
+    __syncthreads();
+    // replicas 1.. into replica 0
+    for (uint32_t e = threadIdx.x; e < (uint32_t)(R - 1) * (S + 1); e += blockDim.x) {
+      const STab x = rep(1 + (int)(e / (S + 1)));
+      const uint32_t i = e % (S + 1);
+      const bool used = i < S ? x.keys[i] != kEmptyKey : (unsigned)*x.state(s.count_state, i) != 0;
+      if (!used) continue;
+      const uint32_t d = i < S ? stab_slot(t0, x.keys[i]) : S;
+      if (d > S) {
+        full = true;
+        continue;
+      }
+      for (int a = 0; a < s.nst; ++a) {
+        const unsigned long long wv = *x.state(a, i);
+        unsigned long long* dp = t0.state(a, d);
+        switch (s.kind[a]) {
+          case ST_SUM: sh_sum(dp, (long long)stab_value(ST_SUM, wv)); break;
+          case ST_COUNT: atomicAdd((unsigned*)dp, (unsigned)wv); break;
+          case ST_MIN: sh_min(dp, (long long)wv); break;
+          default: sh_max(dp, (long long)wv); break;
+        }
+      }
+    }
     if (full) atomicExch(s.flags, 1);
     __syncthreads();
     // count used slots, claim an output run, write the groups
+    t = t0;
     for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) {
       const bool used = i < t.S ? t.keys[i] != kEmptyKey : (unsigned)*t.state(s.count_state, i) != 0;
       if (used) atomicAdd(&s_cnt, 1);
@@ -451,6 +485,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
       put_out_key(s, pos, i < t.S ? t.keys[i] : kEmptyKey);
       put_out_aggs(s, pos, lo, hi);
     }
+    t = rep((threadIdx.x >> 5) % R);
     __syncthreads();
   }
   (void)g;
@@ -691,14 +726,20 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
     GsGlobal g{};
     if (part) {
       const int P = Pn;
-      const size_t smem = (size_t)(kGsPartSlots + 1) * 8 * (1 + s.nst);
+      // per-partition table: 2 x the expected groups (>= 64 slots, <= kGsPartSlots), replicated
+      // up to 16 ways within ~200 KB
+      uint32_t Sp = 64;
+      while (Sp < (uint32_t)kGsPartSlots && Sp < (uint32_t)(2 * (groups_hint / P + 1))) Sp <<= 1;
+      const size_t tabp = (size_t)(Sp + 1) * 8 * (1 + s.nst);
+      const int Rp = (int)std::max<size_t>(1, std::min<size_t>(16, (200u << 10) / tabp));
+      const size_t smem = tabp * Rp;
       SX_TRY(with_sig(sig, [&](auto sg) -> sx_status {
         using SIG = decltype(sg);
         SX_CUDA(cudaFuncSetAttribute(k_gbs_part<SIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
         SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbs_part<SIG>, kGsThreads, smem));
         const unsigned grid = (unsigned)std::min<int64_t>(P, (int64_t)ctx->num_sms * std::max(1, per_sm));
-        k_gbs_part<SIG><<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, d_off, P, g);
+        k_gbs_part<SIG><<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, d_off, P, Sp, Rp, g);
         SX_CHECK_LAUNCH();
         return SX_OK;
       }));
