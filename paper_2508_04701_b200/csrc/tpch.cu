@@ -852,7 +852,7 @@ struct Q9FusedProg {
   // issued together: five column gathers, then the supplier and orders direct arrays (bitmap word
   // and value read speculatively, both inside the key range) and the partsupp table's first slot.
   static constexpr int kWChunks = 2;
-  static constexpr int kWRows = 3;  // (2: 4.25 ms for Q9 at SF100)
+  static constexpr int kWRows = 2;  // (3 rows per lane: 4.58 vs 4.25 ms for Q9 at SF100)
   // K10wr interface (gb_host.cuh): the six lineitem columns through the tile ring
   static constexpr bool kWRing = true;
   using KeyT = KT;
