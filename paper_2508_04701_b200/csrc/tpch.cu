@@ -717,19 +717,31 @@ __global__ void k_date_fill_sorted(const KT* __restrict__ keys, const int32_t* _
     const uint4 sent = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
     for (long long u = a / 8 + lane; u < b / 8; u += 32) __stcs((uint4*)val + u, sent);
     __syncwarp();
-    // 2. the dates at the keys (and the order check)
+    // 2. the dates at the keys (and the order check); every key and date load of the chunk is
+    //    issued together, the previous key comes from the neighbouring lane
+    long long kk[K];
+    int32_t dd[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int64_t o = o0 + k * 32 + lane;
+      kk[k] = o < o1 ? (long long)__ldg(keys + o) : LLONG_MAX;
+      dd[k] = o < o1 ? __ldg(dates + o) : 0;
+    }
+    const long long before = o0 > 0 ? (long long)__ldg(keys + o0 - 1) : mn - 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t o = o0 + k * 32 + lane;
+      long long prev = __shfl_up_sync(kFull, kk[k], 1);
+      const long long last_prev = __shfl_sync(kFull, k > 0 ? kk[k > 0 ? k - 1 : 0] : before, 31);
+      if (lane == 0) prev = k == 0 ? before : last_prev;
       if (o >= o1) continue;
-      const long long key = (long long)__ldg(keys + o);
-      const long long prev = o > 0 ? (long long)__ldg(keys + o - 1) : mn - 1;
+      const long long key = kk[k];
       const long long off = key - mn;
       if (key <= prev || off < p0 || off >= p1) {
         unsorted = true;
         continue;
       }
-      const int32_t x = __ldg(dates + o);
+      const int32_t x = dd[k];
       wide |= (int32_t)(int16_t)x != x || (int16_t)x == kNoDate;
       val[off] = (int16_t)x;
     }
