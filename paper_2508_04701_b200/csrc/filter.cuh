@@ -279,34 +279,59 @@ struct ContainsFn {
     const int nr = (int)(wr1 - wr0);
     for (int k = lane; k <= nr; k += 32) wo[k] = (int32_t)(__ldg(offsets + wr0 + k) - S);
     __syncwarp();
-    const uint32_t p4 = 0x01010101u * pat[0];
-    // 16-byte aligned chunks of absolute addresses covering [S, E): a chunk that holds a byte of
-    // the span lies inside the chars allocation's mapped granularity
+    // Candidates are 4-byte windows equal to the pattern's first min(plen, 4) bytes: each lane
+    // forms the 16 windows that start in its 16 bytes (funnel shifts over its 4 words plus the
+    // next lane's first word), so only true prefix matches reach the byte-wise verification.
+    uint32_t p4 = 0, pm = 0;
+    for (int k = 0; k < 4 && k < plen; ++k) {
+      p4 |= (uint32_t)pat[k] << (8 * k);
+      pm |= 0xFFu << (8 * k);
+    }
     const uintptr_t a0 = ((uintptr_t)(chars + S)) & ~(uintptr_t)15;
     const uintptr_t aE = (uintptr_t)(chars + E);
-    for (uintptr_t cb = a0; cb < aE; cb += 1024) {  // warp-uniform; two 512-byte steps per trip
-      uint4 v[2];
-      uint32_t cm[2];
+    constexpr int kSteps = 4;  // 512-byte warp steps per trip (16 B in flight per lane and step)
+    for (uintptr_t cb = a0; cb < aE; cb += 512 * kSteps) {  // warp-uniform
+      uint4 v[kSteps];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kSteps; ++h) {
         const uintptr_t p = cb + 512 * h + 16 * lane;
         v[h] = p < aE ? __ldg((const uint4*)p) : make_uint4(0u, 0u, 0u, 0u);
-        cm[h] = p < aE ? ((__vcmpeq4(v[h].x, p4) & 0x01010101u) | ((__vcmpeq4(v[h].y, p4) & 0x01010101u) << 1) |
-                          ((__vcmpeq4(v[h].z, p4) & 0x01010101u) << 2) | ((__vcmpeq4(v[h].w, p4) & 0x01010101u) << 3))
-                       : 0u;
+      }
+      uint32_t cm[kSteps];
+#pragma unroll
+      for (int h = 0; h < kSteps; ++h) {
+        // bytes 16..19 after this lane's chunk: the next lane's first word (lane 31: the next
+        // step's lane 0, or a load past the trip)
+        uint32_t nx = __shfl_down_sync(0xffffffffu, v[h].x, 1);
+        const uint32_t n0 = __shfl_sync(0xffffffffu, h + 1 < kSteps ? v[h + 1 < kSteps ? h + 1 : h].x : 0u, 0);
+        if (lane == 31) {
+          if (h + 1 < kSteps) {
+            nx = n0;
+          } else {
+            const uintptr_t p = cb + 512 * kSteps;
+            nx = p < aE ? __ldg((const uint32_t*)p) : 0u;
+          }
+        }
+        const uint32_t w[5] = {v[h].x, v[h].y, v[h].z, v[h].w, nx};
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          c |= (((w[i] & pm) == p4) ? 1u : 0u) << (4 * i);
+#pragma unroll
+          for (int o = 1; o < 4; ++o) c |= (((__funnelshift_r(w[i], w[i + 1], 8 * o) & pm) == p4) ? 1u : 0u) << (4 * i + o);
+        }
+        cm[h] = c;
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kSteps; ++h) {
         uint32_t c = cm[h];
         while (c) {
-          // bit 8b + 4... encodes byte 4*word + b: bit (8*b + word) for word w, byte b
-          const int bit = __ffs(c) - 1;
+          const int j = __ffs(c) - 1;
           c &= c - 1;
-          const int j = 4 * (bit & 3) + (bit >> 3);
           const int64_t q = (int64_t)((const uint8_t*)(cb + 512 * h + 16 * lane) - chars) + j;
           if (q < S || q + plen > E) continue;
           bool ok = true;
-          for (int k = 1; k < plen && ok; ++k) ok = __ldg(chars + q + k) == pat[k];
+          for (int k = 4; k < plen && ok; ++k) ok = __ldg(chars + q + k) == pat[k];
           if (!ok) continue;
           const int32_t qr = (int32_t)(q - S);
           int lo = 0, hi = nr - 1;  // last row whose string starts at or before q

@@ -524,7 +524,7 @@ def test_filter_contains_edges(ctx, maxlen):
     offs = np.zeros(n + 1, np.int64)
     offs[1:] = np.cumsum([len(x) for x in strs])
     chars = np.frombuffer(b"".join(strs), np.uint8).copy()
-    for pat in (b"green", b"gre", b"", b"q", LONG):
+    for pat in (b"green", b"gre", b"gr", b"gree", b"", b"q", LONG):
         sel, _ = ctx.filter([sx.col(dev(chars), A.SX_STR, offsets=dev(offs))], [(0, "contains", pat)])
         assert np.array_equal(sel.cpu().numpy(), oracle.contains(offs, chars, pat)), pat
     # a chars buffer that does not start on a 16-byte boundary
@@ -533,6 +533,20 @@ def test_filter_contains_edges(ctx, maxlen):
     for pat in (b"green", LONG):
         sel, _ = ctx.filter([sx.col(pad[3:], A.SX_STR, offsets=dev(offs))], [(0, "contains", pat)])
         assert np.array_equal(sel.cpu().numpy(), oracle.contains(offs, chars, pat)), pat
+
+
+@pytest.mark.parametrize("pat", [b"a", b"ab", b"aba", b"abab", b"aabab", b"babbaabab"])
+def test_filter_contains_dense_alphabet(ctx, pat):
+    """Two-letter alphabet: overlapping occurrences, candidates in every 4-byte window, matches that
+    straddle lane (16-byte) and warp-step (512-byte) boundaries, patterns of 1..9 bytes."""
+    rng = np.random.default_rng(len(pat))
+    n = 20_011
+    lens = rng.integers(0, 24, n)
+    offs = np.zeros(n + 1, np.int64)
+    offs[1:] = np.cumsum(lens)
+    chars = rng.choice(np.frombuffer(b"ab", np.uint8), int(offs[-1]), p=[0.6, 0.4]).astype(np.uint8)
+    sel, _ = ctx.filter([sx.col(dev(chars), A.SX_STR, offsets=dev(offs))], [(0, "contains", pat)])
+    assert np.array_equal(sel.cpu().numpy(), oracle.contains(offs, chars, pat))
 
 
 def test_misaligned_and_strided_columns_rejected(ctx):
