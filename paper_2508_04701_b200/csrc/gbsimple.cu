@@ -23,6 +23,7 @@
 // path.  Output group order is unspecified (R13).
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "gb_host.cuh"
@@ -535,6 +536,262 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_subpart(const __grid_constan
   }
 }
 
+// ---- K19: atomic-free warp-private aggregation ---------------------------------------------
+// ncu on K18s at G = 4 (r2r_gb4): 24 ms for 2^30 rows, 755 GB/s — a shared atomic whose old
+// value is used costs ~2 cycles per lane (B300_MICROARCH "ATOMS spread-addr"), and K18's SUM
+// needs the old word for its carry.  K19t updates shared state with plain loads and stores only:
+// every warp owns a dictionary key -> dense id (<= kGtD ids) and LANE-PRIVATE cells [id][lane]
+// for count / sum / min / max, so no two lanes (and no two warps) ever write the same word.  The
+// common row costs one dictionary read (home slot or the next), and four conflict-free
+// read-modify-writes of its lane's cells; a batch whose rows all qualify takes that fast path,
+// any other batch (a key's first rows, a displaced key, a wide value, the key kEmptyKey, groups
+// beyond kGtD) the general per-row path, where rows without a cell take g_row's exact global
+// atomics.  Above kGtD hinted groups the input is first radix-partitioned (K7) to ~8 groups per
+// partition, so a warp's chunk of one partition fits its cells.  A warp aggregates one chunk of
+// rows (never spanning two partitions), reduces each id's cells over its lanes and merges the
+// group into the global table (one atomic per group and state, K18s's merge table), which
+// k_gbs_emit turns into the output.  Exactness as K18 (R2/R3): a chunk has <= 2^21 rows and only
+// values with |v| < 2^40 are summed in the 64-bit cells.
+constexpr int kGwThreads = 256;
+constexpr int kGwWarps = kGwThreads / 32;
+constexpr int kGwU = 8;       // rows per lane per batch (their loads issued together)
+constexpr int kGtD = 16;      // K19t: ids per warp
+constexpr int kGtSlots = 256;  // K19t: dictionary slots per warp (load <= 1/16: keys stay home)
+
+// multiplicative slot hash (top bits; independent of hash64's partition bits 48..57)
+__device__ __forceinline__ uint32_t gw_hash(long long k) {
+  const uint64_t x = (uint64_t)k;
+  return (uint32_t)x * 0x9E3779B1u + (uint32_t)(x >> 32) * 0x85EBCA77u + ((uint32_t)(x >> 32) >> 15);
+}
+
+// Read-only probe of a warp table (S slots, power of two; slot S = the side slot of kEmptyKey,
+// present when has_side).  slot >= 0: found; miss: the key is absent (insert it); neither: the
+// table is full (S probes).
+__device__ __forceinline__ int gw_probe(const long long* keys, uint32_t S, int shift, long long k, bool act, bool has_side,
+                                        bool& miss) {
+  int slot = -1;
+  miss = false;
+  bool pend = act && k != kEmptyKey;
+  if (act && k == kEmptyKey) {
+    if (has_side) slot = (int)S;
+    else miss = true;
+  }
+  uint32_t h = gw_hash(k) >> shift, probes = 0;
+  while (__any_sync(kFull, pend)) {
+    if (pend) {
+      const long long cur = keys[h];
+      if (cur == k) {
+        slot = (int)h;
+        pend = false;
+      } else if (cur == kEmptyKey) {
+        miss = true;
+        pend = false;
+      } else {
+        h = (h + 1) & (S - 1);
+        if (++probes >= S) pend = false;
+      }
+    }
+  }
+  return slot;
+}
+
+// Insert path (lanes with ins; warp-synchronous): returns the slot, -1 when the table is full.
+__device__ __forceinline__ int gw_insert(long long* keys, uint32_t S, int shift, long long k, bool ins) {
+  int slot = -1;
+  bool pend = ins && k != kEmptyKey;
+  if (ins && k == kEmptyKey) slot = (int)S;
+  uint32_t h = gw_hash(k) >> shift, probes = 0;
+  while (__any_sync(kFull, pend)) {
+    const long long cur = pend ? keys[h] : 0;
+    __syncwarp();
+    const bool wrote = pend && cur == kEmptyKey;
+    if (wrote) keys[h] = k;
+    __syncwarp();
+    if (pend) {
+      const long long now = wrote ? keys[h] : cur;
+      if (now == k) {
+        slot = (int)h;
+        pend = false;
+      } else {
+        h = (h + 1) & (S - 1);
+        if (++probes >= S) pend = false;
+      }
+    }
+  }
+  __syncwarp();
+  return slot;
+}
+
+struct GwChunks {
+  const int64_t* lo;  // [nchunks] first row
+  const int64_t* hi;  // [nchunks] end row
+  int nchunks;
+};
+
+template <int KB, int VB>
+__device__ __forceinline__ void gw_load(const GsSpec& s, int64_t b, int64_t hi, int lane, long long (&k)[kGwU],
+                                        long long (&v)[kGwU], bool (&in)[kGwU]) {
+#pragma unroll
+  for (int u = 0; u < kGwU; ++u) {
+    const int64_t r = b + (int64_t)u * 32 + lane;
+    in[u] = r < hi;
+    if constexpr (KB == 8) k[u] = in[u] ? __ldcs((const long long*)s.key + r) : 0;
+    else k[u] = in[u] ? (long long)__ldcs((const int32_t*)s.key + r) : 0;
+    if constexpr (VB == 8) v[u] = in[u] ? __ldcs((const long long*)s.val[0] + r) : 0;
+    else v[u] = in[u] ? (long long)__ldcs((const int32_t*)s.val[0] + r) : 0;
+  }
+}
+
+template <class SIG>
+__device__ __forceinline__ void gw_merge_group(const GsGlobal& g, const GsSpec& s, long long key, unsigned long long cnt,
+                                               long long sum, long long mn, long long mx) {
+  const uint64_t gs = g_slot(g, key, s.flags);
+  g_add(g, s, gs, 0, cnt, true);
+  if constexpr (SIG::kHasSum) g_add(g, s, gs, SIG::kSum, (unsigned long long)sum, true);
+  if constexpr (SIG::kHasMin) g_add(g, s, gs, SIG::kMin, (unsigned long long)mn, true);
+  if constexpr (SIG::kHasMax) g_add(g, s, gs, SIG::kMax, (unsigned long long)mx, true);
+}
+
+// K19t.  Per warp: dictionary keys[kGtSlots + 1] / ids (int8: -1 none, kGtD overflow), id ->
+// key, lane-private cells cnt[kGtD][32] u32 and sum / min / max [kGtD][32] i64.
+struct GtWarp {
+  long long keys[kGtSlots + 2];
+  long long idkey[kGtD];
+  long long sum[kGtD + 1][32];  // (row kGtD: the sink of the fast path's inactive rows)
+  long long mn[kGtD + 1][32];
+  long long mx[kGtD + 1][32];
+  unsigned cnt[kGtD + 1][32];
+  signed char id[kGtSlots + 2];
+};
+constexpr int kGtShift = 32 - 8;  // log2(kGtSlots)
+
+template <class SIG>
+__device__ __forceinline__ void gt_cell(GtWarp& W, int id, int lane, long long v) {
+  W.cnt[id][lane] += 1u;
+  if constexpr (SIG::kHasSum) W.sum[id][lane] += v;
+  if constexpr (SIG::kHasMin) W.mn[id][lane] = min(W.mn[id][lane], v);
+  if constexpr (SIG::kHasMax) W.mx[id][lane] = max(W.mx[id][lane], v);
+}
+
+// The general per-row path (a key's first rows, displaced keys, wide values, the key
+// kEmptyKey, more than kGtD groups in the chunk: those rows take g_row's global atomics).
+template <class SIG>
+__device__ __noinline__ void gt_slow_batch(GtWarp& W, const GsSpec& s, const GsGlobal& g, int lane, int& nid,
+                                           bool& side, const long long (&k)[kGwU], const long long (&v)[kGwU],
+                                           const bool (&in)[kGwU]) {
+#pragma unroll 1
+  for (int u = 0; u < kGwU; ++u) {
+    const long long ku = k[u], vu = v[u];
+    bool act = in[u];
+    bool wide = act && !small_v(vu);
+    act = act && !wide;
+    bool miss;
+    int slot = gw_probe(W.keys, kGtSlots, kGtShift, ku, act, side, miss);
+    if (__any_sync(kFull, miss)) {  // first rows of new keys: insert, one id per new slot
+      const int ns = gw_insert(W.keys, kGtSlots, kGtShift, ku, miss);
+      if (miss) slot = ns;
+      const bool need = miss && ns >= 0 && W.id[ns] < 0;
+      const unsigned nm = __ballot_sync(kFull, need);
+      bool lead = false;
+      if (need) lead = (__ffs(__match_any_sync(nm, ns)) - 1) == lane;
+      const unsigned lm = __ballot_sync(kFull, lead);
+      if (lead) {
+        const int nidx = nid + __popc(lm & lanemask_lt());
+        W.id[ns] = (signed char)(nidx < kGtD ? nidx : kGtD);
+        if (nidx < kGtD) W.idkey[nidx] = ku;
+      }
+      nid += __popc(lm);
+      side = side || __any_sync(kFull, miss && ku == kEmptyKey);
+      __syncwarp();
+    }
+    const int id = slot >= 0 ? W.id[slot] : -1;
+    if (act && (id < 0 || id >= kGtD)) wide = true;  // no cell: the exact global path
+    if (wide) {
+      long long vv[kGsMaxVals] = {vu, 0, 0, 0};
+      g_row(g, s, ku, vv);
+    } else if (act) {
+      gt_cell<SIG>(W, id, lane, vu);
+    }
+    __syncwarp();
+  }
+}
+
+template <class SIG, int KB, int VB>
+__global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSpec s, const __grid_constant__ GwChunks ch,
+                                                    const __grid_constant__ GsGlobal g) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  GtWarp& W = ((GtWarp*)smem)[threadIdx.x >> 5];
+  const int gw = blockIdx.x * kGwWarps + (threadIdx.x >> 5), nw = gridDim.x * kGwWarps;
+  for (int c = gw; c < ch.nchunks; c += nw) {
+    for (int i = lane; i < kGtSlots + 2; i += 32) {
+      W.keys[i] = kEmptyKey;  // (slot kGtSlots + 1: a never-used pad, probed as "home + 1")
+      W.id[i] = -1;
+    }
+#pragma unroll
+    for (int d = 0; d <= kGtD; ++d) {
+      W.cnt[d][lane] = 0;
+      W.sum[d][lane] = 0;
+      W.mn[d][lane] = LLONG_MAX;
+      W.mx[d][lane] = LLONG_MIN;
+    }
+    int nid = 0;
+    bool side = false;  // the key kEmptyKey has an id
+    __syncwarp();
+    const int64_t lo = ch.lo[c], hi = ch.hi[c];
+    long long k[kGwU], v[kGwU];
+    bool in[kGwU];
+    gw_load<KB, VB>(s, lo, hi, lane, k, v, in);
+    for (int64_t b = lo; b < hi; b += 32 * kGwU) {
+      long long kn[kGwU], vn[kGwU];
+      bool inn[kGwU];
+      gw_load<KB, VB>(s, b + 32 * kGwU, hi, lane, kn, vn, inn);
+      // fast path: every row's key at its home slot or the next, with an id, and a small value
+      // (branch-free: bitwise tests; a row past the chunk updates the sink row kGtD)
+      int id[kGwU];
+      int ok = 1;
+#pragma unroll
+      for (int u = 0; u < kGwU; ++u) {
+        const uint32_t h = gw_hash(k[u]) >> kGtShift;
+        const long long c0 = W.keys[h], c1 = W.keys[h + 1];
+        const int i0 = W.id[h], i1 = W.id[h + 1];
+        const int iu = c0 == k[u] ? i0 : c1 == k[u] ? i1 : -1;
+        const int good = ((unsigned)iu < (unsigned)kGtD) & (k[u] != kEmptyKey) & small_v(v[u]);
+        ok &= (!in[u]) | good;
+        id[u] = in[u] ? iu : kGtD;
+      }
+      if (__all_sync(kFull, ok)) {
+#pragma unroll
+        for (int u = 0; u < kGwU; ++u) gt_cell<SIG>(W, id[u], lane, v[u]);
+      } else {
+        gt_slow_batch<SIG>(W, s, g, lane, nid, side, k, v, in);
+      }
+#pragma unroll
+      for (int u = 0; u < kGwU; ++u) {
+        k[u] = kn[u];
+        v[u] = vn[u];
+        in[u] = inn[u];
+      }
+    }
+    __syncwarp();
+    // the warp's groups: each id's cells reduced over the lanes; lane d merges group d
+    const int nd = min(nid, kGtD);
+    for (int d = 0; d < nd; ++d) {
+      unsigned cn = W.cnt[d][lane];
+      long long sm = W.sum[d][lane], mn = W.mn[d][lane], mx = W.mx[d][lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        cn += __shfl_xor_sync(kFull, cn, o);
+        sm += __shfl_xor_sync(kFull, sm, o);
+        mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+        mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+      }
+      if (lane == d && cn) gw_merge_group<SIG>(g, s, W.idkey[d], cn, sm, mn, mx);
+    }
+    __syncwarp();
+  }
+}
+
 template <class F>
 sx_status with_sig(int sig, F&& f) {
   switch (sig) {
@@ -558,6 +815,119 @@ bool plain_col_expr(const sx_expr& e, int* col) {
   return true;
 }
 
+
+// K19 host side (see the kernels): SX_EUNSUPPORTED (nothing allocated) when the shape does not
+// fit (not the fixed signature, or more than kGtHintMax hinted groups) or the hinted global merge
+// table overflowed.
+constexpr int64_t kGtHintMax = 4096;  // 1024 partitions x ~4 groups
+sx_status gb_k19(sx_ctx* ctx, GsSpec s, int sig, const sx_col& kc, int vtype, int naggs, const sx_agg* aggs,
+                 int64_t groups_hint, int64_t n, sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups) {
+  if (sig < 0 || s.nv != 1 || groups_hint > kGtHintMax) return SX_EUNSUPPORTED;
+  Scratch scr(ctx);
+  // fan-out (above kGtD groups): ~4 expected groups per partition, so a warp's chunk of one
+  // partition practically never exceeds its kGtD cells (rows of groups beyond them would take
+  // global atomics: at ~8 per partition, the few partitions past 16 groups made one warp's chunk
+  // 7x slower than the rest, ncu r2u_gb4k)
+  int bits = 0;
+  while (bits < 10 && groups_hint > kGtD && ((int64_t)4 << bits) < groups_hint) ++bits;
+  const int P = 1 << bits;
+  std::vector<int64_t> offs{0, n};
+  if (P > 1) {
+    DCol kd{s.key, s.key_type, 0};
+    DCol carry[2] = {kd, DCol{s.val[0], vtype, 0}};
+    int width[2] = {s.key_bytes, s.vbytes[0]};
+    void* outp[2];
+    for (int c = 0; c < 2; ++c) SX_TRY(scr.get((char**)&outp[c], (size_t)n * width[c]));
+    offs.assign((size_t)P + 1, 0);
+    SX_TRY(radix_partition_carry(ctx, kd, kd, 1, carry, width, 2, nullptr, n, bits, outp, offs.data()));
+    s.key = outp[0];
+    s.val[0] = outp[1];
+  }
+  // chunks: ~4 per resident warp (partition tails even out), <= 2^21 rows (exact 64-bit warp
+  // sums), never across partitions
+  const int nwarps = ctx->num_sms * kGwWarps;
+  const int64_t L = std::min<int64_t>(1 << 21, std::max<int64_t>(32 * kGwU, (n + 4 * nwarps - 1) / (4 * nwarps)));
+  std::vector<int64_t> clo, chi;
+  for (int p = 0; p < (int)offs.size() - 1; ++p)
+    for (int64_t a = offs[p]; a < offs[p + 1]; a += L) {
+      clo.push_back(a);
+      chi.push_back(std::min(a + L, offs[p + 1]));
+    }
+  const int nch = (int)clo.size();
+  int64_t* d_ch;
+  SX_TRY(scr.get(&d_ch, (size_t)std::max(1, 2 * nch)));
+  if (nch) {
+    std::vector<int64_t> both(clo);
+    both.insert(both.end(), chi.begin(), chi.end());
+    SX_CUDA(cudaMemcpyAsync(d_ch, both.data(), sizeof(int64_t) * 2 * nch, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  GwChunks ch{d_ch, d_ch + nch, nch};
+  // global merge table (load <= 0.5 at the hint) and the outputs (every slot + the side slot)
+  GsGlobal g{};
+  uint64_t C = 64;
+  while (C < (uint64_t)(2 * groups_hint)) C <<= 1;
+  SX_TRY(scr.get(&g.keys, C + 1));
+  SX_TRY(scr.get(&g.used, C + 1));
+  for (int a = 0; a < s.nst; ++a) {
+    SX_TRY(scr.get(&g.st[a], C + 1));
+    g.hi[a] = nullptr;
+    if (s.kind[a] == ST_SUM) SX_TRY(scr.get(&g.hi[a], C + 1));
+  }
+  g.mask = C - 1;
+  const int64_t cap = (int64_t)std::min<uint64_t>((uint64_t)n, C + 1);
+  void* okey;
+  void* oagg[SX_MAX_AGGS];
+  SX_TRY(scr.get((char**)&okey, (size_t)std::max<int64_t>(cap, 1) * s.key_bytes));
+  for (int j = 0; j < naggs; ++j)
+    SX_TRY(scr.get((char**)&oagg[j], (size_t)std::max<int64_t>(cap, 1) * type_width(agg_out_type(aggs[j].op))));
+  s.out_key = okey;
+  for (int j = 0; j < naggs; ++j) s.out_agg[j] = oagg[j];
+  s.out_cap = cap;
+  unsigned long long* cursor = (unsigned long long*)ctx->d_counters;
+  s.out_cursor = cursor;
+  s.flags = ctx->d_flags;
+  SX_CUDA(cudaMemsetAsync(cursor, 0, 8, ctx->stream));
+  SX_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(int), ctx->stream));
+  k_gbs_init<<<persistent_grid(ctx, 4, (C + kBlock) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(s, g);
+  SX_CHECK_LAUNCH();
+  SX_TRY(with_sig(sig, [&](auto sg) -> sx_status {
+    using SIG = decltype(sg);
+    if constexpr (!SIG::kFixed) {
+      return SX_EUNSUPPORTED;
+    } else {
+      auto go = [&](auto kbc, auto vbc) -> sx_status {
+        constexpr int KB = decltype(kbc)::value, VB = decltype(vbc)::value;
+        const size_t smem = sizeof(GtWarp) * kGwWarps;
+        SX_CUDA(cudaFuncSetAttribute(k_gbt<SIG, KB, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 1;
+        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbt<SIG, KB, VB>, kGwThreads, smem));
+        const unsigned grid = (unsigned)std::max(1, std::min(nch, ctx->num_sms * std::max(1, per_sm)));
+        k_gbt<SIG, KB, VB><<<grid, kGwThreads, smem, SX_STREAM(ctx)>>>(s, ch, g);
+        SX_CHECK_LAUNCH();
+        return SX_OK;
+      };
+      using I4 = std::integral_constant<int, 4>;
+      using I8 = std::integral_constant<int, 8>;
+      if (s.key_bytes == 8) return s.vbytes[0] == 8 ? go(I8{}, I8{}) : go(I8{}, I4{});
+      return s.vbytes[0] == 8 ? go(I4{}, I8{}) : go(I4{}, I4{});
+    }
+  }));
+  k_gbs_emit<<<persistent_grid(ctx, 4, (C + kBlock) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(s, g);
+  SX_CHECK_LAUNCH();
+  int64_t ng = 0;
+  SX_TRY(read_i64(ctx, cursor, &ng));
+  int fl = 0;
+  SX_CUDA(cudaMemcpy(&fl, s.flags, sizeof(int), cudaMemcpyDeviceToHost));
+  if (fl || ng > cap) return SX_EUNSUPPORTED;  // a warp table / the hinted global table overflowed
+  out_keys[0] = sx_col{kc.type, kc.scale, ng, okey, nullptr, nullptr};
+  scr.release(okey);
+  for (int j = 0; j < naggs; ++j) {
+    out_aggs[j] = sx_col{agg_out_type(aggs[j].op), 0, ng, oagg[j], nullptr, nullptr};
+    scr.release(oagg[j]);
+  }
+  *out_ngroups = ng;
+  return SX_OK;
+}
 }  // namespace
 
 namespace sx {
@@ -650,6 +1020,13 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
   for (int c = 0; c < s.nv; ++c)
     if ((uintptr_t)s.val[c] % 16) return SX_EUNSUPPORTED;
   if ((uintptr_t)s.key % 16) return SX_EUNSUPPORTED;
+  // K19 (atomic-free warp tables) for the fixed signature up to 2^18 hinted groups (SX_GB_K19=0: K18)
+  if (!(getenv("SX_GB_K19") && getenv("SX_GB_K19")[0] == '0')) {
+    const sx_status k19 = gb_k19(ctx, s, sig, kc, s.nv == 1 ? cols[vcol_of[0]].type : 0, naggs, aggs, groups_hint, n,
+                                 out_keys, out_aggs, out_ngroups);
+    if (k19 != SX_EUNSUPPORTED) return k19;
+    ctx->err.clear();
+  }
   Scratch scr(ctx);
   // outputs (capacity from the hint; rerun with the exact count if it was low)
   int64_t cap = std::min<int64_t>(n, 2 * groups_hint + 1024);

@@ -152,6 +152,41 @@ def test_groupby_plain_shape(ctx, G, hint, wide):
     assert g == len(want)
 
 
+FIXED_AGGS = [("sum", [(1, [(1, 1, 0)])]), ("count", []), ("min", [(1, [(1, 1, 0)])]), ("max", [(1, [(1, 1, 0)])]),
+              ("avg", [(1, [(1, 1, 0)])], 2)]
+
+
+@pytest.mark.parametrize("G,hint,wide,v32", [(4, 4, False, False), (13, 16, True, False), (40, 16, False, False),
+                                             (100, 128, False, True), (256, 256, True, False),
+                                             (1000, 1024, False, False), (5000, 5000, False, False),
+                                             (200_000, 200_000, False, False), (3000, 300, False, False),
+                                             (262_144, 262_144, False, True)])
+def test_groupby_fixed_signature(ctx, G, hint, wide, v32):
+    """K19 (one value column: count + sum/min/max/avg, >= 2^20 rows): lane-private cells
+    (hint <= 16), warp tables unpartitioned (hint <= 128) and behind a radix partition (up to
+    2^18 groups); under-hinted G (a warp dictionary / the merge table overflows: K18 or the
+    generic path takes over), the key INT64_MIN (side slot), values >= 2^40 (exact global path),
+    an int32 value column — against the oracle."""
+    rng = np.random.default_rng(G + hint)
+    n = (1 << 20) + 4_321
+    keys = np.unique(rng.integers(-(2**63), 2**63 - 1, G * 2, dtype=np.int64))[:G]
+    keys[0] = -(2**63)
+    k = keys[rng.integers(0, G, n)]
+    if v32:
+        v = rng.integers(-(2**31), 2**31 - 1, n).astype(np.int32)
+        vc = sx.col(dev(v), A.SX_I32)
+    else:
+        v = rng.integers(-(10**9), 10**9, n).astype(np.int64)
+        if wide:
+            v[rng.integers(0, n, 50)] = -(2**61)
+        vc = sx.col(dev(v), A.SX_DEC64, 2)
+    keys_o, aggs_o, g = ctx.groupby([sx.col(dev(k)), vc], [(0, "id")], FIXED_AGGS, groups_hint=hint)
+    got = canon(keys_o, aggs_o, [a[0] for a in FIXED_AGGS])
+    want = oracle.groupby([k, v], [0], FIXED_AGGS)
+    check_gb(got, want)
+    assert g == len(want)
+
+
 @pytest.mark.parametrize("hint", [4, 64])
 def test_groupby_two_u8_keys_where(ctx, hint):
     rng = np.random.default_rng(11)
