@@ -49,6 +49,27 @@ def test_radix_partition(ctx, n, bits, key_t):
         assert sx.lib().sx_radix_of(int(k) & (2**64 - 1), bits) == part[list(keys).index(k)]
 
 
+@pytest.mark.parametrize("n,bits,key_t", [(70_001, 3, np.int64), (1_000_003, 10, np.int64), (4_097, 9, np.int64),
+                                          (500_000, 7, np.int32)])
+def test_radix_partition_register_path(ctx, n, bits, key_t):
+    """No row ids: K7r (the register-resident scatter, shared-atomic ranks) — each partition holds
+    exactly its rows' (key, payload) pairs."""
+    rng = np.random.default_rng(n + bits)
+    keys = rng.integers(-2**40, 2**40, n, dtype=np.int64).astype(key_t)
+    pay = rng.integers(-2**62, 2**62, n, dtype=np.int64)
+    (pk, pp), _, offs = ctx.radix_partition([sx.col(dev(keys)), sx.col(dev(pay))], [0], bits, rows=False)
+    pk, pp = pk.cpu().numpy(), pp.cpu().numpy()
+    P = 1 << bits
+    part = ((np_fmix64(keys.astype(np.int64).view(np.uint64)) >> np.uint64(48)) & np.uint64(P - 1)).astype(np.int64)
+    assert offs[0] == 0 and offs[-1] == n
+    assert np.array_equal(np.diff(offs), np.bincount(part, minlength=P))
+    for p_ in range(P):
+        lo, hi = offs[p_], offs[p_ + 1]
+        got = sorted(zip(pk[lo:hi].tolist(), pp[lo:hi].tolist()))
+        want = sorted(zip(keys[part == p_].tolist(), pay[part == p_].tolist()))
+        assert got == want, p_
+
+
 def test_radix_partition_with_selection(ctx):
     n = 70_001
     keys = np.arange(n, dtype=np.int32) * 7
