@@ -822,7 +822,9 @@ bool plain_col_expr(const sx_expr& e, int* col) {
 constexpr int64_t kGtHintMax = 4096;  // 1024 partitions x ~4 groups
 sx_status gb_k19(sx_ctx* ctx, GsSpec s, int sig, const sx_col& kc, int vtype, int naggs, const sx_agg* aggs,
                  int64_t groups_hint, int64_t n, sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups) {
-  if (sig < 0 || s.nv != 1 || groups_hint > kGtHintMax) return SX_EUNSUPPORTED;
+  // (17..32 hinted groups: K18s's replicated shared tables measured faster, 12.1 vs 17.1 ms)
+  if (sig < 0 || s.nv != 1 || groups_hint > kGtHintMax || (groups_hint > kGtD && groups_hint <= 32))
+    return SX_EUNSUPPORTED;
   Scratch scr(ctx);
   // fan-out (above kGtD groups): ~4 expected groups per partition, so a warp's chunk of one
   // partition practically never exceeds its kGtD cells (rows of groups beyond them would take

@@ -160,13 +160,14 @@ FIXED_AGGS = [("sum", [(1, [(1, 1, 0)])]), ("count", []), ("min", [(1, [(1, 1, 0
                                              (100, 128, False, True), (256, 256, True, False),
                                              (1000, 1024, False, False), (5000, 5000, False, False),
                                              (200_000, 200_000, False, False), (3000, 300, False, False),
-                                             (262_144, 262_144, False, True)])
+                                             (262_144, 262_144, False, True), (6000, 6000, True, False),
+                                             (100_000, 8192, False, False), (1_500_000, 2_000_000, False, False)])
 def test_groupby_fixed_signature(ctx, G, hint, wide, v32):
-    """K19 (one value column: count + sum/min/max/avg, >= 2^20 rows): lane-private cells
-    (hint <= 16), warp tables unpartitioned (hint <= 128) and behind a radix partition (up to
-    2^18 groups); under-hinted G (a warp dictionary / the merge table overflows: K18 or the
-    generic path takes over), the key INT64_MIN (side slot), values >= 2^40 (exact global path),
-    an int32 value column — against the oracle."""
+    """The fixed signature (one value column: count + sum/min/max/avg, >= 2^20 rows): K19t
+    lane-private cells (hint <= 16 direct, <= 4096 behind a radix partition), K18 above and for
+    17..32; under-hinted G (a warp dictionary or a hinted table overflows: K18 or the generic path
+    takes over), the key INT64_MIN (side slot), values >= 2^40 (K19's exact global path), an int32
+    value column — against the oracle."""
     rng = np.random.default_rng(G + hint)
     n = (1 << 20) + 4_321
     keys = np.unique(rng.integers(-(2**63), 2**63 - 1, G * 2, dtype=np.int64))[:G]
