@@ -79,7 +79,7 @@ def join(args, ctx, zipf: bool):
 
     used_auto = step(0)
     ms = {}
-    for name, st in (("flat", 1), ("partitioned", 2)):
+    for name, st in (("flat", 1), ("partitioned", 2), ("flat_inline", 3)):
         ms[name] = _time(lambda: step(st), args.steps, args.warmup, stream)
     sx.lib().sx_launch_count(ctx.h, 1)
     ms_auto = _time(lambda: step(0), args.steps, 0, stream)
@@ -102,13 +102,15 @@ def join(args, ctx, zipf: bool):
     t_or = time.time() - t0
     parity = "closed form (oracle, all %d pairs): %s" % (want["count"], "OK" if got == want else f"MISMATCH {got} vs {want}")
     algo = (nb + npr) * 16 + want["count"] * 16
-    strat = {1: "flat", 2: "partitioned"}[used_auto]
+    strat = {1: "flat", 2: "partitioned", 3: "flat_inline"}[used_auto]
     return {
         "workload": f"join µbench {'Zipf(1.0)' if zipf else 'uniform'}: build 2^{args.mb_build_log2} x probe "
                     f"2^{args.mb_probe_log2} int64 (SURVEY §8(d) C5a)",
         "ms": ms_auto, "algo_bytes": algo, "launches": launches, "parity": parity,
         "extra": {"strategy_auto": strat, "ms_flat": round(ms["flat"], 3), "ms_partitioned": round(ms["partitioned"], 3),
+                  "ms_flat_inline": round(ms["flat_inline"], 3),
                   "gbs_flat": round(algo / ms["flat"] / 1e6, 1), "gbs_partitioned": round(algo / ms["partitioned"] / 1e6, 1),
+                  "gbs_flat_inline": round(algo / ms["flat_inline"] / 1e6, 1),
                   "oracle_check_s": round(t_or, 1), "rows_per_s": round(npr / (ms_auto / 1e3), 1)},
         "kernel": f"sx_hash_join ({strat})",
     }

@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_subpart(const __grid_constan
 // group into the global table (one atomic per group and state, K18s's merge table), which
 // k_gbs_emit turns into the output.  Exactness as K18 (R2/R3): a chunk has <= 2^21 rows and only
 // values with |v| < 2^40 are summed in the 64-bit cells.
-constexpr int kGwThreads = 256;
+constexpr int kGwThreads = 256;  // (12 warps per CTA measured slower: 5.9 vs 5.2 ms at G = 4)
 constexpr int kGwWarps = kGwThreads / 32;
 constexpr int kGwU = 8;       // rows per lane per batch (their loads issued together)
 constexpr int kGtD = 16;      // K19t: ids per warp
@@ -1050,7 +1050,13 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
     // fan-out 1024 (the partitioner's maximum): <= 2048 expected groups per shared table, and
     // enough partitions to spread over every SM whatever G is; above 2^21 groups a second level
     // (K18p2) splits every partition 32 ways
-    bits = 10;
+    // 512 partitions for 2^17..2^19 hinted groups (256..1024 per partition: 44 vs 57 ms for 2^30
+    // rows, the 512-way scatter moves less partial-sector traffic); fewer groups per partition
+    // put too many threads on too few shared words (2^13 groups over 512: 172 vs 52 ms), 256
+    // partitions leave SMs idle (163-176 ms) — profiles/r02_mb_gb_variants_v3.txt
+    bits = (groups_hint >= (1 << 17) && groups_hint <= (1 << 19)) ? 9 : 10;
+    if (getenv("SX_GB_PBITS")) bits = std::max(6, std::min(10, atoi(getenv("SX_GB_PBITS"))));
+    if ((groups_hint >> bits) > 2048) bits = 10;
     const bool two = (groups_hint >> bits) > 2048;
     if (two && (groups_hint >> (bits + kSubBits)) > 2048) return SX_EUNSUPPORTED;
     const int P = 1 << bits;

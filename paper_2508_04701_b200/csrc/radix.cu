@@ -856,11 +856,12 @@ SX_EXPORT sx_status sx_hash_join(sx_ctx* ctx, const sx_col* build_cols, int nbui
   const int64_t nb = build_sel ? build_sel->len : build_cols[build_keys[0]].len;
   const int64_t np = probe_sel ? probe_sel->len : probe_cols[probe_keys[0]].len;
   if (nb > INT32_MAX || np > INT32_MAX) return set_err(ctx, SX_EINDEX, "join side exceeds INT32_MAX rows");
-  // strategy: 1 flat, 2 partitioned, 0 auto (partitioned when the flat table would exceed half the L2)
+  // strategy: 1 flat, 2 partitioned, 3 flat inline (K8f, below), 0 auto (partitioned when the flat
+  // table would exceed half the L2)
   uint64_t flat_cap = 64;
   while (flat_cap < (uint64_t)(2 * nb)) flat_cap <<= 1;
   const size_t flat_bytes = flat_cap * (size_t)(kb == 4 ? 8 : 16);
-  bool part = strategy == 2 || (strategy == 0 && flat_bytes > ctx->l2_bytes / 2);
+  bool part = strategy >= 2 || (strategy == 0 && flat_bytes > ctx->l2_bytes / 2);
   if (join_type != SX_INNER || !unique_hint) part = false;  // partitioned path: PK build, INNER
   if (!part) {
     if (used_strategy) *used_strategy = 1;
@@ -876,6 +877,79 @@ SX_EXPORT sx_status sx_hash_join(sx_ctx* ctx, const sx_col* build_cols, int nbui
     else sx_free(ctx, op.idx);
     if (out_build) *out_build = ob;
     else sx_free(ctx, ob.idx);
+    return SX_OK;
+  }
+  // strategy 3 (flat inline, K8f): the K8i kernels over the unpartitioned columns with zero
+  // partition bits — one {key, value} table of 2^ceil(log2(2 nb)) 16-byte slots (HBM-resident
+  // above ~60 MB), built once, probed once; no partition passes.  Needs one key column, no
+  // selections, and at most one payload column per side (no row ids).
+  if (strategy == 3 && nkeys == 1 && !build_sel && !probe_sel && !out_build && !out_probe && nbp <= 1 && npp <= 1 &&
+      (nbp == 0 || type_width(build_cols[bp[0]].type) <= 8) && (npp == 0 || type_width(probe_cols[pp[0]].type) <= 8)) {
+    if (used_strategy) *used_strategy = 3;
+    ProfScope ps(ctx, "join_flat_inline");
+    Scratch scr(ctx);
+    DCol bdc[SX_MAX_COLS], pdc[SX_MAX_COLS];
+    SX_TRY(to_dcols(ctx, build_cols, nbuild_cols, bdc));
+    SX_TRY(to_dcols(ctx, probe_cols, nprobe_cols, pdc));
+    PJoinI a{};
+    a.bkey = build_cols[build_keys[0]].data;
+    a.pkey = probe_cols[probe_keys[0]].data;
+    a.kb = kb;
+    a.bits = 0;
+    a.p0 = 0;
+    a.cap = flat_cap;
+    void* ob_out = nullptr;
+    void* op_out = nullptr;
+    const size_t ocap = (size_t)(np > 0 ? np : 1);
+    if (nbp == 1) {
+      a.bval = bdc[bp[0]];
+      a.bw = type_width(build_cols[bp[0]].type);
+      SX_TRY(scr.get((char**)&ob_out, ocap * a.bw));
+    }
+    if (npp == 1) {
+      a.pval = pdc[pp[0]];
+      a.pw = type_width(probe_cols[pp[0]].type);
+      SX_TRY(scr.get((char**)&op_out, ocap * a.pw));
+    }
+    a.out_b = ob_out;
+    a.out_p = op_out;
+    unsigned long long* side;
+    SX_TRY(scr.get(&side, 2));
+    SX_CUDA(cudaMemsetAsync(side, 0, 16, ctx->stream));
+    a.side = side;
+    a.cursor = (unsigned long long*)ctx->d_counters;
+    SX_CUDA(cudaMemsetAsync(a.cursor, 0, 8, ctx->stream));
+    ulonglong2* slots;
+    SX_TRY(scr.get(&slots, (size_t)flat_cap));
+    SX_CUDA(cudaMemsetAsync(slots, 0xff, (size_t)flat_cap * sizeof(ulonglong2), ctx->stream));
+    a.slots = slots;
+    a.b_lo = 0;
+    a.b_hi = nb;
+    a.p_lo = 0;
+    a.p_hi = np;
+    if (nb > 0 && np > 0) {
+      k_pji_build<<<persistent_grid(ctx, 8, (nb + kBlock - 1) / kBlock), kBlock, 0, SX_STREAM(ctx)>>>(a);
+      k_pji_probe<<<persistent_grid(ctx, 3, (np + kPiTile - 1) / kPiTile), kBlock, 0, SX_STREAM(ctx)>>>(a);
+      SX_CHECK_LAUNCH();
+    }
+    int64_t count = 0;
+    SX_TRY(read_i64(ctx, a.cursor, &count));
+    if (nbp == 1) {
+      out_payload[0] = build_cols[bp[0]];
+      out_payload[0].len = count;
+      out_payload[0].data = ob_out;
+      out_payload[0].offsets = nullptr;
+      scr.release(ob_out);
+    }
+    if (npp == 1) {
+      out_payload[nbp] = probe_cols[pp[0]];
+      out_payload[nbp].len = count;
+      out_payload[nbp].data = op_out;
+      out_payload[nbp].offsets = nullptr;
+      scr.release(op_out);
+    }
+    const double kbytes = type_width(build_cols[build_keys[0]].type);
+    ps.set_bytes(kbytes * (nb + np) + 2.0 * (a.bw + a.pw) * count);
     return SX_OK;
   }
   if (used_strategy) *used_strategy = 2;

@@ -98,20 +98,40 @@ def test_join_mbench_vs_closed_form(ctx, zipf, strategy):
     assert np.array_equal(brow.cpu().numpy().astype(np.int64), gb)
 
 
+@pytest.mark.parametrize("strategy", [2, 3])
 @pytest.mark.parametrize("zipf", [False, True])
-def test_join_mbench_inline_payloads(ctx, zipf):
+def test_join_mbench_inline_payloads(ctx, zipf, strategy):
     """The µbench's own call shape (payload pairs only, no row ids): the partitioned join's
-    inline-value path (K8i) vs the closed form."""
+    inline-value path (K8i) and the flat inline table (K8f) vs the closed form."""
     nb, np_ = 1 << 17, (1 << 21) + 7
     bk, bp = gen.mb_join_build(nb, device="cuda")
     pk, pp = gen.mb_join_probe(nb, np_, zipf, seed=5, device="cuda")
     want = oracle.mb_join_closed(nb, pk.cpu().numpy(), pp.cpu().numpy())
     _, _, (gb, gp), used = ctx.hash_join([sx.col(bk), sx.col(bp)], [0], [sx.col(pk), sx.col(pp)], [0], "inner",
-                                         unique=True, bp=[1], pp=[1], strategy=2, rows=(False, False))
-    assert used == 2
+                                         unique=True, bp=[1], pp=[1], strategy=strategy, rows=(False, False))
+    assert used == strategy
     gb, gp = gb.cpu().numpy(), gp.cpu().numpy()
     got = {"count": len(gb), "sum_build": int(gb.sum()), "sum_probe": int(gp.sum()), "pair_hash": np_pair_mix(gb, gp)}
     assert got == want
+
+
+def test_flat_inline_join_reserved_key(ctx):
+    """K8f: int64 keys including -1 (the table's EMPTY marker: side cell), 0 and the extremes,
+    misses on both sides, payload widths 4 and 8 — against the oracle's join."""
+    rng = np.random.default_rng(4)
+    nb, np_ = 50_000, 300_001
+    bkey = np.unique(rng.integers(-(2**63), 2**63 - 1, nb * 2, dtype=np.int64))[:nb]
+    bkey[:4] = [-1, 0, -(2**63), 2**63 - 1]
+    bkey = rng.permutation(bkey)
+    pkey = np.where(rng.random(np_) < 0.6, bkey[rng.integers(0, nb, np_)], rng.integers(-(2**63), 2**63 - 1, np_, dtype=np.int64))
+    pkey[:3] = [-1, -1, 5]
+    bpay = rng.integers(-(2**31), 2**31 - 1, nb).astype(np.int32)
+    ppay = rng.integers(-(2**62), 2**62, np_)
+    _, _, (gb, gp), used = ctx.hash_join([sx.col(dev(bkey)), sx.col(dev(bpay))], [0], [sx.col(dev(pkey)), sx.col(dev(ppay))],
+                                         [0], "inner", unique=True, bp=[1], pp=[1], strategy=3, rows=(False, False))
+    assert used == 3
+    op, ob = oracle.join(bkey, pkey, "inner")
+    assert sorted(zip(gb.cpu().numpy().tolist(), gp.cpu().numpy().tolist())) == sorted(zip(bpay[ob].tolist(), ppay[op].tolist()))
 
 
 @pytest.mark.parametrize("inline", ["1", "0"])
