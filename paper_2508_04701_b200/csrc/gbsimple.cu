@@ -1,4 +1,8 @@
-// gbsimple.cu — K18: the plain-shape fast path of sx_groupby_agg (H7).
+// gbsimple.cu — K18 / K19t: the plain-shape fast paths of sx_groupby_agg (H7).
+//
+// Dispatch (gb_simple): the fixed signature (one value column: COUNT + SUM/MIN/MAX/AVG) with
+// <= 16 or 33..4096 hinted groups takes K19t (atomic-free lane-private cells, below); everything
+// else of the plain shape takes K18.
 //
 // group-by is substantial where few groups cause memory contention (Q1) and where
 // many groups need a large table (Q10/Q18); SURVEY §8(d) C5b sweeps G = 2^2 .. 2^26.  For the plain
