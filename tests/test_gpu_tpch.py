@@ -418,13 +418,26 @@ def test_upload_from_host_tables(ctx):
 
 @pytest.mark.parametrize("scan", ["wscan", "gather"])
 def test_q9_wide_orderdates_fall_back(ctx, monkeypatch, scan):
-    """The fused Q9 keeps o_orderdate as int16 days (1880..2059): an order dated outside that range
-    (here year 2100 and 1850) makes it step aside to the operator-at-a-time plan, still exact."""
+    """The fused Q9 keeps year(o_orderdate) as one byte (1900..2027): an order dated outside that
+    range (here 2100 and 1850, then 2030 just past the byte's range) makes it step aside to the
+    operator-at-a-time plan, still exact; 1901 and 2027 stay inside."""
     monkeypatch.setenv("SX_Q9_SCAN", scan)
     host = gen.cpu_tables(10, seed=5)
     od = host["orders"]["o_orderdate"].copy()
     od[::97] += 47000   # ~2100
     od[1::97] -= 44000  # ~1850
+    host["orders"]["o_orderdate"] = od
+    T = tpch.Tpch(ctx, to_dev(host))
+    want = oracle.run_query("q9", host)
+    got = T.run("q9")
+    assert rows_equal(got, want), diff_rows(got, want)
+    od = gen.cpu_tables(10, seed=5)["orders"]["o_orderdate"].copy()
+    od[::53] = 22066   # 2030-06-01
+    host["orders"]["o_orderdate"] = od
+    T = tpch.Tpch(ctx, to_dev(host))
+    assert rows_equal(T.run("q9"), oracle.run_query("q9", host))
+    od[::53] = -25000  # 1901-07-28
+    od[1::53] = 20800  # 2026-12-13
     host["orders"]["o_orderdate"] = od
     T = tpch.Tpch(ctx, to_dev(host))
     want = oracle.run_query("q9", host)
