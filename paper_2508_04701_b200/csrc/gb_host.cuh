@@ -537,13 +537,54 @@ __global__ void __launch_bounds__(kBlock, 4) k_runs_lean(const __grid_constant__
       *(int*)(d + o4) = s < 0 ? -1 : 0;
     }
   };
-  // (loading the next window before aggregating this one measured slower: 2.35 vs 1.98 ms at
-  // 3 CTAs/SM — the extra registers cost a CTA per SM)
-  for (int64_t wbase = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R; wbase < n; wbase += stride) {
+  // The next window's 8 keys + 8 values per lane are copied into this thread's slot of a
+  // shared double buffer by cp.async while the current window is aggregated (ncu: the register
+  // version was long-scoreboard bound at 4.0 TB/s; loading the next window into registers
+  // measured slower, 2.35 vs 1.98 ms — the extra registers cost a CTA per SM).
+  __shared__ __align__(16) int32_t s_k[2][kBlock * R];
+  __shared__ __align__(16) long long s_v[2][kBlock * R];
+  const int32_t* gk = prog.lean_kp();
+  const long long* gv = prog.lean_vp();
+  auto issue = [&](int64_t rr, int b) {  // whole 8-row chunks only (the tail loads directly)
+    if (rr + R <= n) {
+      const unsigned sk = (unsigned)__cvta_generic_to_shared(&s_k[b][threadIdx.x * R]);
+      const unsigned sv = (unsigned)__cvta_generic_to_shared(&s_v[b][threadIdx.x * R]);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sk + 16 * j), "l"(gk + rr + 4 * j));
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sv + 16 * j), "l"(gv + rr + 2 * j));
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  int buf = 0;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * R;
+  if (w0 < n) issue(w0 + (int64_t)lane * R, 0);
+  for (int64_t wbase = w0; wbase < n; wbase += stride) {
     const int64_t r0 = wbase + (int64_t)lane * R;
+    issue(wbase + stride + (int64_t)lane * R, buf ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
     int32_t k[R];
     long long v[R];
-    prog.lean_load(r0, n, k, v);  // rows >= n: v = 0, k = 0 (masked by m below)
+    if (r0 + R <= n) {  // (16-byte shared reads of this thread's own slot)
+      const int4* pk = (const int4*)&s_k[buf][threadIdx.x * R];
+      const longlong2* pv = (const longlong2*)&s_v[buf][threadIdx.x * R];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int4 a = pk[j];
+        k[4 * j] = a.x; k[4 * j + 1] = a.y; k[4 * j + 2] = a.z; k[4 * j + 3] = a.w;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const longlong2 q = pv[j];
+        v[2 * j] = q.x;
+        v[2 * j + 1] = q.y;
+      }
+    } else {
+      prog.lean_load(r0, n, k, v);  // rows >= n: v = 0, k = 0 (masked by m below)
+    }
+    buf ^= 1;
     const int m = (int)max((int64_t)0, min((int64_t)R, n - r0));
     int32_t pk = __shfl_up_sync(kFull, k[R - 1], 1);
     if (lane == 0 && r0 > 0 && r0 <= n) pk = prog.lean_key(r0 - 1);

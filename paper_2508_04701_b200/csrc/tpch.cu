@@ -533,6 +533,9 @@ struct Q18Prog {
   }
   __device__ __forceinline__ int32_t lean_key(int64_t r) const { return (int32_t)__ldg(okey + r); }
   __device__ __forceinline__ long long lean_val(int64_t r) const { return __ldg(qty + r); }
+  // the key / value columns themselves (K10l's cp.async double buffer copies whole 8-row chunks)
+  __device__ __forceinline__ const int32_t* lean_kp() const { return (const int32_t*)okey; }
+  __device__ __forceinline__ const long long* lean_vp() const { return qty; }
   // Dense rows for k_runs_own: R consecutive rows (r0 % R == 0) with 128-bit streaming loads.
   static constexpr bool kDenseRuns = true;
   template <int R>
