@@ -187,13 +187,14 @@ def test_q6_lazy_levels(ctx, monkeypatch, lazy3):
 
 
 
-@pytest.mark.parametrize("case", ["sorted", "hash", "customer-shuffled", "customer-missing"])
+@pytest.mark.parametrize("case", ["sorted", "lookup", "hash", "customer-shuffled", "customer-missing"])
 def test_q18_join_modes(ctx, monkeypatch, case):
-    """Q18's orders/customer joins by sorted-PK lookups (default), by hash joins (SX_Q18_JOIN=hash),
-    with the customer rows shuffled (lookups fail: hash joins), and with qualifying orders whose
-    customer is missing (inner-join semantics: those orders drop out)."""
-    if case == "hash":
-        monkeypatch.setenv("SX_Q18_JOIN", "hash")
+    """Q18's orders/customer joins by the fused sorted-PK lookup kernel (default), by separate
+    lookups + gathers (SX_Q18_JOIN=lookup), by hash joins (SX_Q18_JOIN=hash), with the customer
+    rows shuffled (lookups fail: hash joins), and with qualifying orders whose customer is missing
+    (inner-join semantics: those orders drop out)."""
+    if case in ("hash", "lookup"):
+        monkeypatch.setenv("SX_Q18_JOIN", case)
     host = gen.cpu_tables(100, seed=29)
     host = dict(host)
     c = host["customer"]
