@@ -188,6 +188,26 @@ def test_groupby_fixed_signature(ctx, G, hint, wide, v32):
     assert g == len(want)
 
 
+@pytest.mark.parametrize("n,G,hint,keytype", [((1 << 20) + 1, 1, 1, np.int64), ((1 << 21) - 7, 3, 4, np.int32),
+                                              ((1 << 20) + 255, 17, 16, np.int64), ((1 << 20) + 33, 2000, 2048, np.int32)])
+def test_groupby_k19_edges(ctx, n, G, hint, keytype):
+    """K19t edge cases: one group, a ragged tail (n not a multiple of the 256-row warp batch),
+    int32 keys, more groups than the hint allows a warp's 16 cells (rows of the 17th group take
+    the exact global path), partitioned with int32 keys; values straddling 2^32 (the split sums)."""
+    rng = np.random.default_rng(n + G)
+    keys = np.unique(rng.integers(-(2**31), 2**31 - 1, G * 4))[:G].astype(keytype)
+    k = keys[rng.integers(0, G, n)]
+    v = rng.integers(-(2**39), 2**39, n).astype(np.int64)
+    v[::7] = (2**32) - 1
+    v[1::7] = -(2**32)
+    kc = sx.col(dev(k), A.SX_I32 if keytype == np.int32 else A.SX_I64)
+    keys_o, aggs_o, g = ctx.groupby([kc, sx.col(dev(v), A.SX_DEC64, 2)], [(0, "id")], FIXED_AGGS, groups_hint=hint)
+    got = canon(keys_o, aggs_o, [a[0] for a in FIXED_AGGS])
+    want = oracle.groupby([k.astype(np.int64), v], [0], FIXED_AGGS)
+    check_gb(got, want)
+    assert g == len(want)
+
+
 @pytest.mark.parametrize("hint", [4, 64])
 def test_groupby_two_u8_keys_where(ctx, hint):
     rng = np.random.default_rng(11)
