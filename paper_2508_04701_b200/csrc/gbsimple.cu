@@ -1,8 +1,8 @@
 // gbsimple.cu — K18 / K19t: the plain-shape fast paths of sx_groupby_agg (H7).
 //
 // Dispatch (gb_simple): the fixed signature (one value column: COUNT + SUM/MIN/MAX/AVG) with
-// <= 16 or 33..4096 hinted groups takes K19t (atomic-free lane-private cells, below); everything
-// else of the plain shape takes K18.
+// <= 16384 hinted groups takes K19t (lane-private count/sum cells, below); everything else of the
+// plain shape takes K18.
 //
 // group-by is substantial where few groups cause memory contention (Q1) and where
 // many groups need a large table (Q10/Q18); SURVEY §8(d) C5b sweeps G = 2^2 .. 2^26.  For the plain
@@ -540,26 +540,26 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_subpart(const __grid_constan
   }
 }
 
-// ---- K19: atomic-free warp-private aggregation ---------------------------------------------
+// ---- K19: warp-private aggregation without returning shared atomics ---------------------
 // ncu on K18s at G = 4 (r2r_gb4): 24 ms for 2^30 rows, 755 GB/s — a shared atomic whose old
 // value is used costs ~2 cycles per lane (B300_MICROARCH "ATOMS spread-addr"), and K18's SUM
-// needs the old word for its carry.  K19t updates shared state with plain loads and stores only:
-// every warp owns a dictionary key -> dense id (<= kGtD ids) and LANE-PRIVATE cells [id][lane]
-// for count / sum / min / max, so no two lanes (and no two warps) ever write the same word.  The
-// common row costs one dictionary read (home slot or the next), and four conflict-free
-// read-modify-writes of its lane's cells; a batch whose rows all qualify takes that fast path,
-// any other batch (a key's first rows, a displaced key, a wide value, the key kEmptyKey, groups
-// beyond kGtD) the general per-row path, where rows without a cell take g_row's exact global
-// atomics.  Above kGtD hinted groups the input is first radix-partitioned (K7) to ~8 groups per
-// partition, so a warp's chunk of one partition fits its cells.  A warp aggregates one chunk of
-// rows (never spanning two partitions), reduces each id's cells over its lanes and merges the
-// group into the global table (one atomic per group and state, K18s's merge table), which
-// k_gbs_emit turns into the output.  Exactness as K18 (R2/R3): a chunk has <= 2^21 rows and only
-// values with |v| < 2^40 are summed in the 64-bit cells.
+// needs the old word for its carry.  K19t updates COUNT and SUM with plain loads and stores: every
+// warp owns a dictionary key -> dense id (<= D ids: 16 or 48) and LANE-PRIVATE cells [id][lane], so no
+// two lanes (and no two warps) ever write the same count/sum word; MIN/MAX are lane-private too
+// (16 ids) or live per warp and id and change only when a row improves on them (48 ids: a shared
+// CAS, rare after a group's first rows) — see GtWarp for the measured choice.
+// The common row costs one dictionary read (home slot or the next) and the cell updates; a batch
+// whose rows all qualify takes that fast path, any other batch (a key's first rows, a displaced
+// key, a wide value, the key kEmptyKey, groups beyond D) the general per-row path, where rows
+// without a cell take g_row's exact global atomics.  Above D hinted groups the input is first
+// radix-partitioned (K7) to ~4 (16 ids) or ~16 (48 ids) groups per partition, so a warp's chunk of
+// one partition fits its cells.  A warp aggregates one chunk of rows (never spanning two partitions), reduces each id's
+// cells over its lanes and merges the group into the global table (one atomic per group and
+// state, K18s's merge table), which k_gbs_emit turns into the output.  Exactness as K18 (R2/R3):
+// a chunk has <= 2^21 rows and only values with |v| < 2^40 are summed in the 64-bit cells.
 constexpr int kGwThreads = 256;  // (12 warps per CTA measured slower: 5.9 vs 5.2 ms at G = 4)
 constexpr int kGwWarps = kGwThreads / 32;
 constexpr int kGwU = 8;       // rows per lane per batch (their loads issued together)
-constexpr int kGtD = 16;      // K19t: ids per warp
 constexpr int kGtSlots = 256;  // K19t: dictionary slots per warp (load <= 1/16: keys stay home)
 
 // multiplicative slot hash (top bits; independent of hash64's partition bits 48..57)
@@ -656,31 +656,59 @@ __device__ __forceinline__ void gw_merge_group(const GsGlobal& g, const GsSpec& 
   if constexpr (SIG::kHasMax) g_add(g, s, gs, SIG::kMax, (unsigned long long)mx, true);
 }
 
-// K19t.  Per warp: dictionary keys[kGtSlots + 1] / ids (int8: -1 none, kGtD overflow), id ->
-// key, lane-private cells cnt[kGtD][32] u32 and sum / min / max [kGtD][32] i64.
+// K19t.  Per warp: dictionary keys[kGtSlots + 1] / ids (int8: -1 none, D overflow), id -> key,
+// lane-private cells cnt[D][32] u32 and sum[D][32] i64, and MIN/MAX either lane-private too (LP:
+// [D][32] i64 each — conflict-free stores, but 16 B per id and lane held the warp to 16 ids) or
+// per warp and id (!LP: a row changes them only when it improves on the value read, by a shared
+// CAS — rare after a group's first rows — which lets a warp hold 48 ids).  Measured (2^30 rows):
+// G = 4..16 direct 5.2 ms <16, LP> vs 6.9 <48>; G = 32 direct 7.4 <48> (K18s 10.6); G = 64..2048
+// at ~4 groups per partition <16, LP> 17-28 ms vs 19-29 at ~16 <48>; G = 4096..16384 at ~16 per
+// partition <48> 28 / 36 / 49 ms vs 36 / 53 / 54 (profiles/r02_mb_gb_variants_v3.txt).
+template <int D, bool LP>
 struct GtWarp {
   long long keys[kGtSlots + 2];
-  long long idkey[kGtD];
-  long long sum[kGtD + 1][32];  // (row kGtD: the sink of the fast path's inactive rows)
-  long long mn[kGtD + 1][32];
-  long long mx[kGtD + 1][32];
-  unsigned cnt[kGtD + 1][32];
+  long long idkey[D];
+  long long sum[D + 1][32];  // (row D: the sink of the fast path's inactive rows)
+  unsigned cnt[D + 1][32];
+  long long mn[D + 1][LP ? 32 : 1];
+  long long mx[D + 1][LP ? 32 : 1];
   signed char id[kGtSlots + 2];
 };
 constexpr int kGtShift = 32 - 8;  // log2(kGtSlots)
 
-template <class SIG>
-__device__ __forceinline__ void gt_cell(GtWarp& W, int id, int lane, long long v) {
+template <class SIG, int D, bool LP>
+__device__ __forceinline__ void gt_cell(GtWarp<D, LP>& W, int id, int lane, long long v) {
   W.cnt[id][lane] += 1u;
   if constexpr (SIG::kHasSum) W.sum[id][lane] += v;
-  if constexpr (SIG::kHasMin) W.mn[id][lane] = min(W.mn[id][lane], v);
-  if constexpr (SIG::kHasMax) W.mx[id][lane] = max(W.mx[id][lane], v);
+  if constexpr (LP) {
+    if constexpr (SIG::kHasMin) W.mn[id][lane] = min(W.mn[id][lane], v);
+    if constexpr (SIG::kHasMax) W.mx[id][lane] = max(W.mx[id][lane], v);
+  } else {
+    if constexpr (SIG::kHasMin) {
+      long long cur = W.mn[id][0];
+      while (v < cur) {
+        const long long old = (long long)atomicCAS((unsigned long long*)&W.mn[id][0], (unsigned long long)cur,
+                                                   (unsigned long long)v);
+        if (old == cur) break;
+        cur = old;
+      }
+    }
+    if constexpr (SIG::kHasMax) {
+      long long cur = W.mx[id][0];
+      while (v > cur) {
+        const long long old = (long long)atomicCAS((unsigned long long*)&W.mx[id][0], (unsigned long long)cur,
+                                                   (unsigned long long)v);
+        if (old == cur) break;
+        cur = old;
+      }
+    }
+  }
 }
 
 // The general per-row path (a key's first rows, displaced keys, wide values, the key
-// kEmptyKey, more than kGtD groups in the chunk: those rows take g_row's global atomics).
-template <class SIG>
-__device__ __noinline__ void gt_slow_batch(GtWarp& W, const GsSpec& s, const GsGlobal& g, int lane, int& nid,
+// kEmptyKey, more than D groups in the chunk: those rows take g_row's global atomics).
+template <class SIG, int D, bool LP>
+__device__ __noinline__ void gt_slow_batch(GtWarp<D, LP>& W, const GsSpec& s, const GsGlobal& g, int lane, int& nid,
                                            bool& side, const long long (&k)[kGwU], const long long (&v)[kGwU],
                                            const bool (&in)[kGwU]) {
 #pragma unroll 1
@@ -701,31 +729,31 @@ __device__ __noinline__ void gt_slow_batch(GtWarp& W, const GsSpec& s, const GsG
       const unsigned lm = __ballot_sync(kFull, lead);
       if (lead) {
         const int nidx = nid + __popc(lm & lanemask_lt());
-        W.id[ns] = (signed char)(nidx < kGtD ? nidx : kGtD);
-        if (nidx < kGtD) W.idkey[nidx] = ku;
+        W.id[ns] = (signed char)(nidx < D ? nidx : D);
+        if (nidx < D) W.idkey[nidx] = ku;
       }
       nid += __popc(lm);
       side = side || __any_sync(kFull, miss && ku == kEmptyKey);
       __syncwarp();
     }
     const int id = slot >= 0 ? W.id[slot] : -1;
-    if (act && (id < 0 || id >= kGtD)) wide = true;  // no cell: the exact global path
+    if (act && (id < 0 || id >= D)) wide = true;  // no cell: the exact global path
     if (wide) {
       long long vv[kGsMaxVals] = {vu, 0, 0, 0};
       g_row(g, s, ku, vv);
     } else if (act) {
-      gt_cell<SIG>(W, id, lane, vu);
+      gt_cell<SIG, D, LP>(W, id, lane, vu);
     }
     __syncwarp();
   }
 }
 
-template <class SIG, int KB, int VB>
+template <class SIG, int KB, int VB, int D, bool LP>
 __global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSpec s, const __grid_constant__ GwChunks ch,
                                                     const __grid_constant__ GsGlobal g) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
-  GtWarp& W = ((GtWarp*)smem)[threadIdx.x >> 5];
+  GtWarp<D, LP>& W = ((GtWarp<D, LP>*)smem)[threadIdx.x >> 5];
   const int gw = blockIdx.x * kGwWarps + (threadIdx.x >> 5), nw = gridDim.x * kGwWarps;
   for (int c = gw; c < ch.nchunks; c += nw) {
     for (int i = lane; i < kGtSlots + 2; i += 32) {
@@ -733,12 +761,19 @@ __global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSp
       W.id[i] = -1;
     }
 #pragma unroll
-    for (int d = 0; d <= kGtD; ++d) {
+    for (int d = 0; d <= D; ++d) {
       W.cnt[d][lane] = 0;
       W.sum[d][lane] = 0;
-      W.mn[d][lane] = LLONG_MAX;
-      W.mx[d][lane] = LLONG_MIN;
+      if constexpr (LP) {
+        W.mn[d][lane] = LLONG_MAX;
+        W.mx[d][lane] = LLONG_MIN;
+      }
     }
+    if constexpr (!LP)
+      for (int d = lane; d <= D; d += 32) {
+        W.mn[d][0] = LLONG_MAX;
+        W.mx[d][0] = LLONG_MIN;
+      }
     int nid = 0;
     bool side = false;  // the key kEmptyKey has an id
     __syncwarp();
@@ -751,7 +786,7 @@ __global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSp
       bool inn[kGwU];
       gw_load<KB, VB>(s, b + 32 * kGwU, hi, lane, kn, vn, inn);
       // fast path: every row's key at its home slot or the next, with an id, and a small value
-      // (branch-free: bitwise tests; a row past the chunk updates the sink row kGtD)
+      // (branch-free: bitwise tests; a row past the chunk updates the sink row D)
       int id[kGwU];
       int ok = 1;
 #pragma unroll
@@ -760,15 +795,15 @@ __global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSp
         const long long c0 = W.keys[h], c1 = W.keys[h + 1];
         const int i0 = W.id[h], i1 = W.id[h + 1];
         const int iu = c0 == k[u] ? i0 : c1 == k[u] ? i1 : -1;
-        const int good = ((unsigned)iu < (unsigned)kGtD) & (k[u] != kEmptyKey) & small_v(v[u]);
+        const int good = ((unsigned)iu < (unsigned)D) & (k[u] != kEmptyKey) & small_v(v[u]);
         ok &= (!in[u]) | good;
-        id[u] = in[u] ? iu : kGtD;
+        id[u] = in[u] ? iu : D;
       }
       if (__all_sync(kFull, ok)) {
 #pragma unroll
-        for (int u = 0; u < kGwU; ++u) gt_cell<SIG>(W, id[u], lane, v[u]);
+        for (int u = 0; u < kGwU; ++u) gt_cell<SIG, D, LP>(W, id[u], lane, v[u]);
       } else {
-        gt_slow_batch<SIG>(W, s, g, lane, nid, side, k, v, in);
+        gt_slow_batch<SIG, D, LP>(W, s, g, lane, nid, side, k, v, in);
       }
 #pragma unroll
       for (int u = 0; u < kGwU; ++u) {
@@ -779,18 +814,21 @@ __global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSp
     }
     __syncwarp();
     // the warp's groups: each id's cells reduced over the lanes; lane d merges group d
-    const int nd = min(nid, kGtD);
+    const int nd = min(nid, D);
     for (int d = 0; d < nd; ++d) {
       unsigned cn = W.cnt[d][lane];
-      long long sm = W.sum[d][lane], mn = W.mn[d][lane], mx = W.mx[d][lane];
+      long long sm = W.sum[d][lane];
+      long long mn = W.mn[d][LP ? lane : 0], mx = W.mx[d][LP ? lane : 0];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         cn += __shfl_xor_sync(kFull, cn, o);
         sm += __shfl_xor_sync(kFull, sm, o);
-        mn = min(mn, __shfl_xor_sync(kFull, mn, o));
-        mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        if constexpr (LP) {
+          mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+          mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        }
       }
-      if (lane == d && cn) gw_merge_group<SIG>(g, s, W.idkey[d], cn, sm, mn, mx);
+      if (lane == (d & 31) && cn) gw_merge_group<SIG>(g, s, W.idkey[d], cn, sm, mn, mx);
     }
     __syncwarp();
   }
@@ -823,19 +861,20 @@ bool plain_col_expr(const sx_expr& e, int* col) {
 // K19 host side (see the kernels): SX_EUNSUPPORTED (nothing allocated) when the shape does not
 // fit (not the fixed signature, or more than kGtHintMax hinted groups) or the hinted global merge
 // table overflowed.
-constexpr int64_t kGtHintMax = 4096;  // 1024 partitions x ~4 groups
+constexpr int64_t kGtHintMax = 16384;  // 1024 partitions x ~16 groups
 sx_status gb_k19(sx_ctx* ctx, GsSpec s, int sig, const sx_col& kc, int vtype, int naggs, const sx_agg* aggs,
                  int64_t groups_hint, int64_t n, sx_col* out_keys, sx_col* out_aggs, int64_t* out_ngroups) {
-  // (17..32 hinted groups: K18s's replicated shared tables measured faster, 12.1 vs 17.1 ms)
-  if (sig < 0 || s.nv != 1 || groups_hint > kGtHintMax || (groups_hint > kGtD && groups_hint <= 32))
-    return SX_EUNSUPPORTED;
+  if (sig < 0 || s.nv != 1 || groups_hint > kGtHintMax) return SX_EUNSUPPORTED;
   Scratch scr(ctx);
-  // fan-out (above kGtD groups): ~4 expected groups per partition, so a warp's chunk of one
-  // partition practically never exceeds its kGtD cells (rows of groups beyond them would take
-  // global atomics: at ~8 per partition, the few partitions past 16 groups made one warp's chunk
-  // 7x slower than the rest, ncu r2u_gb4k)
+  // variant and fan-out (measured, see GtWarp): <16, LP> directly up to 16 hinted groups and at ~4
+  // groups per partition for 49..2048; <48, !LP> directly for 17..48 and at ~16 per partition above
+  // 2048.  A partition's expected groups stay far below the warp's ids (rows of groups beyond them
+  // take global atomics: with 16 ids and ~8 groups per partition, the few partitions past 16
+  // groups made one warp's chunk 7x slower than the rest, ncu r2u_gb4k).
+  const bool big = (groups_hint > 16 && groups_hint <= 48) || groups_hint > 2048;
+  const int per = big ? 16 : 4, dmax = big ? 48 : 16;
   int bits = 0;
-  while (bits < 10 && groups_hint > kGtD && ((int64_t)4 << bits) < groups_hint) ++bits;
+  while (bits < 10 && groups_hint > dmax && ((int64_t)per << bits) < groups_hint) ++bits;
   const int P = 1 << bits;
   std::vector<int64_t> offs{0, n};
   if (P > 1) {
@@ -903,12 +942,17 @@ sx_status gb_k19(sx_ctx* ctx, GsSpec s, int sig, const sx_col& kc, int vtype, in
     } else {
       auto go = [&](auto kbc, auto vbc) -> sx_status {
         constexpr int KB = decltype(kbc)::value, VB = decltype(vbc)::value;
-        const size_t smem = sizeof(GtWarp) * kGwWarps;
-        SX_CUDA(cudaFuncSetAttribute(k_gbt<SIG, KB, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 1;
-        SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbt<SIG, KB, VB>, kGwThreads, smem));
-        const unsigned grid = (unsigned)std::max(1, std::min(nch, ctx->num_sms * std::max(1, per_sm)));
-        k_gbt<SIG, KB, VB><<<grid, kGwThreads, smem, SX_STREAM(ctx)>>>(s, ch, g);
+        auto launch = [&](auto kern, size_t wbytes) -> sx_status {
+          const size_t smem = wbytes * kGwWarps;
+          SX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          int per_sm = 1;
+          SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGwThreads, smem));
+          const unsigned grid = (unsigned)std::max(1, std::min(nch, ctx->num_sms * std::max(1, per_sm)));
+          kern<<<grid, kGwThreads, smem, SX_STREAM(ctx)>>>(s, ch, g);
+          return SX_OK;
+        };
+        if (big) SX_TRY(launch(k_gbt<SIG, KB, VB, 48, false>, sizeof(GtWarp<48, false>)));
+        else SX_TRY(launch(k_gbt<SIG, KB, VB, 16, true>, sizeof(GtWarp<16, true>)));
         SX_CHECK_LAUNCH();
         return SX_OK;
       };

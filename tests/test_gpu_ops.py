@@ -164,10 +164,10 @@ FIXED_AGGS = [("sum", [(1, [(1, 1, 0)])]), ("count", []), ("min", [(1, [(1, 1, 0
                                              (100_000, 8192, False, False), (1_500_000, 2_000_000, False, False)])
 def test_groupby_fixed_signature(ctx, G, hint, wide, v32):
     """The fixed signature (one value column: count + sum/min/max/avg, >= 2^20 rows): K19t
-    lane-private cells (hint <= 16 direct, <= 4096 behind a radix partition), K18 above and for
-    17..32; under-hinted G (a warp dictionary or a hinted table overflows: K18 or the generic path
-    takes over), the key INT64_MIN (side slot), values >= 2^40 (K19's exact global path), an int32
-    value column — against the oracle."""
+    lane-private cells (hint <= 48 direct, <= 16384 behind a radix partition), K18 above;
+    under-hinted G (a warp dictionary or a hinted table overflows: K18 or the generic path takes
+    over), the key INT64_MIN (side slot), values >= 2^40 (K19's exact global path), an int32 value
+    column — against the oracle."""
     rng = np.random.default_rng(G + hint)
     n = (1 << 20) + 4_321
     keys = np.unique(rng.integers(-(2**63), 2**63 - 1, G * 2, dtype=np.int64))[:G]
@@ -189,11 +189,11 @@ def test_groupby_fixed_signature(ctx, G, hint, wide, v32):
 
 
 @pytest.mark.parametrize("n,G,hint,keytype", [((1 << 20) + 1, 1, 1, np.int64), ((1 << 21) - 7, 3, 4, np.int32),
-                                              ((1 << 20) + 255, 17, 16, np.int64), ((1 << 20) + 33, 2000, 2048, np.int32)])
+                                              ((1 << 20) + 255, 60, 48, np.int64), ((1 << 20) + 33, 2000, 2048, np.int32)])
 def test_groupby_k19_edges(ctx, n, G, hint, keytype):
     """K19t edge cases: one group, a ragged tail (n not a multiple of the 256-row warp batch),
-    int32 keys, more groups than the hint allows a warp's 16 cells (rows of the 17th group take
-    the exact global path), partitioned with int32 keys; values straddling 2^32 (the split sums)."""
+    int32 keys, more groups than a warp's 48 cells (rows of the groups past them take the exact
+    global path), partitioned with int32 keys; values straddling 2^32 (the split sums)."""
     rng = np.random.default_rng(n + G)
     keys = np.unique(rng.integers(-(2**31), 2**31 - 1, G * 4))[:G].astype(keytype)
     k = keys[rng.integers(0, G, n)]
