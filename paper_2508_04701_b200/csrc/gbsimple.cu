@@ -661,18 +661,18 @@ __device__ __forceinline__ void gw_merge_group(const GsGlobal& g, const GsSpec& 
 // [D][32] i64 each — conflict-free stores, but 16 B per id and lane held the warp to 16 ids) or
 // per warp and id (!LP: a row changes them only when it improves on the value read, by a shared
 // CAS — rare after a group's first rows — which lets a warp hold 48 ids).  Measured (2^30 rows):
-// G = 4..16 direct 5.2 ms <16, LP> vs 6.9 <48>; G = 32 direct 7.4 <48> (K18s 10.6); G = 64..2048
-// at ~4 groups per partition <16, LP> 17-28 ms vs 19-29 at ~16 <48>; G = 4096..16384 at ~16 per
-// partition <48> 28 / 36 / 49 ms vs 36 / 53 / 54 (profiles/r02_mb_gb_variants_v3.txt).
+// G = 4..16 direct 5.2 ms <16, LP> vs 6.9 <48>; G = 32 direct 8.3 <48> (K18s 10.6); G = 64..1024
+// at ~4 groups per partition <16, LP> 17-21 ms vs 21-22 at ~16 <48>; G = 2048..16384 at ~16 per
+// partition <48> 23 / 25 / 35 / 43 ms vs 29 / 36 / 53 / 54 (profiles/r02_mb_gb_variants_v3.txt).
 template <int D, bool LP>
 struct GtWarp {
-  long long keys[kGtSlots + 2];
+  long long keys[kGtSlots + 4];
   long long idkey[D];
   long long sum[D + 1][32];  // (row D: the sink of the fast path's inactive rows)
   unsigned cnt[D + 1][32];
   long long mn[D + 1][LP ? 32 : 1];
   long long mx[D + 1][LP ? 32 : 1];
-  signed char id[kGtSlots + 2];
+  signed char id[kGtSlots + 4];
 };
 constexpr int kGtShift = 32 - 8;  // log2(kGtSlots)
 
@@ -756,8 +756,8 @@ __global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSp
   GtWarp<D, LP>& W = ((GtWarp<D, LP>*)smem)[threadIdx.x >> 5];
   const int gw = blockIdx.x * kGwWarps + (threadIdx.x >> 5), nw = gridDim.x * kGwWarps;
   for (int c = gw; c < ch.nchunks; c += nw) {
-    for (int i = lane; i < kGtSlots + 2; i += 32) {
-      W.keys[i] = kEmptyKey;  // (slot kGtSlots + 1: a never-used pad, probed as "home + 1")
+    for (int i = lane; i < kGtSlots + 4; i += 32) {
+      W.keys[i] = kEmptyKey;  // (slots kGtSlots + 1..3: never-used pads, probed as "home + 1..3")
       W.id[i] = -1;
     }
 #pragma unroll
@@ -792,9 +792,19 @@ __global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSp
 #pragma unroll
       for (int u = 0; u < kGwU; ++u) {
         const uint32_t h = gw_hash(k[u]) >> kGtShift;
-        const long long c0 = W.keys[h], c1 = W.keys[h + 1];
-        const int i0 = W.id[h], i1 = W.id[h + 1];
-        const int iu = c0 == k[u] ? i0 : c1 == k[u] ? i1 : -1;
+        // the home slot and the next (<16>), or the next three (<48>: with up to ~48 keys in 256
+        // slots a key sits two or more slots past home in ~6% of the chunks, which then ran the
+        // slow path throughout: one SM 2x the average, ncu r2ba_gb8k)
+        int iu;
+        if constexpr (LP) {
+          const long long c0 = W.keys[h], c1 = W.keys[h + 1];
+          const int i0 = W.id[h], i1 = W.id[h + 1];
+          iu = c0 == k[u] ? i0 : c1 == k[u] ? i1 : -1;
+        } else {
+          const long long c0 = W.keys[h], c1 = W.keys[h + 1], c2 = W.keys[h + 2], c3 = W.keys[h + 3];
+          const int j = c0 == k[u] ? 0 : c1 == k[u] ? 1 : c2 == k[u] ? 2 : c3 == k[u] ? 3 : -1;
+          iu = j >= 0 ? (int)W.id[h + j] : -1;
+        }
         const int good = ((unsigned)iu < (unsigned)D) & (k[u] != kEmptyKey) & small_v(v[u]);
         ok &= (!in[u]) | good;
         id[u] = in[u] ? iu : D;
@@ -867,11 +877,12 @@ sx_status gb_k19(sx_ctx* ctx, GsSpec s, int sig, const sx_col& kc, int vtype, in
   if (sig < 0 || s.nv != 1 || groups_hint > kGtHintMax) return SX_EUNSUPPORTED;
   Scratch scr(ctx);
   // variant and fan-out (measured, see GtWarp): <16, LP> directly up to 16 hinted groups and at ~4
-  // groups per partition for 49..2048; <48, !LP> directly for 17..48 and at ~16 per partition above
-  // 2048.  A partition's expected groups stay far below the warp's ids (rows of groups beyond them
+  // groups per partition for 49..1024; <48, !LP> directly for 17..48 and at ~16 per partition above
+  // 1024 (SX_GB_K19V=48: <48> above 16, the A/B switch).  A partition's expected groups stay far below the warp's ids (rows of groups beyond them
   // take global atomics: with 16 ids and ~8 groups per partition, the few partitions past 16
   // groups made one warp's chunk 7x slower than the rest, ncu r2u_gb4k).
-  const bool big = (groups_hint > 16 && groups_hint <= 48) || groups_hint > 2048;
+  bool big = (groups_hint > 16 && groups_hint <= 48) || groups_hint > 1024;
+  if (getenv("SX_GB_K19V")) big = atoi(getenv("SX_GB_K19V")) == 48 || groups_hint > 16;  // A/B: force <48> above 16
   const int per = big ? 16 : 4, dmax = big ? 48 : 16;
   int bits = 0;
   while (bits < 10 && groups_hint > dmax && ((int64_t)per << bits) < groups_hint) ++bits;
