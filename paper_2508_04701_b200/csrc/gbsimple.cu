@@ -391,7 +391,8 @@ template <class SIG>
 // words (ncu: 38% barrier/serialisation stalls).  The replicas are merged into replica 0 (shared
 // atomics) before its groups are written.
 __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__ GsSpec s, const int64_t* __restrict__ off,
-                                                         int P, uint32_t S, int R, const __grid_constant__ GsGlobal g) {
+                                                         int P, uint32_t S, int R, const __grid_constant__ GsGlobal g,
+                                                         unsigned* work) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_cnt;
   __shared__ unsigned long long s_base;
@@ -405,7 +406,14 @@ __global__ void __launch_bounds__(kGsThreads) k_gbs_part(const __grid_constant__
   };
   STab t = rep((threadIdx.x >> 5) % R);
   const STab t0 = rep(0);
-  for (int p = blockIdx.x; p < P; p += gridDim.x) {
+  // partitions are claimed one at a time from a global counter (a static round-robin left the
+  // CTAs that drew one partition more running alone: ncu r2x_gb64k, SM cycles max 1.5x avg)
+  __shared__ int s_p;
+  for (;;) {
+    if (threadIdx.x == 0) s_p = (int)atomicAdd(work, 1u);
+    __syncthreads();
+    const int p = s_p;
+    if (p >= P) break;
     for (int r = 0; r < R; ++r) stab_init(rep(r), s, threadIdx.x, blockDim.x);
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
@@ -750,12 +758,18 @@ __device__ __noinline__ void gt_slow_batch(GtWarp<D, LP>& W, const GsSpec& s, co
 
 template <class SIG, int KB, int VB, int D, bool LP>
 __global__ void __launch_bounds__(kGwThreads) k_gbt(const __grid_constant__ GsSpec s, const __grid_constant__ GwChunks ch,
-                                                    const __grid_constant__ GsGlobal g) {
+                                                    const __grid_constant__ GsGlobal g, unsigned* work) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   GtWarp<D, LP>& W = ((GtWarp<D, LP>*)smem)[threadIdx.x >> 5];
   const int gw = blockIdx.x * kGwWarps + (threadIdx.x >> 5), nw = gridDim.x * kGwWarps;
-  for (int c = gw; c < ch.nchunks; c += nw) {
+  (void)gw;
+  (void)nw;
+  for (;;) {  // chunks claimed one at a time per warp (balances partition tails and slow chunks)
+    int c = 0;
+    if (lane == 0) c = (int)atomicAdd(work, 1u);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= ch.nchunks) break;
     for (int i = lane; i < kGtSlots + 4; i += 32) {
       W.keys[i] = kEmptyKey;  // (slots kGtSlots + 1..3: never-used pads, probed as "home + 1..3")
       W.id[i] = -1;
@@ -959,7 +973,8 @@ sx_status gb_k19(sx_ctx* ctx, GsSpec s, int sig, const sx_col& kc, int vtype, in
           int per_sm = 1;
           SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGwThreads, smem));
           const unsigned grid = (unsigned)std::max(1, std::min(nch, ctx->num_sms * std::max(1, per_sm)));
-          kern<<<grid, kGwThreads, smem, SX_STREAM(ctx)>>>(s, ch, g);
+          SX_CUDA(cudaMemsetAsync(ctx->d_counters + 16, 0, sizeof(unsigned), ctx->stream));
+          kern<<<grid, kGwThreads, smem, SX_STREAM(ctx)>>>(s, ch, g, ctx->d_counters + 16);
           return SX_OK;
         };
         if (big) SX_TRY(launch(k_gbt<SIG, KB, VB, 48, false>, sizeof(GtWarp<48, false>)));
@@ -1183,7 +1198,8 @@ sx_status gb_simple(sx_ctx* ctx, const sx_col* cols, int ncols, const sx_key* ke
         int per_sm = 0;
         SX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gbs_part<SIG>, kGsThreads, smem));
         const unsigned grid = (unsigned)std::min<int64_t>(P, (int64_t)ctx->num_sms * std::max(1, per_sm));
-        k_gbs_part<SIG><<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, d_off, P, Sp, Rp, g);
+        SX_CUDA(cudaMemsetAsync(ctx->d_counters + 16, 0, sizeof(unsigned), ctx->stream));
+        k_gbs_part<SIG><<<grid, kGsThreads, smem, SX_STREAM(ctx)>>>(s, d_off, P, Sp, Rp, g, ctx->d_counters + 16);
         SX_CHECK_LAUNCH();
         return SX_OK;
       }));
