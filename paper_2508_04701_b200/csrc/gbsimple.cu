@@ -896,7 +896,10 @@ sx_status gb_k19(sx_ctx* ctx, GsSpec s, int sig, const sx_col& kc, int vtype, in
   // take global atomics: with 16 ids and ~8 groups per partition, the few partitions past 16
   // groups made one warp's chunk 7x slower than the rest, ncu r2u_gb4k).
   bool big = (groups_hint > 16 && groups_hint <= 48) || groups_hint > 1024;
-  if (getenv("SX_GB_K19V")) big = atoi(getenv("SX_GB_K19V")) == 48 || groups_hint > 16;  // A/B: force <48> above 16
+  if (getenv("SX_GB_K19V")) {  // A/B: 48 forces <48> above 16 groups, 16 keeps <16> above 48
+    const int v = atoi(getenv("SX_GB_K19V"));
+    big = v == 48 ? groups_hint > 16 : (groups_hint > 16 && groups_hint <= 48);
+  }
   const int per = big ? 16 : 4, dmax = big ? 48 : 16;
   int bits = 0;
   while (bits < 10 && groups_hint > dmax && ((int64_t)per << bits) < groups_hint) ++bits;
